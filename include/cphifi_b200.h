@@ -1,0 +1,214 @@
+/*
+ * cphifi_b200.h — C-ABI of the B200-native CP-HIFI infinite-mode subproblem solver.
+ *
+ * This is the drop-in boundary for the reference's hot path.  Every
+ * entry point below replaces one reference C++ function or object; the citation on each
+ * is `file:line` relative to /root/reference/proj/include/cphifi/.  All matrices are
+ * fp64 COLUMN-MAJOR (first index fastest), exactly as Eigen::MatrixXd in the reference
+ * (tensor.hpp:12-13); vec(W) of an n x r matrix is i + n*j.  Indices are 0-based.
+ *
+ * Conventions
+ *  - No C++ types and no exceptions cross this boundary.  Every function returns an
+ *    int status; on failure cphifi_last_error() returns a thread-local message that
+ *    reuses the reference's exception text where one exists.
+ *      CPHIFI_INVALID_ARGUMENT  <-> std::invalid_argument in the reference
+ *      CPHIFI_RUNTIME_ERROR     <-> std::runtime_error in the reference
+ *      CPHIFI_CUDA_ERROR / CPHIFI_NCCL_ERROR: device or collective failures
+ *  - Host pointers are plain host memory (pinned or pageable) unless a function name
+ *    ends in _device, in which case they are device pointers on the context's GPU and the
+ *    call is asynchronous on the context stream.
+ *  - There is no CPU fallback: every compute entry point runs sm_100a kernels.  On a
+ *    machine without a usable GPU cphifi_ctx_create fails with CPHIFI_CUDA_ERROR.
+ *  - Thread safety mirrors the reference objects: different handles may be used from
+ *    different host threads; one handle is not re-entrant.
+ */
+#ifndef CPHIFI_B200_H
+#define CPHIFI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPHIFI_ABI_VERSION 1
+
+enum cphifi_status {
+    CPHIFI_OK = 0,
+    CPHIFI_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    CPHIFI_RUNTIME_ERROR = 2,    /* std::runtime_error in the reference */
+    CPHIFI_CUDA_ERROR = 3,
+    CPHIFI_NCCL_ERROR = 4
+};
+
+typedef struct cphifi_ctx_s* cphifi_ctx;             /* device, stream, optional NCCL comm */
+typedef struct cphifi_mode_s* cphifi_mode;           /* RkhsMode analogue (kernel.hpp:53-101) */
+typedef struct cphifi_obs_s* cphifi_obs;             /* ObservationSet analogue (observations.hpp:18-79) */
+typedef struct cphifi_unaligned_s* cphifi_unaligned; /* UnalignedSubproblem (unaligned.hpp:18-33) */
+typedef struct cphifi_tensor_s* cphifi_tensor;       /* DenseTensor (tensor.hpp:14-68), device-resident */
+
+/* PcgConfig (solvers.hpp:23-27). Defaults in the reference: tol 1e-6, max_iter 75. */
+typedef struct cphifi_pcg_config {
+    double tol;
+    int32_t max_iter;
+    int32_t record_history;
+} cphifi_pcg_config;
+
+/* SolveReport (solvers.hpp:29-35) plus a phase breakdown.  residual_history is a
+ * CALLER-OWNED buffer of history_capacity doubles (>= max_iter + 1 to hold the whole
+ * history); history_len receives the number of entries the reference would record. */
+typedef struct cphifi_solve_report {
+    int32_t iterations;
+    int32_t converged;
+    double relative_residual;
+    double wall_time_s;
+    double* residual_history;
+    int32_t history_capacity;
+    int32_t history_len;
+    /* B200 extras (seconds, CUDA-event timed on the context stream) */
+    double setup_s;    /* RHS K*B, eig(V), preconditioner diagonal */
+    double matvec_s;   /* total time in the operator */
+    double precond_s;  /* total time in M^-1 applies */
+    int32_t matvecs;   /* operator applications */
+    int32_t pad_;
+} cphifi_solve_report;
+
+/* ---- status / context ------------------------------------------------------------ */
+const char* cphifi_last_error(void);
+int cphifi_abi_version(void);
+
+/* One context per (process, GPU). */
+int cphifi_ctx_create(int device, cphifi_ctx* out);
+int cphifi_ctx_destroy(cphifi_ctx ctx);
+int cphifi_ctx_synchronize(cphifi_ctx ctx);
+/* The context's CUDA stream (cudaStream_t) so callers can order their own work. */
+int cphifi_ctx_stream(cphifi_ctx ctx, void** stream_out);
+/* Multi-GPU: NCCL communicator over `nranks` processes (one per GPU).  Rank 0 creates the
+ * 128-byte id with cphifi_comm_unique_id and distributes it (e.g. torch.distributed).
+ * Once set, operator applications all-reduce the n x r partial accumulator. */
+int cphifi_comm_unique_id(uint8_t id_out[128]);
+int cphifi_ctx_init_comm(cphifi_ctx ctx, int nranks, int rank, const uint8_t id[128]);
+int cphifi_ctx_world(cphifi_ctx ctx, int* nranks, int* rank);
+
+/* ---- mode (RkhsMode, kernel.hpp:53-101) ------------------------------------------- */
+/* RkhsMode(points, sigma, lambda): Gaussian kernel K(i,j)=exp(-(x_i-x_j)^2/(2 sigma^2))
+ * built on device (gaussian_kernel, kernel.hpp:17-30); throws like the reference for
+ * sigma <= 0 and lambda < 0. */
+int cphifi_mode_create_gaussian(cphifi_ctx ctx, int64_t n, const double* points,
+                                double sigma, double lambda, cphifi_mode* out);
+/* Matern-3/2 kernel (1 + sqrt3 d/l) exp(-sqrt3 d/l); not in the reference. */
+int cphifi_mode_create_matern32(cphifi_ctx ctx, int64_t n, const double* points,
+                                double lengthscale, double lambda, cphifi_mode* out);
+/* Caller-supplied symmetric K (n x n column-major). */
+int cphifi_mode_create(cphifi_ctx ctx, int64_t n, const double* kernel, double lambda,
+                       cphifi_mode* out);
+int cphifi_mode_destroy(cphifi_mode mode);
+int cphifi_mode_size(cphifi_mode mode, int64_t* n);
+int cphifi_mode_lambda(cphifi_mode mode, double* lambda);
+int cphifi_mode_get_kernel(cphifi_mode mode, double* kernel_out);
+/* RkhsMode::eig (kernel.hpp:77-83 -> sym_eig :40-49): symmetry check at
+ * 1e-12*max(scale,1), device syevd, clamp at 0; computed at most once. */
+int cphifi_mode_eig(cphifi_mode mode);
+/* Shared eigendecomposition: install (U_K, mu_K) from outside, counted as the
+ * one factorization.  mu is clamped at 0 exactly as sym_eig does. */
+int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu);
+int cphifi_mode_get_eig(cphifi_mode mode, double* u_out, double* mu_out);
+int cphifi_mode_eig_count(cphifi_mode mode, int* count); /* eig_factorization_count */
+
+/* ---- observations (ObservationSet, observations.hpp:18-79) ------------------------- */
+#define CPHIFI_OBS_DEVICE_INPUT 1u      /* idx / values are device pointers */
+#define CPHIFI_OBS_REJECT_DUPLICATES 2u /* reference semantics: throw on a repeated index */
+/* Build the observation plan for infinite mode k: q multi-indices stored as d int32
+ * arrays (idx[m*q + l] = index of observation l in mode m), fp64 values.  The plan sorts
+ * by i_k on device (stable), builds CSR row pointers, and keeps the contiguous
+ * equal-count shard [q*s/S, q*(s+1)/S) of the sorted order (s = shard, S = shards; use
+ * 0/1 for a single GPU).  Range errors throw "ObservationSet: index out of range". */
+int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q,
+                      const int32_t* idx, const double* values, int k, uint32_t flags,
+                      int shard, int shards, cphifi_obs* out);
+int cphifi_obs_destroy(cphifi_obs obs);
+int cphifi_obs_info(cphifi_obs obs, int64_t* q_total, int64_t* q_local, double* density);
+
+/* ---- unaligned subproblem (unaligned.hpp:18-161) ---------------------------------- */
+/* make_unaligned_subproblem(obs, model, k, mode, rho) (unaligned.hpp:35-48): factors[m]
+ * is the n_m x r column-major factor of mode m (factors[k] is ignored and may be NULL).
+ * Builds B = sampled_mttkrp(values) (all-reduced over shards) and V = gram_khatri_rao. */
+int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r,
+                            const double* const* factors, double rho,
+                            cphifi_unaligned* out);
+int cphifi_unaligned_destroy(cphifi_unaligned p);
+int cphifi_unaligned_get_b(cphifi_unaligned p, double* b_out);  /* n x r */
+int cphifi_unaligned_get_v(cphifi_unaligned p, double* v_out);  /* r x r */
+/* unaligned_matvec (unaligned.hpp:101-115): y = vec(K*Yhat + lambda*K*X) + rho*x. */
+int cphifi_unaligned_matvec(cphifi_unaligned p, const double* x, double* y);
+int cphifi_unaligned_matvec_device(cphifi_unaligned p, const double* x, double* y);
+/* build_preconditioner(p).apply (unaligned.hpp:120-140): eig(V) is computed on first use;
+ * cphifi_unaligned_set_v_eig installs a shared (U_V, sigma_V) instead. */
+int cphifi_unaligned_set_v_eig(cphifi_unaligned p, const double* u_v, const double* sigma_v);
+int cphifi_unaligned_get_v_eig(cphifi_unaligned p, double* u_v_out, double* sigma_v_out);
+int cphifi_unaligned_precond_apply(cphifi_unaligned p, const double* x, double* y);
+int cphifi_unaligned_precond_apply_device(cphifi_unaligned p, const double* x, double* y);
+/* solve_unaligned_pcg (unaligned.hpp:143-161) with pcg (solvers.hpp:38-88).  warm_start
+ * (n x r, may be NULL) maps directly to x0.  w_out receives W (n x r). */
+int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
+                               cphifi_solve_report* report, const double* warm_start,
+                               double* w_out);
+/* Benchmark hook: `iters` operator applications on DEVICE buffers x, y with CUDA events on
+ * the context stream around each phase; ms_out[0..5] receives the mean milliseconds of
+ * [0] Xhat = K X, [1] scatter-gather main kernel (K1), [2] fix-up, [3] all-reduce,
+ * [4] y = K Yhat + lambda Xhat + rho x, [5] the whole matvec. */
+int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters,
+                                  double* ms_out);
+/* Test hook: Yhat = sampled_mttkrp(gather_rows(Xhat)) for a given Xhat (n x r), i.e.
+ * observations.hpp:174-198 fused, before the final K multiply (all-reduced). */
+int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, double* yhat_out);
+
+/* ---- aligned path (tensor.hpp:174-194, aligned.hpp:41-54) ------------------------- */
+#define CPHIFI_TENSOR_DEVICE_INPUT 1u
+/* Dense d-way tensor, column-major.  With shards > 1 the tensor is split over mode-1
+ * (second mode) slices and this process keeps slice range [n1*s/S, n1*(s+1)/S); `data`
+ * is the FULL tensor (host) or, with CPHIFI_TENSOR_DEVICE_INPUT, already the local slab
+ * (n0 x local_n1 x n2 ...). */
+int cphifi_tensor_create(cphifi_ctx ctx, int d, const int64_t* shape, const double* data,
+                         uint32_t flags, int shard, int shards, cphifi_tensor* out);
+int cphifi_tensor_destroy(cphifi_tensor t);
+/* mttkrp(t, model, k) = unfold(t,k) * khatri_rao_excluding(model,k) (tensor.hpp:174-182);
+ * k = 0 (the infinite mode) is the accelerated path.  All-reduced over shards. */
+int cphifi_mttkrp(cphifi_tensor t, int k, int64_t r, const double* const* factors,
+                  double* b_out);
+/* gram_khatri_rao(model, k) (tensor.hpp:186-194): Hadamard product of A_m' A_m, m != k. */
+int cphifi_gram_khatri_rao(cphifi_ctx ctx, int d, const int64_t* shape, int64_t r,
+                           const double* const* factors, int k, double* v_out);
+/* solve_aligned_decoupled (aligned.hpp:41-54): W = U_K((U_K' B U_V) ./ (sigma_j mu_i +
+ * lambda)) U_V'.  u_v / sigma_v may be NULL (eig(V) on device) or a shared eig (F1). */
+int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
+                                   const double* v, const double* u_v,
+                                   const double* sigma_v, double* w_out);
+/* Fused aligned update for mode k: MTTKRP + Gram + decoupled solve, one device pass,
+ * eig(V) on device.  b_out / v_out may be NULL. */
+int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
+                         const double* const* factors, double* w_out, double* b_out,
+                         double* v_out);
+
+/* ---- host-side seeded generators (test/bench inputs; no device work) -------------- */
+/* std::mt19937_64 with libstdc++'s uniform_real_distribution / uniform_int_distribution
+ * / normal_distribution algorithms, reproduced bit-exactly (pinned by tests/golden). */
+typedef struct cphifi_rng_s* cphifi_rng;
+int cphifi_rng_create(uint64_t seed, cphifi_rng* out);
+int cphifi_rng_destroy(cphifi_rng rng);
+int cphifi_rng_next_u64(cphifi_rng rng, uint64_t* n_out, int64_t count);
+int cphifi_rng_uniform_real(cphifi_rng rng, double lo, double hi, double* out, int64_t count);
+int cphifi_rng_uniform_int(cphifi_rng rng, int64_t lo, int64_t hi, int64_t* out, int64_t count);
+/* normal_distribution(mean, stddev) draws; the distribution's cached second variate is
+ * kept in the rng handle (one distribution object per handle). */
+int cphifi_rng_normal(cphifi_rng rng, double mean, double stddev, double* out, int64_t count);
+/* Discard the cached variate (equivalent to constructing a fresh normal_distribution). */
+int cphifi_rng_normal_reset(cphifi_rng rng);
+/* sample_uniform's index draw (observations.hpp:90-121): q distinct linear indices of
+ * [0, n_total) by partial Fisher-Yates with a sparse map, seeded mt19937_64(seed). */
+int cphifi_sample_uniform_linear(int64_t n_total, int64_t q, uint64_t seed, int64_t* picked);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPHIFI_B200_H */

@@ -1,0 +1,623 @@
+"""paper_2603_25691_b200 — B200-native CP-HIFI infinite-mode subproblem solver.
+
+Python mirror of the reference's C++ interface for the hot path (names, argument meaning and
+exception classes follow proj/include/cphifi/*.hpp).  Every compute call
+goes through the C-ABI of ``libcphifi_b200.so`` (include/cphifi_b200.h) to hand-written
+sm_100a kernels; there is no CPU fallback.
+
+Reference object                        -> here
+  RkhsMode (kernel.hpp:53-101)          -> RkhsMode (device kernel + cached device eig)
+  ObservationSet (observations.hpp:18)  -> ObservationSet (host arrays; device plans per k)
+  KruskalModel / DenseTensor            -> KruskalModel / DenseTensor (numpy, column-major)
+  make_unaligned_subproblem (unaligned.hpp:35-48), unaligned_matvec (:101-115),
+  build_preconditioner (:120-140), solve_unaligned_pcg (:143-161)
+  mttkrp / gram_khatri_rao (tensor.hpp:174-194), solve_aligned_decoupled (aligned.hpp:41-54)
+  PcgConfig / SolveReport (solvers.hpp:23-35)
+std::invalid_argument -> CphifiInvalidArgument (a ValueError); std::runtime_error ->
+CphifiRuntimeError (a RuntimeError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import (CphifiDeviceError, CphifiInvalidArgument, CphifiRuntimeError, c_double_p, c_int64_p,
+                    call)
+
+__all__ = [
+    "Context", "default_context", "RkhsMode", "SymEig", "ObservationSet", "DenseTensor", "KruskalModel",
+    "sample_uniform", "full_observations", "make_unaligned_subproblem", "UnalignedSubproblem",
+    "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
+    "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
+    "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
+]
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(c_double_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+# ---- context ---------------------------------------------------------------------------
+class Context:
+    """One GPU (and optionally an NCCL communicator) — owns the CUDA stream."""
+
+    def __init__(self, device: int | None = None):
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", os.environ.get("CPHIFI_DEVICE", "0")))
+        h = ctypes.c_void_p()
+        call("cphifi_ctx_create", device, ctypes.byref(h))
+        self.handle = h
+        self.device = device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        call("cphifi_comm_unique_id", buf)
+        return buf.raw
+
+    def init_comm(self, nranks: int, rank: int, uid: bytes) -> None:
+        call("cphifi_ctx_init_comm", self.handle, nranks, rank, uid)
+
+    def world(self):
+        n, r = ctypes.c_int(), ctypes.c_int()
+        call("cphifi_ctx_world", self.handle, ctypes.byref(n), ctypes.byref(r))
+        return n.value, r.value
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        call("cphifi_ctx_stream", self.handle, ctypes.byref(s))
+        return s.value or 0
+
+    def synchronize(self) -> None:
+        call("cphifi_ctx_synchronize", self.handle)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _capi.load().cphifi_ctx_destroy(self.handle)
+            self.handle = None
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+# ---- RNG (std::mt19937_64 + libstdc++ distributions; test/bench inputs) -------------------
+class Mt19937_64:
+    def __init__(self, seed: int):
+        h = ctypes.c_void_p()
+        call("cphifi_rng_create", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), ctypes.byref(h))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _capi.load().cphifi_rng_destroy(self.h)
+
+    def __call__(self) -> int:
+        return int(self.next_u64(1)[0])
+
+    def next_u64(self, count: int) -> np.ndarray:
+        out = np.zeros(count, dtype=np.uint64)
+        call("cphifi_rng_next_u64", self.h, out.ctypes.data_as(_capi.c_uint64_p), count)
+        return out
+
+    def uniform_real(self, lo: float, hi: float, count: int) -> np.ndarray:
+        out = np.zeros(count)
+        call("cphifi_rng_uniform_real", self.h, lo, hi, _dp(out), count)
+        return out
+
+    def uniform_int(self, lo: int, hi: int, count: int = 1) -> np.ndarray:
+        out = np.zeros(count, dtype=np.int64)
+        call("cphifi_rng_uniform_int", self.h, lo, hi, out.ctypes.data_as(c_int64_p), count)
+        return out
+
+    def normal(self, mean: float, std: float, count: int) -> np.ndarray:
+        out = np.zeros(count)
+        call("cphifi_rng_normal", self.h, mean, std, _dp(out), count)
+        return out
+
+    def normal_reset(self) -> None:
+        call("cphifi_rng_normal_reset", self.h)
+
+    def random_matrix(self, rows: int, cols: int, lo=-1.0, hi=1.0) -> np.ndarray:
+        """test_util.hpp:10-17: column-major fill."""
+        return np.asfortranarray(self.uniform_real(lo, hi, rows * cols).reshape((rows, cols), order="F"))
+
+
+# ---- kernel.hpp ------------------------------------------------------------------------
+@dataclass
+class SymEig:
+    u: np.ndarray
+    d: np.ndarray
+
+
+class RkhsMode:
+    """RkhsMode(points, sigma, lambda) (kernel.hpp:53-101) with the kernel and its one-time
+    eigendecomposition resident on the GPU."""
+
+    def __init__(self, design_points, sigma: float, lambda_: float, ctx: Context | None = None,
+                 kernel: str = "gaussian", kernel_matrix=None):
+        self.ctx = ctx or default_context()
+        pts = np.ascontiguousarray(design_points, dtype=np.float64).reshape(-1)
+        self._points = pts
+        self._sigma = float(sigma)
+        self._lambda = float(lambda_)
+        h = ctypes.c_void_p()
+        if kernel_matrix is not None:
+            km = _f64(kernel_matrix)
+            call("cphifi_mode_create", self.ctx.handle, km.shape[0], _dp(km), self._lambda, ctypes.byref(h))
+        elif kernel == "gaussian":
+            call("cphifi_mode_create_gaussian", self.ctx.handle, pts.size, _dp(pts), self._sigma, self._lambda,
+                 ctypes.byref(h))
+        elif kernel == "matern32":
+            call("cphifi_mode_create_matern32", self.ctx.handle, pts.size, _dp(pts), self._sigma, self._lambda,
+                 ctypes.byref(h))
+        else:
+            raise CphifiInvalidArgument(f"RkhsMode: unknown kernel {kernel!r}")
+        self.handle = h
+
+    @staticmethod
+    def regular_grid(n: int, sigma: float, lambda_: float, ctx: Context | None = None) -> "RkhsMode":
+        return RkhsMode(np.arange(1, n + 1, dtype=np.float64), sigma, lambda_, ctx)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _capi.load().cphifi_mode_destroy(self.handle)
+
+    def size(self) -> int:
+        n = ctypes.c_int64()
+        call("cphifi_mode_size", self.handle, ctypes.byref(n))
+        return n.value
+
+    def sigma(self) -> float:
+        return self._sigma
+
+    def lambda_(self) -> float:
+        return self._lambda
+
+    def points(self) -> np.ndarray:
+        return self._points
+
+    def kernel(self) -> np.ndarray:
+        n = self.size()
+        k = np.zeros((n, n), order="F")
+        call("cphifi_mode_get_kernel", self.handle, _dp(k))
+        return k
+
+    def eig(self) -> SymEig:
+        n = self.size()
+        u = np.zeros((n, n), order="F")
+        d = np.zeros(n)
+        call("cphifi_mode_get_eig", self.handle, _dp(u), _dp(d))
+        return SymEig(u, d)
+
+    def set_eig(self, u, d) -> None:
+        """Install a shared eigendecomposition."""
+        u = _f64(u)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        call("cphifi_mode_set_eig", self.handle, _dp(u), _dp(d))
+
+    def eig_factorization_count(self) -> int:
+        c = ctypes.c_int()
+        call("cphifi_mode_eig_count", self.handle, ctypes.byref(c))
+        return c.value
+
+
+# ---- tensor.hpp ------------------------------------------------------------------------
+class DenseTensor:
+    """Dense d-way tensor, column-major (tensor.hpp:14-68), host resident."""
+
+    def __init__(self, shape, data=None):
+        shape = [int(s) for s in shape]
+        if not shape:
+            raise CphifiInvalidArgument("DenseTensor: empty shape")
+        if any(s <= 0 for s in shape):
+            raise CphifiInvalidArgument("DenseTensor: nonpositive mode size")
+        n = int(np.prod(shape))
+        if data is None:
+            flat = np.zeros(n)
+        else:
+            flat = np.asarray(data, dtype=np.float64).reshape(-1, order="F")
+            if flat.size != n:
+                raise CphifiInvalidArgument("DenseTensor: data length does not match shape")
+        self._shape = shape
+        self._data = np.ascontiguousarray(flat)
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "DenseTensor":
+        return DenseTensor(a.shape, np.asarray(a).reshape(-1, order="F"))
+
+    def order(self) -> int:
+        return len(self._shape)
+
+    def shape(self):
+        return list(self._shape)
+
+    def size(self) -> int:
+        return self._data.size
+
+    def data(self) -> np.ndarray:
+        return self._data
+
+    def array(self) -> np.ndarray:
+        return self._data.reshape(self._shape, order="F")
+
+
+class KruskalModel:
+    def __init__(self, factors):
+        if not factors:
+            raise CphifiInvalidArgument("KruskalModel: no factors")
+        self.factors = [_f64(f) for f in factors]
+        r = self.rank()
+        for a in self.factors:
+            if a.shape[1] != r:
+                raise CphifiInvalidArgument("KruskalModel: rank mismatch")
+
+    def order(self) -> int:
+        return len(self.factors)
+
+    def rank(self) -> int:
+        return self.factors[0].shape[1]
+
+    def shape(self):
+        return [a.shape[0] for a in self.factors]
+
+
+def _factor_array(factors, skip: int):
+    arrs = [None if (i == skip or f is None) else _f64(f) for i, f in enumerate(factors)]
+    ptrs = (c_double_p * len(arrs))(*[(_dp(a) if a is not None else c_double_p()) for a in arrs])
+    return arrs, ptrs
+
+
+# ---- observations.hpp ------------------------------------------------------------------
+class ObservationSet:
+    """The set Omega (observations.hpp:18-79).  Indices are held host-side as (d, q) int32;
+    device plans (sorted by i_k, CSR, sharded) are built per mode on first use.  With
+    ``multiset=True`` repeated multi-indices are summed instead of rejected."""
+
+    def __init__(self, shape, indices, values, multiset: bool = False):
+        self._shape = [int(s) for s in shape]
+        d = len(self._shape)
+        vals = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        idx = np.asarray(indices, dtype=np.int64)
+        if idx.size == 0:
+            idx = np.zeros((d, 0), dtype=np.int64)
+        elif idx.ndim == 2 and idx.shape[1] == d and idx.shape[0] == vals.size and not (
+                idx.shape[0] == d and idx.shape[1] == vals.size):
+            idx = idx.T
+        if idx.ndim != 2 or idx.shape[1] != vals.size:
+            raise CphifiInvalidArgument("ObservationSet: index/value count mismatch")
+        if idx.shape[0] != d:
+            raise CphifiInvalidArgument("ObservationSet: index arity mismatch")
+        for k in range(d):
+            if idx.shape[1] and (idx[k].min() < 0 or idx[k].max() >= self._shape[k]):
+                raise CphifiInvalidArgument("ObservationSet: index out of range")
+        self._idx = np.ascontiguousarray(idx.astype(np.int32))
+        self._values = vals
+        self.multiset = multiset
+        self._plans = {}
+        if not multiset and vals.size > 1:
+            strides = np.cumprod([1] + self._shape[:-1]).astype(np.int64)
+            lin = (self._idx.astype(np.int64) * strides[:, None]).sum(axis=0)
+            if np.unique(lin).size != lin.size:
+                raise CphifiInvalidArgument("ObservationSet: duplicate index")
+
+    def shape(self):
+        return list(self._shape)
+
+    def num_obs(self) -> int:
+        return self._values.size
+
+    def num_entries(self) -> int:
+        return int(np.prod(self._shape))
+
+    def density(self) -> float:
+        return float(self.num_obs()) / float(self.num_entries())
+
+    def aligned(self) -> bool:
+        return self.num_obs() == self.num_entries()
+
+    def values(self) -> np.ndarray:
+        return self._values
+
+    def index_array(self) -> np.ndarray:
+        return self._idx
+
+    def index(self, l: int, k: int) -> int:
+        return int(self._idx[k, l])
+
+    def plan(self, k: int, ctx: Context, shard: int = 0, shards: int = 1):
+        key = (k, id(ctx), shard, shards)
+        if key not in self._plans:
+            h = ctypes.c_void_p()
+            shape = np.ascontiguousarray(self._shape, dtype=np.int64)
+            flags = 0 if self.multiset else _capi.OBS_REJECT_DUPLICATES
+            call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p),
+                 self.num_obs(), self._idx.ctypes.data, self._values.ctypes.data, k, flags, shard, shards,
+                 ctypes.byref(h))
+            self._plans[key] = _Handle(h, "cphifi_obs_destroy")
+        return self._plans[key].h
+
+
+class _Handle:
+    def __init__(self, h, destroy):
+        self.h = h
+        self.destroy = destroy
+
+    def __del__(self):
+        if self.h:
+            getattr(_capi.load(), self.destroy)(self.h)
+
+
+def sample_uniform(source: DenseTensor, q: int, seed: int, multiset: bool = False) -> ObservationSet:
+    """observations.hpp:90-121: q distinct entries drawn by partial Fisher-Yates."""
+    n_total = source.size()
+    picked = np.zeros(max(q, 0), dtype=np.int64)
+    call("cphifi_sample_uniform_linear", n_total, q, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF),
+         picked.ctypes.data_as(c_int64_p))
+    shape = source.shape()
+    idx = np.zeros((len(shape), q), dtype=np.int64)
+    lin = picked.copy()
+    for k, s in enumerate(shape):
+        idx[k] = lin % s
+        lin //= s
+    return ObservationSet(shape, idx, source.data()[picked], multiset=multiset)
+
+
+def full_observations(t: DenseTensor) -> ObservationSet:
+    """observations.hpp:124-138: every entry in storage order."""
+    shape = t.shape()
+    lin = np.arange(t.size(), dtype=np.int64)
+    idx = np.zeros((len(shape), t.size()), dtype=np.int64)
+    for k, s in enumerate(shape):
+        idx[k] = lin % s
+        lin //= s
+    return ObservationSet(shape, idx, t.data().copy())
+
+
+# ---- solvers.hpp -----------------------------------------------------------------------
+@dataclass
+class PcgConfig:
+    tol: float = 1e-6
+    max_iter: int = 75
+    record_history: bool = False
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    relative_residual: float = 0.0
+    wall_time_s: float = 0.0
+    converged: bool = False
+    residual_history: list = field(default_factory=list)
+    setup_s: float = 0.0
+    matvecs: int = 0
+
+
+@dataclass
+class LinearOperator:
+    dim: int
+    apply: object
+
+
+# ---- unaligned.hpp ---------------------------------------------------------------------
+class UnalignedSubproblem:
+    """unaligned.hpp:18-33 — a device plan: sorted observations, packed factors, B, V."""
+
+    def __init__(self, obs: ObservationSet, model: KruskalModel, k: int, mode: RkhsMode, rho: float,
+                 shard: int = 0, shards: int = 1):
+        self.obs = obs
+        self.mode = mode
+        self.mode_index = k
+        self.rho = float(rho)
+        for i in range(model.order()):
+            if i != k and model.factors[i].shape[0] != obs.shape()[i]:
+                raise CphifiInvalidArgument("build_zhat: shape mismatch")
+        self._r = model.rank()
+        self._n = mode.size()
+        arrs, ptrs = _factor_array(model.factors, k)
+        plan = obs.plan(k, mode.ctx, shard, shards)
+        h = ctypes.c_void_p()
+        call("cphifi_unaligned_create", plan, mode.handle, self._r, ptrs, self.rho, ctypes.byref(h))
+        self._h = _Handle(h, "cphifi_unaligned_destroy")
+        self.handle = h
+
+    def n(self) -> int:
+        return self._n
+
+    def r(self) -> int:
+        return self._r
+
+    def q(self) -> int:
+        return self.obs.num_obs()
+
+    def lambda_(self) -> float:
+        return self.mode.lambda_()
+
+    def density(self) -> float:
+        return self.obs.density()
+
+    @property
+    def b(self) -> np.ndarray:
+        out = np.zeros((self._n, self._r), order="F")
+        call("cphifi_unaligned_get_b", self.handle, _dp(out))
+        return out
+
+    @property
+    def v(self) -> np.ndarray:
+        out = np.zeros((self._r, self._r), order="F")
+        call("cphifi_unaligned_get_v", self.handle, _dp(out))
+        return out
+
+    def set_v_eig(self, u, d) -> None:
+        u = _f64(u)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        call("cphifi_unaligned_set_v_eig", self.handle, _dp(u), _dp(d))
+
+    def v_eig(self) -> SymEig:
+        u = np.zeros((self._r, self._r), order="F")
+        d = np.zeros(self._r)
+        call("cphifi_unaligned_get_v_eig", self.handle, _dp(u), _dp(d))
+        return SymEig(u, d)
+
+    def scatter_gather(self, xhat) -> np.ndarray:
+        """Yhat = sampled_mttkrp(gather_rows(Xhat)) (observations.hpp:174-198), fused."""
+        xhat = _f64(xhat)
+        out = np.zeros((self._n, self._r), order="F")
+        call("cphifi_unaligned_scatter_gather", self.handle, _dp(xhat), _dp(out))
+        return out
+
+
+def make_unaligned_subproblem(obs: ObservationSet, model: KruskalModel, k: int, mode: RkhsMode,
+                              rho: float, shard: int = 0, shards: int = 1) -> UnalignedSubproblem:
+    """unaligned.hpp:35-48."""
+    return UnalignedSubproblem(obs, model, k, mode, rho, shard, shards)
+
+
+def unaligned_matvec(p: UnalignedSubproblem, x) -> np.ndarray:
+    """unaligned.hpp:101-115: y = (F'F + lambda (I kron K) + rho I) x."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    if x.size != p.n() * p.r():
+        raise CphifiInvalidArgument("unaligned_matvec: size mismatch")
+    y = np.zeros_like(x)
+    call("cphifi_unaligned_matvec", p.handle, _dp(x), _dp(y))
+    return y
+
+
+def build_preconditioner(p: UnalignedSubproblem) -> LinearOperator:
+    """unaligned.hpp:120-140: M^-1 = U_K((U_K' X U_V) .* D)U_V' on device."""
+    p.v_eig()  # builds eig(V) and D now, like the reference (throws here on bad D)
+
+    def apply(x):
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        y = np.zeros_like(x)
+        call("cphifi_unaligned_precond_apply", p.handle, _dp(x), _dp(y))
+        return y
+
+    return LinearOperator(p.n() * p.r(), apply)
+
+
+def solve_unaligned_pcg(p: UnalignedSubproblem, cfg: PcgConfig | None = None, report: SolveReport | None = None,
+                        warm_start=None) -> np.ndarray:
+    """unaligned.hpp:143-161 / solvers.hpp:38-88, entirely on device."""
+    cfg = cfg or PcgConfig()
+    n, r = p.n(), p.r()
+    ccfg = _capi.PcgConfigC(cfg.tol, int(cfg.max_iter), int(bool(cfg.record_history)))
+    cap = int(cfg.max_iter) + 2
+    hist = np.zeros(cap)
+    rep = _capi.SolveReportC()
+    rep.residual_history = _dp(hist)
+    rep.history_capacity = cap
+    w = np.zeros((n, r), order="F")
+    ws = None if warm_start is None else _f64(warm_start)
+    call("cphifi_solve_unaligned_pcg", p.handle, ctypes.byref(ccfg), ctypes.byref(rep),
+         _dp(ws) if ws is not None else c_double_p(), _dp(w))
+    if report is not None:
+        report.iterations = rep.iterations
+        report.relative_residual = rep.relative_residual
+        report.wall_time_s = rep.wall_time_s
+        report.converged = bool(rep.converged)
+        report.residual_history = list(hist[: rep.history_len]) if cfg.record_history else []
+        report.setup_s = rep.setup_s
+        report.matvecs = rep.matvecs
+    return w
+
+
+# ---- aligned path ----------------------------------------------------------------------
+class _DeviceTensor:
+    def __init__(self, t: DenseTensor, ctx: Context, shard=0, shards=1):
+        shape = np.ascontiguousarray(t.shape(), dtype=np.int64)
+        h = ctypes.c_void_p()
+        call("cphifi_tensor_create", ctx.handle, len(t.shape()), shape.ctypes.data_as(c_int64_p),
+             t.data().ctypes.data, 0, shard, shards, ctypes.byref(h))
+        self._h = _Handle(h, "cphifi_tensor_destroy")
+        self.handle = h
+
+
+def _device_tensor(t: DenseTensor, ctx: Context, shard=0, shards=1):
+    cache = t.__dict__.setdefault("_dev", {})
+    key = (id(ctx), shard, shards)
+    if key not in cache:
+        cache[key] = _DeviceTensor(t, ctx, shard, shards)
+    return cache[key]
+
+
+def mttkrp(t: DenseTensor, model: KruskalModel, k: int, ctx: Context | None = None) -> np.ndarray:
+    """tensor.hpp:174-182 (k = 0, the infinite mode, on device)."""
+    ctx = ctx or default_context()
+    if t.order() != model.order():
+        raise CphifiInvalidArgument("mttkrp: order mismatch")
+    for i in range(t.order()):
+        if i != k and t.shape()[i] != model.factors[i].shape[0]:
+            raise CphifiInvalidArgument("mttkrp: shape mismatch")
+    dt = _device_tensor(t, ctx)
+    arrs, ptrs = _factor_array(model.factors, k)
+    b = np.zeros((t.shape()[k], model.rank()), order="F")
+    call("cphifi_mttkrp", dt.handle, k, model.rank(), ptrs, _dp(b))
+    return b
+
+
+def gram_khatri_rao(model: KruskalModel, k: int, ctx: Context | None = None) -> np.ndarray:
+    """tensor.hpp:186-194."""
+    ctx = ctx or default_context()
+    shape = np.ascontiguousarray(model.shape(), dtype=np.int64)
+    arrs, ptrs = _factor_array(model.factors, k)
+    r = model.rank()
+    v = np.zeros((r, r), order="F")
+    call("cphifi_gram_khatri_rao", ctx.handle, model.order(), shape.ctypes.data_as(c_int64_p), r, ptrs, k, _dp(v))
+    return v
+
+
+@dataclass
+class AlignedSubproblem:
+    """aligned.hpp:16-25."""
+    b: np.ndarray
+    v: np.ndarray
+    mode: RkhsMode
+
+    def n(self):
+        return self.b.shape[0]
+
+    def r(self):
+        return self.b.shape[1]
+
+
+def solve_aligned_decoupled(p: AlignedSubproblem, v_eig: SymEig | None = None) -> np.ndarray:
+    """aligned.hpp:41-54 on device; eig(V) on device unless a shared one is given."""
+    b = _f64(p.b)
+    v = _f64(p.v)
+    n, r = b.shape
+    w = np.zeros((n, r), order="F")
+    if v_eig is not None:
+        uv = _f64(v_eig.u)
+        sv = np.ascontiguousarray(v_eig.d, dtype=np.float64)
+        call("cphifi_solve_aligned_decoupled", p.mode.handle, r, _dp(b), _dp(v), _dp(uv), _dp(sv), _dp(w))
+    else:
+        call("cphifi_solve_aligned_decoupled", p.mode.handle, r, _dp(b), _dp(v), c_double_p(), c_double_p(),
+             _dp(w))
+    return w
+
+
+def aligned_solve(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode):
+    """Fused aligned update (MTTKRP + Gram + decoupled solve on device). Returns (W, B, V)."""
+    dt = _device_tensor(t, mode.ctx)
+    arrs, ptrs = _factor_array(model.factors, k)
+    n, r = mode.size(), model.rank()
+    w = np.zeros((n, r), order="F")
+    b = np.zeros((n, r), order="F")
+    v = np.zeros((r, r), order="F")
+    call("cphifi_aligned_solve", dt.handle, mode.handle, k, r, ptrs, _dp(w), _dp(b), _dp(v))
+    return w, b, v

@@ -1,0 +1,1105 @@
+// capi.cu — the C-ABI (include/cphifi_b200.h): host orchestration of the sm_100a kernels.
+//
+// Each entry point restates one reference function (cited per function, paths relative to
+// proj/include/cphifi/) on device-resident plans.  C++ exceptions never cross the ABI:
+// `guard` maps them to status codes and a thread-local message.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "kernels.cuh"
+
+using namespace cphifi;
+
+namespace cphifi {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace cphifi
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CPHIFI_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("out of host memory");
+        return CPHIFI_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return CPHIFI_RUNTIME_ERROR;
+    } catch (...) {
+        set_last_error("unknown error");
+        return CPHIFI_RUNTIME_ERROR;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CPHIFI_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void need(const void* p, const char* what) {
+    if (!p) throw_invalid(std::string(what) + ": null argument");
+}
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes) CPHIFI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+}
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes) CPHIFI_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    CPHIFI_CUDA(cudaStreamSynchronize(s));
+}
+
+void allreduce(cphifi_ctx ctx, double* buf, size_t count) {
+    if (ctx->comm && ctx->nranks > 1 && count)
+        CPHIFI_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+int read_flag(cphifi_ctx ctx, int* dflag) {
+    int h = 0;
+    d2h_sync(&h, dflag, sizeof(int), ctx->stream);
+    return h;
+}
+
+// sym_eig (kernel.hpp:40-49) on a device matrix: symmetry check, syevd, clamp at 0.
+void device_sym_eig(cphifi_ctx ctx, const double* a, int64_t n, double* u_out, double* d_out) {
+    DevBuf<double> chk(2);
+    max_asym(a, n, chk.get(), ctx->stream);
+    double h[2];
+    d2h_sync(h, chk.get(), sizeof h, ctx->stream);
+    if (h[0] > 1e-12 * std::max(h[1], 1.0)) throw_invalid("sym_eig: matrix is not symmetric");
+    CPHIFI_CUDA(cudaMemcpyAsync(u_out, a, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    int lwork = 0;
+    CPHIFI_SOLVER(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                              (int)n, u_out, (int)n, d_out, &lwork));
+    DevBuf<double> work(std::max(lwork, 1));
+    DevBuf<int> info(1);
+    CPHIFI_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, u_out,
+                                   (int)n, d_out, work.get(), lwork, info.get()));
+    int hinfo = 0;
+    d2h_sync(&hinfo, info.get(), sizeof(int), ctx->stream);
+    if (hinfo != 0) throw_runtime("sym_eig: eigendecomposition failed");
+    clamp_nonneg(d_out, n, ctx->stream);
+}
+
+void mode_eig_once(cphifi_mode m) {
+    std::call_once(m->once, [m] {
+        std::lock_guard<std::mutex> lk(m->mu_lock);
+        if (m->have_eig) return;  // installed via cphifi_mode_set_eig
+        DeviceGuard dg(m->ctx->device);
+        m->u.alloc(m->n * m->n);
+        m->mu.alloc(m->n);
+        device_sym_eig(m->ctx, m->kernel.get(), m->n, m->u.get(), m->mu.get());
+        m->have_eig = true;
+        m->eig_count = 1;
+    });
+}
+
+// GEMM helpers (column-major unless stated)
+void gemm_nn(cphifi_ctx ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
+             int64_t ldb, double* c, int64_t ldc) {
+    GemmArgs g;
+    g.m = m; g.n = n; g.k = k;
+    g.a = a; g.a_rs = 1; g.a_cs = lda;
+    g.b = b; g.b_rs = 1; g.b_cs = ldb;
+    g.c = c; g.c_rs = 1; g.c_cs = ldc;
+    gemm(g, ctx->num_sms, ctx->stream);
+}
+
+cphifi_mode new_mode(cphifi_ctx ctx, int64_t n, double lambda) {
+    auto* m = new cphifi_mode_s;
+    m->ctx = ctx;
+    m->n = n;
+    m->lambda = lambda;
+    m->kernel.alloc(n * n);
+    return m;
+}
+
+// ---- unaligned pieces ------------------------------------------------------------------
+SgArgs sg_args(cphifi_unaligned p) {
+    cphifi_obs o = p->obs;
+    SgArgs a;
+    a.n = p->n;
+    a.rp = p->rp;
+    a.q = o->q_local;
+    a.dother = o->d - 1;
+    a.row_ptr = o->row_ptr.get();
+    a.idx = o->idx_o.get();
+    a.fac = p->fac.get();
+    for (int m = 0; m < o->d - 1; ++m) a.fac_off[m] = p->fac_off[m];
+    a.yhat = p->yhat_rm.get();
+    a.slot_a = p->slot_a.get();
+    a.slot_b = p->slot_b.get();
+    a.units = p->units;
+    a.chunk = p->chunk;
+    return a;
+}
+
+// y = vec(K Yhat + lambda Xhat) + rho x with Xhat = K X  (unaligned.hpp:101-115)
+void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    const double* kmat = p->mode->kernel.get();
+    {   // Xhat = K X -> column-major copy (lambda term) + row-major padded copy (K1 input)
+        GemmArgs g;
+        g.m = n; g.n = r; g.k = n;
+        g.a = kmat; g.a_rs = 1; g.a_cs = n;
+        g.b = x; g.b_rs = 1; g.b_cs = n;
+        g.c = p->xhat_cm.get(); g.c_rs = 1; g.c_cs = n;
+        g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
+        gemm(g, ctx->num_sms, ctx->stream);
+    }
+    SgArgs a = sg_args(p);
+    a.xhat = p->xhat_rm.get();
+    scatter_gather(a, ctx->stream);
+    allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+    {   // y = (K Yhat + lambda Xhat) + rho x
+        GemmArgs g;
+        g.m = n; g.n = r; g.k = n;
+        g.a = kmat; g.a_rs = 1; g.a_cs = n;
+        g.b = p->yhat_rm.get(); g.b_rs = p->rp; g.b_cs = 1;
+        g.c = y; g.c_rs = 1; g.c_cs = n;
+        g.epi = EPI_AXPY2;
+        g.e1 = p->xhat_cm.get(); g.e2 = x; g.ld_e = n;
+        g.beta1 = p->mode->lambda; g.beta2 = p->rho;
+        gemm(g, ctx->num_sms, ctx->stream);
+    }
+}
+
+// build_preconditioner (unaligned.hpp:120-134): eig(K) (cached), eig(V), D
+void ensure_precond(cphifi_unaligned p) {
+    mode_eig_once(p->mode);
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    if (!p->have_veig) {
+        p->uv.alloc(r * r);
+        p->sv.alloc(r);
+        device_sym_eig(ctx, p->v.get(), r, p->uv.get(), p->sv.get());
+        p->have_veig = true;
+    }
+    if (!p->dmat.n) {
+        p->dmat.alloc(n * r);
+        DevBuf<int> flag(1);
+        CPHIFI_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
+        precond_diag(p->mode->mu.get(), p->sv.get(), n, r, p->obs->density, p->mode->lambda, p->rho,
+                     p->dmat.get(), flag.get(), ctx->stream);
+        if (read_flag(ctx, flag.get())) {
+            p->dmat.release();
+            throw_runtime("build_preconditioner: nonpositive denominator");
+        }
+    }
+}
+
+// M^-1 x = U_K ((U_K' X U_V) .* D) U_V'   (unaligned.hpp:135-139), left-to-right
+void precond_dev(cphifi_unaligned p, const double* x, double* y) {
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    const double* uk = p->mode->u.get();
+    GemmArgs g;
+    g.m = n; g.n = r; g.k = n;                    // t1 = U_K' X
+    g.a = uk; g.a_rs = n; g.a_cs = 1;
+    g.b = x; g.b_rs = 1; g.b_cs = n;
+    g.c = p->t1.get(); g.c_rs = 1; g.c_cs = n;
+    gemm(g, ctx->num_sms, ctx->stream);
+    GemmArgs h;
+    h.m = n; h.n = r; h.k = r;                    // t2 = (t1 U_V) .* D
+    h.a = p->t1.get(); h.a_rs = 1; h.a_cs = n;
+    h.b = p->uv.get(); h.b_rs = 1; h.b_cs = r;
+    h.c = p->t2.get(); h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_HADAMARD; h.e1 = p->dmat.get(); h.ld_e = n;
+    gemm(h, ctx->num_sms, ctx->stream);
+    gemm_nn(ctx, n, r, n, uk, n, p->t2.get(), n, p->t1.get(), n);  // t1 = U_K t2
+    GemmArgs o;
+    o.m = n; o.n = r; o.k = r;                    // y = t1 U_V'
+    o.a = p->t1.get(); o.a_rs = 1; o.a_cs = n;
+    o.b = p->uv.get(); o.b_rs = r; o.b_cs = 1;
+    o.c = y; o.c_rs = 1; o.c_cs = n;
+    gemm(o, ctx->num_sms, ctx->stream);
+}
+
+// solve_aligned_decoupled core on device buffers (aligned.hpp:41-54)
+void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* uv, const double* sv, double* w,
+                   DevBuf<double>& t1, DevBuf<double>& core) {
+    cphifi_ctx ctx = mode->ctx;
+    const int64_t n = mode->n;
+    if (t1.n < (size_t)(n * r)) t1.alloc(n * r);
+    if (core.n < (size_t)(n * r)) core.alloc(n * r);
+    GemmArgs g;
+    g.m = n; g.n = r; g.k = n;                    // t1 = U_K' B
+    g.a = mode->u.get(); g.a_rs = n; g.a_cs = 1;
+    g.b = b; g.b_rs = 1; g.b_cs = n;
+    g.c = t1.get(); g.c_rs = 1; g.c_cs = n;
+    gemm(g, ctx->num_sms, ctx->stream);
+    DevBuf<int> flag(1);
+    CPHIFI_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
+    GemmArgs h;
+    h.m = n; h.n = r; h.k = r;                    // core = (t1 U_V) ./ (sigma_j mu_i + lambda)
+    h.a = t1.get(); h.a_rs = 1; h.a_cs = n;
+    h.b = uv; h.b_rs = 1; h.b_cs = r;
+    h.c = core.get(); h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_SCALE_DIV; h.e_row = mode->mu.get(); h.e_col = sv; h.beta1 = mode->lambda;
+    h.flag = flag.get();
+    gemm(h, ctx->num_sms, ctx->stream);
+    if (read_flag(ctx, flag.get()))
+        throw_runtime("solve_aligned_decoupled: zero eigenvalue pair; use lambda > 0");
+    gemm_nn(ctx, n, r, n, mode->u.get(), n, core.get(), n, t1.get(), n);  // U_K core
+    GemmArgs o;
+    o.m = n; o.n = r; o.k = r;                    // W = (.) U_V'
+    o.a = t1.get(); o.a_rs = 1; o.a_cs = n;
+    o.b = uv; o.b_rs = r; o.b_cs = 1;
+    o.c = w; o.c_rs = 1; o.c_cs = n;
+    gemm(o, ctx->num_sms, ctx->stream);
+}
+
+void upload_factors_cm(cphifi_ctx ctx, int d, const int64_t* shape, int k, int64_t r, const double* const* factors,
+                       DevBuf<double>& buf, std::vector<const double*>& ptrs) {
+    int64_t tot = 0;
+    for (int m = 0; m < d; ++m)
+        if (m != k) tot += shape[m] * r;
+    buf.alloc(std::max<int64_t>(tot, 1));
+    ptrs.assign(d, nullptr);
+    int64_t off = 0;
+    for (int m = 0; m < d; ++m) {
+        if (m == k) continue;
+        need(factors[m], "factor");
+        h2d(buf.get() + off, factors[m], sizeof(double) * shape[m] * r, ctx->stream);
+        ptrs[m] = buf.get() + off;
+        off += shape[m] * r;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cphifi_last_error(void) { return g_last_error.c_str(); }
+int cphifi_abi_version(void) { return CPHIFI_ABI_VERSION; }
+
+// ---- context -------------------------------------------------------------------------
+int cphifi_ctx_create(int device, cphifi_ctx* out) {
+    return guard([&] {
+        need(out, "cphifi_ctx_create");
+        int count = 0;
+        CPHIFI_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) throw_invalid("cphifi_ctx_create: device out of range");
+        CPHIFI_CUDA(cudaSetDevice(device));
+        auto* c = new cphifi_ctx_s;
+        c->device = device;
+        CPHIFI_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CPHIFI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CPHIFI_SOLVER(cusolverDnCreate(&c->solver));
+        CPHIFI_SOLVER(cusolverDnSetStream(c->solver, c->stream));
+        CPHIFI_CUDA(cudaEventCreate(&c->ev0));
+        CPHIFI_CUDA(cudaEventCreate(&c->ev1));
+        CPHIFI_CUDA(cudaMallocHost(&c->host_scalars, 64 * sizeof(double)));
+        *out = c;
+    });
+}
+
+int cphifi_ctx_destroy(cphifi_ctx ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        DeviceGuard dg(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
+        if (ctx->solver) cusolverDnDestroy(ctx->solver);
+        if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+        if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+        if (ctx->host_scalars) cudaFreeHost(ctx->host_scalars);
+        if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int cphifi_ctx_synchronize(cphifi_ctx ctx) {
+    return guard([&] {
+        need(ctx, "ctx");
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cphifi_ctx_stream(cphifi_ctx ctx, void** stream_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(stream_out, "stream_out");
+        *stream_out = (void*)ctx->stream;
+    });
+}
+
+int cphifi_comm_unique_id(uint8_t id_out[128]) {
+    return guard([&] {
+        need(id_out, "id_out");
+        ncclUniqueId id;
+        CPHIFI_NCCL(ncclGetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(id_out, &id, 128);
+    });
+}
+
+int cphifi_ctx_init_comm(cphifi_ctx ctx, int nranks, int rank, const uint8_t id[128]) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(id, "id");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw_invalid("cphifi_ctx_init_comm: bad rank");
+        DeviceGuard dg(ctx->device);
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+        CPHIFI_NCCL(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+    });
+}
+
+int cphifi_ctx_world(cphifi_ctx ctx, int* nranks, int* rank) {
+    return guard([&] {
+        need(ctx, "ctx");
+        if (nranks) *nranks = ctx->nranks;
+        if (rank) *rank = ctx->rank;
+    });
+}
+
+// ---- modes (kernel.hpp:17-30, 53-101) -----------------------------------------------
+int cphifi_mode_create_gaussian(cphifi_ctx ctx, int64_t n, const double* points, double sigma, double lambda,
+                                cphifi_mode* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (n < 1) throw_invalid("RkhsMode: empty design");
+        need(points, "points");
+        if (sigma <= 0.0) throw_invalid("gaussian_kernel: sigma must be positive");
+        if (lambda < 0.0) throw_invalid("RkhsMode: lambda must be nonnegative");
+        DeviceGuard dg(ctx->device);
+        cphifi_mode m = new_mode(ctx, n, lambda);
+        DevBuf<double> pts(n);
+        h2d(pts.get(), points, sizeof(double) * n, ctx->stream);
+        kernel_matrix(0, pts.get(), n, 1.0 / (2.0 * sigma * sigma), m->kernel.get(), ctx->stream);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = m;
+    });
+}
+
+int cphifi_mode_create_matern32(cphifi_ctx ctx, int64_t n, const double* points, double lengthscale,
+                                double lambda, cphifi_mode* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (n < 1) throw_invalid("RkhsMode: empty design");
+        need(points, "points");
+        if (lengthscale <= 0.0) throw_invalid("matern32_kernel: lengthscale must be positive");
+        if (lambda < 0.0) throw_invalid("RkhsMode: lambda must be nonnegative");
+        DeviceGuard dg(ctx->device);
+        cphifi_mode m = new_mode(ctx, n, lambda);
+        DevBuf<double> pts(n);
+        h2d(pts.get(), points, sizeof(double) * n, ctx->stream);
+        kernel_matrix(1, pts.get(), n, std::sqrt(3.0) / lengthscale, m->kernel.get(), ctx->stream);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = m;
+    });
+}
+
+int cphifi_mode_create(cphifi_ctx ctx, int64_t n, const double* kernel, double lambda, cphifi_mode* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        need(kernel, "kernel");
+        if (n < 1) throw_invalid("RkhsMode: empty design");
+        if (lambda < 0.0) throw_invalid("RkhsMode: lambda must be nonnegative");
+        DeviceGuard dg(ctx->device);
+        cphifi_mode m = new_mode(ctx, n, lambda);
+        h2d(m->kernel.get(), kernel, sizeof(double) * n * n, ctx->stream);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = m;
+    });
+}
+
+int cphifi_mode_destroy(cphifi_mode mode) {
+    return guard([&] {
+        if (!mode) return;
+        DeviceGuard dg(mode->ctx->device);
+        cudaStreamSynchronize(mode->ctx->stream);
+        delete mode;
+    });
+}
+
+int cphifi_mode_size(cphifi_mode mode, int64_t* n) {
+    return guard([&] { need(mode, "mode"); need(n, "n"); *n = mode->n; });
+}
+int cphifi_mode_lambda(cphifi_mode mode, double* lambda) {
+    return guard([&] { need(mode, "mode"); need(lambda, "lambda"); *lambda = mode->lambda; });
+}
+int cphifi_mode_get_kernel(cphifi_mode mode, double* kernel_out) {
+    return guard([&] {
+        need(mode, "mode");
+        need(kernel_out, "kernel_out");
+        DeviceGuard dg(mode->ctx->device);
+        d2h_sync(kernel_out, mode->kernel.get(), sizeof(double) * mode->n * mode->n, mode->ctx->stream);
+    });
+}
+int cphifi_mode_eig(cphifi_mode mode) {
+    return guard([&] {
+        need(mode, "mode");
+        mode_eig_once(mode);
+    });
+}
+int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
+    return guard([&] {
+        need(mode, "mode");
+        need(u, "u");
+        need(mu, "mu");
+        DeviceGuard dg(mode->ctx->device);
+        std::lock_guard<std::mutex> lk(mode->mu_lock);
+        const int64_t n = mode->n;
+        mode->u.alloc(n * n);
+        mode->mu.alloc(n);
+        h2d(mode->u.get(), u, sizeof(double) * n * n, mode->ctx->stream);
+        h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
+        clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);
+        CPHIFI_CUDA(cudaStreamSynchronize(mode->ctx->stream));
+        mode->have_eig = true;
+        mode->eig_count = 1;
+    });
+}
+int cphifi_mode_get_eig(cphifi_mode mode, double* u_out, double* mu_out) {
+    return guard([&] {
+        need(mode, "mode");
+        mode_eig_once(mode);
+        DeviceGuard dg(mode->ctx->device);
+        if (u_out) d2h_sync(u_out, mode->u.get(), sizeof(double) * mode->n * mode->n, mode->ctx->stream);
+        if (mu_out) d2h_sync(mu_out, mode->mu.get(), sizeof(double) * mode->n, mode->ctx->stream);
+    });
+}
+int cphifi_mode_eig_count(cphifi_mode mode, int* count) {
+    return guard([&] { need(mode, "mode"); need(count, "count"); *count = mode->eig_count; });
+}
+
+// ---- observations (observations.hpp:18-79) --------------------------------------------
+int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, const int32_t* idx,
+                      const double* values, int k, uint32_t flags, int shard, int shards, cphifi_obs* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        need(shape, "shape");
+        if (d < 2 || d > 6) throw_invalid("ObservationSet: tensor order must be in [2, 6]");
+        if (k < 0 || k >= d) throw_invalid("ObservationSet: mode out of range");
+        if (q < 0) throw_invalid("ObservationSet: index/value count mismatch");
+        if (q > (int64_t)INT32_MAX) throw_invalid("ObservationSet: more than 2^31-1 observations per plan");
+        if (shards < 1 || shard < 0 || shard >= shards) throw_invalid("ObservationSet: bad shard");
+        double ntot = 1.0;
+        for (int m = 0; m < d; ++m) {
+            if (shape[m] <= 0) throw_invalid("DenseTensor: nonpositive mode size");
+            if (shape[m] > (int64_t)INT32_MAX) throw_invalid("ObservationSet: mode size exceeds int32");
+        }
+        int64_t ntot_i = 1;
+        for (int m = 0; m < d; ++m) ntot_i *= shape[m];
+        ntot = (double)ntot_i;
+        if (q > 0) {
+            need(idx, "idx");
+            need(values, "values");
+        }
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const bool dev_in = flags & CPHIFI_OBS_DEVICE_INPUT;
+        auto* o = new cphifi_obs_s;
+        std::unique_ptr<cphifi_obs_s> hold(o);
+        o->ctx = ctx;
+        o->d = d;
+        o->k = k;
+        o->shape.assign(shape, shape + d);
+        o->q_total = q;
+        o->density = (double)q / ntot;
+        const int64_t nk = shape[k];
+
+        DevBuf<int32_t> idx_up;
+        DevBuf<double> val_up;
+        const int32_t* didx = idx;
+        const double* dval = values;
+        if (!dev_in && q > 0) {
+            idx_up.alloc((size_t)d * q);
+            val_up.alloc(q);
+            h2d(idx_up.get(), idx, sizeof(int32_t) * d * q, s);
+            h2d(val_up.get(), values, sizeof(double) * q, s);
+            didx = idx_up.get();
+            dval = val_up.get();
+        }
+        DevBuf<int> flag(1);
+        DevBuf<int64_t> dshape(d);
+        CPHIFI_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), s));
+        h2d(dshape.get(), shape, sizeof(int64_t) * d, s);
+        check_range(didx, d, q, dshape.get(), flag.get(), s);
+        if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: index out of range");
+        if ((flags & CPHIFI_OBS_REJECT_DUPLICATES) && q > 1) {
+            std::vector<int64_t> stride(d);
+            int64_t st = 1;
+            for (int m = 0; m < d; ++m) { stride[m] = st; st *= shape[m]; }
+            h2d(dshape.get(), stride.data(), sizeof(int64_t) * d, s);
+            DevBuf<uint64_t> lin(q), lin2(q);
+            linear_index(didx, d, q, dshape.get(), lin.get(), s);
+            const size_t tb = radix_sort_keys64_bytes(q);
+            DevBuf<unsigned char> tmp(tb);
+            radix_sort_keys64(tmp.get(), tb, lin.get(), lin2.get(), q, s);
+            adjacent_equal(lin2.get(), q, flag.get(), s);
+            if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: duplicate index");
+        }
+        // stable sort by i_k -> permutation
+        const int64_t lo = q * shard / shards, hi = q * (shard + 1) / shards;
+        const int64_t ql = hi - lo;
+        o->q_local = ql;
+        DevBuf<int32_t> keys_out(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
+            perm_out(std::max<int64_t>(q, 1));
+        if (q > 0) {
+            int bits = 1;
+            while ((int64_t(1) << bits) < nk) ++bits;
+            iota32(perm_in.get(), q, s);
+            const size_t tb = radix_sort_pairs_bytes(q, bits);
+            DevBuf<unsigned char> tmp(tb);
+            radix_sort_pairs(tmp.get(), tb, didx + (int64_t)k * q, keys_out.get(), perm_in.get(), perm_out.get(), q,
+                             bits, s);
+        }
+        o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * ql, 1));
+        o->values.alloc(std::max<int64_t>(ql, 1));
+        int mm = 0;
+        for (int m = 0; m < d; ++m) {
+            if (m == k) continue;
+            gather_i32(didx + (int64_t)m * q, perm_out.get(), lo, ql, o->idx_o.get() + (int64_t)mm * ql, s);
+            ++mm;
+        }
+        gather_f64(dval, perm_out.get(), lo, ql, o->values.get(), s);
+        o->row_ptr.alloc(nk + 1);
+        csr_from_sorted(keys_out.get() + lo, ql, nk, o->row_ptr.get(), s);
+        CPHIFI_CUDA(cudaStreamSynchronize(s));
+        *out = hold.release();
+    });
+}
+
+int cphifi_obs_destroy(cphifi_obs obs) {
+    return guard([&] {
+        if (!obs) return;
+        DeviceGuard dg(obs->ctx->device);
+        cudaStreamSynchronize(obs->ctx->stream);
+        delete obs;
+    });
+}
+
+int cphifi_obs_info(cphifi_obs obs, int64_t* q_total, int64_t* q_local, double* density) {
+    return guard([&] {
+        need(obs, "obs");
+        if (q_total) *q_total = obs->q_total;
+        if (q_local) *q_local = obs->q_local;
+        if (density) *density = obs->density;
+    });
+}
+
+// ---- unaligned subproblem (unaligned.hpp:35-48) ----------------------------------------
+int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const double* const* factors, double rho,
+                            cphifi_unaligned* out) {
+    return guard([&] {
+        need(obs, "obs");
+        need(mode, "mode");
+        need(factors, "factors");
+        need(out, "out");
+        if (r < 1) throw_invalid("KruskalModel: rank must be positive");
+        if (r > 128) throw_invalid("unaligned: rank above 128 is not supported");
+        if (mode->n != obs->shape[obs->k]) throw_invalid("unaligned: kernel size mismatch");
+        cphifi_ctx ctx = obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        auto* p = new cphifi_unaligned_s;
+        std::unique_ptr<cphifi_unaligned_s> hold(p);
+        p->obs = obs;
+        p->mode = mode;
+        p->n = mode->n;
+        p->r = r;
+        p->rp = pow2_at_least(r, 4);
+        p->rho = rho;
+        const int d = obs->d, k = obs->k;
+        // factors: column-major upload, then row-major padded packing for the K1 gathers
+        DevBuf<double> fcm;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, d, obs->shape.data(), k, r, factors, fcm, fptr);
+        int64_t tot = 0;
+        p->fac_off.clear();
+        for (int m = 0; m < d; ++m) {
+            if (m == k) continue;
+            p->fac_off.push_back(tot);
+            tot += obs->shape[m] * p->rp;
+        }
+        p->fac.alloc(tot);
+        int mm = 0;
+        for (int m = 0; m < d; ++m) {
+            if (m == k) continue;
+            pack_rows(fptr[m], obs->shape[m], obs->shape[m], r, p->rp, p->fac.get() + p->fac_off[mm], s);
+            ++mm;
+        }
+        // V = gram_khatri_rao (tensor.hpp:186-194)
+        p->v.alloc(r * r);
+        gram_kr(d, obs->shape.data(), r, fptr.data(), k, p->v.get(), s);
+        // scratch
+        const int64_t n = p->n;
+        sg_plan(obs->q_local, p->rp, ctx->num_sms, &p->units, &p->chunk);
+        p->slot_a.alloc(p->units * p->rp);
+        p->slot_b.alloc(p->units * p->rp);
+        p->xhat_rm.alloc(n * p->rp);
+        p->yhat_rm.alloc(n * p->rp);
+        p->xhat_cm.alloc(n * r);
+        p->t1.alloc(n * r);
+        p->t2.alloc(n * r);
+        p->vx.alloc(n * r);
+        p->vy.alloc(n * r);
+        // B = sampled_mttkrp(obs, zhat, k) with the observed values (observations.hpp:186-188)
+        SgArgs a = sg_args(p);
+        a.weights = obs->values.get();
+        scatter_gather(a, s);
+        allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+        p->b.alloc(n * r);
+        rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->b.get(), s);
+        CPHIFI_CUDA(cudaStreamSynchronize(s));
+        *out = hold.release();
+    });
+}
+
+int cphifi_unaligned_destroy(cphifi_unaligned p) {
+    return guard([&] {
+        if (!p) return;
+        DeviceGuard dg(p->obs->ctx->device);
+        cudaStreamSynchronize(p->obs->ctx->stream);
+        delete p;
+    });
+}
+
+int cphifi_unaligned_get_b(cphifi_unaligned p, double* b_out) {
+    return guard([&] {
+        need(p, "p");
+        need(b_out, "b_out");
+        DeviceGuard dg(p->obs->ctx->device);
+        d2h_sync(b_out, p->b.get(), sizeof(double) * p->n * p->r, p->obs->ctx->stream);
+    });
+}
+int cphifi_unaligned_get_v(cphifi_unaligned p, double* v_out) {
+    return guard([&] {
+        need(p, "p");
+        need(v_out, "v_out");
+        DeviceGuard dg(p->obs->ctx->device);
+        d2h_sync(v_out, p->v.get(), sizeof(double) * p->r * p->r, p->obs->ctx->stream);
+    });
+}
+
+int cphifi_unaligned_matvec_device(cphifi_unaligned p, const double* x, double* y) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        DeviceGuard dg(p->obs->ctx->device);
+        matvec_dev(p, x, y);
+    });
+}
+
+int cphifi_unaligned_matvec(cphifi_unaligned p, const double* x, double* y) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        const size_t bytes = sizeof(double) * p->n * p->r;
+        h2d(p->vx.get(), x, bytes, ctx->stream);
+        matvec_dev(p, p->vx.get(), p->vy.get());
+        d2h_sync(y, p->vy.get(), bytes, ctx->stream);
+    });
+}
+
+int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters, double* ms_out) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        need(ms_out, "ms_out");
+        if (iters < 1) throw_invalid("cphifi_unaligned_matvec_timed: iters must be positive");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const int64_t n = p->n, r = p->r;
+        cudaEvent_t ev[6];
+        for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        const double* kmat = p->mode->kernel.get();
+        for (int it = 0; it < iters; ++it) {
+            CPHIFI_CUDA(cudaEventRecord(ev[0], s));
+            GemmArgs g;
+            g.m = n; g.n = r; g.k = n;
+            g.a = kmat; g.a_rs = 1; g.a_cs = n;
+            g.b = x; g.b_rs = 1; g.b_cs = n;
+            g.c = p->xhat_cm.get(); g.c_rs = 1; g.c_cs = n;
+            g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
+            gemm(g, ctx->num_sms, s);
+            CPHIFI_CUDA(cudaEventRecord(ev[1], s));
+            SgArgs a = sg_args(p);
+            a.xhat = p->xhat_rm.get();
+            sg_main(a, s);
+            CPHIFI_CUDA(cudaEventRecord(ev[2], s));
+            sg_fixup(a, s);
+            CPHIFI_CUDA(cudaEventRecord(ev[3], s));
+            allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+            CPHIFI_CUDA(cudaEventRecord(ev[4], s));
+            GemmArgs h;
+            h.m = n; h.n = r; h.k = n;
+            h.a = kmat; h.a_rs = 1; h.a_cs = n;
+            h.b = p->yhat_rm.get(); h.b_rs = p->rp; h.b_cs = 1;
+            h.c = y; h.c_rs = 1; h.c_cs = n;
+            h.epi = EPI_AXPY2;
+            h.e1 = p->xhat_cm.get(); h.e2 = x; h.ld_e = n;
+            h.beta1 = p->mode->lambda; h.beta2 = p->rho;
+            gemm(h, ctx->num_sms, s);
+            CPHIFI_CUDA(cudaEventRecord(ev[5], s));
+            CPHIFI_CUDA(cudaEventSynchronize(ev[5]));
+            float ms;
+            for (int ph = 0; ph < 5; ++ph) {
+                CPHIFI_CUDA(cudaEventElapsedTime(&ms, ev[ph], ev[ph + 1]));
+                acc[ph] += ms;
+            }
+            CPHIFI_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[5]));
+            acc[5] += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int i = 0; i < 6; ++i) ms_out[i] = acc[i] / iters;
+    });
+}
+
+int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, double* yhat_out) {
+    return guard([&] {
+        need(p, "p");
+        need(xhat, "xhat");
+        need(yhat_out, "yhat_out");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        const int64_t n = p->n, r = p->r;
+        h2d(p->vx.get(), xhat, sizeof(double) * n * r, ctx->stream);
+        pack_rows(p->vx.get(), n, n, r, p->rp, p->xhat_rm.get(), ctx->stream);
+        SgArgs a = sg_args(p);
+        a.xhat = p->xhat_rm.get();
+        scatter_gather(a, ctx->stream);
+        allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+        rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->vy.get(), ctx->stream);
+        d2h_sync(yhat_out, p->vy.get(), sizeof(double) * n * r, ctx->stream);
+    });
+}
+
+int cphifi_unaligned_set_v_eig(cphifi_unaligned p, const double* u_v, const double* sigma_v) {
+    return guard([&] {
+        need(p, "p");
+        need(u_v, "u_v");
+        need(sigma_v, "sigma_v");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        const int64_t r = p->r;
+        p->uv.alloc(r * r);
+        p->sv.alloc(r);
+        h2d(p->uv.get(), u_v, sizeof(double) * r * r, ctx->stream);
+        h2d(p->sv.get(), sigma_v, sizeof(double) * r, ctx->stream);
+        clamp_nonneg(p->sv.get(), r, ctx->stream);
+        p->have_veig = true;
+        p->dmat.release();
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cphifi_unaligned_get_v_eig(cphifi_unaligned p, double* u_v_out, double* sigma_v_out) {
+    return guard([&] {
+        need(p, "p");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        ensure_precond(p);
+        if (u_v_out) d2h_sync(u_v_out, p->uv.get(), sizeof(double) * p->r * p->r, ctx->stream);
+        if (sigma_v_out) d2h_sync(sigma_v_out, p->sv.get(), sizeof(double) * p->r, ctx->stream);
+    });
+}
+
+int cphifi_unaligned_precond_apply_device(cphifi_unaligned p, const double* x, double* y) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        DeviceGuard dg(p->obs->ctx->device);
+        ensure_precond(p);
+        precond_dev(p, x, y);
+    });
+}
+
+int cphifi_unaligned_precond_apply(cphifi_unaligned p, const double* x, double* y) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        ensure_precond(p);
+        const size_t bytes = sizeof(double) * p->n * p->r;
+        h2d(p->vx.get(), x, bytes, ctx->stream);
+        precond_dev(p, p->vx.get(), p->vy.get());
+        d2h_sync(y, p->vy.get(), bytes, ctx->stream);
+    });
+}
+
+// solve_unaligned_pcg (unaligned.hpp:143-161) + pcg (solvers.hpp:38-88)
+int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg, cphifi_solve_report* report,
+                               const double* warm_start, double* w_out) {
+    return guard([&] {
+        need(p, "p");
+        need(cfg, "cfg");
+        need(w_out, "w_out");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const auto t0 = std::chrono::steady_clock::now();
+        if (p->rho <= 0.0) throw_invalid("solve_unaligned_pcg: rho must be positive");
+        const int64_t n = p->n, r = p->r, nr = n * r;
+        DevBuf<double> bvec(nr), x(nr), res(nr), z(nr), pv(nr), ap(nr);
+        DevBuf<double> partial(80);  // 64 partials + ticket
+        DevBuf<PcgState> st(1);
+        CPHIFI_CUDA(cudaMemsetAsync(partial.get(), 0, sizeof(double) * 80, s));
+        CPHIFI_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(PcgState), s));
+        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec.get(), n);  // rhs = vec(K B)
+        ensure_precond(p);                                                                 // build_preconditioner
+        if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
+        const auto t_setup = std::chrono::steady_clock::now();
+        double* hs = ctx->host_scalars;
+        dot_to(bvec.get(), bvec.get(), nr, partial.get(), &st.get()->bnorm, s);
+        d2h_sync(hs, &st.get()->bnorm, sizeof(double), s);
+        const double bnorm = std::sqrt(hs[0]);
+        std::vector<double> hist;
+        cphifi_solve_report rep{};
+        int matvecs = 0;
+        if (bnorm == 0.0) {
+            CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
+            rep.converged = 1;
+        } else {
+            CPHIFI_CUDA(cudaMemcpyAsync(&st.get()->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
+            if (warm_start) {
+                h2d(x.get(), warm_start, sizeof(double) * nr, s);
+                matvec_dev(p, x.get(), ap.get());
+                ++matvecs;
+                axpby(res.get(), bvec.get(), 1.0, ap.get(), -1.0, nr, s);  // r = b - A x0
+            } else {
+                CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
+                CPHIFI_CUDA(cudaMemcpyAsync(res.get(), bvec.get(), sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
+            }
+            precond_dev(p, res.get(), z.get());
+            pcg_init(res.get(), z.get(), pv.get(), nr, st.get(), partial.get(), s);
+            PcgState hst;
+            d2h_sync(&hst, st.get(), sizeof(PcgState), s);
+            double rel = hst.rel;
+            if (cfg->record_history) hist.push_back(rel);
+            int it = 0;
+            while (rel > cfg->tol && it < cfg->max_iter) {
+                matvec_dev(p, pv.get(), ap.get());
+                ++matvecs;
+                pcg_step_a(x.get(), res.get(), pv.get(), ap.get(), nr, st.get(), partial.get(), s);
+                d2h_sync(&hst, st.get(), sizeof(PcgState), s);
+                if (hst.flag == 1) throw_runtime("pcg: non-finite value encountered");
+                if (hst.flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
+                ++it;
+                rel = hst.rel;
+                if (cfg->record_history) hist.push_back(rel);
+                if (rel <= cfg->tol) break;
+                precond_dev(p, res.get(), z.get());
+                pcg_step_b(res.get(), z.get(), pv.get(), nr, st.get(), partial.get(), s);
+            }
+            rep.iterations = it;
+            rep.relative_residual = rel;
+            rep.converged = rel <= cfg->tol;
+        }
+        d2h_sync(w_out, x.get(), sizeof(double) * nr, s);
+        const auto t1 = std::chrono::steady_clock::now();
+        rep.wall_time_s = std::chrono::duration<double>(t1 - t0).count();
+        rep.setup_s = std::chrono::duration<double>(t_setup - t0).count();
+        rep.matvecs = matvecs;
+        if (report) {
+            double* hbuf = report->residual_history;
+            const int cap = report->history_capacity;
+            rep.residual_history = hbuf;
+            rep.history_capacity = cap;
+            rep.history_len = (int32_t)hist.size();
+            if (hbuf) std::memcpy(hbuf, hist.data(), sizeof(double) * std::min<size_t>(hist.size(), (size_t)std::max(cap, 0)));
+            *report = rep;
+        }
+    });
+}
+
+// ---- aligned path ----------------------------------------------------------------------
+int cphifi_tensor_create(cphifi_ctx ctx, int d, const int64_t* shape, const double* data, uint32_t flags, int shard,
+                         int shards, cphifi_tensor* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(shape, "shape");
+        need(data, "data");
+        need(out, "out");
+        if (d < 2 || d > 8) throw_invalid("DenseTensor: order must be in [2, 8]");
+        for (int m = 0; m < d; ++m)
+            if (shape[m] <= 0) throw_invalid("DenseTensor: nonpositive mode size");
+        if (shards < 1 || shard < 0 || shard >= shards) throw_invalid("DenseTensor: bad shard");
+        DeviceGuard dg(ctx->device);
+        auto* t = new cphifi_tensor_s;
+        std::unique_ptr<cphifi_tensor_s> hold(t);
+        t->ctx = ctx;
+        t->d = d;
+        t->shape.assign(shape, shape + d);
+        t->slab_lo = shape[1] * shard / shards;
+        t->slab_hi = shape[1] * (shard + 1) / shards;
+        const int64_t n0 = shape[0], n1 = shape[1], w = t->slab_hi - t->slab_lo;
+        int64_t rest = 1;
+        for (int m = 2; m < d; ++m) rest *= shape[m];
+        t->data.alloc(std::max<int64_t>(n0 * w * rest, 1));
+        if (flags & CPHIFI_TENSOR_DEVICE_INPUT) {
+            CPHIFI_CUDA(cudaMemcpyAsync(t->data.get(), data, sizeof(double) * n0 * w * rest, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+        } else if (w > 0) {
+            CPHIFI_CUDA(cudaMemcpy2DAsync(t->data.get(), sizeof(double) * n0 * w, data + n0 * t->slab_lo,
+                                          sizeof(double) * n0 * n1, sizeof(double) * n0 * w, rest,
+                                          cudaMemcpyHostToDevice, ctx->stream));
+        }
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = hold.release();
+    });
+}
+
+int cphifi_tensor_destroy(cphifi_tensor t) {
+    return guard([&] {
+        if (!t) return;
+        DeviceGuard dg(t->ctx->device);
+        cudaStreamSynchronize(t->ctx->stream);
+        delete t;
+    });
+}
+
+namespace {
+void mttkrp_dev(cphifi_tensor t, int k, int64_t r, const std::vector<const double*>& fptr, double* b_dev,
+                DevBuf<double>& work) {
+    if (k != 0) throw_invalid("mttkrp: only the infinite mode k = 0 is accelerated");
+    cphifi_ctx ctx = t->ctx;
+    MttkrpArgs a;
+    a.d = t->d;
+    for (int m = 0; m < t->d; ++m) {
+        a.shape[m] = t->shape[m];
+        a.fac[m] = fptr[m];
+        a.ld[m] = t->shape[m];
+    }
+    a.shape[1] = t->slab_hi - t->slab_lo;
+    a.off1 = t->slab_lo;
+    a.r = r;
+    a.t = t->data.get();
+    a.b = b_dev;
+    if (a.shape[1] > 0) {
+        mttkrp_mode0(a, ctx->num_sms, ctx->stream, work);
+    } else {
+        CPHIFI_CUDA(cudaMemsetAsync(b_dev, 0, sizeof(double) * t->shape[0] * r, ctx->stream));
+    }
+    allreduce(ctx, b_dev, (size_t)t->shape[0] * r);
+}
+}  // namespace
+
+int cphifi_mttkrp(cphifi_tensor t, int k, int64_t r, const double* const* factors, double* b_out) {
+    return guard([&] {
+        need(t, "tensor");
+        need(factors, "factors");
+        need(b_out, "b_out");
+        if (k < 0 || k >= t->d) throw_invalid("unfold: mode out of range");
+        if (r < 1) throw_invalid("KruskalModel: rank must be positive");
+        cphifi_ctx ctx = t->ctx;
+        DeviceGuard dg(ctx->device);
+        DevBuf<double> fbuf, b(t->shape[0] * r), work;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
+        mttkrp_dev(t, k, r, fptr, b.get(), work);
+        d2h_sync(b_out, b.get(), sizeof(double) * t->shape[0] * r, ctx->stream);
+    });
+}
+
+int cphifi_gram_khatri_rao(cphifi_ctx ctx, int d, const int64_t* shape, int64_t r, const double* const* factors,
+                           int k, double* v_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(shape, "shape");
+        need(factors, "factors");
+        need(v_out, "v_out");
+        if (d < 1 || d > 8) throw_invalid("KruskalModel: bad order");
+        if (r < 1) throw_invalid("KruskalModel: rank must be positive");
+        DeviceGuard dg(ctx->device);
+        DevBuf<double> fbuf, v(r * r);
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, d, shape, k, r, factors, fbuf, fptr);
+        gram_kr(d, shape, r, fptr.data(), k, v.get(), ctx->stream);
+        d2h_sync(v_out, v.get(), sizeof(double) * r * r, ctx->stream);
+    });
+}
+
+int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b, const double* v, const double* u_v,
+                                   const double* sigma_v, double* w_out) {
+    return guard([&] {
+        need(mode, "mode");
+        need(b, "b");
+        need(w_out, "w_out");
+        if (r < 1) throw_invalid("solve_aligned_decoupled: rank must be positive");
+        if (!(u_v && sigma_v)) need(v, "v");
+        cphifi_ctx ctx = mode->ctx;
+        DeviceGuard dg(ctx->device);
+        mode_eig_once(mode);
+        const int64_t n = mode->n;
+        DevBuf<double> db(n * r), uv(r * r), sv(r), w(n * r), t1, core;
+        h2d(db.get(), b, sizeof(double) * n * r, ctx->stream);
+        if (u_v && sigma_v) {
+            h2d(uv.get(), u_v, sizeof(double) * r * r, ctx->stream);
+            h2d(sv.get(), sigma_v, sizeof(double) * r, ctx->stream);
+            clamp_nonneg(sv.get(), r, ctx->stream);
+        } else {
+            DevBuf<double> dv(r * r);
+            h2d(dv.get(), v, sizeof(double) * r * r, ctx->stream);
+            device_sym_eig(ctx, dv.get(), r, uv.get(), sv.get());
+        }
+        decoupled_dev(mode, r, db.get(), uv.get(), sv.get(), w.get(), t1, core);
+        d2h_sync(w_out, w.get(), sizeof(double) * n * r, ctx->stream);
+    });
+}
+
+int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, const double* const* factors,
+                         double* w_out, double* b_out, double* v_out) {
+    return guard([&] {
+        need(t, "tensor");
+        need(mode, "mode");
+        need(factors, "factors");
+        need(w_out, "w_out");
+        if (k < 0 || k >= t->d) throw_invalid("unfold: mode out of range");
+        if (mode->n != t->shape[k]) throw_invalid("aligned: kernel size mismatch");
+        cphifi_ctx ctx = t->ctx;
+        DeviceGuard dg(ctx->device);
+        mode_eig_once(mode);
+        const int64_t n = mode->n;
+        DevBuf<double> fbuf, b(n * r), v(r * r), uv(r * r), sv(r), w(n * r), t1, core, work;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
+        mttkrp_dev(t, k, r, fptr, b.get(), work);
+        gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), ctx->stream);
+        device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());
+        decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+        d2h_sync(w_out, w.get(), sizeof(double) * n * r, ctx->stream);
+        if (b_out) d2h_sync(b_out, b.get(), sizeof(double) * n * r, ctx->stream);
+        if (v_out) d2h_sync(v_out, v.get(), sizeof(double) * r * r, ctx->stream);
+    });
+}
+
+}  // extern "C"

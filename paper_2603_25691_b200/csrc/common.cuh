@@ -1,0 +1,154 @@
+// common.cuh — shared internals of libcphifi_b200 (not part of the public ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cphifi_b200.h"
+
+namespace cphifi {
+
+// ---- error plumbing: C++ exceptions inside, int status at the ABI --------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void throw_invalid(const std::string& m) { throw Error(CPHIFI_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void throw_runtime(const std::string& m) { throw Error(CPHIFI_RUNTIME_ERROR, m); }
+
+void set_last_error(const std::string& m);
+
+#define CPHIFI_CUDA(call)                                                                   \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            throw ::cphifi::Error(CPHIFI_CUDA_ERROR, std::string(#call) + ": " +             \
+                                                         cudaGetErrorString(e_));           \
+    } while (0)
+#define CPHIFI_CHECK_LAUNCH() CPHIFI_CUDA(cudaGetLastError())
+#define CPHIFI_NCCL(call)                                                                   \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            throw ::cphifi::Error(CPHIFI_NCCL_ERROR, std::string(#call) + ": " +             \
+                                                         ncclGetErrorString(r_));           \
+    } while (0)
+#define CPHIFI_SOLVER(call)                                                                 \
+    do {                                                                                    \
+        cusolverStatus_t s_ = (call);                                                       \
+        if (s_ != CUSOLVER_STATUS_SUCCESS)                                                  \
+            throw ::cphifi::Error(CPHIFI_CUDA_ERROR,                                        \
+                                  std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
+    } while (0)
+
+// ---- device buffer (RAII) ------------------------------------------------------------
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) CPHIFI_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+inline int64_t pow2_at_least(int64_t v, int64_t lo) {
+    int64_t p = lo;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace cphifi
+
+// ---- opaque handle definitions -------------------------------------------------------
+struct cphifi_ctx_s {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cusolverDnHandle_t solver = nullptr;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // pinned scratch for small D2H reads (PCG scalars)
+    double* host_scalars = nullptr;
+};
+
+struct cphifi_mode_s {
+    cphifi_ctx ctx = nullptr;
+    int64_t n = 0;
+    double lambda = 0.0;
+    cphifi::DevBuf<double> kernel;  // n x n column-major (symmetric)
+    cphifi::DevBuf<double> u;       // eigenvectors, n x n column-major
+    cphifi::DevBuf<double> mu;      // eigenvalues (ascending, clamped at 0)
+    std::once_flag once;
+    bool have_eig = false;
+    int eig_count = 0;
+    std::mutex mu_lock;
+};
+
+struct cphifi_obs_s {
+    cphifi_ctx ctx = nullptr;
+    int d = 0, k = 0;
+    std::vector<int64_t> shape;
+    int64_t q_total = 0;  // all shards
+    int64_t q_local = 0;  // this shard
+    double density = 0.0; // q_total / prod(shape)  (observations.hpp:58-60)
+    cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
+    cphifi::DevBuf<int32_t> idx_o;    // (d-1) x q_local, other modes ascending, sorted by i_k
+    cphifi::DevBuf<double> values;    // q_local, sorted
+};
+
+struct cphifi_unaligned_s {
+    cphifi_obs obs = nullptr;
+    cphifi_mode mode = nullptr;
+    int64_t n = 0, r = 0, rp = 0;  // rank and padded rank (power of two >= 4)
+    double rho = 1e-6;
+    std::vector<int64_t> fac_off;     // offsets of the packed row-major padded factors
+    cphifi::DevBuf<double> fac;       // packed other-mode factors, row-major n_m x rp
+    cphifi::DevBuf<double> b;         // n x r column-major (sampled MTTKRP with values)
+    cphifi::DevBuf<double> v;         // r x r
+    // preconditioner state (lazy): eig(V), D
+    bool have_veig = false;
+    cphifi::DevBuf<double> uv, sv, dmat;
+    // scatter-gather scratch
+    int64_t units = 0, chunk = 1;
+    cphifi::DevBuf<double> slot_a, slot_b;  // units x rp
+    cphifi::DevBuf<double> xhat_rm, yhat_rm;  // n x rp row-major
+    cphifi::DevBuf<double> xhat_cm;           // n x r column-major
+    cphifi::DevBuf<double> t1, t2;            // n x r scratch (preconditioner)
+    cphifi::DevBuf<double> vx, vy;            // n x r device in/out for host-buffer calls
+};
+
+struct cphifi_tensor_s {
+    cphifi_ctx ctx = nullptr;
+    int d = 0;
+    std::vector<int64_t> shape;        // full shape
+    int64_t slab_lo = 0, slab_hi = 0;  // mode-1 slice range held locally
+    cphifi::DevBuf<double> data;       // local slab, column-major n0 x (hi-lo) x n2 x ...
+};
+
+struct cphifi_rng_s;

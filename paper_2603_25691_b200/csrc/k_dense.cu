@@ -1,0 +1,522 @@
+// k_dense.cu — FP64 tensor-core (DMMA m8n8k4) contractions for sm_100a.
+//
+// tcgen05.mma has no f64 kind, so the FP64 tensor path on B200 is the warp-level
+// `mma.sync.aligned.m8n8k4.row.col.f64` (SASS: DMMA.8x8x4).  These kernels cover every
+// dense contraction on the hot path:
+//   * K*X, K*Yhat + lambda*Xhat + rho*x   (unaligned.hpp:106,112-114)
+//   * U_K' X, (.)U_V .* D, U_K(.), (.)U_V' (unaligned.hpp:137; aligned.hpp:44-53)
+//   * dense MTTKRP T_(1) Z for k = 0      (tensor.hpp:174-182) with Z generated on the fly
+// Split-K partial sums are reduced in a FIXED order (thread-block cluster + distributed
+// shared memory for the GEMMs, an ordered second pass for the MTTKRP), so results are
+// bit-reproducible run to run.
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cphifi {
+namespace {
+
+constexpr int BM = 64;       // rows per CTA tile (4 warps x 16 rows)
+constexpr int BK = 32;       // K per pipeline stage
+constexpr int NT = 128;      // threads per CTA
+constexpr int STAGES = 3;
+constexpr int APAD = BM + 4; // smem row pitch (doubles); == 4 mod 16 -> conflict-free frags
+
+template <int BN>
+struct GemmSmem {
+    double a[STAGES][BK][APAD];
+    double b[STAGES][BK][BN + 4];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// A tile: sm.a[st][kk][ii] = A(i0+ii, k0+kk); zero outside [m) x [k0, kend)
+template <int BN>
+__device__ __forceinline__ void load_a(GemmSmem<BN>& sm, int st, const double* __restrict__ a,
+                                       int64_t a_rs, int64_t a_cs, int64_t m, int64_t i0,
+                                       int64_t k0, int64_t kend) {
+    if (a_rs == 1) {
+        for (int e = threadIdx.x; e < BM * BK; e += NT) {
+            const int ii = e % BM, kk = e / BM;
+            const int64_t i = i0 + ii, kx = k0 + kk;
+            const bool p = (i < m) && (kx < kend);
+            cp_async8(&sm.a[st][kk][ii], p ? a + i + kx * a_cs : a, p);
+        }
+    } else {
+        for (int e = threadIdx.x; e < BM * BK; e += NT) {
+            const int kk = e % BK, ii = e / BK;
+            const int64_t i = i0 + ii, kx = k0 + kk;
+            const bool p = (i < m) && (kx < kend);
+            cp_async8(&sm.a[st][kk][ii], p ? a + i * a_rs + kx * a_cs : a, p);
+        }
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void load_b(GemmSmem<BN>& sm, int st, const double* __restrict__ b,
+                                       int64_t b_rs, int64_t b_cs, int64_t n, int64_t j0,
+                                       int64_t k0, int64_t kend) {
+    if (b_cs == 1) {
+        for (int e = threadIdx.x; e < BN * BK; e += NT) {
+            const int jj = e % BN, kk = e / BN;
+            const int64_t j = j0 + jj, kx = k0 + kk;
+            const bool p = (j < n) && (kx < kend);
+            cp_async8(&sm.b[st][kk][jj], p ? b + kx * b_rs + j : b, p);
+        }
+    } else {
+        for (int e = threadIdx.x; e < BN * BK; e += NT) {
+            const int kk = e % BK, jj = e / BK;
+            const int64_t j = j0 + jj, kx = k0 + kk;
+            const bool p = (j < n) && (kx < kend);
+            cp_async8(&sm.b[st][kk][jj], p ? b + kx * b_rs + j * b_cs : b, p);
+        }
+    }
+}
+
+template <int BN>
+__device__ __forceinline__ void mma_stage(const GemmSmem<BN>& sm, int st, double (&acc)[2][BN / 8][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, g = lane >> 2;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+        const int kr = ks * 4 + kq;
+        const double a0 = sm.a[st][kr][warp * 16 + g];
+        const double a1 = sm.a[st][kr][warp * 16 + 8 + g];
+#pragma unroll
+        for (int nf = 0; nf < BN / 8; ++nf) {
+            const double bv = sm.b[st][kr][nf * 8 + g];
+            dmma(acc[0][nf], a0, bv);
+            dmma(acc[1][nf], a1, bv);
+        }
+    }
+}
+
+__device__ __forceinline__ void epilogue_store(const GemmArgs& g, int64_t i, int64_t j, double v) {
+    if (i >= g.m) return;
+    if (j < g.n) {
+        double out = v;
+        switch (g.epi) {
+            case EPI_AXPY2: {
+                const int64_t e = i + g.ld_e * j;
+                out = v + g.beta1 * g.e1[e];
+                out = out + g.beta2 * g.e2[e];
+                break;
+            }
+            case EPI_HADAMARD:
+                out = v * g.e1[i + g.ld_e * j];
+                break;
+            case EPI_SCALE_DIV: {
+                const double den = g.e_col[j] * g.e_row[i] + g.beta1;
+                if (den == 0.0) *g.flag = 1;
+                out = v / den;
+                break;
+            }
+            default:
+                break;
+        }
+        if (g.c) g.c[i * g.c_rs + j * g.c_cs] = out;
+        if (g.c2) g.c2[i * g.ld2 + j] = out;
+    } else if (g.c2 && j < g.ld2) {
+        g.c2[i * g.ld2 + j] = 0.0;
+    }
+}
+
+// grid: (ceil(m/BM), S, ceil(n/BN)); cluster (1, S, 1) splits K across the S CTAs.
+template <int BN>
+__global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmArgs g) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(smem_raw);
+    const int S = gridDim.y, rank = blockIdx.y;
+    const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.z * BN;
+    int64_t kchunk = (g.k + S - 1) / S;
+    kchunk = (kchunk + BK - 1) / BK * BK;
+    const int64_t kbeg = (int64_t)rank * kchunk;
+    const int64_t kend = min(g.k, kbeg + kchunk);
+    const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+    double acc[2][BN / 8][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < BN / 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    // prologue
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles) {
+            load_a<BN>(sm, s, g.a, g.a_rs, g.a_cs, g.m, i0, kbeg + (int64_t)s * BK, kend);
+            load_b<BN>(sm, s, g.b, g.b_rs, g.b_cs, g.n, j0, kbeg + (int64_t)s * BK, kend);
+        }
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntiles; ++t) {
+        const int nxt = t + STAGES - 1;
+        if (nxt < ntiles) {
+            load_a<BN>(sm, nxt % STAGES, g.a, g.a_rs, g.a_cs, g.m, i0, kbeg + (int64_t)nxt * BK, kend);
+            load_b<BN>(sm, nxt % STAGES, g.b, g.b_rs, g.b_cs, g.n, j0, kbeg + (int64_t)nxt * BK, kend);
+        }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
+        __syncthreads();
+        mma_stage<BN>(sm, t % STAGES, acc);
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    if (S == 1) {
+#pragma unroll
+        for (int mf = 0; mf < 2; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < BN / 8; ++nf)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    epilogue_store(g, i0 + warp * 16 + mf * 8 + gq, j0 + nf * 8 + tq * 2 + h, acc[mf][nf][h]);
+        return;
+    }
+    // cluster split-K: stage the partial tile in smem, reduce over ranks in rank order
+    __syncthreads();
+    double* part = reinterpret_cast<double*>(smem_raw);  // BM x (BN+1)
+    constexpr int PP = BN + 1;
+#pragma unroll
+    for (int mf = 0; mf < 2; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < BN / 8; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                part[(warp * 16 + mf * 8 + gq) * PP + nf * 8 + tq * 2 + h] = acc[mf][nf][h];
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    const int rows_per = BM / S;
+    for (int e = threadIdx.x; e < rows_per * BN; e += NT) {
+        const int ii = rank * rows_per + e / BN, jj = e % BN;
+        double s = 0.0;
+        for (int src = 0; src < S; ++src) {
+            const double* rp = cluster.map_shared_rank(part, src);
+            s += rp[ii * PP + jj];
+        }
+        epilogue_store(g, i0 + ii, j0 + jj, s);
+    }
+    cluster.sync();
+}
+
+template <int BN>
+void launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
+    const int mt = (int)((g.m + BM - 1) / BM);
+    const int nt = (int)((g.n + BN - 1) / BN);
+    int S = 1;
+    while (S < 8 && (int64_t)mt * nt * S < 2 * num_sms && g.k / (2 * S) >= 2 * BK) S *= 2;
+    const size_t smem = sizeof(GemmSmem<BN>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        CPHIFI_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(mt, S, nt);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = S;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CPHIFI_CUDA(cudaLaunchKernelEx(&cfg, gemm_dmma_kernel<BN>, g));
+}
+
+// ---- MTTKRP (k = 0): A = T slab (n0 x Mloc, column-major), B = Z rows generated -------
+template <int BN>
+__device__ __forceinline__ void gen_z(GemmSmem<BN>& sm, int st, const MttkrpArgs& a, int64_t j0,
+                                      int64_t k0, int64_t kend) {
+    for (int e = threadIdx.x; e < BN * BK; e += NT) {
+        const int jj = e % BN, kk = e / BN;
+        const int64_t j = j0 + jj, c = k0 + kk;
+        double z = 0.0;
+        if (j < a.r && c < kend) {
+            // column c of the unfolding: mode 1 fastest (tensor.hpp:70-73)
+            int64_t sub[8];
+            int64_t rem = c;
+            for (int m = 1; m < a.d; ++m) {
+                sub[m] = rem % a.shape[m];
+                rem /= a.shape[m];
+            }
+            sub[1] += a.off1;
+            // khatri_rao(A_{d-1}, ..., A_1): left-to-right in descending mode order
+            z = a.fac[a.d - 1][sub[a.d - 1] + a.ld[a.d - 1] * j];
+            for (int m = a.d - 2; m >= 1; --m) z *= a.fac[m][sub[m] + a.ld[m] * j];
+        }
+        sm.b[st][kk][jj] = z;
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NT) mttkrp_dmma_kernel(const MttkrpArgs a, int64_t mcols,
+                                                         double* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(smem_raw);
+    const int P = gridDim.y, split = blockIdx.y;
+    const int64_t n0 = a.shape[0];
+    const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.z * BN;
+    const int64_t ktiles = (mcols + BK - 1) / BK;
+    const int64_t tb = ktiles * split / P, te = ktiles * (split + 1) / P;
+    const int64_t kbeg = tb * BK, kend = min(mcols, te * BK);
+    const int ntiles = (int)(te - tb);
+
+    double acc[2][BN / 8][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < BN / 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles) {
+            load_a<BN>(sm, s, a.t, 1, n0, n0, i0, kbeg + (int64_t)s * BK, kend);
+            gen_z<BN>(sm, s, a, j0, kbeg + (int64_t)s * BK, kend);
+        }
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntiles; ++t) {
+        const int nxt = t + STAGES - 1;
+        if (nxt < ntiles) {
+            load_a<BN>(sm, nxt % STAGES, a.t, 1, n0, n0, i0, kbeg + (int64_t)nxt * BK, kend);
+            gen_z<BN>(sm, nxt % STAGES, a, j0, kbeg + (int64_t)nxt * BK, kend);
+        }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
+        __syncthreads();
+        mma_stage<BN>(sm, t % STAGES, acc);
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    double* out = work + (int64_t)split * n0 * a.r;
+#pragma unroll
+    for (int mf = 0; mf < 2; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < BN / 8; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t i = i0 + warp * 16 + mf * 8 + gq, j = j0 + nf * 8 + tq * 2 + h;
+                if (i < n0 && j < a.r) out[i + n0 * j] = acc[mf][nf][h];
+            }
+}
+
+__global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int64_t cnt,
+                                     double* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = 0; p < P; ++p) s += work[(int64_t)p * cnt + e];
+        out[e] = s;
+    }
+}
+
+template <int BN>
+void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work) {
+    const int64_t n0 = a.shape[0];
+    int64_t mcols = 1;
+    for (int m = 1; m < a.d; ++m) mcols *= a.shape[m];
+    const int mt = (int)((n0 + BM - 1) / BM);
+    const int nt = (int)((a.r + BN - 1) / BN);
+    const int64_t ktiles = (mcols + BK - 1) / BK;
+    int64_t P = (2 * (int64_t)num_sms + mt * nt - 1) / (mt * nt);
+    P = std::max<int64_t>(1, std::min<int64_t>(P, ktiles));
+    P = std::min<int64_t>(P, 1024);
+    const size_t need = (size_t)P * n0 * a.r;
+    if (work.n < need) work.alloc(need);
+    const size_t smem = sizeof(GemmSmem<BN>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        attr_set = true;
+    }
+    mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NT, smem, s>>>(a, mcols, work.get());
+    CPHIFI_CHECK_LAUNCH();
+    const int64_t cnt = n0 * a.r;
+    reduce_splits_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(
+        work.get(), (int)P, cnt, a.b);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+// ---- small kernels -------------------------------------------------------------------
+__global__ void gram_kernel(int d, int k, int64_t r, const double* const* fac, const int64_t* shape,
+                            double* v) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= r * r) return;
+    const int64_t row = e % r, col = e / r;  // V(row, col)
+    double acc = 1.0;
+    for (int m = 0; m < d; ++m) {
+        if (m == k) continue;
+        const double* a = fac[m];
+        const int64_t nm = shape[m];
+        double s = 0.0;
+        for (int64_t i = 0; i < nm; ++i) s += a[i + nm * row] * a[i + nm * col];
+        acc *= s;
+    }
+    v[e] = acc;
+}
+
+__global__ void kernel_matrix_kernel(int kind, const double* __restrict__ pts, int64_t n, double p,
+                                     double* __restrict__ kmat) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n * n) return;
+    const int64_t i = e % n, j = e / n;
+    double v;
+    if (i == j) {
+        v = 1.0;
+    } else {
+        // evaluate on the (max, min) ordered pair exactly as kernel.hpp:29-33 does for j < i
+        const int64_t a = i > j ? i : j, b = i > j ? j : i;
+        if (kind == 0) {
+            const double dd = pts[a] - pts[b];
+            v = exp(-dd * dd * p);  // p = 1 / (2 sigma^2)
+        } else {
+            const double t = p * fabs(pts[a] - pts[b]);  // p = sqrt(3) / ell
+            v = (1.0 + t) * exp(-t);
+        }
+    }
+    kmat[e] = v;
+}
+
+__global__ void clamp_kernel(double* v, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = v[i] < 0.0 ? 0.0 : v[i];
+}
+
+__global__ void max_asym_kernel(const double* a, int64_t n, double* out2) {
+    __shared__ double s_asym[256], s_abs[256];
+    double m1 = 0.0, m2 = 0.0;
+    for (int64_t e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        const double v = a[e];
+        m1 = fmax(m1, fabs(v - a[j + n * i]));
+        m2 = fmax(m2, fabs(v));
+    }
+    s_asym[threadIdx.x] = m1;
+    s_abs[threadIdx.x] = m2;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            s_asym[threadIdx.x] = fmax(s_asym[threadIdx.x], s_asym[threadIdx.x + w]);
+            s_abs[threadIdx.x] = fmax(s_abs[threadIdx.x], s_abs[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out2[0] = s_asym[0];
+        out2[1] = s_abs[0];
+    }
+}
+
+// D(i,j) = 1 / (gamma sigma_j mu_i^2 + lambda mu_i + rho)   (unaligned.hpp:125-133)
+__global__ void precond_diag_kernel(const double* mu, const double* sv, int64_t n, int64_t r, double gamma,
+                                    double lambda, double rho, double* dmat, int* flag) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n * r) return;
+    const int64_t i = e % n, j = e / n;
+    const double den = gamma * sv[j] * mu[i] * mu[i] + lambda * mu[i] + rho;
+    if (den <= 0.0) *flag = 1;
+    dmat[e] = 1.0 / den;
+}
+
+__global__ void pack_rows_kernel(const double* src, int64_t rows, int64_t ld, int64_t r, int64_t rp,
+                                 double* dst) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= rows * rp) return;
+    const int64_t i = e / rp, j = e % rp;
+    dst[e] = j < r ? src[i + ld * j] : 0.0;
+}
+
+__global__ void rm_to_cm_kernel(const double* src, int64_t rows, int64_t rp, int64_t r, double* dst) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= rows * r) return;
+    const int64_t i = e % rows, j = e / rows;
+    dst[e] = src[i * rp + j];
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+}  // namespace
+
+void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
+    if (g.m <= 0 || g.n <= 0) return;
+    if (g.k <= 0) {
+        // empty contraction: run a zero-K GEMM (epilogue only) through the S=1 path
+    }
+    const int64_t np = (g.n + 7) / 8 * 8;
+    if (np <= 8) launch_gemm<8>(g, num_sms, s);
+    else if (np <= 16) launch_gemm<16>(g, num_sms, s);
+    else if (np <= 32) launch_gemm<32>(g, num_sms, s);
+    else launch_gemm<64>(g, num_sms, s);
+}
+
+void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work) {
+    const int64_t np = (a.r + 7) / 8 * 8;
+    if (np <= 8) launch_mttkrp<8>(a, num_sms, s, work);
+    else if (np <= 16) launch_mttkrp<16>(a, num_sms, s, work);
+    else if (np <= 32) launch_mttkrp<32>(a, num_sms, s, work);
+    else launch_mttkrp<64>(a, num_sms, s, work);
+}
+
+void gram_kr(int d, const int64_t* shape, int64_t r, const double* const* fac, int k, double* v,
+             cudaStream_t s) {
+    DevBuf<const double*> dfac(d);
+    DevBuf<int64_t> dshape(d);
+    CPHIFI_CUDA(cudaMemcpyAsync(dfac.get(), fac, sizeof(double*) * d, cudaMemcpyHostToDevice, s));
+    CPHIFI_CUDA(cudaMemcpyAsync(dshape.get(), shape, sizeof(int64_t) * d, cudaMemcpyHostToDevice, s));
+    gram_kernel<<<blocks_for(r * r, 128), 128, 0, s>>>(d, k, r, dfac.get(), dshape.get(), v);
+    CPHIFI_CHECK_LAUNCH();
+    CPHIFI_CUDA(cudaStreamSynchronize(s));  // dfac/dshape are freed on return
+}
+
+void kernel_matrix(int kind, const double* pts, int64_t n, double param, double* kmat, cudaStream_t s) {
+    kernel_matrix_kernel<<<blocks_for(n * n, 256), 256, 0, s>>>(kind, pts, n, param, kmat);
+    CPHIFI_CHECK_LAUNCH();
+}
+void clamp_nonneg(double* v, int64_t n, cudaStream_t s) {
+    clamp_kernel<<<blocks_for(n, 256), 256, 0, s>>>(v, n);
+    CPHIFI_CHECK_LAUNCH();
+}
+void max_asym(const double* a, int64_t n, double* out2, cudaStream_t s) {
+    max_asym_kernel<<<1, 256, 0, s>>>(a, n, out2);
+    CPHIFI_CHECK_LAUNCH();
+}
+void precond_diag(const double* mu, const double* sv, int64_t n, int64_t r, double gamma, double lambda,
+                  double rho, double* dmat, int* flag, cudaStream_t s) {
+    precond_diag_kernel<<<blocks_for(n * r, 256), 256, 0, s>>>(mu, sv, n, r, gamma, lambda, rho, dmat, flag);
+    CPHIFI_CHECK_LAUNCH();
+}
+void pack_rows(const double* src_cm, int64_t rows, int64_t ld, int64_t r, int64_t rp, double* dst_rm,
+               cudaStream_t s) {
+    pack_rows_kernel<<<blocks_for(rows * rp, 256), 256, 0, s>>>(src_cm, rows, ld, r, rp, dst_rm);
+    CPHIFI_CHECK_LAUNCH();
+}
+void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double* dst_cm, cudaStream_t s) {
+    rm_to_cm_kernel<<<blocks_for(rows * r, 256), 256, 0, s>>>(src_rm, rows, rp, r, dst_cm);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+}  // namespace cphifi

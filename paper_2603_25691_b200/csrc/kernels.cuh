@@ -1,0 +1,116 @@
+// kernels.cuh — launch wrappers for the sm_100a kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace cphifi {
+
+// ---- dense FP64 tensor-core (DMMA) GEMM: C = op(A) * B with fused epilogues ------------
+// Element (i,k) of A is a[i*a_rs + k*a_cs]; (k,j) of B is b[k*b_rs + j*b_cs].  Output
+// (i,j) goes to c[i*c_rs + j*c_cs] (optional) and to the row-major padded copy c2[i*ld2+j]
+// (optional; columns j in [n, ld2) are written as 0).
+enum EpiOp : int {
+    EPI_STORE = 0,    // C = AB
+    EPI_AXPY2 = 1,    // C = (AB + beta1*E1) + beta2*E2     (unaligned.hpp:112-114 order)
+    EPI_HADAMARD = 2, // C = AB .* E1                        (unaligned.hpp:137)
+    EPI_SCALE_DIV = 3 // C = AB / (e_row[i]*e_col[j] + beta1) with zero-denominator flag
+};
+
+struct GemmArgs {
+    int64_t m = 0, n = 0, k = 0;
+    const double* a = nullptr; int64_t a_rs = 1, a_cs = 0;
+    const double* b = nullptr; int64_t b_rs = 1, b_cs = 0;
+    double* c = nullptr; int64_t c_rs = 1, c_cs = 0;
+    double* c2 = nullptr; int64_t ld2 = 0;
+    int epi = EPI_STORE;
+    const double* e1 = nullptr; const double* e2 = nullptr; int64_t ld_e = 0;  // col-major
+    double beta1 = 0.0, beta2 = 0.0;
+    const double* e_row = nullptr; const double* e_col = nullptr;
+    int* flag = nullptr;  // set to 1 if EPI_SCALE_DIV meets a zero denominator
+};
+void gemm(const GemmArgs& g, int num_sms, cudaStream_t s);
+
+// ---- dense MTTKRP for mode 0 (tensor.hpp:174-182): B = T_(1) * Z with Z generated on the
+// fly from the factors (khatri_rao order, last listed factor fastest).  T is the local
+// slab n0 x (n1 range) x n2 x ...; factors are column-major originals.  Deterministic
+// split over the column range with an ordered reduction.
+struct MttkrpArgs {
+    int d = 0;
+    int64_t shape[8] = {0};   // local slab shape (shape[1] = slab extent)
+    int64_t off1 = 0;         // global offset of the slab in mode 1
+    int64_t r = 0;
+    const double* t = nullptr;
+    const double* fac[8] = {nullptr};  // device column-major, fac[m] has ld = full n_m
+    int64_t ld[8] = {0};
+    double* b = nullptr;      // n0 x r column-major output
+};
+void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work);
+
+// ---- Khatri-Rao Gram (tensor.hpp:186-194), factors column-major device ----------------
+void gram_kr(int d, const int64_t* shape, int64_t r, const double* const* fac, int k, double* v,
+             cudaStream_t s);
+
+// ---- small kernels ---------------------------------------------------------------------
+void kernel_matrix(int kind, const double* pts, int64_t n, double param, double* kmat, cudaStream_t s);
+void clamp_nonneg(double* v, int64_t n, cudaStream_t s);
+void max_asym(const double* a, int64_t n, double* out2, cudaStream_t s);  // out2 = {max|a-a'|, max|a|}
+void precond_diag(const double* mu, const double* sv, int64_t n, int64_t r, double gamma,
+                  double lambda, double rho, double* dmat, int* flag, cudaStream_t s);
+void pack_rows(const double* src_cm, int64_t rows, int64_t ld, int64_t r, int64_t rp, double* dst_rm,
+               cudaStream_t s);
+void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double* dst_cm, cudaStream_t s);
+
+// ---- unaligned scatter-gather (K1) + deterministic fix-up ------------------------------
+struct SgArgs {
+    int64_t n = 0, rp = 0, q = 0;
+    int dother = 0;
+    const int64_t* row_ptr = nullptr;
+    const int32_t* idx = nullptr;       // dother x q
+    const double* fac = nullptr;        // packed row-major padded factors
+    int64_t fac_off[8] = {0};
+    const double* weights = nullptr;    // non-null: s_l = weights[l] (RHS), else s_l = xhat . z
+    const double* xhat = nullptr;       // n x rp row-major
+    double* yhat = nullptr;             // n x rp row-major
+    double* slot_a = nullptr;
+    double* slot_b = nullptr;
+    int64_t units = 0, chunk = 1;
+};
+void sg_plan(int64_t q, int64_t rp, int num_sms, int64_t* units, int64_t* chunk);
+void scatter_gather(const SgArgs& a, cudaStream_t s);  // = sg_main + sg_fixup
+void sg_main(const SgArgs& a, cudaStream_t s);
+void sg_fixup(const SgArgs& a, cudaStream_t s);
+
+// ---- PCG vector kernels (deterministic reductions) --------------------------------------
+struct PcgState {
+    double rz, pap, alpha, rr, bnorm, rel, beta, rz_new;
+    int flag;  // 1 = non-finite p'Ap, 2 = p'Ap <= 0
+    int pad;
+};
+void dot_to(const double* x, const double* y, int64_t n, double* partial, double* out, cudaStream_t s);
+// pap = p.ap; flag; alpha = rz/pap; x += alpha p; r -= alpha ap; rr = r.r; rel = sqrt(rr)/bnorm
+void pcg_step_a(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st,
+                double* partial, cudaStream_t s);
+// rz_new = r.z; beta = rz_new/rz; p = z + beta p; rz = rz_new
+void pcg_step_b(const double* r, const double* z, double* p, int64_t n, PcgState* st, double* partial,
+                cudaStream_t s);
+// init: rz = r.z, rr = r.r, rel = sqrt(rr)/bnorm, p = z
+void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* st, double* partial,
+              cudaStream_t s);
+void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n,
+           cudaStream_t s);  // y = alpha*a + beta*b
+
+// ---- observation plan helpers ------------------------------------------------------------
+void check_range(const int32_t* idx, int d, int64_t q, const int64_t* shape_dev, int* flag, cudaStream_t s);
+void linear_index(const int32_t* idx, int d, int64_t q, const int64_t* shape, uint64_t* lin, cudaStream_t s);
+void adjacent_equal(const uint64_t* sorted, int64_t q, int* flag, cudaStream_t s);
+void iota32(int32_t* p, int64_t q, cudaStream_t s);
+void gather_i32(const int32_t* src, const int32_t* perm, int64_t lo, int64_t cnt, int32_t* dst, cudaStream_t s);
+void gather_f64(const double* src, const int32_t* perm, int64_t lo, int64_t cnt, double* dst, cudaStream_t s);
+void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr, cudaStream_t s);
+size_t radix_sort_pairs_bytes(int64_t q, int bits);
+void radix_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
+                      const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
+size_t radix_sort_keys64_bytes(int64_t q);
+void radix_sort_keys64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t q,
+                       cudaStream_t s);
+
+}  // namespace cphifi

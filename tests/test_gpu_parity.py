@@ -1,0 +1,360 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on the same seeded
+inputs, at reference-test sizes, config 0/1/2 sizes, plus the reference's error contract.
+
+Tolerances (written per test): matvec / scatter-gather / MTTKRP relative 1e-12 against the
+oracle (different fp64 summation order only); reference dense-oracle tolerances where the
+reference states them; decoupled W <= 1e-10 with a SHARED eig; PCG iteration
+count within +-1 of the oracle and final relative residual <= tol (north_star).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import refinst as ri
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cp(ctx):
+    import paper_2603_25691_b200 as cp
+    return cp
+
+
+def dev_problem(cp, inst, shared_eig=True, multiset=False):
+    mode = cp.RkhsMode(inst.points, inst.sigma, inst.lam)
+    obs = cp.ObservationSet(inst.shape, inst.idx, inst.vals, multiset=multiset)
+    p = cp.make_unaligned_subproblem(obs, cp.KruskalModel(inst.factors), inst.k, mode, inst.rho)
+    if shared_eig:
+        ek = orc.sym_eig(inst.kernel)
+        mode.set_eig(ek.u, ek.d)
+    return mode, obs, p
+
+
+# ---- K1 + dense GEMMs: the operator ---------------------------------------------------
+def test_device_kernel_matches_oracle_kernel(cp):
+    pts = np.sort(cp.Mt19937_64(3).uniform_real(0, 1, 300))
+    mode = cp.RkhsMode(pts, 0.05, 1e-3)
+    k = mode.kernel()
+    ko = orc.gaussian_kernel(pts, 0.05)
+    assert np.array_equal(k, k.T) and np.all(np.diag(k) == 1.0)
+    assert np.abs(k - ko).max() <= 2e-16  # device exp vs libm exp: <= 1 ulp
+    m2 = cp.RkhsMode(pts, 0.05, 1e-3, kernel="matern32")
+    assert np.abs(m2.kernel() - orc.matern32_kernel(pts, 0.05)).max() <= 4e-16
+
+
+def test_matvec_dense_oracle_sweep_50_seeds(cp):
+    # test_unaligned_solvers.cpp:171-186 on device: vs dense oracle (1e-10) and vs the oracle (1e-12)
+    for seed in range(50):
+        g = cp.Mt19937_64(seed * 31 + 1)
+        n = int(g.uniform_int(3, 10)[0])
+        r = int(g.uniform_int(1, 4)[0])
+        shape = [n, 5, 4]
+        q = min(int(g.uniform_int(1, 60)[0]), n * 5 * 4)
+        inst = ri.Inst(shape, r, q, 0, 1.5, 0.1, 1e-6, seed)
+        x = ri.random_matrix(g, n * r, 1).reshape(-1)
+        mode, obs, p = dev_problem(cp, inst, shared_eig=False)
+        inst.kernel = mode.kernel()
+        inst.sub.kernel = inst.kernel
+        y = cp.unaligned_matvec(p, x)
+        expect = ri.dense_sym_operator(inst.sub) @ x
+        assert np.linalg.norm(y - expect) / max(np.linalg.norm(expect), 1e-12) < 1e-10, seed
+        assert ri.rel(y, orc.unaligned_matvec(inst.sub, x)) < 1e-12, seed
+
+
+def test_acceptance_c2_on_device(cp):
+    g = cp.Mt19937_64(202)
+    worst = 0.0
+    for trial in range(50):
+        n = 3 + int(g() % 8)
+        r = 1 + int(g() % 4)
+        q = 1 + int(g() % min(60, n ** 3))
+        inst = ri.Inst([n, n, n], r, q, 0, 1.0 + 0.1 * (trial % 5), 0.1, 1e-6, None, acceptance_rng=g)
+        x = ri.random_matrix(g, n * r, 1).reshape(-1)
+        mode, obs, p = dev_problem(cp, inst, shared_eig=False)
+        inst.sub.kernel = mode.kernel()
+        y_ref = ri.dense_sym_operator(inst.sub) @ x
+        worst = max(worst, ri.rel(cp.unaligned_matvec(p, x), y_ref))
+    assert worst <= 1e-10
+
+
+def test_matvec_empty_and_b_v(cp):
+    # test_unaligned_solvers.cpp:131-143: q = 0 -> lambda K X + rho x
+    mode = cp.RkhsMode.regular_grid(3, 1.0, 0.5)
+    obs = cp.ObservationSet([3, 3], np.zeros((2, 0)), np.zeros(0))
+    p = cp.make_unaligned_subproblem(obs, cp.KruskalModel([np.ones((3, 2)), np.ones((3, 2))]), 0, mode, 0.25)
+    x = ri.random_matrix(cp.Mt19937_64(4), 6, 1).reshape(-1)
+    kx = (mode.kernel() @ x.reshape((3, 2), order="F")).reshape(-1, order="F")
+    assert np.linalg.norm(cp.unaligned_matvec(p, x) - (0.5 * kx + 0.25 * x)) < 1e-12
+    assert np.linalg.norm(p.b) == 0.0
+
+
+@pytest.mark.parametrize("shape,r,q", [([57, 9, 8], 3, 2000), ([33, 7, 6, 5], 8, 3000), ([20, 30], 17, 500),
+                                       ([64, 10, 11], 32, 5000), ([31, 12, 9], 64, 3000), ([16, 9, 9], 100, 900)])
+def test_scatter_gather_b_and_v_vs_oracle(cp, shape, r, q):
+    inst = ri.Inst(shape, r, q, 0, 0.7, 0.1, 1e-6, 1234 + r)
+    mode, obs, p = dev_problem(cp, inst, shared_eig=False)
+    assert ri.rel(p.b, inst.sub.b) < 1e-12
+    assert ri.rel(p.v, inst.sub.v) < 1e-12
+    assert np.array_equal(p.v, p.v.T)
+    xhat = ri.random_matrix(inst.rng, shape[0], r)
+    xbar = orc.gather_rows(xhat, inst.sub.zhat, inst.idx[0])
+    yo = orc.sampled_mttkrp(shape[0], inst.sub.zhat, inst.idx[0], xbar)
+    assert ri.rel(p.scatter_gather(xhat), yo) < 1e-12
+    x = ri.random_matrix(inst.rng, shape[0] * r, 1).reshape(-1)
+    inst.sub.kernel = mode.kernel()
+    assert ri.rel(cp.unaligned_matvec(p, x), orc.unaligned_matvec(inst.sub, x)) < 1e-12
+
+
+def test_nonzero_mode_k_and_skewed_rows(cp):
+    # infinite mode k = 1 and a row-skewed (Zipf-like) observation set with empty rows
+    g = cp.Mt19937_64(77)
+    shape = [6, 50, 7]
+    r = 5
+    factors = ri.random_model(shape, r, g)
+    q = 4000
+    rs = np.random.default_rng(5)
+    i1 = np.minimum((rs.zipf(1.3, q) - 1), 49)
+    i1[i1 == 7] = 8  # leave row 7 empty
+    idx = np.stack([rs.integers(0, 6, q), i1, rs.integers(0, 7, q)]).astype(np.int32)
+    vals = rs.normal(size=q)
+    pts = np.linspace(0, 1, 50)
+    mode = cp.RkhsMode(pts, 0.1, 1e-2)
+    kern = mode.kernel()
+    obs = cp.ObservationSet(shape, idx, vals, multiset=True)
+    p = cp.make_unaligned_subproblem(obs, cp.KruskalModel(factors), 1, mode, 1e-6)
+    sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 1, kern, 1e-2, 1e-6)
+    assert ri.rel(p.b, sub.b) < 1e-12
+    x = ri.random_matrix(g, 50 * r, 1).reshape(-1)
+    assert ri.rel(cp.unaligned_matvec(p, x), orc.unaligned_matvec(sub, x)) < 1e-12
+
+
+# ---- preconditioner ---------------------------------------------------------------------
+def test_preconditioner_shared_eig_and_dense(cp):
+    g = cp.Mt19937_64(9)
+    for trial in range(10):
+        inst = ri.Inst([8, 4, 3], 3, 30, 0, 1.5, 0.1, 1e-6, trial + 100)
+        mode, obs, p = dev_problem(cp, inst, shared_eig=True)
+        ev = orc.sym_eig(inst.sub.v)
+        p.set_v_eig(ev.u, ev.d)
+        x = ri.random_matrix(g, 24, 1).reshape(-1)
+        m = cp.build_preconditioner(p)
+        mo = orc.build_preconditioner(inst.sub, orc.sym_eig(inst.kernel), ev)
+        assert ri.rel(m.apply(x), mo.apply(x)) < 1e-12
+    # device-computed eig(K), eig(V): dense inverse oracle at the reference tolerance 1e-8
+    for trial in range(10):
+        inst = ri.Inst([8, 4, 3], 3, 30, 0, 1.5, 0.1, 1e-6, trial + 100)
+        mode, obs, p = dev_problem(cp, inst, shared_eig=False)
+        inst.sub.kernel = mode.kernel()
+        x = ri.random_matrix(g, 24, 1).reshape(-1)
+        expect = np.linalg.solve(ri.dense_preconditioner(inst.sub), x)
+        assert ri.rel(cp.build_preconditioner(p).apply(x), expect) < 1e-8
+    assert mode.eig_factorization_count() == 1
+
+
+# ---- PCG ----------------------------------------------------------------------------------
+def test_pcg_reference_contract(cp):
+    # zero RHS (test_unaligned_solvers.cpp:237-246)
+    mode = cp.RkhsMode.regular_grid(3, 1.0, 0.5)
+    obs = cp.ObservationSet([3, 3], [[0], [0]], [0.0])
+    p = cp.make_unaligned_subproblem(obs, cp.KruskalModel([np.ones((3, 2)), np.ones((3, 2))]), 0, mode, 1e-6)
+    rep = cp.SolveReport()
+    w = cp.solve_unaligned_pcg(p, cp.PcgConfig(), rep)
+    assert np.linalg.norm(w) < 1e-14 and rep.iterations <= 1 and rep.converged
+    # exact at full density (test_unaligned_solvers.cpp:219-235): <= 2 iterations
+    g = cp.Mt19937_64(10)
+    flat = ri.random_tensor([5, 4, 3], g)
+    idx, vals = ri.full_obs([5, 4, 3], flat)
+    factors = ri.random_model([5, 4, 3], 2, g)
+    for lam in (0.01, 0.5):
+        for rho in (1e-6, 0.1):
+            mode = cp.RkhsMode.regular_grid(5, 1.5, lam)
+            p = cp.make_unaligned_subproblem(cp.ObservationSet([5, 4, 3], idx, vals), cp.KruskalModel(factors), 0,
+                                             mode, rho)
+            rep = cp.SolveReport()
+            cp.solve_unaligned_pcg(p, cp.PcgConfig(1e-8, 75), rep)
+            assert rep.iterations <= 2, (lam, rho)
+    # rho <= 0 and bad configs are std::invalid_argument
+    with pytest.raises(cp.CphifiInvalidArgument, match="rho must be positive"):
+        cp.solve_unaligned_pcg(cp.make_unaligned_subproblem(cp.ObservationSet([5, 4, 3], idx, vals),
+                                                            cp.KruskalModel(factors), 0, mode, 0.0))
+    with pytest.raises(cp.CphifiInvalidArgument, match="pcg: invalid config"):
+        cp.solve_unaligned_pcg(p, cp.PcgConfig(0.0, 10))
+
+
+def test_pcg_dense_cholesky_and_iteration_parity(cp):
+    inst = ri.Inst([20, 6, 5], 4, 400, 0, 0.8, 0.1, 1e-6, 11)
+    mode, obs, p = dev_problem(cp, inst, shared_eig=True)
+    inst.sub.kernel = mode.kernel()
+    ev = orc.sym_eig(inst.sub.v)
+    p.set_v_eig(ev.u, ev.d)
+    sysm = ri.dense_sym_operator(inst.sub)
+    rhs = (inst.sub.kernel @ inst.sub.b).reshape(-1, order="F")
+    w_ref = np.linalg.solve(sysm, rhs)
+    rep = cp.SolveReport()
+    w = cp.solve_unaligned_pcg(p, cp.PcgConfig(1e-10, 200, True), rep)
+    assert ri.rel(w.reshape(-1, order="F"), w_ref) < 1e-5
+    orep = orc.SolveReport()
+    orc.solve_unaligned_pcg(inst.sub, orc.PcgConfig(1e-10, 200, True), orc.sym_eig(inst.sub.kernel), ev, report=orep)
+    assert abs(rep.iterations - orep.iterations) <= 1
+    assert rep.relative_residual <= 1e-10 and rep.converged
+    assert len(rep.residual_history) == rep.iterations + 1
+
+
+def test_row_order_irrelevant(cp):
+    inst = ri.Inst([6, 5, 4], 2, 40, 0, 1.0, 0.1, 1e-6, 15)
+    mode, obs, p = dev_problem(cp, inst, shared_eig=False)
+    w1 = cp.solve_unaligned_pcg(p, cp.PcgConfig(1e-10, 200))
+    perm = np.random.default_rng(99).permutation(inst.sub.q)
+    obs2 = cp.ObservationSet(inst.shape, inst.idx[:, perm], inst.vals[perm])
+    p2 = cp.make_unaligned_subproblem(obs2, cp.KruskalModel(inst.factors), 0, mode, 1e-6)
+    w2 = cp.solve_unaligned_pcg(p2, cp.PcgConfig(1e-10, 200))
+    assert ri.rel(w2, w1) < 1e-8
+
+
+def test_config1_pcg_parity(cp):
+    """BASELINE config 1 at full size: iterations within +-1 of the oracle, residual <= 1e-8."""
+    from paper_2603_25691_b200 import configs
+    c = configs.config1()
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    obs = cp.ObservationSet(c.shape, c.idx, c.vals)
+    model = cp.KruskalModel([np.zeros((c.shape[0], c.r))] + c.factors[1:])
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, c.rho)
+    sub = orc.make_unaligned_subproblem(c.shape, c.idx, c.vals, model.factors, 0, kern, c.lam, c.rho)
+    assert ri.rel(p.b, sub.b) < 1e-12 and ri.rel(p.v, sub.v) < 1e-12
+    ev = orc.sym_eig(sub.v)
+    p.set_v_eig(ev.u, ev.d)
+    rep = cp.SolveReport()
+    w = cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter, True), rep)
+    orep = orc.SolveReport()
+    wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(c.tol, c.max_iter, True), ek, ev, report=orep)
+    assert rep.converged and rep.relative_residual <= c.tol
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+    # true residual of the device solution, evaluated by the oracle operator
+    rhs = (kern @ sub.b).reshape(-1, order="F")
+    tr = np.linalg.norm(rhs - orc.unaligned_matvec(sub, w.reshape(-1, order="F"))) / np.linalg.norm(rhs)
+    assert tr <= 10 * c.tol
+    hd, ho = np.array(rep.residual_history), np.array(orep.residual_history)
+    m = min(len(hd), len(ho))
+    assert np.allclose(hd[:m], ho[:m], rtol=1e-6, atol=0)
+    assert ri.rel(w, wo) < 1e-6
+
+
+# ---- aligned ------------------------------------------------------------------------------
+def test_mttkrp_gram_vs_oracle(cp):
+    g = cp.Mt19937_64(21)
+    for shape, r in (([37, 11, 9], 5), ([64, 8, 6, 5], 32), ([100, 30], 10), ([70, 13, 17], 64), ([9, 4, 3], 1)):
+        flat = ri.random_tensor(shape, g)
+        factors = ri.random_model(shape, r, g)
+        t = cp.DenseTensor(shape, flat)
+        b = cp.mttkrp(t, cp.KruskalModel(factors), 0)
+        bo = orc.mttkrp(flat.reshape(shape, order="F"), factors, 0)
+        assert ri.rel(b, bo) < 1e-12, shape
+        for k in range(len(shape)):
+            v = cp.gram_khatri_rao(cp.KruskalModel(factors), k)
+            assert ri.rel(v, orc.gram_khatri_rao(factors, k)) < 1e-12
+
+
+def test_decoupled_known_answers_device(cp):
+    g = cp.Mt19937_64(4)
+    b = ri.random_matrix(g, 4, 2)
+    mode = cp.RkhsMode(ri.identity_points(4), 1.0, 1.0)
+    w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, np.eye(2), mode))
+    assert np.linalg.norm(w - 0.5 * b) < 1e-10
+    g = cp.Mt19937_64(5)
+    b = ri.random_matrix(g, 3, 2)
+    v = np.diag([2.0, 5.0])
+    mode0 = cp.RkhsMode(ri.identity_points(3), 1.0, 0.0)
+    w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, v, mode0))
+    assert np.abs(w - b / np.diag(v)[None, :]).max() < 1e-10
+    with pytest.raises(cp.CphifiRuntimeError, match="zero eigenvalue pair"):
+        cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, np.zeros((2, 2)), mode0))
+    with pytest.raises(cp.CphifiInvalidArgument, match="not symmetric"):
+        cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, np.array([[1.0, 2.0], [3.0, 4.0]]), mode0))
+
+
+def test_acceptance_c1_decoupled_device(cp):
+    g = cp.Mt19937_64(101)
+    grid = [(n, r, lam) for n in (10, 20, 40) for r in (2, 5, 8) for lam in (0.1, 1.0)]
+    grid += [(30, 6, 0.1), (25, 4, 1.0)]
+    worst = 0.0
+    for n, r, lam in grid:
+        b = ri.random_matrix(g, n, r)
+        v = ri.random_spd(g, r)
+        mode = cp.RkhsMode.regular_grid(n, 2.0, lam)
+        kern = mode.kernel()
+        wd = np.linalg.solve(np.kron(v, kern) + lam * np.eye(n * r), b.reshape(-1, order="F"))
+        w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, v, mode))
+        worst = max(worst, ri.rel(w.reshape(-1, order="F"), wd))
+    assert worst <= 1e-8
+
+
+@pytest.mark.parametrize("which", ["config0", "config2"])
+def test_aligned_config_parity(cp, which):
+    """W relative error <= 1e-10 vs the oracle with a shared eig(K), eig(V)."""
+    from paper_2603_25691_b200 import configs
+    c = getattr(configs, which)()
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    t = cp.DenseTensor(c.shape, c.tensor)
+    model = cp.KruskalModel([np.zeros((c.shape[0], c.r))] + c.factors[1:])
+    b = cp.mttkrp(t, model, 0)
+    bo = orc.mttkrp(c.tensor.reshape(c.shape, order="F"), model.factors, 0, threads=orc.max_threads())
+    assert ri.rel(b, bo) < 1e-12
+    vo = orc.gram_khatri_rao(model.factors, 0)
+    ev = orc.sym_eig(vo)
+    w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(bo, vo, mode), ev)
+    wo = orc.solve_aligned_decoupled(bo, ek, ev, c.lam, threads=orc.max_threads())
+    assert ri.rel(w, wo) < 1e-10
+    # fused device path (device MTTKRP + Gram + device eig(V)) stays within 1e-10 as well
+    wf, bf, vf = cp.aligned_solve(t, model, 0, mode)
+    assert ri.rel(bf, bo) < 1e-12 and ri.rel(vf, vo) < 1e-12
+    assert ri.rel(wf, wo) < 1e-10
+
+
+# ---- ObservationSet contract --------------------------------------------------------------
+def test_observation_errors(cp):
+    with pytest.raises(cp.CphifiInvalidArgument, match="duplicate index"):
+        cp.ObservationSet([3, 3], [[0, 0], [1, 1]], [1.0, 2.0])
+    with pytest.raises(cp.CphifiInvalidArgument, match="out of range"):
+        cp.ObservationSet([3, 3], [[0], [3]], [1.0])
+    # device-side checks of the same contract through the raw C-ABI
+    import ctypes
+    from paper_2603_25691_b200 import _capi
+    ctx = cp.default_context()
+    shape = np.array([3, 3], dtype=np.int64)
+    idx = np.array([[0, 0], [1, 1]], dtype=np.int32)
+    vals = np.array([1.0, 2.0])
+    h = ctypes.c_void_p()
+    rc = _capi.load().cphifi_obs_create(ctx.handle, 2, shape.ctypes.data_as(_capi.c_int64_p), 2, idx.ctypes.data,
+                                        vals.ctypes.data, 0, _capi.OBS_REJECT_DUPLICATES, 0, 1, ctypes.byref(h))
+    assert rc == _capi.INVALID_ARGUMENT and b"duplicate" in _capi.load().cphifi_last_error()
+    idx[1, 1] = 5
+    rc = _capi.load().cphifi_obs_create(ctx.handle, 2, shape.ctypes.data_as(_capi.c_int64_p), 2, idx.ctypes.data,
+                                        vals.ctypes.data, 0, 0, 0, 1, ctypes.byref(h))
+    assert rc == _capi.INVALID_ARGUMENT and b"out of range" in _capi.load().cphifi_last_error()
+
+
+def test_sharded_plans_sum_to_full(cp):
+    """Multi-GPU math on one GPU: shard s of S holds an equal-count slice of the sorted
+    observations; the shards' un-reduced Yhat partials sum to the full Yhat (what NCCL
+    all-reduces per matvec)."""
+    inst = ri.Inst([40, 9, 8], 6, 2000, 0, 0.5, 0.1, 1e-6, 31)
+    mode = cp.RkhsMode(inst.points, inst.sigma, inst.lam)
+    obs = cp.ObservationSet(inst.shape, inst.idx, inst.vals)
+    full = cp.make_unaligned_subproblem(obs, cp.KruskalModel(inst.factors), 0, mode, 1e-6)
+    xhat = ri.random_matrix(inst.rng, 40, 6)
+    yf = full.scatter_gather(xhat)
+    for shards in (2, 3, 8):
+        acc = np.zeros_like(yf)
+        bacc = np.zeros_like(yf)
+        for s in range(shards):
+            ps = cp.make_unaligned_subproblem(obs, cp.KruskalModel(inst.factors), 0, mode, 1e-6, s, shards)
+            acc += ps.scatter_gather(xhat)
+            bacc += ps.b
+        assert ri.rel(acc, yf) < 1e-12 and ri.rel(bacc, full.b) < 1e-12
