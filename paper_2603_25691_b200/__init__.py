@@ -348,18 +348,23 @@ class ObservationSet:
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p),
                  self.num_obs(), self._idx.ctypes.data, self._values.ctypes.data, k, flags, shard, shards,
                  ctypes.byref(h))
-            self._plans[key] = _Handle(h, "cphifi_obs_destroy")
-        return self._plans[key].h
+            self._plans[key] = _Handle(h, "cphifi_obs_destroy", deps=(ctx,))
+        return self._plans[key]
 
 
 class _Handle:
-    def __init__(self, h, destroy):
+    """Owns one C-ABI handle.  `deps` keeps the handles it points into (observation plan,
+    mode, context) alive until after this one is destroyed."""
+
+    def __init__(self, h, destroy, deps=()):
         self.h = h
         self.destroy = destroy
+        self.deps = tuple(deps)
 
     def __del__(self):
         if self.h:
             getattr(_capi.load(), self.destroy)(self.h)
+            self.h = None
 
 
 def sample_uniform(source: DenseTensor, q: int, seed: int, multiset: bool = False) -> ObservationSet:
@@ -431,8 +436,8 @@ class UnalignedSubproblem:
         arrs, ptrs = _factor_array(model.factors, k)
         plan = obs.plan(k, mode.ctx, shard, shards)
         h = ctypes.c_void_p()
-        call("cphifi_unaligned_create", plan, mode.handle, self._r, ptrs, self.rho, ctypes.byref(h))
-        self._h = _Handle(h, "cphifi_unaligned_destroy")
+        call("cphifi_unaligned_create", plan.h, mode.handle, self._r, ptrs, self.rho, ctypes.byref(h))
+        self._h = _Handle(h, "cphifi_unaligned_destroy", deps=(plan, mode))
         self.handle = h
 
     def n(self) -> int:
@@ -543,7 +548,7 @@ class _DeviceTensor:
         h = ctypes.c_void_p()
         call("cphifi_tensor_create", ctx.handle, len(t.shape()), shape.ctypes.data_as(c_int64_p),
              t.data().ctypes.data, 0, shard, shards, ctypes.byref(h))
-        self._h = _Handle(h, "cphifi_tensor_destroy")
+        self._h = _Handle(h, "cphifi_tensor_destroy", deps=(ctx,))
         self.handle = h
 
 

@@ -131,54 +131,85 @@ cphifi_mode new_mode(cphifi_ctx ctx, int64_t n, double lambda) {
 }
 
 // ---- unaligned pieces ------------------------------------------------------------------
-SgArgs sg_args(cphifi_unaligned p) {
+FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     cphifi_obs o = p->obs;
-    SgArgs a;
+    FusedArgs a;
     a.n = p->n;
+    a.r = p->r;
     a.rp = p->rp;
     a.q = o->q_local;
     a.dother = o->d - 1;
+    a.phases = phases;
     a.row_ptr = o->row_ptr.get();
     a.idx = o->idx_o.get();
     a.fac = p->fac.get();
     for (int m = 0; m < o->d - 1; ++m) a.fac_off[m] = p->fac_off[m];
-    a.yhat = p->yhat_rm.get();
+    a.fac_total = (int64_t)p->fac.n;
+    a.kmat = p->mode->kernel.get();
+    a.xhat_rm = p->xhat_rm.get();
+    a.yhat_rm = p->yhat_rm.get();
     a.slot_a = p->slot_a.get();
     a.slot_b = p->slot_b.get();
-    a.units = p->units;
+    a.cta_rows = p->cta_rows.get();
     a.chunk = p->chunk;
+    a.lambda = p->mode->lambda;
+    a.rho = p->rho;
+    a.barrier = p->barrier.get();
     return a;
 }
 
-// y = vec(K Yhat + lambda Xhat) + rho x with Xhat = K X  (unaligned.hpp:101-115)
+void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
+    fused_matvec(a, p->grid, p->smem, p->smem_factors, p->obs->ctx->stream);
+}
+
+// Xhat = K X -> column-major copy (lambda term) + row-major padded copy (kernel input)
+void xhat_gemm(cphifi_unaligned p, const double* x) {
+    cphifi_ctx ctx = p->obs->ctx;
+    GemmArgs g;
+    g.m = p->n; g.n = p->r; g.k = p->n;
+    g.a = p->mode->kernel.get(); g.a_rs = 1; g.a_cs = p->n;
+    g.b = x; g.b_rs = 1; g.b_cs = p->n;
+    g.c = p->xhat_cm.get(); g.c_rs = 1; g.c_cs = p->n;
+    g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
+    gemm(g, ctx->num_sms, ctx->stream);
+}
+
+// y = (K Yhat + lambda Xhat) + rho x
+void y_gemm(cphifi_unaligned p, const double* x, double* y) {
+    cphifi_ctx ctx = p->obs->ctx;
+    GemmArgs g;
+    g.m = p->n; g.n = p->r; g.k = p->n;
+    g.a = p->mode->kernel.get(); g.a_rs = 1; g.a_cs = p->n;
+    g.b = p->yhat_rm.get(); g.b_rs = p->rp; g.b_cs = 1;
+    g.c = y; g.c_rs = 1; g.c_cs = p->n;
+    g.epi = EPI_AXPY2;
+    g.e1 = p->xhat_cm.get(); g.e2 = x; g.ld_e = p->n;
+    g.beta1 = p->mode->lambda; g.beta2 = p->rho;
+    gemm(g, ctx->num_sms, ctx->stream);
+}
+
+// y = vec(K Yhat + lambda Xhat) + rho x with Xhat = K X  (unaligned.hpp:101-115).
+// Small n on one GPU: ONE cooperative launch.  Otherwise DMMA GEMMs around the fused
+// scatter-gather, with the NCCL all-reduce of Yhat between them on multi-GPU.
 void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     cphifi_ctx ctx = p->obs->ctx;
-    const int64_t n = p->n, r = p->r;
-    const double* kmat = p->mode->kernel.get();
-    {   // Xhat = K X -> column-major copy (lambda term) + row-major padded copy (K1 input)
-        GemmArgs g;
-        g.m = n; g.n = r; g.k = n;
-        g.a = kmat; g.a_rs = 1; g.a_cs = n;
-        g.b = x; g.b_rs = 1; g.b_cs = n;
-        g.c = p->xhat_cm.get(); g.c_rs = 1; g.c_cs = n;
-        g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
-        gemm(g, ctx->num_sms, ctx->stream);
+    const bool multi = ctx->comm && ctx->nranks > 1;
+    if (p->small_n) {
+        FusedArgs a = fused_args(p, multi ? (PH_A | PH_B | PH_C1) : (PH_A | PH_B | PH_C1 | PH_C2));
+        a.x = x;
+        a.y = y;
+        launch_fused(p, a);
+        if (multi) {
+            allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
+            a.phases = PH_C2;
+            launch_fused(p, a);
+        }
+        return;
     }
-    SgArgs a = sg_args(p);
-    a.xhat = p->xhat_rm.get();
-    scatter_gather(a, ctx->stream);
-    allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
-    {   // y = (K Yhat + lambda Xhat) + rho x
-        GemmArgs g;
-        g.m = n; g.n = r; g.k = n;
-        g.a = kmat; g.a_rs = 1; g.a_cs = n;
-        g.b = p->yhat_rm.get(); g.b_rs = p->rp; g.b_cs = 1;
-        g.c = y; g.c_rs = 1; g.c_cs = n;
-        g.epi = EPI_AXPY2;
-        g.e1 = p->xhat_cm.get(); g.e2 = x; g.ld_e = n;
-        g.beta1 = p->mode->lambda; g.beta2 = p->rho;
-        gemm(g, ctx->num_sms, ctx->stream);
-    }
+    xhat_gemm(p, x);
+    launch_fused(p, fused_args(p, PH_B | PH_C1));
+    allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
+    y_gemm(p, x, y);
 }
 
 // build_preconditioner (unaligned.hpp:120-134): eig(K) (cached), eig(V), D
@@ -652,9 +683,18 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         gram_kr(d, obs->shape.data(), r, fptr.data(), k, p->v.get(), s);
         // scratch
         const int64_t n = p->n;
-        sg_plan(obs->q_local, p->rp, ctx->num_sms, &p->units, &p->chunk);
-        p->slot_a.alloc(p->units * p->rp);
-        p->slot_b.alloc(p->units * p->rp);
+        // fused-kernel launch shape: all CTAs co-resident, equal observation count per CTA
+        p->small_n = n <= 512;
+        p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;
+        p->smem = fused_smem_bytes(p->rp, (int64_t)p->fac.n, p->smem_factors);
+        p->grid = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        p->chunk = std::max<int64_t>(1, (obs->q_local + p->grid - 1) / p->grid);
+        p->slot_a.alloc((size_t)p->grid * p->rp);
+        p->slot_b.alloc((size_t)p->grid * p->rp);
+        p->cta_rows.alloc(2 * (size_t)p->grid);
+        p->barrier.alloc(2);
+        CPHIFI_CUDA(cudaMemsetAsync(p->barrier.get(), 0, 2 * sizeof(unsigned), s));
+        fused_cta_rows(obs->row_ptr.get(), n, obs->q_local, p->chunk, p->grid, p->cta_rows.get(), s);
         p->xhat_rm.alloc(n * p->rp);
         p->yhat_rm.alloc(n * p->rp);
         p->xhat_cm.alloc(n * r);
@@ -663,9 +703,9 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         p->vx.alloc(n * r);
         p->vy.alloc(n * r);
         // B = sampled_mttkrp(obs, zhat, k) with the observed values (observations.hpp:186-188)
-        SgArgs a = sg_args(p);
+        FusedArgs a = fused_args(p, PH_B | PH_C1);
         a.weights = obs->values.get();
-        scatter_gather(a, s);
+        launch_fused(p, a);
         allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
         p->b.alloc(n * r);
         rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->b.get(), s);
@@ -734,38 +774,29 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
         cphifi_ctx ctx = p->obs->ctx;
         DeviceGuard dg(ctx->device);
         cudaStream_t s = ctx->stream;
-        const int64_t n = p->n, r = p->r;
+        const bool multi = ctx->comm && ctx->nranks > 1;
         cudaEvent_t ev[6];
         for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
         double acc[6] = {0, 0, 0, 0, 0, 0};
-        const double* kmat = p->mode->kernel.get();
         for (int it = 0; it < iters; ++it) {
             CPHIFI_CUDA(cudaEventRecord(ev[0], s));
-            GemmArgs g;
-            g.m = n; g.n = r; g.k = n;
-            g.a = kmat; g.a_rs = 1; g.a_cs = n;
-            g.b = x; g.b_rs = 1; g.b_cs = n;
-            g.c = p->xhat_cm.get(); g.c_rs = 1; g.c_cs = n;
-            g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
-            gemm(g, ctx->num_sms, s);
+            if (!p->small_n) xhat_gemm(p, x);
             CPHIFI_CUDA(cudaEventRecord(ev[1], s));
-            SgArgs a = sg_args(p);
-            a.xhat = p->xhat_rm.get();
-            sg_main(a, s);
+            FusedArgs a = fused_args(p, p->small_n ? (multi ? (PH_A | PH_B | PH_C1) : (PH_A | PH_B | PH_C1 | PH_C2))
+                                                  : (PH_B | PH_C1));
+            a.x = x;
+            a.y = y;
+            launch_fused(p, a);
             CPHIFI_CUDA(cudaEventRecord(ev[2], s));
-            sg_fixup(a, s);
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
-            allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+            allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
             CPHIFI_CUDA(cudaEventRecord(ev[4], s));
-            GemmArgs h;
-            h.m = n; h.n = r; h.k = n;
-            h.a = kmat; h.a_rs = 1; h.a_cs = n;
-            h.b = p->yhat_rm.get(); h.b_rs = p->rp; h.b_cs = 1;
-            h.c = y; h.c_rs = 1; h.c_cs = n;
-            h.epi = EPI_AXPY2;
-            h.e1 = p->xhat_cm.get(); h.e2 = x; h.ld_e = n;
-            h.beta1 = p->mode->lambda; h.beta2 = p->rho;
-            gemm(h, ctx->num_sms, s);
+            if (!p->small_n) {
+                y_gemm(p, x, y);
+            } else if (multi) {
+                a.phases = PH_C2;
+                launch_fused(p, a);
+            }
             CPHIFI_CUDA(cudaEventRecord(ev[5], s));
             CPHIFI_CUDA(cudaEventSynchronize(ev[5]));
             float ms;
@@ -791,9 +822,7 @@ int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, doub
         const int64_t n = p->n, r = p->r;
         h2d(p->vx.get(), xhat, sizeof(double) * n * r, ctx->stream);
         pack_rows(p->vx.get(), n, n, r, p->rp, p->xhat_rm.get(), ctx->stream);
-        SgArgs a = sg_args(p);
-        a.xhat = p->xhat_rm.get();
-        scatter_gather(a, ctx->stream);
+        launch_fused(p, fused_args(p, PH_B | PH_C1));
         allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
         rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->vy.get(), ctx->stream);
         d2h_sync(yhat_out, p->vy.get(), sizeof(double) * n * r, ctx->stream);

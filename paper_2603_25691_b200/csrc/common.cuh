@@ -134,9 +134,15 @@ struct cphifi_unaligned_s {
     // preconditioner state (lazy): eig(V), D
     bool have_veig = false;
     cphifi::DevBuf<double> uv, sv, dmat;
-    // scatter-gather scratch
-    int64_t units = 0, chunk = 1;
-    cphifi::DevBuf<double> slot_a, slot_b;  // units x rp
+    // fused operator kernel launch shape (k_fused.cu)
+    int grid = 0;                 // CTAs (all co-resident)
+    int64_t chunk = 1;            // observations per CTA
+    size_t smem = 0;              // dynamic shared memory bytes
+    bool smem_factors = false;    // factors staged in shared memory
+    bool small_n = false;         // phases A and C2 inside the fused kernel
+    cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid
+    cphifi::DevBuf<unsigned> barrier;   // grid barrier state
+    cphifi::DevBuf<double> slot_a, slot_b;  // grid x rp
     cphifi::DevBuf<double> xhat_rm, yhat_rm;  // n x rp row-major
     cphifi::DevBuf<double> xhat_cm;           // n x r column-major
     cphifi::DevBuf<double> t1, t2;            // n x r scratch (preconditioner)

@@ -1,5 +1,5 @@
-// k_unaligned.cu — the per-observation hot loop of the unaligned operator
-// plus PCG vector kernels and observation-plan helpers, for sm_100a.
+// k_unaligned.cu — PCG vector kernels and observation-plan helpers for sm_100a.  (The
+// per-observation operator kernel lives in k_fused.cu; its design notes follow.)
 //
 // K1 fuses the reference's two q-loops — gather_rows (observations.hpp:191-198) and
 // sampled_mttkrp (:174-184) — into ONE pass over observations pre-sorted by i_k (CSR):
@@ -19,153 +19,6 @@ namespace cphifi {
 namespace {
 
 constexpr int SG_THREADS = 256;
-
-__device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ row_ptr, int64_t n, int64_t pos) {
-    // largest i with row_ptr[i] <= pos  (upper_bound - 1)
-    int64_t lo = 0, hi = n;  // row_ptr[0] = 0 <= pos < row_ptr[n]
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldg(row_ptr + mid) <= pos) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
-template <int VPL>
-struct Vec;
-template <> struct Vec<1> {
-    double v[1];
-    __device__ __forceinline__ void load(const double* p) { v[0] = __ldg(p); }
-};
-template <> struct Vec<2> {
-    double v[2];
-    __device__ __forceinline__ void load(const double* p) {
-        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
-        v[0] = t.x; v[1] = t.y;
-    }
-};
-template <> struct Vec<4> {
-    double v[4];
-    __device__ __forceinline__ void load(const double* p) {
-        const double2 t0 = __ldg(reinterpret_cast<const double2*>(p));
-        const double2 t1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
-        v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-    }
-};
-
-// RP = padded rank (power of two >= 4); DO = number of other modes (d - 1).
-template <int RP, int DO>
-__global__ void __launch_bounds__(SG_THREADS) scatter_gather_kernel(const SgArgs a) {
-    constexpr int G = RP < 32 ? RP : 32;  // lanes per observation group
-    constexpr int VPL = RP / G;           // values per lane
-    const int lane = threadIdx.x & 31;
-    const int glane = lane % G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - glane));
-    const int64_t unit = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-    if (unit >= a.units) return;
-    const int64_t beg = unit * a.chunk;
-    const int64_t end = min(a.q, beg + a.chunk);
-    if (beg >= end) return;
-    const int jb = glane * VPL;
-
-    int64_t row = row_of(a.row_ptr, a.n, beg);
-    const int64_t first_row = row;
-    const int64_t last_row = row_of(a.row_ptr, a.n, end - 1);
-    int64_t row_end = __ldg(a.row_ptr + row + 1);
-
-    Vec<VPL> xh;
-    double acc[VPL];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
-    const bool dot = a.weights == nullptr;
-    if (dot) xh.load(a.xhat + row * RP + jb);
-
-    auto flush = [&](int64_t rr) {
-        double* dst;
-        if (rr == first_row) dst = a.slot_a + unit * RP;
-        else if (rr == last_row) dst = a.slot_b + unit * RP;
-        else dst = a.yhat + rr * RP;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) dst[jb + v] = acc[v];
-    };
-
-    for (int64_t l = beg; l < end; ++l) {
-        if (l >= row_end) {
-            flush(row);
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
-            do {
-                ++row;
-                row_end = __ldg(a.row_ptr + row + 1);
-            } while (l >= row_end);
-            if (dot) xh.load(a.xhat + row * RP + jb);
-        }
-        // z = A_{m0}(i) * A_{m1}(i) * ...   (ascending modes, starting from the first factor)
-        Vec<VPL> z;
-        {
-            const int64_t ix = __ldg(a.idx + l);
-            z.load(a.fac + a.fac_off[0] + ix * RP + jb);
-        }
-#pragma unroll
-        for (int m = 1; m < DO; ++m) {
-            const int64_t ix = __ldg(a.idx + (int64_t)m * a.q + l);
-            Vec<VPL> f;
-            f.load(a.fac + a.fac_off[m] + ix * RP + jb);
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) z.v[v] *= f.v[v];
-        }
-        double s;
-        if (dot) {
-            double p = 0.0;
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) p = fma(xh.v[v], z.v[v], p);
-#pragma unroll
-            for (int off = G / 2; off > 0; off >>= 1) p += __shfl_xor_sync(gmask, p, off, G);
-            s = p;
-        } else {
-            s = __ldg(a.weights + l);
-        }
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) acc[v] = fma(s, z.v[v], acc[v]);
-    }
-    flush(row);
-}
-
-// Fix-up: one thread per (row, column j < rp).  See the file comment for the slot rules.
-__global__ void sg_fixup_kernel(const SgArgs a) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= a.n * a.rp) return;
-    const int64_t i = e / a.rp, j = e % a.rp;
-    const int64_t rb = a.row_ptr[i], re = a.row_ptr[i + 1];
-    if (rb == re) {
-        a.yhat[e] = 0.0;
-        return;
-    }
-    const int64_t u0 = rb / a.chunk, u1 = (re - 1) / a.chunk;
-    auto uend = [&](int64_t u) { return min(a.q, (u + 1) * a.chunk); };
-    if (u0 == u1) {
-        const bool is_first = (rb == u0 * a.chunk);
-        const bool is_last = (re == uend(u0));
-        if (is_first) a.yhat[e] = a.slot_a[u0 * a.rp + j];
-        else if (is_last) a.yhat[e] = a.slot_b[u0 * a.rp + j];
-        // else interior: written directly by the unit
-        return;
-    }
-    double s = (rb == u0 * a.chunk) ? a.slot_a[u0 * a.rp + j] : a.slot_b[u0 * a.rp + j];
-    for (int64_t u = u0 + 1; u <= u1; ++u) s += a.slot_a[u * a.rp + j];
-    a.yhat[e] = s;
-}
-
-template <int RP>
-void launch_sg_rp(const SgArgs& a, unsigned blocks, cudaStream_t s) {
-    switch (a.dother) {
-        case 1: scatter_gather_kernel<RP, 1><<<blocks, SG_THREADS, 0, s>>>(a); break;
-        case 2: scatter_gather_kernel<RP, 2><<<blocks, SG_THREADS, 0, s>>>(a); break;
-        case 3: scatter_gather_kernel<RP, 3><<<blocks, SG_THREADS, 0, s>>>(a); break;
-        case 4: scatter_gather_kernel<RP, 4><<<blocks, SG_THREADS, 0, s>>>(a); break;
-        case 5: scatter_gather_kernel<RP, 5><<<blocks, SG_THREADS, 0, s>>>(a); break;
-        default: throw_invalid("unaligned: tensor order above 6 is not supported");
-    }
-}
 
 // ---- PCG vector kernels ------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
@@ -336,46 +189,6 @@ inline unsigned grid_for(int64_t n, int t, int cap = 8192) {
 }
 
 }  // namespace
-
-void sg_plan(int64_t q, int64_t rp, int num_sms, int64_t* units, int64_t* chunk) {
-    const int64_t g = rp < 32 ? rp : 32;
-    const int64_t groups_per_block = SG_THREADS / g;
-    // enough resident groups to fill every SM several times, but >= 16 observations each
-    int64_t u = (int64_t)num_sms * 8 * groups_per_block;
-    u = std::min<int64_t>(u, std::max<int64_t>(1, (q + 15) / 16));
-    int64_t c = std::max<int64_t>(1, (q + u - 1) / u);
-    u = std::max<int64_t>(1, (q + c - 1) / c);
-    *units = u;
-    *chunk = c;
-}
-
-void scatter_gather(const SgArgs& a, cudaStream_t s) {
-    sg_main(a, s);
-    sg_fixup(a, s);
-}
-
-void sg_main(const SgArgs& a, cudaStream_t s) {
-    if (a.q > 0) {
-        const int64_t g = a.rp < 32 ? a.rp : 32;
-        const int64_t threads = a.units * g;
-        const unsigned blocks = (unsigned)((threads + SG_THREADS - 1) / SG_THREADS);
-        switch (a.rp) {
-            case 4: launch_sg_rp<4>(a, blocks, s); break;
-            case 8: launch_sg_rp<8>(a, blocks, s); break;
-            case 16: launch_sg_rp<16>(a, blocks, s); break;
-            case 32: launch_sg_rp<32>(a, blocks, s); break;
-            case 64: launch_sg_rp<64>(a, blocks, s); break;
-            case 128: launch_sg_rp<128>(a, blocks, s); break;
-            default: throw_invalid("unaligned: rank above 128 is not supported");
-        }
-        CPHIFI_CHECK_LAUNCH();
-    }
-}
-
-void sg_fixup(const SgArgs& a, cudaStream_t s) {
-    sg_fixup_kernel<<<grid_for(a.n * a.rp, 256, 1 << 20), 256, 0, s>>>(a);
-    CPHIFI_CHECK_LAUNCH();
-}
 
 void dot_to(const double* x, const double* y, int64_t n, double* partial, double* out, cudaStream_t s) {
     dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, y, n, partial, out);

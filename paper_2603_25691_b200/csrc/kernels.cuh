@@ -59,25 +59,35 @@ void pack_rows(const double* src_cm, int64_t rows, int64_t ld, int64_t r, int64_
                cudaStream_t s);
 void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double* dst_cm, cudaStream_t s);
 
-// ---- unaligned scatter-gather (K1) + deterministic fix-up ------------------------------
-struct SgArgs {
-    int64_t n = 0, rp = 0, q = 0;
+// ---- the unaligned operator as one persistent cooperative kernel (k_fused.cu) -----------
+enum : unsigned { PH_A = 1u, PH_B = 2u, PH_C1 = 4u, PH_C2 = 8u };
+struct FusedArgs {
+    int64_t n = 0, r = 0, rp = 0, q = 0;
     int dother = 0;
-    const int64_t* row_ptr = nullptr;
-    const int32_t* idx = nullptr;       // dother x q
-    const double* fac = nullptr;        // packed row-major padded factors
+    unsigned phases = 0;
+    const int64_t* row_ptr = nullptr;   // local CSR over sorted i_k (n + 1)
+    const int32_t* idx = nullptr;       // dother x q, other modes ascending
+    const double* fac = nullptr;        // packed row-major rp-padded factors
     int64_t fac_off[8] = {0};
-    const double* weights = nullptr;    // non-null: s_l = weights[l] (RHS), else s_l = xhat . z
-    const double* xhat = nullptr;       // n x rp row-major
-    double* yhat = nullptr;             // n x rp row-major
-    double* slot_a = nullptr;
+    int64_t fac_total = 0;              // doubles in fac
+    const double* weights = nullptr;    // non-null: s_l = weights[l] (RHS B), else Xhat . z_l
+    const double* kmat = nullptr;       // n x n column-major, symmetric
+    const double* x = nullptr;          // n x r column-major
+    double* y = nullptr;                // n x r column-major
+    double* xhat_rm = nullptr;          // n x rp
+    double* yhat_rm = nullptr;          // n x rp
+    double* slot_a = nullptr;           // C x rp
     double* slot_b = nullptr;
-    int64_t units = 0, chunk = 1;
+    const int64_t* cta_rows = nullptr;  // 2 x C: first / last row of each CTA's range
+    int64_t chunk = 1;                  // observations per CTA
+    double lambda = 0.0, rho = 0.0;
+    unsigned* barrier = nullptr;        // 2 x uint, zero-initialised once
 };
-void sg_plan(int64_t q, int64_t rp, int num_sms, int64_t* units, int64_t* chunk);
-void scatter_gather(const SgArgs& a, cudaStream_t s);  // = sg_main + sg_fixup
-void sg_main(const SgArgs& a, cudaStream_t s);
-void sg_fixup(const SgArgs& a, cudaStream_t s);
+size_t fused_smem_bytes(int64_t rp, int64_t fac_total, bool smemf);
+int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
+void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out,
+                    cudaStream_t s);
+void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s);
 
 // ---- PCG vector kernels (deterministic reductions) --------------------------------------
 struct PcgState {
