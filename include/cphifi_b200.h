@@ -159,6 +159,11 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
  * [4] y = K Yhat + lambda Xhat + rho x, [5] the whole matvec. */
 int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters,
                                   double* ms_out);
+/* Tracing hook: one operator application on DEVICE buffers with per-CTA %globaltimer stamps
+ * (8 per CTA: entry, phase A done, barrier 1, phase B done, barrier 2, fix-up done,
+ * barrier 3, exit; 0 = phase not run).  *ctas receives the CTA count. */
+int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y,
+                                  uint64_t* stamps, int capacity, int* ctas);
 /* Test hook: Yhat = sampled_mttkrp(gather_rows(Xhat)) for a given Xhat (n x r), i.e.
  * observations.hpp:174-198 fused, before the final K multiply (all-reduced). */
 int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, double* yhat_out);

@@ -100,6 +100,8 @@ _SIGS = [
     ("cphifi_solve_unaligned_pcg", ctypes.c_int,
      [_H, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC), c_double_p, c_double_p]),
     ("cphifi_unaligned_matvec_timed", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c_double_p]),
+    ("cphifi_unaligned_matvec_trace", ctypes.c_int,
+     [_H, ctypes.c_void_p, ctypes.c_void_p, c_uint64_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_unaligned_scatter_gather", ctypes.c_int, [_H, c_double_p, c_double_p]),
     ("cphifi_tensor_create", ctypes.c_int,
      [_H, ctypes.c_int, c_int64_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, c_void_pp]),

@@ -131,6 +131,19 @@ cphifi_mode new_mode(cphifi_ctx ctx, int64_t n, double lambda) {
 }
 
 // ---- unaligned pieces ------------------------------------------------------------------
+bool is_multi(cphifi_unaligned p) { return p->obs->ctx->comm && p->obs->ctx->nranks > 1; }
+
+// The complete (all-rank) Yhat: the local one on one GPU, the NCCL sum otherwise.
+double* yhat_result(cphifi_unaligned p) { return is_multi(p) ? p->yhat_sum.get() : p->yhat_rm.get(); }
+
+// Out-of-place sum of the ranks' partial Yhat (the local buffer keeps its zero rows).
+void allreduce_yhat(cphifi_unaligned p) {
+    cphifi_ctx ctx = p->obs->ctx;
+    if (is_multi(p))
+        CPHIFI_NCCL(ncclAllReduce(p->yhat_rm.get(), p->yhat_sum.get(), (size_t)p->n * p->rp, ncclDouble, ncclSum,
+                                  ctx->comm, ctx->stream));
+}
+
 FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     cphifi_obs o = p->obs;
     FusedArgs a;
@@ -155,11 +168,23 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     a.lambda = p->mode->lambda;
     a.rho = p->rho;
     a.barrier = p->barrier.get();
+    a.rowcnt = p->rowcnt.get();
+    a.prefetch = p->prefetch ? 1 : 0;
+    a.yhat_c2 = yhat_result(p);
     return a;
 }
 
 void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
     fused_matvec(a, p->grid, p->smem, p->smem_factors, p->obs->ctx->stream);
+}
+
+// Phase sets of the operator launches (see kernels.cuh).  part 0 = the (first) launch,
+// part 1 = the launch after the NCCL all-reduce (multi-GPU, small n).
+unsigned matvec_phases(cphifi_unaligned p, bool multi, int part) {
+    const unsigned ax = p->local_x ? PH_AL : PH_A;
+    if (!p->small_n) return PH_B;
+    if (!multi) return ax | PH_B | PH_C2;
+    return part == 0 ? (ax | PH_B) : ((p->local_x ? PH_AL : 0u) | PH_C2);
 }
 
 // Xhat = K X -> column-major copy (lambda term) + row-major padded copy (kernel input)
@@ -180,7 +205,7 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
     GemmArgs g;
     g.m = p->n; g.n = p->r; g.k = p->n;
     g.a = p->mode->kernel.get(); g.a_rs = 1; g.a_cs = p->n;
-    g.b = p->yhat_rm.get(); g.b_rs = p->rp; g.b_cs = 1;
+    g.b = yhat_result(p); g.b_rs = p->rp; g.b_cs = 1;
     g.c = y; g.c_rs = 1; g.c_cs = p->n;
     g.epi = EPI_AXPY2;
     g.e1 = p->xhat_cm.get(); g.e2 = x; g.ld_e = p->n;
@@ -195,20 +220,20 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     cphifi_ctx ctx = p->obs->ctx;
     const bool multi = ctx->comm && ctx->nranks > 1;
     if (p->small_n) {
-        FusedArgs a = fused_args(p, multi ? (PH_A | PH_B | PH_C1) : (PH_A | PH_B | PH_C1 | PH_C2));
+        FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
         a.x = x;
         a.y = y;
         launch_fused(p, a);
         if (multi) {
-            allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
-            a.phases = PH_C2;
+            allreduce_yhat(p);
+            a.phases = matvec_phases(p, multi, 1);
             launch_fused(p, a);
         }
         return;
     }
     xhat_gemm(p, x);
-    launch_fused(p, fused_args(p, PH_B | PH_C1));
-    allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
+    launch_fused(p, fused_args(p, PH_B));
+    allreduce_yhat(p);
     y_gemm(p, x, y);
 }
 
@@ -684,31 +709,52 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // scratch
         const int64_t n = p->n;
         // fused-kernel launch shape: all CTAs co-resident, equal observation count per CTA
-        p->small_n = n <= 512;
+        p->small_n = n <= 512 && n * r <= 8192;
+        p->prefetch = p->small_n;
         p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;
-        p->smem = fused_smem_bytes(p->rp, (int64_t)p->fac.n, p->smem_factors);
+        if (const char* e = std::getenv("CPHIFI_SMEM_FACTORS")) p->smem_factors = p->smem_factors && std::atoi(e) != 0;
+        const int64_t crows = (n + ctx->num_sms - 1) / ctx->num_sms;  // >= rows per CTA in PH_C2
+        const int64_t pref = p->prefetch ? n * r + (fused_maxloc() + crows) * n : 0;
+        p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
         p->grid = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        p->rowcnt.alloc(n);
+        CPHIFI_CUDA(cudaMemsetAsync(p->rowcnt.get(), 0, n * sizeof(unsigned), s));
         p->chunk = std::max<int64_t>(1, (obs->q_local + p->grid - 1) / p->grid);
         p->slot_a.alloc((size_t)p->grid * p->rp);
         p->slot_b.alloc((size_t)p->grid * p->rp);
         p->cta_rows.alloc(2 * (size_t)p->grid);
-        p->barrier.alloc(2);
-        CPHIFI_CUDA(cudaMemsetAsync(p->barrier.get(), 0, 2 * sizeof(unsigned), s));
+        const size_t bw = barrier_words(p->grid, 16);
+        p->barrier.alloc(bw);
+        CPHIFI_CUDA(cudaMemsetAsync(p->barrier.get(), 0, bw * sizeof(unsigned), s));
         fused_cta_rows(obs->row_ptr.get(), n, obs->q_local, p->chunk, p->grid, p->cta_rows.get(), s);
+        {   // CTA-local Xhat rows (no grid barrier before the scatter-gather) when every CTA's
+            // observation range touches at most MAXLOC rows
+            std::vector<int64_t> cr(2 * (size_t)p->grid);
+            d2h_sync(cr.data(), p->cta_rows.get(), sizeof(int64_t) * cr.size(), s);
+            int64_t span = 0;
+            for (int c = 0; c < p->grid; ++c)
+                if (std::min<int64_t>(obs->q_local, (int64_t)c * p->chunk) < obs->q_local)
+                    span = std::max<int64_t>(span, cr[2 * c + 1] - cr[2 * c] + 1);
+            p->local_x = p->small_n && span <= fused_maxloc();
+        }
         p->xhat_rm.alloc(n * p->rp);
         p->yhat_rm.alloc(n * p->rp);
+        // rows without observations in this shard are never written: keep them zero
+        CPHIFI_CUDA(cudaMemsetAsync(p->yhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
+        CPHIFI_CUDA(cudaMemsetAsync(p->xhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
+        if (ctx->comm && ctx->nranks > 1) p->yhat_sum.alloc(n * p->rp);
         p->xhat_cm.alloc(n * r);
         p->t1.alloc(n * r);
         p->t2.alloc(n * r);
         p->vx.alloc(n * r);
         p->vy.alloc(n * r);
         // B = sampled_mttkrp(obs, zhat, k) with the observed values (observations.hpp:186-188)
-        FusedArgs a = fused_args(p, PH_B | PH_C1);
+        FusedArgs a = fused_args(p, PH_B);
         a.weights = obs->values.get();
         launch_fused(p, a);
-        allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
+        allreduce_yhat(p);
         p->b.alloc(n * r);
-        rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->b.get(), s);
+        rm_to_cm(yhat_result(p), n, p->rp, r, p->b.get(), s);
         CPHIFI_CUDA(cudaStreamSynchronize(s));
         *out = hold.release();
     });
@@ -782,19 +828,18 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
             CPHIFI_CUDA(cudaEventRecord(ev[0], s));
             if (!p->small_n) xhat_gemm(p, x);
             CPHIFI_CUDA(cudaEventRecord(ev[1], s));
-            FusedArgs a = fused_args(p, p->small_n ? (multi ? (PH_A | PH_B | PH_C1) : (PH_A | PH_B | PH_C1 | PH_C2))
-                                                  : (PH_B | PH_C1));
+            FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
             a.x = x;
             a.y = y;
             launch_fused(p, a);
             CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
-            allreduce(ctx, p->yhat_rm.get(), (size_t)p->n * p->rp);
+            allreduce_yhat(p);
             CPHIFI_CUDA(cudaEventRecord(ev[4], s));
             if (!p->small_n) {
                 y_gemm(p, x, y);
             } else if (multi) {
-                a.phases = PH_C2;
+                a.phases = matvec_phases(p, multi, 1);
                 launch_fused(p, a);
             }
             CPHIFI_CUDA(cudaEventRecord(ev[5], s));
@@ -812,6 +857,32 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
     });
 }
 
+int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y, uint64_t* stamps, int capacity,
+                                  int* ctas) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        need(ctas, "ctas");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        *ctas = p->grid;
+        const size_t cnt = (size_t)p->grid * TRACE_SLOTS;
+        DevBuf<unsigned long long> tr(cnt);
+        CPHIFI_CUDA(cudaMemsetAsync(tr.get(), 0, cnt * sizeof(unsigned long long), ctx->stream));
+        const bool multi = ctx->comm && ctx->nranks > 1;
+        if (!p->small_n) xhat_gemm(p, x);
+        FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
+        a.x = x;
+        a.y = y;
+        a.trace = tr.get();
+        launch_fused(p, a);
+        if (stamps && capacity > 0)
+            d2h_sync(stamps, tr.get(), sizeof(uint64_t) * std::min(cnt, (size_t)capacity), ctx->stream);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, double* yhat_out) {
     return guard([&] {
         need(p, "p");
@@ -822,9 +893,11 @@ int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, doub
         const int64_t n = p->n, r = p->r;
         h2d(p->vx.get(), xhat, sizeof(double) * n * r, ctx->stream);
         pack_rows(p->vx.get(), n, n, r, p->rp, p->xhat_rm.get(), ctx->stream);
-        launch_fused(p, fused_args(p, PH_B | PH_C1));
-        allreduce(ctx, p->yhat_rm.get(), (size_t)n * p->rp);
-        rm_to_cm(p->yhat_rm.get(), n, p->rp, r, p->vy.get(), ctx->stream);
+        FusedArgs a = fused_args(p, PH_B);
+        a.phases = PH_B;
+        launch_fused(p, a);
+        allreduce_yhat(p);
+        rm_to_cm(yhat_result(p), n, p->rp, r, p->vy.get(), ctx->stream);
         d2h_sync(yhat_out, p->vy.get(), sizeof(double) * n * r, ctx->stream);
     });
 }

@@ -140,6 +140,10 @@ struct cphifi_unaligned_s {
     size_t smem = 0;              // dynamic shared memory bytes
     bool smem_factors = false;    // factors staged in shared memory
     bool small_n = false;         // phases A and C2 inside the fused kernel
+    bool local_x = false;         // every CTA spans <= MAXLOC rows: CTA-local Xhat (PH_AL)
+    bool prefetch = false;        // X and K columns staged in shared memory (small n * r)
+    cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters
+    cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU)
     cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid
     cphifi::DevBuf<unsigned> barrier;   // grid barrier state
     cphifi::DevBuf<double> slot_a, slot_b;  // grid x rp

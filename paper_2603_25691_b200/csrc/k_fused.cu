@@ -2,173 +2,365 @@
 //
 //   y = vec(K Yhat + lambda Xhat) + rho x,  Xhat = K X,
 //   Yhat(i,:) = sum_{l: i_k(l)=i} (Xhat(i,:) . z_l) z_l,  z_l = prod_{m!=k} A_m(i_m(l),:)
-// (unaligned.hpp:101-115 with gather_rows + sampled_mttkrp, observations.hpp:174-198, fused).
+// (unaligned.hpp:101-115 with gather_rows + sampled_mttkrp, observations.hpp:174-198, fused;
+// Zhat is never materialised).
 //
-// Phases, separated by a software grid barrier (all CTAs co-resident: cooperative launch):
-//   A  Xhat rows            CTA c computes rows [c n / C, (c+1) n / C)      (small n only)
-//   B  scatter-gather       CTA c streams observations [c*chunk, (c+1)*chunk) of the i_k-sorted
-//                           set in ROUNDS of NG consecutive observations, one per lane group
-//                           (G lanes x VPL doubles = the padded rank).  Each group keeps its
-//                           row accumulator in registers; when the round crosses a row boundary
-//                           the CTA reduces the groups' accumulators in group order through
-//                           shared memory and writes the row: directly to Yhat if the row is
-//                           interior to the CTA, else to the CTA's slot A (first row) / B (last).
-//   C1 fix-up               rows split across CTAs = slot sums in CTA order
-//   C2 y rows               y = K Yhat + lambda Xhat + rho x                  (small n only)
-// Every reduction has a fixed order, so results are bit-reproducible for a given launch shape.
-// Factor rows are staged in shared memory when they fit (SURVEY §7 hard part 4).
-#include <cooperative_groups.h>
-
+// Phases (small n, one GPU: a single launch with ONE grid barrier):
+//   AL  Xhat rows     each CTA computes the (<= MAXLOC) rows its own observations touch, from
+//                     X and K columns prefetched into shared memory at entry
+//   (A  fallback      rows distributed over CTAs + a grid barrier)
+//   B   scatter-gather CTA c streams observations [c*chunk, (c+1)*chunk) of the i_k-sorted set
+//                     in ROUNDS of NG consecutive observations, one per lane group (G lanes x
+//                     VPL doubles = the padded rank), four rounds in flight per group.  Each
+//                     group keeps its row accumulator in registers; at a row boundary the CTA
+//                     reduces the groups in group order (fixed tree) and writes the row:
+//                     directly to Yhat if the row is interior to the CTA; otherwise to the CTA's
+//                     slot (A = first row, B = last row), and the LAST CTA to finish a split row
+//                     (per-row arrival counter) sums its slots in CTA order into Yhat.
+//   --  grid barrier
+//   C2  y rows        y = K Yhat + lambda Xhat + rho x for rows [c n / C, (c+1) n / C)
+// Every reduction has a fixed order, so results are bit-reproducible for a launch shape.
+// Large n: the DMMA GEMM kernels compute Xhat and y; this kernel runs phase B only.
+//
+// Memory pipeline: the observation stream (int32 index columns, fp64 weights) is staged in
+// shared memory tile by tile with cp.async (tiles 0 and 1 issued at kernel entry, so their HBM
+// latency hides behind phase AL); packed factor rows are staged in shared memory when they fit
+// (SURVEY §7 hard part 4), so the round loop runs from shared memory.
 #include "kernels.cuh"
 
 namespace cphifi {
 namespace {
 
-constexpr int FT = 256;  // threads per CTA
+constexpr int FT = 512;    // threads per CTA
+constexpr int TILE = 512;  // observations per staged tile
+constexpr int MAXLOC = 4;  // PH_AL: max rows one CTA computes Xhat for
+constexpr int UNR = 4;     // rounds in flight per group in the fast path
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Two-level software grid barrier (all CTAs co-resident: cooperative launch).  CTAs arrive on
+// per-group counters (one 128-byte line each, `group` CTAs per counter); the last arriver of a
+// group arrives on the top counter; the last group bumps the generation word.  Counters are
+// never reset: an episode is complete when a counter reaches a multiple of its member count.
+// Layout: bar[0] top count, bar[32] generation, bar[64 + 32*k] count of group k.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int group) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* vb = bar;
-        const unsigned gen = vb[1];
-        __threadfence();
-        const unsigned arrived = atomicAdd(bar, 1u);
-        if (arrived == gridDim.x - 1) {
-            vb[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (vb[1] == gen) __nanosleep(40);
+        const int C = gridDim.x, k = blockIdx.x / group;
+        const unsigned ngrp = (unsigned)((C + group - 1) / group);
+        const unsigned members = (unsigned)min(group, C - k * group);
+        const unsigned gen = ld_acquire(bar + 32);
+        __threadfence();  // cumulative: this CTA's writes (ordered by bar.sync) before arrival
+        const unsigned old = atom_add_acqrel(bar + 64 + 32 * k, 1u);
+        if ((old + 1) % members == 0) {
+            const unsigned old2 = atom_add_acqrel(bar, 1u);
+            if ((old2 + 1) % ngrp == 0) red_release_add(bar + 32, 1u);
         }
-        __threadfence();
+        while (ld_acquire(bar + 32) == gen) {
+        }
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void stamp(const FusedArgs& a, int slot) {
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[(size_t)blockIdx.x * TRACE_SLOTS + slot] = t;
+    }
 }
 
 template <int VPL>
 __device__ __forceinline__ void ldv(double (&v)[VPL], const double* p) {
     if constexpr (VPL == 1) {
         v[0] = p[0];
-    } else if constexpr (VPL == 2) {
-        const double2 t = *reinterpret_cast<const double2*>(p);
-        v[0] = t.x; v[1] = t.y;
     } else {
 #pragma unroll
         for (int u = 0; u < VPL; u += 2) {
             const double2 t = *reinterpret_cast<const double2*>(p + u);
-            v[u] = t.x; v[u + 1] = t.y;
+            v[u] = t.x;
+            v[u + 1] = t.y;
         }
     }
 }
 
-// Small dense row kernel: out(i, j) = sum_k M(k, i) * V(k, j) for rows i of this CTA (M is
-// symmetric n x n column-major, so column i is row i; V(k, j) at v[k*vs_r + j*vs_c]).
-// thread t -> column j = t / S, k-slice s = t % S; slices are summed in order.
+// out[j] = sum_k kc[k] * V(k, j), j < r, for one row (kc = the row's K column, length n).
+// thread t -> column j = t / S, slice s = t % S over k; the S partials are combined by a
+// fixed xor-shuffle tree inside the warp (and an ordered smem pass when S > 32).
 template <int RP>
-__device__ __forceinline__ void rows_times(const FusedArgs& a, int64_t i, const double* __restrict__ v,
-                                           int64_t vs_r, int64_t vs_c, double* red, double* out_j) {
+__device__ __forceinline__ void row_dot(const FusedArgs& a, const double* __restrict__ kc, const double* __restrict__ v,
+                                        int64_t vs_r, int64_t vs_c, double* red, double* out) {
     constexpr int S = FT / RP;
+    constexpr int W = S < 32 ? S : 32;
     const int j = threadIdx.x / S, s = threadIdx.x % S;
     double t = 0.0;
     if (j < a.r) {
-        const double* mcol = a.kmat + i * a.n;
-        for (int64_t k = s; k < a.n; k += S) t = fma(mcol[k], v[k * vs_r + j * vs_c], t);
+        const double* vj = v + j * vs_c;
+#pragma unroll 8
+        for (int64_t k = s; k < a.n; k += S) t = fma(kc[k], vj[k * vs_r], t);
     }
-    red[threadIdx.x] = t;
-    __syncthreads();
-    if (threadIdx.x < RP) {
-        double acc = 0.0;
-        for (int q = 0; q < S; ++q) acc += red[threadIdx.x * S + q];
-        out_j[threadIdx.x] = acc;
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if constexpr (S > 32) {
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x < RP) {
+            double acc = 0.0;
+            for (int q = 0; q < S / 32; ++q) acc += red[threadIdx.x * (S / 32) + q];
+            out[threadIdx.x] = threadIdx.x < a.r ? acc : 0.0;
+        }
+    } else {
+        if (s == 0) out[j] = j < a.r ? t : 0.0;
     }
     __syncthreads();
 }
 
 template <int RP, int DO, bool SMEMF>
 __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
-    constexpr int G = RP < 32 ? RP : 32;
-    constexpr int VPL = RP / G;
-    constexpr int NG = FT / G;
+    constexpr int VPL = 4;                // doubles per lane (two LDS.128 per factor row)
+    constexpr int G = RP / VPL;           // lanes per observation: few shuffle steps per dot
+    constexpr int NG = FT / G;            // observations per round
+    constexpr int P = (NG < 8 ? NG : 8) < FT / RP ? (NG < 8 ? NG : 8) : FT / RP;  // flush tree fan-in
     extern __shared__ __align__(16) double smem[];
-    double* red = smem;                    // NG * RP doubles (>= FT)
-    double* rowbuf = red + (NG * RP > FT ? NG * RP : FT);  // 2 * RP doubles
-    double* sfac = rowbuf + 2 * RP;        // staged factors (SMEMF)
+    double* red = smem;                   // FT * VPL doubles (= NG * RP)
+    double* red2 = red + FT * VPL;        // FT doubles
+    double* rowbuf = red2 + FT;           // 2 * RP doubles
+    double* xloc = rowbuf + 2 * RP;       // MAXLOC * RP: this CTA's Xhat rows (PH_AL)
+    double* sw = xloc + MAXLOC * RP;      // 2 x TILE weights (RHS mode)
+    int32_t* sidx = reinterpret_cast<int32_t*>(sw + 2 * TILE);       // 2 x DO x TILE
+    double* sfac = reinterpret_cast<double*>(sidx + 2 * DO * TILE);   // staged factors (SMEMF)
+    double* xs = sfac + (SMEMF ? a.fac_total : 0);                   // X, n x r (prefetch)
+    double* kcs = xs + (a.prefetch ? a.n * a.r : 0);                 // K columns (prefetch)
     __shared__ int64_t s_rows[2];
+    __shared__ int s_last;
 
     const int c = blockIdx.x, C = gridDim.x;
     const int g = threadIdx.x / G, glane = threadIdx.x % G, jb = glane * VPL;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - lane % G));
+    const bool dot = a.weights == nullptr;
+    const int64_t ca = min(a.q, (int64_t)c * a.chunk), cb = min(a.q, ca + a.chunk);
+    const int ntiles = (a.phases & PH_B) && ca < cb ? (int)((cb - ca + TILE - 1) / TILE) : 0;
+    const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
 
-    // stage the packed factors (row-major, rp-padded) in shared memory
-    if constexpr (SMEMF) {
-        const double2* src = reinterpret_cast<const double2*>(a.fac);
-        double2* dst = reinterpret_cast<double2*>(sfac);
-        for (int64_t e = threadIdx.x; e < a.fac_total / 2; e += FT) dst[e] = src[e];
+    auto issue_tile = [&](int t) {
+        const int buf = t & 1;
+        const int64_t t0 = ca + (int64_t)t * TILE;
+        const int cnt = (int)min((int64_t)TILE, cb - t0);
+#pragma unroll
+        for (int m = 0; m < DO; ++m)
+            for (int o = threadIdx.x; o < cnt; o += FT)
+                cp_async4(sidx + (buf * DO + m) * TILE + o, a.idx + (int64_t)m * a.q + t0 + o);
+        if (!dot)
+            for (int o = threadIdx.x; o < cnt; o += FT) cp_async8(sw + buf * TILE + o, a.weights + t0 + o);
+    };
+
+    stamp(a, 0);
+    if (ntiles > 0 && threadIdx.x == 0) {
+        s_rows[0] = a.cta_rows[2 * c];
+        s_rows[1] = a.cta_rows[2 * c + 1];
+    }
+    __syncthreads();
+    const int64_t first_row = s_rows[0], last_row = s_rows[1];
+    const bool do_al = (a.phases & PH_AL) && ntiles > 0 && dot;
+    const int nal = do_al ? (int)(last_row - first_row + 1) : 0;
+
+    // ---- entry: async prefetch (group 0: factors, X, K columns, tile 0; group 1: tile 1) ----
+    if (ntiles > 0) {
+        if constexpr (SMEMF) {
+            const double2* src = reinterpret_cast<const double2*>(a.fac);
+            for (int64_t e = threadIdx.x; e < a.fac_total / 2; e += FT) cp_async16(sfac + 2 * e, src + e);
+        }
+    }
+    const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
+    if (pf) {
+        for (int64_t e = threadIdx.x; e < a.n * a.r; e += FT) cp_async8(xs + e, a.x + e);
+        for (int rr = 0; rr < nal; ++rr)
+            for (int64_t k = threadIdx.x; k < a.n; k += FT) cp_async8(kcs + rr * a.n + k, a.kmat + (first_row + rr) * a.n + k);
+        if (a.phases & PH_C2)
+            for (int64_t i = i0; i < i1; ++i)
+                for (int64_t k = threadIdx.x; k < a.n; k += FT)
+                    cp_async8(kcs + (MAXLOC + i - i0) * a.n + k, a.kmat + i * a.n + k);
+    }
+    if (ntiles > 0) issue_tile(0);
+    cp_commit();
+    if (ntiles > 1) {
+        issue_tile(1);
+        cp_commit();
     }
     const double* fac = SMEMF ? sfac : a.fac;
 
-    // ---- phase A: Xhat rows (small n) ----------------------------------------------------
-    if (a.phases & PH_A) {
-        const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;
-        for (int64_t i = i0; i < i1; ++i) {
-            rows_times<RP>(a, i, a.x, 1, a.n, red, rowbuf);
-            if (threadIdx.x < RP) a.xhat_rm[i * RP + threadIdx.x] = threadIdx.x < a.r ? rowbuf[threadIdx.x] : 0.0;
+    // ---- phase A: Xhat rows -----------------------------------------------------------------
+    if (a.phases & PH_AL) {  // only the rows this CTA's observations touch, from shared memory
+        if (ntiles > 1) cp_wait<1>();
+        else cp_wait<0>();
+        __syncthreads();
+        for (int rr = 0; rr < nal; ++rr) {
+            row_dot<RP>(a, kcs + rr * a.n, xs, 1, a.n, red, xloc + rr * RP);
+            if (threadIdx.x < RP) a.xhat_rm[(first_row + rr) * RP + threadIdx.x] = xloc[rr * RP + threadIdx.x];
         }
-        grid_barrier(a.barrier);
+        stamp(a, 1);
+    } else if (a.phases & PH_A) {  // rows distributed over CTAs, then a grid barrier
+        for (int64_t i = i0; i < i1; ++i) {
+            row_dot<RP>(a, a.kmat + i * a.n, a.x, 1, a.n, red, rowbuf);
+            if (threadIdx.x < RP) a.xhat_rm[i * RP + threadIdx.x] = rowbuf[threadIdx.x];
+        }
+        stamp(a, 1);
+        grid_barrier(a.barrier, a.bar_groups);
+        stamp(a, 2);
     }
+    const bool local_x = (a.phases & PH_AL) != 0;
 
     // ---- phase B: fused gather / scatter over this CTA's observations ---------------------
-    if (a.phases & PH_B) {
-        const int64_t ca = min(a.q, (int64_t)c * a.chunk), cb = min(a.q, ca + a.chunk);
-        if (ca < cb) {
-            if (threadIdx.x == 0) {
-                s_rows[0] = a.cta_rows[2 * c];
-                s_rows[1] = a.cta_rows[2 * c + 1];
+    if (ntiles > 0) {
+        int64_t cur = first_row;
+        int64_t cur_end = a.row_ptr[cur + 1];
+        double xh[VPL], acc[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
+        auto load_xh = [&]() {
+            if (dot) ldv<VPL>(xh, local_x ? xloc + (cur - first_row) * RP + jb : a.xhat_rm + cur * RP + jb);
+        };
+        load_xh();
+
+        auto flush = [&](int64_t row) {
+            __syncthreads();
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) red[g * RP + jb + v] = acc[v];
+            __syncthreads();
+            if (threadIdx.x < P * RP) {  // fixed two-level tree over the NG groups
+                const int j = threadIdx.x % RP, part = threadIdx.x / RP;
+                double s = 0.0;
+                for (int q = part * (NG / P); q < (part + 1) * (NG / P); ++q) s += red[q * RP + j];
+                red2[part * RP + j] = s;
             }
             __syncthreads();
-            const int64_t first_row = s_rows[0], last_row = s_rows[1];
-            int64_t cur = first_row;
-            int64_t cur_end = a.row_ptr[cur + 1];
-            const bool dot = a.weights == nullptr;
-            double xh[VPL], acc[VPL];
+            const int64_t rb = a.row_ptr[row], re = a.row_ptr[row + 1];
+            // positions and chunk are < 2^31 (q is capped at INT32_MAX): 32-bit divisions
+            const int64_t u0 = (uint32_t)rb / (uint32_t)a.chunk, u1 = (uint32_t)(re - 1) / (uint32_t)a.chunk;
+            const bool split = u1 > u0;  // the row continues in other CTAs
+            if (threadIdx.x < RP) {
+                double s = 0.0;
+#pragma unroll
+                for (int part = 0; part < P; ++part) s += red2[part * RP + threadIdx.x];
+                double* dst = !split ? a.yhat_rm + row * RP
+                            : row == first_row ? a.slot_a + (int64_t)c * RP
+                                               : a.slot_b + (int64_t)c * RP;
+                dst[threadIdx.x] = s;
+            }
 #pragma unroll
             for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
-            if (dot) ldv<VPL>(xh, a.xhat_rm + cur * RP + jb);
-
-            auto flush = [&](int64_t row) {
+            if (split) {  // the last of the row's CTAs to arrive sums the slots in CTA order
                 __syncthreads();
-#pragma unroll
-                for (int v = 0; v < VPL; ++v) red[g * RP + jb + v] = acc[v];
-                __syncthreads();
-                if (threadIdx.x < RP) {
-                    double s = 0.0;
-                    for (int q = 0; q < NG; ++q) s += red[q * RP + threadIdx.x];
-                    double* dst = row == first_row ? a.slot_a + (int64_t)c * RP
-                                : row == last_row ? a.slot_b + (int64_t)c * RP
-                                                  : a.yhat_rm + row * RP;
-                    dst[threadIdx.x] = s;
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    const unsigned need = (unsigned)(u1 - u0 + 1);
+                    s_last = atom_add_acqrel(a.rowcnt + row, 1u) == need - 1;
+                    if (s_last) a.rowcnt[row] = 0;  // ready for the next launch
                 }
-#pragma unroll
-                for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
-            };
+                __syncthreads();
+                if (s_last && threadIdx.x < RP) {
+                    const int j = threadIdx.x;
+                    double s = rb == u0 * a.chunk ? __ldcg(a.slot_a + u0 * RP + j) : __ldcg(a.slot_b + u0 * RP + j);
+                    for (int64_t u = u0 + 1; u <= u1; ++u) s += __ldcg(a.slot_a + u * RP + j);
+                    a.yhat_rm[row * RP + j] = s;
+                }
+            }
+        };
 
-            for (int64_t base = ca; base < cb; base += NG) {
+        for (int t = 0; t < ntiles; ++t) {
+            if (t + 1 < ntiles) cp_wait<1>();
+            else cp_wait<0>();
+            __syncthreads();
+            if (t == 0) stamp(a, 2);
+            const int buf = t & 1;
+            const int64_t t0 = ca + (int64_t)t * TILE;
+            const int64_t t1 = min(cb, t0 + TILE);
+            const int32_t* ti = sidx + buf * DO * TILE;
+            const double* tw = sw + buf * TILE;
+            int64_t base = t0;
+            while (base < t1) {
+                // fast path: UNR full rounds inside the current row, four chains in flight
+                if (base + UNR * NG <= min(t1, cur_end)) {
+                    double z[UNR][VPL], s[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        const int o = (int)(base + u * NG + g - t0);
+                        ldv<VPL>(z[u], fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
+#pragma unroll
+                        for (int m = 1; m < DO; ++m) {
+                            double f[VPL];
+                            ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)ti[m * TILE + o] * RP + jb);
+#pragma unroll
+                            for (int v = 0; v < VPL; ++v) z[u][v] *= f[v];
+                        }
+                        if (dot) {
+                            double p = 0.0;
+#pragma unroll
+                            for (int v = 0; v < VPL; ++v) p = fma(xh[v], z[u][v], p);
+                            s[u] = p;
+                        } else {
+                            s[u] = tw[o];
+                        }
+                    }
+                    if (dot) {
+#pragma unroll
+                        for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+                            for (int u = 0; u < UNR; ++u) s[u] += __shfl_xor_sync(gmask, s[u], off, G);
+                    }
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                        for (int v = 0; v < VPL; ++v) acc[v] = fma(s[u], z[u][v], acc[v]);
+                    base += UNR * NG;
+                    continue;
+                }
+                // general round: one observation per group, may cross row boundaries
                 const int64_t l = base + g;
-                const bool valid = l < cb;
-                const int64_t last_l = min(base + NG, cb) - 1;
+                const bool valid = l < t1;
+                const int o = (int)(l - t0);
+                const int64_t last_l = min(base + NG, t1) - 1;
                 double z[VPL];
                 double w = 0.0;
                 if (valid) {
-                    ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)__ldg(a.idx + l) * RP + jb);
+                    ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
 #pragma unroll
                     for (int m = 1; m < DO; ++m) {
                         double f[VPL];
-                        ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)__ldg(a.idx + (int64_t)m * a.q + l) * RP + jb);
+                        ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)ti[m * TILE + o] * RP + jb);
 #pragma unroll
                         for (int v = 0; v < VPL; ++v) z[v] *= f[v];
                     }
-                    if (!dot) w = __ldg(a.weights + l);
+                    if (!dot) w = tw[o];
                 }
                 auto contribute = [&]() {
                     double s;
@@ -185,7 +377,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
 #pragma unroll
                     for (int v = 0; v < VPL; ++v) acc[v] = fma(s, z[v], acc[v]);
                 };
-                if (last_l < cur_end) {  // whole round inside the current row (common case)
+                if (last_l < cur_end) {  // whole round inside the current row
                     if (valid) contribute();
                 } else {
                     bool done = !valid;
@@ -196,57 +388,54 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                         }
                         if (last_l < cur_end) break;
                         flush(cur);
-                        // next row holding observation position cur_end (skip empty rows)
-                        const int64_t pos = cur_end;
+                        const int64_t pos = cur_end;  // next row holding position cur_end
                         do {
                             ++cur;
                             cur_end = a.row_ptr[cur + 1];
                         } while (cur_end <= pos);
-                        if (dot) ldv<VPL>(xh, a.xhat_rm + cur * RP + jb);
+                        load_xh();
                     }
                 }
+                base += NG;
             }
-            flush(cur);
+            __syncthreads();  // all groups are done with buffer t & 1
+            if (t + 2 < ntiles) {
+                issue_tile(t + 2);
+                cp_commit();
+            }
         }
-        if (a.phases & (PH_C1 | PH_C2)) grid_barrier(a.barrier);
+        stamp(a, 3);
+        flush(cur);
     }
-
-    // ---- phase C1: rows split across CTAs = ordered slot sums ----------------------------
-    if (a.phases & PH_C1) {
-        for (int64_t e = (int64_t)c * FT + threadIdx.x; e < a.n * RP; e += (int64_t)C * FT) {
-            const int64_t i = e / RP, j = e % RP;
-            const int64_t rb = a.row_ptr[i], re = a.row_ptr[i + 1];
-            if (rb == re) {
-                a.yhat_rm[e] = 0.0;
-                continue;
-            }
-            const int64_t u0 = rb / a.chunk, u1 = (re - 1) / a.chunk;
-            const bool first_of_u0 = rb == u0 * a.chunk;
-            if (u0 == u1) {
-                const bool last_of_u0 = re == min(a.q, (u0 + 1) * a.chunk);
-                if (first_of_u0) a.yhat_rm[e] = a.slot_a[u0 * RP + j];
-                else if (last_of_u0) a.yhat_rm[e] = a.slot_b[u0 * RP + j];
-                continue;  // else interior: written in phase B
-            }
-            double s = first_of_u0 ? a.slot_a[u0 * RP + j] : a.slot_b[u0 * RP + j];
-            for (int64_t u = u0 + 1; u <= u1; ++u) s += a.slot_a[u * RP + j];
-            a.yhat_rm[e] = s;
-        }
-        if (a.phases & PH_C2) grid_barrier(a.barrier);
-    }
+    stamp(a, 4);
 
     // ---- phase C2: y = (K Yhat + lambda Xhat) + rho x  (small n) ------------------------------
     if (a.phases & PH_C2) {
-        const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;
+        if (a.phases & PH_B) grid_barrier(a.barrier, a.bar_groups);
+        stamp(a, 5);
+        cp_wait<0>();
+        __syncthreads();
         for (int64_t i = i0; i < i1; ++i) {
-            rows_times<RP>(a, i, a.yhat_rm, RP, 1, red, rowbuf);
+            const double* kc = pf ? kcs + (MAXLOC + i - i0) * a.n : a.kmat + i * a.n;
+            row_dot<RP>(a, kc, a.yhat_c2, RP, 1, red, rowbuf);
+            if (local_x && a.row_ptr[i + 1] == a.row_ptr[i]) {
+                // no observation on row i here, so no CTA produced Xhat(i,:): compute it
+                row_dot<RP>(a, kc, pf ? xs : a.x, 1, a.n, red, rowbuf + RP);
+            } else {
+                if (threadIdx.x < RP) rowbuf[RP + threadIdx.x] = __ldcg(a.xhat_rm + i * RP + threadIdx.x);
+                __syncthreads();
+            }
             if (threadIdx.x < a.r) {
                 const int64_t e = i + a.n * threadIdx.x;
-                double out = rowbuf[threadIdx.x] + a.lambda * a.xhat_rm[i * RP + threadIdx.x];
+                const double out = rowbuf[threadIdx.x] + a.lambda * rowbuf[RP + threadIdx.x];
                 a.y[e] = out + a.rho * a.x[e];
             }
+            __syncthreads();
         }
+    } else {
+        cp_wait<0>();
     }
+    stamp(a, 7);
 }
 
 template <int RP, int DO, bool SMEMF>
@@ -254,7 +443,7 @@ void launch_fused_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     auto kern = fused_matvec_kernel<RP, DO, SMEMF>;
     static bool attr = false;
     if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
     }
     void* args[] = {const_cast<FusedArgs*>(&a)};
@@ -273,26 +462,36 @@ void launch_fused_do(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) 
     }
 }
 
-template <int RP>
-void launch_fused_rp(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s) {
-    if (smemf) launch_fused_do<RP, true>(a, grid, smem, s);
-    else launch_fused_do<RP, false>(a, grid, smem, s);
-}
-
 template <int RP, int DO, bool SMEMF>
 int occupancy_t(size_t smem) {
     int blocks = 0;
     CPHIFI_CUDA(cudaFuncSetAttribute(fused_matvec_kernel<RP, DO, SMEMF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
+                                     220 * 1024));
     CPHIFI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_matvec_kernel<RP, DO, SMEMF>, FT, smem));
     return blocks;
+}
+
+template <int RP, bool SMEMF>
+int occupancy_do(int dother, size_t smem) {
+    switch (dother) {
+        case 1: return occupancy_t<RP, 1, SMEMF>(smem);
+        case 2: return occupancy_t<RP, 2, SMEMF>(smem);
+        case 3: return occupancy_t<RP, 3, SMEMF>(smem);
+        case 4: return occupancy_t<RP, 4, SMEMF>(smem);
+        default: return occupancy_t<RP, 5, SMEMF>(smem);
+    }
+}
+
+template <int RP>
+int occupancy_rp(int dother, bool smemf, size_t smem) {
+    return smemf ? occupancy_do<RP, true>(dother, smem) : occupancy_do<RP, false>(dother, smem);
 }
 
 __global__ void cta_rows_kernel(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     const int64_t ca = min(q, (int64_t)c * chunk), cb = min(q, ca + chunk);
-    auto row_of = [&](int64_t pos) {
+    auto row_of = [&](int64_t pos) {  // largest i with row_ptr[i] <= pos
         int64_t lo = 0, hi = n;
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) >> 1;
@@ -306,32 +505,29 @@ __global__ void cta_rows_kernel(const int64_t* row_ptr, int64_t n, int64_t q, in
 
 }  // namespace
 
-size_t fused_smem_bytes(int64_t rp, int64_t fac_total, bool smemf) {
-    const int64_t g = rp < 32 ? rp : 32;
-    const int64_t ng = FT / g;
-    const int64_t red = std::max<int64_t>(ng * rp, FT);
-    return sizeof(double) * (red + 2 * rp + (smemf ? fac_total : 0));
+size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems) {
+    const int64_t vpl = 4;  // must match fused_matvec_kernel
+    return sizeof(double) * (FT * vpl + FT + 2 * rp + MAXLOC * rp + 2 * TILE) + sizeof(int32_t) * 2 * dother * TILE +
+           sizeof(double) * ((smemf ? fac_total : 0) + prefetch_elems);
 }
+
+int fused_maxloc() { return MAXLOC; }
 
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms) {
     int occ = 0;
-#define OCC(RPV)                                                                    \
-    case RPV:                                                                       \
-        switch (dother) {                                                           \
-            case 1: occ = smemf ? occupancy_t<RPV, 1, true>(smem) : occupancy_t<RPV, 1, false>(smem); break; \
-            case 2: occ = smemf ? occupancy_t<RPV, 2, true>(smem) : occupancy_t<RPV, 2, false>(smem); break; \
-            case 3: occ = smemf ? occupancy_t<RPV, 3, true>(smem) : occupancy_t<RPV, 3, false>(smem); break; \
-            case 4: occ = smemf ? occupancy_t<RPV, 4, true>(smem) : occupancy_t<RPV, 4, false>(smem); break; \
-            default: occ = smemf ? occupancy_t<RPV, 5, true>(smem) : occupancy_t<RPV, 5, false>(smem); break; \
-        }                                                                           \
-        break;
     switch (rp) {
-        OCC(4) OCC(8) OCC(16) OCC(32) OCC(64) OCC(128)
+        case 4: occ = occupancy_rp<4>(dother, smemf, smem); break;
+        case 8: occ = occupancy_rp<8>(dother, smemf, smem); break;
+        case 16: occ = occupancy_rp<16>(dother, smemf, smem); break;
+        case 32: occ = occupancy_rp<32>(dother, smemf, smem); break;
+        case 64: occ = occupancy_rp<64>(dother, smemf, smem); break;
+        case 128: occ = occupancy_rp<128>(dother, smemf, smem); break;
         default: throw_invalid("unaligned: rank above 128 is not supported");
     }
-#undef OCC
     if (occ < 1) throw_runtime("fused matvec: kernel does not fit on an SM");
-    return num_sms * std::min(occ, 4);
+    int cap = 2;  // CTAs per SM (tunable for experiments: CPHIFI_FUSED_OCC)
+    if (const char* e = std::getenv("CPHIFI_FUSED_OCC")) cap = std::max(1, std::atoi(e));
+    return num_sms * std::min(occ, cap);
 }
 
 void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out,
@@ -341,15 +537,16 @@ void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk,
 }
 
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s) {
+#define RPCASE(RPV)                                                        \
+    case RPV:                                                              \
+        if (smemf) launch_fused_do<RPV, true>(a, grid, smem, s);           \
+        else launch_fused_do<RPV, false>(a, grid, smem, s);                \
+        break;
     switch (a.rp) {
-        case 4: launch_fused_rp<4>(a, grid, smem, smemf, s); break;
-        case 8: launch_fused_rp<8>(a, grid, smem, smemf, s); break;
-        case 16: launch_fused_rp<16>(a, grid, smem, smemf, s); break;
-        case 32: launch_fused_rp<32>(a, grid, smem, smemf, s); break;
-        case 64: launch_fused_rp<64>(a, grid, smem, smemf, s); break;
-        case 128: launch_fused_rp<128>(a, grid, smem, smemf, s); break;
+        RPCASE(4) RPCASE(8) RPCASE(16) RPCASE(32) RPCASE(64) RPCASE(128)
         default: throw_invalid("unaligned: rank above 128 is not supported");
     }
+#undef RPCASE
 }
 
 }  // namespace cphifi

@@ -60,7 +60,11 @@ void pack_rows(const double* src_cm, int64_t rows, int64_t ld, int64_t r, int64_
 void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double* dst_cm, cudaStream_t s);
 
 // ---- the unaligned operator as one persistent cooperative kernel (k_fused.cu) -----------
-enum : unsigned { PH_A = 1u, PH_B = 2u, PH_C1 = 4u, PH_C2 = 8u };
+// PH_A: Xhat rows distributed + barrier; PH_AL: each CTA computes only the Xhat rows its own
+// observations touch (no barrier); PH_B: scatter-gather (Yhat complete in global memory at the
+// end of the phase: split rows are finished by their last CTA); PH_C2: y rows (after a grid
+// barrier when PH_B ran in the same launch).
+enum : unsigned { PH_A = 1u, PH_B = 2u, PH_C2 = 8u, PH_AL = 16u };
 struct FusedArgs {
     int64_t n = 0, r = 0, rp = 0, q = 0;
     int dother = 0;
@@ -81,9 +85,17 @@ struct FusedArgs {
     const int64_t* cta_rows = nullptr;  // 2 x C: first / last row of each CTA's range
     int64_t chunk = 1;                  // observations per CTA
     double lambda = 0.0, rho = 0.0;
-    unsigned* barrier = nullptr;        // 2 x uint, zero-initialised once
+    const double* yhat_c2 = nullptr;    // complete Yhat read by PH_C2 (yhat_rm or the NCCL sum)
+    unsigned* rowcnt = nullptr;         // n per-row arrival counters, zero-initialised once
+    int prefetch = 0;                   // stage X and the needed K columns in smem (small n)
+    unsigned* barrier = nullptr;        // barrier_words(grid) uints, zero-initialised once
+    int bar_groups = 16;                // CTAs per first-level barrier counter
+    unsigned long long* trace = nullptr;  // optional: TRACE_SLOTS %globaltimer stamps per CTA
 };
-size_t fused_smem_bytes(int64_t rp, int64_t fac_total, bool smemf);
+constexpr int TRACE_SLOTS = 8;  // entry, A done, barrier 1, B done, barrier 2, C1 done, barrier 3, end
+inline size_t barrier_words(int grid, int group) { return 64 + 32 * (size_t)((grid + group - 1) / group); }
+size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems);
+int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
 void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out,
                     cudaStream_t s);
