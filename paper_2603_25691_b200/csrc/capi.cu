@@ -130,6 +130,79 @@ cphifi_mode new_mode(cphifi_ctx ctx, int64_t n, double lambda) {
     return m;
 }
 
+// ---- row-aligned CTA partition of the sorted observations (the fused kernel's schedule) --
+// Greedy packing of WHOLE rows into CTAs of at most L observations; a row longer than L is cut
+// into ceil(len / L) near-equal pieces (the only split rows).  L starts at ceil(q / cmax) and
+// grows until the plan fits the co-resident CTA budget cmax.  The launch is padded with empty
+// CTAs up to `cmin` so that the dense row phases still spread over the whole chip.
+struct PartitionPlan {
+    int ctas = 0;
+    int64_t max_span = 0;                 // max rows touched by one CTA
+    std::vector<int64_t> beg;             // ctas + 1
+    std::vector<int64_t> rows;            // 2 * ctas: first / last row per CTA
+    std::vector<int32_t> row_first_cta;   // n
+    std::vector<int32_t> row_ncta;        // n
+};
+
+void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, PartitionPlan& pl) {
+    const int64_t n = (int64_t)rp.size() - 1, q = rp[n];
+    std::vector<int64_t> starts;
+    auto build = [&](int64_t L) {
+        starts.assign(1, 0);
+        int64_t load = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t len = rp[i + 1] - rp[i];
+            if (len == 0) continue;
+            if (len > L) {
+                if (load > 0) starts.push_back(rp[i]);
+                const int64_t pieces = (len + L - 1) / L;
+                for (int64_t pc = 1; pc < pieces; ++pc) starts.push_back(rp[i] + len * pc / pieces);
+                starts.push_back(rp[i + 1]);
+                load = 0;
+            } else {
+                if (load > 0 && load + len > L) {
+                    starts.push_back(rp[i]);
+                    load = 0;
+                }
+                load += len;
+            }
+        }
+        starts.push_back(q);
+        starts.erase(std::unique(starts.begin(), starts.end()), starts.end());  // drop empty CTAs
+        if (starts.size() < 2) starts.assign({0, q});
+    };
+    int64_t L = std::max<int64_t>(1, (q + cmax - 1) / std::max(cmax, 1));
+    for (;;) {
+        build(L);
+        if ((int64_t)starts.size() - 1 <= cmax) break;
+        L = L + L / 8 + 1;
+    }
+    while ((int64_t)starts.size() - 1 < cmin) starts.push_back(q);  // empty padding CTAs
+    pl.ctas = (int)starts.size() - 1;
+    pl.beg = starts;
+    pl.rows.assign(2 * (size_t)pl.ctas, 0);
+    pl.row_first_cta.assign(n, -1);
+    pl.row_ncta.assign(n, 0);
+    pl.max_span = 0;
+    auto row_of = [&](int64_t pos) {  // largest i with rp[i] <= pos
+        return (int64_t)(std::upper_bound(rp.begin(), rp.end(), pos) - rp.begin()) - 1;
+    };
+    for (int c = 0; c < pl.ctas; ++c) {
+        const int64_t a = starts[c], b = starts[c + 1];
+        if (a >= b) continue;
+        const int64_t r0 = row_of(a), r1 = row_of(b - 1);
+        pl.rows[2 * c] = r0;
+        pl.rows[2 * c + 1] = r1;
+        pl.max_span = std::max(pl.max_span, r1 - r0 + 1);
+        for (int64_t i = r0; i <= r1; ++i) {
+            if (rp[i + 1] == rp[i]) continue;
+            if (pl.row_first_cta[i] < 0) pl.row_first_cta[i] = c;
+            ++pl.row_ncta[i];
+        }
+    }
+    for (auto& v : pl.row_first_cta) v = std::max(v, 0);
+}
+
 // ---- unaligned pieces ------------------------------------------------------------------
 bool is_multi(cphifi_unaligned p) { return p->obs->ctx->comm && p->obs->ctx->nranks > 1; }
 
@@ -164,7 +237,9 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     a.slot_a = p->slot_a.get();
     a.slot_b = p->slot_b.get();
     a.cta_rows = p->cta_rows.get();
-    a.chunk = p->chunk;
+    a.cta_beg = p->cta_beg.get();
+    a.row_first_cta = p->row_first_cta.get();
+    a.row_ncta = p->row_ncta.get();
     a.lambda = p->mode->lambda;
     a.rho = p->rho;
     a.barrier = p->barrier.get();
@@ -708,7 +783,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         gram_kr(d, obs->shape.data(), r, fptr.data(), k, p->v.get(), s);
         // scratch
         const int64_t n = p->n;
-        // fused-kernel launch shape: all CTAs co-resident, equal observation count per CTA
+        // fused-kernel launch shape: all CTAs co-resident (cooperative launch)
         p->small_n = n <= 512 && n * r <= 8192;
         p->prefetch = p->small_n;
         p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;
@@ -716,27 +791,31 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         const int64_t crows = (n + ctx->num_sms - 1) / ctx->num_sms;  // >= rows per CTA in PH_C2
         const int64_t pref = p->prefetch ? n * r + (fused_maxloc() + crows) * n : 0;
         p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
-        p->grid = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        const int cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        PartitionPlan plan;
+        {
+            std::vector<int64_t> rp_host(n + 1);
+            d2h_sync(rp_host.data(), obs->row_ptr.get(), sizeof(int64_t) * (n + 1), s);
+            plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
+        }
+        p->grid = plan.ctas;
+        p->local_x = p->small_n && plan.max_span <= fused_maxloc();
+        p->cta_beg.alloc(plan.beg.size());
+        h2d(p->cta_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
+        p->cta_rows.alloc(plan.rows.size());
+        h2d(p->cta_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
+        p->row_first_cta.alloc(n);
+        h2d(p->row_first_cta.get(), plan.row_first_cta.data(), sizeof(int32_t) * n, s);
+        p->row_ncta.alloc(n);
+        h2d(p->row_ncta.get(), plan.row_ncta.data(), sizeof(int32_t) * n, s);
         p->rowcnt.alloc(n);
         CPHIFI_CUDA(cudaMemsetAsync(p->rowcnt.get(), 0, n * sizeof(unsigned), s));
-        p->chunk = std::max<int64_t>(1, (obs->q_local + p->grid - 1) / p->grid);
         p->slot_a.alloc((size_t)p->grid * p->rp);
         p->slot_b.alloc((size_t)p->grid * p->rp);
-        p->cta_rows.alloc(2 * (size_t)p->grid);
         const size_t bw = barrier_words(p->grid, 16);
         p->barrier.alloc(bw);
         CPHIFI_CUDA(cudaMemsetAsync(p->barrier.get(), 0, bw * sizeof(unsigned), s));
-        fused_cta_rows(obs->row_ptr.get(), n, obs->q_local, p->chunk, p->grid, p->cta_rows.get(), s);
-        {   // CTA-local Xhat rows (no grid barrier before the scatter-gather) when every CTA's
-            // observation range touches at most MAXLOC rows
-            std::vector<int64_t> cr(2 * (size_t)p->grid);
-            d2h_sync(cr.data(), p->cta_rows.get(), sizeof(int64_t) * cr.size(), s);
-            int64_t span = 0;
-            for (int c = 0; c < p->grid; ++c)
-                if (std::min<int64_t>(obs->q_local, (int64_t)c * p->chunk) < obs->q_local)
-                    span = std::max<int64_t>(span, cr[2 * c + 1] - cr[2 * c] + 1);
-            p->local_x = p->small_n && span <= fused_maxloc();
-        }
+        CPHIFI_CUDA(cudaStreamSynchronize(s));  // plan vectors are freed on scope exit
         p->xhat_rm.alloc(n * p->rp);
         p->yhat_rm.alloc(n * p->rp);
         // rows without observations in this shard are never written: keep them zero

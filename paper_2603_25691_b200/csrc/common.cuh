@@ -136,7 +136,9 @@ struct cphifi_unaligned_s {
     cphifi::DevBuf<double> uv, sv, dmat;
     // fused operator kernel launch shape (k_fused.cu)
     int grid = 0;                 // CTAs (all co-resident)
-    int64_t chunk = 1;            // observations per CTA
+    cphifi::DevBuf<int64_t> cta_beg;        // grid + 1 partition boundaries
+    cphifi::DevBuf<int32_t> row_first_cta;  // n
+    cphifi::DevBuf<int32_t> row_ncta;       // n
     size_t smem = 0;              // dynamic shared memory bytes
     bool smem_factors = false;    // factors staged in shared memory
     bool small_n = false;         // phases A and C2 inside the fused kernel

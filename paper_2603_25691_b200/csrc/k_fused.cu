@@ -9,7 +9,9 @@
 //   AL  Xhat rows     each CTA computes the (<= MAXLOC) rows its own observations touch, from
 //                     X and K columns prefetched into shared memory at entry
 //   (A  fallback      rows distributed over CTAs + a grid barrier)
-//   B   scatter-gather CTA c streams observations [c*chunk, (c+1)*chunk) of the i_k-sorted set
+//   B   scatter-gather CTA c streams observations [beg[c], beg[c+1]) of the i_k-sorted set (a
+//                     host-planned ROW-ALIGNED partition: whole rows packed per CTA, only rows
+//                     longer than the target load split across CTAs)
 //                     in ROUNDS of NG consecutive observations, one per lane group (G lanes x
 //                     VPL doubles = the padded rank), four rounds in flight per group.  Each
 //                     group keeps its row accumulator in registers; at a row boundary the CTA
@@ -32,9 +34,9 @@ namespace cphifi {
 namespace {
 
 constexpr int FT = 512;    // threads per CTA
-constexpr int TILE = 512;  // observations per staged tile
+constexpr int TILE = 1024; // observations per staged tile
 constexpr int MAXLOC = 4;  // PH_AL: max rows one CTA computes Xhat for
-constexpr int UNR = 4;     // rounds in flight per group in the fast path
+constexpr int UNR = 2;     // rounds in flight per group in the fast path
 
 __device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
     unsigned old;
@@ -148,10 +150,10 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     constexpr int VPL = 4;                // doubles per lane (two LDS.128 per factor row)
     constexpr int G = RP / VPL;           // lanes per observation: few shuffle steps per dot
     constexpr int NG = FT / G;            // observations per round
-    constexpr int P = (NG < 8 ? NG : 8) < FT / RP ? (NG < 8 ? NG : 8) : FT / RP;  // flush tree fan-in
+    constexpr int NW = FT / 32;
     extern __shared__ __align__(16) double smem[];
-    double* red = smem;                   // FT * VPL doubles (= NG * RP)
-    double* red2 = red + FT * VPL;        // FT doubles
+    double* red = smem;                   // RP x (NG + 1) doubles (transposed group partials)
+    double* red2 = red + FT * VPL + RP;   // FT doubles
     double* rowbuf = red2 + FT;           // 2 * RP doubles
     double* xloc = rowbuf + 2 * RP;       // MAXLOC * RP: this CTA's Xhat rows (PH_AL)
     double* sw = xloc + MAXLOC * RP;      // 2 x TILE weights (RHS mode)
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - lane % G));
     const bool dot = a.weights == nullptr;
-    const int64_t ca = min(a.q, (int64_t)c * a.chunk), cb = min(a.q, ca + a.chunk);
+    const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];  // row-aligned partition (host plan)
     const int ntiles = (a.phases & PH_B) && ca < cb ? (int)((cb - ca + TILE - 1) / TILE) : 0;
     const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
 
@@ -251,30 +253,29 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
         };
         load_xh();
 
+        // Row reduction over the NG groups in a FIXED order: group partials are stored
+        // transposed (red[j][g]); warp w reduces columns j = w, w + NW, ...: each lane sums the
+        // groups g = lane, lane + 32, ... in order, then a 5-step xor-shuffle tree.
         auto flush = [&](int64_t row) {
             __syncthreads();
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) red[g * RP + jb + v] = acc[v];
+            for (int v = 0; v < VPL; ++v) red[(jb + v) * (NG + 1) + g] = acc[v];
             __syncthreads();
-            if (threadIdx.x < P * RP) {  // fixed two-level tree over the NG groups
-                const int j = threadIdx.x % RP, part = threadIdx.x / RP;
+            for (int j = threadIdx.x >> 5; j < RP; j += NW) {
                 double s = 0.0;
-                for (int q = part * (NG / P); q < (part + 1) * (NG / P); ++q) s += red[q * RP + j];
-                red2[part * RP + j] = s;
+                for (int q = lane; q < NG; q += 32) s += red[j * (NG + 1) + q];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (lane == 0) red2[j] = s;
             }
             __syncthreads();
-            const int64_t rb = a.row_ptr[row], re = a.row_ptr[row + 1];
-            // positions and chunk are < 2^31 (q is capped at INT32_MAX): 32-bit divisions
-            const int64_t u0 = (uint32_t)rb / (uint32_t)a.chunk, u1 = (uint32_t)(re - 1) / (uint32_t)a.chunk;
-            const bool split = u1 > u0;  // the row continues in other CTAs
+            const int ncta = a.row_ncta[row];
+            const bool split = ncta > 1;  // the row continues in other CTAs
             if (threadIdx.x < RP) {
-                double s = 0.0;
-#pragma unroll
-                for (int part = 0; part < P; ++part) s += red2[part * RP + threadIdx.x];
                 double* dst = !split ? a.yhat_rm + row * RP
                             : row == first_row ? a.slot_a + (int64_t)c * RP
                                                : a.slot_b + (int64_t)c * RP;
-                dst[threadIdx.x] = s;
+                dst[threadIdx.x] = red2[threadIdx.x];
             }
 #pragma unroll
             for (int v = 0; v < VPL; ++v) acc[v] = 0.0;
@@ -282,15 +283,16 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     __threadfence();
-                    const unsigned need = (unsigned)(u1 - u0 + 1);
-                    s_last = atom_add_acqrel(a.rowcnt + row, 1u) == need - 1;
+                    s_last = atom_add_acqrel(a.rowcnt + row, 1u) == (unsigned)ncta - 1;
                     if (s_last) a.rowcnt[row] = 0;  // ready for the next launch
                 }
                 __syncthreads();
                 if (s_last && threadIdx.x < RP) {
                     const int j = threadIdx.x;
-                    double s = rb == u0 * a.chunk ? __ldcg(a.slot_a + u0 * RP + j) : __ldcg(a.slot_b + u0 * RP + j);
-                    for (int64_t u = u0 + 1; u <= u1; ++u) s += __ldcg(a.slot_a + u * RP + j);
+                    const int u0 = a.row_first_cta[row];
+                    double s = a.row_ptr[row] == a.cta_beg[u0] ? __ldcg(a.slot_a + (int64_t)u0 * RP + j)
+                                                               : __ldcg(a.slot_b + (int64_t)u0 * RP + j);
+                    for (int u = u0 + 1; u < u0 + ncta; ++u) s += __ldcg(a.slot_a + (int64_t)u * RP + j);
                     a.yhat_rm[row * RP + j] = s;
                 }
             }
@@ -487,27 +489,11 @@ int occupancy_rp(int dother, bool smemf, size_t smem) {
     return smemf ? occupancy_do<RP, true>(dother, smem) : occupancy_do<RP, false>(dother, smem);
 }
 
-__global__ void cta_rows_kernel(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
-    const int64_t ca = min(q, (int64_t)c * chunk), cb = min(q, ca + chunk);
-    auto row_of = [&](int64_t pos) {  // largest i with row_ptr[i] <= pos
-        int64_t lo = 0, hi = n;
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (row_ptr[mid] <= pos) lo = mid; else hi = mid;
-        }
-        return lo;
-    };
-    out[2 * c] = ca < cb ? row_of(ca) : 0;
-    out[2 * c + 1] = ca < cb ? row_of(cb - 1) : 0;
-}
-
 }  // namespace
 
 size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems) {
     const int64_t vpl = 4;  // must match fused_matvec_kernel
-    return sizeof(double) * (FT * vpl + FT + 2 * rp + MAXLOC * rp + 2 * TILE) + sizeof(int32_t) * 2 * dother * TILE +
+    return sizeof(double) * (FT * vpl + rp + FT + 2 * rp + MAXLOC * rp + 2 * TILE) + sizeof(int32_t) * 2 * dother * TILE +
            sizeof(double) * ((smemf ? fac_total : 0) + prefetch_elems);
 }
 
@@ -528,12 +514,6 @@ int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms) {
     int cap = 2;  // CTAs per SM (tunable for experiments: CPHIFI_FUSED_OCC)
     if (const char* e = std::getenv("CPHIFI_FUSED_OCC")) cap = std::max(1, std::atoi(e));
     return num_sms * std::min(occ, cap);
-}
-
-void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out,
-                    cudaStream_t s) {
-    cta_rows_kernel<<<(C + 127) / 128, 128, 0, s>>>(row_ptr, n, q, chunk, C, out);
-    CPHIFI_CHECK_LAUNCH();
 }
 
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s) {

@@ -82,8 +82,11 @@ struct FusedArgs {
     double* yhat_rm = nullptr;          // n x rp
     double* slot_a = nullptr;           // C x rp
     double* slot_b = nullptr;
+    // row-aligned CTA partition (host plan, see plan_partition in capi.cu)
+    const int64_t* cta_beg = nullptr;   // C + 1: CTA c streams observations [cta_beg[c], cta_beg[c+1])
     const int64_t* cta_rows = nullptr;  // 2 x C: first / last row of each CTA's range
-    int64_t chunk = 1;                  // observations per CTA
+    const int32_t* row_first_cta = nullptr;  // n: first CTA touching the row
+    const int32_t* row_ncta = nullptr;       // n: CTAs touching the row (> 1 = split row)
     double lambda = 0.0, rho = 0.0;
     const double* yhat_c2 = nullptr;    // complete Yhat read by PH_C2 (yhat_rm or the NCCL sum)
     unsigned* rowcnt = nullptr;         // n per-row arrival counters, zero-initialised once
@@ -97,8 +100,6 @@ inline size_t barrier_words(int grid, int group) { return 64 + 32 * (size_t)((gr
 size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems);
 int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
-void fused_cta_rows(const int64_t* row_ptr, int64_t n, int64_t q, int64_t chunk, int C, int64_t* out,
-                    cudaStream_t s);
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s);
 
 // ---- PCG vector kernels (deterministic reductions) --------------------------------------
