@@ -352,6 +352,48 @@ class ObservationSet:
         return self._plans[key]
 
 
+class DeviceObservations:
+    """Observations already resident on the GPU (d x q int32 indices, q fp64 values, e.g. torch
+    tensors or raw device pointers): multiset semantics, no host copy.  Plans are built per
+    (k, shard) exactly like ObservationSet.plan."""
+
+    def __init__(self, shape, idx_ptr: int, vals_ptr: int, q: int, keepalive=()):
+        self._shape = [int(s) for s in shape]
+        self._idx_ptr = int(idx_ptr)
+        self._vals_ptr = int(vals_ptr)
+        self._q = int(q)
+        self._keep = tuple(keepalive)
+        self._plans = {}
+        self.multiset = True
+
+    def shape(self):
+        return list(self._shape)
+
+    def num_obs(self) -> int:
+        return self._q
+
+    def num_entries(self) -> int:
+        return int(np.prod(self._shape))
+
+    def density(self) -> float:
+        return float(self._q) / float(np.prod(np.asarray(self._shape, dtype=np.float64)))
+
+    def plan(self, k: int, ctx: "Context", shard: int = 0, shards: int = 1):
+        key = (k, id(ctx), shard, shards)
+        if key not in self._plans:
+            h = ctypes.c_void_p()
+            shape = np.ascontiguousarray(self._shape, dtype=np.int64)
+            call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p), self._q,
+                 ctypes.c_void_p(self._idx_ptr), ctypes.c_void_p(self._vals_ptr), k, _capi.OBS_DEVICE_INPUT,
+                 shard, shards, ctypes.byref(h))
+            self._plans[key] = _Handle(h, "cphifi_obs_destroy", deps=(ctx,))
+        return self._plans[key]
+
+    def release_inputs(self):
+        """Drop the references to the raw input buffers (plans own sorted copies)."""
+        self._keep = ()
+
+
 class _Handle:
     """Owns one C-ABI handle.  `deps` keeps the handles it points into (observation plan,
     mode, context) alive until after this one is destroyed."""

@@ -113,6 +113,9 @@ _SIGS = [
      [_H, ctypes.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, c_double_p]),
+    ("cphifi_synth_observations", ctypes.c_int,
+     [_H, ctypes.c_int, c_int64_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
+      ctypes.POINTER(c_double_p), ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
     ("cphifi_rng_create", ctypes.c_int, [ctypes.c_uint64, c_void_pp]),
     ("cphifi_rng_destroy", ctypes.c_int, [_H]),
     ("cphifi_rng_next_u64", ctypes.c_int, [_H, c_uint64_p, ctypes.c_int64]),

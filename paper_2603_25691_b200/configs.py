@@ -130,3 +130,77 @@ def small_unaligned(shape=(40, 12, 10), r=4, q=1500, seed=5) -> UnalignedConfig:
     obs = sample_uniform(DenseTensor(list(shape), t), q, seed + 1)
     return UnalignedConfig("small", list(shape), r, 1e-3, 1e-6, 1e-8, 500, pts, "gaussian", 0.1, factors, w,
                            obs.index_array(), obs.values())
+
+
+# ---- configs 3 and 4: observations generated on the device --------------------------------
+@dataclass
+class DeviceUnalignedConfig:
+    """Factors are host arrays; the q observations are drawn on the GPU by
+    cphifi_synth_observations (counter-based, seed-reproducible)."""
+    name: str
+    shape: list
+    r: int
+    lam: float
+    rho: float
+    tol: float
+    max_iter: int
+    points: np.ndarray
+    kernel: str
+    ell: float
+    factors: list
+    w_true: np.ndarray
+    q: int
+    seed: int
+    zipf_mode: int
+    zipf_s: float
+    noise_std: float = 0.1
+
+
+def config3() -> DeviceUnalignedConfig:
+    """Unaligned 4-way 2048x256x256x256, Matern-3/2 (0.05) on 2048 sorted uniform points,
+    q = 2e8 uniform draws (multiset), rank 32, lambda 1e-4, PCG tol 1e-8."""
+    n, r = 2048, 32
+    rng = _rng(3)
+    pts = np.sort(rng.uniform_real(0.0, 1.0, n))
+    w = _normal_matrix(rng, n, r)
+    others = [_normal_matrix(rng, 256, r) for _ in range(3)]
+    a1 = np.asfortranarray(kernel_matrix(pts, "matern32", 0.05) @ w)
+    return DeviceUnalignedConfig("config3", [n, 256, 256, 256], r, 1e-4, 1e-6, 1e-8, 500, pts, "matern32", 0.05,
+                                 [a1] + others, w, 200_000_000, 3, -1, 0.0)
+
+
+def config4() -> DeviceUnalignedConfig:
+    """Unaligned skewed 3-way 4096x512x512, RBF (0.02) on 4096 clustered points (8 Gaussian
+    clusters, sigma 0.03, clipped to [0,1]), q = 1e9 draws with i_1 ~ Zipf(1.1), rank 64,
+    lambda 1e-5, PCG tol 1e-8."""
+    n, r = 4096, 64
+    rng = _rng(4)
+    centres = rng.uniform_real(0.0, 1.0, 8)
+    which = rng.uniform_int(0, 7, n)
+    pts = np.sort(np.clip(centres[which] + 0.03 * rng.normal(0.0, 1.0, n), 0.0, 1.0))
+    w = _normal_matrix(rng, n, r)
+    others = [_normal_matrix(rng, 512, r) for _ in range(2)]
+    a1 = np.asfortranarray(kernel_matrix(pts, "gaussian", 0.02) @ w)
+    return DeviceUnalignedConfig("config4", [n, 512, 512], r, 1e-5, 1e-6, 1e-8, 500, pts, "gaussian", 0.02,
+                                 [a1] + others, w, 1_000_000_000, 4, 0, 1.1)
+
+
+def generate_device(cfg: DeviceUnalignedConfig, ctx, q: int | None = None):
+    """Draw the observations on cfg's GPU: returns torch tensors idx (d, q) int32, vals (q,) f64."""
+    import ctypes
+
+    import torch
+
+    from . import _capi
+    q = cfg.q if q is None else q
+    d = len(cfg.shape)
+    dev = torch.device("cuda", ctx.device)
+    idx = torch.empty((d, q), dtype=torch.int32, device=dev)
+    vals = torch.empty(q, dtype=torch.float64, device=dev)
+    shape = np.ascontiguousarray(cfg.shape, dtype=np.int64)
+    facs = [np.asfortranarray(f) for f in cfg.factors]
+    ptrs = (_capi.c_double_p * d)(*[f.ctypes.data_as(_capi.c_double_p) for f in facs])
+    _capi.call("cphifi_synth_observations", ctx.handle, d, shape.ctypes.data_as(_capi.c_int64_p), q,
+               ctypes.c_uint64(cfg.seed), cfg.zipf_mode, cfg.zipf_s, cfg.r, ptrs, cfg.noise_std, idx.data_ptr(),
+               vals.data_ptr())
+    return idx, vals

@@ -1229,6 +1229,28 @@ int cphifi_gram_khatri_rao(cphifi_ctx ctx, int d, const int64_t* shape, int64_t 
     });
 }
 
+int cphifi_synth_observations(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, uint64_t seed, int zipf_mode,
+                              double zipf_s, int64_t r, const double* const* factors, double noise_std, int32_t* idx_out,
+                              double* vals_out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(shape, "shape");
+        need(factors, "factors");
+        if (d < 1 || d > 8) throw_invalid("synth: bad order");
+        if (q < 0 || r < 1) throw_invalid("synth: bad size");
+        if (q > 0) {
+            need(idx_out, "idx_out");
+            need(vals_out, "vals_out");
+        }
+        DeviceGuard dg(ctx->device);
+        DevBuf<double> fbuf;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, d, shape, -1, r, factors, fbuf, fptr);
+        synth_observations(d, shape, q, seed, zipf_mode, zipf_s, r, fptr.data(), noise_std, idx_out, vals_out,
+                           ctx->num_sms, ctx->stream);
+    });
+}
+
 int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b, const double* v, const double* u_v,
                                    const double* sigma_v, double* w_out) {
     return guard([&] {

@@ -102,6 +102,11 @@ int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s);
 
+// ---- seeded device-side observation generator (configs 3/4; k_synth.cu) -----------------
+void synth_observations(int d, const int64_t* shape, int64_t q, uint64_t seed, int zipf_mode, double zipf_s, int64_t r,
+                        const double* const* fac_dev, double noise_std, int32_t* idx, double* vals, int num_sms,
+                        cudaStream_t s);
+
 // ---- PCG vector kernels (deterministic reductions) --------------------------------------
 struct PcgState {
     double rz, pap, alpha, rr, bnorm, rel, beta, rz_new;

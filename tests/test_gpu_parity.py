@@ -363,3 +363,33 @@ def test_sharded_plans_sum_to_full(cp):
             acc += ps.scatter_gather(xhat)
             bacc += ps.b
         assert ri.rel(acc, yf) < 1e-12 and ri.rel(bacc, full.b) < 1e-12
+
+
+# ---- configs 3 / 4 structure (device-generated multiset observations), reduced q --------------
+@pytest.mark.parametrize("which,q", [("config3", 2_000_000), ("config4", 3_000_000)])
+def test_large_config_structure_vs_oracle(cp, which, q):
+    """Full-size modes, factors and kernels of configs 3/4 with a reduced number of draws:
+    device generation -> device sort/CSR plan (multiset) -> operator, against the oracle's
+    streaming restatement on the same draws (copied back)."""
+    import torch
+    from paper_2603_25691_b200 import configs
+    cfg = getattr(configs, which)()
+    ctx = cp.default_context()
+    idx, vals = configs.generate_device(cfg, ctx, q)
+    hidx, hvals = idx.cpu().numpy(), vals.cpu().numpy()
+    n, r = cfg.shape[0], cfg.r
+    assert hidx.min() >= 0 and all(hidx[m].max() < cfg.shape[m] for m in range(len(cfg.shape)))
+    mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
+    kern = mode.kernel()
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
+    b_o = orc.sampled_mttkrp_stream(cfg.shape, 0, hidx, hvals, model.factors, n)
+    assert ri.rel(p.b, b_o) < 1e-12
+    x = np.random.default_rng(1).normal(size=n * r)
+    y = cp.unaligned_matvec(p, x)
+    y_o = orc.unaligned_matvec_stream(cfg.shape, 0, hidx, model.factors, kern, cfg.lam, cfg.rho, x)
+    assert ri.rel(y, y_o) < 1e-12
+    if cfg.zipf_mode == 0:  # Zipf head: row 0 carries ~16 % of the draws
+        frac0 = float((hidx[0] == 0).mean())
+        assert 0.14 < frac0 < 0.18
