@@ -139,6 +139,16 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r,
 int cphifi_unaligned_destroy(cphifi_unaligned p);
 int cphifi_unaligned_get_b(cphifi_unaligned p, double* b_out);  /* n x r */
 int cphifi_unaligned_get_v(cphifi_unaligned p, double* v_out);  /* r x r */
+/* Operator form used by matvec / PCG.  STREAM (default) is the reference's structure: every
+ * application gathers and scatters over all q observations (observations.hpp:174-198).  GRAM
+ * uses the exact identity Yhat(i,:) = G_i Xhat(i,:), G_i = sum_{l in row i} z_l z_l', with G
+ * built once on first use (O(q rp^2)); each application is then O(n rp^2).  AUTO picks GRAM
+ * when rp <= 64 and the rows carry on average >= 2 rp observations. */
+#define CPHIFI_OP_STREAM 0
+#define CPHIFI_OP_GRAM 1
+#define CPHIFI_OP_AUTO 2
+int cphifi_unaligned_set_operator(cphifi_unaligned p, int op);
+int cphifi_unaligned_get_operator(cphifi_unaligned p, int* op);
 /* unaligned_matvec (unaligned.hpp:101-115): y = vec(K*Yhat + lambda*K*X) + rho*x. */
 int cphifi_unaligned_matvec(cphifi_unaligned p, const double* x, double* y);
 int cphifi_unaligned_matvec_device(cphifi_unaligned p, const double* x, double* y);

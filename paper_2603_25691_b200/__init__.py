@@ -509,6 +509,19 @@ class UnalignedSubproblem:
         call("cphifi_unaligned_get_v", self.handle, _dp(out))
         return out
 
+    _OPS = {"stream": 0, "gram": 1, "auto": 2}
+
+    def set_operator(self, op: str) -> str:
+        """'stream' (reference structure, default), 'gram' (row-Gram form, G built once) or
+        'auto'; returns the resolved form."""
+        call("cphifi_unaligned_set_operator", self.handle, self._OPS[op])
+        return self.operator()
+
+    def operator(self) -> str:
+        v = ctypes.c_int()
+        call("cphifi_unaligned_get_operator", self.handle, ctypes.byref(v))
+        return "gram" if v.value == 1 else "stream"
+
     def set_v_eig(self, u, d) -> None:
         u = _f64(u)
         d = np.ascontiguousarray(d, dtype=np.float64)

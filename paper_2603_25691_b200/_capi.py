@@ -91,6 +91,8 @@ _SIGS = [
     ("cphifi_unaligned_destroy", ctypes.c_int, [_H]),
     ("cphifi_unaligned_get_b", ctypes.c_int, [_H, c_double_p]),
     ("cphifi_unaligned_get_v", ctypes.c_int, [_H, c_double_p]),
+    ("cphifi_unaligned_set_operator", ctypes.c_int, [_H, ctypes.c_int]),
+    ("cphifi_unaligned_get_operator", ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_unaligned_matvec", ctypes.c_int, [_H, c_double_p, c_double_p]),
     ("cphifi_unaligned_matvec_device", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p]),
     ("cphifi_unaligned_set_v_eig", ctypes.c_int, [_H, c_double_p, c_double_p]),

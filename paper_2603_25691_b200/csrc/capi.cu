@@ -253,6 +253,37 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
     fused_matvec(a, p->grid, p->smem, p->smem_factors, p->obs->ctx->stream);
 }
 
+// Row-Gram operator: build G_i = sum_l z_l z_l' once (k_gram.cu), on first use.
+void ensure_gram(cphifi_unaligned p) {
+    if (p->gram.n) return;
+    if (p->rp > 64) throw_invalid("gram operator: padded rank above 64 is not supported");
+    cphifi_obs o = p->obs;
+    cphifi_ctx ctx = o->ctx;
+    const size_t rp2 = (size_t)p->rp * p->rp;
+    p->gram.alloc((size_t)p->n * rp2);
+    CPHIFI_CUDA(cudaMemsetAsync(p->gram.get(), 0, sizeof(double) * p->n * rp2, ctx->stream));
+    p->gslot_a.alloc((size_t)p->grid * rp2);
+    p->gslot_b.alloc((size_t)p->grid * rp2);
+    GramArgs g;
+    g.n = p->n;
+    g.rp = p->rp;
+    g.q = o->q_local;
+    g.dother = o->d - 1;
+    g.row_ptr = o->row_ptr.get();
+    g.idx = o->idx_o.get();
+    g.fac = p->fac.get();
+    for (int m = 0; m < o->d - 1; ++m) g.fac_off[m] = p->fac_off[m];
+    g.cta_beg = p->cta_beg.get();
+    g.cta_rows = p->cta_rows.get();
+    g.row_first_cta = p->row_first_cta.get();
+    g.row_ncta = p->row_ncta.get();
+    g.rowcnt = p->rowcnt.get();
+    g.slot_a = p->gslot_a.get();
+    g.slot_b = p->gslot_b.get();
+    g.g = p->gram.get();
+    if (o->q_local > 0) gram_build(g, p->grid, ctx->stream);
+}
+
 // Phase sets of the operator launches (see kernels.cuh).  part 0 = the (first) launch,
 // part 1 = the launch after the NCCL all-reduce (multi-GPU, small n).
 unsigned matvec_phases(cphifi_unaligned p, bool multi, int part) {
@@ -294,10 +325,13 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
 void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     cphifi_ctx ctx = p->obs->ctx;
     const bool multi = ctx->comm && ctx->nranks > 1;
+    if (p->op == 1) ensure_gram(p);
+    const double* gr = p->op == 1 ? p->gram.get() : nullptr;
     if (p->small_n) {
         FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
         a.x = x;
         a.y = y;
+        a.gram = gr;
         launch_fused(p, a);
         if (multi) {
             allreduce_yhat(p);
@@ -307,7 +341,8 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
         return;
     }
     xhat_gemm(p, x);
-    launch_fused(p, fused_args(p, PH_B));
+    if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), ctx->stream);
+    else launch_fused(p, fused_args(p, PH_B));
     allreduce_yhat(p);
     y_gemm(p, x, y);
 }
@@ -865,6 +900,30 @@ int cphifi_unaligned_get_v(cphifi_unaligned p, double* v_out) {
     });
 }
 
+int cphifi_unaligned_set_operator(cphifi_unaligned p, int op) {
+    return guard([&] {
+        need(p, "p");
+        if (op < CPHIFI_OP_STREAM || op > CPHIFI_OP_AUTO) throw_invalid("cphifi_unaligned_set_operator: unknown operator");
+        if (op == CPHIFI_OP_AUTO) {
+            // row-Gram pays off when the rows carry on average >= 2 rp observations (each
+            // application then costs O(n rp^2) instead of O(q d rp)) and G fits comfortably
+            const double g_bytes = 8.0 * (double)p->n * (double)p->rp * (double)p->rp;
+            op = (p->rp <= 64 && p->obs->q_local >= 2 * p->rp * p->n && g_bytes <= 8e9) ? CPHIFI_OP_GRAM
+                                                                                         : CPHIFI_OP_STREAM;
+        }
+        if (op == CPHIFI_OP_GRAM && p->rp > 64) throw_invalid("gram operator: padded rank above 64 is not supported");
+        p->op = op;
+    });
+}
+
+int cphifi_unaligned_get_operator(cphifi_unaligned p, int* op) {
+    return guard([&] {
+        need(p, "p");
+        need(op, "op");
+        *op = p->op;
+    });
+}
+
 int cphifi_unaligned_matvec_device(cphifi_unaligned p, const double* x, double* y) {
     return guard([&] {
         need(p, "p");
@@ -903,6 +962,8 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
         cudaEvent_t ev[6];
         for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
         double acc[6] = {0, 0, 0, 0, 0, 0};
+        if (p->op == 1) ensure_gram(p);
+        const double* gr = p->op == 1 ? p->gram.get() : nullptr;
         for (int it = 0; it < iters; ++it) {
             CPHIFI_CUDA(cudaEventRecord(ev[0], s));
             if (!p->small_n) xhat_gemm(p, x);
@@ -910,7 +971,9 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
             FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
             a.x = x;
             a.y = y;
-            launch_fused(p, a);
+            a.gram = gr;
+            if (!p->small_n && gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), s);
+            else launch_fused(p, a);
             CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
             allreduce_yhat(p);
@@ -950,11 +1013,13 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
         DevBuf<unsigned long long> tr(cnt);
         CPHIFI_CUDA(cudaMemsetAsync(tr.get(), 0, cnt * sizeof(unsigned long long), ctx->stream));
         const bool multi = ctx->comm && ctx->nranks > 1;
+        if (p->op == 1) ensure_gram(p);
         if (!p->small_n) xhat_gemm(p, x);
         FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
         a.x = x;
         a.y = y;
         a.trace = tr.get();
+        a.gram = p->op == 1 ? p->gram.get() : nullptr;
         launch_fused(p, a);
         if (stamps && capacity > 0)
             d2h_sync(stamps, tr.get(), sizeof(uint64_t) * std::min(cnt, (size_t)capacity), ctx->stream);

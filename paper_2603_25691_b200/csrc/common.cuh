@@ -145,6 +145,10 @@ struct cphifi_unaligned_s {
     bool local_x = false;         // every CTA spans <= MAXLOC rows: CTA-local Xhat (PH_AL)
     bool prefetch = false;        // X and K columns staged in shared memory (small n * r)
     cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters
+    // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
+    int op = 0;
+    cphifi::DevBuf<double> gram;            // n x rp x rp (built lazily)
+    cphifi::DevBuf<double> gslot_a, gslot_b;  // grid x rp x rp
     cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU)
     cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid
     cphifi::DevBuf<unsigned> barrier;   // grid barrier state

@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - lane % G));
     const bool dot = a.weights == nullptr;
     const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];  // row-aligned partition (host plan)
-    const int ntiles = (a.phases & PH_B) && ca < cb ? (int)((cb - ca + TILE - 1) / TILE) : 0;
+    const bool has_obs = (a.phases & PH_B) && ca < cb;
+    const int ntiles = has_obs && !a.gram ? (int)((cb - ca + TILE - 1) / TILE) : 0;
     const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
 
     auto issue_tile = [&](int t) {
@@ -186,13 +187,13 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     };
 
     stamp(a, 0);
-    if (ntiles > 0 && threadIdx.x == 0) {
+    if (has_obs && threadIdx.x == 0) {
         s_rows[0] = a.cta_rows[2 * c];
         s_rows[1] = a.cta_rows[2 * c + 1];
     }
     __syncthreads();
     const int64_t first_row = s_rows[0], last_row = s_rows[1];
-    const bool do_al = (a.phases & PH_AL) && ntiles > 0 && dot;
+    const bool do_al = (a.phases & PH_AL) && has_obs && dot;
     const int nal = do_al ? (int)(last_row - first_row + 1) : 0;
 
     // ---- entry: async prefetch (group 0: factors, X, K columns, tile 0; group 1: tile 1) ----
@@ -240,6 +241,20 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
         stamp(a, 2);
     }
     const bool local_x = (a.phases & PH_AL) != 0;
+
+    // ---- phase B (row-Gram form): Yhat(i,:) = G_i Xhat(i,:) for the rows this CTA owns -----
+    if (has_obs && a.gram) {
+        for (int64_t row = first_row; row <= last_row; ++row) {
+            if (a.row_ptr[row + 1] == a.row_ptr[row] || a.row_first_cta[row] != c) continue;
+            const double* xr = local_x ? xloc + (row - first_row) * RP : a.xhat_rm + row * RP;
+            if (threadIdx.x < RP) {
+                const double* gi = a.gram + row * RP * RP;
+                double s = 0.0;
+                for (int b = 0; b < RP; ++b) s = fma(gi[b * RP + threadIdx.x], xr[b], s);
+                a.yhat_rm[row * RP + threadIdx.x] = s;
+            }
+        }
+    }
 
     // ---- phase B: fused gather / scatter over this CTA's observations ---------------------
     if (ntiles > 0) {

@@ -1,0 +1,180 @@
+// k_gram.cu — the row-Gram form of the unaligned operator (sm_100a).
+//
+// For every row i of the infinite mode, the reference's gather + scatter
+// (observations.hpp:174-198, called per PCG iteration by unaligned.hpp:110-111) is
+//     Yhat(i,:) = sum_{l: i_k(l)=i} (Xhat(i,:) . z_l) z_l = Xhat(i,:) G_i,
+//     G_i = sum_{l: i_k(l)=i} z_l z_l'      (rp x rp, symmetric, independent of X)
+// — an exact algebraic identity.  G is built ONCE per subproblem (O(q rp^2) flops, one pass over
+// the observations) and every operator application then costs O(n rp^2) instead of O(q d r).
+// Duplicated multi-indices (multiset configs) are handled for free: they add z z' twice.
+//
+// gram_build_kernel: CTA c walks the same row-aligned observation ranges as the fused kernel,
+//   building z for batches of GB observations of one row in shared memory and accumulating
+//   Z'Z in registers (each thread owns a BLK x BLK block of G).  Rows split across CTAs are
+//   finished by the last CTA (per-row arrival counter, ordered slot sum) — deterministic.
+// gram_apply_kernel: Yhat(i, a) = sum_b G_i(b, a) Xhat(i, b); thread (i, a), consecutive a
+//   read consecutive G entries (G_i symmetric, so its row-major and column-major layouts agree).
+#include "kernels.cuh"
+
+namespace cphifi {
+namespace {
+
+constexpr int GT = 256;  // threads per CTA
+constexpr int GB = 32;   // observations per z batch
+
+__device__ __forceinline__ unsigned atom_add_acqrel_g(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+template <int RP, int DO>
+__global__ void __launch_bounds__(GT) gram_build_kernel(const GramArgs a) {
+    constexpr int BLK = RP >= 64 ? 4 : (RP >= 32 ? 2 : 1);  // thread block of G entries
+    constexpr int NB = RP / BLK;                           // blocks per dimension
+    constexpr int NACT = NB * NB;                          // active threads (<= GT)
+    static_assert(NACT <= GT, "G tile does not fit the CTA");
+    __shared__ __align__(16) double zs[GB][RP + 2];
+    __shared__ int s_last;
+    const int c = blockIdx.x;
+    const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];
+    if (ca >= cb) return;
+    const int tid = threadIdx.x;
+    const bool act = tid < NACT;
+    const int ba = (tid / NB) * BLK, bb = (tid % NB) * BLK;
+    const int64_t first_row = a.cta_rows[2 * c];
+    double acc[BLK][BLK];
+#pragma unroll
+    for (int x = 0; x < BLK; ++x)
+#pragma unroll
+        for (int y = 0; y < BLK; ++y) acc[x][y] = 0.0;
+
+    int64_t row = first_row;
+    int64_t row_end = a.row_ptr[row + 1];
+    auto finish_row = [&](int64_t rr) {
+        const int ncta = a.row_ncta[rr];
+        double* dst = ncta == 1 ? a.g + rr * RP * RP
+                    : rr == first_row ? a.slot_a + (int64_t)c * RP * RP
+                                      : a.slot_b + (int64_t)c * RP * RP;
+        if (act) {
+#pragma unroll
+            for (int x = 0; x < BLK; ++x)
+#pragma unroll
+                for (int y = 0; y < BLK; ++y) dst[(ba + x) * RP + bb + y] = acc[x][y];
+        }
+#pragma unroll
+        for (int x = 0; x < BLK; ++x)
+#pragma unroll
+            for (int y = 0; y < BLK; ++y) acc[x][y] = 0.0;
+        if (ncta > 1) {  // the last CTA of a split row sums the slots in CTA order
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                s_last = atom_add_acqrel_g(a.rowcnt + rr, 1u) == (unsigned)ncta - 1;
+                if (s_last) a.rowcnt[rr] = 0;
+            }
+            __syncthreads();
+            if (s_last) {
+                const int u0 = a.row_first_cta[rr];
+                const bool starts = a.row_ptr[rr] == a.cta_beg[u0];
+                for (int e = tid; e < RP * RP; e += GT) {
+                    double s = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
+                                      : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
+                    for (int u = u0 + 1; u < u0 + ncta; ++u) s += __ldcg(a.slot_a + (int64_t)u * RP * RP + e);
+                    a.g[rr * RP * RP + e] = s;
+                }
+            }
+        }
+    };
+
+    int64_t pos = ca;
+    while (pos < cb) {
+        while (pos >= row_end) {  // advance to the row holding `pos` (skip empty rows)
+            finish_row(row);
+            do {
+                ++row;
+                row_end = a.row_ptr[row + 1];
+            } while (row_end <= pos);
+        }
+        const int cnt = (int)min((int64_t)GB, min(cb, row_end) - pos);
+        __syncthreads();  // previous batch consumed
+        for (int e = tid; e < GB * RP; e += GT) {
+            const int t = e / RP, j = e % RP;
+            double z = 0.0;
+            if (t < cnt) {
+                const int64_t l = pos + t;
+                z = a.fac[a.fac_off[0] + (int64_t)__ldg(a.idx + l) * RP + j];
+#pragma unroll
+                for (int m = 1; m < DO; ++m) z *= a.fac[a.fac_off[m] + (int64_t)__ldg(a.idx + (int64_t)m * a.q + l) * RP + j];
+            }
+            zs[t][j] = z;
+        }
+        __syncthreads();
+        if (act) {
+            for (int t = 0; t < cnt; ++t) {
+                double za[BLK], zb[BLK];
+#pragma unroll
+                for (int x = 0; x < BLK; ++x) {
+                    za[x] = zs[t][ba + x];
+                    zb[x] = zs[t][bb + x];
+                }
+#pragma unroll
+                for (int x = 0; x < BLK; ++x)
+#pragma unroll
+                    for (int y = 0; y < BLK; ++y) acc[x][y] = fma(za[x], zb[y], acc[x][y]);
+            }
+        }
+        pos += cnt;
+    }
+    __syncthreads();
+    finish_row(row);
+}
+
+// Yhat(i, a) = sum_b G_i(b, a) Xhat(i, b) for rows with observations (others stay zero).
+__global__ void gram_apply_kernel(const double* __restrict__ g, const double* __restrict__ xhat, const int64_t* row_ptr,
+                                  int64_t n, int64_t rp, double* __restrict__ yhat) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n * rp) return;
+    const int64_t i = e / rp, aa = e % rp;
+    if (row_ptr[i + 1] == row_ptr[i]) return;
+    const double* gi = g + i * rp * rp;
+    const double* xi = xhat + i * rp;
+    double s = 0.0;
+    for (int64_t b = 0; b < rp; ++b) s = fma(gi[b * rp + aa], xi[b], s);
+    yhat[e] = s;
+}
+
+template <int RP>
+void launch_build_rp(const GramArgs& a, int grid, cudaStream_t s) {
+    switch (a.dother) {
+        case 1: gram_build_kernel<RP, 1><<<grid, GT, 0, s>>>(a); break;
+        case 2: gram_build_kernel<RP, 2><<<grid, GT, 0, s>>>(a); break;
+        case 3: gram_build_kernel<RP, 3><<<grid, GT, 0, s>>>(a); break;
+        case 4: gram_build_kernel<RP, 4><<<grid, GT, 0, s>>>(a); break;
+        case 5: gram_build_kernel<RP, 5><<<grid, GT, 0, s>>>(a); break;
+        default: throw_invalid("unaligned: tensor order above 6 is not supported");
+    }
+}
+
+}  // namespace
+
+void gram_build(const GramArgs& a, int grid, cudaStream_t s) {
+    switch (a.rp) {
+        case 4: launch_build_rp<4>(a, grid, s); break;
+        case 8: launch_build_rp<8>(a, grid, s); break;
+        case 16: launch_build_rp<16>(a, grid, s); break;
+        case 32: launch_build_rp<32>(a, grid, s); break;
+        case 64: launch_build_rp<64>(a, grid, s); break;
+        default: throw_invalid("gram operator: padded rank above 64 is not supported");
+    }
+    CPHIFI_CHECK_LAUNCH();
+}
+
+void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
+                cudaStream_t s) {
+    const int64_t tot = n * rp;
+    gram_apply_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(g, xhat_rm, row_ptr, n, rp, yhat_rm);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+}  // namespace cphifi

@@ -89,6 +89,7 @@ struct FusedArgs {
     const int32_t* row_ncta = nullptr;       // n: CTAs touching the row (> 1 = split row)
     double lambda = 0.0, rho = 0.0;
     const double* yhat_c2 = nullptr;    // complete Yhat read by PH_C2 (yhat_rm or the NCCL sum)
+    const double* gram = nullptr;       // non-null: phase B applies the row-Gram operator instead
     unsigned* rowcnt = nullptr;         // n per-row arrival counters, zero-initialised once
     int prefetch = 0;                   // stage X and the needed K columns in smem (small n)
     unsigned* barrier = nullptr;        // barrier_words(grid) uints, zero-initialised once
@@ -101,6 +102,27 @@ size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, i
 int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s);
+
+// ---- row-Gram operator (k_gram.cu): Yhat(i,:) = G_i Xhat(i,:), G_i = sum_l z_l z_l' ---------
+struct GramArgs {
+    int64_t n = 0, rp = 0, q = 0;
+    int dother = 0;
+    const int64_t* row_ptr = nullptr;
+    const int32_t* idx = nullptr;
+    const double* fac = nullptr;
+    int64_t fac_off[8] = {0};
+    const int64_t* cta_beg = nullptr;
+    const int64_t* cta_rows = nullptr;
+    const int32_t* row_first_cta = nullptr;
+    const int32_t* row_ncta = nullptr;
+    unsigned* rowcnt = nullptr;
+    double* slot_a = nullptr;  // grid x rp x rp
+    double* slot_b = nullptr;
+    double* g = nullptr;       // n x rp x rp
+};
+void gram_build(const GramArgs& a, int grid, cudaStream_t s);
+void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
+                cudaStream_t s);
 
 // ---- seeded device-side observation generator (configs 3/4; k_synth.cu) -----------------
 void synth_observations(int d, const int64_t* shape, int64_t q, uint64_t seed, int zipf_mode, double zipf_s, int64_t r,

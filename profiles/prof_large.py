@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--q", type=int, default=0)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--trace", type=int, default=1)
+    ap.add_argument("--solve", type=int, default=0)
     args = ap.parse_args()
     cfg = configs.config3() if args.config == 3 else configs.config4()
     q = args.q or cfg.q
@@ -85,6 +86,38 @@ def main():
     sym = abs(float(z @ y) - float(x @ az)) / abs(float(z @ y))
     lin = float(torch.linalg.norm(axs - (y + 2.5 * az)) / torch.linalg.norm(axs))
     out.update({"symmetry_rel": sym, "linearity_rel": lin})
+    # row-Gram operator: one-time build, then applications
+    _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))  # streaming A x
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    p.set_operator("gram")
+    ytmp = torch.empty_like(y)
+    _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), ytmp.data_ptr()))
+    ctx.synchronize()
+    out["gram_build_plus_first_s"] = time.perf_counter() - t0
+    yg = torch.empty_like(y)
+    ts = []
+    for _ in range(max(3, args.iters)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), yg.data_ptr()))
+            b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    out["gram_matvec_ms"] = float(np.median(ts))
+    out["gram_vs_stream_rel"] = float(torch.linalg.norm(yg - y) / torch.linalg.norm(y))
+    if args.solve:
+        t0 = time.perf_counter()
+        mode.eig() if hasattr(mode, "eig") else None
+        out["eigK_s"] = time.perf_counter() - t0
+        rep = cp.SolveReport()
+        cp.solve_unaligned_pcg(p, cp.PcgConfig(cfg.tol, cfg.max_iter, True), rep)
+        out["pcg_gram"] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
+                           "converged": rep.converged, "wall_s": rep.wall_time_s, "setup_s": rep.setup_s,
+                           "history_tail": rep.residual_history[-3:]}
+        p.set_operator("stream")
+    p.set_operator("stream")
     if args.trace:
         cap = 8 * 4096
         st = np.zeros(cap, dtype=np.uint64)

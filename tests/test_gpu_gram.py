@@ -1,0 +1,115 @@
+"""Row-Gram form of the unaligned operator (k_gram.cu) against the CPU oracle.
+
+Yhat(i,:) = G_i Xhat(i,:) with G_i = sum_{l in row i} z_l z_l' is an exact identity of the
+reference's gather/scatter (observations.hpp:174-198); only the fp64 association changes, so the
+bar is 1e-12 relative like the streaming operator, PCG iterations within +-1 of the oracle and
+the final residual <= tol.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import refinst as ri
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cp(ctx):
+    import paper_2603_25691_b200 as cp
+    return cp
+
+
+@pytest.mark.parametrize("shape,r,q", [([57, 9, 8], 3, 2000), ([33, 7, 6, 5], 8, 3000), ([20, 30], 17, 500),
+                                       ([64, 10, 11], 32, 5000), ([31, 12, 9], 64, 3000), ([12, 40, 40], 10, 1)])
+def test_gram_matvec_vs_oracle(cp, shape, r, q):
+    inst = ri.Inst(shape, r, q, 0, 0.7, 0.1, 1e-6, 99 + r)
+    mode = cp.RkhsMode(inst.points, inst.sigma, inst.lam)
+    inst.sub.kernel = mode.kernel()
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(inst.shape, inst.idx, inst.vals),
+                                     cp.KruskalModel(inst.factors), 0, mode, inst.rho)
+    assert p.set_operator("gram") == "gram"
+    x = ri.random_matrix(inst.rng, shape[0] * r, 1).reshape(-1)
+    assert ri.rel(cp.unaligned_matvec(p, x), orc.unaligned_matvec(inst.sub, x)) < 1e-12
+    p.set_operator("stream")
+    assert ri.rel(cp.unaligned_matvec(p, x), orc.unaligned_matvec(inst.sub, x)) < 1e-12
+
+
+def test_gram_split_rows_and_empty_rows(cp):
+    """One huge row (split over many CTAs by the partition planner) plus empty rows."""
+    g = cp.Mt19937_64(5)
+    shape = [40, 30, 20]
+    r = 16
+    factors = ri.random_model(shape, r, g)
+    rs = np.random.default_rng(3)
+    q = 400_000
+    i0 = np.where(rs.random(q) < 0.7, 3, rs.integers(0, 40, q))  # row 3 holds ~70 % of the draws
+    i0[i0 == 17] = 18                                             # row 17 empty
+    idx = np.stack([i0, rs.integers(0, 30, q), rs.integers(0, 20, q)]).astype(np.int32)
+    vals = rs.normal(size=q)
+    mode = cp.RkhsMode(np.linspace(0, 1, 40), 0.1, 1e-3)
+    kern = mode.kernel()
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals, multiset=True), cp.KruskalModel(factors), 0,
+                                     mode, 1e-6)
+    x = np.random.default_rng(4).normal(size=40 * r)
+    y_o = orc.unaligned_matvec_stream(shape, 0, idx, factors, kern, 1e-3, 1e-6, x)
+    assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12
+    p.set_operator("gram")
+    assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12
+    assert ri.rel(p.b, orc.sampled_mttkrp_stream(shape, 0, idx, vals, factors, 40)) < 1e-12
+
+
+def test_gram_auto_resolution(cp):
+    c = ri.Inst([10, 8, 8], 4, 600, 0, 0.5, 0.1, 1e-6, 7)   # 60 obs / row >= 2 * rp = 8 -> gram
+    mode = cp.RkhsMode(c.points, c.sigma, c.lam)
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(c.shape, c.idx, c.vals), cp.KruskalModel(c.factors), 0, mode,
+                                     c.rho)
+    assert p.set_operator("auto") == "gram"
+    c2 = ri.Inst([50, 8, 8], 4, 60, 0, 0.5, 0.1, 1e-6, 8)   # ~1 obs / row -> stream
+    mode2 = cp.RkhsMode(c2.points, c2.sigma, c2.lam)
+    p2 = cp.make_unaligned_subproblem(cp.ObservationSet(c2.shape, c2.idx, c2.vals), cp.KruskalModel(c2.factors), 0,
+                                      mode2, c2.rho)
+    assert p2.set_operator("auto") == "stream"
+
+
+def test_gram_pcg_config1(cp):
+    """Config 1 PCG with the row-Gram operator: iterations within +-1, residual <= 1e-8."""
+    from paper_2603_25691_b200 import configs
+    c = configs.config1()
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    model = cp.KruskalModel([np.zeros((c.shape[0], c.r))] + c.factors[1:])
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(c.shape, c.idx, c.vals), model, 0, mode, c.rho)
+    sub = orc.make_unaligned_subproblem(c.shape, c.idx, c.vals, model.factors, 0, kern, c.lam, c.rho)
+    ev = orc.sym_eig(sub.v)
+    p.set_v_eig(ev.u, ev.d)
+    assert p.set_operator("gram") == "gram"
+    rep, orep = cp.SolveReport(), orc.SolveReport()
+    w = cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
+    orc.solve_unaligned_pcg(sub, orc.PcgConfig(c.tol, c.max_iter), ek, ev, report=orep)
+    assert rep.converged and rep.relative_residual <= c.tol
+    assert abs(rep.iterations - orep.iterations) <= 1
+    rhs = (kern @ sub.b).reshape(-1, order="F")
+    tr = np.linalg.norm(rhs - orc.unaligned_matvec(sub, w.reshape(-1, order="F"))) / np.linalg.norm(rhs)
+    assert tr <= 10 * c.tol
+
+
+@pytest.mark.parametrize("which,q", [("config3", 2_000_000), ("config4", 3_000_000)])
+def test_gram_large_config_structure(cp, which, q):
+    from paper_2603_25691_b200 import configs
+    cfg = getattr(configs, which)()
+    ctx = cp.default_context()
+    idx, vals = configs.generate_device(cfg, ctx, q)
+    hidx = idx.cpu().numpy()
+    n, r = cfg.shape[0], cfg.r
+    mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
+    kern = mode.kernel()
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
+    assert p.set_operator("gram") == "gram"
+    x = np.random.default_rng(1).normal(size=n * r)
+    y_o = orc.unaligned_matvec_stream(cfg.shape, 0, hidx, model.factors, kern, cfg.lam, cfg.rho, x)
+    assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12
