@@ -120,6 +120,29 @@ def cpu_port_matvec(c, threads, seconds):
     return n_done / el, n_done
 
 
+def secondary(args, ctx, cp, p, c, lib, x, y, stream, flush):
+    """Other BASELINE configs and the PCG solve, measured in the same run (N = 1)."""
+    import bench_secondary as bs
+    sec = {}
+
+    def attempt(key, fn):
+        try:
+            sec[key] = fn()
+        except Exception as e:  # report, never hide: the key carries the failure
+            sec[key] = {"error": f"{type(e).__name__}: {e}"}
+
+    attempt("fp64_peak", lambda: bs.fp64_peaks(ctx))
+    fp64 = sec["fp64_peak"].get("dmma_tflops", 40.0) if isinstance(sec["fp64_peak"], dict) else 40.0
+    attempt("config1_pcg_solve", lambda: bs.config1_pcg(cp, p, c))
+    attempt("config1_gram_matvec_ms_l2_flushed", lambda: bs.gram_matvec_ms(p, lib, x, y, stream, flush))
+    attempt("config0_aligned", lambda: bs.aligned("config0", ctx, 20, fp64))
+    attempt("config2_aligned", lambda: bs.aligned("config2", ctx, 10, fp64))
+    if args.large:
+        attempt("config3", lambda: bs.large("config3", ctx))
+        attempt("config4", lambda: bs.large("config4", ctx))
+    return sec
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -159,6 +182,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--secondary", type=int, default=1, help="aligned configs 0/2, PCG solves, FP64 peaks")
+    ap.add_argument("--large", type=int, default=1, help="configs 3/4 at full size inside --secondary")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
@@ -296,6 +321,8 @@ def main():
             out["cpu_baseline"] = {"value": v_cpu, "unit": "matvecs/s", "cores": threads, "kind": "port",
                                    "sample": f"config1 full operator application (q=200000) x {n_cpu}, "
                                              f"fused streaming C restatement, {threads} threads"}
+        if world == 1 and args.secondary:
+            out["secondary"] = secondary(args, ctx, cp, p, c, lib, x, y, stream, flush)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -1,0 +1,167 @@
+"""Secondary measurements reported inside bench.py's JSON line (N = 1 only).
+
+Everything is device-timed with CUDA events on the library stream unless stated; numbers that
+use the row-Gram operator are labelled as such (it reads G, not the observations, per
+application, so its roofline is computed on its own bytes, not the as-given per-observation
+bytes of SURVEY §8d).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def fp64_peaks(ctx):
+    from paper_2603_25691_b200 import _capi
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _capi.call("cphifi_fp64_peak", ctx.handle, ctypes.byref(a), ctypes.byref(b))
+    return {"dfma_tflops": a.value, "dmma_tflops": b.value}
+
+
+def aligned(which, ctx, iters, fp64_tf):
+    """Aligned solve (MTTKRP + Gram + decoupled rotate/divide/rotate; eig(V) reported as setup)."""
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import _capi, configs
+    c = getattr(configs, which)()
+    n, r = c.shape[0], c.r
+    mode = cp.RkhsMode(c.points, c.ell, c.lam, ctx=ctx)
+    t0 = time.perf_counter()
+    mode.eig()
+    eig_k_s = time.perf_counter() - t0
+    t = cp.DenseTensor(c.shape, c.tensor)
+    dt = cp._device_tensor(t, ctx)
+    model = cp.KruskalModel([np.zeros((n, r))] + c.factors[1:])
+    arrs, ptrs = cp._factor_array(model.factors, 0)
+    w = np.zeros((n, r), order="F")
+    ms = (ctypes.c_double * 5)()
+    _capi.call("cphifi_aligned_solve_timed", dt.handle, mode.handle, 0, r, ptrs, iters, w.ctypes.data_as(_capi.c_double_p),
+               ms)
+    N = int(np.prod(c.shape))
+    b_alg = 8 * N + 16 * n * n + 32 * n * r
+    f_alg = 2 * N * r + 4 * n * n * r + 4 * n * r * r
+    t_s = ms[4] / 1e3
+    hbm = hbm_peak()
+    t_roof = max(b_alg / (hbm * 1e9), f_alg / (fp64_tf * 1e12))
+    return {"solves_per_s": 1.0 / t_s, "solve_ms": ms[4], "mttkrp_ms": ms[0], "gram_ms": ms[1],
+            "eigV_setup_ms": ms[2], "decoupled_ms": ms[3], "eigK_setup_s": eig_k_s,
+            "alg_bytes": b_alg, "alg_flops": f_alg, "hbm_frac": b_alg / t_s / 1e9 / hbm,
+            "fp64_tflops": f_alg / t_s / 1e12, "roofline_frac": t_roof / t_s,
+            "note": "tensor device-resident; L2 " + ("flushed implicitly (537 MB tensor > L2)" if N * 8 > 2**27
+                                                     else "warm (16 MB tensor < L2)")}
+
+
+def config1_pcg(cp, p, c):
+    """Full device PCG solves of config 1 with both operator forms (wall clock, host loop)."""
+    out = {}
+    for op in ("stream", "gram"):
+        p.set_operator(op)
+        rep = cp.SolveReport()
+        t0 = time.perf_counter()
+        cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)  # first: includes G build for gram
+        first = time.perf_counter() - t0
+        rep = cp.SolveReport()
+        cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
+        out[op] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual, "wall_s": rep.wall_time_s,
+                   "first_call_s": first, "matvecs": rep.matvecs}
+    p.set_operator("stream")
+    return out
+
+
+def gram_matvec_ms(p, lib, x, y, stream, flush, steps=50):
+    import torch
+    from paper_2603_25691_b200 import _capi
+    p.set_operator("gram")
+    _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))  # builds G
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.add_(1)
+            a.record(stream)
+            _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
+            b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    p.set_operator("stream")
+    return float(np.median(ts))
+
+
+def large(which, ctx, iters=3, solve=True):
+    """Configs 3/4 at full size: per-observation operator, row-Gram operator, PCG (row-Gram)."""
+    import torch
+
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import _capi, configs
+    cfg = getattr(configs, which)()
+    n, r, d, q = cfg.shape[0], cfg.r, len(cfg.shape), cfg.q
+    lib = _capi.load()
+    t0 = time.perf_counter()
+    idx, vals = configs.generate_device(cfg, ctx)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    t0 = time.perf_counter()
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
+    plan_s = time.perf_counter() - t0
+    del idx, vals
+    obs.release_inputs()
+    torch.cuda.empty_cache()
+    dev = torch.device("cuda", ctx.device)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    x = torch.randn(n * r, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+
+    def timed(k):
+        ts = []
+        for _ in range(k):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+                _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
+                b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    timed(1)
+    stream_ms = timed(iters)
+    t0 = time.perf_counter()
+    p.set_operator("gram")
+    timed(1)
+    gram_build_s = time.perf_counter() - t0
+    gram_ms = timed(max(5, iters))
+    hbm = hbm_peak()
+    b_alg = 4 * d * q + 16 * n * n + 48 * n * r
+    rp = max(4, 1 << (r - 1).bit_length())
+    b_gram = 16 * n * n + 8 * n * rp * rp + 48 * n * r
+    out = {"q": q, "gen_s": gen_s, "plan_s": plan_s,
+           "stream_matvec_ms": stream_ms, "stream_matvecs_per_s": 1e3 / stream_ms,
+           "stream_hbm_frac_as_given": b_alg / (stream_ms / 1e3) / 1e9 / hbm,
+           "gram_build_s": gram_build_s, "gram_matvec_ms": gram_ms, "gram_matvecs_per_s": 1e3 / gram_ms,
+           "gram_hbm_frac_own_bytes": b_gram / (gram_ms / 1e3) / 1e9 / hbm}
+    if solve:
+        t0 = time.perf_counter()
+        mode.eig()
+        out["eigK_s"] = time.perf_counter() - t0
+        rep = cp.SolveReport()
+        cp.solve_unaligned_pcg(p, cp.PcgConfig(cfg.tol, cfg.max_iter), rep)
+        out["pcg_gram"] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
+                           "converged": rep.converged, "wall_s": rep.wall_time_s}
+    del p, obs
+    torch.cuda.empty_cache()
+    return out

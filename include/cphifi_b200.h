@@ -83,6 +83,9 @@ int cphifi_ctx_destroy(cphifi_ctx ctx);
 int cphifi_ctx_synchronize(cphifi_ctx ctx);
 /* The context's CUDA stream (cudaStream_t) so callers can order their own work. */
 int cphifi_ctx_stream(cphifi_ctx ctx, void** stream_out);
+/* Measured FP64 peaks of this GPU (TFLOP/s): a DFMA loop and a DMMA (m8n8k4) loop — the FP64
+ * roofline denominators. */
+int cphifi_fp64_peak(cphifi_ctx ctx, double* dfma_tflops, double* dmma_tflops);
 /* Multi-GPU: NCCL communicator over `nranks` processes (one per GPU).  Rank 0 creates the
  * 128-byte id with cphifi_comm_unique_id and distributes it (e.g. torch.distributed).
  * Once set, operator applications all-reduce the n x r partial accumulator. */
@@ -204,6 +207,13 @@ int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
 int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                          const double* const* factors, double* w_out, double* b_out,
                          double* v_out);
+
+/* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
+ * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup), [3] decoupled
+ * rotate/divide/rotate, [4] timed solve = [0] + [1] + [3]. */
+int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
+                               const double* const* factors, int iters, double* w_out,
+                               double* ms_out);
 
 /* ---- host-side seeded generators (test/bench inputs; no device work) -------------- */
 /* std::mt19937_64 with libstdc++'s uniform_real_distribution / uniform_int_distribution

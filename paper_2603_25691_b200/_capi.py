@@ -65,6 +65,7 @@ _SIGS = [
     ("cphifi_ctx_destroy", ctypes.c_int, [_H]),
     ("cphifi_ctx_synchronize", ctypes.c_int, [_H]),
     ("cphifi_ctx_stream", ctypes.c_int, [_H, c_void_pp]),
+    ("cphifi_fp64_peak", ctypes.c_int, [_H, c_double_p, c_double_p]),
     ("cphifi_comm_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("cphifi_ctx_init_comm", ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
     ("cphifi_ctx_world", ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
@@ -115,6 +116,8 @@ _SIGS = [
      [_H, ctypes.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, c_double_p]),
+    ("cphifi_aligned_solve_timed", ctypes.c_int,
+     [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), ctypes.c_int, c_double_p, c_double_p]),
     ("cphifi_synth_observations", ctypes.c_int,
      [_H, ctypes.c_int, c_int64_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
       ctypes.POINTER(c_double_p), ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),

@@ -507,6 +507,16 @@ int cphifi_ctx_stream(cphifi_ctx ctx, void** stream_out) {
     });
 }
 
+int cphifi_fp64_peak(cphifi_ctx ctx, double* dfma_tflops, double* dmma_tflops) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(dfma_tflops, "dfma_tflops");
+        need(dmma_tflops, "dmma_tflops");
+        DeviceGuard dg(ctx->device);
+        fp64_peaks(ctx->num_sms, ctx->stream, dfma_tflops, dmma_tflops);
+    });
+}
+
 int cphifi_comm_unique_id(uint8_t id_out[128]) {
     return guard([&] {
         need(id_out, "id_out");
@@ -1341,6 +1351,53 @@ int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
         }
         decoupled_dev(mode, r, db.get(), uv.get(), sv.get(), w.get(), t1, core);
         d2h_sync(w_out, w.get(), sizeof(double) * n * r, ctx->stream);
+    });
+}
+
+int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, const double* const* factors,
+                               int iters, double* w_out, double* ms_out) {
+    return guard([&] {
+        need(t, "tensor");
+        need(mode, "mode");
+        need(factors, "factors");
+        need(w_out, "w_out");
+        need(ms_out, "ms_out");
+        if (iters < 1) throw_invalid("cphifi_aligned_solve_timed: iters must be positive");
+        if (k < 0 || k >= t->d) throw_invalid("unfold: mode out of range");
+        if (mode->n != t->shape[k]) throw_invalid("aligned: kernel size mismatch");
+        cphifi_ctx ctx = t->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        mode_eig_once(mode);
+        const int64_t n = mode->n;
+        DevBuf<double> fbuf, b(n * r), v(r * r), uv(r * r), sv(r), w(n * r), t1, core, work;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
+        cudaEvent_t ev[5];
+        for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (int it = 0; it <= iters; ++it) {  // iteration 0 warms up (workspace allocation)
+            CPHIFI_CUDA(cudaEventRecord(ev[0], s));
+            mttkrp_dev(t, k, r, fptr, b.get(), work);
+            CPHIFI_CUDA(cudaEventRecord(ev[1], s));
+            gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), s);
+            CPHIFI_CUDA(cudaEventRecord(ev[2], s));
+            device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());  // setup per north_star
+            CPHIFI_CUDA(cudaEventRecord(ev[3], s));
+            decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+            CPHIFI_CUDA(cudaEventRecord(ev[4], s));
+            CPHIFI_CUDA(cudaEventSynchronize(ev[4]));
+            if (it == 0) continue;
+            float ms;
+            for (int ph = 0; ph < 4; ++ph) {
+                CPHIFI_CUDA(cudaEventElapsedTime(&ms, ev[ph], ev[ph + 1]));
+                acc[ph] += ms;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int i = 0; i < 4; ++i) ms_out[i] = acc[i] / iters;
+        ms_out[4] = ms_out[0] + ms_out[1] + ms_out[3];  // the timed solve excludes eig(V) (setup)
+        d2h_sync(w_out, w.get(), sizeof(double) * n * r, s);
     });
 }
 

@@ -459,7 +459,63 @@ __global__ void rm_to_cm_kernel(const double* src, int64_t rows, int64_t rp, int
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
+// FP64 peak probes (the roofline denominators MEASURED_PEAKS.json lacks): 8 independent
+// dependency chains per thread (DFMA) / per warp (DMMA m8n8k4 = 256 FMA per instruction).
+__global__ void peak_dfma_kernel(int iters, double seed, double* out) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = seed + u * 1e-3 + threadIdx.x * 1e-9;
+    const double b = 0.999999, c = 1e-7;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = fma(a[u], b, c);
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += a[u];
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+__global__ void peak_dmma_kernel(int iters, double seed, double* out) {
+    double acc[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const double av = seed + threadIdx.x * 1e-9, bv = 1.0 - threadIdx.x * 1e-9;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dmma(acc[u], av, bv);
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += acc[u][0] + acc[u][1];
+    if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
+
+void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_tflops) {
+    DevBuf<double> sink(1);
+    cudaEvent_t e0, e1;
+    CPHIFI_CUDA(cudaEventCreate(&e0));
+    CPHIFI_CUDA(cudaEventCreate(&e1));
+    const int blocks = num_sms * 8, threads = 256, iters = 4096;
+    float ms = 0.0f;
+    peak_dfma_kernel<<<blocks, threads, 0, s>>>(iters, 1.0, sink.get());  // warm-up
+    CPHIFI_CUDA(cudaEventRecord(e0, s));
+    peak_dfma_kernel<<<blocks, threads, 0, s>>>(iters, 1.0, sink.get());
+    CPHIFI_CUDA(cudaEventRecord(e1, s));
+    CPHIFI_CUDA(cudaEventSynchronize(e1));
+    CPHIFI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *dfma_tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+    peak_dmma_kernel<<<blocks, threads, 0, s>>>(iters / 4, 1.0, sink.get());
+    CPHIFI_CUDA(cudaEventRecord(e0, s));
+    peak_dmma_kernel<<<blocks, threads, 0, s>>>(iters / 4, 1.0, sink.get());
+    CPHIFI_CUDA(cudaEventRecord(e1, s));
+    CPHIFI_CUDA(cudaEventSynchronize(e1));
+    CPHIFI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *dmma_tflops = 2.0 * 256.0 * 8.0 * (iters / 4) * (double)blocks * (threads / 32) / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CPHIFI_CHECK_LAUNCH();
+}
 
 void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     if (g.m <= 0 || g.n <= 0) return;

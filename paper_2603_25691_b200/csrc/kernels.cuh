@@ -45,6 +45,9 @@ struct MttkrpArgs {
 };
 void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work);
 
+// FP64 peak probes (DFMA / DMMA loops, TFLOP/s) for the roofline denominators
+void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_tflops);
+
 // ---- Khatri-Rao Gram (tensor.hpp:186-194), factors column-major device ----------------
 void gram_kr(int d, const int64_t* shape, int64_t r, const double* const* fac, int k, double* v,
              cudaStream_t s);
