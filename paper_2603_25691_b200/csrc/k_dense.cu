@@ -24,11 +24,16 @@ constexpr int NT = 128;      // threads per CTA
 constexpr int STAGES = 3;
 constexpr int APAD = BM + 4; // smem row pitch (doubles); == 4 mod 16 -> conflict-free frags
 
-template <int BN>
+template <int BN, int BMv = BM, int ST = STAGES>
 struct GemmSmem {
-    double a[STAGES][BK][APAD];
-    double b[STAGES][BK][BN + 4];
+    double a[ST][BK][BMv + 4];  // pitch == 4 mod 16 doubles: conflict-free fragment loads
+    double b[ST][BK][BN + 4];
 };
+
+// MTTKRP tile shape: 128 rows (8 warps x 16), 4 cp.async stages (one CTA per SM)
+constexpr int BMM = 128;
+constexpr int NTM = 256;
+constexpr int STM = 4;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -88,8 +93,8 @@ __device__ __forceinline__ void load_b(GemmSmem<BN>& sm, int st, const double* _
     }
 }
 
-template <int BN>
-__device__ __forceinline__ void mma_stage(const GemmSmem<BN>& sm, int st, double (&acc)[2][BN / 8][2]) {
+template <int BN, int BMv = BM, int ST = STAGES>
+__device__ __forceinline__ void mma_stage(const GemmSmem<BN, BMv, ST>& sm, int st, double (&acc)[2][BN / 8][2]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kq = lane & 3, g = lane >> 2;
 #pragma unroll
@@ -221,7 +226,8 @@ void launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     const int mt = (int)((g.m + BM - 1) / BM);
     const int nt = (int)((g.n + BN - 1) / BN);
     int S = 1;
-    while (S < 8 && (int64_t)mt * nt * S < 2 * num_sms && g.k / (2 * S) >= 2 * BK) S *= 2;
+    // largest split (power of two <= 8) that still fits one wave of co-resident CTAs
+    while (S < 8 && (int64_t)mt * nt * (2 * S) <= 2 * num_sms && g.k / (2 * S) >= 2 * BK) S *= 2;
     const size_t smem = sizeof(GemmSmem<BN>);
     static bool attr_set = false;
     if (!attr_set) {
@@ -246,41 +252,103 @@ void launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
 }
 
 // ---- MTTKRP (k = 0): A = T slab (n0 x Mloc, column-major), B = Z rows generated -------
+// The K dimension (unfolding columns c = i1 + n1 * outer, mode 1 fastest, tensor.hpp:70-73) is
+// walked in tiles that never straddle an `outer` index (i2, ..., i_{d-1}): a tile is BK
+// consecutive i1 of one outer, so its Khatri-Rao rows are A_1(i1, :) * Wout(outer, :) with
+// Wout(o, :) = A_{d-1}(i_{d-1}, :) * ... * A_2(i2, :) precomputed once (the reference's
+// khatri_rao multiplies left to right in descending mode order, matrix_ops.hpp:24-42; A_1 is
+// the last factor, so the association — and every rounding — is the same).
+__global__ void kr_outer_kernel(const MttkrpArgs a, int64_t n_outer, double* __restrict__ wout) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_outer * a.r) return;
+    const int64_t o = e / a.r, j = e % a.r;
+    if (a.d == 2) {
+        wout[e] = 1.0;
+        return;
+    }
+    int64_t sub[8];
+    int64_t rem = o;
+    for (int m = 2; m < a.d; ++m) {
+        sub[m] = rem % a.shape[m];
+        rem /= a.shape[m];
+    }
+    double w = a.fac[a.d - 1][sub[a.d - 1] + a.ld[a.d - 1] * j];
+    for (int m = a.d - 2; m >= 2; --m) w *= a.fac[m][sub[m] + a.ld[m] * j];
+    wout[e] = w;
+}
+
 template <int BN>
-__device__ __forceinline__ void gen_z(GemmSmem<BN>& sm, int st, const MttkrpArgs& a, int64_t j0,
-                                      int64_t k0, int64_t kend) {
-    for (int e = threadIdx.x; e < BN * BK; e += NT) {
-        const int jj = e % BN, kk = e / BN;
-        const int64_t j = j0 + jj, c = k0 + kk;
-        double z = 0.0;
-        if (j < a.r && c < kend) {
-            // column c of the unfolding: mode 1 fastest (tensor.hpp:70-73)
-            int64_t sub[8];
-            int64_t rem = c;
-            for (int m = 1; m < a.d; ++m) {
-                sub[m] = rem % a.shape[m];
-                rem /= a.shape[m];
-            }
-            sub[1] += a.off1;
-            // khatri_rao(A_{d-1}, ..., A_1): left-to-right in descending mode order
-            z = a.fac[a.d - 1][sub[a.d - 1] + a.ld[a.d - 1] * j];
-            for (int m = a.d - 2; m >= 1; --m) z *= a.fac[m][sub[m] + a.ld[m] * j];
+__device__ __forceinline__ void load_tile_mttkrp(GemmSmem<BN, BMM, STM>& sm, double* ws, int st, const MttkrpArgs& a,
+                                                 int64_t chunks, const double* __restrict__ wout, int64_t i0, int64_t j0,
+                                                 int64_t tile) {
+    const int64_t n0 = a.shape[0], n1 = a.shape[1];
+    const int64_t outer = tile / chunks, c1 = (tile - outer * chunks) * BK;
+    const int cnt = (int)min((int64_t)BK, n1 - c1);
+    const double* tcol = a.t + (c1 + n1 * outer) * n0;  // first T column of the tile
+    if ((n0 & 1) == 0) {  // 16-byte copies: column segments are 16-byte aligned
+        for (int e = threadIdx.x; e < (BMM / 2) * BK; e += NTM) {
+            const int ii = 2 * (e % (BMM / 2)), kk = e / (BMM / 2);
+            const int64_t i = i0 + ii;
+            const bool p = (i < n0) && (kk < cnt);
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&sm.a[st][kk][ii]));
+            const double* src = p ? tcol + i + (int64_t)kk * n0 : a.t;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(p ? 16 : 0));
         }
-        sm.b[st][kk][jj] = z;
+    } else {
+        for (int e = threadIdx.x; e < BMM * BK; e += NTM) {
+            const int ii = e % BMM, kk = e / BMM;
+            const int64_t i = i0 + ii;
+            const bool p = (i < n0) && (kk < cnt);
+            cp_async8(&sm.a[st][kk][ii], p ? tcol + i + (int64_t)kk * n0 : a.t, p);
+        }
+    }
+    // B tile staged RAW (A_1 block and the Wout row, both cp.async); the product
+    // z = A_1(i1, j) * Wout(outer, j) is formed when the DMMA fragment is loaded
+    const double* a1 = a.fac[1] + c1 + a.off1;
+    for (int e = threadIdx.x; e < BN * BK; e += NTM) {
+        const int kk = e % BK, jj = e / BK;  // consecutive threads: consecutive i1 (coalesced)
+        const int64_t j = j0 + jj;
+        const bool p = (j < a.r) && (kk < cnt);
+        cp_async8(&sm.b[st][kk][jj], p ? a1 + kk + a.ld[1] * j : a.fac[1], p);
+    }
+    if (threadIdx.x < BN) {
+        const int64_t j = j0 + threadIdx.x;
+        cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.r + j : wout, j < a.r);
     }
 }
 
 template <int BN>
-__global__ void __launch_bounds__(NT) mttkrp_dmma_kernel(const MttkrpArgs a, int64_t mcols,
-                                                         double* __restrict__ work) {
+__device__ __forceinline__ void mma_stage_scaled(const GemmSmem<BN, BMM, STM>& sm, const double* ws, int st,
+                                                 double (&acc)[2][BN / 8][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, g = lane >> 2;
+    double w[BN / 8];
+#pragma unroll
+    for (int nf = 0; nf < BN / 8; ++nf) w[nf] = ws[st * BN + nf * 8 + g];
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+        const int kr = ks * 4 + kq;
+        const double a0 = sm.a[st][kr][warp * 16 + g];
+        const double a1 = sm.a[st][kr][warp * 16 + 8 + g];
+#pragma unroll
+        for (int nf = 0; nf < BN / 8; ++nf) {
+            const double bv = sm.b[st][kr][nf * 8 + g] * w[nf];
+            dmma(acc[0][nf], a0, bv);
+            dmma(acc[1][nf], a1, bv);
+        }
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NTM) mttkrp_dmma_kernel(const MttkrpArgs a, int64_t chunks, int64_t ktiles,
+                                                         const double* __restrict__ wout, double* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    GemmSmem<BN>& sm = *reinterpret_cast<GemmSmem<BN>*>(smem_raw);
+    GemmSmem<BN, BMM, STM>& sm = *reinterpret_cast<GemmSmem<BN, BMM, STM>*>(smem_raw);
+    double* ws = reinterpret_cast<double*>(smem_raw + sizeof(GemmSmem<BN, BMM, STM>));  // STM x BN
     const int P = gridDim.y, split = blockIdx.y;
     const int64_t n0 = a.shape[0];
-    const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.z * BN;
-    const int64_t ktiles = (mcols + BK - 1) / BK;
+    const int64_t i0 = (int64_t)blockIdx.x * BMM, j0 = (int64_t)blockIdx.z * BN;
     const int64_t tb = ktiles * split / P, te = ktiles * (split + 1) / P;
-    const int64_t kbeg = tb * BK, kend = min(mcols, te * BK);
     const int ntiles = (int)(te - tb);
 
     double acc[2][BN / 8][2];
@@ -290,23 +358,17 @@ __global__ void __launch_bounds__(NT) mttkrp_dmma_kernel(const MttkrpArgs a, int
         for (int y = 0; y < BN / 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < ntiles) {
-            load_a<BN>(sm, s, a.t, 1, n0, n0, i0, kbeg + (int64_t)s * BK, kend);
-            gen_z<BN>(sm, s, a, j0, kbeg + (int64_t)s * BK, kend);
-        }
+    for (int s = 0; s < STM - 1; ++s) {
+        if (s < ntiles) load_tile_mttkrp<BN>(sm, ws, s, a, chunks, wout, i0, j0, tb + s);
         cp_async_commit();
     }
     for (int t = 0; t < ntiles; ++t) {
-        const int nxt = t + STAGES - 1;
-        if (nxt < ntiles) {
-            load_a<BN>(sm, nxt % STAGES, a.t, 1, n0, n0, i0, kbeg + (int64_t)nxt * BK, kend);
-            gen_z<BN>(sm, nxt % STAGES, a, j0, kbeg + (int64_t)nxt * BK, kend);
-        }
+        const int nxt = t + STM - 1;
+        if (nxt < ntiles) load_tile_mttkrp<BN>(sm, ws, nxt % STM, a, chunks, wout, i0, j0, tb + nxt);
         cp_async_commit();
-        cp_async_wait<STAGES - 1>();
+        cp_async_wait<STM - 1>();
         __syncthreads();
-        mma_stage<BN>(sm, t % STAGES, acc);
+        mma_stage_scaled<BN>(sm, ws, t % STM, acc);
         __syncthreads();
     }
     cp_async_wait<0>();
@@ -336,24 +398,29 @@ __global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int
 template <int BN>
 void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work) {
     const int64_t n0 = a.shape[0];
-    int64_t mcols = 1;
-    for (int m = 1; m < a.d; ++m) mcols *= a.shape[m];
-    const int mt = (int)((n0 + BM - 1) / BM);
+    int64_t n_outer = 1;
+    for (int m = 2; m < a.d; ++m) n_outer *= a.shape[m];
+    const int64_t chunks = (a.shape[1] + BK - 1) / BK;
+    const int64_t ktiles = n_outer * chunks;
+    const int mt = (int)((n0 + BMM - 1) / BMM);
     const int nt = (int)((a.r + BN - 1) / BN);
-    const int64_t ktiles = (mcols + BK - 1) / BK;
-    int64_t P = (2 * (int64_t)num_sms + mt * nt - 1) / (mt * nt);
+    // exactly one wave (one CTA per SM): a partial second wave would double the duration
+    int64_t P = std::max<int64_t>(1, (int64_t)num_sms / (mt * nt));
     P = std::max<int64_t>(1, std::min<int64_t>(P, ktiles));
     P = std::min<int64_t>(P, 1024);
-    const size_t need = (size_t)P * n0 * a.r;
+    const size_t need = (size_t)P * n0 * a.r + (size_t)n_outer * a.r;
     if (work.n < need) work.alloc(need);
-    const size_t smem = sizeof(GemmSmem<BN>);
+    double* wout = work.get() + (size_t)P * n0 * a.r;
+    kr_outer_kernel<<<(unsigned)((n_outer * a.r + 255) / 256), 256, 0, s>>>(a, n_outer, wout);
+    CPHIFI_CHECK_LAUNCH();
+    const size_t smem = sizeof(GemmSmem<BN, BMM, STM>) + sizeof(double) * STM * BN;
     static bool attr_set = false;
     if (!attr_set) {
         CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
         attr_set = true;
     }
-    mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NT, smem, s>>>(a, mcols, work.get());
+    mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTM, smem, s>>>(a, chunks, ktiles, wout, work.get());
     CPHIFI_CHECK_LAUNCH();
     const int64_t cnt = n0 * a.r;
     reduce_splits_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(
