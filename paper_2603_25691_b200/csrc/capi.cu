@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 
@@ -421,8 +422,6 @@ void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     h.epi = EPI_SCALE_DIV; h.e_row = mode->mu.get(); h.e_col = sv; h.beta1 = mode->lambda;
     h.flag = flag.get();
     gemm(h, ctx->num_sms, ctx->stream);
-    if (read_flag(ctx, flag.get()))
-        throw_runtime("solve_aligned_decoupled: zero eigenvalue pair; use lambda > 0");
     gemm_nn(ctx, n, r, n, mode->u.get(), n, core.get(), n, t1.get(), n);  // U_K core
     GemmArgs o;
     o.m = n; o.n = r; o.k = r;                    // W = (.) U_V'
@@ -430,6 +429,9 @@ void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     o.b = uv; o.b_rs = r; o.b_cs = 1;
     o.c = w; o.c_rs = 1; o.c_cs = n;
     gemm(o, ctx->num_sms, ctx->stream);
+    // checked once the four GEMMs are queued (no bubble mid-pipeline); W is discarded on error
+    if (read_flag(ctx, flag.get()))
+        throw_runtime("solve_aligned_decoupled: zero eigenvalue pair; use lambda > 0");
 }
 
 void upload_factors_cm(cphifi_ctx ctx, int d, const int64_t* shape, int k, int64_t r, const double* const* factors,
@@ -1030,7 +1032,26 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
         a.y = y;
         a.trace = tr.get();
         a.gram = p->op == 1 ? p->gram.get() : nullptr;
+        DevBuf<long long> dbg;
+        const bool want_dbg = std::getenv("CPHIFI_DBG") != nullptr;  // developer timeline
+        if (want_dbg) {
+            dbg.alloc((size_t)p->grid * DBG_SLOTS);
+            CPHIFI_CUDA(cudaMemsetAsync(dbg.get(), 0xff, dbg.n * sizeof(long long), ctx->stream));
+            a.dbg = dbg.get();
+        }
         launch_fused(p, a);
+        if (want_dbg) {
+            std::vector<long long> h(dbg.n);
+            d2h_sync(h.data(), dbg.get(), sizeof(long long) * h.size(), ctx->stream);
+            for (int c = 0; c < std::min(p->grid, 4); ++c) {
+                std::printf("cta %d:", c);
+                const long long t0 = h[(size_t)c * DBG_SLOTS + 1];
+                for (int e = 0; e < DBG_SLOTS / 2 && h[(size_t)c * DBG_SLOTS + 2 * e] >= 0; ++e)
+                    std::printf(" %lld@%lld", h[(size_t)c * DBG_SLOTS + 2 * e], h[(size_t)c * DBG_SLOTS + 2 * e + 1] - t0);
+                std::printf("\n");
+            }
+            std::fflush(stdout);
+        }
         if (stamps && capacity > 0)
             d2h_sync(stamps, tr.get(), sizeof(uint64_t) * std::min(cnt, (size_t)capacity), ctx->stream);
         CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));

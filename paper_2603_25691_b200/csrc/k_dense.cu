@@ -429,21 +429,31 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
 }
 
 // ---- small kernels -------------------------------------------------------------------
-__global__ void gram_kernel(int d, int k, int64_t r, const double* const* fac, const int64_t* shape,
-                            double* v) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= r * r) return;
-    const int64_t row = e % r, col = e / r;  // V(row, col)
+// V(row, col) = prod_{m != k} (A_m' A_m)(row, col): one warp per entry, lanes stride the rows
+// of A_m (coalesced), fixed xor-shuffle tree; V is exactly symmetric (same products, same order).
+struct GramKrArgs {
+    int d = 0, k = 0;
+    int64_t r = 0;
+    const double* fac[8] = {nullptr};
+    int64_t shape[8] = {0};
+};
+__global__ void gram_kernel(const GramKrArgs g, double* v) {
+    const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= g.r * g.r) return;
+    const int64_t row = e % g.r, col = e / g.r;
     double acc = 1.0;
-    for (int m = 0; m < d; ++m) {
-        if (m == k) continue;
-        const double* a = fac[m];
-        const int64_t nm = shape[m];
+    for (int m = 0; m < g.d; ++m) {
+        if (m == g.k) continue;
+        const double* a = g.fac[m];
+        const int64_t nm = g.shape[m];
         double s = 0.0;
-        for (int64_t i = 0; i < nm; ++i) s += a[i + nm * row] * a[i + nm * col];
+        for (int64_t i = lane; i < nm; i += 32) s = fma(a[i + nm * row], a[i + nm * col], s);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         acc *= s;
     }
-    v[e] = acc;
+    if (lane == 0) v[e] = acc;
 }
 
 __global__ void kernel_matrix_kernel(int kind, const double* __restrict__ pts, int64_t n, double p,
@@ -606,13 +616,17 @@ void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doubl
 
 void gram_kr(int d, const int64_t* shape, int64_t r, const double* const* fac, int k, double* v,
              cudaStream_t s) {
-    DevBuf<const double*> dfac(d);
-    DevBuf<int64_t> dshape(d);
-    CPHIFI_CUDA(cudaMemcpyAsync(dfac.get(), fac, sizeof(double*) * d, cudaMemcpyHostToDevice, s));
-    CPHIFI_CUDA(cudaMemcpyAsync(dshape.get(), shape, sizeof(int64_t) * d, cudaMemcpyHostToDevice, s));
-    gram_kernel<<<blocks_for(r * r, 128), 128, 0, s>>>(d, k, r, dfac.get(), dshape.get(), v);
+    if (d > 8) throw_invalid("gram_khatri_rao: order above 8 is not supported");
+    GramKrArgs g;
+    g.d = d;
+    g.k = k;
+    g.r = r;
+    for (int m = 0; m < d; ++m) {
+        g.fac[m] = fac[m];
+        g.shape[m] = shape[m];
+    }
+    gram_kernel<<<blocks_for(r * r * 32, 256), 256, 0, s>>>(g, v);
     CPHIFI_CHECK_LAUNCH();
-    CPHIFI_CUDA(cudaStreamSynchronize(s));  // dfac/dshape are freed on return
 }
 
 void kernel_matrix(int kind, const double* pts, int64_t n, double param, double* kmat, cudaStream_t s) {

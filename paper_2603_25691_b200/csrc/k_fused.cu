@@ -57,13 +57,14 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 // group arrives on the top counter; the last group bumps the generation word.  Counters are
 // never reset: an episode is complete when a counter reaches a multiple of its member count.
 // Layout: bar[0] top count, bar[32] generation, bar[64 + 32*k] count of group k.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, int group) {
+// `gen` is thread 0's copy of the generation word, read once at kernel entry (it only changes
+// when this kernel's own barriers complete), so the critical path starts with the arrival.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int group, unsigned& gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const int C = gridDim.x, k = blockIdx.x / group;
         const unsigned ngrp = (unsigned)((C + group - 1) / group);
         const unsigned members = (unsigned)min(group, C - k * group);
-        const unsigned gen = ld_acquire(bar + 32);
         __threadfence();  // cumulative: this CTA's writes (ordered by bar.sync) before arrival
         const unsigned old = atom_add_acqrel(bar + 64 + 32 * k, 1u);
         if ((old + 1) % members == 0) {
@@ -72,6 +73,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int group) {
         }
         while (ld_acquire(bar + 32) == gen) {
         }
+        ++gen;
     }
     __syncthreads();
 }
@@ -115,39 +117,54 @@ __device__ __forceinline__ void ldv(double (&v)[VPL], const double* p) {
 }
 
 // out[j] = sum_k kc[k] * V(k, j), j < r, for one row (kc = the row's K column, length n).
-// thread t -> column j = t / S, slice s = t % S over k; the S partials are combined by a
-// fixed xor-shuffle tree inside the warp (and an ordered smem pass when S > 32).
+// thread t -> column j = t % RP, k-slice s = t / RP: consecutive lanes read consecutive
+// columns, so a warp load of a row-major V covers contiguous row segments; kc[k] is a
+// broadcast.  Loads go out in predicated batches of 8 (V may live in L2).  Lanes sharing j are
+// combined by xor shuffles, then the per-warp (or per-slice) partials in a fixed order.
 template <int RP>
 __device__ __forceinline__ void row_dot(const FusedArgs& a, const double* __restrict__ kc, const double* __restrict__ v,
                                         int64_t vs_r, int64_t vs_c, double* red, double* out) {
     constexpr int S = FT / RP;
-    constexpr int W = S < 32 ? S : 32;
-    const int j = threadIdx.x / S, s = threadIdx.x % S;
+    const int j = threadIdx.x % RP, s = threadIdx.x / RP;
     double t = 0.0;
     if (j < a.r) {
         const double* vj = v + j * vs_c;
-#pragma unroll 8
-        for (int64_t k = s; k < a.n; k += S) t = fma(kc[k], vj[k * vs_r], t);
-    }
+        for (int64_t k0 = s; k0 < a.n; k0 += 8 * S) {
+            double kv[8], vv[8];
 #pragma unroll
-    for (int off = W / 2; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if constexpr (S > 32) {
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
-        __syncthreads();
-        if (threadIdx.x < RP) {
-            double acc = 0.0;
-            for (int q = 0; q < S / 32; ++q) acc += red[threadIdx.x * (S / 32) + q];
-            out[threadIdx.x] = threadIdx.x < a.r ? acc : 0.0;
+            for (int u = 0; u < 8; ++u) {
+                const int64_t k = k0 + (int64_t)u * S;
+                const bool ok = k < a.n;
+                kv[u] = ok ? kc[k] : 0.0;
+                vv[u] = ok ? vj[k * vs_r] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t = fma(kv[u], vv[u], t);
         }
-    } else {
-        if (s == 0) out[j] = j < a.r ? t : 0.0;
+    }
+    if constexpr (RP < 32) {
+#pragma unroll
+        for (int off = 16; off >= RP; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    }
+    constexpr int PW = RP < 32 ? FT / 32 : S;  // partials per column
+    const int pidx = RP < 32 ? (int)(threadIdx.x >> 5) : s;
+    if (RP >= 32 || (threadIdx.x & 31) < RP) red[pidx * RP + j] = t;
+    __syncthreads();
+    if (threadIdx.x < RP) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < PW; ++q) acc += red[q * RP + threadIdx.x];
+        out[threadIdx.x] = threadIdx.x < a.r ? acc : 0.0;
     }
     __syncthreads();
 }
 
 template <int RP, int DO, bool SMEMF>
 __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
-    constexpr int VPL = 4;                // doubles per lane (two LDS.128 per factor row)
+    // 2 doubles per lane: one LDS.128 per factor row, and every 8-lane phase of the warp reads
+    // one contiguous 128-byte row segment -> conflict-free gathers (the loop is bound by
+    // shared-memory wavefronts, SURVEY §7 hard part 4)
+    constexpr int VPL = (RP >= 8 && RP <= 64) ? 2 : 4;  // G = RP / VPL <= 32 lanes
     constexpr int G = RP / VPL;           // lanes per observation: few shuffle steps per dot
     constexpr int NG = FT / G;            // observations per round
     constexpr int NW = FT / 32;
@@ -187,12 +204,29 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     };
 
     stamp(a, 0);
+    unsigned bar_gen = threadIdx.x == 0 ? ld_acquire(a.barrier + 32) : 0u;
+    __shared__ unsigned s_c2_empty;  // bit t: y row i0 + t has no observation in this shard
+    if (threadIdx.x < 32) {
+        const bool e = (a.phases & PH_C2) && i0 + threadIdx.x < i1 &&
+                       a.row_ptr[i0 + threadIdx.x + 1] == a.row_ptr[i0 + threadIdx.x];
+        const unsigned m = __ballot_sync(0xffffffffu, e);
+        if (threadIdx.x == 0) s_c2_empty = m;
+    }
     if (has_obs && threadIdx.x == 0) {
         s_rows[0] = a.cta_rows[2 * c];
         s_rows[1] = a.cta_rows[2 * c + 1];
     }
     __syncthreads();
     const int64_t first_row = s_rows[0], last_row = s_rows[1];
+    int dbg_n = 0;
+    auto dbg_mark = [&](int ev) {  // debug timeline (thread 0): (event, clock64) pairs
+        if (a.dbg && threadIdx.x == 0 && dbg_n < DBG_SLOTS / 2) {
+            a.dbg[(size_t)blockIdx.x * DBG_SLOTS + 2 * dbg_n] = ev;
+            a.dbg[(size_t)blockIdx.x * DBG_SLOTS + 2 * dbg_n + 1] = clock64();
+            ++dbg_n;
+        }
+    };
+    dbg_mark(0);
     const bool do_al = (a.phases & PH_AL) && has_obs && dot;
     const int nal = do_al ? (int)(last_row - first_row + 1) : 0;
 
@@ -237,7 +271,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             if (threadIdx.x < RP) a.xhat_rm[i * RP + threadIdx.x] = rowbuf[threadIdx.x];
         }
         stamp(a, 1);
-        grid_barrier(a.barrier, a.bar_groups);
+        grid_barrier(a.barrier, a.bar_groups, bar_gen);
         stamp(a, 2);
     }
     const bool local_x = (a.phases & PH_AL) != 0;
@@ -318,102 +352,82 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             else cp_wait<0>();
             __syncthreads();
             if (t == 0) stamp(a, 2);
+            dbg_mark(1);  // tile ready
             const int buf = t & 1;
             const int64_t t0 = ca + (int64_t)t * TILE;
             const int64_t t1 = min(cb, t0 + TILE);
             const int32_t* ti = sidx + buf * DO * TILE;
             const double* tw = sw + buf * TILE;
-            int64_t base = t0;
-            while (base < t1) {
-                // fast path: UNR full rounds inside the current row, four chains in flight
-                if (base + UNR * NG <= min(t1, cur_end)) {
-                    double z[UNR][VPL], s[UNR];
+            auto build_z = [&](int o, double (&z)[VPL]) {
+                ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
 #pragma unroll
-                    for (int u = 0; u < UNR; ++u) {
-                        const int o = (int)(base + u * NG + g - t0);
-                        ldv<VPL>(z[u], fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
+                for (int m = 1; m < DO; ++m) {
+                    double f[VPL];
+                    ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)ti[m * TILE + o] * RP + jb);
 #pragma unroll
-                        for (int m = 1; m < DO; ++m) {
-                            double f[VPL];
-                            ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)ti[m * TILE + o] * RP + jb);
-#pragma unroll
-                            for (int v = 0; v < VPL; ++v) z[u][v] *= f[v];
-                        }
-                        if (dot) {
-                            double p = 0.0;
-#pragma unroll
-                            for (int v = 0; v < VPL; ++v) p = fma(xh[v], z[u][v], p);
-                            s[u] = p;
-                        } else {
-                            s[u] = tw[o];
-                        }
-                    }
-                    if (dot) {
-#pragma unroll
-                        for (int off = G / 2; off > 0; off >>= 1)
-#pragma unroll
-                            for (int u = 0; u < UNR; ++u) s[u] += __shfl_xor_sync(gmask, s[u], off, G);
-                    }
-#pragma unroll
-                    for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                        for (int v = 0; v < VPL; ++v) acc[v] = fma(s[u], z[u][v], acc[v]);
-                    base += UNR * NG;
-                    continue;
+                    for (int v = 0; v < VPL; ++v) z[v] *= f[v];
                 }
-                // general round: one observation per group, may cross row boundaries
-                const int64_t l = base + g;
-                const bool valid = l < t1;
-                const int o = (int)(l - t0);
-                const int64_t last_l = min(base + NG, t1) - 1;
-                double z[VPL];
-                double w = 0.0;
-                if (valid) {
-                    ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
+            };
+            auto partial_dot = [&](const double (&z)[VPL]) {
+                double p = 0.0;
 #pragma unroll
-                    for (int m = 1; m < DO; ++m) {
-                        double f[VPL];
-                        ldv<VPL>(f, fac + a.fac_off[m] + (int64_t)ti[m * TILE + o] * RP + jb);
-#pragma unroll
-                        for (int v = 0; v < VPL; ++v) z[v] *= f[v];
-                    }
-                    if (!dot) w = tw[o];
-                }
-                auto contribute = [&]() {
-                    double s;
+                for (int v = 0; v < VPL; ++v) p = fma(xh[v], z[v], p);
+                return p;
+            };
+            // Row segments: [seg, seg_end) lies in row `cur`; a tight strided loop with two
+            // observations in flight per group and no per-round row bookkeeping.
+            int64_t seg = t0;
+            while (seg < t1) {
+                const int64_t seg_end = min(t1, cur_end);
+                const int o_end = (int)(seg_end - t0);
+                int o = (int)(seg - t0) + g;
+                for (; o + NG < o_end; o += 2 * NG) {
+                    double z0[VPL], z1[VPL];
+                    build_z(o, z0);
+                    build_z(o + NG, z1);
+                    double s0, s1;
                     if (dot) {
-                        double p = 0.0;
+                        s0 = partial_dot(z0);
+                        s1 = partial_dot(z1);
 #pragma unroll
-                        for (int v = 0; v < VPL; ++v) p = fma(xh[v], z[v], p);
-#pragma unroll
-                        for (int off = G / 2; off > 0; off >>= 1) p += __shfl_xor_sync(gmask, p, off, G);
-                        s = p;
+                        for (int off = G / 2; off > 0; off >>= 1) {
+                            s0 += __shfl_xor_sync(gmask, s0, off, G);
+                            s1 += __shfl_xor_sync(gmask, s1, off, G);
+                        }
                     } else {
-                        s = w;
+                        s0 = tw[o];
+                        s1 = tw[o + NG];
                     }
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s, z[v], acc[v]);
-                };
-                if (last_l < cur_end) {  // whole round inside the current row
-                    if (valid) contribute();
-                } else {
-                    bool done = !valid;
-                    while (true) {
-                        if (!done && l < cur_end) {
-                            contribute();
-                            done = true;
-                        }
-                        if (last_l < cur_end) break;
-                        flush(cur);
-                        const int64_t pos = cur_end;  // next row holding position cur_end
-                        do {
-                            ++cur;
-                            cur_end = a.row_ptr[cur + 1];
-                        } while (cur_end <= pos);
-                        load_xh();
-                    }
+                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s0, z0[v], acc[v]);
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s1, z1[v], acc[v]);
                 }
-                base += NG;
+                if (o < o_end) {
+                    double z0[VPL];
+                    build_z(o, z0);
+                    double s0;
+                    if (dot) {
+                        s0 = partial_dot(z0);
+#pragma unroll
+                        for (int off = G / 2; off > 0; off >>= 1) s0 += __shfl_xor_sync(gmask, s0, off, G);
+                    } else {
+                        s0 = tw[o];
+                    }
+#pragma unroll
+                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s0, z0[v], acc[v]);
+                }
+                seg = seg_end;
+                dbg_mark(2);  // segment done
+                if (seg_end == cur_end && seg_end < cb) {  // row complete, more rows follow
+                    flush(cur);
+                    dbg_mark(3);  // flush done
+                    do {
+                        ++cur;
+                        cur_end = a.row_ptr[cur + 1];
+                    } while (cur_end <= seg_end);
+                    load_xh();
+                }
             }
             __syncthreads();  // all groups are done with buffer t & 1
             if (t + 2 < ntiles) {
@@ -428,30 +442,38 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
 
     // ---- phase C2: y = (K Yhat + lambda Xhat) + rho x  (small n) ------------------------------
     if (a.phases & PH_C2) {
-        if (a.phases & PH_B) grid_barrier(a.barrier, a.bar_groups);
+        if (a.phases & PH_B) grid_barrier(a.barrier, a.bar_groups, bar_gen);
         stamp(a, 5);
+        dbg_mark(4);
         cp_wait<0>();
         __syncthreads();
         for (int64_t i = i0; i < i1; ++i) {
             const double* kc = pf ? kcs + (MAXLOC + i - i0) * a.n : a.kmat + i * a.n;
+            // no observation on row i here -> no CTA produced Xhat(i,:): recompute it below
+            const bool empty = local_x && (i - i0 < 32 ? ((s_c2_empty >> (i - i0)) & 1u) != 0
+                                                       : a.row_ptr[i + 1] == a.row_ptr[i]);
+            double xr = 0.0;  // issued before the Yhat dot so the two L2 round trips overlap
+            if (!empty && threadIdx.x < RP) xr = __ldcg(a.xhat_rm + i * RP + threadIdx.x);
+            dbg_mark(5);
             row_dot<RP>(a, kc, a.yhat_c2, RP, 1, red, rowbuf);
-            if (local_x && a.row_ptr[i + 1] == a.row_ptr[i]) {
-                // no observation on row i here, so no CTA produced Xhat(i,:): compute it
+            dbg_mark(6);
+            if (empty) {
                 row_dot<RP>(a, kc, pf ? xs : a.x, 1, a.n, red, rowbuf + RP);
             } else {
-                if (threadIdx.x < RP) rowbuf[RP + threadIdx.x] = __ldcg(a.xhat_rm + i * RP + threadIdx.x);
+                if (threadIdx.x < RP) rowbuf[RP + threadIdx.x] = xr;
                 __syncthreads();
             }
             if (threadIdx.x < a.r) {
                 const int64_t e = i + a.n * threadIdx.x;
                 const double out = rowbuf[threadIdx.x] + a.lambda * rowbuf[RP + threadIdx.x];
-                a.y[e] = out + a.rho * a.x[e];
+                a.y[e] = out + a.rho * (pf ? xs[e] : a.x[e]);
             }
             __syncthreads();
         }
     } else {
         cp_wait<0>();
     }
+    dbg_mark(7);
     stamp(a, 7);
 }
 
@@ -507,7 +529,7 @@ int occupancy_rp(int dother, bool smemf, size_t smem) {
 }  // namespace
 
 size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems) {
-    const int64_t vpl = 4;  // must match fused_matvec_kernel
+    const int64_t vpl = (rp >= 8 && rp <= 64) ? 2 : 4;  // must match fused_matvec_kernel
     return sizeof(double) * (FT * vpl + rp + FT + 2 * rp + MAXLOC * rp + 2 * TILE) + sizeof(int32_t) * 2 * dother * TILE +
            sizeof(double) * ((smemf ? fac_total : 0) + prefetch_elems);
 }

@@ -98,7 +98,9 @@ struct FusedArgs {
     unsigned* barrier = nullptr;        // barrier_words(grid) uints, zero-initialised once
     int bar_groups = 16;                // CTAs per first-level barrier counter
     unsigned long long* trace = nullptr;  // optional: TRACE_SLOTS %globaltimer stamps per CTA
+    long long* dbg = nullptr;             // optional: DBG_SLOTS (event, clock64) pairs per CTA
 };
+constexpr int DBG_SLOTS = 64;
 constexpr int TRACE_SLOTS = 8;  // entry, A done, barrier 1, B done, barrier 2, C1 done, barrier 3, end
 inline size_t barrier_words(int grid, int group) { return 64 + 32 * (size_t)((grid + group - 1) / group); }
 size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems);
