@@ -722,34 +722,70 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
         h2d(dshape.get(), shape, sizeof(int64_t) * d, s);
         check_range(didx, d, q, dshape.get(), flag.get(), s);
         if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: index out of range");
-        if ((flags & CPHIFI_OBS_REJECT_DUPLICATES) && q > 1) {
-            std::vector<int64_t> stride(d);
-            int64_t st = 1;
-            for (int m = 0; m < d; ++m) { stride[m] = st; st *= shape[m]; }
-            h2d(dshape.get(), stride.data(), sizeof(int64_t) * d, s);
-            DevBuf<uint64_t> lin(q), lin2(q);
-            linear_index(didx, d, q, dshape.get(), lin.get(), s);
-            const size_t tb = radix_sort_keys64_bytes(q);
-            DevBuf<unsigned char> tmp(tb);
-            radix_sort_keys64(tmp.get(), tb, lin.get(), lin2.get(), q, s);
-            adjacent_equal(lin2.get(), q, flag.get(), s);
-            if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: duplicate index");
-        }
-        // stable sort by i_k -> permutation
+        // Plan order: lexicographic in (i_k, other modes ascending).  For k = 0 this is the storage
+        // order of the reference's std::set of multi-indices (observations.hpp:27-41), so each row's
+        // observations are summed in the reference's order; the first other mode forms runs that the
+        // operator kernel hoists (k_fused.cu).  A multi-index wider than 63 bits falls back to a
+        // stable i_k-only order.
+        unsigned __int128 prod = 1;
+        for (int m = 0; m < d; ++m) prod *= (unsigned __int128)shape[m];
+        const bool lex = prod <= ((unsigned __int128)1 << 63);
         const int64_t lo = q * shard / shards, hi = q * (shard + 1) / shards;
         const int64_t ql = hi - lo;
         o->q_local = ql;
-        DevBuf<int32_t> keys_out(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
-            perm_out(std::max<int64_t>(q, 1));
-        if (q > 0) {
-            int bits = 1;
-            while ((int64_t(1) << bits) < nk) ++bits;
-            iota32(perm_in.get(), q, s);
-            const size_t tb = radix_sort_pairs_bytes(q, bits);
-            DevBuf<unsigned char> tmp(tb);
-            radix_sort_pairs(tmp.get(), tb, didx + (int64_t)k * q, keys_out.get(), perm_in.get(), perm_out.get(), q,
-                             bits, s);
+        o->lex = lex;
+        const int64_t qa = std::max<int64_t>(q, 1);
+        DevBuf<int32_t> perm_in(qa), perm_out(qa);
+        DevBuf<uint64_t> key(lex ? qa : 1), key_s(lex ? qa : 1);
+        DevBuf<int32_t> keys_out(lex ? 1 : qa);
+        uint64_t span = 1;
+        if (lex) {
+            std::vector<int64_t> stride(d);
+            for (int m = d - 1; m >= 0; --m) {
+                if (m == k) continue;
+                stride[m] = (int64_t)span;
+                span *= (uint64_t)shape[m];
+            }
+            stride[k] = (int64_t)span;
+            h2d(dshape.get(), stride.data(), sizeof(int64_t) * d, s);
+            if (q > 0) {
+                int bits = 1;
+                while (bits < 64 && ((unsigned __int128)1 << bits) < prod) ++bits;
+                linear_index(didx, d, q, dshape.get(), key.get(), s);
+                iota32(perm_in.get(), q, s);
+                const size_t tb = radix_sort_pairs64_bytes(q, bits);
+                DevBuf<unsigned char> tmp(tb);
+                radix_sort_pairs64(tmp.get(), tb, key.get(), key_s.get(), perm_in.get(), perm_out.get(), q, bits, s);
+            }
+            if ((flags & CPHIFI_OBS_REJECT_DUPLICATES) && q > 1) {
+                adjacent_equal(key_s.get(), q, flag.get(), s);
+                if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: duplicate index");
+            }
+        } else {
+            if ((flags & CPHIFI_OBS_REJECT_DUPLICATES) && q > 1) {
+                std::vector<int64_t> stride(d);
+                int64_t st = 1;
+                for (int m = 0; m < d; ++m) { stride[m] = st; st *= shape[m]; }
+                h2d(dshape.get(), stride.data(), sizeof(int64_t) * d, s);
+                DevBuf<uint64_t> lin(q), lin2(q);
+                linear_index(didx, d, q, dshape.get(), lin.get(), s);
+                const size_t tb = radix_sort_keys64_bytes(q);
+                DevBuf<unsigned char> tmp(tb);
+                radix_sort_keys64(tmp.get(), tb, lin.get(), lin2.get(), q, s);
+                adjacent_equal(lin2.get(), q, flag.get(), s);
+                if (read_flag(ctx, flag.get())) throw_invalid("ObservationSet: duplicate index");
+            }
+            if (q > 0) {  // stable sort by i_k -> permutation
+                int bits = 1;
+                while ((int64_t(1) << bits) < nk) ++bits;
+                iota32(perm_in.get(), q, s);
+                const size_t tb = radix_sort_pairs_bytes(q, bits);
+                DevBuf<unsigned char> tmp(tb);
+                radix_sort_pairs(tmp.get(), tb, didx + (int64_t)k * q, keys_out.get(), perm_in.get(), perm_out.get(),
+                                 q, bits, s);
+            }
         }
+        key = DevBuf<uint64_t>();
         o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * ql, 1));
         o->values.alloc(std::max<int64_t>(ql, 1));
         int mm = 0;
@@ -760,7 +796,8 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
         }
         gather_f64(dval, perm_out.get(), lo, ql, o->values.get(), s);
         o->row_ptr.alloc(nk + 1);
-        csr_from_sorted(keys_out.get() + lo, ql, nk, o->row_ptr.get(), s);
+        if (lex) csr_from_sorted64(key_s.get() + lo, ql, nk, span, o->row_ptr.get(), s);
+        else csr_from_sorted(keys_out.get() + lo, ql, nk, o->row_ptr.get(), s);
         CPHIFI_CUDA(cudaStreamSynchronize(s));
         *out = hold.release();
     });
@@ -833,10 +870,10 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // fused-kernel launch shape: all CTAs co-resident (cooperative launch)
         p->small_n = n <= 512 && n * r <= 8192;
         p->prefetch = p->small_n;
-        p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;
+        p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;  // keeps two CTAs per SM
         if (const char* e = std::getenv("CPHIFI_SMEM_FACTORS")) p->smem_factors = p->smem_factors && std::atoi(e) != 0;
         const int64_t crows = (n + ctx->num_sms - 1) / ctx->num_sms;  // >= rows per CTA in PH_C2
-        const int64_t pref = p->prefetch ? n * r + (fused_maxloc() + crows) * n : 0;
+        const int64_t pref = p->prefetch ? (n | 1) * r + (fused_maxloc() + crows) * n : 0;
         p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
         const int cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
         PartitionPlan plan;

@@ -117,6 +117,7 @@ struct cphifi_obs_s {
     int64_t q_total = 0;  // all shards
     int64_t q_local = 0;  // this shard
     double density = 0.0; // q_total / prod(shape)  (observations.hpp:58-60)
+    bool lex = false;     // plan order is lexicographic (i_k, other modes ascending)
     cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
     cphifi::DevBuf<int32_t> idx_o;    // (d-1) x q_local, other modes ascending, sorted by i_k
     cphifi::DevBuf<double> values;    // q_local, sorted

@@ -36,6 +36,7 @@ namespace {
 constexpr int FT = 512;    // threads per CTA
 constexpr int TILE = 1024; // observations per staged tile
 constexpr int MAXLOC = 4;  // PH_AL: max rows one CTA computes Xhat for
+constexpr int MAX_SMEM = 226 * 1024;  // dynamic shared memory cap (227 KB opt-in minus static)
 constexpr int UNR = 2;     // rounds in flight per group in the fast path
 
 __device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
@@ -176,8 +177,11 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     double* sw = xloc + MAXLOC * RP;      // 2 x TILE weights (RHS mode)
     int32_t* sidx = reinterpret_cast<int32_t*>(sw + 2 * TILE);       // 2 x DO x TILE
     double* sfac = reinterpret_cast<double*>(sidx + 2 * DO * TILE);   // staged factors (SMEMF)
-    double* xs = sfac + (SMEMF ? a.fac_total : 0);                   // X, n x r (prefetch)
-    double* kcs = xs + (a.prefetch ? a.n * a.r : 0);                 // K columns (prefetch)
+    // X staged column-major with an odd column stride: the j-fastest lanes of row_dot and the
+    // element-order staging writes both hit distinct banks
+    const int64_t ldx = a.n | 1;
+    double* xs = sfac + (SMEMF ? a.fac_total : 0);                   // X, ldx x r (prefetch)
+    double* kcs = xs + (a.prefetch ? ldx * a.r : 0);                 // K columns (prefetch)
     __shared__ int64_t s_rows[2];
     __shared__ int s_last;
 
@@ -239,7 +243,8 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     }
     const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
     if (pf) {
-        for (int64_t e = threadIdx.x; e < a.n * a.r; e += FT) cp_async8(xs + e, a.x + e);
+        const int nn = (int)a.n, nr = (int)(a.n * a.r), odd = (int)(ldx - a.n);  // small n: n * r <= 8192
+        for (int e = threadIdx.x; e < nr; e += FT) cp_async8(xs + e + odd * (e / nn), a.x + e);
         for (int rr = 0; rr < nal; ++rr)
             for (int64_t k = threadIdx.x; k < a.n; k += FT) cp_async8(kcs + rr * a.n + k, a.kmat + (first_row + rr) * a.n + k);
         if (a.phases & PH_C2)
@@ -254,16 +259,19 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
         cp_commit();
     }
     const double* fac = SMEMF ? sfac : a.fac;
+    dbg_mark(8);  // prefetch issued
 
     // ---- phase A: Xhat rows -----------------------------------------------------------------
     if (a.phases & PH_AL) {  // only the rows this CTA's observations touch, from shared memory
         if (ntiles > 1) cp_wait<1>();
         else cp_wait<0>();
         __syncthreads();
+        dbg_mark(9);  // prefetch landed
         for (int rr = 0; rr < nal; ++rr) {
-            row_dot<RP>(a, kcs + rr * a.n, xs, 1, a.n, red, xloc + rr * RP);
+            row_dot<RP>(a, kcs + rr * a.n, xs, 1, ldx, red, xloc + rr * RP);
             if (threadIdx.x < RP) a.xhat_rm[(first_row + rr) * RP + threadIdx.x] = xloc[rr * RP + threadIdx.x];
         }
+        dbg_mark(10);
         stamp(a, 1);
     } else if (a.phases & PH_A) {  // rows distributed over CTAs, then a grid barrier
         for (int64_t i = i0; i < i1; ++i) {
@@ -358,6 +366,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             const int64_t t1 = min(cb, t0 + TILE);
             const int32_t* ti = sidx + buf * DO * TILE;
             const double* tw = sw + buf * TILE;
+            // z = the Khatri-Rao row, modes ascending (observations.hpp:150-156)
             auto build_z = [&](int o, double (&z)[VPL]) {
                 ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
 #pragma unroll
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             row_dot<RP>(a, kc, a.yhat_c2, RP, 1, red, rowbuf);
             dbg_mark(6);
             if (empty) {
-                row_dot<RP>(a, kc, pf ? xs : a.x, 1, a.n, red, rowbuf + RP);
+                row_dot<RP>(a, kc, pf ? xs : a.x, 1, pf ? ldx : a.n, red, rowbuf + RP);
             } else {
                 if (threadIdx.x < RP) rowbuf[RP + threadIdx.x] = xr;
                 __syncthreads();
@@ -466,7 +475,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             if (threadIdx.x < a.r) {
                 const int64_t e = i + a.n * threadIdx.x;
                 const double out = rowbuf[threadIdx.x] + a.lambda * rowbuf[RP + threadIdx.x];
-                a.y[e] = out + a.rho * (pf ? xs[e] : a.x[e]);
+                a.y[e] = out + a.rho * (pf ? xs[i + ldx * threadIdx.x] : a.x[e]);
             }
             __syncthreads();
         }
@@ -482,7 +491,7 @@ void launch_fused_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     auto kern = fused_matvec_kernel<RP, DO, SMEMF>;
     static bool attr = false;
     if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM));
         attr = true;
     }
     void* args[] = {const_cast<FusedArgs*>(&a)};
@@ -505,7 +514,7 @@ template <int RP, int DO, bool SMEMF>
 int occupancy_t(size_t smem) {
     int blocks = 0;
     CPHIFI_CUDA(cudaFuncSetAttribute(fused_matvec_kernel<RP, DO, SMEMF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     220 * 1024));
+                                     MAX_SMEM));
     CPHIFI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fused_matvec_kernel<RP, DO, SMEMF>, FT, smem));
     return blocks;
 }

@@ -184,6 +184,20 @@ __global__ void csr_kernel(const int32_t* keys, int64_t q, int64_t n, int64_t* r
     row_ptr[i] = lo;
 }
 
+// row_ptr[i] = lower_bound(keys, i * span) for i in [0, n] (keys = lexicographic u64 keys with
+// the row index i_k as the most significant digit, span = product of the other mode sizes)
+__global__ void csr64_kernel(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, int64_t* row_ptr) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const uint64_t key = (uint64_t)i * span;
+    int64_t lo = 0, hi = q;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    row_ptr[i] = lo;
+}
+
 inline unsigned grid_for(int64_t n, int t, int cap = 8192) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + t - 1) / t, cap));
 }
@@ -252,6 +266,11 @@ void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr
     CPHIFI_CHECK_LAUNCH();
 }
 
+void csr_from_sorted64(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, int64_t* row_ptr, cudaStream_t s) {
+    csr64_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(keys, q, n, span, row_ptr);
+    CPHIFI_CHECK_LAUNCH();
+}
+
 size_t radix_sort_pairs_bytes(int64_t q, int bits) {
     size_t bytes = 0;
     CPHIFI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
@@ -260,6 +279,17 @@ size_t radix_sort_pairs_bytes(int64_t q, int bits) {
 }
 void radix_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
                       const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s) {
+    CPHIFI_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, q, 0,
+                                                bits, s));
+}
+size_t radix_sort_pairs64_bytes(int64_t q, int bits) {
+    size_t bytes = 0;
+    CPHIFI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                                (const int32_t*)nullptr, (int32_t*)nullptr, q, 0, bits));
+    return bytes;
+}
+void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
+                        const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s) {
     CPHIFI_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, q, 0,
                                                 bits, s));
 }

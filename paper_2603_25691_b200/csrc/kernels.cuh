@@ -164,6 +164,10 @@ void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr
 size_t radix_sort_pairs_bytes(int64_t q, int bits);
 void radix_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
                       const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
+void csr_from_sorted64(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, int64_t* row_ptr, cudaStream_t s);
+size_t radix_sort_pairs64_bytes(int64_t q, int bits);
+void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
+                        const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
 size_t radix_sort_keys64_bytes(int64_t q);
 void radix_sort_keys64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t q,
                        cudaStream_t s);
