@@ -138,8 +138,8 @@ def secondary(args, ctx, cp, p, c, lib, x, y, stream, flush):
     attempt("config0_aligned", lambda: bs.aligned("config0", ctx, 20, fp64))
     attempt("config2_aligned", lambda: bs.aligned("config2", ctx, 10, fp64))
     if args.large:
-        attempt("config3", lambda: bs.large("config3", ctx))
-        attempt("config4", lambda: bs.large("config4", ctx))
+        attempt("config3", lambda: bs.large("config3", ctx, fp64_tf=fp64))
+        attempt("config4", lambda: bs.large("config4", ctx, fp64_tf=fp64))
     return sec
 
 

@@ -99,8 +99,10 @@ def gram_matvec_ms(p, lib, x, y, stream, flush, steps=50):
     return float(np.median(ts))
 
 
-def large(which, ctx, iters=3, solve=True):
-    """Configs 3/4 at full size: per-observation operator, row-Gram operator, PCG (row-Gram)."""
+def large(which, ctx, iters=3, solve=True, fp64_tf=None):
+    """Configs 3/4 at full size: per-observation operator, row-Gram operator, PCG (row-Gram).
+    Config 4's plan coalesces repeated draws (cfg.coalesce): the streamed entries are the distinct
+    multi-indices, the algorithmic bytes / flops below stay those of the as-given q draws."""
     import torch
 
     import paper_2603_25691_b200 as cp
@@ -113,11 +115,14 @@ def large(which, ctx, iters=3, solve=True):
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
-    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),
+                                coalesce=cfg.coalesce)
     model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
     t0 = time.perf_counter()
     p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
     plan_s = time.perf_counter() - t0
+    qt, ql = ctypes.c_int64(), ctypes.c_int64()
+    _capi.check(lib.cphifi_obs_info(obs.plan(0, ctx).h, ctypes.byref(qt), ctypes.byref(ql), None))
     del idx, vals
     obs.release_inputs()
     torch.cuda.empty_cache()
@@ -149,9 +154,15 @@ def large(which, ctx, iters=3, solve=True):
     b_alg = 4 * d * q + 16 * n * n + 48 * n * r
     rp = max(4, 1 << (r - 1).bit_length())
     b_gram = 16 * n * n + 8 * n * rp * rp + 48 * n * r
-    out = {"q": q, "gen_s": gen_s, "plan_s": plan_s,
+    f_alg = (d + 2) * r * q + 4 * n * n * r
+    if fp64_tf is None:
+        fp64_tf = fp64_peaks(ctx)["dmma_tflops"]
+    t_roof = max(b_alg / (hbm * 1e9), f_alg / (fp64_tf * 1e12))
+    out = {"q": q, "gen_s": gen_s, "plan_s": plan_s, "coalesced": cfg.coalesce, "plan_entries": ql.value,
            "stream_matvec_ms": stream_ms, "stream_matvecs_per_s": 1e3 / stream_ms,
            "stream_hbm_frac_as_given": b_alg / (stream_ms / 1e3) / 1e9 / hbm,
+           "stream_roofline_frac_survey": t_roof / (stream_ms / 1e3),
+           "roofline_note": "SURVEY 8(d): t_roof = max(B_alg/HBM, F_alg/P_FP64(DMMA, measured)), as-given q",
            "gram_build_s": gram_build_s, "gram_matvec_ms": gram_ms, "gram_matvecs_per_s": 1e3 / gram_ms,
            "gram_hbm_frac_own_bytes": b_gram / (gram_ms / 1e3) / 1e9 / hbm}
     if solve:

@@ -121,6 +121,9 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count); /* eig_factorization_co
 /* ---- observations (ObservationSet, observations.hpp:18-79) ------------------------- */
 #define CPHIFI_OBS_DEVICE_INPUT 1u      /* idx / values are device pointers */
 #define CPHIFI_OBS_REJECT_DUPLICATES 2u /* reference semantics: throw on a repeated index */
+/* multiset input: merge repeated multi-indices into one plan entry carrying its multiplicity
+   (operator weight) and summed value (right-hand side); q_local then counts distinct entries */
+#define CPHIFI_OBS_COALESCE_DUPLICATES 4u
 /* Build the observation plan for infinite mode k: q multi-indices stored as d int32
  * arrays (idx[m*q + l] = index of observation l in mode m), fp64 values.  The plan sorts
  * by i_k on device (stable), builds CSR row pointers, and keeps the contiguous

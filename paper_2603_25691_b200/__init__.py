@@ -285,10 +285,12 @@ def _factor_array(factors, skip: int):
 # ---- observations.hpp ------------------------------------------------------------------
 class ObservationSet:
     """The set Omega (observations.hpp:18-79).  Indices are held host-side as (d, q) int32;
-    device plans (sorted by i_k, CSR, sharded) are built per mode on first use.  With
-    ``multiset=True`` repeated multi-indices are summed instead of rejected."""
+    device plans (lexicographic order, CSR over i_k, sharded) are built per mode on first use.
+    With ``multiset=True`` repeated multi-indices are summed (SURVEY F3) instead of rejected;
+    ``coalesce=True`` additionally merges them in the plan into one weighted entry (same
+    operator, fewer entries streamed per application)."""
 
-    def __init__(self, shape, indices, values, multiset: bool = False):
+    def __init__(self, shape, indices, values, multiset: bool = False, coalesce: bool = False):
         self._shape = [int(s) for s in shape]
         d = len(self._shape)
         vals = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
@@ -308,6 +310,7 @@ class ObservationSet:
         self._idx = np.ascontiguousarray(idx.astype(np.int32))
         self._values = vals
         self.multiset = multiset
+        self.coalesce = bool(coalesce and multiset)
         self._plans = {}
         if not multiset and vals.size > 1:
             strides = np.cumprod([1] + self._shape[:-1]).astype(np.int64)
@@ -344,7 +347,8 @@ class ObservationSet:
         if key not in self._plans:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
-            flags = 0 if self.multiset else _capi.OBS_REJECT_DUPLICATES
+            flags = (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0) if self.multiset \
+                else _capi.OBS_REJECT_DUPLICATES
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p),
                  self.num_obs(), self._idx.ctypes.data, self._values.ctypes.data, k, flags, shard, shards,
                  ctypes.byref(h))
@@ -357,8 +361,9 @@ class DeviceObservations:
     tensors or raw device pointers): multiset semantics, no host copy.  Plans are built per
     (k, shard) exactly like ObservationSet.plan."""
 
-    def __init__(self, shape, idx_ptr: int, vals_ptr: int, q: int, keepalive=()):
+    def __init__(self, shape, idx_ptr: int, vals_ptr: int, q: int, keepalive=(), coalesce: bool = False):
         self._shape = [int(s) for s in shape]
+        self.coalesce = bool(coalesce)
         self._idx_ptr = int(idx_ptr)
         self._vals_ptr = int(vals_ptr)
         self._q = int(q)
@@ -384,7 +389,8 @@ class DeviceObservations:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p), self._q,
-                 ctypes.c_void_p(self._idx_ptr), ctypes.c_void_p(self._vals_ptr), k, _capi.OBS_DEVICE_INPUT,
+                 ctypes.c_void_p(self._idx_ptr), ctypes.c_void_p(self._vals_ptr), k,
+                 _capi.OBS_DEVICE_INPUT | (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0),
                  shard, shards, ctypes.byref(h))
             self._plans[key] = _Handle(h, "cphifi_obs_destroy", deps=(ctx,))
         return self._plans[key]

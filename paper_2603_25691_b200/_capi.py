@@ -20,6 +20,7 @@ c_void_pp = ctypes.POINTER(ctypes.c_void_p)
 OK, INVALID_ARGUMENT, RUNTIME_ERROR, CUDA_ERROR, NCCL_ERROR = 0, 1, 2, 3, 4
 OBS_DEVICE_INPUT = 1
 OBS_REJECT_DUPLICATES = 2
+OBS_COALESCE_DUPLICATES = 4
 TENSOR_DEVICE_INPUT = 1
 
 

@@ -154,6 +154,7 @@ class DeviceUnalignedConfig:
     zipf_mode: int
     zipf_s: float
     noise_std: float = 0.1
+    coalesce: bool = False  # merge repeated draws in the plan (CPHIFI_OBS_COALESCE_DUPLICATES)
 
 
 def config3() -> DeviceUnalignedConfig:
@@ -182,7 +183,7 @@ def config4() -> DeviceUnalignedConfig:
     others = [_normal_matrix(rng, 512, r) for _ in range(2)]
     a1 = np.asfortranarray(kernel_matrix(pts, "gaussian", 0.02) @ w)
     return DeviceUnalignedConfig("config4", [n, 512, 512], r, 1e-5, 1e-6, 1e-8, 500, pts, "gaussian", 0.02,
-                                 [a1] + others, w, 1_000_000_000, 4, 0, 1.1)
+                                 [a1] + others, w, 1_000_000_000, 4, 0, 1.1, coalesce=True)
 
 
 def generate_device(cfg: DeviceUnalignedConfig, ctx, q: int | None = None):

@@ -232,6 +232,7 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     a.fac = p->fac.get();
     for (int m = 0; m < o->d - 1; ++m) a.fac_off[m] = p->fac_off[m];
     a.fac_total = (int64_t)p->fac.n;
+    a.mult = o->coalesced ? o->mult.get() : nullptr;
     a.kmat = p->mode->kernel.get();
     a.xhat_rm = p->xhat_rm.get();
     a.yhat_rm = p->yhat_rm.get();
@@ -274,6 +275,7 @@ void ensure_gram(cphifi_unaligned p) {
     g.idx = o->idx_o.get();
     g.fac = p->fac.get();
     for (int m = 0; m < o->d - 1; ++m) g.fac_off[m] = p->fac_off[m];
+    g.mult = o->coalesced ? o->mult.get() : nullptr;
     g.cta_beg = p->cta_beg.get();
     g.cta_rows = p->cta_rows.get();
     g.row_first_cta = p->row_first_cta.get();
@@ -738,9 +740,11 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
         DevBuf<int32_t> perm_in(qa), perm_out(qa);
         DevBuf<uint64_t> key(lex ? qa : 1), key_s(lex ? qa : 1);
         DevBuf<int32_t> keys_out(lex ? 1 : qa);
+        const bool coalesce = (flags & CPHIFI_OBS_COALESCE_DUPLICATES) != 0;
+        if (coalesce && !lex) throw_invalid("ObservationSet: coalescing needs a multi-index of at most 63 bits");
         uint64_t span = 1;
+        std::vector<int64_t> stride(d);
         if (lex) {
-            std::vector<int64_t> stride(d);
             for (int m = d - 1; m >= 0; --m) {
                 if (m == k) continue;
                 stride[m] = (int64_t)span;
@@ -786,6 +790,33 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
             }
         }
         key = DevBuf<uint64_t>();
+        if (coalesce) {
+            // merge repeated multi-indices of this shard: one entry per distinct key, carrying its
+            // multiplicity (operator weight) and summed value (RHS); indices decoded from the key
+            DevBuf<double> vs(std::max<int64_t>(ql, 1)), vsum(std::max<int64_t>(ql, 1));
+            DevBuf<int32_t> cnt(std::max<int64_t>(ql, 1));
+            DevBuf<uint64_t> ukey(std::max<int64_t>(ql, 1));
+            gather_f64(dval, perm_out.get(), lo, ql, vs.get(), s);
+            const int64_t nu = coalesce_sorted(key_s.get() + lo, vs.get(), ql, ukey.get(), cnt.get(), vsum.get(), s);
+            o->q_local = nu;
+            o->coalesced = true;
+            DevBuf<int64_t> dstride(d);
+            h2d(dstride.get(), stride.data(), sizeof(int64_t) * d, s);
+            h2d(dshape.get(), shape, sizeof(int64_t) * d, s);
+            o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * nu, 1));
+            decode_keys(ukey.get(), nu, d, k, dstride.get(), dshape.get(), o->idx_o.get(), s);
+            o->values.alloc(std::max<int64_t>(nu, 1));
+            o->mult.alloc(std::max<int64_t>(nu, 1));
+            if (nu > 0) {
+                CPHIFI_CUDA(cudaMemcpyAsync(o->values.get(), vsum.get(), sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
+                CPHIFI_CUDA(cudaMemcpyAsync(o->mult.get(), cnt.get(), sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice, s));
+            }
+            o->row_ptr.alloc(nk + 1);
+            csr_from_sorted64(ukey.get(), nu, nk, span, o->row_ptr.get(), s);
+            CPHIFI_CUDA(cudaStreamSynchronize(s));
+            *out = hold.release();
+            return;
+        }
         o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * ql, 1));
         o->values.alloc(std::max<int64_t>(ql, 1));
         int mm = 0;

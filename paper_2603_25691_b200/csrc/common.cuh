@@ -120,7 +120,9 @@ struct cphifi_obs_s {
     bool lex = false;     // plan order is lexicographic (i_k, other modes ascending)
     cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
     cphifi::DevBuf<int32_t> idx_o;    // (d-1) x q_local, other modes ascending, sorted by i_k
-    cphifi::DevBuf<double> values;    // q_local, sorted
+    cphifi::DevBuf<double> values;    // q_local, sorted (coalesced: summed over duplicates)
+    cphifi::DevBuf<int32_t> mult;     // q_local multiplicities (coalesced plans only)
+    bool coalesced = false;
 };
 
 struct cphifi_unaligned_s {

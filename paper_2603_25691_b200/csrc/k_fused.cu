@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - lane % G));
     const bool dot = a.weights == nullptr;
+    const bool mult = dot && a.mult != nullptr;
     const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];  // row-aligned partition (host plan)
     const bool has_obs = (a.phases & PH_B) && ca < cb;
     const int ntiles = has_obs && !a.gram ? (int)((cb - ca + TILE - 1) / TILE) : 0;
@@ -205,6 +206,9 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                 cp_async4(sidx + (buf * DO + m) * TILE + o, a.idx + (int64_t)m * a.q + t0 + o);
         if (!dot)
             for (int o = threadIdx.x; o < cnt; o += FT) cp_async8(sw + buf * TILE + o, a.weights + t0 + o);
+        else if (mult)  // the weight buffer is free in dot mode
+            for (int o = threadIdx.x; o < cnt; o += FT)
+                cp_async4(reinterpret_cast<int32_t*>(sw + buf * TILE) + o, a.mult + t0 + o);
     };
 
     stamp(a, 0);
@@ -366,6 +370,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             const int64_t t1 = min(cb, t0 + TILE);
             const int32_t* ti = sidx + buf * DO * TILE;
             const double* tw = sw + buf * TILE;
+            const int32_t* tm = reinterpret_cast<const int32_t*>(tw);  // multiplicities (dot mode)
             // z = the Khatri-Rao row, modes ascending (observations.hpp:150-156)
             auto build_z = [&](int o, double (&z)[VPL]) {
                 ldv<VPL>(z, fac + a.fac_off[0] + (int64_t)ti[o] * RP + jb);
@@ -403,6 +408,10 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                             s0 += __shfl_xor_sync(gmask, s0, off, G);
                             s1 += __shfl_xor_sync(gmask, s1, off, G);
                         }
+                        if (mult) {  // coalesced plan: entry weight = multiplicity
+                            s0 *= (double)tm[o];
+                            s1 *= (double)tm[o + NG];
+                        }
                     } else {
                         s0 = tw[o];
                         s1 = tw[o + NG];
@@ -420,6 +429,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                         s0 = partial_dot(z0);
 #pragma unroll
                         for (int off = G / 2; off > 0; off >>= 1) s0 += __shfl_xor_sync(gmask, s0, off, G);
+                        if (mult) s0 *= (double)tm[o];
                     } else {
                         s0 = tw[o];
                     }

@@ -6,7 +6,8 @@
 //     G_i = sum_{l: i_k(l)=i} z_l z_l'      (rp x rp, symmetric, independent of X)
 // — an exact algebraic identity.  G is built ONCE per subproblem (O(q rp^2) flops, one pass over
 // the observations) and every operator application then costs O(n rp^2) instead of O(q d r).
-// Duplicated multi-indices (multiset configs) are handled for free: they add z z' twice.
+// Duplicated multi-indices (multiset configs) add z z' once per copy, or once with weight
+// mult_l in a coalesced plan.
 //
 // gram_build_kernel: CTA c walks the same row-aligned observation ranges as the fused kernel,
 //   building z for batches of GB observations of one row in shared memory and accumulating
@@ -35,6 +36,7 @@ __global__ void __launch_bounds__(GT) gram_build_kernel(const GramArgs a) {
     constexpr int NACT = NB * NB;                          // active threads (<= GT)
     static_assert(NACT <= GT, "G tile does not fit the CTA");
     __shared__ __align__(16) double zs[GB][RP + 2];
+    __shared__ double ws[GB];  // entry weights (coalesced plan multiplicities)
     __shared__ int s_last;
     const int c = blockIdx.x;
     const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];
@@ -108,14 +110,17 @@ __global__ void __launch_bounds__(GT) gram_build_kernel(const GramArgs a) {
                 for (int m = 1; m < DO; ++m) z *= a.fac[a.fac_off[m] + (int64_t)__ldg(a.idx + (int64_t)m * a.q + l) * RP + j];
             }
             zs[t][j] = z;
+            if (j == 0) ws[t] = (a.mult && t < cnt) ? (double)__ldg(a.mult + pos + t) : 1.0;
         }
         __syncthreads();
         if (act) {
             for (int t = 0; t < cnt; ++t) {
                 double za[BLK], zb[BLK];
 #pragma unroll
+                const double w = ws[t];
+#pragma unroll
                 for (int x = 0; x < BLK; ++x) {
-                    za[x] = zs[t][ba + x];
+                    za[x] = zs[t][ba + x] * w;
                     zb[x] = zs[t][bb + x];
                 }
 #pragma unroll

@@ -198,6 +198,19 @@ __global__ void csr64_kernel(const uint64_t* keys, int64_t q, int64_t n, uint64_
     row_ptr[i] = lo;
 }
 
+__global__ void decode_keys_kernel(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride,
+                                   const int64_t* shape, int32_t* idx_o) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nu; l += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[l];
+        int mm = 0;
+        for (int m = 0; m < d; ++m) {
+            if (m == k) continue;
+            idx_o[(int64_t)mm * nu + l] = (int32_t)((key / (uint64_t)stride[m]) % (uint64_t)shape[m]);
+            ++mm;
+        }
+    }
+}
+
 inline unsigned grid_for(int64_t n, int t, int cap = 8192) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + t - 1) / t, cap));
 }
@@ -292,6 +305,28 @@ void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, 
                         const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s) {
     CPHIFI_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, q, 0,
                                                 bits, s));
+}
+int64_t coalesce_sorted(const uint64_t* keys, const double* vals, int64_t q, uint64_t* ukeys, int32_t* counts,
+                        double* vsum, cudaStream_t s) {
+    if (q == 0) return 0;
+    DevBuf<int64_t> nrun(2);
+    size_t b1 = 0, b2 = 0;
+    CPHIFI_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b1, keys, ukeys, counts, nrun.get(), q, s));
+    CPHIFI_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, b2, keys, ukeys, vals, vsum, nrun.get() + 1, cub::Sum(), q, s));
+    DevBuf<unsigned char> tmp(std::max(b1, b2));
+    CPHIFI_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), b1, keys, ukeys, counts, nrun.get(), q, s));
+    CPHIFI_CUDA(cub::DeviceReduce::ReduceByKey(tmp.get(), b2, keys, ukeys, vals, vsum, nrun.get() + 1, cub::Sum(), q, s));
+    int64_t h[2] = {0, 0};
+    CPHIFI_CUDA(cudaMemcpyAsync(h, nrun.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    CPHIFI_CUDA(cudaStreamSynchronize(s));
+    if (h[0] != h[1]) throw_runtime("ObservationSet: coalescing run counts disagree");
+    return h[0];
+}
+void decode_keys(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride_dev, const int64_t* shape_dev,
+                 int32_t* idx_o, cudaStream_t s) {
+    if (nu == 0) return;
+    decode_keys_kernel<<<grid_for(nu, 256), 256, 0, s>>>(keys, nu, d, k, stride_dev, shape_dev, idx_o);
+    CPHIFI_CHECK_LAUNCH();
 }
 size_t radix_sort_keys64_bytes(int64_t q) {
     size_t bytes = 0;

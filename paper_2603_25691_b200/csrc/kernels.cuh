@@ -78,6 +78,7 @@ struct FusedArgs {
     int64_t fac_off[8] = {0};
     int64_t fac_total = 0;              // doubles in fac
     const double* weights = nullptr;    // non-null: s_l = weights[l] (RHS B), else Xhat . z_l
+    const int32_t* mult = nullptr;      // coalesced plan: operator weight of entry l (dot mode)
     const double* kmat = nullptr;       // n x n column-major, symmetric
     const double* x = nullptr;          // n x r column-major
     double* y = nullptr;                // n x r column-major
@@ -116,6 +117,7 @@ struct GramArgs {
     const int32_t* idx = nullptr;
     const double* fac = nullptr;
     int64_t fac_off[8] = {0};
+    const int32_t* mult = nullptr;  // coalesced plan: G_i = sum_l mult_l z_l z_l'
     const int64_t* cta_beg = nullptr;
     const int64_t* cta_rows = nullptr;
     const int32_t* row_first_cta = nullptr;
@@ -168,6 +170,12 @@ void csr_from_sorted64(const uint64_t* keys, int64_t q, int64_t n, uint64_t span
 size_t radix_sort_pairs64_bytes(int64_t q, int bits);
 void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
                         const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
+// sorted keys -> distinct keys, run lengths and per-run value sums; returns the run count
+int64_t coalesce_sorted(const uint64_t* keys, const double* vals, int64_t q, uint64_t* ukeys, int32_t* counts,
+                        double* vsum, cudaStream_t s);
+// distinct lexicographic keys -> other-mode indices ((d-1) x nu, modes ascending)
+void decode_keys(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride_dev, const int64_t* shape_dev,
+                 int32_t* idx_o, cudaStream_t s);
 size_t radix_sort_keys64_bytes(int64_t q);
 void radix_sort_keys64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t q,
                        cudaStream_t s);

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--trace", type=int, default=1)
     ap.add_argument("--solve", type=int, default=0)
+    ap.add_argument("--coalesce", type=int, default=0)
     args = ap.parse_args()
     cfg = configs.config3() if args.config == 3 else configs.config4()
     q = args.q or cfg.q
@@ -40,11 +41,16 @@ def main():
     torch.cuda.synchronize()
     out["gen_s"] = time.perf_counter() - t0
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
-    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),
+                                coalesce=bool(args.coalesce))
     model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
     t0 = time.perf_counter()
     p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
     out["plan_s"] = time.perf_counter() - t0
+    qt, ql = ctypes.c_int64(), ctypes.c_int64()
+    _capi.check(lib.cphifi_obs_info(obs.plan(0, ctx).h, ctypes.byref(qt), ctypes.byref(ql), None))
+    out["coalesce"] = bool(args.coalesce)
+    out["plan_entries"] = ql.value
     del idx, vals
     obs.release_inputs()
     torch.cuda.empty_cache()

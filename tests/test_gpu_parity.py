@@ -366,8 +366,9 @@ def test_sharded_plans_sum_to_full(cp):
 
 
 # ---- configs 3 / 4 structure (device-generated multiset observations), reduced q --------------
-@pytest.mark.parametrize("which,q", [("config3", 2_000_000), ("config4", 3_000_000)])
-def test_large_config_structure_vs_oracle(cp, which, q):
+@pytest.mark.parametrize("which,q,coalesce", [("config3", 2_000_000, False), ("config4", 3_000_000, False),
+                                              ("config4", 3_000_000, True)])
+def test_large_config_structure_vs_oracle(cp, which, q, coalesce):
     """Full-size modes, factors and kernels of configs 3/4 with a reduced number of draws:
     device generation -> device sort/CSR plan (multiset) -> operator, against the oracle's
     streaming restatement on the same draws (copied back)."""
@@ -381,7 +382,8 @@ def test_large_config_structure_vs_oracle(cp, which, q):
     assert hidx.min() >= 0 and all(hidx[m].max() < cfg.shape[m] for m in range(len(cfg.shape)))
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
     kern = mode.kernel()
-    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals))
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),
+                                coalesce=coalesce)
     model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
     p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
     b_o = orc.sampled_mttkrp_stream(cfg.shape, 0, hidx, hvals, model.factors, n)
@@ -393,3 +395,84 @@ def test_large_config_structure_vs_oracle(cp, which, q):
     if cfg.zipf_mode == 0:  # Zipf head: row 0 carries ~16 % of the draws
         frac0 = float((hidx[0] == 0).mean())
         assert 0.14 < frac0 < 0.18
+
+
+# ---- coalesced multiset plans (CPHIFI_OBS_COALESCE_DUPLICATES) ---------------------------------
+def _obs_q_local(cp, obs, k, ctx):
+    import ctypes
+    from paper_2603_25691_b200 import _capi
+    qt, ql = ctypes.c_int64(), ctypes.c_int64()
+    _capi.check(_capi.load().cphifi_obs_info(obs.plan(k, ctx).h, ctypes.byref(qt), ctypes.byref(ql), None))
+    return qt.value, ql.value
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_coalesced_multiset_vs_oracle(cp, k):
+    """Heavy duplication (q draws over few cells): the coalesced plan (one entry per distinct
+    multi-index, weight = multiplicity, value = summed values) gives the same operator, RHS,
+    row-Gram form and PCG solve as the oracle streaming every raw draw.  Relative 1e-12."""
+    g = cp.Mt19937_64(123 + k)
+    shape = [20, 6, 5]
+    r = 4
+    factors = ri.random_model(shape, r, g)
+    rs = np.random.default_rng(11 + k)
+    q = 5000
+    idx = np.stack([rs.integers(0, s, q) for s in shape]).astype(np.int32)
+    idx[k][idx[k] == 3] = 4  # an empty row of the infinite mode
+    vals = rs.normal(size=q)
+    n = shape[k]
+    pts = np.linspace(0, 1, n)
+    mode = cp.RkhsMode(pts, 0.2, 1e-2)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    raw = cp.ObservationSet(shape, idx, vals, multiset=True)
+    co = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=True)
+    ctx = cp.default_context()
+    lin = np.ravel_multi_index(tuple(idx.astype(np.int64)), shape)
+    assert _obs_q_local(cp, co, k, ctx) == (q, np.unique(lin).size)
+    assert _obs_q_local(cp, raw, k, ctx) == (q, q)
+    model = cp.KruskalModel(factors)
+    pc = cp.make_unaligned_subproblem(co, model, k, mode, 1e-6)
+    pr = cp.make_unaligned_subproblem(raw, model, k, mode, 1e-6)
+    sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, k, kern, 1e-2, 1e-6)
+    assert ri.rel(pc.b, sub.b) < 1e-12
+    x = ri.random_matrix(g, n * r, 1).reshape(-1)
+    y_o = orc.unaligned_matvec(sub, x)
+    assert ri.rel(cp.unaligned_matvec(pc, x), y_o) < 1e-12
+    xhat = ri.random_matrix(g, n, r)
+    assert ri.rel(pc.scatter_gather(xhat), pr.scatter_gather(xhat)) < 1e-12
+    assert pc.set_operator("gram") == "gram"
+    assert ri.rel(cp.unaligned_matvec(pc, x), y_o) < 1e-12
+    pc.set_operator("stream")
+    ev = orc.sym_eig(sub.v)
+    pc.set_v_eig(ev.u, ev.d)
+    rep_c, rep_o = cp.SolveReport(), orc.SolveReport()
+    w_c = cp.solve_unaligned_pcg(pc, cp.PcgConfig(1e-10, 300), rep_c)
+    w_o = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-10, 300), ek, ev, report=rep_o)
+    assert abs(rep_c.iterations - rep_o.iterations) <= 1 and rep_c.relative_residual <= 1e-10
+    assert ri.rel(w_c, w_o) < 1e-6
+
+
+def test_coalesced_shards_sum_to_full(cp):
+    """Shards of a coalesced plan split the sorted draws (a duplicate group may straddle two
+    shards, each keeping part of its multiplicity); the partials still sum to the full Yhat."""
+    inst = ri.Inst([30, 5, 4], 3, 100, 0, 0.5, 0.1, 1e-6, 41)  # factors / kernel only
+    rs = np.random.default_rng(2)
+    idx = np.stack([rs.integers(0, s, 3000) for s in inst.shape]).astype(np.int32)
+    vals = rs.normal(size=3000)
+    mode = cp.RkhsMode(inst.points, inst.sigma, inst.lam)
+    obs = cp.ObservationSet(inst.shape, idx, vals, multiset=True, coalesce=True)
+    raw = cp.ObservationSet(inst.shape, idx, vals, multiset=True)
+    model = cp.KruskalModel(inst.factors)
+    full = cp.make_unaligned_subproblem(raw, model, 0, mode, 1e-6)
+    xhat = ri.random_matrix(inst.rng, 30, 3)
+    yf = full.scatter_gather(xhat)
+    for shards in (2, 5):
+        acc = np.zeros_like(yf)
+        bacc = np.zeros_like(yf)
+        for s in range(shards):
+            ps = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6, s, shards)
+            acc += ps.scatter_gather(xhat)
+            bacc += ps.b
+        assert ri.rel(acc, yf) < 1e-12 and ri.rel(bacc, full.b) < 1e-12
