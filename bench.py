@@ -90,6 +90,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(kernel_substr):
+    """DRAM bytes per launch (read + write) of the named kernel from the committed `ncu --set full`
+    capture of this bench's own command (profiles/round*/ncu_full_*.json, newest round first)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_full_fused_matvec_config1.json")),
+                       reverse=True):
+        try:
+            caps = [d for d in json.load(open(path)) if kernel_substr in d["kernel"]]
+        except Exception:
+            continue
+        if caps:
+            return sum(d["traffic_bytes"] for d in caps) / len(caps), os.path.relpath(path, ROOT)
+    return None, None
+
+
 def alg_bytes_matvec(d, q, n, r):
     """unaligned matvec algorithmic bytes (int32 index stream read once,
     K read twice, six n x r fp64 vectors)."""
@@ -290,6 +305,7 @@ def main():
         fused_whole = world == 1 and n <= 512  # one cooperative kernel = the whole operator
         k1_bytes = alg_bytes_matvec(d, q, n, r) if fused_whole else alg_bytes_k1(d, q // world, n, r)
         achieved = k1_bytes / k1_launch_s / 1e9
+        traffic, traffic_src = ncu_traffic("fused_matvec_kernel")
         mv_bytes = alg_bytes_matvec(d, q, n, r)
         out = {
             "metric": "unaligned PCG matvecs/s (config 1, q=200k, r=10)",
@@ -302,7 +318,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "fused_matvec_kernel (whole operator)" if fused_whole
                          else "fused_matvec_kernel (scatter-gather + fix-up)", "achieved": achieved,
                          "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "alg_bytes_per_launch": k1_bytes,
+                         "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": k1_bytes,
                          "kernel_ms": k1_ms / args.steps},
             "matvec_hbm_frac": mv_bytes / ((total_ms / args.steps) / 1e3) / 1e9 / hbm,
             "phase_ms": {nm: v / args.steps for nm, v in
