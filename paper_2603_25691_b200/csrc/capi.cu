@@ -224,7 +224,7 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     a.n = p->n;
     a.r = p->r;
     a.rp = p->rp;
-    a.q = o->q_local;
+    a.q = o->ldq;
     a.dother = o->d - 1;
     a.phases = phases;
     a.row_ptr = o->row_ptr.get();
@@ -255,6 +255,14 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
     fused_matvec(a, p->grid, p->smem, p->smem_factors, p->obs->ctx->stream);
 }
 
+// Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
+// fused kernel restricted to PH_B.
+void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
+    a.phases = PH_B;
+    if (p->stream) stream_scatter_gather(a, p->grid, p->stream_sf, p->obs->ctx->stream);
+    else launch_fused(p, a);
+}
+
 // Row-Gram operator: build G_i = sum_l z_l z_l' once (k_gram.cu), on first use.
 void ensure_gram(cphifi_unaligned p) {
     if (p->gram.n) return;
@@ -269,7 +277,7 @@ void ensure_gram(cphifi_unaligned p) {
     GramArgs g;
     g.n = p->n;
     g.rp = p->rp;
-    g.q = o->q_local;
+    g.q = o->ldq;
     g.dother = o->d - 1;
     g.row_ptr = o->row_ptr.get();
     g.idx = o->idx_o.get();
@@ -345,7 +353,7 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     }
     xhat_gemm(p, x);
     if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), ctx->stream);
-    else launch_fused(p, fused_args(p, PH_B));
+    else launch_phase_b(p, fused_args(p, PH_B));
     allreduce_yhat(p);
     y_gemm(p, x, y);
 }
@@ -670,6 +678,9 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count) {
 }
 
 // ---- observations (observations.hpp:18-79) --------------------------------------------
+// Plan columns carry OBS_PAD slack elements: k_stream.cu's TMA bulk copies round each staged
+// column to 16-byte boundaries and may read a few elements past the last one.
+constexpr int64_t OBS_PAD = 16;
 int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, const int32_t* idx,
                       const double* values, int k, uint32_t flags, int shard, int shards, cphifi_obs* out) {
     return guard([&] {
@@ -799,14 +810,15 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
             gather_f64(dval, perm_out.get(), lo, ql, vs.get(), s);
             const int64_t nu = coalesce_sorted(key_s.get() + lo, vs.get(), ql, ukey.get(), cnt.get(), vsum.get(), s);
             o->q_local = nu;
+            o->ldq = (nu + 3) / 4 * 4;
             o->coalesced = true;
             DevBuf<int64_t> dstride(d);
             h2d(dstride.get(), stride.data(), sizeof(int64_t) * d, s);
             h2d(dshape.get(), shape, sizeof(int64_t) * d, s);
-            o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * nu, 1));
-            decode_keys(ukey.get(), nu, d, k, dstride.get(), dshape.get(), o->idx_o.get(), s);
-            o->values.alloc(std::max<int64_t>(nu, 1));
-            o->mult.alloc(std::max<int64_t>(nu, 1));
+            o->idx_o.alloc((int64_t)(d - 1) * o->ldq + OBS_PAD);
+            decode_keys(ukey.get(), nu, d, k, dstride.get(), dshape.get(), o->idx_o.get(), o->ldq, s);
+            o->values.alloc(nu + OBS_PAD);
+            o->mult.alloc(nu + OBS_PAD);
             if (nu > 0) {
                 CPHIFI_CUDA(cudaMemcpyAsync(o->values.get(), vsum.get(), sizeof(double) * nu, cudaMemcpyDeviceToDevice, s));
                 CPHIFI_CUDA(cudaMemcpyAsync(o->mult.get(), cnt.get(), sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice, s));
@@ -817,12 +829,13 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
             *out = hold.release();
             return;
         }
-        o->idx_o.alloc(std::max<int64_t>((int64_t)(d - 1) * ql, 1));
-        o->values.alloc(std::max<int64_t>(ql, 1));
+        o->ldq = (ql + 3) / 4 * 4;
+        o->idx_o.alloc((int64_t)(d - 1) * o->ldq + OBS_PAD);
+        o->values.alloc(ql + OBS_PAD);
         int mm = 0;
         for (int m = 0; m < d; ++m) {
             if (m == k) continue;
-            gather_i32(didx + (int64_t)m * q, perm_out.get(), lo, ql, o->idx_o.get() + (int64_t)mm * ql, s);
+            gather_i32(didx + (int64_t)m * q, perm_out.get(), lo, ql, o->idx_o.get() + (int64_t)mm * o->ldq, s);
             ++mm;
         }
         gather_f64(dval, perm_out.get(), lo, ql, o->values.get(), s);
@@ -905,8 +918,21 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         if (const char* e = std::getenv("CPHIFI_SMEM_FACTORS")) p->smem_factors = p->smem_factors && std::atoi(e) != 0;
         const int64_t crows = (n + ctx->num_sms - 1) / ctx->num_sms;  // >= rows per CTA in PH_C2
         const int64_t pref = p->prefetch ? (n | 1) * r + (fused_maxloc() + crows) * n : 0;
-        p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
-        const int cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        // large plans with >= 2 other modes in lexicographic order: k_stream.cu, one CTA per SM
+        p->stream = !p->small_n && obs->lex && stream_supported(p->rp, d - 1);
+        if (const char* e = std::getenv("CPHIFI_STREAM")) p->stream = p->stream && std::atoi(e) != 0;
+        int cmax;
+        if (p->stream) {
+            const int64_t sf = (int64_t)p->fac.n - obs->shape[k == 0 ? 1 : 0] * p->rp;  // all but the hoisted mode
+            const int o_aux = obs->coalesced ? 4 : 0;  // the operator launches' staged aux column
+            bool use_sf = stream_smem_bytes(p->rp, d - 1, sf, o_aux) <= stream_smem_cap();
+            if (const char* e = std::getenv("CPHIFI_STREAM_SF")) use_sf = use_sf && std::atoi(e) != 0;
+            p->stream_sf = use_sf ? sf : 0;
+            cmax = ctx->num_sms;
+        } else {
+            p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
+            cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
+        }
         PartitionPlan plan;
         {
             std::vector<int64_t> rp_host(n + 1);
@@ -945,7 +971,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // B = sampled_mttkrp(obs, zhat, k) with the observed values (observations.hpp:186-188)
         FusedArgs a = fused_args(p, PH_B);
         a.weights = obs->values.get();
-        launch_fused(p, a);
+        launch_phase_b(p, a);
         allreduce_yhat(p);
         p->b.alloc(n * r);
         rm_to_cm(yhat_result(p), n, p->rp, r, p->b.get(), s);
@@ -1053,6 +1079,7 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
             a.y = y;
             a.gram = gr;
             if (!p->small_n && gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), s);
+            else if (!p->small_n) launch_phase_b(p, a);
             else launch_fused(p, a);
             CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
@@ -1107,7 +1134,8 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
             CPHIFI_CUDA(cudaMemsetAsync(dbg.get(), 0xff, dbg.n * sizeof(long long), ctx->stream));
             a.dbg = dbg.get();
         }
-        launch_fused(p, a);
+        if (p->stream) launch_phase_b(p, a);  // no phase stamps in k_stream.cu
+        else launch_fused(p, a);
         if (want_dbg) {
             std::vector<long long> h(dbg.n);
             d2h_sync(h.data(), dbg.get(), sizeof(long long) * h.size(), ctx->stream);
@@ -1136,9 +1164,7 @@ int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, doub
         const int64_t n = p->n, r = p->r;
         h2d(p->vx.get(), xhat, sizeof(double) * n * r, ctx->stream);
         pack_rows(p->vx.get(), n, n, r, p->rp, p->xhat_rm.get(), ctx->stream);
-        FusedArgs a = fused_args(p, PH_B);
-        a.phases = PH_B;
-        launch_fused(p, a);
+        launch_phase_b(p, fused_args(p, PH_B));
         allreduce_yhat(p);
         rm_to_cm(yhat_result(p), n, p->rp, r, p->vy.get(), ctx->stream);
         d2h_sync(yhat_out, p->vy.get(), sizeof(double) * n * r, ctx->stream);

@@ -119,7 +119,8 @@ struct cphifi_obs_s {
     double density = 0.0; // q_total / prod(shape)  (observations.hpp:58-60)
     bool lex = false;     // plan order is lexicographic (i_k, other modes ascending)
     cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
-    cphifi::DevBuf<int32_t> idx_o;    // (d-1) x q_local, other modes ascending, sorted by i_k
+    cphifi::DevBuf<int32_t> idx_o;    // (d-1) columns of stride ldq, other modes ascending, sorted by i_k
+    int64_t ldq = 0;                  // idx_o column stride: q_local rounded up to a multiple of 4
     cphifi::DevBuf<double> values;    // q_local, sorted (coalesced: summed over duplicates)
     cphifi::DevBuf<int32_t> mult;     // q_local multiplicities (coalesced plans only)
     bool coalesced = false;
@@ -147,6 +148,8 @@ struct cphifi_unaligned_s {
     bool small_n = false;         // phases A and C2 inside the fused kernel
     bool local_x = false;         // every CTA spans <= MAXLOC rows: CTA-local Xhat (PH_AL)
     bool prefetch = false;        // X and K columns staged in shared memory (small n * r)
+    bool stream = false;          // phase B runs k_stream.cu (large plans) instead of k_fused.cu
+    int64_t stream_sf = 0;        // doubles of per-observation factors k_stream.cu stages in smem (0: L1)
     cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters
     // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
     int op = 0;

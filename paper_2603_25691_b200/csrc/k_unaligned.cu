@@ -199,13 +199,13 @@ __global__ void csr64_kernel(const uint64_t* keys, int64_t q, int64_t n, uint64_
 }
 
 __global__ void decode_keys_kernel(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride,
-                                   const int64_t* shape, int32_t* idx_o) {
+                                   const int64_t* shape, int32_t* idx_o, int64_t ldq) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nu; l += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t key = keys[l];
         int mm = 0;
         for (int m = 0; m < d; ++m) {
             if (m == k) continue;
-            idx_o[(int64_t)mm * nu + l] = (int32_t)((key / (uint64_t)stride[m]) % (uint64_t)shape[m]);
+            idx_o[(int64_t)mm * ldq + l] = (int32_t)((key / (uint64_t)stride[m]) % (uint64_t)shape[m]);
             ++mm;
         }
     }
@@ -323,9 +323,9 @@ int64_t coalesce_sorted(const uint64_t* keys, const double* vals, int64_t q, uin
     return h[0];
 }
 void decode_keys(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride_dev, const int64_t* shape_dev,
-                 int32_t* idx_o, cudaStream_t s) {
+                 int32_t* idx_o, int64_t ldq, cudaStream_t s) {
     if (nu == 0) return;
-    decode_keys_kernel<<<grid_for(nu, 256), 256, 0, s>>>(keys, nu, d, k, stride_dev, shape_dev, idx_o);
+    decode_keys_kernel<<<grid_for(nu, 256), 256, 0, s>>>(keys, nu, d, k, stride_dev, shape_dev, idx_o, ldq);
     CPHIFI_CHECK_LAUNCH();
 }
 size_t radix_sort_keys64_bytes(int64_t q) {

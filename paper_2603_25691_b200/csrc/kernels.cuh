@@ -69,11 +69,11 @@ void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double*
 // barrier when PH_B ran in the same launch).
 enum : unsigned { PH_A = 1u, PH_B = 2u, PH_C2 = 8u, PH_AL = 16u };
 struct FusedArgs {
-    int64_t n = 0, r = 0, rp = 0, q = 0;
+    int64_t n = 0, r = 0, rp = 0, q = 0;  // q: column stride of idx (multiple of 4)
     int dother = 0;
     unsigned phases = 0;
     const int64_t* row_ptr = nullptr;   // local CSR over sorted i_k (n + 1)
-    const int32_t* idx = nullptr;       // dother x q, other modes ascending
+    const int32_t* idx = nullptr;       // dother columns of stride q, other modes ascending
     const double* fac = nullptr;        // packed row-major rp-padded factors
     int64_t fac_off[8] = {0};
     int64_t fac_total = 0;              // doubles in fac
@@ -108,6 +108,16 @@ size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, i
 int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
 void fused_matvec(const FusedArgs& a, int grid, size_t smem, bool smemf, cudaStream_t s);
+
+// ---- large-plan scatter-gather (k_stream.cu): phase B as a streaming kernel with the first
+// other mode hoisted per run (needs >= 2 other modes and the lexicographic plan order); a normal
+// launch, one CTA per SM, TMA bulk-copied observation tiles, per-observation factors in shared
+// memory when `sf`.
+bool stream_supported(int64_t rp, int dother);
+size_t stream_smem_bytes(int64_t rp, int dother, int64_t sf_doubles, int aux_bytes);
+size_t stream_smem_cap();
+// sf_doubles > 0: that many doubles of per-observation factors are staged in shared memory
+void stream_scatter_gather(const FusedArgs& a, int grid, int64_t sf_doubles, cudaStream_t s);
 
 // ---- row-Gram operator (k_gram.cu): Yhat(i,:) = G_i Xhat(i,:), G_i = sum_l z_l z_l' ---------
 struct GramArgs {
@@ -173,9 +183,9 @@ void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, 
 // sorted keys -> distinct keys, run lengths and per-run value sums; returns the run count
 int64_t coalesce_sorted(const uint64_t* keys, const double* vals, int64_t q, uint64_t* ukeys, int32_t* counts,
                         double* vsum, cudaStream_t s);
-// distinct lexicographic keys -> other-mode indices ((d-1) x nu, modes ascending)
+// distinct lexicographic keys -> other-mode indices ((d-1) columns of stride ldq, modes ascending)
 void decode_keys(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride_dev, const int64_t* shape_dev,
-                 int32_t* idx_o, cudaStream_t s);
+                 int32_t* idx_o, int64_t ldq, cudaStream_t s);
 size_t radix_sort_keys64_bytes(int64_t q);
 void radix_sort_keys64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int64_t q,
                        cudaStream_t s);
