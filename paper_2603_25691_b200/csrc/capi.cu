@@ -111,6 +111,26 @@ void mode_eig_once(cphifi_mode m) {
     });
 }
 
+// U' for the sandwich's second phase (k_sandwich.cu), built once per installed eigenbasis
+const double* mode_ut(cphifi_mode m) {
+    std::lock_guard<std::mutex> lk(m->mu_lock);
+    if (!m->have_ut) {
+        m->ut.alloc(m->n * m->n);
+        transpose_sq(m->u.get(), m->n, m->ut.get(), m->ctx->stream);
+        m->have_ut = true;
+    }
+    return m->ut.get();
+}
+
+// Per-thread pinned, device-mapped status word for kernels that report a data error (zero
+// decoupled denominator): no allocation and no extra synchronisation per call; the caller reads
+// it after the synchronisation it performs anyway.
+int* thread_flag() {
+    static thread_local int* f = nullptr;
+    if (!f) CPHIFI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f), sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    return f;
+}
+
 // GEMM helpers (column-major unless stated)
 void gemm_nn(cphifi_ctx ctx, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, const double* b,
              int64_t ldb, double* c, int64_t ldc) {
@@ -387,6 +407,20 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
     const double* uk = p->mode->u.get();
+    if (sandwich_supported(n, r)) {
+        const int64_t rp8 = sandwich_rp(r);
+        if (p->t1.n < (size_t)(n * rp8)) p->t1.alloc(n * rp8);
+        SandArgs a;
+        a.n = n; a.r = r;
+        a.u = uk; a.ut = mode_ut(p->mode);
+        a.x = x; a.ldx = n;
+        a.uv = p->uv.get();
+        a.op = SW_MUL; a.dmat = p->dmat.get();
+        a.core_out = p->t1.get();
+        a.y = y; a.ldy = n;
+        sandwich(a, ctx->num_sms, ctx->stream);
+        return;
+    }
     GemmArgs g;
     g.m = n; g.n = r; g.k = n;                    // t1 = U_K' X
     g.a = uk; g.a_rs = n; g.a_cs = 1;
@@ -410,10 +444,28 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
 }
 
 // solve_aligned_decoupled core on device buffers (aligned.hpp:41-54)
-void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* uv, const double* sv, double* w,
+// Enqueues only: the zero-denominator status lands in the returned mapped word, which the caller
+// checks (decoupled_check) after its own synchronisation.
+int* decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* uv, const double* sv, double* w,
                    DevBuf<double>& t1, DevBuf<double>& core) {
     cphifi_ctx ctx = mode->ctx;
     const int64_t n = mode->n;
+    int* flag = thread_flag();
+    *flag = 0;
+    if (sandwich_supported(n, r)) {
+        const int64_t rp8 = sandwich_rp(r);
+        if (core.n < (size_t)(n * rp8)) core.alloc(n * rp8);
+        SandArgs a;
+        a.n = n; a.r = r;
+        a.u = mode->u.get(); a.ut = mode_ut(mode);
+        a.x = b; a.ldx = n;
+        a.uv = uv;
+        a.op = SW_DIV; a.e_row = mode->mu.get(); a.e_col = sv; a.beta = mode->lambda; a.flag = flag;
+        a.core_out = core.get();
+        a.y = w; a.ldy = n;
+        sandwich(a, ctx->num_sms, ctx->stream);
+        return flag;
+    }
     if (t1.n < (size_t)(n * r)) t1.alloc(n * r);
     if (core.n < (size_t)(n * r)) core.alloc(n * r);
     GemmArgs g;
@@ -422,15 +474,13 @@ void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     g.b = b; g.b_rs = 1; g.b_cs = n;
     g.c = t1.get(); g.c_rs = 1; g.c_cs = n;
     gemm(g, ctx->num_sms, ctx->stream);
-    DevBuf<int> flag(1);
-    CPHIFI_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
     GemmArgs h;
     h.m = n; h.n = r; h.k = r;                    // core = (t1 U_V) ./ (sigma_j mu_i + lambda)
     h.a = t1.get(); h.a_rs = 1; h.a_cs = n;
     h.b = uv; h.b_rs = 1; h.b_cs = r;
     h.c = core.get(); h.c_rs = 1; h.c_cs = n;
     h.epi = EPI_SCALE_DIV; h.e_row = mode->mu.get(); h.e_col = sv; h.beta1 = mode->lambda;
-    h.flag = flag.get();
+    h.flag = flag;
     gemm(h, ctx->num_sms, ctx->stream);
     gemm_nn(ctx, n, r, n, mode->u.get(), n, core.get(), n, t1.get(), n);  // U_K core
     GemmArgs o;
@@ -439,8 +489,12 @@ void decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     o.b = uv; o.b_rs = r; o.b_cs = 1;
     o.c = w; o.c_rs = 1; o.c_cs = n;
     gemm(o, ctx->num_sms, ctx->stream);
-    // checked once the four GEMMs are queued (no bubble mid-pipeline); W is discarded on error
-    if (read_flag(ctx, flag.get()))
+    return flag;
+}
+
+// after the caller's synchronisation (W is discarded on error, aligned.hpp:48-50)
+void decoupled_check(const int* flag) {
+    if (*reinterpret_cast<const volatile int*>(flag))
         throw_runtime("solve_aligned_decoupled: zero eigenvalue pair; use lambda > 0");
 }
 
@@ -458,6 +512,64 @@ void upload_factors_cm(cphifi_ctx ctx, int d, const int64_t* shape, int k, int64
         h2d(buf.get() + off, factors[m], sizeof(double) * shape[m] * r, ctx->stream);
         ptrs[m] = buf.get() + off;
         off += shape[m] * r;
+    }
+}
+
+// The device-resident PCG loop needs a single GPU (no NCCL inside the graph body); opt out with
+// CPHIFI_PCG_GRAPH=0.  A failed capture or instantiation falls back to the host loop for good.
+bool pcg_graph_ok(cphifi_unaligned p) {
+    if (p->pcg_graph_failed || is_multi(p)) return false;
+    if (const char* e = std::getenv("CPHIFI_PCG_GRAPH")) return std::atoi(e) != 0;
+    return true;
+}
+
+// Capture `body` (one PCG iteration) into the body graph of a WHILE conditional node and
+// instantiate it, once per plan and operator form.  The captured pointers are the plan's
+// persistent PCG vectors, so later solves reuse the executable graph.
+template <class F>
+bool ensure_pcg_graph(cphifi_unaligned p, F&& body) {
+    if (p->pcg_exec && p->pcg_graph_op == p->op) return true;
+    if (p->pcg_exec) cudaGraphExecDestroy(p->pcg_exec);
+    if (p->pcg_graph) cudaGraphDestroy(p->pcg_graph);
+    p->pcg_exec = nullptr;
+    p->pcg_graph = nullptr;
+    cudaStream_t s = p->obs->ctx->stream;
+    CPHIFI_CUDA(cudaStreamSynchronize(s));
+    cudaGraph_t g = nullptr;
+    bool capturing = false;
+    try {
+        CPHIFI_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CPHIFI_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CPHIFI_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        CPHIFI_CUDA(cudaStreamBeginCaptureToGraph(s, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        body(h);
+        capturing = false;
+        CPHIFI_CUDA(cudaStreamEndCapture(s, &bodyg));
+        cudaGraphExec_t ex = nullptr;
+        CPHIFI_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        p->pcg_graph = g;
+        p->pcg_exec = ex;
+        p->pcg_graph_op = p->op;
+        return true;
+    } catch (const Error& e) {
+        if (capturing) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(s, &junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        p->pcg_graph_failed = true;
+        if (std::getenv("CPHIFI_DEBUG")) std::fprintf(stderr, "cphifi: PCG graph disabled: %s\n", e.what());
+        return false;
     }
 }
 
@@ -656,6 +768,7 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         const int64_t n = mode->n;
         mode->u.alloc(n * n);
         mode->mu.alloc(n);
+        mode->have_ut = false;
         h2d(mode->u.get(), u, sizeof(double) * n * n, mode->ctx->stream);
         h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
         clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);
@@ -1240,62 +1353,109 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         const auto t0 = std::chrono::steady_clock::now();
         if (p->rho <= 0.0) throw_invalid("solve_unaligned_pcg: rho must be positive");
         const int64_t n = p->n, r = p->r, nr = n * r;
-        DevBuf<double> bvec(nr), x(nr), res(nr), z(nr), pv(nr), ap(nr);
-        DevBuf<double> partial(80);  // 64 partials + ticket
-        DevBuf<PcgState> st(1);
-        CPHIFI_CUDA(cudaMemsetAsync(partial.get(), 0, sizeof(double) * 80, s));
-        CPHIFI_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(PcgState), s));
-        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec.get(), n);  // rhs = vec(K B)
-        ensure_precond(p);                                                                 // build_preconditioner
+        if (!p->pcg_vec.n) {
+            p->pcg_vec.alloc(6 * nr);
+            p->pcg_aux.alloc(80 + (sizeof(PcgState) + sizeof(PcgCtl) + 7) / 8);
+        }
+        double* bvec = p->pcg_vec.get();
+        double *x = bvec + nr, *res = bvec + 2 * nr, *z = bvec + 3 * nr, *pv = bvec + 4 * nr, *ap = bvec + 5 * nr;
+        double* partial = p->pcg_aux.get();
+        PcgState* st = reinterpret_cast<PcgState*>(partial + 80);
+        PcgCtl* ctl = reinterpret_cast<PcgCtl*>(partial + 80 + (sizeof(PcgState) + 7) / 8);
+        CPHIFI_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * 80, s));
+        CPHIFI_CUDA(cudaMemsetAsync(st, 0, sizeof(PcgState), s));
+        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
+        ensure_precond(p);                                                        // build_preconditioner
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;
-        dot_to(bvec.get(), bvec.get(), nr, partial.get(), &st.get()->bnorm, s);
-        d2h_sync(hs, &st.get()->bnorm, sizeof(double), s);
+        dot_to(bvec, bvec, nr, partial, &st->bnorm, s);
+        d2h_sync(hs, &st->bnorm, sizeof(double), s);
         const double bnorm = std::sqrt(hs[0]);
         std::vector<double> hist;
         cphifi_solve_report rep{};
         int matvecs = 0;
         if (bnorm == 0.0) {
-            CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
+            CPHIFI_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nr, s));
             rep.converged = 1;
         } else {
-            CPHIFI_CUDA(cudaMemcpyAsync(&st.get()->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
+            CPHIFI_CUDA(cudaMemcpyAsync(&st->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
             if (warm_start) {
-                h2d(x.get(), warm_start, sizeof(double) * nr, s);
-                matvec_dev(p, x.get(), ap.get());
+                h2d(x, warm_start, sizeof(double) * nr, s);
+                matvec_dev(p, x, ap);
                 ++matvecs;
-                axpby(res.get(), bvec.get(), 1.0, ap.get(), -1.0, nr, s);  // r = b - A x0
+                axpby(res, bvec, 1.0, ap, -1.0, nr, s);  // r = b - A x0
             } else {
-                CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
-                CPHIFI_CUDA(cudaMemcpyAsync(res.get(), bvec.get(), sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
+                CPHIFI_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nr, s));
+                CPHIFI_CUDA(cudaMemcpyAsync(res, bvec, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
             }
-            precond_dev(p, res.get(), z.get());
-            pcg_init(res.get(), z.get(), pv.get(), nr, st.get(), partial.get(), s);
+            precond_dev(p, res, z);
+            pcg_init(res, z, pv, nr, st, partial, s);
             PcgState hst;
-            d2h_sync(&hst, st.get(), sizeof(PcgState), s);
+            d2h_sync(&hst, st, sizeof(PcgState), s);
             double rel = hst.rel;
             if (cfg->record_history) hist.push_back(rel);
             int it = 0;
-            while (rel > cfg->tol && it < cfg->max_iter) {
-                matvec_dev(p, pv.get(), ap.get());
+            // one PCG iteration (solvers.hpp:59-80): the host loop below and the graph body
+            auto body_a = [&] {
+                matvec_dev(p, pv, ap);
+                pcg_step_a(x, res, pv, ap, nr, st, partial, s);
+            };
+            auto body_b = [&] {
+                precond_dev(p, res, z);
+                pcg_step_b(res, z, pv, nr, st, partial, s);
+            };
+            bool done = false;
+            if (p->op == 1) ensure_gram(p);  // lazily built state must exist before the capture
+            if (rel > cfg->tol && pcg_graph_ok(p)) {
+                // device-resident loop: a CUDA graph whose WHILE node repeats the iteration until
+                // pcg_ctl clears the condition; no host round trip per iteration
+                if (ensure_pcg_graph(p, [&](cudaGraphConditionalHandle h) {
+                        body_a();
+                        pcg_ctl(st, ctl, h, s);
+                        body_b();
+                    })) {
+                    const int cap = cfg->record_history ? cfg->max_iter : 0;
+                    if (cap > 0 && p->pcg_hist.n < (size_t)cap) p->pcg_hist.alloc(cap);
+                    PcgCtl hc{};
+                    hc.tol = cfg->tol;
+                    hc.max_iter = cfg->max_iter;
+                    hc.hist = cap > 0 ? p->pcg_hist.get() : nullptr;
+                    hc.hist_cap = cap;
+                    CPHIFI_CUDA(cudaMemcpyAsync(ctl, &hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+                    CPHIFI_CUDA(cudaGraphLaunch(p->pcg_exec, s));
+                    d2h_sync(&hc, ctl, sizeof(PcgCtl), s);
+                    d2h_sync(&hst, st, sizeof(PcgState), s);
+                    if (hst.flag == 1) throw_runtime("pcg: non-finite value encountered");
+                    if (hst.flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
+                    it = hc.it;
+                    matvecs += it;
+                    rel = hst.rel;
+                    if (cap > 0) {
+                        const size_t h0 = hist.size();
+                        hist.resize(h0 + std::min(it, cap));
+                        d2h_sync(hist.data() + h0, p->pcg_hist.get(), sizeof(double) * std::min(it, cap), s);
+                    }
+                    done = true;
+                }
+            }
+            while (!done && rel > cfg->tol && it < cfg->max_iter) {
+                body_a();
                 ++matvecs;
-                pcg_step_a(x.get(), res.get(), pv.get(), ap.get(), nr, st.get(), partial.get(), s);
-                d2h_sync(&hst, st.get(), sizeof(PcgState), s);
+                d2h_sync(&hst, st, sizeof(PcgState), s);
                 if (hst.flag == 1) throw_runtime("pcg: non-finite value encountered");
                 if (hst.flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
                 ++it;
                 rel = hst.rel;
                 if (cfg->record_history) hist.push_back(rel);
                 if (rel <= cfg->tol) break;
-                precond_dev(p, res.get(), z.get());
-                pcg_step_b(res.get(), z.get(), pv.get(), nr, st.get(), partial.get(), s);
+                body_b();
             }
             rep.iterations = it;
             rep.relative_residual = rel;
             rep.converged = rel <= cfg->tol;
         }
-        d2h_sync(w_out, x.get(), sizeof(double) * nr, s);
+        d2h_sync(w_out, x, sizeof(double) * nr, s);
         const auto t1 = std::chrono::steady_clock::now();
         rep.wall_time_s = std::chrono::duration<double>(t1 - t0).count();
         rep.setup_s = std::chrono::duration<double>(t_setup - t0).count();
@@ -1464,7 +1624,9 @@ int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
             h2d(dv.get(), v, sizeof(double) * r * r, ctx->stream);
             device_sym_eig(ctx, dv.get(), r, uv.get(), sv.get());
         }
-        decoupled_dev(mode, r, db.get(), uv.get(), sv.get(), w.get(), t1, core);
+        const int* flag = decoupled_dev(mode, r, db.get(), uv.get(), sv.get(), w.get(), t1, core);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        decoupled_check(flag);
         d2h_sync(w_out, w.get(), sizeof(double) * n * r, ctx->stream);
     });
 }
@@ -1499,9 +1661,10 @@ int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t
             CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());  // setup per north_star
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
-            decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+            const int* flag = decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
             CPHIFI_CUDA(cudaEventRecord(ev[4], s));
             CPHIFI_CUDA(cudaEventSynchronize(ev[4]));
+            decoupled_check(flag);
             if (it == 0) continue;
             float ms;
             for (int ph = 0; ph < 4; ++ph) {
@@ -1535,7 +1698,9 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, co
         mttkrp_dev(t, k, r, fptr, b.get(), work);
         gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), ctx->stream);
         device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());
-        decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+        const int* flag = decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+        CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+        decoupled_check(flag);
         d2h_sync(w_out, w.get(), sizeof(double) * n * r, ctx->stream);
         if (b_out) d2h_sync(b_out, b.get(), sizeof(double) * n * r, ctx->stream);
         if (v_out) d2h_sync(v_out, v.get(), sizeof(double) * r * r, ctx->stream);

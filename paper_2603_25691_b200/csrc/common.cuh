@@ -104,6 +104,8 @@ struct cphifi_mode_s {
     cphifi::DevBuf<double> kernel;  // n x n column-major (symmetric)
     cphifi::DevBuf<double> u;       // eigenvectors, n x n column-major
     cphifi::DevBuf<double> mu;      // eigenvalues (ascending, clamped at 0)
+    cphifi::DevBuf<double> ut;      // U' (k_sandwich.cu phase 2), built on first use
+    bool have_ut = false;
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;
@@ -163,6 +165,18 @@ struct cphifi_unaligned_s {
     cphifi::DevBuf<double> xhat_cm;           // n x r column-major
     cphifi::DevBuf<double> t1, t2;            // n x r scratch (preconditioner)
     cphifi::DevBuf<double> vx, vy;            // n x r device in/out for host-buffer calls
+    // device-resident PCG: persistent vectors + a CUDA graph whose WHILE node runs the iterations
+    cphifi::DevBuf<double> pcg_vec;           // b, x, r, z, p, Ap (n r each)
+    cphifi::DevBuf<double> pcg_aux;           // reduction partials | PcgState | PcgCtl
+    cphifi::DevBuf<double> pcg_hist;          // device residual history
+    cudaGraph_t pcg_graph = nullptr;
+    cudaGraphExec_t pcg_exec = nullptr;
+    int pcg_graph_op = -1;                    // operator form the graph was captured with
+    bool pcg_graph_failed = false;
+    ~cphifi_unaligned_s() {
+        if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+        if (pcg_graph) cudaGraphDestroy(pcg_graph);
+    }
 };
 
 struct cphifi_tensor_s {

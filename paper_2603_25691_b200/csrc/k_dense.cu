@@ -12,6 +12,7 @@
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -386,12 +387,321 @@ __global__ void __launch_bounds__(NTM) mttkrp_dmma_kernel(const MttkrpArgs a, in
             }
 }
 
+// MTTKRP v2 (BN <= 32): 16 warps = 4 row groups (32 rows x BN each, 4 x BN/8 independent DMMA
+// accumulators per k-step) x 4 k-groups (each takes 2 of the 8 k-steps of a stage; their
+// partials are summed in k-group order at the end).  The B tile is scaled by Wout once per stage
+// in shared memory (one DMUL per element instead of one per warp and fragment), so the DMMA
+// chain has no FP64 dependency in front of it.  ncu on the v1 kernel (8 warps, per-warp B
+// scaling): DMMA pipe 46 % active, stalls dominated by fixed-latency waits with 2 warps per
+// scheduler.
+constexpr int NTV = 512;
+constexpr int KGV = 4;  // k-groups
+template <int BN>
+__global__ void __launch_bounds__(NTV, 1) mttkrp_v2_kernel(const MttkrpArgs a, int64_t chunks, int64_t ktiles,
+                                                           const double* __restrict__ wout, double* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GemmSmem<BN, BMM, STM>& sm = *reinterpret_cast<GemmSmem<BN, BMM, STM>*>(smem_raw);
+    double* ws = reinterpret_cast<double*>(smem_raw + sizeof(GemmSmem<BN, BMM, STM>));  // STM x BN
+    constexpr int NF = BN / 8;
+    const int P = gridDim.y, split = blockIdx.y;
+    const int64_t n0 = a.shape[0];
+    const int64_t i0 = (int64_t)blockIdx.x * BMM, j0 = (int64_t)blockIdx.z * BN;
+    const int64_t tb = ktiles * split / P, te = ktiles * (split + 1) / P;
+    const int ntiles = (int)(te - tb);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rg = warp & 3, kg = warp >> 2;
+    const int kq = lane & 3, g = lane >> 2;
+
+    double acc[4][NF][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < NF; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+
+    auto load = [&](int st, int64_t tile) {  // the v1 tile loader, 512 threads
+        const int64_t n1 = a.shape[1];
+        const int64_t outer = tile / chunks, c1 = (tile - outer * chunks) * BK;
+        const int cnt = (int)min((int64_t)BK, n1 - c1);
+        const double* tcol = a.t + (c1 + n1 * outer) * n0;
+        if ((n0 & 1) == 0) {
+            for (int e = threadIdx.x; e < (BMM / 2) * BK; e += NTV) {
+                const int ii = 2 * (e % (BMM / 2)), kk = e / (BMM / 2);
+                const int64_t i = i0 + ii;
+                const bool p = (i < n0) && (kk < cnt);
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&sm.a[st][kk][ii]));
+                const double* src = p ? tcol + i + (int64_t)kk * n0 : a.t;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(p ? 16 : 0));
+            }
+        } else {
+            for (int e = threadIdx.x; e < BMM * BK; e += NTV) {
+                const int ii = e % BMM, kk = e / BMM;
+                const int64_t i = i0 + ii;
+                const bool p = (i < n0) && (kk < cnt);
+                cp_async8(&sm.a[st][kk][ii], p ? tcol + i + (int64_t)kk * n0 : a.t, p);
+            }
+        }
+        const double* a1 = a.fac[1] + c1 + a.off1;
+        for (int e = threadIdx.x; e < BN * BK; e += NTV) {
+            const int kk = e % BK, jj = e / BK;
+            const int64_t j = j0 + jj;
+            const bool p = (j < a.r) && (kk < cnt);
+            cp_async8(&sm.b[st][kk][jj], p ? a1 + kk + a.ld[1] * j : a.fac[1], p);
+        }
+        if (threadIdx.x < BN) {
+            const int64_t j = j0 + threadIdx.x;
+            cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.r + j : wout, j < a.r);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STM - 1; ++s) {
+        if (s < ntiles) load(s, tb + s);
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntiles; ++t) {
+        const int st = t % STM;
+        cp_async_wait<STM - 2>();  // stage t landed (this thread's copies)
+        __syncthreads();           // ... everyone's; and every warp is done with stage t - 1
+        if (t + STM - 1 < ntiles) load((t + STM - 1) % STM, tb + t + STM - 1);
+        cp_async_commit();
+        // z = A_1(i1, j) * Wout(outer, j): scale the B tile once, in place
+        for (int e = threadIdx.x; e < BN * BK; e += NTV) {
+            const int kk = e / BN, jj = e % BN;
+            sm.b[st][kk][jj] *= ws[st * BN + jj];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k2 = 0; k2 < BK / 4 / KGV; ++k2) {
+            const int kr = (kg * (BK / 4 / KGV) + k2) * 4 + kq;
+            double af[4], bf[NF];
+#pragma unroll
+            for (int mf = 0; mf < 4; ++mf) af[mf] = sm.a[st][kr][rg * 32 + mf * 8 + g];
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.b[st][kr][nf * 8 + g];
+#pragma unroll
+            for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf) dmma(acc[mf][nf], af[mf], bf[nf]);
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // k-group partials -> shared memory, summed in k-group order
+    double* red = reinterpret_cast<double*>(smem_raw);  // KGV x BMM x BN
+#pragma unroll
+    for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ii = rg * 32 + mf * 8 + g, jj = nf * 8 + kq * 2 + h;
+                red[(kg * BMM + ii) * BN + jj] = acc[mf][nf][h];
+            }
+    __syncthreads();
+    double* out = work + (int64_t)split * n0 * a.r;
+    for (int e = threadIdx.x; e < BMM * BN; e += NTV) {
+        const int ii = e % BMM, jj = e / BMM;
+        const int64_t i = i0 + ii, j = j0 + jj;
+        if (i < n0 && j < a.r) {
+            double s = red[ii * BN + jj];
+#pragma unroll
+            for (int k = 1; k < KGV; ++k) s += red[(k * BMM + ii) * BN + jj];
+            out[i + n0 * j] = s;
+        }
+    }
+}
+
+// MTTKRP v3 (BN <= 32, tensor-map TMA): a warp-specialised 5-stage ring.  Warp 8 is the
+// producer: per tile ONE 2-D tensor copy brings the T box (132 rows x 32 unfolding columns; the 4
+// extra rows land in the conflict-free pitch padding, rows past n0 read as zero), ONE brings the
+// A_1 box (36 i1 x BN columns, transposed layout k fastest, j past r read as zero) and one bulk
+// copy the Wout row, all completing on the slot's `full` mbarrier.  (Per-column bulk copies — 65
+// instructions per stage — capped the stream at ~2 TB/s: the copy engine's per-instruction
+// cost, not DRAM, was the limit.)  Warps 0-7 consume (4 row groups of 32 rows x 2 k-groups; one
+// warp per scheduler already saturates DMMA, profiles/micro/dmma_issue.cu) and release the slot
+// on its `empty` mbarrier: no CTA-wide barrier inside the loop.  The B fragment is scaled by Wout
+// on load and masked past the tile's k extent.  Splits interleave tile by tile so the grid
+// streams one contiguous window of T at a time.
+constexpr int ST3 = 5;
+constexpr int KG3 = 2;                // k-groups
+template <int WR>
+struct V3 {                           // WR rows per consumer warp
+    static constexpr int RG = BMM / WR;           // row groups
+    static constexpr int NC = RG * KG3 * 32;      // consumer threads
+    static constexpr int MF = WR / 8;             // A fragments per k-step
+};
+constexpr int AP3 = BMM + 4;          // T box rows = smem pitch
+constexpr int BKP3 = BK + 4;          // A_1 box rows = smem pitch of the transposed B tile
+template <int BN>
+struct Mttkrp3Smem {
+    double a[ST3][BK][AP3];
+    double bt[ST3][BN][BKP3];
+    double w[ST3][BN];
+    uint64_t full[ST3], empty[ST3];
+};
+template <int BN, int WR>
+__global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const MttkrpArgs a, const __grid_constant__ CUtensorMap tm_t,
+                                                                const __grid_constant__ CUtensorMap tm_a1, int64_t chunks,
+                                                                int64_t ktiles, const double* __restrict__ wout,
+                                                                double* __restrict__ work) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Mttkrp3Smem<BN>& sm = *reinterpret_cast<Mttkrp3Smem<BN>*>(smem_raw);
+    constexpr int NF = BN / 8;
+    constexpr int NC3 = V3<WR>::NC, MF = V3<WR>::MF, RG = V3<WR>::RG;
+    const int P = gridDim.y, split = blockIdx.y;
+    const int64_t n0 = a.shape[0], n1 = a.shape[1];
+    const int64_t i0 = (int64_t)blockIdx.x * BMM, j0 = (int64_t)blockIdx.z * BN;
+    // splits interleave tile by tile: split s takes tiles s, s + P, ...
+    const int ntiles = (int)((ktiles - split + P - 1) / P);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rows = (int)min((int64_t)BMM, n0 - i0);
+    const int bcols = (int)min((int64_t)BN, a.r - j0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST3; ++s) {
+            tma::mbar_init(&sm.full[s], 1);
+            tma::mbar_init(&sm.empty[s], NC3 / 32);
+        }
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+
+    // tile (outer, chunk) of this split's t-th step, advanced without 64-bit division (tiles
+    // step by P: P = dq chunks-rows + dr)
+    struct TileIt {
+        int64_t outer, cidx;
+    };
+    const int64_t dq = P / chunks, dr = P % chunks;
+    auto tile_first = [&]() { return TileIt{split / chunks, split % chunks}; };
+    auto tile_next = [&](TileIt& it) {
+        it.outer += dq;
+        it.cidx += dr;
+        if (it.cidx >= chunks) {
+            it.cidx -= chunks;
+            ++it.outer;
+        }
+    };
+
+    if (warp == NC3 / 32) {  // ---- producer warp (one lane) ----
+        if (lane == 0) {
+            const unsigned wb = (unsigned)((bcols * 8 + 15) & ~15);
+            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + BN * BKP3)) + wb;
+            // L2 prefetch runs l2_ahead tiles in front of the ring: the shared-memory stages then
+            // fill from L2, and the loaded-HBM latency hides behind the prefetch distance
+            const int pf = a.l2_ahead;
+            TileIt it = tile_first(), itp = tile_first();
+            for (int t = 0; t < min(pf, ntiles); ++t) {
+                tma::tensor_prefetch_l2_2d(&tm_t, (int)i0, (int)(itp.cidx * BK + n1 * itp.outer));
+                tile_next(itp);
+            }
+            for (int t = 0; t < ntiles; ++t, tile_next(it)) {
+                const int st = t % ST3;
+                if (pf > 0 && t + pf < ntiles) {
+                    tma::tensor_prefetch_l2_2d(&tm_t, (int)i0, (int)(itp.cidx * BK + n1 * itp.outer));
+                    tile_next(itp);
+                }
+                if (t >= ST3) tma::mbar_wait(&sm.empty[st], (unsigned)(((t / ST3) - 1) & 1));
+                const int64_t outer = it.outer, c1 = it.cidx * BK;
+                if (a.probe >= 2 && t >= ST3) {  // profiling: compute only (stale stages)
+                    tma::mbar_arrive(&sm.full[st]);
+                    continue;
+                }
+                tma::mbar_expect_tx(&sm.full[st], bytes);
+                tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
+                tma::tensor_g2s_2d(&sm.bt[st][0][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
+                tma::bulk_g2s(&sm.w[st][0], wout + outer * a.r + j0, wb, &sm.full[st]);
+            }
+        }
+    } else {  // ---- consumer warps ----
+        const int rg = warp % RG, kg = warp / RG;
+        const int kq = lane & 3, g = lane >> 2;
+        double acc[MF][NF][2];
+#pragma unroll
+        for (int x = 0; x < MF; ++x)
+#pragma unroll
+            for (int y = 0; y < NF; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+        TileIt it = tile_first();
+        for (int t = 0; t < ntiles; ++t, tile_next(it)) {
+            const int st = t % ST3;
+            const int cnt = (int)min((int64_t)BK, n1 - it.cidx * BK);
+            tma::mbar_wait(&sm.full[st], (unsigned)((t / ST3) & 1));
+            if (a.probe != 1) {
+                double wv[NF];
+#pragma unroll
+                for (int nf = 0; nf < NF; ++nf) wv[nf] = sm.w[st][nf * 8 + g];
+#pragma unroll
+                for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
+                    const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
+                    const bool kin = kr < cnt;
+                    double af[MF], bf[NF];
+#pragma unroll
+                    for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
+#pragma unroll
+                    for (int nf = 0; nf < NF; ++nf)
+                        bf[nf] = a.probe == 3 ? sm.bt[st][nf * 8 + g][kr] : (kin ? sm.bt[st][nf * 8 + g][kr] * wv[nf] : 0.0);
+#pragma unroll
+                    for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+                        for (int nf = 0; nf < NF; ++nf) dmma(acc[mf][nf], af[mf], bf[nf]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&sm.empty[st]);
+        }
+        __syncthreads();  // (1) the ring is drained by every consumer
+        double* red = reinterpret_cast<double*>(smem_raw);  // KG3 x BMM x BN
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int ii = rg * WR + mf * 8 + g, jj = nf * 8 + kq * 2 + h;
+                    red[(kg * BMM + ii) * BN + jj] = acc[mf][nf][h];
+                }
+    }
+    if (warp == NC3 / 32) __syncthreads();  // the producer's side of (1)
+    __syncthreads();
+    const double* red = reinterpret_cast<const double*>(smem_raw);
+    double* out = work + (int64_t)split * n0 * a.r;
+    for (int e = threadIdx.x; e < BMM * BN; e += blockDim.x) {
+        const int ii = e % BMM, jj = e / BMM;
+        const int64_t i = i0 + ii, j = j0 + jj;
+        if (ii < rows && j < a.r) {
+            double s = red[ii * BN + jj];
+#pragma unroll
+            for (int k = 1; k < KG3; ++k) s += red[(k * BMM + ii) * BN + jj];
+            out[i + n0 * j] = s;
+        }
+    }
+}
+
 __global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int64_t cnt,
                                      double* __restrict__ out) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int p = 0; p < P; ++p) s += work[(int64_t)p * cnt + e];
         out[e] = s;
+    }
+}
+
+template <int BN, int WR>
+void launch_v3(const MttkrpArgs& ap, const CUtensorMap& tm_t, const CUtensorMap& tm_a1, int mt, int64_t P, int nt,
+               int64_t chunks, int64_t ktiles, const double* wout, double* work, cudaStream_t s) {
+    const size_t smem3 = sizeof(Mttkrp3Smem<BN>);
+    static bool attr3 = false;
+    if (!attr3) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+        attr3 = true;
+    }
+    mttkrp_v3_kernel<BN, WR><<<dim3(mt, (unsigned)P, nt), V3<WR>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks, ktiles,
+                                                                                     wout, work);
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR>);
+        throw Error(CPHIFI_CUDA_ERROR, std::string("mttkrp_v3 launch: ") + cudaGetErrorString(le) + " regs " +
+                                           std::to_string(fa.numRegs) + " maxthreads " + std::to_string(fa.maxThreadsPerBlock));
     }
 }
 
@@ -408,7 +718,7 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
     int64_t P = std::max<int64_t>(1, (int64_t)num_sms / (mt * nt));
     P = std::max<int64_t>(1, std::min<int64_t>(P, ktiles));
     P = std::min<int64_t>(P, 1024);
-    const size_t need = (size_t)P * n0 * a.r + (size_t)n_outer * a.r;
+    const size_t need = (size_t)P * n0 * a.r + (size_t)n_outer * a.r + 2;
     if (work.n < need) work.alloc(need);
     double* wout = work.get() + (size_t)P * n0 * a.r;
     kr_outer_kernel<<<(unsigned)((n_outer * a.r + 255) / 256), 256, 0, s>>>(a, n_outer, wout);
@@ -420,7 +730,39 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
                                          (int)smem));
         attr_set = true;
     }
-    mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTM, smem, s>>>(a, chunks, ktiles, wout, work.get());
+    bool v2 = BN <= 32;
+    if (const char* e = std::getenv("CPHIFI_MTTKRP_V1")) v2 = v2 && std::atoi(e) == 0;
+    // v3 (tensor-map TMA ring) needs 16-byte aligned bases and leading dimensions (even n0 and
+    // A_1 leading dimension) and int32 box coordinates
+    int64_t ncols = 1;
+    for (int m = 1; m < a.d; ++m) ncols *= a.shape[m];
+    CUtensorMap tm_t, tm_a1;
+    bool v3 = v2 && (n0 % 2 == 0) && (a.ld[1] % 2 == 0) && ncols < (1LL << 31) &&
+              encode_tmap_2d_f64(&tm_t, a.t, (uint64_t)n0, (uint64_t)ncols, (uint64_t)n0, BMM + 4, BK) &&
+              encode_tmap_2d_f64(&tm_a1, a.fac[1], (uint64_t)a.ld[1], (uint64_t)a.r, (uint64_t)a.ld[1], BK + 4, BN);
+    if (const char* e = std::getenv("CPHIFI_MTTKRP_V3")) v3 = v3 && std::atoi(e) != 0;
+    MttkrpArgs ap = a;
+    if (const char* e = std::getenv("CPHIFI_MTTKRP_PROBE")) ap.probe = std::atoi(e);
+    if (const char* e = std::getenv("CPHIFI_MTTKRP_L2AHEAD")) ap.l2_ahead = std::atoi(e);
+    if constexpr (BN <= 32) {
+        static_assert(sizeof(double) * KGV * BMM * BN <= sizeof(GemmSmem<BN, BMM, STM>), "reduction fits");
+        if (v3) {
+            int wr = 32;
+            if (const char* e = std::getenv("CPHIFI_MTTKRP_WR")) wr = std::atoi(e) == 16 ? 16 : 32;
+            if (wr == 16) launch_v3<BN, 16>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            else launch_v3<BN, 32>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+        } else if (v2) {
+            static bool attr2 = false;
+            if (!attr2) {
+                CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+                attr2 = true;
+            }
+            mttkrp_v2_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTV, smem, s>>>(a, chunks, ktiles, wout, work.get());
+        }
+    }
+    if (!v2)
+        mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTM, smem, s>>>(a, chunks, ktiles, wout, work.get());
     CPHIFI_CHECK_LAUNCH();
     const int64_t cnt = n0 * a.r;
     reduce_splits_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(
@@ -567,6 +909,29 @@ __global__ void peak_dmma_kernel(int iters, double seed, double* out) {
 }
 
 }  // namespace
+
+bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
+                        uint32_t box1) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<Fn>(p);
+    }();
+    if (!fn || reinterpret_cast<uintptr_t>(base) % 16 != 0 || (ld * sizeof(double)) % 16 != 0) return false;
+    const cuuint64_t dims[2] = {rows, cols};
+    const cuuint64_t strides[1] = {ld * sizeof(double)};
+    const cuuint32_t box[2] = {box0, box1};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_tflops) {
     DevBuf<double> sink(1);

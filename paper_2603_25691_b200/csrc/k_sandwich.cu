@@ -1,0 +1,219 @@
+// k_sandwich.cu — the eigenbasis "sandwich"  Y = U ((U' X U_V) op E) U_V'  in two launches.
+//
+// Both hot-path consumers of the Kronecker eigenbasis have this shape:
+//   * build_preconditioner's apply (unaligned.hpp:135-139): M^-1 x = U_K ((U_K' X U_V) .* D) U_V'
+//   * solve_aligned_decoupled (aligned.hpp:44-53):  W = U_K ((U_K' B U_V) ./ (sigma_j mu_i + lambda)) U_V'
+// Evaluated left to right like the reference (Eigen's (A*B)*C), each phase is a ROW-LOCAL
+// contraction once the n x n factor is read column-wise:
+//   phase 1  core(i,:) = op( (U(:,i)' X) U_V )          (U column i contiguous)
+//   phase 2  Y(i,:)    = (U'(:,i)' core) U_V'            (U' column i = U row i, contiguous)
+// so a CTA owns RB rows, streams its RB columns of U (or U') together with the matching k-chunk
+// of X (or core) through a 4-stage cp.async ring (64 k per stage), and finishes the r x r product and the
+// element-wise op in its epilogue.  Two launches replace four DMMA GEMM launches plus an
+// epilogue pass; the n x n factor is read once per phase (HBM/L2 bound: 8 n^2 bytes per phase),
+// the r x n chunks come from L2.  Every sum has a fixed order: bit-reproducible.
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace cphifi {
+namespace {
+
+constexpr int SW_T = 256;   // threads per CTA
+constexpr int SW_KC = 64;   // k per stage
+constexpr int SW_ST = 4;    // stages
+
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int RP, int RB>
+struct SwSmem {
+    static constexpr int MP = RP + 1;  // pitch of the k x j chunk: conflict-free transposed fills
+    double m[SW_ST][SW_KC][MP];        // X (phase 1) or core (phase 2) rows k0 .. k0 + KC
+    double u[SW_ST][SW_KC][RB];        // u[kk][row] = F(k0 + kk, i0 + row), F = U or U'
+    double tt[RB][MP];                 // reduced (F' M) rows of this CTA
+    double red[SW_T * RB];             // k-slice partials (S x RB x RP)
+};
+
+// PH = 1: core(i, j) = op((U' X U_V)(i, j)) row-major [i * RP + j] (zero pad j >= r)
+// PH = 2: y(i + n j) = (U core U_V')(i, j)
+template <int RP, int RB, int PH>
+__global__ void __launch_bounds__(SW_T) sandwich_kernel(const SandArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SwSmem<RP, RB>& sm = *reinterpret_cast<SwSmem<RP, RB>*>(smem_raw);
+    constexpr int S = SW_T / RP;  // k-slices
+    const int64_t n = a.n;
+    const int r = (int)a.r;
+    const int64_t i0 = (int64_t)blockIdx.x * RB;
+    const int rb = (int)min((int64_t)RB, n - i0);
+    const int j = threadIdx.x % RP, s = threadIdx.x / RP;
+    const double* F = PH == 1 ? a.u : a.ut;  // column i of F = the row's coefficients
+    const int nchunks = (int)((n + SW_KC - 1) / SW_KC);
+
+    auto load = [&](int st, int c) {
+        const int64_t k0 = (int64_t)c * SW_KC;
+        const int kc = (int)min((int64_t)SW_KC, n - k0);
+        for (int e = threadIdx.x; e < SW_KC * RB; e += SW_T) {
+            const int kk = e % SW_KC, row = e / SW_KC;
+            const bool p = kk < kc && row < rb;
+            cpa8(&sm.u[st][kk][row], p ? F + (k0 + kk) + n * (i0 + row) : F, p);
+        }
+        if constexpr (PH == 1) {  // X column-major: consecutive threads walk k (coalesced)
+            for (int e = threadIdx.x; e < SW_KC * RP; e += SW_T) {
+                const int kk = e % SW_KC, jj = e / SW_KC;
+                const bool p = kk < kc && jj < r;
+                cpa8(&sm.m[st][kk][jj], p ? a.x + (k0 + kk) + a.ldx * jj : a.x, p);
+            }
+        } else {  // core row-major (pad columns are zero)
+            for (int e = threadIdx.x; e < SW_KC * RP; e += SW_T) {
+                const int kk = e / RP, jj = e % RP;
+                const bool p = kk < kc;
+                cpa8(&sm.m[st][kk][jj], p ? a.core + (k0 + kk) * RP + jj : a.core, p);
+            }
+        }
+    };
+
+    double acc[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int st = 0; st < SW_ST - 1; ++st) {
+        if (st < nchunks) load(st, st);
+        cpa_commit();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const int st = c % SW_ST;
+        cpa_wait<SW_ST - 2>();
+        __syncthreads();
+        if (c + SW_ST - 1 < nchunks) load((c + SW_ST - 1) % SW_ST, c + SW_ST - 1);
+        cpa_commit();
+#pragma unroll
+        for (int kk = s; kk < SW_KC; kk += S) {
+            const double xv = sm.m[st][kk][j];
+#pragma unroll
+            for (int q = 0; q < RB; ++q) acc[q] = fma(sm.u[st][kk][q], xv, acc[q]);
+        }
+    }
+    cpa_wait<0>();
+    __syncthreads();
+    // reduce the S k-slices in slice order
+    double* red = sm.red;
+#pragma unroll
+    for (int q = 0; q < RB; ++q) red[(s * RB + q) * RP + j] = acc[q];
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RP; e += SW_T) {
+        const int q = e / RP, jj = e % RP;
+        double t = 0.0;
+        for (int z = 0; z < S; ++z) t += red[(z * RB + q) * RP + jj];
+        sm.tt[q][jj] = t;
+    }
+    __syncthreads();
+    // epilogue: (row of F' M) times U_V (phase 1) or U_V' (phase 2), then the element-wise op
+    for (int e = threadIdx.x; e < RB * RP; e += SW_T) {
+        const int q = e / RP, jj = e % RP;
+        if (q >= rb) continue;
+        const int64_t i = i0 + q;
+        if (jj >= r) {
+            if constexpr (PH == 1) a.core_out[i * RP + jj] = 0.0;
+            continue;
+        }
+        double c = 0.0;
+        for (int m = 0; m < r; ++m) c = fma(sm.tt[q][m], PH == 1 ? a.uv[m + (int64_t)r * jj] : a.uv[jj + (int64_t)r * m], c);
+        if constexpr (PH == 1) {
+            double out;
+            if (a.op == SW_MUL) {
+                out = c * a.dmat[i + n * jj];
+            } else {
+                const double den = a.e_col[jj] * a.e_row[i] + a.beta;
+                if (den == 0.0) *a.flag = 1;
+                out = c / den;
+            }
+            a.core_out[i * RP + jj] = out;
+        } else {
+            a.y[i + a.ldy * jj] = c;
+        }
+    }
+}
+
+template <int RP, int RB, int PH>
+void launch_t(const SandArgs& a, cudaStream_t s) {
+    auto kern = sandwich_kernel<RP, RB, PH>;
+    const size_t smem = sizeof(SwSmem<RP, RB>);
+    static bool attr = false;
+    if (!attr) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((a.n + RB - 1) / RB);
+    kern<<<grid, SW_T, smem, s>>>(a);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+template <int RP, int PH>
+void launch_rb(const SandArgs& a, int rb, cudaStream_t s) {
+    switch (rb) {
+        case 1: launch_t<RP, 1, PH>(a, s); break;
+        case 2: launch_t<RP, 2, PH>(a, s); break;
+        case 4: launch_t<RP, 4, PH>(a, s); break;
+        default: launch_t<RP, 8, PH>(a, s); break;
+    }
+}
+
+template <int PH>
+void launch_ph(const SandArgs& a, int rb, cudaStream_t s) {
+    switch (a.rp) {
+        case 8: launch_rb<8, PH>(a, rb, s); break;
+        case 16: launch_rb<16, PH>(a, rb, s); break;
+        case 32: launch_rb<32, PH>(a, rb, s); break;
+        case 64: launch_rb<64, PH>(a, rb, s); break;
+        default: throw_invalid("sandwich: padded rank must be 8, 16, 32 or 64");
+    }
+}
+
+}  // namespace
+
+int64_t sandwich_rp(int64_t r) { return pow2_at_least(r, 8); }
+
+bool sandwich_supported(int64_t n, int64_t r) {
+    if (const char* e = std::getenv("CPHIFI_SANDWICH")) {
+        if (std::atoi(e) == 0) return false;
+    }
+    return r >= 1 && r <= 64 && n >= 1 && n <= 2048;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ at) {
+    __shared__ double t[32][33];
+    const int64_t bx = (int64_t)blockIdx.x * 32, by = (int64_t)blockIdx.y * 32;
+    for (int yy = threadIdx.y; yy < 32; yy += 8) {
+        const int64_t i = bx + threadIdx.x, j = by + yy;
+        if (i < n && j < n) t[yy][threadIdx.x] = a[i + n * j];
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += 8) {
+        const int64_t i = by + threadIdx.x, j = bx + yy;  // at(i, j) = a(j, i)
+        if (i < n && j < n) at[i + n * j] = t[threadIdx.x][yy];
+    }
+}
+
+void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {
+    const unsigned g = (unsigned)((n + 31) / 32);
+    transpose_kernel<<<dim3(g, g), dim3(32, 8), 0, s>>>(a, n, at);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
+    a.rp = sandwich_rp(a.r);
+    a.core = a.core_out;
+    // rows per CTA: about two CTAs per SM, at most 8
+    int rb = 1;
+    while (rb < 8 && (a.n + rb - 1) / rb > 2 * num_sms) rb *= 2;
+    launch_ph<1>(a, rb, s);
+    launch_ph<2>(a, rb, s);
+}
+
+}  // namespace cphifi

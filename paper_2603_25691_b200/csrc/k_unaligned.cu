@@ -135,6 +135,16 @@ __global__ void pcg_rr_kernel(const double* __restrict__ r, int64_t n, PcgState*
     });
 }
 
+__global__ void pcg_ctl_kernel(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h) {
+    const int it = ++c->it;
+    const double rel = st->rel;
+    if (c->hist && it - 1 < c->hist_cap) c->hist[it - 1] = rel;
+    if (st->flag != 0 || !(rel > c->tol) || it >= c->max_iter) {
+        c->stop = 1;
+        cudaGraphSetConditional(h, 0);
+    }
+}
+
 __global__ void axpby_kernel(double* y, const double* a, double alpha, const double* b, double beta, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = alpha * a[i] + beta * b[i];
@@ -237,6 +247,10 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
               cudaStream_t s) {
     pcg_init_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, z, p, n, st, partial);
     pcg_rr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, n, st, partial);
+    CPHIFI_CHECK_LAUNCH();
+}
+void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s) {
+    pcg_ctl_kernel<<<1, 1, 0, s>>>(st, c, h);
     CPHIFI_CHECK_LAUNCH();
 }
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n, cudaStream_t s) {

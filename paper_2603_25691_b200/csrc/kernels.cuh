@@ -42,6 +42,9 @@ struct MttkrpArgs {
     const double* fac[8] = {nullptr};  // device column-major, fac[m] has ld = full n_m
     int64_t ld[8] = {0};
     double* b = nullptr;      // n0 x r column-major output
+    int probe = 0;            // profiling only (CPHIFI_MTTKRP_PROBE, v3): 1 = stream T without the DMMA work,
+                              // 2 = DMMA work on stale stages without the stream, 3 = as 2 without the B scaling
+    int l2_ahead = 8;         // v3: tiles of T prefetched into L2 ahead of the shared-memory ring
 };
 void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work);
 
@@ -61,6 +64,31 @@ void precond_diag(const double* mu, const double* sv, int64_t n, int64_t r, doub
 void pack_rows(const double* src_cm, int64_t rows, int64_t ld, int64_t r, int64_t rp, double* dst_rm,
                cudaStream_t s);
 void rm_to_cm(const double* src_rm, int64_t rows, int64_t rp, int64_t r, double* dst_cm, cudaStream_t s);
+
+// ---- eigenbasis sandwich Y = U ((U' X U_V) op E) U_V' (k_sandwich.cu): two row-local launches
+enum : int { SW_MUL = 0, SW_DIV = 1 };
+struct SandArgs {
+    int64_t n = 0, r = 0, rp = 0;       // rp set by sandwich()
+    const double* u = nullptr;          // n x n column-major
+    const double* ut = nullptr;         // U' (n x n column-major)
+    const double* x = nullptr;          // n x r, column stride ldx
+    int64_t ldx = 0;
+    const double* uv = nullptr;         // r x r column-major
+    int op = SW_MUL;
+    const double* dmat = nullptr;       // SW_MUL: n x r column-major
+    const double* e_row = nullptr;      // SW_DIV: den = e_col[j] * e_row[i] + beta
+    const double* e_col = nullptr;
+    double beta = 0.0;
+    int* flag = nullptr;                // SW_DIV: set to 1 on a zero denominator
+    double* core_out = nullptr;         // n x rp row-major scratch (phase 1 output)
+    const double* core = nullptr;       // the same buffer (phase 2 input)
+    double* y = nullptr;                // n x r, column stride ldy
+    int64_t ldy = 0;
+};
+bool sandwich_supported(int64_t n, int64_t r);
+int64_t sandwich_rp(int64_t r);
+void sandwich(SandArgs a, int num_sms, cudaStream_t s);
+void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
 
 // ---- the unaligned operator as one persistent cooperative kernel (k_fused.cu) -----------
 // PH_A: Xhat rows distributed + barrier; PH_AL: each CTA computes only the Xhat rows its own
@@ -152,6 +180,16 @@ struct PcgState {
     int flag;  // 1 = non-finite p'Ap, 2 = p'Ap <= 0
     int pad;
 };
+// Device-resident PCG loop control (the body of a CUDA-graph WHILE node): counts the iteration,
+// records rel, and clears the loop condition exactly where solvers.hpp:59-80 leaves the loop
+// (non-finite / non-positive p'Ap, rel <= tol, it == max_iter).
+struct PcgCtl {
+    double tol;
+    int max_iter, it;
+    double* hist;  // device history (rel after each iteration), hist_cap entries
+    int hist_cap, stop;
+};
+void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
 void dot_to(const double* x, const double* y, int64_t n, double* partial, double* out, cudaStream_t s);
 // pap = p.ap; flag; alpha = rz/pap; x += alpha p; r -= alpha ap; rr = r.r; rel = sqrt(rr)/bnorm
 void pcg_step_a(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st,
