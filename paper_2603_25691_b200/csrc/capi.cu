@@ -165,9 +165,16 @@ struct PartitionPlan {
     std::vector<int32_t> row_ncta;        // n
 };
 
-void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, PartitionPlan& pl) {
+// equal > 0: exactly `equal` CTAs of equal observation count (rows split wherever a boundary
+// falls; the kernel finishes split rows through its slots), else the row-aligned plan below.
+void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, PartitionPlan& pl, int equal = 0) {
     const int64_t n = (int64_t)rp.size() - 1, q = rp[n];
     std::vector<int64_t> starts;
+    if (equal > 0) {  // (empty CTAs dropped: the CTAs sharing a split row must be consecutive)
+        for (int c = 0; c <= equal; ++c) starts.push_back(q * c / equal);
+        starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+        if (starts.size() < 2) starts.assign({0, q});
+    }
     auto build = [&](int64_t L) {
         starts.assign(1, 0);
         int64_t load = 0;
@@ -193,7 +200,7 @@ void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, Partitio
         if (starts.size() < 2) starts.assign({0, q});
     };
     int64_t L = std::max<int64_t>(1, (q + cmax - 1) / std::max(cmax, 1));
-    for (;;) {
+    for (; equal <= 0;) {
         build(L);
         if ((int64_t)starts.size() - 1 <= cmax) break;
         L = L + L / 8 + 1;
@@ -1026,11 +1033,12 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         const int64_t n = p->n;
         // fused-kernel launch shape: all CTAs co-resident (cooperative launch)
         p->small_n = n <= 512 && n * r <= 8192;
+        if (const char* e = std::getenv("CPHIFI_SMALL_N")) p->small_n = p->small_n && std::atoi(e) != 0;
         p->prefetch = p->small_n;
         p->smem_factors = (int64_t)p->fac.n * 8 <= 96 * 1024;  // keeps two CTAs per SM
         if (const char* e = std::getenv("CPHIFI_SMEM_FACTORS")) p->smem_factors = p->smem_factors && std::atoi(e) != 0;
         const int64_t crows = (n + ctx->num_sms - 1) / ctx->num_sms;  // >= rows per CTA in PH_C2
-        const int64_t pref = p->prefetch ? (n | 1) * r + (fused_maxloc() + crows) * n : 0;
+        const int64_t pref = p->prefetch ? fused_ldx(n) * r + (fused_maxloc() + crows) * n : 0;
         // large plans with >= 2 other modes in lexicographic order: k_stream.cu, one CTA per SM
         p->stream = !p->small_n && obs->lex && stream_supported(p->rp, d - 1);
         if (const char* e = std::getenv("CPHIFI_STREAM")) p->stream = p->stream && std::atoi(e) != 0;
@@ -1050,7 +1058,16 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         {
             std::vector<int64_t> rp_host(n + 1);
             d2h_sync(rp_host.data(), obs->row_ptr.get(), sizeof(int64_t) * (n + 1), s);
-            plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
+            // optional equal-count plan (CPHIFI_EQUAL_PART=<ctas>); measured slower than the
+            // row-aligned plan at config 1 (split rows cost a slot round trip per CTA)
+            int equal = 0;
+            if (const char* e = std::getenv("CPHIFI_EQUAL_PART")) equal = p->small_n ? std::atoi(e) : 0;
+            if (equal > cmax) equal = 0;
+            if (equal > 0) {
+                plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan, equal);
+                if (plan.max_span > fused_maxloc()) equal = 0;  // too many rows per CTA for local Xhat
+            }
+            if (equal <= 0) plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
         }
         p->grid = plan.ctas;
         p->local_x = p->small_n && plan.max_span <= fused_maxloc();
@@ -1252,7 +1269,21 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
         if (want_dbg) {
             std::vector<long long> h(dbg.n);
             d2h_sync(h.data(), dbg.get(), sizeof(long long) * h.size(), ctx->stream);
-            for (int c = 0; c < std::min(p->grid, 4); ++c) {
+            // the CTAs with the longest and the median event span (clock64 is per SM: deltas only)
+            std::vector<std::pair<long long, int>> span;
+            for (int c = 0; c < p->grid; ++c) {
+                long long lo = -1, hi = -1;
+                for (int e = 0; e < DBG_SLOTS / 2 && h[(size_t)c * DBG_SLOTS + 2 * e] >= 0; ++e) {
+                    const long long t = h[(size_t)c * DBG_SLOTS + 2 * e + 1];
+                    if (lo < 0) lo = t;
+                    hi = t;
+                }
+                span.push_back({hi - lo, c});
+            }
+            std::sort(span.begin(), span.end());
+            std::vector<int> show = {span.back().second, span[span.size() - 2].second, span[span.size() / 2].second,
+                                     span.front().second};
+            for (int c : show) {
                 std::printf("cta %d:", c);
                 const long long t0 = h[(size_t)c * DBG_SLOTS + 1];
                 for (int e = 0; e < DBG_SLOTS / 2 && h[(size_t)c * DBG_SLOTS + 2 * e] >= 0; ++e)

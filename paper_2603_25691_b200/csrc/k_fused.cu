@@ -29,6 +29,8 @@
 // latency hides behind phase AL); packed factor rows are staged in shared memory when they fit
 // (SURVEY §7 hard part 4), so the round loop runs from shared memory.
 #include "kernels.cuh"
+#include "lanegroup.cuh"
+#include "tma.cuh"
 
 namespace cphifi {
 namespace {
@@ -37,7 +39,7 @@ constexpr int FT = 512;    // threads per CTA
 constexpr int TILE = 1024; // observations per staged tile
 constexpr int MAXLOC = 4;  // PH_AL: max rows one CTA computes Xhat for
 constexpr int MAX_SMEM = 226 * 1024;  // dynamic shared memory cap (227 KB opt-in minus static)
-constexpr int UNR = 2;     // rounds in flight per group in the fast path
+constexpr int UNR = 4;     // observations in flight per lane group in the fast path
 
 __device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
     unsigned old;
@@ -53,28 +55,26 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Two-level software grid barrier (all CTAs co-resident: cooperative launch).  CTAs arrive on
-// per-group counters (one 128-byte line each, `group` CTAs per counter); the last arriver of a
-// group arrives on the top counter; the last group bumps the generation word.  Counters are
-// never reset: an episode is complete when a counter reaches a multiple of its member count.
-// Layout: bar[0] top count, bar[32] generation, bar[64 + 32*k] count of group k.
-// `gen` is thread 0's copy of the generation word, read once at kernel entry (it only changes
-// when this kernel's own barriers complete), so the critical path starts with the arrival.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, int group, unsigned& gen) {
+// Software grid barrier (all CTAs co-resident: cooperative launch) on ONE 64-bit counter that
+// is never reset: a CTA arrives with a relaxed add after a gpu-scope fence (cumulative over the
+// CTA's writes, ordered by bar.sync) and waits until the counter reaches the next multiple of the
+// grid size.  Two L2 round trips on the critical path (the arrival and the observing load); the
+// former two-level counter tree + generation word took ~3 us from the last arrival to release.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int C = gridDim.x, k = blockIdx.x / group;
-        const unsigned ngrp = (unsigned)((C + group - 1) / group);
-        const unsigned members = (unsigned)min(group, C - k * group);
-        __threadfence();  // cumulative: this CTA's writes (ordered by bar.sync) before arrival
-        const unsigned old = atom_add_acqrel(bar + 64 + 32 * k, 1u);
-        if ((old + 1) % members == 0) {
-            const unsigned old2 = atom_add_acqrel(bar, 1u);
-            if ((old2 + 1) % ngrp == 0) red_release_add(bar + 32, 1u);
+        unsigned long long* ctr = reinterpret_cast<unsigned long long*>(bar);
+        const unsigned long long C = gridDim.x;
+        __threadfence();
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        const unsigned long long target = old - old % C + C;
+        while (ld_acquire_u64(ctr) < target) {
         }
-        while (ld_acquire(bar + 32) == gen) {
-        }
-        ++gen;
     }
     __syncthreads();
 }
@@ -161,7 +161,7 @@ __device__ __forceinline__ void row_dot(const FusedArgs& a, const double* __rest
 }
 
 template <int RP, int DO, bool SMEMF>
-__global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) {
     // 2 doubles per lane: one LDS.128 per factor row, and every 8-lane phase of the warp reads
     // one contiguous 128-byte row segment -> conflict-free gathers (the loop is bound by
     // shared-memory wavefronts, SURVEY §7 hard part 4)
@@ -179,13 +179,41 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     double* sfac = reinterpret_cast<double*>(sidx + 2 * DO * TILE);   // staged factors (SMEMF)
     // X staged column-major with an odd column stride: the j-fastest lanes of row_dot and the
     // element-order staging writes both hit distinct banks
-    const int64_t ldx = a.n | 1;
+    const int64_t ldx = fused_ldx(a.n);
     double* xs = sfac + (SMEMF ? a.fac_total : 0);                   // X, ldx x r (prefetch)
     double* kcs = xs + (a.prefetch ? ldx * a.r : 0);                 // K columns (prefetch)
     __shared__ int64_t s_rows[2];
     __shared__ int s_last;
+    __shared__ __align__(8) uint64_t s_fbar;  // plan-independent TMA prefetch (factors, X, C2 K columns)
 
     const int c = blockIdx.x, C = gridDim.x;
+    const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
+    const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
+    // ---- entry, before any dependent load: one thread issues the bulk copies that need no plan
+    // data (even n: 16-byte aligned columns), so their HBM latency overlaps the plan reads
+    const bool tma_entry = (a.n % 2) == 0;
+    const bool tma_fac = tma_entry && SMEMF && (a.phases & PH_B) && !a.gram;
+    const bool tma_any = tma_fac || (tma_entry && pf);
+    if (tma_any && threadIdx.x == 0) {
+        tma::mbar_init(&s_fbar, 1);
+        tma::fence_mbar_init();
+        const unsigned colb = (unsigned)(a.n * 8);
+        unsigned bytes = 0;
+        if (tma_fac) bytes += (unsigned)(a.fac_total * 8);
+        if (pf) bytes += colb * (unsigned)a.r;
+        if (pf && (a.phases & PH_C2)) bytes += colb * (unsigned)(i1 - i0);
+        tma::mbar_expect_tx(&s_fbar, bytes);
+        if (tma_fac)
+            for (int64_t b0 = 0; b0 < a.fac_total * 8; b0 += 32768)
+                tma::bulk_g2s(reinterpret_cast<unsigned char*>(sfac) + b0, reinterpret_cast<const unsigned char*>(a.fac) + b0,
+                              (unsigned)min((int64_t)32768, a.fac_total * 8 - b0), &s_fbar);
+        if (pf) {
+            for (int j = 0; j < (int)a.r; ++j) tma::bulk_g2s(xs + ldx * j, a.x + a.n * j, colb, &s_fbar);
+            if (a.phases & PH_C2)
+                for (int64_t i = i0; i < i1; ++i)
+                    tma::bulk_g2s(kcs + (MAXLOC + i - i0) * a.n, a.kmat + i * a.n, colb, &s_fbar);
+        }
+    }
     const int g = threadIdx.x / G, glane = threadIdx.x % G, jb = glane * VPL;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - lane % G));
@@ -194,7 +222,6 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];  // row-aligned partition (host plan)
     const bool has_obs = (a.phases & PH_B) && ca < cb;
     const int ntiles = has_obs && !a.gram ? (int)((cb - ca + TILE - 1) / TILE) : 0;
-    const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
 
     auto issue_tile = [&](int t) {
         const int buf = t & 1;
@@ -212,7 +239,6 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     };
 
     stamp(a, 0);
-    unsigned bar_gen = threadIdx.x == 0 ? ld_acquire(a.barrier + 32) : 0u;
     __shared__ unsigned s_c2_empty;  // bit t: y row i0 + t has no observation in this shard
     if (threadIdx.x < 32) {
         const bool e = (a.phases & PH_C2) && i0 + threadIdx.x < i1 &&
@@ -239,22 +265,23 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     const int nal = do_al ? (int)(last_row - first_row + 1) : 0;
 
     // ---- entry: async prefetch (group 0: factors, X, K columns, tile 0; group 1: tile 1) ----
-    if (ntiles > 0) {
+    if (ntiles > 0 && !tma_fac) {
         if constexpr (SMEMF) {
             const double2* src = reinterpret_cast<const double2*>(a.fac);
             for (int64_t e = threadIdx.x; e < a.fac_total / 2; e += FT) cp_async16(sfac + 2 * e, src + e);
         }
     }
-    const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
     if (pf) {
-        const int nn = (int)a.n, nr = (int)(a.n * a.r), odd = (int)(ldx - a.n);  // small n: n * r <= 8192
-        for (int e = threadIdx.x; e < nr; e += FT) cp_async8(xs + e + odd * (e / nn), a.x + e);
+        if (!tma_entry) {
+            const int nn = (int)a.n, nr = (int)(a.n * a.r), odd = (int)(ldx - a.n);  // small n: n * r <= 8192
+            for (int e = threadIdx.x; e < nr; e += FT) cp_async8(xs + e + odd * (e / nn), a.x + e);
+            if (a.phases & PH_C2)
+                for (int64_t i = i0; i < i1; ++i)
+                    for (int64_t k = threadIdx.x; k < a.n; k += FT)
+                        cp_async8(kcs + (MAXLOC + i - i0) * a.n + k, a.kmat + i * a.n + k);
+        }
         for (int rr = 0; rr < nal; ++rr)
             for (int64_t k = threadIdx.x; k < a.n; k += FT) cp_async8(kcs + rr * a.n + k, a.kmat + (first_row + rr) * a.n + k);
-        if (a.phases & PH_C2)
-            for (int64_t i = i0; i < i1; ++i)
-                for (int64_t k = threadIdx.x; k < a.n; k += FT)
-                    cp_async8(kcs + (MAXLOC + i - i0) * a.n + k, a.kmat + i * a.n + k);
     }
     if (ntiles > 0) issue_tile(0);
     cp_commit();
@@ -269,6 +296,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
     if (a.phases & PH_AL) {  // only the rows this CTA's observations touch, from shared memory
         if (ntiles > 1) cp_wait<1>();
         else cp_wait<0>();
+        if (tma_any) tma::mbar_wait(&s_fbar, 0);
         __syncthreads();
         dbg_mark(9);  // prefetch landed
         for (int rr = 0; rr < nal; ++rr) {
@@ -283,7 +311,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
             if (threadIdx.x < RP) a.xhat_rm[i * RP + threadIdx.x] = rowbuf[threadIdx.x];
         }
         stamp(a, 1);
-        grid_barrier(a.barrier, a.bar_groups, bar_gen);
+        grid_barrier(a.barrier);
         stamp(a, 2);
     }
     const bool local_x = (a.phases & PH_AL) != 0;
@@ -362,6 +390,7 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
         for (int t = 0; t < ntiles; ++t) {
             if (t + 1 < ntiles) cp_wait<1>();
             else cp_wait<0>();
+            if (t == 0 && tma_any) tma::mbar_wait(&s_fbar, 0);
             __syncthreads();
             if (t == 0) stamp(a, 2);
             dbg_mark(1);  // tile ready
@@ -395,46 +424,39 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
                 const int64_t seg_end = min(t1, cur_end);
                 const int o_end = (int)(seg_end - t0);
                 int o = (int)(seg - t0) + g;
-                for (; o + NG < o_end; o += 2 * NG) {
-                    double z0[VPL], z1[VPL];
-                    build_z(o, z0);
-                    build_z(o + NG, z1);
-                    double s0, s1;
-                    if (dot) {
-                        s0 = partial_dot(z0);
-                        s1 = partial_dot(z1);
+                // UNR observations per lane group per round, every group of the warp running the
+                // warp's maximum round count (padding observations contribute exactly zero), so
+                // the partial dots reduce with full-mask shuffles as one transposed butterfly
+                // (lanegroup.cuh).  Accumulation order per group: o, o + NG, o + 2 NG, ...
+                const int mine = o < o_end ? (o_end - o + NG - 1) / NG : 0;
+                const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)((mine + UNR - 1) / UNR));
+                for (int rd = 0; rd < rounds; ++rd, o += UNR * NG) {
+                    double z[UNR][VPL], sv[UNR];
+                    bool val[UNR];
 #pragma unroll
-                        for (int off = G / 2; off > 0; off >>= 1) {
-                            s0 += __shfl_xor_sync(gmask, s0, off, G);
-                            s1 += __shfl_xor_sync(gmask, s1, off, G);
-                        }
+                    for (int u = 0; u < UNR; ++u) {
+                        val[u] = o + u * NG < o_end;
+                        build_z(val[u] ? o + u * NG : o_end - 1, z[u]);
+                    }
+                    if (dot) {
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u) sv[u] = partial_dot(z[u]);
+                        group_reduce<UNR, G>(sv, lane);
                         if (mult) {  // coalesced plan: entry weight = multiplicity
-                            s0 *= (double)tm[o];
-                            s1 *= (double)tm[o + NG];
+#pragma unroll
+                            for (int u = 0; u < UNR; ++u) sv[u] *= (double)tm[val[u] ? o + u * NG : o_end - 1];
                         }
                     } else {
-                        s0 = tw[o];
-                        s1 = tw[o + NG];
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u) sv[u] = tw[val[u] ? o + u * NG : o_end - 1];
                     }
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s0, z0[v], acc[v]);
+                    for (int u = 0; u < UNR; ++u) {
+                        if (val[u]) {
 #pragma unroll
-                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s1, z1[v], acc[v]);
-                }
-                if (o < o_end) {
-                    double z0[VPL];
-                    build_z(o, z0);
-                    double s0;
-                    if (dot) {
-                        s0 = partial_dot(z0);
-#pragma unroll
-                        for (int off = G / 2; off > 0; off >>= 1) s0 += __shfl_xor_sync(gmask, s0, off, G);
-                        if (mult) s0 *= (double)tm[o];
-                    } else {
-                        s0 = tw[o];
+                            for (int v = 0; v < VPL; ++v) acc[v] = fma(sv[u], z[u][v], acc[v]);
+                        }
                     }
-#pragma unroll
-                    for (int v = 0; v < VPL; ++v) acc[v] = fma(s0, z0[v], acc[v]);
                 }
                 seg = seg_end;
                 dbg_mark(2);  // segment done
@@ -461,10 +483,11 @@ __global__ void __launch_bounds__(FT) fused_matvec_kernel(const FusedArgs a) {
 
     // ---- phase C2: y = (K Yhat + lambda Xhat) + rho x  (small n) ------------------------------
     if (a.phases & PH_C2) {
-        if (a.phases & PH_B) grid_barrier(a.barrier, a.bar_groups, bar_gen);
+        if (a.phases & PH_B) grid_barrier(a.barrier);
         stamp(a, 5);
         dbg_mark(4);
         cp_wait<0>();
+        if (tma_any) tma::mbar_wait(&s_fbar, 0);
         __syncthreads();
         for (int64_t i = i0; i < i1; ++i) {
             const double* kc = pf ? kcs + (MAXLOC + i - i0) * a.n : a.kmat + i * a.n;

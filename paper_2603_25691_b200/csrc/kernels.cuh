@@ -132,6 +132,9 @@ struct FusedArgs {
 constexpr int DBG_SLOTS = 64;
 constexpr int TRACE_SLOTS = 8;  // entry, A done, barrier 1, B done, barrier 2, C1 done, barrier 3, end
 inline size_t barrier_words(int grid, int group) { return 64 + 32 * (size_t)((grid + group - 1) / group); }
+// column stride of X staged in the fused kernel's shared memory: odd (conflict-free row dots)
+// for odd n; n + 2 for even n so every column is a 16-byte aligned bulk copy
+__host__ __device__ inline int64_t fused_ldx(int64_t n) { return (n & 1) ? n : n + 2; }
 size_t fused_smem_bytes(int64_t rp, int dother, int64_t fac_total, bool smemf, int64_t prefetch_elems);
 int fused_maxloc();
 int fused_grid(int64_t rp, int dother, bool smemf, size_t smem, int num_sms);
