@@ -175,6 +175,13 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
  * [4] y = K Yhat + lambda Xhat + rho x, [5] the whole matvec. */
 int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters,
                                   double* ms_out);
+/* Benchmark hook: `steps` operator applications on DEVICE buffers x, y captured in ONE CUDA
+ * graph, each preceded (outside its event pair) by a memset of `flush_bytes` at `flush` that
+ * evicts L2; the graph is launched once to warm up and once timed.  ms_out[i] receives the
+ * event-timed milliseconds of application i (the per-launch host overhead of a plain launch is
+ * not in them: the way the operator runs inside the device-resident PCG loop). */
+int cphifi_unaligned_matvec_graph_timed(cphifi_unaligned p, const double* x, double* y, void* flush,
+                                        size_t flush_bytes, int steps, float* ms_out);
 /* Tracing hook: one operator application on DEVICE buffers with per-CTA %globaltimer stamps
  * (8 per CTA: entry, phase A done, barrier 1, phase B done, barrier 2, fix-up done,
  * barrier 3, exit; 0 = phase not run).  *ctas receives the CTA count. */
@@ -212,8 +219,9 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                          double* v_out);
 
 /* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
- * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup), [3] decoupled
- * rotate/divide/rotate, [4] timed solve = [0] + [1] + [3]. */
+ * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup: wall clock of the
+ * warm-up pass; the timed passes reuse it), [3] decoupled rotate/divide/rotate, [4] timed solve
+ * = [0] + [1] + [3]. */
 int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                                const double* const* factors, int iters, double* w_out,
                                double* ms_out);

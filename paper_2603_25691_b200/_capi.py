@@ -104,6 +104,9 @@ _SIGS = [
     ("cphifi_solve_unaligned_pcg", ctypes.c_int,
      [_H, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC), c_double_p, c_double_p]),
     ("cphifi_unaligned_matvec_timed", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c_double_p]),
+    ("cphifi_unaligned_matvec_graph_timed", ctypes.c_int,
+     [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+      ctypes.POINTER(ctypes.c_float)]),
     ("cphifi_unaligned_matvec_trace", ctypes.c_int,
      [_H, ctypes.c_void_p, ctypes.c_void_p, c_uint64_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_unaligned_scatter_gather", ctypes.c_int, [_H, c_double_p, c_double_p]),

@@ -171,11 +171,21 @@ struct cphifi_unaligned_s {
     cphifi::DevBuf<double> pcg_hist;          // device residual history
     cudaGraph_t pcg_graph = nullptr;
     cudaGraphExec_t pcg_exec = nullptr;
+    // host-buffer matvec (cphifi_unaligned_matvec) as one graph [H2D, operator, D2H] for pinned
+    // buffers; the copy nodes are re-pointed per call
+    cudaGraph_t hv_graph = nullptr;
+    cudaGraphExec_t hv_exec = nullptr;
+    cudaGraphNode_t hv_h2d = nullptr, hv_d2h = nullptr;
+    const double* hv_x = nullptr;
+    double* hv_y = nullptr;
+    bool hv_failed = false;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
     bool pcg_graph_failed = false;
     ~cphifi_unaligned_s() {
         if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
         if (pcg_graph) cudaGraphDestroy(pcg_graph);
+        if (hv_exec) cudaGraphExecDestroy(hv_exec);
+        if (hv_graph) cudaGraphDestroy(hv_graph);
     }
 };
 

@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cphifi {
 namespace {
@@ -140,6 +141,154 @@ __global__ void __launch_bounds__(SW_T) sandwich_kernel(const SandArgs a) {
     }
 }
 
+// ---- v2 (even n, 16-byte aligned columns): bulk-copy ring, k across lanes -----------------
+// Each stage brings KC consecutive k of the CTA's RB columns of F (U or U') and of every column of
+// M (X, or the phase-1 core, both column-major with leading dimension ld) with one bulk copy per
+// column: smem rows contiguous in k, so lanes walk k (conflict-free) and warps split the columns
+// j.  The per-(j, row) partial sums are reduced over the 32 lanes through shared memory in lane
+// order.  Phase 1 writes core column-major (n x r); phase 2 reads it.  (v1 above: one 8-byte
+// cp.async per element, 28-31 us per phase at n = 1024, r = 32 — latency-bound by the request
+// count, like the per-column MTTKRP copies.)
+constexpr int SW2_T = 256, SW2_W = SW2_T / 32, SW2_ST = 3;
+template <int RP>
+struct Sw2 {
+    static constexpr int KC = RP >= 64 ? 64 : (RP >= 32 ? 128 : 256);  // k per stage
+    static constexpr int JPW = RP / SW2_W;                              // columns per warp
+};
+template <int RP, int RB>
+struct Sw2Smem {
+    static constexpr int KC = Sw2<RP>::KC;
+    double m[SW2_ST][RP][KC];
+    double u[SW2_ST][RB][KC];
+    double tt[RB][RP + 1];
+    uint64_t full[SW2_ST];
+};
+template <int RP, int RB, int PH>
+__global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    using SM = Sw2Smem<RP, RB>;
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    constexpr int KC = Sw2<RP>::KC, JPW = Sw2<RP>::JPW;
+    const int64_t n = a.n;
+    const int r = (int)a.r;
+    const int64_t i0 = (int64_t)blockIdx.x * RB;
+    const int rb = (int)min((int64_t)RB, n - i0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* F = PH == 1 ? a.u : a.ut;
+    const double* M = PH == 1 ? a.x : a.core;
+    const int64_t ldm = PH == 1 ? a.ldx : n;
+    const int nch = (int)((n + KC - 1) / KC);
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < SW2_ST; ++st) tma::mbar_init(&sm.full[st], 1);
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int c) {  // thread 0
+        const int st = c % SW2_ST;
+        const int64_t k0 = (int64_t)c * KC;
+        const unsigned bytes = (unsigned)(min((int64_t)KC, n - k0) * 8);
+        tma::mbar_expect_tx(&sm.full[st], bytes * (unsigned)(rb + r));
+        for (int q = 0; q < rb; ++q) tma::bulk_g2s(&sm.u[st][q][0], F + (i0 + q) * n + k0, bytes, &sm.full[st]);
+        for (int j = 0; j < r; ++j) tma::bulk_g2s(&sm.m[st][j][0], M + j * ldm + k0, bytes, &sm.full[st]);
+    };
+    if (threadIdx.x == 0)
+        for (int c = 0; c < min(nch, SW2_ST); ++c) issue(c);
+    double acc[JPW][RB];
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj)
+#pragma unroll
+        for (int q = 0; q < RB; ++q) acc[jj][q] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % SW2_ST;
+        const int kc = (int)min((int64_t)KC, n - (int64_t)c * KC);
+        tma::mbar_wait(&sm.full[st], (unsigned)((c / SW2_ST) & 1));
+        for (int kk = lane; kk < kc; kk += 32) {
+            double uq[RB];
+#pragma unroll
+            for (int q = 0; q < RB; ++q) uq[q] = q < rb ? sm.u[st][q][kk] : 0.0;
+#pragma unroll
+            for (int jj = 0; jj < JPW; ++jj) {
+                const int j = warp + SW2_W * jj;
+                const double xv = j < r ? sm.m[st][j][kk] : 0.0;
+#pragma unroll
+                for (int q = 0; q < RB; ++q) acc[jj][q] = fma(uq[q], xv, acc[jj][q]);
+            }
+        }
+        __syncthreads();  // every warp is done with slot st
+        if (threadIdx.x == 0 && c + SW2_ST < nch) {
+            tma::fence_proxy_async();
+            issue(c + SW2_ST);
+        }
+    }
+    // lane partials -> shared memory (the ring is idle now), summed over lanes in lane order
+    double* red = &sm.m[0][0][0];  // W x 32 x (JPW * RB)
+    static_assert(SW2_T * JPW * RB <= SW2_ST * RP * KC, "reduction fits the ring");
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj)
+#pragma unroll
+        for (int q = 0; q < RB; ++q) red[(warp * 32 + lane) * (JPW * RB) + jj * RB + q] = acc[jj][q];
+    __syncthreads();
+    for (int e = threadIdx.x; e < SW2_W * JPW * RB; e += SW2_T) {
+        const int w = e / (JPW * RB), rem = e % (JPW * RB), jj = rem / RB, q = rem % RB;
+        double t = 0.0;
+        for (int l = 0; l < 32; ++l) t += red[(w * 32 + l) * (JPW * RB) + rem];
+        sm.tt[q][w + SW2_W * jj] = t;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RP; e += SW2_T) {
+        const int q = e / RP, jj = e % RP;
+        if (q >= rb || jj >= r) continue;
+        const int64_t i = i0 + q;
+        double c = 0.0;
+        for (int m = 0; m < r; ++m) c = fma(sm.tt[q][m], PH == 1 ? a.uv[m + (int64_t)r * jj] : a.uv[jj + (int64_t)r * m], c);
+        if constexpr (PH == 1) {
+            double out;
+            if (a.op == SW_MUL) {
+                out = c * a.dmat[i + n * jj];
+            } else {
+                const double den = a.e_col[jj] * a.e_row[i] + a.beta;
+                if (den == 0.0) *a.flag = 1;
+                out = c / den;
+            }
+            a.core_out[i + n * jj] = out;
+        } else {
+            a.y[i + a.ldy * jj] = c;
+        }
+    }
+}
+
+template <int RP, int RB, int PH>
+void launch2_t(const SandArgs& a, cudaStream_t s) {
+    auto kern = sandwich2_kernel<RP, RB, PH>;
+    const size_t smem = sizeof(Sw2Smem<RP, RB>);
+    static bool attr = false;
+    if (!attr) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<(unsigned)((a.n + RB - 1) / RB), SW2_T, smem, s>>>(a);
+    CPHIFI_CHECK_LAUNCH();
+}
+template <int RP, int PH>
+void launch2_rb(const SandArgs& a, int rb, cudaStream_t s) {
+    // accumulators per thread: RP / 8 columns x RB rows <= 32
+    constexpr int RBMAX = 256 / RP >= 8 ? 8 : 256 / RP;
+    if (rb >= 8 && RBMAX >= 8) launch2_t<RP, (RBMAX >= 8 ? 8 : RBMAX), PH>(a, s);
+    else if (rb >= 4 && RBMAX >= 4) launch2_t<RP, (RBMAX >= 4 ? 4 : RBMAX), PH>(a, s);
+    else if (rb >= 2) launch2_t<RP, 2, PH>(a, s);
+    else launch2_t<RP, 1, PH>(a, s);
+}
+template <int PH>
+void launch2_ph(const SandArgs& a, int rb, cudaStream_t s) {
+    switch (a.rp) {
+        case 8: launch2_rb<8, PH>(a, rb, s); break;
+        case 16: launch2_rb<16, PH>(a, rb, s); break;
+        case 32: launch2_rb<32, PH>(a, rb, s); break;
+        case 64: launch2_rb<64, PH>(a, rb, s); break;
+        default: throw_invalid("sandwich: padded rank must be 8, 16, 32 or 64");
+    }
+}
+
 template <int RP, int RB, int PH>
 void launch_t(const SandArgs& a, cudaStream_t s) {
     auto kern = sandwich_kernel<RP, RB, PH>;
@@ -212,6 +361,15 @@ void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
     // rows per CTA: about two CTAs per SM, at most 8
     int rb = 1;
     while (rb < 8 && (a.n + rb - 1) / rb > 2 * num_sms) rb *= 2;
+    bool v2 = a.n % 2 == 0 && a.ldx % 2 == 0 && reinterpret_cast<uintptr_t>(a.u) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(a.ut) % 16 == 0 && reinterpret_cast<uintptr_t>(a.x) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(a.core_out) % 16 == 0;
+    if (const char* e = std::getenv("CPHIFI_SANDWICH_V1")) v2 = v2 && std::atoi(e) == 0;
+    if (v2) {  // core column-major n x r (v2 layout)
+        launch2_ph<1>(a, rb, s);
+        launch2_ph<2>(a, rb, s);
+        return;
+    }
     launch_ph<1>(a, rb, s);
     launch_ph<2>(a, rb, s);
 }
