@@ -220,8 +220,10 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
 
 /* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
  * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup: wall clock of the
- * warm-up pass; the timed passes reuse it), [3] decoupled rotate/divide/rotate, [4] timed solve
- * = [0] + [1] + [3]. */
+ * warm-up pass; the timed passes reuse it), [3] decoupled rotate/divide/rotate (each phase of a
+ * synchronised pass, so it carries its kernels' launch latency), [4] timed solve: the sequence
+ * [0], [1], [3] captured as one CUDA graph and replayed `iters` times back to back (one GPU;
+ * with a communicator, [0] + [1] + [3]). */
 int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                                const double* const* factors, int iters, double* w_out,
                                double* ms_out);

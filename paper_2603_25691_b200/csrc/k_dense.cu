@@ -519,9 +519,12 @@ __global__ void __launch_bounds__(NTV, 1) mttkrp_v2_kernel(const MttkrpArgs a, i
 // instructions per stage — capped the stream at ~2 TB/s: the copy engine's per-instruction
 // cost, not DRAM, was the limit.)  Warps 0-7 consume (4 row groups of 32 rows x 2 k-groups; one
 // warp per scheduler already saturates DMMA, profiles/micro/dmma_issue.cu) and release the slot
-// on its `empty` mbarrier: no CTA-wide barrier inside the loop.  The B fragment is scaled by Wout
-// on load and masked past the tile's k extent.  Splits interleave tile by tile so the grid
-// streams one contiguous window of T at a time.
+// on its `empty` mbarrier: no CTA-wide barrier inside the loop.  Each split takes a contiguous
+// tile range; tiles of one `outer` index share the Wout row, so the DMMAs accumulate the raw
+// T_tile x A_1 tile products into a per-outer accumulator that is scaled by Wout (per output
+// column) and folded into the result when `outer` changes: no FP64 work besides DMMA in the loop
+// (per-fragment scaling + masking cost 8 % of the DMMA throughput).  Partial k chunks (n1 not a
+// multiple of 32) take a masked path.
 constexpr int ST3 = 5;
 constexpr int KG3 = 2;                // k-groups
 template <int WR>
@@ -551,8 +554,8 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
     const int P = gridDim.y, split = blockIdx.y;
     const int64_t n0 = a.shape[0], n1 = a.shape[1];
     const int64_t i0 = (int64_t)blockIdx.x * BMM, j0 = (int64_t)blockIdx.z * BN;
-    // splits interleave tile by tile: split s takes tiles s, s + P, ...
-    const int ntiles = (int)((ktiles - split + P - 1) / P);
+    const int64_t tb = ktiles * split / P, te = ktiles * (split + 1) / P;
+    const int ntiles = (int)(te - tb);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rows = (int)min((int64_t)BMM, n0 - i0);
     const int bcols = (int)min((int64_t)BN, a.r - j0);
@@ -566,26 +569,21 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
     }
     __syncthreads();
 
-    // tile (outer, chunk) of this split's t-th step, advanced without 64-bit division (tiles
-    // step by P: P = dq chunks-rows + dr)
+    // tile (outer, chunk) of this split's t-th step, advanced without 64-bit division
     struct TileIt {
         int64_t outer, cidx;
     };
-    const int64_t dq = P / chunks, dr = P % chunks;
-    auto tile_first = [&]() { return TileIt{split / chunks, split % chunks}; };
+    auto tile_first = [&]() { return TileIt{tb / chunks, tb % chunks}; };
     auto tile_next = [&](TileIt& it) {
-        it.outer += dq;
-        it.cidx += dr;
-        if (it.cidx >= chunks) {
-            it.cidx -= chunks;
+        if (++it.cidx == chunks) {
+            it.cidx = 0;
             ++it.outer;
         }
     };
 
     if (warp == NC3 / 32) {  // ---- producer warp (one lane) ----
         if (lane == 0) {
-            const unsigned wb = (unsigned)((bcols * 8 + 15) & ~15);
-            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + BN * BKP3)) + wb;
+            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + BN * BKP3));
             // L2 prefetch runs l2_ahead tiles in front of the ring: the shared-memory stages then
             // fill from L2, and the loaded-HBM latency hides behind the prefetch distance
             const int pf = a.l2_ahead;
@@ -609,45 +607,78 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                 tma::mbar_expect_tx(&sm.full[st], bytes);
                 tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
                 tma::tensor_g2s_2d(&sm.bt[st][0][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
-                tma::bulk_g2s(&sm.w[st][0], wout + outer * a.r + j0, wb, &sm.full[st]);
             }
         }
     } else {  // ---- consumer warps ----
         const int rg = warp % RG, kg = warp / RG;
         const int kq = lane & 3, g = lane >> 2;
-        double acc[MF][NF][2];
+        double acc[MF][NF][2], tmp[MF][NF][2];
 #pragma unroll
         for (int x = 0; x < MF; ++x)
 #pragma unroll
-            for (int y = 0; y < NF; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+            for (int y = 0; y < NF; ++y) acc[x][y][0] = acc[x][y][1] = tmp[x][y][0] = tmp[x][y][1] = 0.0;
+        // acc += tmp * Wout(outer, column) for the lane's C columns nf * 8 + 2 kq + h (a one-outer
+        // look-ahead of the Wout loads spilled registers and measured slower)
+        auto fold = [&](int64_t outer) {
+            const double* wr = wout + outer * a.r + j0;
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int jj = nf * 8 + 2 * kq + h;
+                    const double wv = jj < bcols ? __ldg(wr + jj) : 0.0;
+#pragma unroll
+                    for (int mf = 0; mf < MF; ++mf) {
+                        acc[mf][nf][h] = fma(tmp[mf][nf][h], wv, acc[mf][nf][h]);
+                        tmp[mf][nf][h] = 0.0;
+                    }
+                }
+        };
         TileIt it = tile_first();
+        int64_t cur_outer = it.outer;
         for (int t = 0; t < ntiles; ++t, tile_next(it)) {
             const int st = t % ST3;
+            if (it.outer != cur_outer) {
+                fold(cur_outer);
+                cur_outer = it.outer;
+            }
             const int cnt = (int)min((int64_t)BK, n1 - it.cidx * BK);
             tma::mbar_wait(&sm.full[st], (unsigned)((t / ST3) & 1));
             if (a.probe != 1) {
-                double wv[NF];
+                if (cnt == BK) {  // full chunk: DMMA only
 #pragma unroll
-                for (int nf = 0; nf < NF; ++nf) wv[nf] = sm.w[st][nf * 8 + g];
+                    for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
+                        const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
+                        double af[MF], bf[NF];
 #pragma unroll
-                for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
-                    const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
-                    const bool kin = kr < cnt;
-                    double af[MF], bf[NF];
+                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
 #pragma unroll
-                    for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][nf * 8 + g][kr];
 #pragma unroll
-                    for (int nf = 0; nf < NF; ++nf)
-                        bf[nf] = a.probe == 3 ? sm.bt[st][nf * 8 + g][kr] : (kin ? sm.bt[st][nf * 8 + g][kr] * wv[nf] : 0.0);
+                        for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
-                    for (int mf = 0; mf < MF; ++mf)
+                            for (int nf = 0; nf < NF; ++nf) dmma(tmp[mf][nf], af[mf], bf[nf]);
+                    }
+                } else {  // partial chunk: k past the extent masked to zero in B
 #pragma unroll
-                        for (int nf = 0; nf < NF; ++nf) dmma(acc[mf][nf], af[mf], bf[nf]);
+                    for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
+                        const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
+                        double af[MF], bf[NF];
+#pragma unroll
+                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
+#pragma unroll
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][nf * 8 + g][kr] : 0.0;
+#pragma unroll
+                        for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+                            for (int nf = 0; nf < NF; ++nf) dmma(tmp[mf][nf], af[mf], bf[nf]);
+                    }
                 }
             }
             __syncwarp();
             if (lane == 0) tma::mbar_arrive(&sm.empty[st]);
         }
+        if (ntiles > 0) fold(cur_outer);
         __syncthreads();  // (1) the ring is drained by every consumer
         double* red = reinterpret_cast<double*>(smem_raw);  // KG3 x BMM x BN
 #pragma unroll

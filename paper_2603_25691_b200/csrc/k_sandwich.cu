@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(SW_T) sandwich_kernel(const SandArgs a) {
 // order.  Phase 1 writes core column-major (n x r); phase 2 reads it.  (v1 above: one 8-byte
 // cp.async per element, 28-31 us per phase at n = 1024, r = 32 — latency-bound by the request
 // count, like the per-column MTTKRP copies.)
-constexpr int SW2_T = 256, SW2_W = SW2_T / 32, SW2_ST = 3;
+constexpr int SW2_T = 256, SW2_W = SW2_T / 32, SW2_ST = 4;
 template <int RP>
 struct Sw2 {
     static constexpr int KC = RP >= 64 ? 64 : (RP >= 32 ? 128 : 256);  // k per stage
@@ -164,7 +164,8 @@ struct Sw2Smem {
     uint64_t full[SW2_ST];
 };
 template <int RP, int RB, int PH>
-__global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a) {
+__global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a, const __grid_constant__ CUtensorMap tm_f,
+                                                          const __grid_constant__ CUtensorMap tm_m) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using SM = Sw2Smem<RP, RB>;
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
@@ -174,22 +175,18 @@ __global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a) {
     const int64_t i0 = (int64_t)blockIdx.x * RB;
     const int rb = (int)min((int64_t)RB, n - i0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* F = PH == 1 ? a.u : a.ut;
-    const double* M = PH == 1 ? a.x : a.core;
-    const int64_t ldm = PH == 1 ? a.ldx : n;
     const int nch = (int)((n + KC - 1) / KC);
     if (threadIdx.x == 0) {
         for (int st = 0; st < SW2_ST; ++st) tma::mbar_init(&sm.full[st], 1);
         tma::fence_mbar_init();
     }
     __syncthreads();
-    auto issue = [&](int c) {  // thread 0
+    auto issue = [&](int c) {  // thread 0: two 2-D tensor copies per stage (out-of-range reads as 0)
         const int st = c % SW2_ST;
-        const int64_t k0 = (int64_t)c * KC;
-        const unsigned bytes = (unsigned)(min((int64_t)KC, n - k0) * 8);
-        tma::mbar_expect_tx(&sm.full[st], bytes * (unsigned)(rb + r));
-        for (int q = 0; q < rb; ++q) tma::bulk_g2s(&sm.u[st][q][0], F + (i0 + q) * n + k0, bytes, &sm.full[st]);
-        for (int j = 0; j < r; ++j) tma::bulk_g2s(&sm.m[st][j][0], M + j * ldm + k0, bytes, &sm.full[st]);
+        const int k0 = c * KC;
+        tma::mbar_expect_tx(&sm.full[st], (unsigned)(sizeof(double) * KC * (RB + RP)));
+        tma::tensor_g2s_2d(&sm.u[st][0][0], &tm_f, k0, (int)i0, &sm.full[st]);
+        tma::tensor_g2s_2d(&sm.m[st][0][0], &tm_m, k0, 0, &sm.full[st]);
     };
     if (threadIdx.x == 0)
         for (int c = 0; c < min(nch, SW2_ST); ++c) issue(c);
@@ -266,12 +263,18 @@ void launch2_t(const SandArgs& a, cudaStream_t s) {
         CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    kern<<<(unsigned)((a.n + RB - 1) / RB), SW2_T, smem, s>>>(a);
+    constexpr int KC = Sw2<RP>::KC;
+    const uint64_t n = (uint64_t)a.n;
+    CUtensorMap tf, tm;  // F = U or U' (n x n), M = X (ld ldx) or core (ld n); r columns of M
+    const bool ok = encode_tmap_2d_f64(&tf, PH == 1 ? a.u : a.ut, n, n, n, KC, RB) &&
+                    encode_tmap_2d_f64(&tm, PH == 1 ? a.x : a.core, n, (uint64_t)a.r, PH == 1 ? (uint64_t)a.ldx : n, KC, RP);
+    if (!ok) throw Error(CPHIFI_CUDA_ERROR, "sandwich: tensor map encoding failed");
+    kern<<<(unsigned)((a.n + RB - 1) / RB), SW2_T, smem, s>>>(a, tf, tm);
     CPHIFI_CHECK_LAUNCH();
 }
 template <int RP, int PH>
 void launch2_rb(const SandArgs& a, int rb, cudaStream_t s) {
-    // accumulators per thread: RP / 8 columns x RB rows <= 32
+    // accumulators per thread: RP / 8 columns x RB rows <= 32 (RB = 16 measured slower)
     constexpr int RBMAX = 256 / RP >= 8 ? 8 : 256 / RP;
     if (rb >= 8 && RBMAX >= 8) launch2_t<RP, (RBMAX >= 8 ? 8 : RBMAX), PH>(a, s);
     else if (rb >= 4 && RBMAX >= 4) launch2_t<RP, (RBMAX >= 4 ? 4 : RBMAX), PH>(a, s);
@@ -365,9 +368,13 @@ void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
               reinterpret_cast<uintptr_t>(a.ut) % 16 == 0 && reinterpret_cast<uintptr_t>(a.x) % 16 == 0 &&
               reinterpret_cast<uintptr_t>(a.core_out) % 16 == 0;
     if (const char* e = std::getenv("CPHIFI_SANDWICH_V1")) v2 = v2 && std::atoi(e) == 0;
-    if (v2) {  // core column-major n x r (v2 layout)
-        launch2_ph<1>(a, rb, s);
-        launch2_ph<2>(a, rb, s);
+    if (v2) {  // core column-major n x r (v2 layout); about one CTA per SM (each CTA streams all
+               // of X / core from L2, so fewer, taller CTAs cut that traffic)
+        int rb2 = 1;
+        while (rb2 < 8 && (a.n + rb2 - 1) / rb2 > num_sms) rb2 *= 2;
+        if (const char* e = std::getenv("CPHIFI_SANDWICH_RB")) rb2 = std::atoi(e);
+        launch2_ph<1>(a, rb2, s);
+        launch2_ph<2>(a, rb2, s);
         return;
     }
     launch_ph<1>(a, rb, s);

@@ -44,7 +44,7 @@ struct MttkrpArgs {
     double* b = nullptr;      // n0 x r column-major output
     int probe = 0;            // profiling only (CPHIFI_MTTKRP_PROBE, v3): 1 = stream T without the DMMA work,
                               // 2 = DMMA work on stale stages without the stream, 3 = as 2 without the B scaling
-    int l2_ahead = 8;         // v3: tiles of T prefetched into L2 ahead of the shared-memory ring
+    int l2_ahead = 0;         // v3: tiles of T prefetched into L2 ahead of the ring (CPHIFI_MTTKRP_L2AHEAD)
 };
 void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work);
 
