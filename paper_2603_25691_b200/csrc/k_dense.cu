@@ -535,14 +535,16 @@ struct V3 {                           // WR rows per consumer warp
 };
 constexpr int AP3 = BMM + 4;          // T box rows = smem pitch
 constexpr int BKP3 = BK + 4;          // A_1 box rows = smem pitch of the transposed B tile
+// B tile: [j][k] (pitch BKP3) from a column-major B (the MTTKRP's A_1, a GEMM's X), or [k][j]
+// (pitch BN + 4, the 4 extra columns read past the tile or as zero) from a row-major B (BROW)
 template <int BN>
 struct Mttkrp3Smem {
+    static constexpr int BSZ = BN * BKP3 > BK * (BN + 4) ? BN * BKP3 : BK * (BN + 4);
     double a[ST3][BK][AP3];
-    double bt[ST3][BN][BKP3];
-    double w[ST3][BN];
+    double bt[ST3][BSZ];
     uint64_t full[ST3], empty[ST3];
 };
-template <int BN, int WR>
+template <int BN, int WR, bool BROW>
 __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const MttkrpArgs a, const __grid_constant__ CUtensorMap tm_t,
                                                                 const __grid_constant__ CUtensorMap tm_a1, int64_t chunks,
                                                                 int64_t ktiles, const double* __restrict__ wout,
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
     const int ntiles = (int)(te - tb);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rows = (int)min((int64_t)BMM, n0 - i0);
+    auto bidx = [](int k, int j) { return BROW ? k * (BN + 4) + j : j * BKP3 + k; };
     const int bcols = (int)min((int64_t)BN, a.r - j0);
 
     if (threadIdx.x == 0) {
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
 
     if (warp == NC3 / 32) {  // ---- producer warp (one lane) ----
         if (lane == 0) {
-            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + BN * BKP3));
+            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + (BROW ? BK * (BN + 4) : BN * BKP3)));
             // L2 prefetch runs l2_ahead tiles in front of the ring: the shared-memory stages then
             // fill from L2, and the loaded-HBM latency hides behind the prefetch distance
             const int pf = a.l2_ahead;
@@ -606,7 +609,8 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                 }
                 tma::mbar_expect_tx(&sm.full[st], bytes);
                 tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
-                tma::tensor_g2s_2d(&sm.bt[st][0][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
+                if constexpr (BROW) tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)j0, (int)(c1 + a.off1), &sm.full[st]);
+                else tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
             }
         }
     } else {  // ---- consumer warps ----
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
 #pragma unroll
-                        for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][nf * 8 + g][kr];
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][bidx(kr, nf * 8 + g)];
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
@@ -667,7 +671,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
 #pragma unroll
-                        for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][nf * 8 + g][kr] : 0.0;
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][bidx(kr, nf * 8 + g)] : 0.0;
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
@@ -716,21 +720,22 @@ __global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int
     }
 }
 
-template <int BN, int WR>
+template <int BN, int WR, bool BROW = false>
 void launch_v3(const MttkrpArgs& ap, const CUtensorMap& tm_t, const CUtensorMap& tm_a1, int mt, int64_t P, int nt,
                int64_t chunks, int64_t ktiles, const double* wout, double* work, cudaStream_t s) {
     const size_t smem3 = sizeof(Mttkrp3Smem<BN>);
     static bool attr3 = false;
     if (!attr3) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, BROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem3));
         attr3 = true;
     }
-    mttkrp_v3_kernel<BN, WR><<<dim3(mt, (unsigned)P, nt), V3<WR>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks, ktiles,
-                                                                                     wout, work);
+    mttkrp_v3_kernel<BN, WR, BROW><<<dim3(mt, (unsigned)P, nt), V3<WR>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
+                                                                                           ktiles, wout, work);
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
         cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR>);
+        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR, BROW>);
         throw Error(CPHIFI_CUDA_ERROR, std::string("mttkrp_v3 launch: ") + cudaGetErrorString(le) + " regs " +
                                            std::to_string(fa.numRegs) + " maxthreads " + std::to_string(fa.maxThreadsPerBlock));
     }
@@ -780,8 +785,8 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
         if (v3) {
             int wr = 32;
             if (const char* e = std::getenv("CPHIFI_MTTKRP_WR")) wr = std::atoi(e) == 16 ? 16 : 32;
-            if (wr == 16) launch_v3<BN, 16>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
-            else launch_v3<BN, 32>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            if (wr == 16) launch_v3<BN, 16, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            else launch_v3<BN, 32, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
         } else if (v2) {
             static bool attr2 = false;
             if (!attr2) {
@@ -990,10 +995,83 @@ void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_t
     CPHIFI_CHECK_LAUNCH();
 }
 
+// ---- large dense GEMMs through the MTTKRP v3 machinery (tensor-map TMA ring, DMMA) ---------
+// C = A B with A column-major (M x K, the n x n kernel / eigenbasis) and B column- or row-major
+// (K x N, N <= 64): a 2-mode "MTTKRP" with Wout = 1 (exact), split-K partials summed in split
+// order by reduce_epi_kernel, which applies the GEMM epilogue.  (The cluster split-K DMMA GEMM
+// above ran the config-4 contractions at ~49 % of the DMMA peak.)
+__global__ void reduce_epi_kernel(const double* __restrict__ work, int P, int64_t m, int64_t ncols, const GemmArgs g) {
+    const int64_t nn = g.c2 ? max(ncols, g.ld2) : ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * nn; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % m, j = e / m;
+        double acc = 0.0;
+        if (j < ncols)
+            for (int p = 0; p < P; ++p) acc += work[(int64_t)p * m * ncols + e];
+        epilogue_store(g, i, j, acc);
+    }
+}
+
+bool gemm_tma_ok(const GemmArgs& g) {
+    if (const char* e = std::getenv("CPHIFI_GEMM_TMA"))
+        if (std::atoi(e) == 0) return false;
+    const bool bcol = g.b_rs == 1, brow = g.b_cs == 1 && !bcol;
+    const int64_t ldb = bcol ? g.b_cs : g.b_rs;
+    return g.m >= 512 && g.k >= 512 && g.n >= 1 && g.n <= 64 && g.a_rs == 1 && g.a_cs % 2 == 0 && (bcol || brow) &&
+           ldb % 2 == 0 && reinterpret_cast<uintptr_t>(g.a) % 16 == 0 && reinterpret_cast<uintptr_t>(g.b) % 16 == 0 &&
+           g.k < (1LL << 31) && g.m < (1LL << 31);
+}
+
+template <int BN>
+void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
+    static thread_local DevBuf<double> work;
+    static thread_local int work_dev = -1;
+    int dev = 0;
+    CPHIFI_CUDA(cudaGetDevice(&dev));
+    if (work_dev != dev) {
+        work.release();
+        work_dev = dev;
+    }
+    const bool brow = !(g.b_rs == 1);
+    const int mt = (int)((g.m + BMM - 1) / BMM), nt = (int)((g.n + BN - 1) / BN);
+    const int64_t chunks = (g.k + BK - 1) / BK;
+    int64_t P = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms / (mt * nt), chunks));
+    const size_t need = (size_t)P * g.m * g.n + (size_t)g.n + 2;
+    if (work.n < need) work.alloc(need);
+    double* wout = work.get() + (size_t)P * g.m * g.n;
+    MttkrpArgs a;
+    a.d = 2;
+    a.shape[0] = g.m;
+    a.shape[1] = g.k;
+    a.r = g.n;
+    a.t = g.a;
+    a.fac[1] = g.b;
+    a.ld[1] = brow ? g.b_rs : g.b_cs;
+    a.off1 = 0;
+    kr_outer_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(a, 1, wout);  // Wout = 1
+    CPHIFI_CHECK_LAUNCH();
+    CUtensorMap tm_a, tm_b;
+    const bool ok = encode_tmap_2d_f64(&tm_a, g.a, (uint64_t)g.m, (uint64_t)g.k, (uint64_t)g.a_cs, BMM + 4, BK) &&
+                    (brow ? encode_tmap_2d_f64(&tm_b, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.b_rs, BN + 4, BK)
+                          : encode_tmap_2d_f64(&tm_b, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.b_cs, BK + 4, BN));
+    if (!ok) throw Error(CPHIFI_CUDA_ERROR, "gemm: tensor map encoding failed");
+    if (brow) launch_v3<BN, 32, true>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
+    else launch_v3<BN, 32, false>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
+    const int64_t cnt = g.m * (g.c2 ? std::max(g.n, g.ld2) : g.n);
+    reduce_epi_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(work.get(), (int)P, g.m,
+                                                                                                  g.n, g);
+    CPHIFI_CHECK_LAUNCH();
+}
+
 void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     if (g.m <= 0 || g.n <= 0) return;
     if (g.k <= 0) {
         // empty contraction: run a zero-K GEMM (epilogue only) through the S=1 path
+    }
+    if (g.k > 0 && gemm_tma_ok(g)) {
+        if (g.n <= 8) gemm_tma_t<8>(g, num_sms, s);
+        else if (g.n <= 16) gemm_tma_t<16>(g, num_sms, s);
+        else gemm_tma_t<32>(g, num_sms, s);
+        return;
     }
     const int64_t np = (g.n + 7) / 8 * 8;
     if (np <= 8) launch_gemm<8>(g, num_sms, s);
