@@ -1170,67 +1170,44 @@ int cphifi_unaligned_matvec_device(cphifi_unaligned p, const double* x, double* 
     });
 }
 
-// pinned (page-locked or registered) host memory: graph copy nodes may address it directly
-bool is_pinned_host(const void* ptr) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeHost;
-}
-
 // One graph launch instead of three API calls (~4 us each here, profiles/micro/launch_rate.cu):
-// [H2D x, operator, D2H y], captured once per plan, copy nodes re-pointed when the buffers change.
+// x is staged by the host into a plan-owned pinned, device-mapped buffer; the graph copies it to
+// HBM with a kernel (a PCIe read stream, no DMA node), applies the operator and copies y back the
+// same way; the host copies it out.  Fixed staging pointers: the graph is captured once per plan.
 bool host_matvec_graph(cphifi_unaligned p, const double* x, double* y) {
     cphifi_ctx ctx = p->obs->ctx;
     if (p->hv_failed || is_multi(p)) return false;
     if (const char* e = std::getenv("CPHIFI_HOST_GRAPH"))
         if (std::atoi(e) == 0) return false;
-    const size_t bytes = sizeof(double) * p->n * p->r;
-    if (p->hv_exec && (p->hv_x != x || p->hv_y != y)) {
-        if (!is_pinned_host(x) || !is_pinned_host(y)) return false;
-        if (cudaGraphExecMemcpyNodeSetParams1D(p->hv_exec, p->hv_h2d, p->vx.get(), x, bytes, cudaMemcpyHostToDevice) !=
-                cudaSuccess ||
-            cudaGraphExecMemcpyNodeSetParams1D(p->hv_exec, p->hv_d2h, y, p->vy.get(), bytes, cudaMemcpyDeviceToHost) !=
-                cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        p->hv_x = x;
-        p->hv_y = y;
-    }
+    const int64_t nr = p->n * p->r;
+    const size_t bytes = sizeof(double) * nr;
     if (!p->hv_exec) {
-        if (!is_pinned_host(x) || !is_pinned_host(y)) return false;
         if (p->op == 1) ensure_gram(p);
         matvec_dev(p, p->vx.get(), p->vy.get());  // lazily built state and launch attributes first
         CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
         cudaGraph_t g = nullptr;
         try {
-            CPHIFI_CUDA(cudaGraphCreate(&g, 0));
-            cudaGraphNode_t h2dn, d2hn, body;
-            CPHIFI_CUDA(cudaGraphAddMemcpyNode1D(&h2dn, g, nullptr, 0, p->vx.get(), x, bytes, cudaMemcpyHostToDevice));
-            cudaGraph_t bg = nullptr;
+            if (!p->hv_hx) CPHIFI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->hv_hx), bytes, cudaHostAllocMapped));
+            if (!p->hv_hy) CPHIFI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->hv_hy), bytes, cudaHostAllocMapped));
+            double *dhx = nullptr, *dhy = nullptr;
+            CPHIFI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhx), p->hv_hx, 0));
+            CPHIFI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhy), p->hv_hy, 0));
             CPHIFI_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
             try {
+                copy_doubles(p->vx.get(), dhx, nr, ctx->stream);
                 matvec_dev(p, p->vx.get(), p->vy.get());
+                copy_doubles(dhy, p->vy.get(), nr, ctx->stream);
             } catch (...) {
-                cudaStreamEndCapture(ctx->stream, &bg);
-                if (bg) cudaGraphDestroy(bg);
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(ctx->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
                 throw;
             }
-            CPHIFI_CUDA(cudaStreamEndCapture(ctx->stream, &bg));
-            CPHIFI_CUDA(cudaGraphAddChildGraphNode(&body, g, &h2dn, 1, bg));
-            cudaGraphDestroy(bg);
-            CPHIFI_CUDA(cudaGraphAddMemcpyNode1D(&d2hn, g, &body, 1, y, p->vy.get(), bytes, cudaMemcpyDeviceToHost));
+            CPHIFI_CUDA(cudaStreamEndCapture(ctx->stream, &g));
             cudaGraphExec_t ex = nullptr;
             CPHIFI_CUDA(cudaGraphInstantiate(&ex, g, 0));
             p->hv_graph = g;
             p->hv_exec = ex;
-            p->hv_h2d = h2dn;
-            p->hv_d2h = d2hn;
-            p->hv_x = x;
-            p->hv_y = y;
         } catch (const Error& e) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
@@ -1239,8 +1216,10 @@ bool host_matvec_graph(cphifi_unaligned p, const double* x, double* y) {
             return false;
         }
     }
+    std::memcpy(p->hv_hx, x, bytes);
     CPHIFI_CUDA(cudaGraphLaunch(p->hv_exec, ctx->stream));
     CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(y, p->hv_hy, bytes);
     return true;
 }
 

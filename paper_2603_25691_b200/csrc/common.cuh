@@ -171,13 +171,12 @@ struct cphifi_unaligned_s {
     cphifi::DevBuf<double> pcg_hist;          // device residual history
     cudaGraph_t pcg_graph = nullptr;
     cudaGraphExec_t pcg_exec = nullptr;
-    // host-buffer matvec (cphifi_unaligned_matvec) as one graph [H2D, operator, D2H] for pinned
-    // buffers; the copy nodes are re-pointed per call
+    // host-buffer matvec (cphifi_unaligned_matvec) as one graph [copy in, operator, copy out]
+    // over plan-owned pinned, device-mapped staging buffers hv_hx / hv_hy
     cudaGraph_t hv_graph = nullptr;
     cudaGraphExec_t hv_exec = nullptr;
-    cudaGraphNode_t hv_h2d = nullptr, hv_d2h = nullptr;
-    const double* hv_x = nullptr;
-    double* hv_y = nullptr;
+    double* hv_hx = nullptr;
+    double* hv_hy = nullptr;
     bool hv_failed = false;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
     bool pcg_graph_failed = false;
@@ -186,6 +185,8 @@ struct cphifi_unaligned_s {
         if (pcg_graph) cudaGraphDestroy(pcg_graph);
         if (hv_exec) cudaGraphExecDestroy(hv_exec);
         if (hv_graph) cudaGraphDestroy(hv_graph);
+        if (hv_hx) cudaFreeHost(hv_hx);
+        if (hv_hy) cudaFreeHost(hv_hy);
     }
 };
 

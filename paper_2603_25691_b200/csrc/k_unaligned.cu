@@ -145,6 +145,12 @@ __global__ void pcg_ctl_kernel(const PcgState* st, PcgCtl* c, cudaGraphCondition
     }
 }
 
+// 16-byte copies (either side may be mapped host memory: one PCIe stream instead of a DMA node)
+__global__ void copy16_kernel(double2* __restrict__ dst, const double2* __restrict__ src, int64_t n2) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 __global__ void axpby_kernel(double* y, const double* a, double alpha, const double* b, double beta, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = alpha * a[i] + beta * b[i];
@@ -251,6 +257,16 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
 }
 void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s) {
     pcg_ctl_kernel<<<1, 1, 0, s>>>(st, c, h);
+    CPHIFI_CHECK_LAUNCH();
+}
+void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s) {
+    if (n % 2 != 0 || reinterpret_cast<uintptr_t>(dst) % 16 != 0 || reinterpret_cast<uintptr_t>(src) % 16 != 0) {
+        CPHIFI_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDefault, s));
+        return;
+    }
+    const int64_t n2 = n / 2;
+    copy16_kernel<<<(unsigned)std::min<int64_t>((n2 + 255) / 256, 64), 256, 0, s>>>(
+        reinterpret_cast<double2*>(dst), reinterpret_cast<const double2*>(src), n2);
     CPHIFI_CHECK_LAUNCH();
 }
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n, cudaStream_t s) {

@@ -203,6 +203,8 @@ void pcg_step_b(const double* r, const double* z, double* p, int64_t n, PcgState
 // init: rz = r.z, rr = r.r, rel = sqrt(rr)/bnorm, p = z
 void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* st, double* partial,
               cudaStream_t s);
+// dst <- src (n doubles), a kernel copy when 16-byte aligned (mapped host memory allowed)
+void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s);
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n,
            cudaStream_t s);  // y = alpha*a + beta*b
 

@@ -7,7 +7,7 @@ siblings (selected by the library's CPHIFI_* switches, read per call or per plan
     solve and the preconditioner                                 (aligned.hpp:41-54, unaligned.hpp:135-139)
   * PCG device-resident CUDA-graph loop vs the host loop: identical iterates and history
     (solvers.hpp:38-88)
-  * host-buffer matvec through the cached [H2D, operator, D2H] graph vs plain calls
+  * host-buffer matvec through the cached [copy in, operator, copy out] graph vs plain calls
   * equal-count vs row-aligned partition of the fused operator (split rows)
 
 Tolerances: 1e-12 relative against the oracle (fp64 summation order only); bitwise equality
