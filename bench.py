@@ -152,6 +152,7 @@ def secondary(args, ctx, cp, p, c, lib, x, y, stream, flush):
     attempt("config1_gram_matvec_ms_l2_flushed", lambda: bs.gram_matvec_ms(p, lib, x, y, stream, flush))
     attempt("config0_aligned", lambda: bs.aligned("config0", ctx, 20, fp64))
     attempt("config2_aligned", lambda: bs.aligned("config2", ctx, 10, fp64))
+    attempt("als_infinite_update", lambda: bs.als_updates(ctx, p, c))
     if args.large:
         attempt("config3", lambda: bs.large("config3", ctx, fp64_tf=fp64))
         attempt("config4", lambda: bs.large("config4", ctx, fp64_tf=fp64))

@@ -181,3 +181,32 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     del p, obs
     torch.cuda.empty_cache()
     return out
+
+
+def als_updates(ctx, p, c):
+    """ALS infinite-mode update on device: config 1 (unaligned, PCG warm-started
+    from the previous W as AlsState does) and config 2 (aligned decoupled), wall clock per update
+    plus the device-timed split (solve / factor update + error terms)."""
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import configs
+    out = {}
+    cfg = cp.PcgConfig(c.tol, c.max_iter)
+    u = cp.update_infinite_mode_unaligned(p, cfg)
+    t0 = time.perf_counter()
+    u2 = cp.update_infinite_mode_unaligned(p, cfg, warm_start=u.w)
+    out["config1_unaligned"] = {"wall_s_warm": time.perf_counter() - t0, "relative_error": u.relative_error,
+                                "iterations_cold": u.report.iterations, "iterations_warm": u2.report.iterations,
+                                "solve_s": u.solve_s, "update_and_error_s": u.update_s}
+    c2 = configs.config2()
+    n, r = c2.shape[0], c2.r
+    mode = cp.RkhsMode(c2.points, c2.ell, c2.lam, ctx=ctx)
+    t = cp.DenseTensor(c2.shape, c2.tensor)
+    model = cp.KruskalModel([np.zeros((n, r))] + c2.factors[1:])
+    cp.update_infinite_mode_aligned(t, model, 0, mode)  # eig(K), tensor upload, ||T||^2 once
+    t0 = time.perf_counter()
+    ua = cp.update_infinite_mode_aligned(t, model, 0, mode)
+    out["config2_aligned"] = {"wall_s": time.perf_counter() - t0, "relative_error": ua.relative_error,
+                              "aligned_residual": ua.residual, "solve_s": ua.solve_s,
+                              "update_and_error_s": ua.update_s,
+                              "note": "relative error via ||T||^2 - 2<A,B> + 1'(A'A o V)1: no N-sized pass"}
+    return out

@@ -218,6 +218,31 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                          const double* const* factors, double* w_out, double* b_out,
                          double* v_out);
 
+/* ---- ALS infinite-mode update ----------------------------------------
+ * AlsState::update_infinite_mode (als.hpp:170-218) followed by AlsState::relative_error
+ * (als.hpp:221-237) and this mode's objective term (als.hpp:243-255), one device pass:
+ *   W = the subproblem solve, A_k = K W (the factor update, als.hpp:214),
+ *   relative_error of the model with A_k in place, lambda * trace(W' K W).
+ * Unaligned: PCG (warm_start as solve_unaligned_pcg; the reference passes the previous W), the
+ * fit over the observed entries (plans with coalesced duplicates are rejected: their values are
+ * sums).  Aligned: MTTKRP + Gram + eig(V) + decoupled solve; `residual` = aligned_residual
+ * (aligned.hpp:104-108); the fit uses ||T - M||^2 = ||T||^2 - 2 <A_k, B> + 1'(A_k'A_k o V)1
+ * (no N-sized reconstruction; absolute error of the squared fit ~1e-15 ||T||^2). */
+typedef struct cphifi_als_report {
+    double relative_error; /* ||data - model|| / ||data|| after the update */
+    double data_norm;      /* ||data|| (observed entries, or the whole tensor) */
+    double reg;            /* lambda * trace(W' K W) */
+    double residual;       /* aligned: aligned_residual(p, W); unaligned: PCG relative residual */
+    double solve_s;        /* device time of the solve (incl. MTTKRP / RHS) */
+    double update_s;       /* device time of A_k = K W and the error terms */
+} cphifi_als_report;
+int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_config* cfg,
+                                         const double* warm_start, double* w_out, double* a_out,
+                                         cphifi_solve_report* solve_report, cphifi_als_report* als);
+int cphifi_als_update_infinite_aligned(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
+                                       const double* const* factors, double* w_out, double* a_out,
+                                       cphifi_als_report* als);
+
 /* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
  * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup: wall clock of the
  * warm-up pass; the timed passes reuse it), [3] decoupled rotate/divide/rotate (each phase of a

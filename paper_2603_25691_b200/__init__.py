@@ -32,6 +32,7 @@ __all__ = [
     "Context", "default_context", "RkhsMode", "SymEig", "ObservationSet", "DenseTensor", "KruskalModel",
     "sample_uniform", "full_observations", "make_unaligned_subproblem", "UnalignedSubproblem",
     "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
+    "AlsUpdate", "update_infinite_mode_unaligned", "update_infinite_mode_aligned",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
     "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
@@ -675,6 +676,66 @@ def solve_aligned_decoupled(p: AlignedSubproblem, v_eig: SymEig | None = None) -
         call("cphifi_solve_aligned_decoupled", p.mode.handle, r, _dp(b), _dp(v), c_double_p(), c_double_p(),
              _dp(w))
     return w
+
+
+# ---- als.hpp: the infinite-mode update of one ALS sweep -----------------
+@dataclass
+class AlsUpdate:
+    """AlsState::update_infinite_mode (als.hpp:170-218) + relative_error (:221-237) + this mode's
+    objective term lambda trace(W'KW) (:243-255), computed in one device pass."""
+    w: np.ndarray
+    a: np.ndarray                # the updated factor A_k = K W (als.hpp:214)
+    relative_error: float
+    data_norm: float
+    reg: float
+    residual: float              # aligned_residual (aligned) / PCG relative residual (unaligned)
+    solve_s: float = 0.0
+    update_s: float = 0.0
+    report: SolveReport | None = None
+
+    def objective_term(self) -> float:
+        """(relative_error * data_norm)^2 + lambda trace(W'KW): objective_from_error with only this
+        infinite mode (als.hpp:243-255)."""
+        fit = self.relative_error * self.data_norm
+        return fit * fit + self.reg
+
+
+def _als_from(c, w, a, report=None) -> AlsUpdate:
+    return AlsUpdate(w, a, c.relative_error, c.data_norm, c.reg, c.residual, c.solve_s, c.update_s, report)
+
+
+def update_infinite_mode_unaligned(p: UnalignedSubproblem, cfg: PcgConfig | None = None,
+                                   warm_start=None) -> AlsUpdate:
+    """The unaligned branch of update_infinite_mode (PCG, als.hpp:198-210) on device."""
+    cfg = cfg or PcgConfig()
+    n, r = p.n(), p.r()
+    ccfg = _capi.PcgConfigC(cfg.tol, int(cfg.max_iter), int(bool(cfg.record_history)))
+    cap = int(cfg.max_iter) + 2
+    hist = np.zeros(cap)
+    rep = _capi.SolveReportC()
+    rep.residual_history = _dp(hist)
+    rep.history_capacity = cap
+    w = np.zeros((n, r), order="F")
+    a = np.zeros((n, r), order="F")
+    ws = None if warm_start is None else _f64(warm_start)
+    c = _capi.AlsReportC()
+    call("cphifi_als_update_infinite_unaligned", p.handle, ctypes.byref(ccfg),
+         _dp(ws) if ws is not None else c_double_p(), _dp(w), _dp(a), ctypes.byref(rep), ctypes.byref(c))
+    sr = SolveReport(rep.iterations, rep.relative_residual, rep.wall_time_s, bool(rep.converged),
+                     list(hist[: rep.history_len]) if cfg.record_history else [], rep.setup_s, rep.matvecs)
+    return _als_from(c, w, a, sr)
+
+
+def update_infinite_mode_aligned(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode) -> AlsUpdate:
+    """The aligned decoupled branch of update_infinite_mode (als.hpp:181-197) on device."""
+    dt = _device_tensor(t, mode.ctx)
+    arrs, ptrs = _factor_array(model.factors, k)
+    n, r = mode.size(), model.rank()
+    w = np.zeros((n, r), order="F")
+    a = np.zeros((n, r), order="F")
+    c = _capi.AlsReportC()
+    call("cphifi_als_update_infinite_aligned", dt.handle, mode.handle, k, r, ptrs, _dp(w), _dp(a), ctypes.byref(c))
+    return _als_from(c, w, a)
 
 
 def aligned_solve(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode):

@@ -28,6 +28,17 @@ class PcgConfigC(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("record_history", ctypes.c_int32)]
 
 
+class AlsReportC(ctypes.Structure):
+    _fields_ = [
+        ("relative_error", ctypes.c_double),
+        ("data_norm", ctypes.c_double),
+        ("reg", ctypes.c_double),
+        ("residual", ctypes.c_double),
+        ("solve_s", ctypes.c_double),
+        ("update_s", ctypes.c_double),
+    ]
+
+
 class SolveReportC(ctypes.Structure):
     _fields_ = [
         ("iterations", ctypes.c_int32),
@@ -120,6 +131,10 @@ _SIGS = [
      [_H, ctypes.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, c_double_p]),
+    ("cphifi_als_update_infinite_unaligned", ctypes.c_int,
+     [_H, ctypes.c_void_p, c_double_p, c_double_p, c_double_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("cphifi_als_update_infinite_aligned", ctypes.c_int,
+     [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, ctypes.c_void_p]),
     ("cphifi_aligned_solve_timed", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), ctypes.c_int, c_double_p, c_double_p]),
     ("cphifi_synth_observations", ctypes.c_int,

@@ -1894,4 +1894,154 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, co
     });
 }
 
+
+// ---- ALS infinite-mode update (als.hpp:170-255) ---------------------------------------------
+int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_config* cfg, const double* warm_start,
+                                         double* w_out, double* a_out, cphifi_solve_report* solve_report,
+                                         cphifi_als_report* als) {
+    return guard([&] {
+        need(p, "p");
+        need(cfg, "cfg");
+        need(w_out, "w_out");
+        need(als, "als");
+        cphifi_obs o = p->obs;
+        if (o->coalesced)
+            throw_invalid("relative_error: a plan with coalesced duplicates has no per-draw values");
+        cphifi_ctx ctx = o->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const int64_t n = p->n, r = p->r, nr = n * r;
+        cudaEvent_t ev[3];
+        for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
+        CPHIFI_CUDA(cudaEventRecord(ev[0], s));
+        cphifi_solve_report rep{};
+        if (solve_report) rep = *solve_report;
+        const int st = cphifi_solve_unaligned_pcg(p, cfg, &rep, warm_start, w_out);
+        if (st != CPHIFI_OK) {
+            for (auto& e : ev) cudaEventDestroy(e);
+            throw Error(st, g_last_error);
+        }
+        if (solve_report) *solve_report = rep;
+        CPHIFI_CUDA(cudaEventRecord(ev[1], s));
+        const double* wdev = p->pcg_vec.get() + nr;  // the solution stays in the plan's x slot
+        DevBuf<double> a(nr), arm((size_t)n * p->rp), scal(4), part(std::max<int64_t>(sq_residual_blocks(o->q_local), 64) + 80);
+        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, wdev, n, a.get(), n);  // A_k = K W (als.hpp:214)
+        pack_rows(a.get(), n, n, r, p->rp, arm.get(), s);
+        SqResidualArgs ra;
+        ra.n = n; ra.r = r; ra.rp = p->rp; ra.q = o->q_local; ra.ldq = o->ldq; ra.dother = o->d - 1;
+        ra.row_ptr = o->row_ptr.get(); ra.idx = o->idx_o.get(); ra.values = o->values.get();
+        ra.fac = p->fac.get();
+        for (int m = 0; m < o->d - 1; ++m) ra.fac_off[m] = p->fac_off[m];
+        ra.ak = arm.get();
+        sq_residual(ra, part.get(), scal.get(), s);                                          // [0] fit^2
+        const int64_t nbn = std::min<int64_t>(std::max<int64_t>(1, (o->q_local + 2047) / 2048), 1024);
+        if (o->q_local > 0) sq_norm(o->values.get(), o->q_local, part.get(), nbn, scal.get() + 1, s);  // [1] ||v||^2
+        else CPHIFI_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
+        CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+        dot_to(wdev, a.get(), nr, part.get(), scal.get() + 2, s);                            // [2] trace(W'KW)
+        allreduce(ctx, scal.get(), 2);  // sharded observations: sum the fit and norm terms
+        CPHIFI_CUDA(cudaEventRecord(ev[2], s));
+        double h[3];
+        d2h_sync(h, scal.get(), sizeof(double) * 3, s);
+        if (a_out) d2h_sync(a_out, a.get(), sizeof(double) * nr, s);
+        float m0 = 0.f, m1 = 0.f;
+        CPHIFI_CUDA(cudaEventElapsedTime(&m0, ev[0], ev[1]));
+        CPHIFI_CUDA(cudaEventElapsedTime(&m1, ev[1], ev[2]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        const double dn = std::sqrt(h[1]);
+        if (dn == 0.0) throw_runtime("relative_error: zero data norm");
+        als->relative_error = std::sqrt(h[0]) / dn;
+        als->data_norm = dn;
+        als->reg = p->mode->lambda * h[2];
+        als->residual = rep.relative_residual;
+        als->solve_s = m0 * 1e-3;
+        als->update_s = m1 * 1e-3;
+    });
+}
+
+int cphifi_als_update_infinite_aligned(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
+                                       const double* const* factors, double* w_out, double* a_out,
+                                       cphifi_als_report* als) {
+    return guard([&] {
+        need(t, "tensor");
+        need(mode, "mode");
+        need(factors, "factors");
+        need(w_out, "w_out");
+        need(als, "als");
+        if (k < 0 || k >= t->d) throw_invalid("unfold: mode out of range");
+        if (mode->n != t->shape[k]) throw_invalid("aligned: kernel size mismatch");
+        cphifi_ctx ctx = t->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        mode_eig_once(mode);
+        const int64_t n = mode->n, nr = n * r;
+        cudaEvent_t ev[3];
+        for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
+        DevBuf<double> fbuf, b(nr), v(r * r), uv(r * r), sv(r), w(nr), t1, core, work;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
+        CPHIFI_CUDA(cudaEventRecord(ev[0], s));
+        mttkrp_dev(t, k, r, fptr, b.get(), work);
+        gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), s);
+        device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());
+        const int* flag = decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+        CPHIFI_CUDA(cudaEventRecord(ev[1], s));
+        DevBuf<double> a(nr), wv(nr), res(nr), g(r * r), scal(8), part(1024 + 80);
+        gemm_nn(ctx, n, r, n, mode->kernel.get(), n, w.get(), n, a.get(), n);  // A_k = K W
+        // aligned_residual: || K W V + lambda W - B || / ||B||  (as K (W V), one association)
+        gemm_nn(ctx, n, r, r, w.get(), n, v.get(), r, wv.get(), n);
+        GemmArgs ga;
+        ga.m = n; ga.n = r; ga.k = n;
+        ga.a = mode->kernel.get(); ga.a_rs = 1; ga.a_cs = n;
+        ga.b = wv.get(); ga.b_rs = 1; ga.b_cs = n;
+        ga.c = res.get(); ga.c_rs = 1; ga.c_cs = n;
+        ga.epi = EPI_AXPY2; ga.e1 = w.get(); ga.e2 = b.get(); ga.ld_e = n; ga.beta1 = mode->lambda; ga.beta2 = -1.0;
+        gemm(ga, ctx->num_sms, s);
+        // G = A_k' A_k
+        GemmArgs gg;
+        gg.m = r; gg.n = r; gg.k = n;
+        gg.a = a.get(); gg.a_rs = n; gg.a_cs = 1;
+        gg.b = a.get(); gg.b_rs = 1; gg.b_cs = n;
+        gg.c = g.get(); gg.c_rs = 1; gg.c_cs = r;
+        gemm(gg, ctx->num_sms, s);
+        auto dot = [&](const double* x, const double* y, int64_t cnt, double* out) {
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            dot_to(x, y, cnt, part.get(), out, s);
+        };
+        dot(res.get(), res.get(), nr, scal.get() + 0);  // ||R||^2
+        dot(b.get(), b.get(), nr, scal.get() + 1);      // ||B||^2
+        dot(a.get(), b.get(), nr, scal.get() + 2);      // <A_k, B>
+        dot(g.get(), v.get(), r * r, scal.get() + 3);   // 1'(A_k'A_k o V)1
+        dot(w.get(), a.get(), nr, scal.get() + 4);      // trace(W' K W)
+        if (!t->have_norm) {  // ||T||^2 of the local slab, once per tensor, summed over shards
+            int64_t cnt = n * (t->slab_hi - t->slab_lo);
+            for (int m = 2; m < t->d; ++m) cnt *= t->shape[m];
+            t->norm2.alloc(1);
+            sq_norm(t->data.get(), cnt, part.get(), 1024, t->norm2.get(), s);
+            allreduce(ctx, t->norm2.get(), 1);
+            t->have_norm = true;
+        }
+        CPHIFI_CUDA(cudaMemcpyAsync(scal.get() + 5, t->norm2.get(), sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CPHIFI_CUDA(cudaEventRecord(ev[2], s));
+        double h[6];
+        d2h_sync(h, scal.get(), sizeof(double) * 6, s);
+        decoupled_check(flag);
+        d2h_sync(w_out, w.get(), sizeof(double) * nr, s);
+        if (a_out) d2h_sync(a_out, a.get(), sizeof(double) * nr, s);
+        float m0 = 0.f, m1 = 0.f;
+        CPHIFI_CUDA(cudaEventElapsedTime(&m0, ev[0], ev[1]));
+        CPHIFI_CUDA(cudaEventElapsedTime(&m1, ev[1], ev[2]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        const double tn = std::sqrt(h[5]);
+        if (tn == 0.0) throw_runtime("relative_error: zero data norm");
+        const double fit2 = h[5] - 2.0 * h[2] + h[3];
+        als->relative_error = std::sqrt(std::max(fit2, 0.0)) / tn;
+        als->data_norm = tn;
+        als->reg = mode->lambda * h[4];
+        const double bn = std::sqrt(h[1]);
+        als->residual = bn == 0.0 ? std::sqrt(h[0]) : std::sqrt(h[0]) / bn;
+        als->solve_s = m0 * 1e-3;
+        als->update_s = m1 * 1e-3;
+    });
+}
 }  // extern "C"

@@ -196,6 +196,8 @@ struct cphifi_tensor_s {
     std::vector<int64_t> shape;        // full shape
     int64_t slab_lo = 0, slab_hi = 0;  // mode-1 slice range held locally
     cphifi::DevBuf<double> data;       // local slab, column-major n0 x (hi-lo) x n2 x ...
+    cphifi::DevBuf<double> norm2;      // ||T||^2 over all shards (ALS relative error), lazily
+    bool have_norm = false;
 };
 
 struct cphifi_rng_s;

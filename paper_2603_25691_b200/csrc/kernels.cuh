@@ -208,6 +208,23 @@ void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s);
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n,
            cudaStream_t s);  // y = alpha*a + beta*b
 
+// ---- ALS error terms (k_als.cu) ----------------------------------------
+struct SqResidualArgs {
+    int64_t n = 0, r = 0, rp = 0, q = 0, ldq = 0;
+    int dother = 0;
+    const int64_t* row_ptr = nullptr;  // CSR over i_k (n + 1)
+    const int32_t* idx = nullptr;      // dother columns of stride ldq, other modes ascending
+    const double* values = nullptr;    // q
+    const double* fac = nullptr;       // packed row-major rp-padded other-mode factors
+    int64_t fac_off[8] = {0};
+    const double* ak = nullptr;        // the updated mode-k factor, n x rp row-major
+};
+int64_t sq_residual_blocks(int64_t q);
+// *out = sum_l (v_l - <A_k(i_k(l),:), z_l>)^2 ; partial >= sq_residual_blocks(q) doubles
+void sq_residual(const SqResidualArgs& a, double* partial, double* out, cudaStream_t s);
+// *out = ||x||^2 with nb blocks (partial >= nb doubles)
+void sq_norm(const double* x, int64_t n, double* partial, int64_t nb, double* out, cudaStream_t s);
+
 // ---- observation plan helpers ------------------------------------------------------------
 void check_range(const int32_t* idx, int d, int64_t q, const int64_t* shape_dev, int* flag, cudaStream_t s);
 void linear_index(const int32_t* idx, int d, int64_t q, const int64_t* shape, uint64_t* lin, cudaStream_t s);

@@ -1,0 +1,109 @@
+"""GPU: the ALS infinite-mode update — update_infinite_mode (als.hpp:170-218),
+relative_error (als.hpp:221-237) and the objective term (als.hpp:243-255) — against numpy
+restatements of the reference on the same seeded inputs.
+
+Tolerances: W, A_k = K W and the unaligned relative error 1e-12 relative (fp64 summation order);
+aligned_residual is rounding-level for the exact decoupled solve (< 1e-9, 1e-10 absolute); the aligned relative error comes from ||T||^2 - 2<A,B> + 1'(A'A o V)1, whose
+cancellation bounds the absolute error of the squared error by ~1e-15 ||T||^2: 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import refinst as ri
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cp(ctx):
+    import paper_2603_25691_b200 as cp
+    return cp
+
+
+def _fitted(a_k, others, idx):
+    """gather_rows with A_k in place of Xhat (observations.hpp:142-198), modes ascending."""
+    z = others[0][idx[1]]
+    for m in range(1, len(others)):
+        z = z * others[m][idx[m + 1]]
+    return np.einsum("lj,lj->l", a_k[idx[0]], z)
+
+
+def test_unaligned_update_config1(cp):
+    from paper_2603_25691_b200 import configs
+    c = configs.config1()
+    n, r = c.shape[0], c.r
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    model = cp.KruskalModel([np.zeros((n, r))] + c.factors[1:])
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(c.shape, c.idx, c.vals), model, 0, mode, c.rho)
+    cfg = cp.PcgConfig(c.tol, c.max_iter)
+    u = cp.update_infinite_mode_unaligned(p, cfg)
+    w_ref = cp.solve_unaligned_pcg(p, cfg)
+    assert np.array_equal(u.w, w_ref)
+    a = kern @ u.w
+    assert ri.rel(u.a, a) < 1e-12
+    idx = np.asarray(c.idx)
+    res = np.asarray(c.vals) - _fitted(a, c.factors[1:], idx)
+    vn = np.linalg.norm(c.vals)
+    assert abs(u.data_norm - vn) <= 1e-12 * vn
+    assert abs(u.relative_error - np.linalg.norm(res) / vn) <= 1e-12 * (np.linalg.norm(res) / vn)
+    assert abs(u.reg - c.lam * np.trace(u.w.T @ kern @ u.w)) <= 1e-12 * abs(u.reg)
+    assert u.report.converged and u.residual <= c.tol
+    # warm start from the previous W (als.hpp:178-180): converges immediately to the same fit
+    u2 = cp.update_infinite_mode_unaligned(p, cfg, warm_start=u.w)
+    assert u2.report.iterations <= 1 and abs(u2.relative_error - u.relative_error) < 1e-9
+
+
+def test_unaligned_update_small_orders(cp):
+    g = cp.Mt19937_64(77)
+    for shape, r, q in (([12, 5, 4], 3, 150), ([9, 4, 3, 3], 2, 80), ([20, 30], 4, 300)):
+        inst = ri.Inst(shape, r, q, 0, 1.5, 0.1, 1e-6, 300 + q)
+        mode = cp.RkhsMode(inst.points, inst.sigma, inst.lam)
+        p = cp.make_unaligned_subproblem(cp.ObservationSet(inst.shape, inst.idx, inst.vals),
+                                         cp.KruskalModel(inst.factors), 0, mode, inst.rho)
+        u = cp.update_infinite_mode_unaligned(p, cp.PcgConfig(1e-10, 200))
+        a = mode.kernel() @ u.w
+        idx = np.asarray(inst.idx)
+        res = np.asarray(inst.vals) - _fitted(a, inst.factors[1:], idx)
+        rel = np.linalg.norm(res) / np.linalg.norm(inst.vals)
+        assert abs(u.relative_error - rel) <= 1e-12 * max(rel, 1e-300), shape
+    # coalesced plans carry summed values: no per-draw fit
+    c_obs = cp.ObservationSet([4, 3, 3], [[0, 0, 1], [1, 1, 2], [2, 2, 0]], [1.0, 2.0, 3.0], multiset=True,
+                              coalesce=True)
+    modes = cp.RkhsMode(ri.identity_points(4), 1.0, 0.1)
+    pc = cp.make_unaligned_subproblem(c_obs, cp.KruskalModel(ri.random_model([4, 3, 3], 2, g)), 0, modes, 1e-6)
+    with pytest.raises(cp.CphifiInvalidArgument, match="coalesced"):
+        cp.update_infinite_mode_unaligned(pc)
+
+
+@pytest.mark.parametrize("which", ["config0"])
+def test_aligned_update(cp, which):
+    from paper_2603_25691_b200 import configs
+    c = getattr(configs, which)()
+    n, r = c.shape[0], c.r
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    t = cp.DenseTensor(c.shape, c.tensor)
+    model = cp.KruskalModel([np.zeros((n, r))] + c.factors[1:])
+    u = cp.update_infinite_mode_aligned(t, model, 0, mode)
+    w_ref, b, v = cp.aligned_solve(t, model, 0, mode)
+    assert ri.rel(u.w, w_ref) < 1e-12
+    a = kern @ u.w
+    assert ri.rel(u.a, a) < 1e-12
+    # aligned_residual (aligned.hpp:104-108)
+    # (the decoupled solve is exact up to rounding: both residuals are rounding-level, compared
+    # in absolute terms)
+    res = kern @ u.w @ v + c.lam * u.w - b
+    res_np = np.linalg.norm(res) / np.linalg.norm(b)
+    assert u.residual < 1e-9 and res_np < 1e-9 and abs(u.residual - res_np) < 1e-10
+    # relative_error against the materialised kruskal_full (tensor.hpp:167-171)
+    full = np.einsum("ir,jr,kr->ijk", a, c.factors[1], c.factors[2])
+    tt = c.tensor.reshape(c.shape, order="F")
+    rel = np.linalg.norm(tt - full) / np.linalg.norm(tt)
+    assert abs(u.data_norm - np.linalg.norm(tt)) <= 1e-12 * np.linalg.norm(tt)
+    assert abs(u.relative_error - rel) <= 1e-9 * rel, (u.relative_error, rel)
+    # trace(W'KW) = <W, KW> sums products of |W| ~ 1e4 (ill-conditioned K) into ~3e3: condition
+    # ~1e6, so the two association orders agree to ~1e-9 relative
+    assert abs(u.reg - c.lam * np.trace(u.w.T @ kern @ u.w)) <= 1e-7 * abs(u.reg)
+    assert np.isfinite(u.objective_term())
