@@ -261,8 +261,13 @@ def main():
     # system, profiles/micro/launch_rate.cu) are measured next to it as value_plain_launch.
     gms = (ctypes.c_float * args.steps)()
     with ClockSampler(local) as clk:
-        _capi.check(lib.cphifi_unaligned_matvec_graph_timed(p.handle, x.data_ptr(), y.data_ptr(), flush.data_ptr(),
-                                                            flush.numel() * 4, args.steps, gms))
+        if world == 1:
+            _capi.check(lib.cphifi_unaligned_matvec_graph_timed(p.handle, x.data_ptr(), y.data_ptr(),
+                                                                flush.data_ptr(), flush.numel() * 4, args.steps, gms))
+        else:  # multi-GPU: NCCL stays outside graph capture; plain launches, same events
+            for i in range(args.steps):
+                step(evs[i])
+            gms[:] = [a.elapsed_time(b) for a, b in evs]
         torch.cuda.synchronize()
     total_ms = float(sum(gms))
     for i in range(args.steps):
@@ -327,7 +332,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1)",
             "config": {"workload": "config1: unaligned 200x100x100, q=200000, r=10, lambda=1e-3, rho=1e-6",
                        "l2": "flushed before every timed step (256 MB memset node); working set 3.1 MB",
-                       "timing": "K steps in one CUDA graph, CUDA events around each operator application",
+                       "timing": ("K steps in one CUDA graph, CUDA events around each operator application"
+                                  if world == 1 else "plain launches, CUDA events around each application"),
                        "parallelism": f"obs-sharded x{world}, n x r all-reduce per step"},
             "roofline": {"bound": "hbm", "kernel": "fused_matvec_kernel (whole operator)" if fused_whole
                          else "fused_matvec_kernel (scatter-gather + fix-up)", "achieved": achieved,
