@@ -218,6 +218,17 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                          const double* const* factors, double* w_out, double* b_out,
                          double* v_out);
 
+/* ---- observation files ------------------------------------------------
+ * Text: the reference format (io.hpp:93-131): `shape: n1 .. nd`, then lines `i1 .. id value`,
+ * 1-based, parsed on all host threads.  Binary: the same header line, `cphifi-obs-binary 1 q <q>`,
+ * then d int32 index columns (0-based, SoA) and q fp64 values — what cphifi_obs_create takes.
+ * cphifi_obs_file_info detects the format (*binary) and returns d, shape[0..d) (d <= 8) and q;
+ * cphifi_obs_file_read fills idx_soa (d x q) and values (q).  Errors reuse io.hpp's messages. */
+int cphifi_obs_file_info(const char* path, int* d, int64_t* shape, int64_t* q, int* binary);
+int cphifi_obs_file_read(const char* path, int d, int64_t q, int32_t* idx_soa, double* values);
+int cphifi_obs_file_write(const char* path, int binary, int d, const int64_t* shape, int64_t q,
+                          const int32_t* idx_soa, const double* values);
+
 /* ---- ALS infinite-mode update ----------------------------------------
  * AlsState::update_infinite_mode (als.hpp:170-218) followed by AlsState::relative_error
  * (als.hpp:221-237) and this mode's objective term (als.hpp:243-255), one device pass:

@@ -33,6 +33,7 @@ __all__ = [
     "sample_uniform", "full_observations", "make_unaligned_subproblem", "UnalignedSubproblem",
     "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
     "AlsUpdate", "update_infinite_mode_unaligned", "update_infinite_mode_aligned",
+    "read_observations", "write_observations",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
     "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
@@ -676,6 +677,32 @@ def solve_aligned_decoupled(p: AlignedSubproblem, v_eig: SymEig | None = None) -
         call("cphifi_solve_aligned_decoupled", p.mode.handle, r, _dp(b), _dp(v), c_double_p(), c_double_p(),
              _dp(w))
     return w
+
+
+# ---- io.hpp: observation files ----------------------------------------
+def read_observations(path: str, multiset: bool = False, coalesce: bool = False) -> ObservationSet:
+    """read_observations (io.hpp:110-131): the reference text format (1-based lines, parsed on all
+    host threads) or the binary format written by write_observations(..., binary=True)."""
+    d = ctypes.c_int()
+    shape = (ctypes.c_int64 * 8)()
+    q = ctypes.c_int64()
+    binary = ctypes.c_int()
+    bp = os.fsencode(path)
+    call("cphifi_obs_file_info", bp, ctypes.byref(d), shape, ctypes.byref(q), ctypes.byref(binary))
+    idx = np.zeros((d.value, q.value), dtype=np.int32)
+    vals = np.zeros(q.value, dtype=np.float64)
+    call("cphifi_obs_file_read", bp, d.value, q.value, idx.ctypes.data_as(ctypes.c_void_p), _dp(vals))
+    return ObservationSet([shape[m] for m in range(d.value)], idx, vals, multiset=multiset, coalesce=coalesce)
+
+
+def write_observations(path: str, obs: ObservationSet, binary: bool = False) -> None:
+    """write_observations (io.hpp:97-107): text, 1-based, 17 significant digits; or the binary
+    format (int32 SoA indices + fp64 values after the `shape:` header)."""
+    shape = np.ascontiguousarray(obs.shape(), dtype=np.int64)
+    idx = np.ascontiguousarray(obs.index_array(), dtype=np.int32)
+    vals = np.ascontiguousarray(obs.values(), dtype=np.float64)
+    call("cphifi_obs_file_write", os.fsencode(path), int(bool(binary)), len(shape),
+         shape.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), vals.size, idx.ctypes.data_as(ctypes.c_void_p), _dp(vals))
 
 
 # ---- als.hpp: the infinite-mode update of one ALS sweep (SURVEY §8f row 1) -----------------

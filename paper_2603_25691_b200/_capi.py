@@ -131,6 +131,14 @@ _SIGS = [
      [_H, ctypes.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, c_double_p]),
+    ("cphifi_obs_file_info", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+      ctypes.POINTER(ctypes.c_int)]),
+    ("cphifi_obs_file_read", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, c_double_p]),
+    ("cphifi_obs_file_write", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_void_p,
+      c_double_p]),
     ("cphifi_als_update_infinite_unaligned", ctypes.c_int,
      [_H, ctypes.c_void_p, c_double_p, c_double_p, c_double_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cphifi_als_update_infinite_aligned", ctypes.c_int,
