@@ -197,6 +197,16 @@ def als_updates(ctx, p, c):
     out["config1_unaligned"] = {"wall_s_warm": time.perf_counter() - t0, "relative_error": u.relative_error,
                                 "iterations_cold": u.report.iterations, "iterations_warm": u2.report.iterations,
                                 "solve_s": u.solve_s, "update_and_error_s": u.update_s}
+    # a whole unaligned ALS sweep on device (mode 0 infinite, modes 1, 2 finite, then the error)
+    st = cp.UnalignedAlsState(cp.ObservationSet(c.shape, c.idx, c.vals), p.mode,
+                              cp.KruskalModel([np.zeros((c.shape[0], c.r))] + c.factors[1:]), rho=c.rho, inner=cfg)
+    its = [st.sweep() for _ in range(4)]  # the first sweep builds the per-mode plans
+    out["config1_unaligned_sweep"] = {"wall_s_per_sweep": float(np.median([it.wall_time_s for it in its[1:]])),
+                                      "first_sweep_s": its[0].wall_time_s,
+                                      "rel_errors": [it.rel_error for it in its],
+                                      "pcg_iterations": [it.pcg_iterations for it in its],
+                                      "note": "infinite mode: PCG warm-started + A_0 = K W; finite modes: row "
+                                              "least squares (row Grams + batched Jacobi pseudo-inverse); error pass"}
     c2 = configs.config2()
     n, r = c2.shape[0], c2.r
     mode = cp.RkhsMode(c2.points, c2.ell, c2.lam, ctx=ctx)

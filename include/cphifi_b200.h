@@ -139,6 +139,7 @@ int cphifi_obs_info(cphifi_obs obs, int64_t* q_total, int64_t* q_local, double* 
 /* make_unaligned_subproblem(obs, model, k, mode, rho) (unaligned.hpp:35-48): factors[m]
  * is the n_m x r column-major factor of mode m (factors[k] is ignored and may be NULL).
  * Builds B = sampled_mttkrp(values) (all-reduced over shards) and V = gram_khatri_rao. */
+/* (mode may be NULL: a finite-mode subproblem for cphifi_als_update_finite_unaligned) */
 int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r,
                             const double* const* factors, double rho,
                             cphifi_unaligned* out);
@@ -253,6 +254,19 @@ int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_co
 int cphifi_als_update_infinite_aligned(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,
                                        const double* const* factors, double* w_out, double* a_out,
                                        cphifi_als_report* als);
+
+/* relative_error (als.hpp:221-237) of the model with factor k = a_k (host n_k x r column-major)
+ * and the plan's other factors, over the observed entries; *data_norm (may be NULL) = ||v||. */
+int cphifi_unaligned_relative_error(cphifi_unaligned p, const double* a_k, double* rel_error,
+                                    double* data_norm);
+/* update_finite_mode, unaligned branch (als.hpp:144-162): every row i of the
+ * plan's mode k gets the minimum-norm least-squares fit of its observations,
+ * a_i = argmin ||Z_i a - t_i||, rows without observations stay zero; a_out is n_k x r column-major.
+ * `p` comes from cphifi_unaligned_create on the mode-k plan with mode = NULL (a finite-mode
+ * subproblem: B, V and the row Grams, no operator).  Solved as G_i^+ (Z_i' t_i) with
+ * G_i = Z_i' Z_i, eigenvalues below r eps lambda_max dropped (COD's rank decision on Z_i agrees
+ * while cond(Z_i) < ~1e7). */
+int cphifi_als_update_finite_unaligned(cphifi_unaligned p, double* a_out);
 
 /* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
  * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup: wall clock of the

@@ -33,7 +33,8 @@ __all__ = [
     "sample_uniform", "full_observations", "make_unaligned_subproblem", "UnalignedSubproblem",
     "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
     "AlsUpdate", "update_infinite_mode_unaligned", "update_infinite_mode_aligned",
-    "read_observations", "write_observations",
+    "read_observations", "write_observations", "update_finite_mode_unaligned", "unaligned_relative_error",
+    "UnalignedAlsState", "FitIteration",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
     "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
@@ -482,12 +483,15 @@ class UnalignedSubproblem:
             if i != k and model.factors[i].shape[0] != obs.shape()[i]:
                 raise CphifiInvalidArgument("build_zhat: shape mismatch")
         self._r = model.rank()
-        self._n = mode.size()
+        # mode None: a finite-mode subproblem (B, V, row Grams; no operator) for the row updates
+        self._n = mode.size() if mode is not None else obs.shape()[k]
+        ctx = mode.ctx if mode is not None else default_context()
         arrs, ptrs = _factor_array(model.factors, k)
-        plan = obs.plan(k, mode.ctx, shard, shards)
+        plan = obs.plan(k, ctx, shard, shards)
         h = ctypes.c_void_p()
-        call("cphifi_unaligned_create", plan.h, mode.handle, self._r, ptrs, self.rho, ctypes.byref(h))
-        self._h = _Handle(h, "cphifi_unaligned_destroy", deps=(plan, mode))
+        call("cphifi_unaligned_create", plan.h, mode.handle if mode is not None else None, self._r, ptrs, self.rho,
+             ctypes.byref(h))
+        self._h = _Handle(h, "cphifi_unaligned_destroy", deps=(plan, mode) if mode is not None else (plan,))
         self.handle = h
 
     def n(self) -> int:
@@ -751,6 +755,80 @@ def update_infinite_mode_unaligned(p: UnalignedSubproblem, cfg: PcgConfig | None
     sr = SolveReport(rep.iterations, rep.relative_residual, rep.wall_time_s, bool(rep.converged),
                      list(hist[: rep.history_len]) if cfg.record_history else [], rep.setup_s, rep.matvecs)
     return _als_from(c, w, a, sr)
+
+
+def update_finite_mode_unaligned(obs: ObservationSet, model: KruskalModel, k: int) -> np.ndarray:
+    """update_finite_mode, unaligned branch (als.hpp:144-162) on device: the minimum-norm least-
+    squares row fits of mode k (rows without observations stay zero).  Returns A_k (n_k x r)."""
+    p = UnalignedSubproblem(obs, model, k, None, 1e-6)
+    a = np.zeros((p.n(), p.r()), order="F")
+    call("cphifi_als_update_finite_unaligned", p.handle, _dp(a))
+    return a
+
+
+def unaligned_relative_error(p: UnalignedSubproblem, a_k) -> tuple[float, float]:
+    """relative_error (als.hpp:221-237) with factor k = a_k and the plan's other factors.
+    Returns (relative error, ||v||)."""
+    rel, nrm = ctypes.c_double(), ctypes.c_double()
+    call("cphifi_unaligned_relative_error", p.handle, _dp(_f64(a_k)), ctypes.byref(rel), ctypes.byref(nrm))
+    return rel.value, nrm.value
+
+
+@dataclass
+class FitIteration:
+    """als.hpp FitIteration: the relative error / objective after a sweep and its wall time."""
+    rel_error: float
+    objective: float
+    wall_time_s: float = 0.0
+    pcg_iterations: int = 0
+
+
+class UnalignedAlsState:
+    """AlsState (als.hpp:66-275) for unaligned data with mode 0 the infinite (RKHS) mode and the
+    other modes finite, every update on device: update_infinite_mode (PCG warm-started from the
+    previous W, A_0 = K W), update_finite_mode (row least squares), relative_error and the
+    objective.  Factors stay host-side between calls (the reference's KruskalModel)."""
+
+    def __init__(self, obs: ObservationSet, mode: RkhsMode, model: KruskalModel, rho: float = 1e-6,
+                 inner: PcgConfig | None = None, warm_start: bool = True):
+        self.obs, self.mode, self.rho = obs, mode, float(rho)
+        self.model = KruskalModel([np.array(f, order="F", dtype=np.float64) for f in model.factors])
+        self.inner = inner or PcgConfig()
+        self.warm_start = warm_start
+        self.weights = None  # W of mode 0 (als.hpp weights_[0])
+
+    def update_infinite_mode(self) -> AlsUpdate:
+        p = make_unaligned_subproblem(self.obs, self.model, 0, self.mode, self.rho)
+        u = update_infinite_mode_unaligned(p, self.inner, self.weights if self.warm_start else None)
+        self.weights = u.w
+        self.model.factors[0] = u.a
+        return u
+
+    def update_finite_mode(self, k: int) -> None:
+        self.model.factors[k] = update_finite_mode_unaligned(self.obs, self.model, k)
+
+    def relative_error(self) -> float:
+        p = UnalignedSubproblem(self.obs, self.model, 0, None, self.rho)
+        return unaligned_relative_error(p, self.model.factors[0])[0]
+
+    def objective_from_error(self, rel: float) -> float:
+        """als.hpp:243-255: fit^2 + lambda trace(W'KW) for the infinite mode."""
+        nrm = float(np.linalg.norm(self.obs.values()))
+        obj = (rel * nrm) ** 2
+        if self.weights is not None:
+            obj += self.mode.lambda_() * float(np.sum(self.weights * self.model.factors[0]))
+        return obj
+
+    def sweep(self) -> FitIteration:
+        """One outer iteration of run_cp_hifi (als.hpp:303-314): every mode in order, then the error."""
+        import time as _time
+        t0 = _time.perf_counter()
+        u = self.update_infinite_mode()
+        for k in range(1, self.model.order()):
+            self.update_finite_mode(k)
+        rel = self.relative_error()
+        return FitIteration(rel, self.objective_from_error(rel), _time.perf_counter() - t0,
+                            u.report.iterations if u.report else 0)
 
 
 def update_infinite_mode_aligned(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode) -> AlsUpdate:

@@ -260,7 +260,7 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     for (int m = 0; m < o->d - 1; ++m) a.fac_off[m] = p->fac_off[m];
     a.fac_total = (int64_t)p->fac.n;
     a.mult = o->coalesced ? o->mult.get() : nullptr;
-    a.kmat = p->mode->kernel.get();
+    a.kmat = p->mode ? p->mode->kernel.get() : nullptr;
     a.xhat_rm = p->xhat_rm.get();
     a.yhat_rm = p->yhat_rm.get();
     a.slot_a = p->slot_a.get();
@@ -269,7 +269,7 @@ FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
     a.cta_beg = p->cta_beg.get();
     a.row_first_cta = p->row_first_cta.get();
     a.row_ncta = p->row_ncta.get();
-    a.lambda = p->mode->lambda;
+    a.lambda = p->mode ? p->mode->lambda : 0.0;
     a.rho = p->rho;
     a.barrier = p->barrier.get();
     a.rowcnt = p->rowcnt.get();
@@ -360,7 +360,12 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
 // y = vec(K Yhat + lambda Xhat) + rho x with Xhat = K X  (unaligned.hpp:101-115).
 // Small n on one GPU: ONE cooperative launch.  Otherwise DMMA GEMMs around the fused
 // scatter-gather, with the NCCL all-reduce of Yhat between them on multi-GPU.
+void need_mode(cphifi_unaligned p) {
+    if (!p->mode) throw_invalid("unaligned: a finite-mode subproblem (no kernel) has no operator");
+}
+
 void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
+    need_mode(p);
     cphifi_ctx ctx = p->obs->ctx;
     const bool multi = ctx->comm && ctx->nranks > 1;
     if (p->op == 1) ensure_gram(p);
@@ -387,6 +392,7 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
 
 // build_preconditioner (unaligned.hpp:120-134): eig(K) (cached), eig(V), D
 void ensure_precond(cphifi_unaligned p) {
+    need_mode(p);
     mode_eig_once(p->mode);
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
@@ -990,12 +996,12 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
                             cphifi_unaligned* out) {
     return guard([&] {
         need(obs, "obs");
-        need(mode, "mode");
         need(factors, "factors");
         need(out, "out");
         if (r < 1) throw_invalid("KruskalModel: rank must be positive");
         if (r > 128) throw_invalid("unaligned: rank above 128 is not supported");
-        if (mode->n != obs->shape[obs->k]) throw_invalid("unaligned: kernel size mismatch");
+        // mode == NULL: a finite-mode subproblem (B, V, row Grams; no operator, no solve)
+        if (mode && mode->n != obs->shape[obs->k]) throw_invalid("unaligned: kernel size mismatch");
         cphifi_ctx ctx = obs->ctx;
         DeviceGuard dg(ctx->device);
         cudaStream_t s = ctx->stream;
@@ -1003,7 +1009,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         std::unique_ptr<cphifi_unaligned_s> hold(p);
         p->obs = obs;
         p->mode = mode;
-        p->n = mode->n;
+        p->n = obs->shape[obs->k];
         p->r = r;
         p->rp = pow2_at_least(r, 4);
         p->rho = rho;
@@ -1894,6 +1900,64 @@ int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, co
     });
 }
 
+
+// relative_error (als.hpp:221-237) of the model whose mode-k factor is a_k (host n x r column-major)
+// and whose other factors are the plan's: the residual pass of the infinite-mode update alone.
+int cphifi_unaligned_relative_error(cphifi_unaligned p, const double* a_k, double* rel_error, double* data_norm) {
+    return guard([&] {
+        need(p, "p");
+        need(a_k, "a_k");
+        need(rel_error, "rel_error");
+        cphifi_obs o = p->obs;
+        if (o->coalesced) throw_invalid("relative_error: a plan with coalesced duplicates has no per-draw values");
+        cphifi_ctx ctx = o->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const int64_t n = p->n, r = p->r;
+        DevBuf<double> a(n * r), arm((size_t)n * p->rp), scal(2),
+            part(std::max<int64_t>(sq_residual_blocks(o->q_local), 1024));
+        h2d(a.get(), a_k, sizeof(double) * n * r, s);
+        pack_rows(a.get(), n, n, r, p->rp, arm.get(), s);
+        SqResidualArgs ra;
+        ra.n = n; ra.r = r; ra.rp = p->rp; ra.q = o->q_local; ra.ldq = o->ldq; ra.dother = o->d - 1;
+        ra.row_ptr = o->row_ptr.get(); ra.idx = o->idx_o.get(); ra.values = o->values.get();
+        ra.fac = p->fac.get();
+        for (int m = 0; m < o->d - 1; ++m) ra.fac_off[m] = p->fac_off[m];
+        ra.ak = arm.get();
+        sq_residual(ra, part.get(), scal.get(), s);
+        const int64_t nbn = std::min<int64_t>(std::max<int64_t>(1, (o->q_local + 2047) / 2048), 1024);
+        if (o->q_local > 0) sq_norm(o->values.get(), o->q_local, part.get(), nbn, scal.get() + 1, s);
+        else CPHIFI_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
+        allreduce(ctx, scal.get(), 2);
+        double h[2];
+        d2h_sync(h, scal.get(), sizeof(double) * 2, s);
+        const double dn = std::sqrt(h[1]);
+        if (dn == 0.0) throw_runtime("relative_error: zero data norm");
+        *rel_error = std::sqrt(h[0]) / dn;
+        if (data_norm) *data_norm = dn;
+    });
+}
+
+// ---- ALS finite-mode update, unaligned (als.hpp:144-162) --------------------
+int cphifi_als_update_finite_unaligned(cphifi_unaligned p, double* a_out) {
+    return guard([&] {
+        need(p, "p");
+        need(a_out, "a_out");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const int64_t n = p->n, r = p->r;
+        if (p->rp > 64) throw_invalid("finite-mode update: padded rank above 64 is not supported");
+        ensure_gram(p);  // G_i = Z_i' Z_i (this shard's observations)
+        if (is_multi(p) && !p->gram_reduced) {
+            allreduce(ctx, p->gram.get(), (size_t)n * p->rp * p->rp);
+            p->gram_reduced = true;
+        }
+        DevBuf<double> a(n * r);
+        rowls_solve(p->gram.get(), p->b.get(), n, r, p->rp, a.get(), s);  // b = Z_i' t_i (all shards)
+        d2h_sync(a_out, a.get(), sizeof(double) * n * r, s);
+    });
+}
 
 // ---- ALS infinite-mode update (als.hpp:170-255) ---------------------------------------------
 int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_config* cfg, const double* warm_start,

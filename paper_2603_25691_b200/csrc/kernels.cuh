@@ -220,6 +220,9 @@ struct SqResidualArgs {
     const double* ak = nullptr;        // the updated mode-k factor, n x rp row-major
 };
 int64_t sq_residual_blocks(int64_t q);
+// finite-mode row least squares (k_rowls.cu): a_i = G_i^+ b_i for every row (G: n x rp x rp,
+// b / a_out: n x r column-major)
+void rowls_solve(const double* g, const double* b, int64_t n, int64_t r, int64_t rp, double* a_out, cudaStream_t s);
 // *out = sum_l (v_l - <A_k(i_k(l),:), z_l>)^2 ; partial >= sq_residual_blocks(q) doubles
 void sq_residual(const SqResidualArgs& a, double* partial, double* out, cudaStream_t s);
 // *out = ||x||^2 with nb blocks (partial >= nb doubles)

@@ -107,3 +107,93 @@ def test_aligned_update(cp, which):
     # ~1e6, so the two association orders agree to ~1e-9 relative
     assert abs(u.reg - c.lam * np.trace(u.w.T @ kern @ u.w)) <= 1e-7 * abs(u.reg)
     assert np.isfinite(u.objective_term())
+
+
+def _ref_finite(shape, idx, vals, factors, k, r):
+    """update_finite_mode, unaligned (als.hpp:144-162): per-row minimum-norm least squares over the
+    row's Zhat rows (modes ascending, observations.hpp:150-156), rows without data stay zero."""
+    d = len(shape)
+    z = np.ones((vals.size, r))
+    for m in range(d):
+        if m != k:
+            z = z * factors[m][idx[m]]
+    a = np.zeros((shape[k], r))
+    for i in range(shape[k]):
+        sel = np.nonzero(idx[k] == i)[0]
+        if sel.size:
+            a[i] = np.linalg.lstsq(z[sel], vals[sel], rcond=None)[0]
+    return a
+
+
+@pytest.mark.parametrize("shape,r,q,k", [([8, 12, 5], 3, 300, 1), ([8, 12, 5], 4, 40, 2), ([6, 5, 4, 7], 5, 500, 3),
+                                         ([30, 40], 6, 600, 1), ([50, 64, 20], 32, 20000, 1), ([10, 9, 8], 7, 63, 2)])
+def test_finite_update_vs_lstsq(cp, shape, r, q, k):
+    g = np.random.default_rng(q + r)
+    lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+    idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+    vals = g.normal(size=q)
+    factors = [g.normal(size=(n, r)) for n in shape]
+    a = cp.update_finite_mode_unaligned(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), k)
+    ref = _ref_finite(shape, idx, vals, factors, k, r)
+    for i in range(shape[k]):
+        cnt = int((idx[k] == i).sum())
+        if cnt == 0:
+            assert np.all(a[i] == 0.0)
+        else:  # full-rank rows 1e-9; rank-deficient rows (cnt < r) pick the same minimum-norm fit
+            assert np.linalg.norm(a[i] - ref[i]) <= 1e-9 * max(np.linalg.norm(ref[i]), 1e-300), (i, cnt)
+
+
+def test_finite_update_multiset_and_coalesced(cp):
+    g = np.random.default_rng(9)
+    shape, r = [7, 9, 6], 3
+    idx = np.array(np.unravel_index(g.integers(0, np.prod(shape), size=400), shape, order="F"), dtype=np.int64)
+    vals = g.normal(size=400)
+    factors = [g.normal(size=(n, r)) for n in shape]
+    ref = _ref_finite(shape, idx, vals, factors, 1, r)  # duplicates = repeated rows of the LS
+    for coalesce in (False, True):
+        obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+        a = cp.update_finite_mode_unaligned(obs, cp.KruskalModel(factors), 1)
+        assert ri.rel(a, ref) < 1e-9, coalesce
+
+
+def test_unaligned_als_sweeps_vs_reference(cp):
+    """run_cp_hifi's outer loop (als.hpp:303-314) for unaligned data, mode 0 infinite: three sweeps on
+    device vs the oracle restatement (PCG oracle with the same eig(K), lstsq finite updates, the
+    reference's error).  The device eig(V) inside the PCG differs from the oracle's by rounding,
+    so W agrees to the PCG tolerance: errors compared at 1e-7 relative."""
+    g = np.random.default_rng(2026)
+    shape, r, q = [40, 12, 10], 3, 1500
+    pts = np.linspace(0.0, 1.0, shape[0])
+    truth = [g.normal(size=(n, r)) for n in shape]
+    lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+    idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+    vals = np.einsum("lr,lr,lr->l", truth[0][idx[0]], truth[1][idx[1]], truth[2][idx[2]]) + 0.01 * g.normal(size=q)
+    init = [np.zeros((shape[0], r))] + [g.normal(size=(n, r)) for n in shape[1:]]
+    lam, rho, sigma = 1e-3, 1e-6, 0.2
+    cfg = cp.PcgConfig(1e-10, 500)
+    mode = cp.RkhsMode(pts, sigma, lam)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    obs = cp.ObservationSet(shape, idx, vals)
+    st = cp.UnalignedAlsState(obs, mode, cp.KruskalModel(init), rho=rho, inner=cfg)
+    # oracle restatement
+    fac = [f.copy() for f in init]
+    w_prev = None
+    objs = []
+    for sweep in range(3):
+        it = st.sweep()
+        objs.append(it.objective)
+        sub = orc.make_unaligned_subproblem(shape, idx, vals, fac, 0, kern, lam, rho)
+        w = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-10, 500), ek, orc.sym_eig(sub.v), warm_start=w_prev)
+        w_prev = w
+        fac[0] = kern @ w
+        for k in (1, 2):
+            fac[k] = _ref_finite(shape, idx, vals, fac, k, r)
+        fit = vals - np.einsum("lr,lr,lr->l", fac[0][idx[0]], fac[1][idx[1]], fac[2][idx[2]])
+        rel = np.linalg.norm(fit) / np.linalg.norm(vals)
+        assert abs(it.rel_error - rel) <= 1e-7 * rel, (sweep, it.rel_error, rel)
+        for k in range(3):
+            assert ri.rel(st.model.factors[k], fac[k]) < 1e-6, (sweep, k)
+    # block coordinate descent: the objective does not increase (up to the inner PCG tolerance)
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:])), objs
