@@ -296,11 +296,30 @@ void ensure_gram(cphifi_unaligned p) {
     if (p->rp > 64) throw_invalid("gram operator: padded rank above 64 is not supported");
     cphifi_obs o = p->obs;
     cphifi_ctx ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
     const size_t rp2 = (size_t)p->rp * p->rp;
     p->gram.alloc((size_t)p->n * rp2);
-    CPHIFI_CUDA(cudaMemsetAsync(p->gram.get(), 0, sizeof(double) * p->n * rp2, ctx->stream));
-    p->gslot_a.alloc((size_t)p->grid * rp2);
-    p->gslot_b.alloc((size_t)p->grid * rp2);
+    CPHIFI_CUDA(cudaMemsetAsync(p->gram.get(), 0, sizeof(double) * p->n * rp2, s));
+    // The build's own row-aligned partition, ~4 CTAs per SM: each CTA alternates a gather phase
+    // and a DMMA phase around barriers, so one CTA per SM (the stream plan's grid) left it
+    // latency-bound.
+    const int cmax = 4 * ctx->num_sms;
+    PartitionPlan plan;
+    {
+        std::vector<int64_t> rp_host(p->n + 1);
+        d2h_sync(rp_host.data(), o->row_ptr.get(), sizeof(int64_t) * (p->n + 1), s);
+        plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
+    }
+    const int grid = plan.ctas;
+    DevBuf<int64_t> cta_beg(plan.beg.size()), cta_rows(plan.rows.size());
+    DevBuf<int32_t> rfc(p->n), rnc(p->n);
+    DevBuf<unsigned> rowcnt(p->n);
+    h2d(cta_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
+    h2d(cta_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
+    h2d(rfc.get(), plan.row_first_cta.data(), sizeof(int32_t) * p->n, s);
+    h2d(rnc.get(), plan.row_ncta.data(), sizeof(int32_t) * p->n, s);
+    CPHIFI_CUDA(cudaMemsetAsync(rowcnt.get(), 0, sizeof(unsigned) * p->n, s));
+    DevBuf<double> slot_a((size_t)grid * rp2), slot_b((size_t)grid * rp2);
     GramArgs g;
     g.n = p->n;
     g.rp = p->rp;
@@ -310,16 +329,18 @@ void ensure_gram(cphifi_unaligned p) {
     g.idx = o->idx_o.get();
     g.fac = p->fac.get();
     for (int m = 0; m < o->d - 1; ++m) g.fac_off[m] = p->fac_off[m];
+    g.fac_total = (int64_t)p->fac.n;
     g.mult = o->coalesced ? o->mult.get() : nullptr;
-    g.cta_beg = p->cta_beg.get();
-    g.cta_rows = p->cta_rows.get();
-    g.row_first_cta = p->row_first_cta.get();
-    g.row_ncta = p->row_ncta.get();
-    g.rowcnt = p->rowcnt.get();
-    g.slot_a = p->gslot_a.get();
-    g.slot_b = p->gslot_b.get();
+    g.cta_beg = cta_beg.get();
+    g.cta_rows = cta_rows.get();
+    g.row_first_cta = rfc.get();
+    g.row_ncta = rnc.get();
+    g.rowcnt = rowcnt.get();
+    g.slot_a = slot_a.get();
+    g.slot_b = slot_b.get();
     g.g = p->gram.get();
-    if (o->q_local > 0) gram_build(g, p->grid, ctx->stream);
+    if (o->q_local > 0) gram_build(g, grid, s);
+    CPHIFI_CUDA(cudaStreamSynchronize(s));  // the plan buffers are released on return
 }
 
 // Phase sets of the operator launches (see kernels.cuh).  part 0 = the (first) launch,

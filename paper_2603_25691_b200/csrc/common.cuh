@@ -156,7 +156,6 @@ struct cphifi_unaligned_s {
     // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
     int op = 0;
     cphifi::DevBuf<double> gram;            // n x rp x rp (built lazily)
-    cphifi::DevBuf<double> gslot_a, gslot_b;  // grid x rp x rp
     bool gram_reduced = false;               // multi-GPU: gram holds the all-shard sum
     cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU)
     cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid

@@ -15,6 +15,8 @@
 //   finished by the last CTA (per-row arrival counter, ordered slot sum) — deterministic.
 // gram_apply_kernel: Yhat(i, a) = sum_b G_i(b, a) Xhat(i, b); thread (i, a), consecutive a
 //   read consecutive G entries (G_i symmetric, so its row-major and column-major layouts agree).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace cphifi {
@@ -135,6 +137,140 @@ __global__ void __launch_bounds__(GT) gram_build_kernel(const GramArgs a) {
     finish_row(row);
 }
 
+// ---- DMMA build: G_i += (W Z)' Z per batch of GB observations ------------------------------
+// The batch's Khatri-Rao rows Z (GB x RP, one row of i_k) are gathered into shared memory (the
+// other-mode factors staged there when they fit), then G's upper-triangle 8x8 tiles accumulate
+// DMMA m8n8k4 products over the batch (k = observations): nt(nt+1)/2 tiles (nt = RP/8) spread
+// over the 8 warps, A fragments pre-weighted by the entry weights.  Row boundaries flush the
+// tiles (and their mirror) exactly like the FMA build; same split-row protocol, deterministic.
+// (FMA build: 85 ms at config 3 — shared-memory operand traffic, one LDS per FMA.)
+__device__ __forceinline__ void dmma_g(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+template <int RP, int DO, bool SF>
+__global__ void __launch_bounds__(GT) gram_build_dmma_kernel(const GramArgs a) {
+    constexpr int NT = RP / 8;                  // 8x8 tiles per dimension
+    constexpr int NUP = NT * (NT + 1) / 2;      // upper-triangle tiles
+    constexpr int NW = GT / 32;
+    constexpr int TPW = (NUP + NW - 1) / NW;    // tiles per warp
+    constexpr int ZP = RP + 4;                  // z row pitch: == 4 mod 16 doubles, conflict-free fragments
+    extern __shared__ __align__(16) double gsm[];
+    double* zs = gsm;                           // GB x ZP
+    double* zw = zs + GB * ZP;                  // GB x ZP (weighted)
+    double* sfac = zw + GB * ZP;                // staged factors (SF)
+    __shared__ int s_last;
+    const int c = blockIdx.x;
+    const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];
+    if (ca >= cb) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, kq = lane & 3;
+    if constexpr (SF) {
+        for (int64_t e = tid; e < a.fac_total; e += GT) sfac[e] = a.fac[e];
+    }
+    const double* fac = SF ? sfac : a.fac;
+    // this warp's tiles (ti <= tj), in a fixed enumeration
+    int tiles_i[TPW], tiles_j[TPW];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+        int t = warp + NW * u, ti = 0;
+        tiles_i[u] = -1;
+        tiles_j[u] = -1;
+        if (t < NUP) {
+            while (t >= NT - ti) {
+                t -= NT - ti;
+                ++ti;
+            }
+            tiles_i[u] = ti;
+            tiles_j[u] = ti + t;
+        }
+    }
+    double acc[TPW][2];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const int64_t first_row = a.cta_rows[2 * c];
+    int64_t row = first_row;
+    int64_t row_end = a.row_ptr[row + 1];
+    auto finish_row = [&](int64_t rr) {
+        const int ncta = a.row_ncta[rr];
+        double* dst = ncta == 1 ? a.g + rr * RP * RP
+                    : rr == first_row ? a.slot_a + (int64_t)c * RP * RP
+                                      : a.slot_b + (int64_t)c * RP * RP;
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            if (tiles_i[u] < 0) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ii = tiles_i[u] * 8 + g, jj = tiles_j[u] * 8 + 2 * kq + h;
+                dst[ii * RP + jj] = acc[u][h];
+                if (tiles_i[u] != tiles_j[u]) dst[jj * RP + ii] = acc[u][h];
+            }
+            acc[u][0] = acc[u][1] = 0.0;
+        }
+        if (ncta > 1) {  // the last CTA of a split row sums the slots in CTA order
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                s_last = atom_add_acqrel_g(a.rowcnt + rr, 1u) == (unsigned)ncta - 1;
+                if (s_last) a.rowcnt[rr] = 0;
+            }
+            __syncthreads();
+            if (s_last) {
+                const int u0 = a.row_first_cta[rr];
+                const bool starts = a.row_ptr[rr] == a.cta_beg[u0];
+                for (int e = tid; e < RP * RP; e += GT) {
+                    double sv = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
+                                       : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
+                    for (int u = u0 + 1; u < u0 + ncta; ++u) sv += __ldcg(a.slot_a + (int64_t)u * RP * RP + e);
+                    a.g[rr * RP * RP + e] = sv;
+                }
+            }
+        }
+    };
+    __syncthreads();  // staged factors
+    int64_t pos = ca;
+    while (pos < cb) {
+        while (pos >= row_end) {
+            finish_row(row);
+            do {
+                ++row;
+                row_end = a.row_ptr[row + 1];
+            } while (row_end <= pos);
+        }
+        const int cnt = (int)min((int64_t)GB, min(cb, row_end) - pos);
+        __syncthreads();  // previous batch consumed
+        for (int e = tid; e < GB * RP; e += GT) {
+            const int t = e / RP, j = e % RP;
+            double z = 0.0, w = 0.0;
+            if (t < cnt) {
+                const int64_t l = pos + t;
+                z = fac[a.fac_off[0] + (int64_t)__ldg(a.idx + l) * RP + j];
+#pragma unroll
+                for (int m = 1; m < DO; ++m) z *= fac[a.fac_off[m] + (int64_t)__ldg(a.idx + (int64_t)m * a.q + l) * RP + j];
+                w = a.mult ? (double)__ldg(a.mult + l) : 1.0;
+            }
+            zs[t * ZP + j] = z;
+            zw[t * ZP + j] = z * w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k0 = 0; k0 < GB; k0 += 4) {
+            const int t = k0 + kq;
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                if (tiles_i[u] < 0) continue;
+                const double av = zw[t * ZP + tiles_i[u] * 8 + g];   // A(i, t) = w_t z_t(i)
+                const double bv = zs[t * ZP + tiles_j[u] * 8 + g];   // B(t, j) = z_t(j)
+                dmma_g(acc[u], av, bv);
+            }
+        }
+        pos += cnt;
+    }
+    __syncthreads();
+    finish_row(row);
+}
+
 // Yhat(i, a) = sum_b G_i(b, a) Xhat(i, b) for rows with observations (others stay zero).
 __global__ void gram_apply_kernel(const double* __restrict__ g, const double* __restrict__ xhat, const int64_t* row_ptr,
                                   int64_t n, int64_t rp, double* __restrict__ yhat) {
@@ -149,8 +285,32 @@ __global__ void gram_apply_kernel(const double* __restrict__ g, const double* __
     yhat[e] = s;
 }
 
+template <int RP, int DO>
+void launch_dmma_do(const GramArgs& a, int grid, cudaStream_t s) {
+    const size_t zbytes = sizeof(double) * 2 * GB * (RP + 4);
+    const bool sf = zbytes + sizeof(double) * a.fac_total <= 200 * 1024;
+    const size_t smem = zbytes + (sf ? sizeof(double) * a.fac_total : 0);
+    auto kern = sf ? gram_build_dmma_kernel<RP, DO, true> : gram_build_dmma_kernel<RP, DO, false>;
+    CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, GT, smem, s>>>(a);
+}
+
 template <int RP>
 void launch_build_rp(const GramArgs& a, int grid, cudaStream_t s) {
+    bool dm = RP >= 8;
+    if (const char* e = std::getenv("CPHIFI_GRAM_DMMA")) dm = dm && std::atoi(e) != 0;
+    if constexpr (RP >= 8) {
+        if (dm) {
+            switch (a.dother) {
+                case 1: launch_dmma_do<RP, 1>(a, grid, s); return;
+                case 2: launch_dmma_do<RP, 2>(a, grid, s); return;
+                case 3: launch_dmma_do<RP, 3>(a, grid, s); return;
+                case 4: launch_dmma_do<RP, 4>(a, grid, s); return;
+                case 5: launch_dmma_do<RP, 5>(a, grid, s); return;
+                default: throw_invalid("unaligned: tensor order above 6 is not supported");
+            }
+        }
+    }
     switch (a.dother) {
         case 1: gram_build_kernel<RP, 1><<<grid, GT, 0, s>>>(a); break;
         case 2: gram_build_kernel<RP, 2><<<grid, GT, 0, s>>>(a); break;

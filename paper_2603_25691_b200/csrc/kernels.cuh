@@ -158,6 +158,7 @@ struct GramArgs {
     const int32_t* idx = nullptr;
     const double* fac = nullptr;
     int64_t fac_off[8] = {0};
+    int64_t fac_total = 0;          // doubles in fac (shared-memory staging of the DMMA build)
     const int32_t* mult = nullptr;  // coalesced plan: G_i = sum_l mult_l z_l z_l'
     const int64_t* cta_beg = nullptr;
     const int64_t* cta_rows = nullptr;

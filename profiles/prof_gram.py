@@ -1,0 +1,37 @@
+"""Row-Gram build time at full config 3 / 4 size: FMA build vs DMMA build (CPHIFI_GRAM_DMMA)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2603_25691_b200 as cp  # noqa: E402
+from paper_2603_25691_b200 import configs  # noqa: E402
+
+ctx = cp.Context(0)
+for which in sys.argv[1:] or ["config3"]:
+    cfg = getattr(configs, which)()
+    n, r = cfg.shape[0], cfg.r
+    idx, vals = configs.generate_device(cfg, ctx)
+    torch.cuda.synchronize()
+    mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), cfg.q, keepalive=(idx, vals),
+                                coalesce=cfg.coalesce)
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    x = np.random.default_rng(0).normal(size=n * r)
+    ys = {}
+    for dm in ("0", "1"):
+        os.environ["CPHIFI_GRAM_DMMA"] = dm
+        p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
+        p.set_operator("gram")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ys[dm] = cp.unaligned_matvec(p, x)  # builds G
+        t1 = time.perf_counter()
+        cp.unaligned_matvec(p, x)
+        t2 = time.perf_counter()
+        print(f"{which} dmma={dm}: build+apply {1e3 * (t1 - t0):.1f} ms, apply {1e3 * (t2 - t1):.2f} ms")
+        del p
+    print(f"{which} G-operator rel diff dmma vs fma {np.linalg.norm(ys['0'] - ys['1']) / np.linalg.norm(ys['0']):.2e}")
