@@ -542,6 +542,7 @@ struct Mttkrp3Smem {
     static constexpr int BSZ = BN * BKP3 > BK * (BN + 4) ? BN * BKP3 : BK * (BN + 4);
     double a[ST3][BK][AP3];
     double bt[ST3][BSZ];
+    double w[ST3][BN];  // the tile's Wout row (its `outer` index)
     uint64_t full[ST3], empty[ST3];
 };
 template <int BN, int WR, bool BROW>
@@ -586,7 +587,8 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
 
     if (warp == NC3 / 32) {  // ---- producer warp (one lane) ----
         if (lane == 0) {
-            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + (BROW ? BK * (BN + 4) : BN * BKP3)));
+            const unsigned wb = (unsigned)((bcols * 8 + 15) & ~15);  // Wout row (2 spare doubles past the end)
+            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + (BROW ? BK * (BN + 4) : BN * BKP3))) + wb;
             // L2 prefetch runs l2_ahead tiles in front of the ring: the shared-memory stages then
             // fill from L2, and the loaded-HBM latency hides behind the prefetch distance
             const int pf = a.l2_ahead;
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                 tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
                 if constexpr (BROW) tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)j0, (int)(c1 + a.off1), &sm.full[st]);
                 else tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
+                tma::bulk_g2s(&sm.w[st][0], wout + outer * a.r + j0, wb, &sm.full[st]);
             }
         }
     } else {  // ---- consumer warps ----
@@ -623,14 +626,15 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
             for (int y = 0; y < NF; ++y) acc[x][y][0] = acc[x][y][1] = tmp[x][y][0] = tmp[x][y][1] = 0.0;
         // acc += tmp * Wout(outer, column) for the lane's C columns nf * 8 + 2 kq + h (a one-outer
         // look-ahead of the Wout loads spilled registers and measured slower)
-        auto fold = [&](int64_t outer) {
-            const double* wr = wout + outer * a.r + j0;
+        // acc += tmp * Wout(outer, column) for the lane's C columns nf * 8 + 2 kq + h, done after
+        // the LAST tile of an outer (its slot still holds that outer's Wout row in shared memory)
+        auto fold = [&](int st) {
 #pragma unroll
             for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int jj = nf * 8 + 2 * kq + h;
-                    const double wv = jj < bcols ? __ldg(wr + jj) : 0.0;
+                    const double wv = jj < bcols ? sm.w[st][jj] : 0.0;
 #pragma unroll
                     for (int mf = 0; mf < MF; ++mf) {
                         acc[mf][nf][h] = fma(tmp[mf][nf][h], wv, acc[mf][nf][h]);
@@ -639,14 +643,12 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                 }
         };
         TileIt it = tile_first();
-        int64_t cur_outer = it.outer;
-        for (int t = 0; t < ntiles; ++t, tile_next(it)) {
+        for (int t = 0; t < ntiles; ++t) {
             const int st = t % ST3;
-            if (it.outer != cur_outer) {
-                fold(cur_outer);
-                cur_outer = it.outer;
-            }
             const int cnt = (int)min((int64_t)BK, n1 - it.cidx * BK);
+            const int64_t outer = it.outer;
+            tile_next(it);
+            const bool last_of_outer = t + 1 == ntiles || it.outer != outer;
             tma::mbar_wait(&sm.full[st], (unsigned)((t / ST3) & 1));
             if (a.probe != 1) {
                 if (cnt == BK) {  // full chunk: DMMA only
@@ -678,11 +680,11 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                             for (int nf = 0; nf < NF; ++nf) dmma(tmp[mf][nf], af[mf], bf[nf]);
                     }
                 }
+                if (last_of_outer) fold(st);
             }
             __syncwarp();
             if (lane == 0) tma::mbar_arrive(&sm.empty[st]);
         }
-        if (ntiles > 0) fold(cur_outer);
         __syncthreads();  // (1) the ring is drained by every consumer
         double* red = reinterpret_cast<double*>(smem_raw);  // KG3 x BMM x BN
 #pragma unroll
