@@ -526,12 +526,19 @@ __global__ void __launch_bounds__(NTV, 1) mttkrp_v2_kernel(const MttkrpArgs a, i
 // (per-fragment scaling + masking cost 8 % of the DMMA throughput).  Partial k chunks (n1 not a
 // multiple of 32) take a masked path.
 constexpr int ST3 = 5;
-constexpr int KG3 = 2;                // k-groups
-template <int WR>
-struct V3 {                           // WR rows per consumer warp
-    static constexpr int RG = BMM / WR;           // row groups
-    static constexpr int NC = RG * KG3 * 32;      // consumer threads
-    static constexpr int MF = WR / 8;             // A fragments per k-step
+// 8 consumer warps tile the 128 x BN CTA tile with WR x WC warp tiles; the rest of the 8 go to
+// k-groups that split each stage's k-steps (their partials are summed in order at the end).
+// 32 x 16 tiles (KG = 1) keep the per-outer accumulators at 2 x 16 doubles per lane, so the
+// compiler can hold the next k-step's fragments in registers (the 32 x 32 / KG = 2 layout at 168
+// registers reloaded fragments right before each DMMA: LDS latency exposed, 75 % of DMMA peak).
+template <int BN, int WR, int WC>
+struct V3 {
+    static constexpr int RG = BMM / WR;                 // row groups
+    static constexpr int CG = BN / WC;                  // column groups
+    static constexpr int KG = 8 / (RG * CG);            // k-groups (8 consumer warps)
+    static constexpr int NC = RG * CG * KG * 32;        // consumer threads
+    static constexpr int MF = WR / 8, NF = WC / 8;      // fragments per k-step
+    static_assert(RG * CG * KG == 8 && KG >= 1, "8 consumer warps");
 };
 constexpr int AP3 = BMM + 4;          // T box rows = smem pitch
 constexpr int BKP3 = BK + 4;          // A_1 box rows = smem pitch of the transposed B tile
@@ -545,15 +552,15 @@ struct Mttkrp3Smem {
     double w[ST3][BN];  // the tile's Wout row (its `outer` index)
     uint64_t full[ST3], empty[ST3];
 };
-template <int BN, int WR, bool BROW>
-__global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const MttkrpArgs a, const __grid_constant__ CUtensorMap tm_t,
+template <int BN, int WR, int WC, bool BROW>
+__global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(const MttkrpArgs a, const __grid_constant__ CUtensorMap tm_t,
                                                                 const __grid_constant__ CUtensorMap tm_a1, int64_t chunks,
                                                                 int64_t ktiles, const double* __restrict__ wout,
                                                                 double* __restrict__ work) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Mttkrp3Smem<BN>& sm = *reinterpret_cast<Mttkrp3Smem<BN>*>(smem_raw);
-    constexpr int NF = BN / 8;
-    constexpr int NC3 = V3<WR>::NC, MF = V3<WR>::MF, RG = V3<WR>::RG;
+    using L = V3<BN, WR, WC>;
+    constexpr int NC3 = L::NC, MF = L::MF, NF = L::NF, RG = L::RG, CG = L::CG, KG = L::KG;
     const int P = gridDim.y, split = blockIdx.y;
     const int64_t n0 = a.shape[0], n1 = a.shape[1];
     const int64_t i0 = (int64_t)blockIdx.x * BMM, j0 = (int64_t)blockIdx.z * BN;
@@ -617,7 +624,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
             }
         }
     } else {  // ---- consumer warps ----
-        const int rg = warp % RG, kg = warp / RG;
+        const int rg = warp % RG, cg = (warp / RG) % CG, kg = warp / (RG * CG);
         const int kq = lane & 3, g = lane >> 2;
         double acc[MF][NF][2], tmp[MF][NF][2];
 #pragma unroll
@@ -633,7 +640,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
             for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int jj = nf * 8 + 2 * kq + h;
+                    const int jj = cg * WC + nf * 8 + 2 * kq + h;
                     const double wv = jj < bcols ? sm.w[st][jj] : 0.0;
 #pragma unroll
                     for (int mf = 0; mf < MF; ++mf) {
@@ -653,13 +660,13 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
             if (a.probe != 1) {
                 if (cnt == BK) {  // full chunk: DMMA only
 #pragma unroll
-                    for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
-                        const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
+                    for (int k2 = 0; k2 < BK / 4 / KG; ++k2) {
+                        const int kr = (kg * (BK / 4 / KG) + k2) * 4 + kq;
                         double af[MF], bf[NF];
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
 #pragma unroll
-                        for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][bidx(kr, nf * 8 + g)];
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][bidx(kr, cg * WC + nf * 8 + g)];
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
@@ -667,13 +674,13 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
                     }
                 } else {  // partial chunk: k past the extent masked to zero in B
 #pragma unroll
-                    for (int k2 = 0; k2 < BK / 4 / KG3; ++k2) {
-                        const int kr = (kg * (BK / 4 / KG3) + k2) * 4 + kq;
+                    for (int k2 = 0; k2 < BK / 4 / KG; ++k2) {
+                        const int kr = (kg * (BK / 4 / KG) + k2) * 4 + kq;
                         double af[MF], bf[NF];
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
 #pragma unroll
-                        for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][bidx(kr, nf * 8 + g)] : 0.0;
+                        for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][bidx(kr, cg * WC + nf * 8 + g)] : 0.0;
 #pragma unroll
                         for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
@@ -686,14 +693,14 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
             if (lane == 0) tma::mbar_arrive(&sm.empty[st]);
         }
         __syncthreads();  // (1) the ring is drained by every consumer
-        double* red = reinterpret_cast<double*>(smem_raw);  // KG3 x BMM x BN
+        double* red = reinterpret_cast<double*>(smem_raw);  // KG x BMM x BN
 #pragma unroll
         for (int mf = 0; mf < MF; ++mf)
 #pragma unroll
             for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int ii = rg * WR + mf * 8 + g, jj = nf * 8 + kq * 2 + h;
+                    const int ii = rg * WR + mf * 8 + g, jj = cg * WC + nf * 8 + kq * 2 + h;
                     red[(kg * BMM + ii) * BN + jj] = acc[mf][nf][h];
                 }
     }
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(V3<WR>::NC + 32, 1) mttkrp_v3_kernel(const Mtt
         if (ii < rows && j < a.r) {
             double s = red[ii * BN + jj];
 #pragma unroll
-            for (int k = 1; k < KG3; ++k) s += red[(k * BMM + ii) * BN + jj];
+            for (int k = 1; k < KG; ++k) s += red[(k * BMM + ii) * BN + jj];
             out[i + n0 * j] = s;
         }
     }
@@ -722,22 +729,22 @@ __global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int
     }
 }
 
-template <int BN, int WR, bool BROW = false>
+template <int BN, int WR, int WC, bool BROW = false>
 void launch_v3(const MttkrpArgs& ap, const CUtensorMap& tm_t, const CUtensorMap& tm_a1, int mt, int64_t P, int nt,
                int64_t chunks, int64_t ktiles, const double* wout, double* work, cudaStream_t s) {
     const size_t smem3 = sizeof(Mttkrp3Smem<BN>);
     static bool attr3 = false;
     if (!attr3) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, BROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, WC, BROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem3));
         attr3 = true;
     }
-    mttkrp_v3_kernel<BN, WR, BROW><<<dim3(mt, (unsigned)P, nt), V3<WR>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
+    mttkrp_v3_kernel<BN, WR, WC, BROW><<<dim3(mt, (unsigned)P, nt), V3<BN, WR, WC>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
                                                                                            ktiles, wout, work);
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
         cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR, BROW>);
+        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR, WC, BROW>);
         throw Error(CPHIFI_CUDA_ERROR, std::string("mttkrp_v3 launch: ") + cudaGetErrorString(le) + " regs " +
                                            std::to_string(fa.numRegs) + " maxthreads " + std::to_string(fa.maxThreadsPerBlock));
     }
@@ -785,10 +792,14 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
     if constexpr (BN <= 32) {
         static_assert(sizeof(double) * KGV * BMM * BN <= sizeof(GemmSmem<BN, BMM, STM>), "reduction fits");
         if (v3) {
-            int wr = 32;
-            if (const char* e = std::getenv("CPHIFI_MTTKRP_WR")) wr = std::atoi(e) == 16 ? 16 : 32;
-            if (wr == 16) launch_v3<BN, 16, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
-            else launch_v3<BN, 32, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            int wc = BN >= 16 ? 16 : BN;  // warp tile 32 x 16 (KG = 1 at BN = 32); CPHIFI_MTTKRP_WC=32 -> 32 x 32, KG = 2
+            if (const char* e = std::getenv("CPHIFI_MTTKRP_WC")) wc = std::atoi(e);
+            if constexpr (BN == 32) {
+                if (wc == 32) launch_v3<BN, 32, 32, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+                else launch_v3<BN, 32, 16, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            } else {
+                launch_v3<BN, 32, BN, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+            }
         } else if (v2) {
             static bool attr2 = false;
             if (!attr2) {
@@ -1056,8 +1067,9 @@ void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
                     (brow ? encode_tmap_2d_f64(&tm_b, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.b_rs, BN + 4, BK)
                           : encode_tmap_2d_f64(&tm_b, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.b_cs, BK + 4, BN));
     if (!ok) throw Error(CPHIFI_CUDA_ERROR, "gemm: tensor map encoding failed");
-    if (brow) launch_v3<BN, 32, true>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
-    else launch_v3<BN, 32, false>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
+    constexpr int WC = BN >= 16 ? 16 : BN;
+    if (brow) launch_v3<BN, 32, WC, true>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
+    else launch_v3<BN, 32, WC, false>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
     const int64_t cnt = g.m * (g.c2 ? std::max(g.n, g.ld2) : g.n);
     reduce_epi_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(work.get(), (int)P, g.m,
                                                                                                   g.n, g);
