@@ -150,6 +150,7 @@ def secondary(args, ctx, cp, p, c, lib, x, y, stream, flush):
     fp64 = sec["fp64_peak"].get("dmma_tflops", 40.0) if isinstance(sec["fp64_peak"], dict) else 40.0
     attempt("config1_pcg_solve", lambda: bs.config1_pcg(cp, p, c))
     attempt("config1_gram_matvec_ms_l2_flushed", lambda: bs.gram_matvec_ms(p, lib, x, y, stream, flush))
+    attempt("config1_precond_apply_ms", lambda: bs.precond_ms(p, lib, c.shape[0], c.r))
     attempt("config0_aligned", lambda: bs.aligned("config0", ctx, 20, fp64))
     attempt("config2_aligned", lambda: bs.aligned("config2", ctx, 10, fp64))
     attempt("als_infinite_update", lambda: bs.als_updates(ctx, p, c))

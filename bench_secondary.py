@@ -169,6 +169,7 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
         t0 = time.perf_counter()
         mode.eig()
         out["eigK_s"] = time.perf_counter() - t0
+        out["precond_apply_ms"] = precond_ms(p, lib, n, r)
         rep = cp.SolveReport()
         cp.solve_unaligned_pcg(p, cp.PcgConfig(cfg.tol, cfg.max_iter), rep)
         out["pcg_gram"] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
@@ -220,3 +221,27 @@ def als_updates(ctx, p, c):
                               "update_and_error_s": ua.update_s,
                               "note": "relative error via ||T||^2 - 2<A,B> + 1'(A'A o V)1: no N-sized pass"}
     return out
+
+
+def precond_ms(p, lib, n, r, iters=20):
+    """Device time of one preconditioner application M^-1 x (unaligned.hpp:135-139), reported
+    per PCG iteration next to the operator."""
+    import torch
+    from paper_2603_25691_b200 import _capi
+    import paper_2603_25691_b200 as cp
+    dev = torch.device("cuda", 0)
+    x = torch.randn(n * r, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    cp.build_preconditioner(p)  # eig(V), D (setup)
+    _capi.check(lib.cphifi_unaligned_precond_apply_device(p.handle, x.data_ptr(), y.data_ptr()))
+    stream = torch.cuda.ExternalStream(p.mode.ctx.stream(), device=dev)
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            _capi.check(lib.cphifi_unaligned_precond_apply_device(p.handle, x.data_ptr(), y.data_ptr()))
+            b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
