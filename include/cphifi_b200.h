@@ -176,6 +176,12 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
  * [4] y = K Yhat + lambda Xhat + rho x, [5] the whole matvec. */
 int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters,
                                   double* ms_out);
+/* Throughput hook: `steps` operator applications back to back in ONE CUDA graph, application t
+ * on plan ps[t % m] with its own DEVICE buffers xs / ys; *total_ms = the event-timed graph (after
+ * one warm-up launch).  With m plans whose working sets together exceed L2, every application
+ * starts L2-cold with no flush inside the timed region. */
+int cphifi_unaligned_matvec_cycle_timed(const cphifi_unaligned* ps, const double* const* xs,
+                                        double* const* ys, int m, int steps, float* total_ms);
 /* Benchmark hook: `steps` operator applications on DEVICE buffers x, y captured in ONE CUDA
  * graph, each preceded (outside its event pair) by a memset of `flush_bytes` at `flush` that
  * evicts L2; the graph is launched once to warm up and once timed.  ms_out[i] receives the

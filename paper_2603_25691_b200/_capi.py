@@ -115,6 +115,9 @@ _SIGS = [
     ("cphifi_solve_unaligned_pcg", ctypes.c_int,
      [_H, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC), c_double_p, c_double_p]),
     ("cphifi_unaligned_matvec_timed", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c_double_p]),
+    ("cphifi_unaligned_matvec_cycle_timed", ctypes.c_int,
+     [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+      ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
     ("cphifi_unaligned_matvec_graph_timed", ctypes.c_int,
      [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
       ctypes.POINTER(ctypes.c_float)]),
