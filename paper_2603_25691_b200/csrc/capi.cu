@@ -122,6 +122,17 @@ const double* mode_ut(cphifi_mode m) {
     return m->ut.get();
 }
 
+// U diag(mu) for the eigenbasis PCG (K X = U diag(mu) U' X with the clamped spectrum)
+const double* mode_um(cphifi_mode m) {
+    std::lock_guard<std::mutex> lk(m->mu_lock);
+    if (!m->have_um) {
+        m->um.alloc(m->n * m->n);
+        scale_cols(m->u.get(), m->n, m->mu.get(), m->um.get(), m->ctx->stream);
+        m->have_um = true;
+    }
+    return m->um.get();
+}
+
 // Per-thread pinned, device-mapped status word for kernels that report a data error (zero
 // decoupled denominator): no allocation and no extra synchronisation per call; the caller reads
 // it after the synchronisation it performs anyway.
@@ -477,6 +488,77 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
     gemm(o, ctx->num_sms, ctx->stream);
 }
 
+// ---- the PCG in the eigenbasis of K (large n) ---------------------------------------------
+// With K = U diag(mu) U' (the clamped spectrum the preconditioner already uses) and the PCG run on
+// x~ = (I x U') x, an orthogonal change of variables (same inner products, same iterates in exact
+// arithmetic):  A~ x~ = mu o (U' Yhat) + lambda mu o x~ + rho x~  with  Xhat = U diag(mu) x~,  and
+// the preconditioner becomes  M~^-1 r~ = ((r~ U_V) o D) U_V'  — no n x n product.  Two n x n x r
+// GEMMs per iteration instead of four (K X, K Yhat, U'R, U Z).  K differs from its clamped
+// reconstruction by the clamped negative eigenvalues (rounding-level for the configs' kernels).
+bool pcg_eigbasis(cphifi_unaligned p) {
+    bool on = !p->small_n;
+    if (const char* e = std::getenv("CPHIFI_PCG_EIGBASIS")) on = std::atoi(e) != 0;
+    return on && p->mode;
+}
+
+void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
+    need_mode(p);
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    GemmArgs g;  // Xhat = U diag(mu) x~  -> row-major padded copy for the gather
+    g.m = n; g.n = r; g.k = n;
+    g.a = mode_um(p->mode); g.a_rs = 1; g.a_cs = n;
+    g.b = xt; g.b_rs = 1; g.b_cs = n;
+    g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
+    gemm(g, ctx->num_sms, ctx->stream);
+    const double* gr = p->op == 1 ? p->gram.get() : nullptr;
+    if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), n, p->rp, p->yhat_rm.get(), ctx->stream);
+    else launch_phase_b(p, fused_args(p, PH_B));
+    allreduce_yhat(p);
+    GemmArgs h;  // y~ = mu o (U' Yhat + lambda x~) + rho x~
+    h.m = n; h.n = r; h.k = n;
+    h.a = mode_ut(p->mode); h.a_rs = 1; h.a_cs = n;
+    h.b = yhat_result(p); h.b_rs = p->rp; h.b_cs = 1;
+    h.c = yt; h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get(); h.e1 = xt; h.ld_e = n;
+    h.beta1 = p->mode->lambda; h.beta2 = p->rho;
+    gemm(h, ctx->num_sms, ctx->stream);
+}
+
+void precond_rot(cphifi_unaligned p, const double* rt, double* zt) {
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    GemmArgs h;  // t2 = (r~ U_V) .* D
+    h.m = n; h.n = r; h.k = r;
+    h.a = rt; h.a_rs = 1; h.a_cs = n;
+    h.b = p->uv.get(); h.b_rs = 1; h.b_cs = r;
+    h.c = p->t2.get(); h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_HADAMARD; h.e1 = p->dmat.get(); h.ld_e = n;
+    gemm(h, ctx->num_sms, ctx->stream);
+    GemmArgs o;  // z~ = t2 U_V'
+    o.m = n; o.n = r; o.k = r;
+    o.a = p->t2.get(); o.a_rs = 1; o.a_cs = n;
+    o.b = p->uv.get(); o.b_rs = r; o.b_cs = 1;
+    o.c = zt; o.c_rs = 1; o.c_cs = n;
+    gemm(o, ctx->num_sms, ctx->stream);
+}
+
+// y = op(U) x (column-major n x r), op = U' (transpose) or U, optionally rows scaled by mu
+void rotate(cphifi_unaligned p, bool transpose, bool scale_mu, const double* x, double* y) {
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t n = p->n, r = p->r;
+    GemmArgs g;
+    g.m = n; g.n = r; g.k = n;
+    g.a = transpose ? mode_ut(p->mode) : p->mode->u.get(); g.a_rs = 1; g.a_cs = n;
+    g.b = x; g.b_rs = 1; g.b_cs = n;
+    g.c = y; g.c_rs = 1; g.c_cs = n;
+    if (scale_mu) {
+        g.epi = EPI_ROWSCALE;
+        g.e_row = p->mode->mu.get();
+    }
+    gemm(g, ctx->num_sms, ctx->stream);
+}
+
 // solve_aligned_decoupled core on device buffers (aligned.hpp:41-54)
 // Enqueues only: the zero-denominator status lands in the returned mapped word, which the caller
 // checks (decoupled_check) after its own synchronisation.
@@ -561,8 +643,8 @@ bool pcg_graph_ok(cphifi_unaligned p) {
 // instantiate it, once per plan and operator form.  The captured pointers are the plan's
 // persistent PCG vectors, so later solves reuse the executable graph.
 template <class F>
-bool ensure_pcg_graph(cphifi_unaligned p, F&& body) {
-    if (p->pcg_exec && p->pcg_graph_op == p->op) return true;
+bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
+    if (p->pcg_exec && p->pcg_graph_op == p->op && p->pcg_graph_rot == (int)rot) return true;
     if (p->pcg_exec) cudaGraphExecDestroy(p->pcg_exec);
     if (p->pcg_graph) cudaGraphDestroy(p->pcg_graph);
     p->pcg_exec = nullptr;
@@ -593,6 +675,7 @@ bool ensure_pcg_graph(cphifi_unaligned p, F&& body) {
         p->pcg_graph = g;
         p->pcg_exec = ex;
         p->pcg_graph_op = p->op;
+        p->pcg_graph_rot = (int)rot;
         return true;
     } catch (const Error& e) {
         if (capturing) {
@@ -803,6 +886,7 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         mode->u.alloc(n * n);
         mode->mu.alloc(n);
         mode->have_ut = false;
+        mode->have_um = false;
         h2d(mode->u.get(), u, sizeof(double) * n * n, mode->ctx->stream);
         h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
         clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);
@@ -1591,8 +1675,10 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         PcgCtl* ctl = reinterpret_cast<PcgCtl*>(partial + 80 + (sizeof(PcgState) + 7) / 8);
         CPHIFI_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * 80, s));
         CPHIFI_CUDA(cudaMemsetAsync(st, 0, sizeof(PcgState), s));
-        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
         ensure_precond(p);                                                        // build_preconditioner
+        const bool rot = pcg_eigbasis(p);
+        if (rot) rotate(p, true, true, p->b.get(), bvec);  // rhs~ = (I x U') vec(K B) = mu o (U' B)
+        else gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;
@@ -1607,16 +1693,29 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             rep.converged = 1;
         } else {
             CPHIFI_CUDA(cudaMemcpyAsync(&st->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
+            auto apply_a = [&](const double* xin, double* yout) {
+                if (rot) matvec_rot(p, xin, yout);
+                else matvec_dev(p, xin, yout);
+            };
+            auto apply_m = [&](const double* rin, double* zout) {
+                if (rot) precond_rot(p, rin, zout);
+                else precond_dev(p, rin, zout);
+            };
             if (warm_start) {
-                h2d(x, warm_start, sizeof(double) * nr, s);
-                matvec_dev(p, x, ap);
+                if (rot) {  // x0~ = (I x U') x0
+                    h2d(ap, warm_start, sizeof(double) * nr, s);
+                    rotate(p, true, false, ap, x);
+                } else {
+                    h2d(x, warm_start, sizeof(double) * nr, s);
+                }
+                apply_a(x, ap);
                 ++matvecs;
                 axpby(res, bvec, 1.0, ap, -1.0, nr, s);  // r = b - A x0
             } else {
                 CPHIFI_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nr, s));
                 CPHIFI_CUDA(cudaMemcpyAsync(res, bvec, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
             }
-            precond_dev(p, res, z);
+            apply_m(res, z);
             pcg_init(res, z, pv, nr, st, partial, s);
             PcgState hst;
             d2h_sync(&hst, st, sizeof(PcgState), s);
@@ -1625,11 +1724,11 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             int it = 0;
             // one PCG iteration (solvers.hpp:59-80): the host loop below and the graph body
             auto body_a = [&] {
-                matvec_dev(p, pv, ap);
+                apply_a(pv, ap);
                 pcg_step_a(x, res, pv, ap, nr, st, partial, s);
             };
             auto body_b = [&] {
-                precond_dev(p, res, z);
+                apply_m(res, z);
                 pcg_step_b(res, z, pv, nr, st, partial, s);
             };
             bool done = false;
@@ -1637,7 +1736,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             if (rel > cfg->tol && pcg_graph_ok(p)) {
                 // device-resident loop: a CUDA graph whose WHILE node repeats the iteration until
                 // pcg_ctl clears the condition; no host round trip per iteration
-                if (ensure_pcg_graph(p, [&](cudaGraphConditionalHandle h) {
+                if (ensure_pcg_graph(p, rot, [&](cudaGraphConditionalHandle h) {
                         body_a();
                         pcg_ctl(st, ctl, h, s);
                         body_b();
@@ -1681,6 +1780,10 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             rep.iterations = it;
             rep.relative_residual = rel;
             rep.converged = rel <= cfg->tol;
+        }
+        if (rot && bnorm != 0.0) {  // W = (I x U) x~
+            rotate(p, false, false, x, ap);
+            CPHIFI_CUDA(cudaMemcpyAsync(x, ap, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
         }
         d2h_sync(w_out, x, sizeof(double) * nr, s);
         const auto t1 = std::chrono::steady_clock::now();

@@ -106,6 +106,8 @@ struct cphifi_mode_s {
     cphifi::DevBuf<double> mu;      // eigenvalues (ascending, clamped at 0)
     cphifi::DevBuf<double> ut;      // U' (k_sandwich.cu phase 2), built on first use
     bool have_ut = false;
+    cphifi::DevBuf<double> um;      // U diag(mu) (eigenbasis PCG: K X = U diag(mu) U'X), lazily
+    bool have_um = false;
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;
@@ -179,6 +181,7 @@ struct cphifi_unaligned_s {
     double* hv_hy = nullptr;
     bool hv_failed = false;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
+    int pcg_graph_rot = -1;                   // basis (0 original, 1 eigenbasis) of the captured graph
     bool pcg_graph_failed = false;
     ~cphifi_unaligned_s() {
         if (pcg_exec) cudaGraphExecDestroy(pcg_exec);

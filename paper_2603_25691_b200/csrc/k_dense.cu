@@ -132,6 +132,11 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, int64_t i, int
                 out = v / den;
                 break;
             }
+            case EPI_ROWSCALE: {
+                const double e = g.e1 ? g.e1[i + g.ld_e * j] : 0.0;
+                out = g.e_row[i] * (v + g.beta1 * e) + g.beta2 * e;
+                break;
+            }
             default:
                 break;
         }

@@ -12,6 +12,7 @@
 // element-wise op in its epilogue.  Two launches replace four DMMA GEMM launches plus an
 // epilogue pass; the n x n factor is read once per phase (HBM/L2 bound: 8 n^2 bytes per phase),
 // the r x n chunks come from L2.  Every sum has a fixed order: bit-reproducible.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -350,6 +351,17 @@ __global__ void transpose_kernel(const double* __restrict__ a, int64_t n, double
         const int64_t i = by + threadIdx.x, j = bx + yy;  // at(i, j) = a(j, i)
         if (i < n && j < n) at[i + n * j] = t[threadIdx.x][yy];
     }
+}
+
+__global__ void scale_cols_kernel(const double* __restrict__ a, int64_t n, const double* __restrict__ d,
+                                  double* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = a[e] * d[e / n];
+}
+
+void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaStream_t s) {
+    scale_cols_kernel<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, s>>>(a, n, d, out);
+    CPHIFI_CHECK_LAUNCH();
 }
 
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {

@@ -12,7 +12,8 @@ enum EpiOp : int {
     EPI_STORE = 0,    // C = AB
     EPI_AXPY2 = 1,    // C = (AB + beta1*E1) + beta2*E2     (unaligned.hpp:112-114 order)
     EPI_HADAMARD = 2, // C = AB .* E1                        (unaligned.hpp:137)
-    EPI_SCALE_DIV = 3 // C = AB / (e_row[i]*e_col[j] + beta1) with zero-denominator flag
+    EPI_SCALE_DIV = 3, // C = AB / (e_row[i]*e_col[j] + beta1) with zero-denominator flag
+    EPI_ROWSCALE = 4   // C = e_row[i] * (AB + beta1*E1) + beta2*E1   (E1 may be null: 0)
 };
 
 struct GemmArgs {
@@ -89,6 +90,8 @@ bool sandwich_supported(int64_t n, int64_t r);
 int64_t sandwich_rp(int64_t r);
 void sandwich(SandArgs a, int num_sms, cudaStream_t s);
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
+// out = a diag(d)  (n x n column-major)
+void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaStream_t s);
 
 // ---- the unaligned operator as one persistent cooperative kernel (k_fused.cu) -----------
 // PH_A: Xhat rows distributed + barrier; PH_AL: each CTA computes only the Xhat rows its own

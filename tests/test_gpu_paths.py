@@ -147,3 +147,42 @@ def test_equal_partition_split_rows(cp, monkeypatch, equal):
     c, p, sub, ek = _config1_problem(cp, shared=False)
     x = np.random.default_rng(5).normal(size=c.shape[0] * c.r)
     assert ri.rel(cp.unaligned_matvec(p, x), orc.unaligned_matvec(sub, x)) < 1e-12
+
+
+@pytest.mark.parametrize("op", ["stream", "gram"])
+def test_pcg_eigenbasis_matches_original_basis(cp, monkeypatch, op):
+    """PCG in the eigenbasis of K (large n: two n x n products per iteration instead of four) vs
+    the reference-structured PCG and the oracle: iterations within +-1, residual <= tol, W within
+    the solve tolerance (the clamped spectrum differs from K only at rounding level)."""
+    g = np.random.default_rng(600)
+    shape, r, q = [600, 30, 20], 8, 30000
+    pts = np.sort(g.uniform(0, 1, shape[0]))
+    lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+    idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+    vals = g.normal(size=q)
+    factors = [np.zeros((shape[0], r))] + [g.normal(size=(n, r)) for n in shape[1:]]
+    mode = cp.RkhsMode(pts, 0.05, 1e-3)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), 0, mode, 1e-6)
+    p.set_operator(op)
+    cfg = cp.PcgConfig(1e-8, 500)
+    out = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("CPHIFI_PCG_EIGBASIS", rot)
+        rep = cp.SolveReport()
+        out[rot] = (cp.solve_unaligned_pcg(p, cfg, rep), rep)
+    sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 0, kern, 1e-3, 1e-6)
+    orep = orc.SolveReport()
+    wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-8, 500), ek, orc.sym_eig(sub.v), report=orep)
+    for rot, (w, rep) in out.items():
+        assert rep.converged and rep.relative_residual <= 1e-8, rot
+        assert abs(rep.iterations - orep.iterations) <= 1, (rot, rep.iterations, orep.iterations)
+        assert ri.rel(w, wo) < 1e-6, rot
+    # warm start from the solution: converges at once in both bases
+    for rot in ("0", "1"):
+        monkeypatch.setenv("CPHIFI_PCG_EIGBASIS", rot)
+        rep = cp.SolveReport()
+        cp.solve_unaligned_pcg(p, cfg, rep, warm_start=out["0"][0])
+        assert rep.iterations <= 1, rot
