@@ -690,6 +690,77 @@ bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
     }
 }
 
+// Whole-solve graph: segment A (captured) -> WHILE node (body captured) -> segment B (captured).
+// Built once per plan, operator form and basis; the captured pointers are the plan's persistent
+// PCG vectors.  Returns false (and disables itself for the plan) when capture fails.
+template <class FA, class FW, class FB>
+bool ensure_pcg_full_graph(cphifi_unaligned p, bool rot, FA&& seg_a, FW&& body, FB&& seg_b) {
+    if (p->pcgf_exec && p->pcgf_op == p->op && p->pcgf_rot == (int)rot) return true;
+    if (p->pcgf_exec) cudaGraphExecDestroy(p->pcgf_exec);
+    if (p->pcgf_graph) cudaGraphDestroy(p->pcgf_graph);
+    p->pcgf_exec = nullptr;
+    p->pcgf_graph = nullptr;
+    cudaStream_t s = p->obs->ctx->stream;
+    CPHIFI_CUDA(cudaStreamSynchronize(s));
+    cudaGraph_t g = nullptr;
+    bool capturing = false;
+    try {
+        CPHIFI_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CPHIFI_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        CPHIFI_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        seg_a(h);
+        capturing = false;
+        CPHIFI_CUDA(cudaStreamEndCapture(s, &g));
+        // leaves of segment A
+        size_t nn = 0;
+        CPHIFI_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn), leaves;
+        CPHIFI_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (auto nd : nodes) {
+            size_t ndep = 0;
+            CPHIFI_CUDA(cudaGraphNodeGetDependentNodes(nd, nullptr, &ndep));
+            if (ndep == 0) leaves.push_back(nd);
+        }
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        CPHIFI_CUDA(cudaGraphAddNode(&wnode, g, leaves.data(), leaves.size(), &cp));
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        CPHIFI_CUDA(cudaStreamBeginCaptureToGraph(s, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        body(h);
+        capturing = false;
+        CPHIFI_CUDA(cudaStreamEndCapture(s, &bodyg));
+        CPHIFI_CUDA(cudaStreamBeginCaptureToGraph(s, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
+        capturing = true;
+        seg_b();
+        capturing = false;
+        CPHIFI_CUDA(cudaStreamEndCapture(s, &g));
+        cudaGraphExec_t ex = nullptr;
+        CPHIFI_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        p->pcgf_graph = g;
+        p->pcgf_exec = ex;
+        p->pcgf_op = p->op;
+        p->pcgf_rot = (int)rot;
+        return true;
+    } catch (const Error& e) {
+        if (capturing) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(s, &junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        p->pcg_graph_failed = true;
+        if (std::getenv("CPHIFI_DEBUG")) std::fprintf(stderr, "cphifi: PCG solve graph disabled: %s\n", e.what());
+        return false;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1682,6 +1753,101 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;
+        auto apply_a = [&](const double* xin, double* yout) {
+            if (rot) matvec_rot(p, xin, yout);
+            else matvec_dev(p, xin, yout);
+        };
+        auto apply_m = [&](const double* rin, double* zout) {
+            if (rot) precond_rot(p, rin, zout);
+            else precond_dev(p, rin, zout);
+        };
+        // ---- whole solve on device: one graph launch, one synchronisation -----------------
+        if (p->op == 1) ensure_gram(p);
+        if (pcg_graph_ok(p)) {
+            if (warm_start) {  // r0 = b - A x0 before the graph (x0 rotated in the eigenbasis)
+                if (rot) {
+                    h2d(ap, warm_start, sizeof(double) * nr, s);
+                    rotate(p, true, false, ap, x);
+                } else {
+                    h2d(x, warm_start, sizeof(double) * nr, s);
+                }
+                apply_a(x, ap);
+                axpby(res, bvec, 1.0, ap, -1.0, nr, s);
+            }
+            const bool ok = ensure_pcg_full_graph(
+                p, rot,
+                [&](cudaGraphConditionalHandle h) {
+                    dot_to(bvec, bvec, nr, partial, &st->bnorm, s);
+                    pcg_prologue(st, ctl, s);
+                    pcg_x0(x, res, bvec, nr, ctl, s);
+                    apply_m(res, z);
+                    pcg_init(res, z, pv, nr, st, partial, s);
+                    pcg_loopctl(st, ctl, h, s);
+                },
+                [&](cudaGraphConditionalHandle h) {
+                    apply_a(pv, ap);
+                    pcg_step_a(x, res, pv, ap, nr, st, partial, s);
+                    pcg_ctl(st, ctl, h, s);
+                    apply_m(res, z);
+                    pcg_step_b(res, z, pv, nr, st, partial, s);
+                },
+                [&] {
+                    if (rot) {  // W = (I x U) x~
+                        rotate(p, false, false, x, ap);
+                        CPHIFI_CUDA(cudaMemcpyAsync(x, ap, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
+                    }
+                });
+            if (ok) {
+                const int cap = cfg->record_history ? cfg->max_iter : 0;
+                if (cap > 0 && p->pcg_hist.n < (size_t)cap) p->pcg_hist.alloc(cap);
+                PcgCtl hc{};
+                hc.tol = cfg->tol;
+                hc.max_iter = cfg->max_iter;
+                hc.hist = cap > 0 ? p->pcg_hist.get() : nullptr;
+                hc.hist_cap = cap;
+                hc.warm = warm_start ? 1 : 0;
+                CPHIFI_CUDA(cudaMemcpyAsync(ctl, &hc, sizeof(PcgCtl), cudaMemcpyHostToDevice, s));
+                CPHIFI_CUDA(cudaGraphLaunch(p->pcgf_exec, s));
+                PcgCtl* hcp = reinterpret_cast<PcgCtl*>(hs);
+                PcgState* hst = reinterpret_cast<PcgState*>(hs + (sizeof(PcgCtl) + 7) / 8);
+                CPHIFI_CUDA(cudaMemcpyAsync(hcp, ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+                CPHIFI_CUDA(cudaMemcpyAsync(hst, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+                d2h_sync(w_out, x, sizeof(double) * nr, s);  // the one synchronisation
+                cphifi_solve_report rep{};
+                std::vector<double> hist;
+                if (hcp->zero_b) {
+                    rep.converged = 1;  // x = 0 (solvers.hpp:49-53)
+                } else {
+                    if (hst->flag == 1) throw_runtime("pcg: non-finite value encountered");
+                    if (hst->flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
+                    const int it = hcp->it;
+                    const double rel = it > 0 ? hst->rel : hcp->rel0;
+                    if (cfg->record_history) {
+                        hist.push_back(hcp->rel0);
+                        const int m = std::min(it, cap);
+                        hist.resize(1 + m);
+                        if (m > 0) d2h_sync(hist.data() + 1, p->pcg_hist.get(), sizeof(double) * m, s);
+                    }
+                    rep.iterations = it;
+                    rep.relative_residual = rel;
+                    rep.converged = rel <= cfg->tol;
+                    rep.matvecs = it + (warm_start ? 1 : 0);
+                }
+                const auto t1 = std::chrono::steady_clock::now();
+                rep.wall_time_s = std::chrono::duration<double>(t1 - t0).count();
+                rep.setup_s = std::chrono::duration<double>(t_setup - t0).count();
+                if (report) {
+                    double* hbuf = report->residual_history;
+                    const int hcap = report->history_capacity;
+                    rep.residual_history = hbuf;
+                    rep.history_capacity = hcap;
+                    rep.history_len = (int32_t)hist.size();
+                    if (hbuf) std::memcpy(hbuf, hist.data(), sizeof(double) * std::min<size_t>(hist.size(), (size_t)std::max(hcap, 0)));
+                    *report = rep;
+                }
+                return;
+            }
+        }
         dot_to(bvec, bvec, nr, partial, &st->bnorm, s);
         d2h_sync(hs, &st->bnorm, sizeof(double), s);
         const double bnorm = std::sqrt(hs[0]);
@@ -1693,14 +1859,6 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             rep.converged = 1;
         } else {
             CPHIFI_CUDA(cudaMemcpyAsync(&st->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
-            auto apply_a = [&](const double* xin, double* yout) {
-                if (rot) matvec_rot(p, xin, yout);
-                else matvec_dev(p, xin, yout);
-            };
-            auto apply_m = [&](const double* rin, double* zout) {
-                if (rot) precond_rot(p, rin, zout);
-                else precond_dev(p, rin, zout);
-            };
             if (warm_start) {
                 if (rot) {  // x0~ = (I x U') x0
                     h2d(ap, warm_start, sizeof(double) * nr, s);

@@ -182,10 +182,17 @@ struct cphifi_unaligned_s {
     bool hv_failed = false;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
     int pcg_graph_rot = -1;                   // basis (0 original, 1 eigenbasis) of the captured graph
+    // the whole solve after the right-hand side as one graph: [bnorm, x0, M^-1 r0, init, loop
+    // control] -> WHILE(iteration) -> [W = U x~]
+    cudaGraph_t pcgf_graph = nullptr;
+    cudaGraphExec_t pcgf_exec = nullptr;
+    int pcgf_op = -1, pcgf_rot = -1;
     bool pcg_graph_failed = false;
     ~cphifi_unaligned_s() {
         if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
         if (pcg_graph) cudaGraphDestroy(pcg_graph);
+        if (pcgf_exec) cudaGraphExecDestroy(pcgf_exec);
+        if (pcgf_graph) cudaGraphDestroy(pcgf_graph);
         if (hv_exec) cudaGraphExecDestroy(hv_exec);
         if (hv_graph) cudaGraphDestroy(hv_graph);
         if (hv_hx) cudaFreeHost(hv_hx);

@@ -145,6 +145,26 @@ __global__ void pcg_ctl_kernel(const PcgState* st, PcgCtl* c, cudaGraphCondition
     }
 }
 
+__global__ void pcg_prologue_kernel(PcgState* st, PcgCtl* c) {
+    const double bn = sqrt(st->bnorm);
+    st->bnorm = bn;
+    c->zero_b = bn == 0.0;
+}
+__global__ void pcg_x0_kernel(double* __restrict__ x, double* __restrict__ res, const double* __restrict__ b, int64_t n,
+                              const PcgCtl* c) {
+    const bool warm = c->warm && !c->zero_b;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!warm) {
+            x[i] = 0.0;
+            res[i] = b[i];
+        }
+    }
+}
+__global__ void pcg_loopctl_kernel(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle hwhile) {
+    c->rel0 = st->rel;
+    if (c->zero_b || !(st->rel > c->tol)) cudaGraphSetConditional(hwhile, 0u);
+}
+
 // 16-byte copies (either side may be mapped host memory: one PCIe stream instead of a DMA node)
 __global__ void copy16_kernel(double2* __restrict__ dst, const double2* __restrict__ src, int64_t n2) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
@@ -253,6 +273,18 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
               cudaStream_t s) {
     pcg_init_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, z, p, n, st, partial);
     pcg_rr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, n, st, partial);
+    CPHIFI_CHECK_LAUNCH();
+}
+void pcg_prologue(PcgState* st, PcgCtl* c, cudaStream_t s) {
+    pcg_prologue_kernel<<<1, 1, 0, s>>>(st, c);
+    CPHIFI_CHECK_LAUNCH();
+}
+void pcg_x0(double* x, double* res, const double* b, int64_t n, const PcgCtl* c, cudaStream_t s) {
+    pcg_x0_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, res, b, n, c);
+    CPHIFI_CHECK_LAUNCH();
+}
+void pcg_loopctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle hwhile, cudaStream_t s) {
+    pcg_loopctl_kernel<<<1, 1, 0, s>>>(st, c, hwhile);
     CPHIFI_CHECK_LAUNCH();
 }
 void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s) {

@@ -195,8 +195,16 @@ struct PcgCtl {
     int max_iter, it;
     double* hist;  // device history (rel after each iteration), hist_cap entries
     int hist_cap, stop;
+    int warm, zero_b;  // whole-solve graph: warm start given; ||b|| == 0
+    double rel0;       // relative residual of the initial guess
 };
 void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
+// whole-solve graph pieces: bnorm = sqrt(bnorm), zero_b
+void pcg_prologue(PcgState* st, PcgCtl* c, cudaStream_t s);
+// x = 0 unless warm (zero_b: x = 0); res = b unless warm
+void pcg_x0(double* x, double* res, const double* b, int64_t n, const PcgCtl* c, cudaStream_t s);
+// after pcg_init: rel0; skip the WHILE body when zero_b or rel <= tol
+void pcg_loopctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle hwhile, cudaStream_t s);
 void dot_to(const double* x, const double* y, int64_t n, double* partial, double* out, cudaStream_t s);
 // pap = p.ap; flag; alpha = rz/pap; x += alpha p; r -= alpha ap; rr = r.r; rel = sqrt(rr)/bnorm
 void pcg_step_a(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st,
