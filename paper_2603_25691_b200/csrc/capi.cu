@@ -1786,8 +1786,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 },
                 [&](cudaGraphConditionalHandle h) {
                     apply_a(pv, ap);
-                    pcg_step_a(x, res, pv, ap, nr, st, partial, s);
-                    pcg_ctl(st, ctl, h, s);
+                    pcg_step_a_ctl(x, res, pv, ap, nr, st, partial, ctl, h, s);
                     apply_m(res, z);
                     pcg_step_b(res, z, pv, nr, st, partial, s);
                 },

@@ -165,6 +165,71 @@ __global__ void pcg_loopctl_kernel(const PcgState* st, PcgCtl* c, cudaGraphCondi
     if (c->zero_b || !(st->rel > c->tol)) cudaGraphSetConditional(hwhile, 0u);
 }
 
+// ---- single-CTA fused PCG steps (small n r): one launch instead of two (or three) ----------
+constexpr int ONE_T = 1024;
+constexpr int64_t ONE_MAX = 32768;  // elements; above this the 64-block kernels are faster
+__device__ __forceinline__ double cta_sum(double v, double* sh) {  // all threads get the total
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < ONE_T / 32; ++w) t += sh[w];
+    __syncthreads();
+    return t;
+}
+// pap, flag, alpha; x += alpha p, r -= alpha ap; rr, rel; then (ctl) the loop control
+__global__ void __launch_bounds__(ONE_T) pcg_step_a1_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p, const double* __restrict__ ap,
+                                                            int64_t n, PcgState* st, PcgCtl* c,
+                                                            cudaGraphConditionalHandle h) {
+    __shared__ double sh[ONE_T / 32];
+    double t = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += ONE_T) t = fma(p[i], ap[i], t);
+    const double pap = cta_sum(t, sh);
+    const int flag = !isfinite(pap) ? 1 : (pap <= 0.0 ? 2 : 0);
+    const double alpha = st->rz / pap;
+    t = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += ONE_T) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * ap[i];
+        r[i] = ri;
+        t = fma(ri, ri, t);
+    }
+    const double rr = cta_sum(t, sh);
+    if (threadIdx.x == 0) {
+        st->pap = pap;
+        st->flag = flag;
+        st->alpha = alpha;
+        st->rr = rr;
+        const double rel = sqrt(rr) / st->bnorm;
+        st->rel = rel;
+        if (c) {  // pcg_ctl_kernel's work
+            const int it = ++c->it;
+            if (c->hist && it - 1 < c->hist_cap) c->hist[it - 1] = rel;
+            if (flag != 0 || !(rel > c->tol) || it >= c->max_iter) {
+                c->stop = 1;
+                cudaGraphSetConditional(h, 0);
+            }
+        }
+    }
+}
+// rz_new, beta, rz; p = z + beta p
+__global__ void __launch_bounds__(ONE_T) pcg_step_b1_kernel(const double* __restrict__ r, const double* __restrict__ z,
+                                                            double* __restrict__ p, int64_t n, PcgState* st) {
+    __shared__ double sh[ONE_T / 32];
+    double t = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += ONE_T) t = fma(r[i], z[i], t);
+    const double rz_new = cta_sum(t, sh);
+    const double beta = rz_new / st->rz;
+    for (int64_t i = threadIdx.x; i < n; i += ONE_T) p[i] = z[i] + beta * p[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->rz_new = rz_new;
+        st->beta = beta;
+        st->rz = rz_new;
+    }
+}
+
 // 16-byte copies (either side may be mapped host memory: one PCIe stream instead of a DMA node)
 __global__ void copy16_kernel(double2* __restrict__ dst, const double2* __restrict__ src, int64_t n2) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
@@ -259,14 +324,32 @@ void dot_to(const double* x, const double* y, int64_t n, double* partial, double
 }
 void pcg_step_a(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st,
                 double* partial, cudaStream_t s) {
-    pcg_pap_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, ap, n, st, partial);
-    pcg_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, ap, n, st, partial);
+    if (n <= ONE_MAX) {
+        pcg_step_a1_kernel<<<1, ONE_T, 0, s>>>(x, r, p, ap, n, st, nullptr, cudaGraphConditionalHandle{});
+    } else {
+        pcg_pap_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, ap, n, st, partial);
+        pcg_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, ap, n, st, partial);
+    }
     CPHIFI_CHECK_LAUNCH();
+}
+void pcg_step_a_ctl(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st, double* partial,
+                    PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s) {
+    if (n <= ONE_MAX) {
+        pcg_step_a1_kernel<<<1, ONE_T, 0, s>>>(x, r, p, ap, n, st, c, h);
+        CPHIFI_CHECK_LAUNCH();
+    } else {
+        pcg_step_a(x, r, p, ap, n, st, partial, s);
+        pcg_ctl(st, c, h, s);
+    }
 }
 void pcg_step_b(const double* r, const double* z, double* p, int64_t n, PcgState* st, double* partial,
                 cudaStream_t s) {
-    pcg_rz_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, z, n, st, partial);
-    pcg_p_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(z, p, n, st);
+    if (n <= ONE_MAX) {
+        pcg_step_b1_kernel<<<1, ONE_T, 0, s>>>(r, z, p, n, st);
+    } else {
+        pcg_rz_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(r, z, n, st, partial);
+        pcg_p_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(z, p, n, st);
+    }
     CPHIFI_CHECK_LAUNCH();
 }
 void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* st, double* partial,

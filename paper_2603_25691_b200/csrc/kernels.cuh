@@ -199,6 +199,9 @@ struct PcgCtl {
     double rel0;       // relative residual of the initial guess
 };
 void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
+// step A followed by the loop control (one launch for n <= 32768)
+void pcg_step_a_ctl(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st, double* partial,
+                    PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
 // whole-solve graph pieces: bnorm = sqrt(bnorm), zero_b
 void pcg_prologue(PcgState* st, PcgCtl* c, cudaStream_t s);
 // x = 0 unless warm (zero_b: x = 0); res = b unless warm
