@@ -29,6 +29,8 @@
 // accumulator stays in registers; runs are folded into a per-lane-group row accumulator in shared
 // memory; rows are reduced over lane groups in a fixed order.  Results are bit-reproducible for a
 // given plan.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace cphifi {
@@ -178,7 +180,18 @@ __device__ __forceinline__ void ld_idx(int (&v)[B], const int32_t* p) {
 
 // aux: 0 = none (operator, uncoalesced), 1 = int32 multiplicities (operator, coalesced plan),
 // 2 = fp64 weights (RHS: the observed values)
-template <int RP, int DO, bool SF, int AUX>
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit_s() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait1_s() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait0_s() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// PF: the mode-1 factor rows of the NEXT batch are copied (cp.async, each lane its own 16-byte
+// chunks, so no lane-group synchronisation) into a 2-slot per-lane-group ring while the current
+// batch computes: factors read through L1 (config 4: 256 KB, not shared-memory resident) stop
+// being a chain of dependent L1-miss -> L2 round trips.
+template <int RP, int DO, bool SF, int AUX, bool PF>
 __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
     using S = Shape<RP>;
     constexpr int VPL = S::VPL, NG = S::NG, RS = S::RS, B = S::B;
@@ -404,8 +417,27 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
                 for (int v = 0; v < VPL; ++v) accg[v] = fma(s[0], z[v], accg[v]);
             }
         };
+        // PF ring: slot (g, sl) holds B rows of RP doubles
+        double* pf_base = sfac + (int64_t)g * 2 * B * RP;
+        auto prefetch = [&](int P, bool valid, int sl) {
+            if constexpr (PF) {
+                int ib[B];
+                if (valid) ld_idx<B>(ib, ti[1] + P);
+                else {
+#pragma unroll
+                    for (int b = 0; b < B; ++b) ib[b] = 0;
+                }
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int u = 0; u < VPL / 2; ++u)
+                        cpa16(pf_base + (sl * B + b) * RP + 2 * u * G + 2 * gl,
+                              fac_m[1] + (int64_t)ib[b] * RP + 2 * u * G + 2 * gl);
+                cpa_commit_s();
+            }
+        };
         // B observations at aligned staged position P, all in one run (else `need` defers them)
-        auto batch = [&](int P, bool valid) {
+        auto batch = [&](int P, bool valid, int sl) {
             int ia[B];
             if (valid) ld_idx<B>(ia, ti[0] + P);
             else {
@@ -427,8 +459,14 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
 #pragma unroll
                     for (int b = 0; b < B; ++b) ib[b] = 0;
                 }
+                if constexpr (PF) {
+                    cpa_wait1_s();  // this lane's copies of this batch have landed
 #pragma unroll
-                for (int b = 0; b < B; ++b) ld_row<RP, SF>(z[b], fac_m[1] + (int64_t)ib[b] * RP, gl);
+                    for (int b = 0; b < B; ++b) ld_row<RP, true>(z[b], pf_base + (sl * B + b) * RP, gl);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < B; ++b) ld_row<RP, SF>(z[b], fac_m[1] + (int64_t)ib[b] * RP, gl);
+                }
             }
 #pragma unroll
             for (int m = 2; m < DO; ++m) {
@@ -496,7 +534,17 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
 #pragma unroll 1
             for (int h = 0; h < nh; ++h) one(pb + h, pb + h < pa);
 #pragma unroll 1
-            for (int j = 0; j < nb; ++j) batch(pa + j * B, j < nbat);
+            if constexpr (PF) {
+                if (nb > 0) prefetch(pa, 0 < nbat, 0);
+                for (int j = 0; j < nb; ++j) {
+                    if (j + 1 < nb) prefetch(pa + (j + 1) * B, j + 1 < nbat, (j + 1) & 1);
+                    else cpa_commit_s();  // keep one group per batch: wait_group 1 = this batch
+                    batch(pa + j * B, j < nbat, j & 1);
+                }
+                cpa_wait0_s();
+            } else {
+                for (int j = 0; j < nb; ++j) batch(pa + j * B, j < nbat, 0);
+            }
 #pragma unroll 1
             for (int h = 0; h < nt; ++h) one(pt + h, pt + h < pe);
             seg = seg_end;
@@ -523,9 +571,9 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
 
 int aux_kind(const FusedArgs& a) { return a.weights ? 2 : (a.mult ? 1 : 0); }
 
-template <int RP, int DO, bool SF, int AUX>
+template <int RP, int DO, bool SF, int AUX, bool PF>
 void launch_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
-    auto kern = stream_kernel<RP, DO, SF, AUX>;
+    auto kern = stream_kernel<RP, DO, SF, AUX, PF>;
     static bool attr = false;
     if (!attr) {
         CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP));
@@ -534,31 +582,35 @@ void launch_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     kern<<<grid, ST, smem, s>>>(a);
 }
 
-template <int RP, int DO, bool SF>
+template <int RP, int DO, bool SF, bool PF>
 void launch_sf(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     switch (aux_kind(a)) {
-        case 0: launch_t<RP, DO, SF, 0>(a, grid, smem, s); break;
-        case 1: launch_t<RP, DO, SF, 1>(a, grid, smem, s); break;
-        default: launch_t<RP, DO, SF, 2>(a, grid, smem, s); break;
+        case 0: launch_t<RP, DO, SF, 0, PF>(a, grid, smem, s); break;
+        case 1: launch_t<RP, DO, SF, 1, PF>(a, grid, smem, s); break;
+        default: launch_t<RP, DO, SF, 2, PF>(a, grid, smem, s); break;
     }
 }
 
 template <int RP, int DO>
-void launch_do(const FusedArgs& a, int grid, size_t smem, bool sf, cudaStream_t s) {
-    if (sf) launch_sf<RP, DO, true>(a, grid, smem, s);
-    else launch_sf<RP, DO, false>(a, grid, smem, s);
+void launch_do(const FusedArgs& a, int grid, size_t smem, bool sf, bool pf, cudaStream_t s) {
+    if (sf) launch_sf<RP, DO, true, false>(a, grid, smem, s);
+    else if (pf) launch_sf<RP, DO, false, true>(a, grid, smem, s);
+    else launch_sf<RP, DO, false, false>(a, grid, smem, s);
 }
 
 template <int RP>
-void launch_rp(const FusedArgs& a, int grid, size_t smem, bool sf, cudaStream_t s) {
+void launch_rp(const FusedArgs& a, int grid, size_t smem, bool sf, bool pf, cudaStream_t s) {
     switch (a.dother) {
-        case 2: launch_do<RP, 2>(a, grid, smem, sf, s); break;
-        case 3: launch_do<RP, 3>(a, grid, smem, sf, s); break;
-        case 4: launch_do<RP, 4>(a, grid, smem, sf, s); break;
-        case 5: launch_do<RP, 5>(a, grid, smem, sf, s); break;
+        case 2: launch_do<RP, 2>(a, grid, smem, sf, pf, s); break;
+        case 3: launch_do<RP, 3>(a, grid, smem, sf, pf, s); break;
+        case 4: launch_do<RP, 4>(a, grid, smem, sf, pf, s); break;
+        case 5: launch_do<RP, 5>(a, grid, smem, sf, pf, s); break;
         default: throw_invalid("stream scatter-gather: needs 2..5 other modes");
     }
 }
+
+template <int RP>
+size_t pf_bytes() { return sizeof(double) * (size_t)Shape<RP>::NG * 2 * Shape<RP>::B * RP; }
 
 }  // namespace
 
@@ -577,12 +629,17 @@ void stream_scatter_gather(const FusedArgs& a, int grid, int64_t sf_doubles, cud
     const int ab = a.weights ? 8 : (a.mult ? 4 : 0);
     // factors through L1 when this launch's tiles leave no room for them (e.g. the RHS build)
     if (stream_smem_bytes(a.rp, a.dother, sf_doubles, ab) > SMEM_CAP) sf_doubles = 0;
-    const size_t smem = stream_smem_bytes(a.rp, a.dother, sf_doubles, ab);
+    size_t smem = stream_smem_bytes(a.rp, a.dother, sf_doubles, ab);
     const bool sf = sf_doubles > 0;
+    // factors through L1: prefetch ring for the per-observation rows when shared memory allows
+    const size_t pfb = a.rp == 16 ? pf_bytes<16>() : (a.rp == 32 ? pf_bytes<32>() : pf_bytes<64>());
+    bool pf = !sf && smem + pfb <= SMEM_CAP;
+    if (const char* e = std::getenv("CPHIFI_STREAM_PF")) pf = pf && std::atoi(e) != 0;
+    if (pf) smem += pfb;
     switch (a.rp) {
-        case 16: launch_rp<16>(a, grid, smem, sf, s); break;
-        case 32: launch_rp<32>(a, grid, smem, sf, s); break;
-        case 64: launch_rp<64>(a, grid, smem, sf, s); break;
+        case 16: launch_rp<16>(a, grid, smem, sf, pf, s); break;
+        case 32: launch_rp<32>(a, grid, smem, sf, pf, s); break;
+        case 64: launch_rp<64>(a, grid, smem, sf, pf, s); break;
         default: throw_invalid("stream scatter-gather: padded rank must be in [16, 64]");
     }
     CPHIFI_CHECK_LAUNCH();
