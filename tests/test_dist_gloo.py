@@ -73,3 +73,69 @@ def test_sharded_operator_allreduce_gloo():
         assert berr < 1e-12, (rank, berr)
         assert uid_ok
         assert tmax == float(world)
+
+
+def _als_worker(rank, world, port, out_q):
+    """The ALS terms' multi-GPU scheme (capi.cu cphifi_als_update_*): every rank holds an equal-count
+    shard of the i_k-sorted observations; the squared fit and ||v||^2 are summed over ranks
+    (all-reduce of 2 scalars), the finite-mode row Grams G_i and right-hand sides B are summed
+    (all-reduce of n x r x r and n x r) before the per-row solves — identical to the unsharded
+    quantities."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = np.random.default_rng(11)
+        shape, r, q, k = [9, 7, 6], 3, 240, 1
+        lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+        idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+        vals = g.normal(size=q)
+        fac = [g.normal(size=(n, r)) for n in shape]
+        order = np.argsort(idx[k], kind="stable")
+        idx, vals = idx[:, order], vals[order]
+        lo, hi = q * rank // world, q * (rank + 1) // world
+        z = np.ones((q, r))
+        for m in range(3):
+            if m != k:
+                z = z * fac[m][idx[m]]
+        fit = np.einsum("lr,lr->l", z, fac[k][idx[k]])
+        terms = torch.tensor([float(((vals[lo:hi] - fit[lo:hi]) ** 2).sum()), float((vals[lo:hi] ** 2).sum())],
+                             dtype=torch.float64)
+        dist.all_reduce(terms, op=dist.ReduceOp.SUM)
+        rel = float(np.sqrt(terms[0]) / np.sqrt(terms[1]))
+        rel_full = float(np.linalg.norm(vals - fit) / np.linalg.norm(vals))
+        gsh = np.zeros((shape[k], r, r))
+        bsh = np.zeros((shape[k], r))
+        for l in range(lo, hi):
+            gsh[idx[k, l]] += np.outer(z[l], z[l])
+            bsh[idx[k, l]] += vals[l] * z[l]
+        gt, bt = torch.from_numpy(gsh), torch.from_numpy(bsh)
+        dist.all_reduce(gt, op=dist.ReduceOp.SUM)
+        dist.all_reduce(bt, op=dist.ReduceOp.SUM)
+        worst = 0.0
+        for i in range(shape[k]):
+            sel = np.nonzero(idx[k] == i)[0]
+            if sel.size:
+                ref = np.linalg.lstsq(z[sel], vals[sel], rcond=None)[0]
+                ai = np.linalg.pinv(gt.numpy()[i]) @ bt.numpy()[i]
+                worst = max(worst, float(np.linalg.norm(ai - ref) / np.linalg.norm(ref)))
+        out_q.put((rank, abs(rel - rel_full) / rel_full, worst))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_als_terms_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_als_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, rel_err, row_err in res:
+        assert rel_err < 1e-13, (rank, rel_err)
+        assert row_err < 1e-9, (rank, row_err)
