@@ -274,6 +274,14 @@ int cphifi_unaligned_relative_error(cphifi_unaligned p, const double* a_k, doubl
  * while cond(Z_i) < ~1e7). */
 int cphifi_als_update_finite_unaligned(cphifi_unaligned p, double* a_out);
 
+/* update_finite_mode, aligned branch (als.hpp:139-143): A_k = B_k V_k^+ with B_k = mttkrp(T, model, k)
+ * and V_k = gram_khatri_rao(model, k), the pseudo-inverse on V_k's eigenbasis (eigenvalues below
+ * r eps sigma_max dropped, COD's rank decision).  Modes k > 0 need a 3-way, unsharded tensor with
+ * even n0 and r <= 64.  a_out: n_k x r column-major; rel_error_out (may be NULL): the relative
+ * error of the model after the update (||T||^2 - 2<A_k, B_k> + 1'(A_k'A_k o V_k)1). */
+int cphifi_als_update_finite_aligned(cphifi_tensor t, int k, int64_t r, const double* const* factors,
+                                     double* a_out, double* rel_error_out);
+
 /* Benchmark hook: `iters` aligned solves on the device-resident tensor with CUDA events per
  * phase; ms_out[0..4] = mean ms of [0] MTTKRP, [1] Gram V, [2] eig(V) (setup: wall clock of the
  * warm-up pass; the timed passes reuse it), [3] decoupled rotate/divide/rotate (each phase of a

@@ -34,7 +34,7 @@ __all__ = [
     "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
     "AlsUpdate", "update_infinite_mode_unaligned", "update_infinite_mode_aligned",
     "read_observations", "write_observations", "update_finite_mode_unaligned", "unaligned_relative_error",
-    "UnalignedAlsState", "FitIteration",
+    "UnalignedAlsState", "FitIteration", "AlignedAlsState", "update_finite_mode_aligned",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
     "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
@@ -628,7 +628,8 @@ def _device_tensor(t: DenseTensor, ctx: Context, shard=0, shards=1):
 
 
 def mttkrp(t: DenseTensor, model: KruskalModel, k: int, ctx: Context | None = None) -> np.ndarray:
-    """tensor.hpp:174-182 (k = 0, the infinite mode, on device)."""
+    """tensor.hpp:174-182 on device: k = 0 (the infinite mode) for any order; k = 1, 2 for 3-way
+    tensors with even n0 (the finite-mode updates)."""
     ctx = ctx or default_context()
     if t.order() != model.order():
         raise CphifiInvalidArgument("mttkrp: order mismatch")
@@ -829,6 +830,43 @@ class UnalignedAlsState:
         rel = self.relative_error()
         return FitIteration(rel, self.objective_from_error(rel), _time.perf_counter() - t0,
                             u.report.iterations if u.report else 0)
+
+
+def update_finite_mode_aligned(t: DenseTensor, model: KruskalModel, k: int, ctx: Context | None = None):
+    """update_finite_mode, aligned branch (als.hpp:139-143) on device: A_k = B_k V_k^+.  Returns
+    (A_k, relative error of the model after the update)."""
+    ctx = ctx or default_context()
+    dt = _device_tensor(t, ctx)
+    arrs, ptrs = _factor_array(model.factors, k)
+    a = np.zeros((t.shape()[k], model.rank()), order="F")
+    rel = ctypes.c_double()
+    call("cphifi_als_update_finite_aligned", dt.handle, k, model.rank(), ptrs, _dp(a), ctypes.byref(rel))
+    return a, rel.value
+
+
+class AlignedAlsState:
+    """AlsState (als.hpp:66-275) for aligned (dense) data with mode 0 the infinite (RKHS) mode and the
+    other modes finite, every update on device: update_infinite_mode (decoupled solve, A_0 = K W),
+    update_finite_mode (A_k = B_k V_k^+), and relative_error from the last update's MTTKRP and Gram
+    (no N-sized reconstruction)."""
+
+    def __init__(self, t: DenseTensor, mode: RkhsMode, model: KruskalModel):
+        self.t, self.mode = t, mode
+        self.model = KruskalModel([np.array(f, order="F", dtype=np.float64) for f in model.factors])
+        self.weights = None
+
+    def sweep(self) -> FitIteration:
+        import time as _time
+        t0 = _time.perf_counter()
+        u = update_infinite_mode_aligned(self.t, self.model, 0, self.mode)
+        self.weights = u.w
+        self.model.factors[0] = u.a
+        rel = u.relative_error
+        for k in range(1, self.model.order()):
+            self.model.factors[k], rel = update_finite_mode_aligned(self.t, self.model, k, self.mode.ctx)
+        nrm = u.data_norm
+        obj = (rel * nrm) ** 2 + self.mode.lambda_() * float(np.sum(self.weights * self.model.factors[0]))
+        return FitIteration(rel, obj, _time.perf_counter() - t0, 0)
 
 
 def update_infinite_mode_aligned(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode) -> AlsUpdate:

@@ -143,6 +143,8 @@ _SIGS = [
      [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_void_p,
       c_double_p]),
     ("cphifi_als_update_finite_unaligned", ctypes.c_int, [_H, c_double_p]),
+    ("cphifi_als_update_finite_aligned", ctypes.c_int,
+     [_H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, ctypes.POINTER(ctypes.c_double)]),
     ("cphifi_unaligned_relative_error", ctypes.c_int, [_H, c_double_p, c_double_p, c_double_p]),
     ("cphifi_als_update_infinite_unaligned", ctypes.c_int,
      [_H, ctypes.c_void_p, c_double_p, c_double_p, c_double_p, ctypes.c_void_p, ctypes.c_void_p]),

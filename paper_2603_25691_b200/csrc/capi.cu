@@ -2008,8 +2008,16 @@ int cphifi_tensor_destroy(cphifi_tensor t) {
 namespace {
 void mttkrp_dev(cphifi_tensor t, int k, int64_t r, const std::vector<const double*>& fptr, double* b_dev,
                 DevBuf<double>& work) {
-    if (k != 0) throw_invalid("mttkrp: only the infinite mode k = 0 is accelerated");
     cphifi_ctx ctx = t->ctx;
+    if (k != 0) {  // middle / last mode of a 3-way tensor (the finite-mode updates)
+        if (!mttkrp_k3_supported(t->d, t->shape.data(), k, r))
+            throw_invalid("mttkrp: modes k > 0 are accelerated for 3-way tensors with even n0 and r <= 64");
+        if (t->slab_lo != 0 || t->slab_hi != t->shape[1])
+            throw_invalid("mttkrp: modes k > 0 need the unsharded tensor");
+        mttkrp_mode_k3(t->data.get(), t->shape.data(), k, r, fptr[0], t->shape[0], fptr[3 - k], t->shape[3 - k], b_dev,
+                       ctx->num_sms, ctx->stream, work);
+        return;
+    }
     MttkrpArgs a;
     a.d = t->d;
     for (int m = 0; m < t->d; ++m) {
@@ -2040,11 +2048,11 @@ int cphifi_mttkrp(cphifi_tensor t, int k, int64_t r, const double* const* factor
         if (r < 1) throw_invalid("KruskalModel: rank must be positive");
         cphifi_ctx ctx = t->ctx;
         DeviceGuard dg(ctx->device);
-        DevBuf<double> fbuf, b(t->shape[0] * r), work;
+        DevBuf<double> fbuf, b(t->shape[k] * r), work;
         std::vector<const double*> fptr;
         upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
         mttkrp_dev(t, k, r, fptr, b.get(), work);
-        d2h_sync(b_out, b.get(), sizeof(double) * t->shape[0] * r, ctx->stream);
+        d2h_sync(b_out, b.get(), sizeof(double) * t->shape[k] * r, ctx->stream);
     });
 }
 
@@ -2278,6 +2286,69 @@ int cphifi_unaligned_relative_error(cphifi_unaligned p, const double* a_k, doubl
         if (dn == 0.0) throw_runtime("relative_error: zero data norm");
         *rel_error = std::sqrt(h[0]) / dn;
         if (data_norm) *data_norm = dn;
+    });
+}
+
+// ---- ALS finite-mode update, aligned (als.hpp:139-143): A_k = B_k V_k^+ (COD of V_k) ----------
+int cphifi_als_update_finite_aligned(cphifi_tensor t, int k, int64_t r, const double* const* factors, double* a_out,
+                                     double* rel_error_out) {
+    return guard([&] {
+        need(t, "tensor");
+        need(factors, "factors");
+        need(a_out, "a_out");
+        if (k < 0 || k >= t->d) throw_invalid("unfold: mode out of range");
+        cphifi_ctx ctx = t->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        const int64_t nk = t->shape[k], nr = nk * r;
+        DevBuf<double> fbuf, b(nr), v(r * r), uv(r * r), sv(r), t1(nr), a(nr), g(r * r), scal(4), part(1024 + 80), work;
+        std::vector<const double*> fptr;
+        upload_factors_cm(ctx, t->d, t->shape.data(), k, r, factors, fbuf, fptr);
+        mttkrp_dev(t, k, r, fptr, b.get(), work);                       // B_k = T_(k) Z_k
+        gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), s);  // V_k
+        device_sym_eig(ctx, v.get(), r, uv.get(), sv.get());
+        // V^+ on its eigenbasis: eigenvalues below r eps sigma_max dropped (COD's rank decision)
+        invert_spectrum(sv.get(), r, s);
+        GemmArgs h;  // t1 = (B U_V) diag(1 / sigma)
+        h.m = nk; h.n = r; h.k = r;
+        h.a = b.get(); h.a_rs = 1; h.a_cs = nk;
+        h.b = uv.get(); h.b_rs = 1; h.b_cs = r;
+        h.c = t1.get(); h.c_rs = 1; h.c_cs = nk;
+        gemm(h, ctx->num_sms, s);
+        scale_columns(t1.get(), nk, r, sv.get(), s);
+        GemmArgs o;  // A = t1 U_V'
+        o.m = nk; o.n = r; o.k = r;
+        o.a = t1.get(); o.a_rs = 1; o.a_cs = nk;
+        o.b = uv.get(); o.b_rs = r; o.b_cs = 1;
+        o.c = a.get(); o.c_rs = 1; o.c_cs = nk;
+        gemm(o, ctx->num_sms, s);
+        if (rel_error_out) {  // relative error of the model after this update (Gram identity)
+            GemmArgs gg;
+            gg.m = r; gg.n = r; gg.k = nk;
+            gg.a = a.get(); gg.a_rs = nk; gg.a_cs = 1;
+            gg.b = a.get(); gg.b_rs = 1; gg.b_cs = nk;
+            gg.c = g.get(); gg.c_rs = 1; gg.c_cs = r;
+            gemm(gg, ctx->num_sms, s);
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            dot_to(a.get(), b.get(), nr, part.get(), scal.get(), s);
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            dot_to(g.get(), v.get(), r * r, part.get(), scal.get() + 1, s);
+            if (!t->have_norm) {
+                int64_t cnt = t->shape[0] * (t->slab_hi - t->slab_lo);
+                for (int m = 2; m < t->d; ++m) cnt *= t->shape[m];
+                t->norm2.alloc(1);
+                sq_norm(t->data.get(), cnt, part.get(), 1024, t->norm2.get(), s);
+                allreduce(ctx, t->norm2.get(), 1);
+                t->have_norm = true;
+            }
+            CPHIFI_CUDA(cudaMemcpyAsync(scal.get() + 2, t->norm2.get(), sizeof(double), cudaMemcpyDeviceToDevice, s));
+            double hsc[3];
+            d2h_sync(hsc, scal.get(), sizeof(double) * 3, s);
+            const double tn = std::sqrt(hsc[2]);
+            if (tn == 0.0) throw_runtime("relative_error: zero data norm");
+            *rel_error_out = std::sqrt(std::max(hsc[2] - 2.0 * hsc[0] + hsc[1], 0.0)) / tn;
+        }
+        d2h_sync(a_out, a.get(), sizeof(double) * nr, s);
     });
 }
 

@@ -268,8 +268,9 @@ __global__ void kr_outer_kernel(const MttkrpArgs a, int64_t n_outer, double* __r
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_outer * a.r) return;
     const int64_t o = e / a.r, j = e % a.r;
+    double* dst = wout + o * a.ldw + j;
     if (a.d == 2) {
-        wout[e] = 1.0;
+        *dst = 1.0;
         return;
     }
     int64_t sub[8];
@@ -280,7 +281,7 @@ __global__ void kr_outer_kernel(const MttkrpArgs a, int64_t n_outer, double* __r
     }
     double w = a.fac[a.d - 1][sub[a.d - 1] + a.ld[a.d - 1] * j];
     for (int m = a.d - 2; m >= 2; --m) w *= a.fac[m][sub[m] + a.ld[m] * j];
-    wout[e] = w;
+    *dst = w;
 }
 
 template <int BN>
@@ -319,7 +320,7 @@ __device__ __forceinline__ void load_tile_mttkrp(GemmSmem<BN, BMM, STM>& sm, dou
     }
     if (threadIdx.x < BN) {
         const int64_t j = j0 + threadIdx.x;
-        cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.r + j : wout, j < a.r);
+        cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.ldw + j : wout, j < a.r);
     }
 }
 
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(NTV, 1) mttkrp_v2_kernel(const MttkrpArgs a, i
         }
         if (threadIdx.x < BN) {
             const int64_t j = j0 + threadIdx.x;
-            cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.r + j : wout, j < a.r);
+            cp_async8(ws + st * BN + threadIdx.x, j < a.r ? wout + outer * a.ldw + j : wout, j < a.r);
         }
     };
 
@@ -549,21 +550,29 @@ constexpr int AP3 = BMM + 4;          // T box rows = smem pitch
 constexpr int BKP3 = BK + 4;          // A_1 box rows = smem pitch of the transposed B tile
 // B tile: [j][k] (pitch BKP3) from a column-major B (the MTTKRP's A_1, a GEMM's X), or [k][j]
 // (pitch BN + 4, the 4 extra columns read past the tile or as zero) from a row-major B (BROW)
-template <int BN>
+// A tile: AM = 0 [k][i] (pitch AP3) from a column-major A (the MTTKRP's unfolding for mode 0, a
+// GEMM's A); AM = 1 / 2 [i][k] (pitch BK + 4) — the transposed unfoldings of the middle / last
+// mode of a 3-way column-major tensor, through a 3-D / 2-D tensor map — with one stage fewer.
+template <int BN, int AM = 0>
 struct Mttkrp3Smem {
+    static constexpr int NST = AM == 0 ? ST3 : ST3 - 1;
+    static constexpr int ASZ = AM == 0 ? BK * AP3 : BMM * (BK + 4);
     static constexpr int BSZ = BN * BKP3 > BK * (BN + 4) ? BN * BKP3 : BK * (BN + 4);
-    double a[ST3][BK][AP3];
-    double bt[ST3][BSZ];
-    double w[ST3][BN];  // the tile's Wout row (its `outer` index)
-    uint64_t full[ST3], empty[ST3];
+    double a[NST][ASZ];
+    double bt[NST][BSZ];
+    double w[NST][BN];  // the tile's Wout row (its `outer` index)
+    uint64_t full[NST], empty[NST];
 };
-template <int BN, int WR, int WC, bool BROW>
+template <int BN, int WR, int WC, bool BROW, int AM = 0>
 __global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(const MttkrpArgs a, const __grid_constant__ CUtensorMap tm_t,
                                                                 const __grid_constant__ CUtensorMap tm_a1, int64_t chunks,
                                                                 int64_t ktiles, const double* __restrict__ wout,
                                                                 double* __restrict__ work) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Mttkrp3Smem<BN>& sm = *reinterpret_cast<Mttkrp3Smem<BN>*>(smem_raw);
+    using SMT = Mttkrp3Smem<BN, AM>;
+    constexpr int ST3 = SMT::NST;
+    SMT& sm = *reinterpret_cast<SMT*>(smem_raw);
+    auto aidx = [](int k, int i) { return AM == 0 ? k * AP3 + i : i * (BK + 4) + k; };
     using L = V3<BN, WR, WC>;
     constexpr int NC3 = L::NC, MF = L::MF, NF = L::NF, RG = L::RG, CG = L::CG, KG = L::KG;
     const int P = gridDim.y, split = blockIdx.y;
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(c
     if (warp == NC3 / 32) {  // ---- producer warp (one lane) ----
         if (lane == 0) {
             const unsigned wb = (unsigned)((bcols * 8 + 15) & ~15);  // Wout row (2 spare doubles past the end)
-            const unsigned bytes = (unsigned)(sizeof(double) * (BK * AP3 + (BROW ? BK * (BN + 4) : BN * BKP3))) + wb;
+            const unsigned bytes = (unsigned)(sizeof(double) * (SMT::ASZ + (BROW ? BK * (BN + 4) : BN * BKP3))) + wb;
             // L2 prefetch runs l2_ahead tiles in front of the ring: the shared-memory stages then
             // fill from L2, and the loaded-HBM latency hides behind the prefetch distance
             const int pf = a.l2_ahead;
@@ -622,10 +631,12 @@ __global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(c
                     continue;
                 }
                 tma::mbar_expect_tx(&sm.full[st], bytes);
-                tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
+                if constexpr (AM == 0) tma::tensor_g2s_2d(&sm.a[st][0], &tm_t, (int)i0, (int)(c1 + n1 * outer), &sm.full[st]);
+                else if constexpr (AM == 2) tma::tensor_g2s_2d(&sm.a[st][0], &tm_t, (int)(c1 + n1 * outer), (int)i0, &sm.full[st]);
+                else tma::tensor_g2s_3d(&sm.a[st][0], &tm_t, (int)c1, (int)i0, (int)outer, &sm.full[st]);
                 if constexpr (BROW) tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)j0, (int)(c1 + a.off1), &sm.full[st]);
                 else tma::tensor_g2s_2d(&sm.bt[st][0], &tm_a1, (int)(c1 + a.off1), (int)j0, &sm.full[st]);
-                tma::bulk_g2s(&sm.w[st][0], wout + outer * a.r + j0, wb, &sm.full[st]);
+                tma::bulk_g2s(&sm.w[st][0], wout + outer * a.ldw + j0, wb, &sm.full[st]);
             }
         }
     } else {  // ---- consumer warps ----
@@ -669,7 +680,7 @@ __global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(c
                         const int kr = (kg * (BK / 4 / KG) + k2) * 4 + kq;
                         double af[MF], bf[NF];
 #pragma unroll
-                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
+                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][aidx(kr, rg * WR + mf * 8 + g)];
 #pragma unroll
                         for (int nf = 0; nf < NF; ++nf) bf[nf] = sm.bt[st][bidx(kr, cg * WC + nf * 8 + g)];
 #pragma unroll
@@ -683,7 +694,7 @@ __global__ void __launch_bounds__(V3<BN, WR, WC>::NC + 32, 1) mttkrp_v3_kernel(c
                         const int kr = (kg * (BK / 4 / KG) + k2) * 4 + kq;
                         double af[MF], bf[NF];
 #pragma unroll
-                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][kr][rg * WR + mf * 8 + g];
+                        for (int mf = 0; mf < MF; ++mf) af[mf] = sm.a[st][aidx(kr, rg * WR + mf * 8 + g)];
 #pragma unroll
                         for (int nf = 0; nf < NF; ++nf) bf[nf] = kr < cnt ? sm.bt[st][bidx(kr, cg * WC + nf * 8 + g)] : 0.0;
 #pragma unroll
@@ -734,22 +745,22 @@ __global__ void reduce_splits_kernel(const double* __restrict__ work, int P, int
     }
 }
 
-template <int BN, int WR, int WC, bool BROW = false>
+template <int BN, int WR, int WC, bool BROW = false, int AM = 0>
 void launch_v3(const MttkrpArgs& ap, const CUtensorMap& tm_t, const CUtensorMap& tm_a1, int mt, int64_t P, int nt,
                int64_t chunks, int64_t ktiles, const double* wout, double* work, cudaStream_t s) {
-    const size_t smem3 = sizeof(Mttkrp3Smem<BN>);
+    const size_t smem3 = sizeof(Mttkrp3Smem<BN, AM>);
     static bool attr3 = false;
     if (!attr3) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, WC, BROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, WC, BROW, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem3));
         attr3 = true;
     }
-    mttkrp_v3_kernel<BN, WR, WC, BROW><<<dim3(mt, (unsigned)P, nt), V3<BN, WR, WC>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
+    mttkrp_v3_kernel<BN, WR, WC, BROW, AM><<<dim3(mt, (unsigned)P, nt), V3<BN, WR, WC>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
                                                                                            ktiles, wout, work);
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
         cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR, WC, BROW>);
+        cudaFuncGetAttributes(&fa, mttkrp_v3_kernel<BN, WR, WC, BROW, AM>);
         throw Error(CPHIFI_CUDA_ERROR, std::string("mttkrp_v3 launch: ") + cudaGetErrorString(le) + " regs " +
                                            std::to_string(fa.numRegs) + " maxthreads " + std::to_string(fa.maxThreadsPerBlock));
     }
@@ -768,10 +779,12 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
     int64_t P = std::max<int64_t>(1, (int64_t)num_sms / (mt * nt));
     P = std::max<int64_t>(1, std::min<int64_t>(P, ktiles));
     P = std::min<int64_t>(P, 1024);
-    const size_t need = (size_t)P * n0 * a.r + (size_t)n_outer * a.r + 2;
+    MttkrpArgs aw = a;
+    aw.ldw = (a.r + 1) & ~1LL;  // 16-byte Wout rows (the v3 producer bulk-copies them)
+    const size_t need = (size_t)P * n0 * a.r + (size_t)n_outer * aw.ldw + 2;
     if (work.n < need) work.alloc(need);
     double* wout = work.get() + (size_t)P * n0 * a.r;
-    kr_outer_kernel<<<(unsigned)((n_outer * a.r + 255) / 256), 256, 0, s>>>(a, n_outer, wout);
+    kr_outer_kernel<<<(unsigned)((n_outer * a.r + 255) / 256), 256, 0, s>>>(aw, n_outer, wout);
     CPHIFI_CHECK_LAUNCH();
     const size_t smem = sizeof(GemmSmem<BN, BMM, STM>) + sizeof(double) * STM * BN;
     static bool attr_set = false;
@@ -791,7 +804,7 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
               encode_tmap_2d_f64(&tm_t, a.t, (uint64_t)n0, (uint64_t)ncols, (uint64_t)n0, BMM + 4, BK) &&
               encode_tmap_2d_f64(&tm_a1, a.fac[1], (uint64_t)a.ld[1], (uint64_t)a.r, (uint64_t)a.ld[1], BK + 4, BN);
     if (const char* e = std::getenv("CPHIFI_MTTKRP_V3")) v3 = v3 && std::atoi(e) != 0;
-    MttkrpArgs ap = a;
+    MttkrpArgs ap = aw;
     if (const char* e = std::getenv("CPHIFI_MTTKRP_PROBE")) ap.probe = std::atoi(e);
     if (const char* e = std::getenv("CPHIFI_MTTKRP_L2AHEAD")) ap.l2_ahead = std::atoi(e);
     if constexpr (BN <= 32) {
@@ -812,11 +825,11 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
                                                  (int)smem));
                 attr2 = true;
             }
-            mttkrp_v2_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTV, smem, s>>>(a, chunks, ktiles, wout, work.get());
+            mttkrp_v2_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTV, smem, s>>>(aw, chunks, ktiles, wout, work.get());
         }
     }
     if (!v2)
-        mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTM, smem, s>>>(a, chunks, ktiles, wout, work.get());
+        mttkrp_dmma_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTM, smem, s>>>(aw, chunks, ktiles, wout, work.get());
     CPHIFI_CHECK_LAUNCH();
     const int64_t cnt = n0 * a.r;
     reduce_splits_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(
@@ -987,6 +1000,29 @@ bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uin
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool encode_tmap_3d_f64(CUtensorMap* map, const double* base, uint64_t n0, uint64_t n1, uint64_t n2, uint32_t b0,
+                        uint32_t b1, uint32_t b2) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<Fn>(p);
+    }();
+    if (!fn || reinterpret_cast<uintptr_t>(base) % 16 != 0 || (n0 * sizeof(double)) % 16 != 0) return false;
+    const cuuint64_t dims[3] = {n0, n1, n2};
+    const cuuint64_t strides[2] = {n0 * sizeof(double), n0 * n1 * sizeof(double)};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_tflops) {
     DevBuf<double> sink(1);
     cudaEvent_t e0, e1;
@@ -1065,6 +1101,7 @@ void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
     a.fac[1] = g.b;
     a.ld[1] = brow ? g.b_rs : g.b_cs;
     a.off1 = 0;
+    a.ldw = (g.n + 1) & ~1LL;
     kr_outer_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(a, 1, wout);  // Wout = 1
     CPHIFI_CHECK_LAUNCH();
     CUtensorMap tm_a, tm_b;
@@ -1097,6 +1134,66 @@ void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     else if (np <= 16) launch_gemm<16>(g, num_sms, s);
     else if (np <= 32) launch_gemm<32>(g, num_sms, s);
     else launch_gemm<64>(g, num_sms, s);
+}
+
+// ---- MTTKRP for the middle (k = 1) / last (k = 2) mode of a 3-way column-major tensor --------
+// B_k = T_(k) Z_k: the contraction runs over (i0, outer) with outer = the remaining mode, in tiles
+// of 32 consecutive i0 of one outer: the B tile is an A_0 block, the tile's Khatri-Rao row the
+// remaining factor's row `outer` (tensor.hpp:158-182: Z_k = A_other (x) A_0, A_0 fastest).  The T
+// tile is the transposed unfolding block through a 3-D (k = 1) or 2-D (k = 2) tensor map.
+__global__ void rows_of_kernel(const double* __restrict__ f, int64_t ld, int64_t nrows, int64_t r, int64_t ldw,
+                               double* __restrict__ wout) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < nrows * r) wout[(e / r) * ldw + e % r] = f[e / r + ld * (e % r)];  // Wout(o, j) = F(o, j)
+}
+
+template <int BN>
+void mttkrp_k3_t(const double* t, const int64_t* shape, int k, int64_t r, const double* a0, int64_t ld0,
+                 const double* aoth, int64_t ldo, double* b_out, int num_sms, cudaStream_t s, DevBuf<double>& work) {
+    const int64_t n0 = shape[0], nk = shape[k], nout = shape[3 - k];
+    const int64_t chunks = (n0 + BK - 1) / BK, ktiles = chunks * nout;
+    const int mt = (int)((nk + BMM - 1) / BMM), nt = (int)((r + BN - 1) / BN);
+    int64_t P = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms / (mt * nt), ktiles));
+    const size_t need = (size_t)P * nk * r + (size_t)nout * ((r + 1) & ~1LL) + 2;
+    if (work.n < need) work.alloc(need);
+    double* wout = work.get() + (size_t)P * nk * r;
+    rows_of_kernel<<<(unsigned)((nout * r + 255) / 256), 256, 0, s>>>(aoth, ldo, nout, r, (r + 1) & ~1LL, wout);
+    CPHIFI_CHECK_LAUNCH();
+    CUtensorMap tm_t, tm_b;
+    bool ok = encode_tmap_2d_f64(&tm_b, a0, (uint64_t)ld0, (uint64_t)r, (uint64_t)ld0, BK + 4, BN);
+    if (k == 1) ok = ok && encode_tmap_3d_f64(&tm_t, t, (uint64_t)n0, (uint64_t)shape[1], (uint64_t)shape[2], BK + 4, BMM, 1);
+    else ok = ok && encode_tmap_2d_f64(&tm_t, t, (uint64_t)(n0 * shape[1]), (uint64_t)shape[2], (uint64_t)(n0 * shape[1]),
+                                       BK + 4, BMM);
+    if (!ok) throw Error(CPHIFI_CUDA_ERROR, "mttkrp: tensor map encoding failed");
+    MttkrpArgs a;
+    a.d = 3;
+    a.shape[0] = nk;   // output rows
+    a.shape[1] = n0;   // chunked contraction extent
+    a.r = r;
+    a.t = t;
+    a.fac[1] = a0;
+    a.ld[1] = ld0;
+    a.off1 = 0;
+    a.ldw = (r + 1) & ~1LL;
+    constexpr int WC = BN >= 16 ? 16 : BN;
+    if (k == 1) launch_v3<BN, 32, WC, false, 1>(a, tm_t, tm_b, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+    else launch_v3<BN, 32, WC, false, 2>(a, tm_t, tm_b, mt, P, nt, chunks, ktiles, wout, work.get(), s);
+    const int64_t cnt = nk * r;
+    reduce_splits_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(work.get(), (int)P,
+                                                                                                    cnt, b_out);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+bool mttkrp_k3_supported(int d, const int64_t* shape, int k, int64_t r) {
+    return d == 3 && (k == 1 || k == 2) && shape[0] % 2 == 0 && r <= 64 && r >= 1 &&
+           shape[0] * shape[1] < (1LL << 31) && shape[1] < (1LL << 31) && shape[2] < (1LL << 31);
+}
+
+void mttkrp_mode_k3(const double* t, const int64_t* shape, int k, int64_t r, const double* a0, int64_t ld0,
+                    const double* aoth, int64_t ldo, double* b_out, int num_sms, cudaStream_t s, DevBuf<double>& work) {
+    if (r <= 8) mttkrp_k3_t<8>(t, shape, k, r, a0, ld0, aoth, ldo, b_out, num_sms, s, work);
+    else if (r <= 16) mttkrp_k3_t<16>(t, shape, k, r, a0, ld0, aoth, ldo, b_out, num_sms, s, work);
+    else mttkrp_k3_t<32>(t, shape, k, r, a0, ld0, aoth, ldo, b_out, num_sms, s, work);
 }
 
 void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work) {

@@ -364,6 +364,26 @@ void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaSt
     CPHIFI_CHECK_LAUNCH();
 }
 
+// sigma_j -> 1 / sigma_j, or 0 below r eps sigma_max (a pseudo-inverse on the eigenbasis)
+__global__ void invert_spectrum_kernel(double* sv, int64_t r) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < r; ++j) mx = fmax(mx, sv[j]);
+    const double tau = mx * (double)r * 2.220446049250313e-16;
+    for (int64_t j = threadIdx.x; j < r; j += blockDim.x) sv[j] = (sv[j] > tau && mx > 0.0) ? 1.0 / sv[j] : 0.0;
+}
+void invert_spectrum(double* sv, int64_t r, cudaStream_t s) {
+    invert_spectrum_kernel<<<1, 64, 0, s>>>(sv, r);
+    CPHIFI_CHECK_LAUNCH();
+}
+__global__ void scale_columns_kernel(double* a, int64_t m, int64_t r, const double* d) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * r; e += (int64_t)gridDim.x * blockDim.x)
+        a[e] *= d[e / m];
+}
+void scale_columns(double* a, int64_t m, int64_t r, const double* d, cudaStream_t s) {
+    scale_columns_kernel<<<(unsigned)std::min<int64_t>((m * r + 255) / 256, 2048), 256, 0, s>>>(a, m, r, d);
+    CPHIFI_CHECK_LAUNCH();
+}
+
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {
     const unsigned g = (unsigned)((n + 31) / 32);
     transpose_kernel<<<dim3(g, g), dim3(32, 8), 0, s>>>(a, n, at);

@@ -43,11 +43,16 @@ struct MttkrpArgs {
     const double* fac[8] = {nullptr};  // device column-major, fac[m] has ld = full n_m
     int64_t ld[8] = {0};
     double* b = nullptr;      // n0 x r column-major output
+    int64_t ldw = 0;          // row stride of the Khatri-Rao outer rows Wout (r rounded up to even: 16-byte rows)
     int probe = 0;            // profiling only (CPHIFI_MTTKRP_PROBE, v3): 1 = stream T without the DMMA work,
                               // 2 = DMMA work on stale stages without the stream, 3 = as 2 without the B scaling
     int l2_ahead = 0;         // v3: tiles of T prefetched into L2 ahead of the ring (CPHIFI_MTTKRP_L2AHEAD)
 };
 void mttkrp_mode0(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<double>& work);
+// MTTKRP for mode k in {1, 2} of a 3-way column-major tensor (even n0): B_k = T_(k) (A_other (x) A_0)
+bool mttkrp_k3_supported(int d, const int64_t* shape, int k, int64_t r);
+void mttkrp_mode_k3(const double* t, const int64_t* shape, int k, int64_t r, const double* a0, int64_t ld0,
+                    const double* aoth, int64_t ldo, double* b_out, int num_sms, cudaStream_t s, DevBuf<double>& work);
 
 // FP64 peak probes (DFMA / DMMA loops, TFLOP/s) for the roofline denominators
 void fp64_peaks(int num_sms, cudaStream_t s, double* dfma_tflops, double* dmma_tflops);
@@ -90,6 +95,10 @@ bool sandwich_supported(int64_t n, int64_t r);
 int64_t sandwich_rp(int64_t r);
 void sandwich(SandArgs a, int num_sms, cudaStream_t s);
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
+// sigma -> pseudo-inverse spectrum (1 / sigma above r eps sigma_max, else 0), in place
+void invert_spectrum(double* sv, int64_t r, cudaStream_t s);
+// a (m x r column-major) <- a diag(d)
+void scale_columns(double* a, int64_t m, int64_t r, const double* d, cudaStream_t s);
 // out = a diag(d)  (n x n column-major)
 void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaStream_t s);
 

@@ -45,6 +45,14 @@ __device__ __forceinline__ void tensor_g2s_2d(void* dst, const CUtensorMap* map,
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// 3-D tensor-map copy of the box at (c0 innermost, c1, c2)
+__device__ __forceinline__ void tensor_g2s_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 // L2 prefetch of a 2-D tensor-map box (no shared memory, no completion)
 __device__ __forceinline__ void tensor_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
@@ -60,5 +68,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // layout violates the TMA constraints (16-byte aligned base and stride).
 bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
                         uint32_t box1);
+// 3-D fp64 tensor map over a column-major n0 x n1 x n2 array (strides n0, n0 n1), box b0 x b1 x b2
+bool encode_tmap_3d_f64(CUtensorMap* map, const double* base, uint64_t n0, uint64_t n1, uint64_t n2, uint32_t b0,
+                        uint32_t b1, uint32_t b2);
 
 }  // namespace cphifi

@@ -197,3 +197,55 @@ def test_unaligned_als_sweeps_vs_reference(cp):
             assert ri.rel(st.model.factors[k], fac[k]) < 1e-6, (sweep, k)
     # block coordinate descent: the objective does not increase (up to the inner PCG tolerance)
     assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:])), objs
+
+
+@pytest.mark.parametrize("shape,r", [([64, 30, 20], 5), ([200, 100, 100], 10), ([128, 7, 9], 32), ([130, 260, 3], 16)])
+def test_mttkrp_middle_and_last_modes(cp, shape, r):
+    """tensor.hpp:174-182 for k = 1, 2 (transposed-unfolding TMA tiles) vs the oracle."""
+    g = cp.Mt19937_64(sum(shape) * r)
+    flat = ri.random_tensor(shape, g)
+    factors = ri.random_model(shape, r, g)
+    t = cp.DenseTensor(shape, flat)
+    for k in (1, 2):
+        b = cp.mttkrp(t, cp.KruskalModel(factors), k)
+        bo = orc.mttkrp(flat.reshape(shape, order="F"), factors, k)
+        assert ri.rel(b, bo) < 1e-12, (shape, k)
+
+
+def test_aligned_finite_update_and_sweeps(cp):
+    """update_finite_mode (aligned, als.hpp:139-143: A_k = B_k V_k^+) and three whole aligned sweeps
+    (mode 0 infinite, decoupled) on config 0 vs a numpy restatement with the same eig(K)."""
+    from paper_2603_25691_b200 import configs
+    c = configs.config0()
+    n, r = c.shape[0], c.r
+    mode = cp.RkhsMode(c.points, c.ell, c.lam)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    tt = c.tensor.reshape(c.shape, order="F")
+    t = cp.DenseTensor(c.shape, c.tensor)
+    g = np.random.default_rng(3)
+    init = [np.zeros((n, r))] + [g.normal(size=(s, r)) for s in c.shape[1:]]
+    # one finite update alone
+    a1, rel1 = cp.update_finite_mode_aligned(t, cp.KruskalModel(init), 1)
+    b1 = orc.mttkrp(tt, init, 1)
+    v1 = orc.gram_khatri_rao(init, 1)
+    assert ri.rel(a1, b1 @ np.linalg.pinv(v1)) < 1e-10
+    st = cp.AlignedAlsState(t, mode, cp.KruskalModel(init))
+    fac = [f.copy() for f in init]
+    objs = []
+    for sweep in range(3):
+        it = st.sweep()
+        objs.append(it.objective)
+        b0 = orc.mttkrp(tt, fac, 0)
+        ev = orc.sym_eig(orc.gram_khatri_rao(fac, 0))
+        w = orc.solve_aligned_decoupled(b0, ek, ev, c.lam)
+        fac[0] = kern @ w
+        for k in (1, 2):
+            fac[k] = orc.mttkrp(tt, fac, k) @ np.linalg.pinv(orc.gram_khatri_rao(fac, k))
+        full = np.einsum("ir,jr,kr->ijk", fac[0], fac[1], fac[2])
+        rel = np.linalg.norm(tt - full) / np.linalg.norm(tt)
+        assert abs(it.rel_error - rel) <= 1e-8 * rel, (sweep, it.rel_error, rel)
+        for k in range(3):
+            assert ri.rel(st.model.factors[k], fac[k]) < 1e-6, (sweep, k)
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:])), objs

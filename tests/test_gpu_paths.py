@@ -186,3 +186,17 @@ def test_pcg_eigenbasis_matches_original_basis(cp, monkeypatch, op):
         rep = cp.SolveReport()
         cp.solve_unaligned_pcg(p, cfg, rep, warm_start=out["0"][0])
         assert rep.iterations <= 1, rot
+
+
+def test_mttkrp_v3_odd_rank_many_outer(cp, monkeypatch):
+    """Odd r with several `outer` rows: the Khatri-Rao rows are 16-byte padded for the bulk copy."""
+    g = cp.Mt19937_64(77)
+    shape, r = [64, 40, 7], 5
+    flat = ri.random_tensor(shape, g)
+    factors = ri.random_model(shape, r, g)
+    t = cp.DenseTensor(shape, flat)
+    bo = orc.mttkrp(flat.reshape(shape, order="F"), factors, 0)
+    for v1, v3 in (("1", "0"), ("0", "0"), ("0", "1")):
+        monkeypatch.setenv("CPHIFI_MTTKRP_V1", v1)
+        monkeypatch.setenv("CPHIFI_MTTKRP_V3", v3)
+        assert ri.rel(cp.mttkrp(t, cp.KruskalModel(factors), 0), bo) < 1e-12, (v1, v3)
