@@ -288,7 +288,9 @@ __global__ void gram_apply_kernel(const double* __restrict__ g, const double* __
 template <int RP, int DO>
 void launch_dmma_do(const GramArgs& a, int grid, cudaStream_t s) {
     const size_t zbytes = sizeof(double) * 2 * GB * (RP + 4);
-    const bool sf = zbytes + sizeof(double) * a.fac_total <= 200 * 1024;
+    size_t sf_cap = 200 * 1024;  // factors staged in shared memory below this (CPHIFI_GRAM_SF_KB)
+    if (const char* e = std::getenv("CPHIFI_GRAM_SF_KB")) sf_cap = (size_t)std::atoi(e) * 1024;
+    const bool sf = zbytes + sizeof(double) * a.fac_total <= sf_cap;
     const size_t smem = zbytes + (sf ? sizeof(double) * a.fac_total : 0);
     auto kern = sf ? gram_build_dmma_kernel<RP, DO, true> : gram_build_dmma_kernel<RP, DO, false>;
     CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -20,7 +20,10 @@ for which in sys.argv[1:] or ["config3"]:
     obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), cfg.q, keepalive=(idx, vals),
                                 coalesce=cfg.coalesce)
     model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
-    x = np.random.default_rng(0).normal(size=n * r)
+    from paper_2603_25691_b200 import _capi
+    lib = _capi.load()
+    xd = torch.randn(n * r, dtype=torch.float64, device="cuda")
+    yd = torch.empty_like(xd)
     ys = {}
     for dm in ("0", "1"):
         os.environ["CPHIFI_GRAM_DMMA"] = dm
@@ -28,9 +31,12 @@ for which in sys.argv[1:] or ["config3"]:
         p.set_operator("gram")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ys[dm] = cp.unaligned_matvec(p, x)  # builds G
+        _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, xd.data_ptr(), yd.data_ptr()))  # builds G
+        torch.cuda.synchronize()
         t1 = time.perf_counter()
-        cp.unaligned_matvec(p, x)
+        ys[dm] = yd.cpu().numpy()
+        _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, xd.data_ptr(), yd.data_ptr()))
+        torch.cuda.synchronize()
         t2 = time.perf_counter()
         print(f"{which} dmma={dm}: build+apply {1e3 * (t1 - t0):.1f} ms, apply {1e3 * (t2 - t1):.2f} ms")
         del p
