@@ -133,6 +133,17 @@ const double* mode_um(cphifi_mode m) {
     return m->um.get();
 }
 
+const double* mode_umt(cphifi_mode m) {
+    const double* ut = mode_ut(m);
+    std::lock_guard<std::mutex> lk(m->mu_lock);
+    if (!m->have_umt) {
+        m->umt.alloc(m->n * m->n);
+        scale_rows(ut, m->n, m->mu.get(), m->umt.get(), m->ctx->stream);
+        m->have_umt = true;
+    }
+    return m->umt.get();
+}
+
 // Per-thread pinned, device-mapped status word for kernels that report a data error (zero
 // decoupled denominator): no allocation and no extra synchronisation per call; the caller reads
 // it after the synchronisation it performs anyway.
@@ -496,7 +507,7 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
 // GEMMs per iteration instead of four (K X, K Yhat, U'R, U Z).  K differs from its clamped
 // reconstruction by the clamped negative eigenvalues (rounding-level for the configs' kernels).
 bool pcg_eigbasis(cphifi_unaligned p) {
-    bool on = !p->small_n;
+    bool on = true;
     if (const char* e = std::getenv("CPHIFI_PCG_EIGBASIS")) on = std::atoi(e) != 0;
     return on && p->mode;
 }
@@ -505,6 +516,24 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
     need_mode(p);
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
+    if (p->small_n) {  // the fused kernel with the eigenbasis columns and epilogue
+        const bool multi = is_multi(p);
+        const double* gr = p->op == 1 ? p->gram.get() : nullptr;
+        FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
+        a.kmat = mode_umt(p->mode);
+        a.kmat_c2 = p->mode->u.get();
+        a.mu_rot = p->mode->mu.get();
+        a.x = xt;
+        a.y = yt;
+        a.gram = gr;
+        launch_fused(p, a);
+        if (multi) {
+            allreduce_yhat(p);
+            a.phases = matvec_phases(p, multi, 1);
+            launch_fused(p, a);
+        }
+        return;
+    }
     GemmArgs g;  // Xhat = U diag(mu) x~  -> row-major padded copy for the gather
     g.m = n; g.n = r; g.k = n;
     g.a = mode_um(p->mode); g.a_rs = 1; g.a_cs = n;
@@ -528,6 +557,10 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
 void precond_rot(cphifi_unaligned p, const double* rt, double* zt) {
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
+    if (r <= 64) {  // one launch: r x r work per row
+        precond_rot_small(rt, p->uv.get(), p->dmat.get(), n, r, zt, ctx->stream);
+        return;
+    }
     GemmArgs h;  // t2 = (r~ U_V) .* D
     h.m = n; h.n = r; h.k = r;
     h.a = rt; h.a_rs = 1; h.a_cs = n;
@@ -958,6 +991,7 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         mode->mu.alloc(n);
         mode->have_ut = false;
         mode->have_um = false;
+        mode->have_umt = false;
         h2d(mode->u.get(), u, sizeof(double) * n * n, mode->ctx->stream);
         h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
         clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);

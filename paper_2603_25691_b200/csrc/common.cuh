@@ -108,6 +108,8 @@ struct cphifi_mode_s {
     bool have_ut = false;
     cphifi::DevBuf<double> um;      // U diag(mu) (eigenbasis PCG: K X = U diag(mu) U'X), lazily
     bool have_um = false;
+    cphifi::DevBuf<double> umt;     // diag(mu) U' (the fused kernel's Xhat columns in the eigenbasis)
+    bool have_umt = false;
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
 
     const int c = blockIdx.x, C = gridDim.x;
     const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
+    const double* kc2 = a.kmat_c2 ? a.kmat_c2 : a.kmat;      // PH_C2 columns (U in the eigenbasis)
     const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
     // ---- entry, before any dependent load: one thread issues the bulk copies that need no plan
     // data (even n: 16-byte aligned columns), so their HBM latency overlaps the plan reads
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
             for (int j = 0; j < (int)a.r; ++j) tma::bulk_g2s(xs + ldx * j, a.x + a.n * j, colb, &s_fbar);
             if (a.phases & PH_C2)
                 for (int64_t i = i0; i < i1; ++i)
-                    tma::bulk_g2s(kcs + (MAXLOC + i - i0) * a.n, a.kmat + i * a.n, colb, &s_fbar);
+                    tma::bulk_g2s(kcs + (MAXLOC + i - i0) * a.n, kc2 + i * a.n, colb, &s_fbar);
         }
     }
     const int g = threadIdx.x / G, glane = threadIdx.x % G, jb = glane * VPL;
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
             if (a.phases & PH_C2)
                 for (int64_t i = i0; i < i1; ++i)
                     for (int64_t k = threadIdx.x; k < a.n; k += FT)
-                        cp_async8(kcs + (MAXLOC + i - i0) * a.n + k, a.kmat + i * a.n + k);
+                        cp_async8(kcs + (MAXLOC + i - i0) * a.n + k, kc2 + i * a.n + k);
         }
         for (int rr = 0; rr < nal; ++rr)
             for (int64_t k = threadIdx.x; k < a.n; k += FT) cp_async8(kcs + rr * a.n + k, a.kmat + (first_row + rr) * a.n + k);
@@ -490,7 +491,17 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
         if (tma_any) tma::mbar_wait(&s_fbar, 0);
         __syncthreads();
         for (int64_t i = i0; i < i1; ++i) {
-            const double* kc = pf ? kcs + (MAXLOC + i - i0) * a.n : a.kmat + i * a.n;
+            const double* kc = pf ? kcs + (MAXLOC + i - i0) * a.n : kc2 + i * a.n;
+            if (a.mu_rot) {  // eigenbasis: y~(i,:) = mu_i (U(:,i)' Yhat + lambda x~(i,:)) + rho x~(i,:)
+                row_dot<RP>(a, kc, a.yhat_c2, RP, 1, red, rowbuf);
+                if (threadIdx.x < a.r) {
+                    const int64_t e = i + a.n * threadIdx.x;
+                    const double xt = pf ? xs[i + ldx * threadIdx.x] : a.x[e];
+                    a.y[e] = a.mu_rot[i] * (rowbuf[threadIdx.x] + a.lambda * xt) + a.rho * xt;
+                }
+                __syncthreads();
+                continue;
+            }
             // no observation on row i here -> no CTA produced Xhat(i,:): recompute it below
             const bool empty = local_x && (i - i0 < 32 ? ((s_c2_empty >> (i - i0)) & 1u) != 0
                                                        : a.row_ptr[i + 1] == a.row_ptr[i]);

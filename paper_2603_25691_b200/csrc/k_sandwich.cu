@@ -359,6 +359,16 @@ __global__ void scale_cols_kernel(const double* __restrict__ a, int64_t n, const
         out[e] = a[e] * d[e / n];
 }
 
+__global__ void scale_rows_kernel(const double* __restrict__ a, int64_t n, const double* __restrict__ d,
+                                  double* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = a[e] * d[e % n];
+}
+void scale_rows(const double* a, int64_t n, const double* d, double* out, cudaStream_t s) {
+    scale_rows_kernel<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, s>>>(a, n, d, out);
+    CPHIFI_CHECK_LAUNCH();
+}
+
 void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaStream_t s) {
     scale_cols_kernel<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, s>>>(a, n, d, out);
     CPHIFI_CHECK_LAUNCH();
@@ -381,6 +391,41 @@ __global__ void scale_columns_kernel(double* a, int64_t m, int64_t r, const doub
 }
 void scale_columns(double* a, int64_t m, int64_t r, const double* d, cudaStream_t s) {
     scale_columns_kernel<<<(unsigned)std::min<int64_t>((m * r + 255) / 256, 2048), 256, 0, s>>>(a, m, r, d);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+// Eigenbasis preconditioner in one launch (small r): z~(i,:) = ((r~(i,:) U_V) o D(i,:)) U_V' for a
+// block of RB rows per CTA, U_V staged in shared memory; fixed summation order (m ascending).
+constexpr int PR_T = 256, PR_RB = 16;
+__global__ void __launch_bounds__(PR_T) precond_rot_kernel(const double* __restrict__ rt, const double* __restrict__ uv,
+                                                           const double* __restrict__ dmat, int64_t n, int r,
+                                                           double* __restrict__ zt) {
+    extern __shared__ double prs[];
+    double* suv = prs;                   // r x r
+    double* st = suv + r * r;            // PR_RB x r
+    const int64_t i0 = (int64_t)blockIdx.x * PR_RB;
+    const int rb = (int)min((int64_t)PR_RB, n - i0);
+    for (int e = threadIdx.x; e < r * r; e += PR_T) suv[e] = uv[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < rb * r; e += PR_T) {
+        const int q = e / r, j = e % r;
+        const int64_t i = i0 + q;
+        double t = 0.0;
+        for (int m = 0; m < r; ++m) t = fma(rt[i + n * m], suv[m + r * j], t);
+        st[q * r + j] = t * dmat[i + n * j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rb * r; e += PR_T) {
+        const int q = e / r, j = e % r;
+        double z = 0.0;
+        for (int m = 0; m < r; ++m) z = fma(st[q * r + m], suv[j + r * m], z);
+        zt[i0 + q + n * j] = z;
+    }
+}
+void precond_rot_small(const double* rt, const double* uv, const double* dmat, int64_t n, int64_t r, double* zt,
+                       cudaStream_t s) {
+    const size_t smem = sizeof(double) * (r * r + PR_RB * r);
+    precond_rot_kernel<<<(unsigned)((n + PR_RB - 1) / PR_RB), PR_T, smem, s>>>(rt, uv, dmat, n, (int)r, zt);
     CPHIFI_CHECK_LAUNCH();
 }
 

@@ -95,10 +95,15 @@ bool sandwich_supported(int64_t n, int64_t r);
 int64_t sandwich_rp(int64_t r);
 void sandwich(SandArgs a, int num_sms, cudaStream_t s);
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
+// eigenbasis preconditioner z~ = ((r~ U_V) o D) U_V' in one launch (r <= 64)
+void precond_rot_small(const double* rt, const double* uv, const double* dmat, int64_t n, int64_t r, double* zt,
+                       cudaStream_t s);
 // sigma -> pseudo-inverse spectrum (1 / sigma above r eps sigma_max, else 0), in place
 void invert_spectrum(double* sv, int64_t r, cudaStream_t s);
 // a (m x r column-major) <- a diag(d)
 void scale_columns(double* a, int64_t m, int64_t r, const double* d, cudaStream_t s);
+// out = diag(d) a  (n x n column-major)
+void scale_rows(const double* a, int64_t n, const double* d, double* out, cudaStream_t s);
 // out = a diag(d)  (n x n column-major)
 void scale_cols(const double* a, int64_t n, const double* d, double* out, cudaStream_t s);
 
@@ -134,6 +139,10 @@ struct FusedArgs {
     double lambda = 0.0, rho = 0.0;
     const double* yhat_c2 = nullptr;    // complete Yhat read by PH_C2 (yhat_rm or the NCCL sum)
     const double* gram = nullptr;       // non-null: phase B applies the row-Gram operator instead
+    // eigenbasis PCG (k_fused PH_C2): y~ rows = mu_i (U(:,i)' Yhat + lambda x~_i) + rho x~_i with the
+    // columns of kmat_c2 (= U); kmat then holds diag(mu) U' so PH_AL/PH_A produce Xhat = U diag(mu) x~
+    const double* kmat_c2 = nullptr;    // null: kmat
+    const double* mu_rot = nullptr;     // non-null: the eigenbasis epilogue
     unsigned* rowcnt = nullptr;         // n per-row arrival counters, zero-initialised once
     int prefetch = 0;                   // stage X and the needed K columns in smem (small n)
     unsigned* barrier = nullptr;        // barrier_words(grid) uints, zero-initialised once
