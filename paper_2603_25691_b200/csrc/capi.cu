@@ -133,6 +133,23 @@ const double* mode_um(cphifi_mode m) {
     return m->um.get();
 }
 
+// Number of leading eigenvalues that are exactly 0 after the clamp (syevd returns them ascending,
+// so the clamped negatives come first), rounded down to a multiple of 8 so the offset GEMM
+// operands stay 16-byte aligned.  The eigenbasis operator skips those rows / columns of U: their
+// mu_i = 0 multiplies them out of K X, and their rows of y~ reduce to rho x~.  One host read per
+// installed eigenbasis.
+int64_t mode_nzero(cphifi_mode m) {
+    std::lock_guard<std::mutex> lk(m->mu_lock);
+    if (m->nzero < 0) {
+        std::vector<double> h((size_t)m->n);
+        d2h_sync(h.data(), m->mu.get(), sizeof(double) * m->n, m->ctx->stream);
+        int64_t z = 0;
+        while (z < m->n && h[(size_t)z] == 0.0) ++z;
+        m->nzero = z & ~int64_t(7);
+    }
+    return m->nzero;
+}
+
 const double* mode_umt(cphifi_mode m) {
     const double* ut = mode_ut(m);
     std::lock_guard<std::mutex> lk(m->mu_lock);
@@ -534,24 +551,29 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
         }
         return;
     }
+    // rows / columns of the clamped null space (mu_i = 0) drop out of both GEMMs (mode_nzero)
+    int64_t z = 0;
+    if (const char* e = std::getenv("CPHIFI_PCG_SKIPZERO"); !e || std::atoi(e) != 0) z = mode_nzero(p->mode);
+    if (z >= n) z = 0;
     GemmArgs g;  // Xhat = U diag(mu) x~  -> row-major padded copy for the gather
-    g.m = n; g.n = r; g.k = n;
-    g.a = mode_um(p->mode); g.a_rs = 1; g.a_cs = n;
-    g.b = xt; g.b_rs = 1; g.b_cs = n;
+    g.m = n; g.n = r; g.k = n - z;
+    g.a = mode_um(p->mode) + z * n; g.a_rs = 1; g.a_cs = n;
+    g.b = xt + z; g.b_rs = 1; g.b_cs = n;
     g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
     gemm(g, ctx->num_sms, ctx->stream);
     const double* gr = p->op == 1 ? p->gram.get() : nullptr;
     if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), n, p->rp, p->yhat_rm.get(), ctx->stream);
     else launch_phase_b(p, fused_args(p, PH_B));
     allreduce_yhat(p);
-    GemmArgs h;  // y~ = mu o (U' Yhat + lambda x~) + rho x~
-    h.m = n; h.n = r; h.k = n;
-    h.a = mode_ut(p->mode); h.a_rs = 1; h.a_cs = n;
+    GemmArgs h;  // y~ = mu o (U' Yhat + lambda x~) + rho x~   (rows i >= z)
+    h.m = n - z; h.n = r; h.k = n;
+    h.a = mode_ut(p->mode) + z; h.a_rs = 1; h.a_cs = n;
     h.b = yhat_result(p); h.b_rs = p->rp; h.b_cs = 1;
-    h.c = yt; h.c_rs = 1; h.c_cs = n;
-    h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get(); h.e1 = xt; h.ld_e = n;
+    h.c = yt + z; h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get() + z; h.e1 = xt + z; h.ld_e = n;
     h.beta1 = p->mode->lambda; h.beta2 = p->rho;
     gemm(h, ctx->num_sms, ctx->stream);
+    if (z > 0) scale_row_block(yt, xt, z, n, r, p->rho, ctx->stream);  // y~ = rho x~  (rows i < z)
 }
 
 void precond_rot(cphifi_unaligned p, const double* rt, double* zt) {
@@ -666,10 +688,13 @@ void upload_factors_cm(cphifi_ctx ctx, int d, const int64_t* shape, int k, int64
 
 // The device-resident PCG loop needs a single GPU (no NCCL inside the graph body); opt out with
 // CPHIFI_PCG_GRAPH=0.  A failed capture or instantiation falls back to the host loop for good.
+// Default: the graph unless the iteration is long enough that the host round trip is cheaper than
+// the WHILE body's per-iteration cost — measured on B200 (profiles/prof_pcg_ab.sh): config 4
+// (n r = 262144) 15.0 ms graph vs 13.0 ms host loop; config 3 (n r = 65536) 0.58 vs 0.64 ms.
 bool pcg_graph_ok(cphifi_unaligned p) {
     if (p->pcg_graph_failed || is_multi(p)) return false;
     if (const char* e = std::getenv("CPHIFI_PCG_GRAPH")) return std::atoi(e) != 0;
-    return true;
+    return p->n * p->r <= 131072;
 }
 
 // Capture `body` (one PCG iteration) into the body graph of a WHILE conditional node and
@@ -677,7 +702,8 @@ bool pcg_graph_ok(cphifi_unaligned p) {
 // persistent PCG vectors, so later solves reuse the executable graph.
 template <class F>
 bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
-    if (p->pcg_exec && p->pcg_graph_op == p->op && p->pcg_graph_rot == (int)rot) return true;
+    const int64_t zkey = rot && p->mode ? p->mode->nzero : -1;
+    if (p->pcg_exec && p->pcg_graph_op == p->op && p->pcg_graph_rot == (int)rot && p->pcg_graph_z == zkey) return true;
     if (p->pcg_exec) cudaGraphExecDestroy(p->pcg_exec);
     if (p->pcg_graph) cudaGraphDestroy(p->pcg_graph);
     p->pcg_exec = nullptr;
@@ -709,6 +735,7 @@ bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
         p->pcg_exec = ex;
         p->pcg_graph_op = p->op;
         p->pcg_graph_rot = (int)rot;
+        p->pcg_graph_z = zkey;
         return true;
     } catch (const Error& e) {
         if (capturing) {
@@ -728,7 +755,8 @@ bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
 // PCG vectors.  Returns false (and disables itself for the plan) when capture fails.
 template <class FA, class FW, class FB>
 bool ensure_pcg_full_graph(cphifi_unaligned p, bool rot, FA&& seg_a, FW&& body, FB&& seg_b) {
-    if (p->pcgf_exec && p->pcgf_op == p->op && p->pcgf_rot == (int)rot) return true;
+    const int64_t zkey = rot && p->mode ? p->mode->nzero : -1;
+    if (p->pcgf_exec && p->pcgf_op == p->op && p->pcgf_rot == (int)rot && p->pcgf_z == zkey) return true;
     if (p->pcgf_exec) cudaGraphExecDestroy(p->pcgf_exec);
     if (p->pcgf_graph) cudaGraphDestroy(p->pcgf_graph);
     p->pcgf_exec = nullptr;
@@ -780,6 +808,7 @@ bool ensure_pcg_full_graph(cphifi_unaligned p, bool rot, FA&& seg_a, FW&& body, 
         p->pcgf_exec = ex;
         p->pcgf_op = p->op;
         p->pcgf_rot = (int)rot;
+        p->pcgf_z = zkey;
         return true;
     } catch (const Error& e) {
         if (capturing) {
@@ -992,6 +1021,7 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         mode->have_ut = false;
         mode->have_um = false;
         mode->have_umt = false;
+        mode->nzero = -1;
         h2d(mode->u.get(), u, sizeof(double) * n * n, mode->ctx->stream);
         h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
         clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);
@@ -1771,17 +1801,18 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         const int64_t n = p->n, r = p->r, nr = n * r;
         if (!p->pcg_vec.n) {
             p->pcg_vec.alloc(6 * nr);
-            p->pcg_aux.alloc(80 + (sizeof(PcgState) + sizeof(PcgCtl) + 7) / 8);
+            p->pcg_aux.alloc(RED_PARTIALS + (sizeof(PcgState) + sizeof(PcgCtl) + 7) / 8);
         }
         double* bvec = p->pcg_vec.get();
         double *x = bvec + nr, *res = bvec + 2 * nr, *z = bvec + 3 * nr, *pv = bvec + 4 * nr, *ap = bvec + 5 * nr;
         double* partial = p->pcg_aux.get();
-        PcgState* st = reinterpret_cast<PcgState*>(partial + 80);
-        PcgCtl* ctl = reinterpret_cast<PcgCtl*>(partial + 80 + (sizeof(PcgState) + 7) / 8);
-        CPHIFI_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * 80, s));
+        PcgState* st = reinterpret_cast<PcgState*>(partial + RED_PARTIALS);
+        PcgCtl* ctl = reinterpret_cast<PcgCtl*>(partial + RED_PARTIALS + (sizeof(PcgState) + 7) / 8);
+        CPHIFI_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * RED_PARTIALS, s));
         CPHIFI_CUDA(cudaMemsetAsync(st, 0, sizeof(PcgState), s));
         ensure_precond(p);                                                        // build_preconditioner
         const bool rot = pcg_eigbasis(p);
+        if (rot && !p->small_n) mode_nzero(p->mode);  // host read here, never inside a graph capture
         if (rot) rotate(p, true, true, p->b.get(), bvec);  // rhs~ = (I x U') vec(K B) = mu o (U' B)
         else gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
@@ -1794,6 +1825,24 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         auto apply_m = [&](const double* rin, double* zout) {
             if (rot) precond_rot(p, rin, zout);
             else precond_dev(p, rin, zout);
+        };
+        // large-n eigenbasis PCG: the iteration's vector work after Ap in one cooperative launch
+        // (k_pcgstep.cu) instead of pap / x,r / control / preconditioner / rz / p launches
+        bool fused_step = rot && !p->small_n && r <= 64;
+        if (const char* e = std::getenv("CPHIFI_PCG_FUSED")) fused_step = fused_step && std::atoi(e) != 0;
+        if (fused_step && !p->pcg_step.n) {
+            p->pcg_step.alloc(1 + pcg_step_fused_partials(n, ctx->num_sms));
+            CPHIFI_CUDA(cudaMemsetAsync(p->pcg_step.get(), 0, sizeof(double), s));
+        }
+        auto step_fused = [&](PcgCtl* c, cudaGraphConditionalHandle h) {
+            PcgStepArgs sa;
+            sa.n = n; sa.r = (int)r;
+            sa.uv = p->uv.get(); sa.dmat = p->dmat.get();
+            sa.x = x; sa.res = res; sa.p = pv; sa.z = z; sa.ap = ap;
+            sa.st = st; sa.ctl = c; sa.h = h;
+            sa.barrier = reinterpret_cast<unsigned long long*>(p->pcg_step.get());
+            sa.partial = p->pcg_step.get() + 1;
+            pcg_step_fused(sa, ctx->num_sms, s);
         };
         // ---- whole solve on device: one graph launch, one synchronisation -----------------
         if (p->op == 1) ensure_gram(p);
@@ -1820,6 +1869,10 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 },
                 [&](cudaGraphConditionalHandle h) {
                     apply_a(pv, ap);
+                    if (fused_step) {
+                        step_fused(ctl, h);
+                        return;
+                    }
                     pcg_step_a_ctl(x, res, pv, ap, nr, st, partial, ctl, h, s);
                     apply_m(res, z);
                     pcg_step_b(res, z, pv, nr, st, partial, s);
@@ -1928,6 +1981,11 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 // device-resident loop: a CUDA graph whose WHILE node repeats the iteration until
                 // pcg_ctl clears the condition; no host round trip per iteration
                 if (ensure_pcg_graph(p, rot, [&](cudaGraphConditionalHandle h) {
+                        if (fused_step) {
+                            apply_a(pv, ap);
+                            step_fused(ctl, h);
+                            return;
+                        }
                         body_a();
                         pcg_ctl(st, ctl, h, s);
                         body_b();
@@ -1957,7 +2015,12 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 }
             }
             while (!done && rel > cfg->tol && it < cfg->max_iter) {
-                body_a();
+                if (fused_step) {  // step B runs inside the same launch (harmless after the last one)
+                    apply_a(pv, ap);
+                    step_fused(nullptr, cudaGraphConditionalHandle{});
+                } else {
+                    body_a();
+                }
                 ++matvecs;
                 d2h_sync(&hst, st, sizeof(PcgState), s);
                 if (hst.flag == 1) throw_runtime("pcg: non-finite value encountered");
@@ -1966,7 +2029,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 rel = hst.rel;
                 if (cfg->record_history) hist.push_back(rel);
                 if (rel <= cfg->tol) break;
-                body_b();
+                if (!fused_step) body_b();
             }
             rep.iterations = it;
             rep.relative_residual = rel;
@@ -2363,9 +2426,9 @@ int cphifi_als_update_finite_aligned(cphifi_tensor t, int k, int64_t r, const do
             gg.b = a.get(); gg.b_rs = 1; gg.b_cs = nk;
             gg.c = g.get(); gg.c_rs = 1; gg.c_cs = r;
             gemm(gg, ctx->num_sms, s);
-            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * RED_PARTIALS, s));
             dot_to(a.get(), b.get(), nr, part.get(), scal.get(), s);
-            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * RED_PARTIALS, s));
             dot_to(g.get(), v.get(), r * r, part.get(), scal.get() + 1, s);
             if (!t->have_norm) {
                 int64_t cnt = t->shape[0] * (t->slab_hi - t->slab_lo);
@@ -2436,7 +2499,7 @@ int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_co
         if (solve_report) *solve_report = rep;
         CPHIFI_CUDA(cudaEventRecord(ev[1], s));
         const double* wdev = p->pcg_vec.get() + nr;  // the solution stays in the plan's x slot
-        DevBuf<double> a(nr), arm((size_t)n * p->rp), scal(4), part(std::max<int64_t>(sq_residual_blocks(o->q_local), 64) + 80);
+        DevBuf<double> a(nr), arm((size_t)n * p->rp), scal(4), part(std::max<int64_t>(sq_residual_blocks(o->q_local), RED_PARTIALS) + 80);
         gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, wdev, n, a.get(), n);  // A_k = K W (als.hpp:214)
         pack_rows(a.get(), n, n, r, p->rp, arm.get(), s);
         SqResidualArgs ra;
@@ -2449,7 +2512,7 @@ int cphifi_als_update_infinite_unaligned(cphifi_unaligned p, const cphifi_pcg_co
         const int64_t nbn = std::min<int64_t>(std::max<int64_t>(1, (o->q_local + 2047) / 2048), 1024);
         if (o->q_local > 0) sq_norm(o->values.get(), o->q_local, part.get(), nbn, scal.get() + 1, s);  // [1] ||v||^2
         else CPHIFI_CUDA(cudaMemsetAsync(scal.get() + 1, 0, sizeof(double), s));
-        CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+        CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * RED_PARTIALS, s));
         dot_to(wdev, a.get(), nr, part.get(), scal.get() + 2, s);                            // [2] trace(W'KW)
         allreduce(ctx, scal.get(), 2);  // sharded observations: sum the fit and norm terms
         CPHIFI_CUDA(cudaEventRecord(ev[2], s));
@@ -2517,7 +2580,7 @@ int cphifi_als_update_infinite_aligned(cphifi_tensor t, cphifi_mode mode, int k,
         gg.c = g.get(); gg.c_rs = 1; gg.c_cs = r;
         gemm(gg, ctx->num_sms, s);
         auto dot = [&](const double* x, const double* y, int64_t cnt, double* out) {
-            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * 80, s));
+            CPHIFI_CUDA(cudaMemsetAsync(part.get(), 0, sizeof(double) * RED_PARTIALS, s));
             dot_to(x, y, cnt, part.get(), out, s);
         };
         dot(res.get(), res.get(), nr, scal.get() + 0);  // ||R||^2

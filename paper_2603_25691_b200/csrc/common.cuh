@@ -110,6 +110,7 @@ struct cphifi_mode_s {
     bool have_um = false;
     cphifi::DevBuf<double> umt;     // diag(mu) U' (the fused kernel's Xhat columns in the eigenbasis)
     bool have_umt = false;
+    int64_t nzero = -1;             // leading exactly-zero (clamped) eigenvalues, rounded down to 8; lazily
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;
@@ -172,6 +173,8 @@ struct cphifi_unaligned_s {
     // device-resident PCG: persistent vectors + a CUDA graph whose WHILE node runs the iterations
     cphifi::DevBuf<double> pcg_vec;           // b, x, r, z, p, Ap (n r each)
     cphifi::DevBuf<double> pcg_aux;           // reduction partials | PcgState | PcgCtl
+    cphifi::DevBuf<double> pcg_step;          // fused vector step (k_pcgstep.cu): barrier word | partials
+    int64_t pcg_graph_z = -1, pcgf_z = -1;    // mode_nzero baked into the captured graphs
     cphifi::DevBuf<double> pcg_hist;          // device residual history
     cudaGraph_t pcg_graph = nullptr;
     cudaGraphExec_t pcg_exec = nullptr;

@@ -1065,6 +1065,52 @@ __global__ void reduce_epi_kernel(const double* __restrict__ work, int P, int64_
     }
 }
 
+// Split-K scratch of the plain GEMM, per host thread: grow-only, and a buffer it outgrows is
+// retired, never freed — instantiated CUDA graphs (the PCG loop, the host-buffer matvec) hold its
+// address for their lifetime, so freeing it would leave them writing into released memory.
+struct GrowScratch {
+    double* p = nullptr;
+    size_t n = 0;
+    int dev = -1;
+    void ensure(int device, size_t need) {
+        if (dev == device && n >= need) return;
+        static std::mutex mu;
+        static std::vector<double*> retired;  // alive until process exit
+        std::lock_guard<std::mutex> lk(mu);
+        if (p) retired.push_back(p);
+        const size_t cnt = std::max(need + need / 2, (size_t)1 << 16);
+        p = nullptr;
+        CPHIFI_CUDA(cudaMalloc(&p, cnt * sizeof(double)));
+        n = cnt;
+        dev = device;
+    }
+    double* get() const { return p; }
+};
+
+// The plain GEMM runs the MTTKRP ring with a single Khatri-Rao outer row Wout = 1: one constant
+// buffer per device, filled once outside any graph capture (inside a capture the fill is a
+// captured node in front of the GEMM, and the buffer is filled again on the next uncaptured call).
+constexpr int ONES_N = 256;
+__global__ void fill_ones_kernel(double* p) {
+    if (threadIdx.x < ONES_N) p[threadIdx.x] = 1.0;
+}
+const double* gemm_ones(int dev, cudaStream_t s) {
+    static std::mutex mu;
+    static double* buf[64] = {nullptr};
+    static bool filled[64] = {false};
+    if (dev < 0 || dev >= 64) throw_runtime("gemm: device index out of range");
+    std::lock_guard<std::mutex> lk(mu);
+    if (!buf[dev]) CPHIFI_CUDA(cudaMalloc(&buf[dev], sizeof(double) * ONES_N));
+    if (!filled[dev]) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CPHIFI_CUDA(cudaStreamIsCapturing(s, &cs));
+        fill_ones_kernel<<<1, ONES_N, 0, s>>>(buf[dev]);
+        CPHIFI_CHECK_LAUNCH();
+        if (cs == cudaStreamCaptureStatusNone) filled[dev] = true;
+    }
+    return buf[dev];
+}
+
 bool gemm_tma_ok(const GemmArgs& g) {
     if (const char* e = std::getenv("CPHIFI_GEMM_TMA"))
         if (std::atoi(e) == 0) return false;
@@ -1077,21 +1123,16 @@ bool gemm_tma_ok(const GemmArgs& g) {
 
 template <int BN>
 void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
-    static thread_local DevBuf<double> work;
-    static thread_local int work_dev = -1;
+    static thread_local GrowScratch work;
     int dev = 0;
     CPHIFI_CUDA(cudaGetDevice(&dev));
-    if (work_dev != dev) {
-        work.release();
-        work_dev = dev;
-    }
     const bool brow = !(g.b_rs == 1);
     const int mt = (int)((g.m + BMM - 1) / BMM), nt = (int)((g.n + BN - 1) / BN);
     const int64_t chunks = (g.k + BK - 1) / BK;
     int64_t P = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms / (mt * nt), chunks));
-    const size_t need = (size_t)P * g.m * g.n + (size_t)g.n + 2;
-    if (work.n < need) work.alloc(need);
-    double* wout = work.get() + (size_t)P * g.m * g.n;
+    const size_t need = (size_t)P * g.m * g.n + 2;
+    work.ensure(dev, need);
+    const double* wout = gemm_ones(dev, s);
     MttkrpArgs a;
     a.d = 2;
     a.shape[0] = g.m;
@@ -1102,8 +1143,6 @@ void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
     a.ld[1] = brow ? g.b_rs : g.b_cs;
     a.off1 = 0;
     a.ldw = (g.n + 1) & ~1LL;
-    kr_outer_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(a, 1, wout);  // Wout = 1
-    CPHIFI_CHECK_LAUNCH();
     CUtensorMap tm_a, tm_b;
     const bool ok = encode_tmap_2d_f64(&tm_a, g.a, (uint64_t)g.m, (uint64_t)g.k, (uint64_t)g.a_cs, BMM + 4, BK) &&
                     (brow ? encode_tmap_2d_f64(&tm_b, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.b_rs, BN + 4, BK)

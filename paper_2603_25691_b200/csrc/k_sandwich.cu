@@ -395,38 +395,90 @@ void scale_columns(double* a, int64_t m, int64_t r, const double* d, cudaStream_
 }
 
 // Eigenbasis preconditioner in one launch (small r): z~(i,:) = ((r~(i,:) U_V) o D(i,:)) U_V' for a
-// block of RB rows per CTA, U_V staged in shared memory; fixed summation order (m ascending).
-constexpr int PR_T = 256, PR_RB = 16;
+// block of 32 rows per CTA.  Lane = row (column-major r~, D, z~: every warp access is one
+// contiguous 256-byte column segment), warp w = columns [w JT, (w + 1) JT); the r~ block and the
+// intermediate t are staged column-major in shared memory (lanes on consecutive rows: conflict-
+// free), U_V' row-major so a thread's JT columns of U_V(m, :) are one broadcast vector load.
+// Fixed summation order (m ascending), as the reference's GEMMs per row.
+constexpr int PR_T = 256, PR_RB = 32, PR_W = PR_T / 32;
+template <int JT>
 __global__ void __launch_bounds__(PR_T) precond_rot_kernel(const double* __restrict__ rt, const double* __restrict__ uv,
                                                            const double* __restrict__ dmat, int64_t n, int r,
                                                            double* __restrict__ zt) {
-    extern __shared__ double prs[];
-    double* suv = prs;                   // r x r
-    double* st = suv + r * r;            // PR_RB x r
+    constexpr int RP = JT * PR_W;  // padded rank (columns)
+    constexpr int LDU = RP + 2;    // padded row stride: the transposed staging writes spread over banks
+    extern __shared__ __align__(16) double prs[];
+    double* suv = prs;                  // suv[m * LDU + j] = U_V(m, j)   (0 beyond r)
+    double* sr = suv + RP * LDU;        // sr[m * PR_RB + q] = r~(i0 + q, m), later t
     const int64_t i0 = (int64_t)blockIdx.x * PR_RB;
-    const int rb = (int)min((int64_t)PR_RB, n - i0);
-    for (int e = threadIdx.x; e < r * r; e += PR_T) suv[e] = uv[e];
-    __syncthreads();
-    for (int e = threadIdx.x; e < rb * r; e += PR_T) {
-        const int q = e / r, j = e % r;
-        const int64_t i = i0 + q;
-        double t = 0.0;
-        for (int m = 0; m < r; ++m) t = fma(rt[i + n * m], suv[m + r * j], t);
-        st[q * r + j] = t * dmat[i + n * j];
+    const int q = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = i0 + q;
+    const bool row_ok = i < n;
+    // every load of the CTA issued before the first use (unrolled): U_V read coalesced (m fastest)
+#pragma unroll
+    for (int k = 0; k < (RP * RP + PR_T - 1) / PR_T; ++k) {
+        const int e = threadIdx.x + k * PR_T;
+        const int m = e % RP, j = e / RP;
+        if (e < RP * RP) suv[m * LDU + j] = (m < r && j < r) ? uv[m + (int64_t)r * j] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < JT; ++k) {
+        const int m = w + k * PR_W;
+        sr[m * PR_RB + q] = (row_ok && m < r) ? rt[i + n * m] : 0.0;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < rb * r; e += PR_T) {
-        const int q = e / r, j = e % r;
-        double z = 0.0;
-        for (int m = 0; m < r; ++m) z = fma(st[q * r + m], suv[j + r * m], z);
-        zt[i0 + q + n * j] = z;
+    double acc[JT];
+#pragma unroll
+    for (int u = 0; u < JT; ++u) acc[u] = 0.0;
+    const int j0 = w * JT;
+    for (int m = 0; m < r; ++m) {
+        const double a = sr[m * PR_RB + q];
+        const double* um = suv + m * LDU + j0;
+#pragma unroll
+        for (int u = 0; u < JT; ++u) acc[u] = fma(a, um[u], acc[u]);
     }
+#pragma unroll
+    for (int u = 0; u < JT; ++u) {
+        const int j = j0 + u;
+        if (j < r && row_ok) acc[u] *= dmat[i + n * j];
+    }
+    __syncthreads();  // everyone is done reading r~
+#pragma unroll
+    for (int u = 0; u < JT; ++u) sr[(j0 + u) * PR_RB + q] = acc[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < JT; ++u) acc[u] = 0.0;
+    for (int m = 0; m < r; ++m) {  // z~(i, j) = sum_m t(i, m) U_V(j, m)
+        const double t = sr[m * PR_RB + q];
+#pragma unroll
+        for (int u = 0; u < JT; ++u) acc[u] = fma(t, suv[(j0 + u) * LDU + m], acc[u]);
+    }
+    if (row_ok) {
+#pragma unroll
+        for (int u = 0; u < JT; ++u)
+            if (j0 + u < r) zt[i + n * (j0 + u)] = acc[u];
+    }
+}
+template <int JT>
+void launch_precond_rot(const double* rt, const double* uv, const double* dmat, int64_t n, int64_t r, double* zt,
+                        cudaStream_t s) {
+    constexpr int RP = JT * PR_W;
+    const size_t smem = sizeof(double) * (RP * (RP + 2) + RP * PR_RB);
+    static bool attr = false;
+    if (!attr) {
+        CPHIFI_CUDA(cudaFuncSetAttribute(precond_rot_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    precond_rot_kernel<JT><<<(unsigned)((n + PR_RB - 1) / PR_RB), PR_T, smem, s>>>(rt, uv, dmat, n, (int)r, zt);
+    CPHIFI_CHECK_LAUNCH();
 }
 void precond_rot_small(const double* rt, const double* uv, const double* dmat, int64_t n, int64_t r, double* zt,
                        cudaStream_t s) {
-    const size_t smem = sizeof(double) * (r * r + PR_RB * r);
-    precond_rot_kernel<<<(unsigned)((n + PR_RB - 1) / PR_RB), PR_T, smem, s>>>(rt, uv, dmat, n, (int)r, zt);
-    CPHIFI_CHECK_LAUNCH();
+    if (r <= 8) launch_precond_rot<1>(rt, uv, dmat, n, r, zt, s);
+    else if (r <= 16) launch_precond_rot<2>(rt, uv, dmat, n, r, zt, s);
+    else if (r <= 32) launch_precond_rot<4>(rt, uv, dmat, n, r, zt, s);
+    else if (r <= 64) launch_precond_rot<8>(rt, uv, dmat, n, r, zt, s);
+    else throw_invalid("precond_rot_small: rank above 64");
 }
 
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {

@@ -22,7 +22,7 @@ constexpr int SG_THREADS = 256;
 
 // ---- PCG vector kernels ------------------------------------------------------------------
 constexpr int RED_THREADS = 256;
-constexpr int RED_BLOCKS = 64;  // fixed -> fixed summation tree -> deterministic
+constexpr int RED_BLOCKS = RED_GRID;  // fixed -> fixed summation tree -> deterministic (2 CTAs per SM)
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -51,12 +51,15 @@ __device__ __forceinline__ void finish_reduce(double local, double* partial, uns
         last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {  // the partials in a fixed tree: thread t sums t, t + blockDim, ...; then block_sum
         __threadfence();
         double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)partial)[b];
-        *ticket = 0;
-        fin(s);
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(partial + b);
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) {
+            *ticket = 0;
+            fin(s);
+        }
     }
 }
 
@@ -241,6 +244,15 @@ __global__ void axpby_kernel(double* y, const double* a, double alpha, const dou
         y[i] = alpha * a[i] + beta * b[i];
 }
 
+// y(i, j) = alpha x(i, j) for rows i < z of column-major n x r blocks
+__global__ void scale_row_block_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t z, int64_t n,
+                                       int64_t r, double alpha) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < z * r; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % z, j = e / z;
+        y[i + n * j] = alpha * x[i + n * j];
+    }
+}
+
 // ---- observation plan helpers -------------------------------------------------------------
 __global__ void check_range_kernel(const int32_t* idx, int d, int64_t q, const int64_t* shape, int* flag) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)d * q;
@@ -386,6 +398,12 @@ void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s) {
 }
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n, cudaStream_t s) {
     axpby_kernel<<<grid_for(n, 256), 256, 0, s>>>(y, a, alpha, b, beta, n);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+void scale_row_block(double* y, const double* x, int64_t z, int64_t n, int64_t r, double alpha, cudaStream_t s) {
+    if (z <= 0 || r <= 0) return;
+    scale_row_block_kernel<<<grid_for(z * r, 256), 256, 0, s>>>(y, x, z, n, r, alpha);
     CPHIFI_CHECK_LAUNCH();
 }
 

@@ -217,6 +217,23 @@ struct PcgCtl {
     double rel0;       // relative residual of the initial guess
 };
 void pcg_ctl(const PcgState* st, PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
+// One PCG iteration's vector work after Ap (pap, x/r update, loop control, eigenbasis
+// preconditioner, rz, p update) as one cooperative launch: k_pcgstep.cu.  r <= 64.
+struct PcgStepArgs {
+    int64_t n = 0;
+    int r = 0;
+    const double* uv = nullptr;    // U_V, r x r column-major
+    const double* dmat = nullptr;  // D, n x r column-major
+    double *x = nullptr, *res = nullptr, *p = nullptr, *z = nullptr;
+    const double* ap = nullptr;
+    PcgState* st = nullptr;
+    PcgCtl* ctl = nullptr;         // loop control (graph body), or nullptr
+    cudaGraphConditionalHandle h{};
+    double* partial = nullptr;     // pcg_step_fused_partials(n, num_sms) doubles
+    unsigned long long* barrier = nullptr;  // zero-initialised once per plan
+};
+int pcg_step_fused_partials(int64_t n, int num_sms);
+void pcg_step_fused(const PcgStepArgs& a, int num_sms, cudaStream_t s);
 // step A followed by the loop control (one launch for n <= 32768)
 void pcg_step_a_ctl(double* x, double* r, const double* p, const double* ap, int64_t n, PcgState* st, double* partial,
                     PcgCtl* c, cudaGraphConditionalHandle h, cudaStream_t s);
@@ -238,6 +255,11 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
               cudaStream_t s);
 // dst <- src (n doubles), a kernel copy when 16-byte aligned (mapped host memory allowed)
 void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s);
+// Grid of the deterministic vector reductions (dot_to / PCG steps); their `partial` scratch needs
+// RED_PARTIALS doubles (RED_GRID partials + the ticket word).
+constexpr int RED_GRID = 296;
+constexpr int RED_PARTIALS = RED_GRID + 8;
+void scale_row_block(double* y, const double* x, int64_t z, int64_t n, int64_t r, double alpha, cudaStream_t s);
 void axpby(double* y, const double* a, double alpha, const double* b, double beta, int64_t n,
            cudaStream_t s);  // y = alpha*a + beta*b
 

@@ -200,3 +200,42 @@ def test_mttkrp_v3_odd_rank_many_outer(cp, monkeypatch):
         monkeypatch.setenv("CPHIFI_MTTKRP_V1", v1)
         monkeypatch.setenv("CPHIFI_MTTKRP_V3", v3)
         assert ri.rel(cp.mttkrp(t, cp.KruskalModel(factors), 0), bo) < 1e-12, (v1, v3)
+
+
+@pytest.mark.parametrize("fused,skipzero", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+def test_pcg_large_n_step_variants(cp, monkeypatch, fused, skipzero):
+    """Large-n eigenbasis PCG: the one-launch cooperative vector step (k_pcgstep.cu) and the GEMMs
+    that skip the clamped null space of K (mu_i = 0 rows / columns) against the oracle — each
+    setting on a fresh plan (the captured solve graph bakes both in).  Residual history within
+    1e-6 relative of the separate-kernel / full-GEMM path's (fp64 summation order only)."""
+    g = np.random.default_rng(601)
+    shape, r, q = [640, 24, 20], 12, 40000
+    pts = np.sort(g.uniform(0, 1, shape[0]))
+    lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+    idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+    vals = g.normal(size=q)
+    factors = [np.zeros((shape[0], r))] + [g.normal(size=(n, r)) for n in shape[1:]]
+    mode = cp.RkhsMode(pts, 0.05, 1e-3)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    assert (ek.d == 0).sum() >= 8  # the null-space skip is exercised
+    mode.set_eig(ek.u, ek.d)
+    cfg = cp.PcgConfig(1e-9, 500, record_history=True)
+    res = {}
+    for f, z in (("0", "0"), (fused, skipzero)):
+        monkeypatch.setenv("CPHIFI_PCG_FUSED", f)
+        monkeypatch.setenv("CPHIFI_PCG_SKIPZERO", z)
+        p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), 0, mode, 1e-6)
+        p.set_operator("gram")
+        rep = cp.SolveReport()
+        res[(f, z)] = (cp.solve_unaligned_pcg(p, cfg, rep), rep)
+    (w0, r0), (w1, r1) = res[("0", "0")], res[(fused, skipzero)]
+    sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 0, kern, 1e-3, 1e-6)
+    orep = orc.SolveReport()
+    wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-9, 500), ek, orc.sym_eig(sub.v), report=orep)
+    assert r1.converged and r1.relative_residual <= 1e-9
+    assert abs(r1.iterations - orep.iterations) <= 1, (r1.iterations, orep.iterations)
+    assert r1.iterations == r0.iterations
+    h0, h1 = np.asarray(r0.residual_history), np.asarray(r1.residual_history)
+    assert h0.size == h1.size and np.all(np.abs(h1 - h0) <= 1e-6 * h0), (h0, h1)
+    assert ri.rel(w1, w0) < 1e-9 and ri.rel(w1, wo) < 1e-6
