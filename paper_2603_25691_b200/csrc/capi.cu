@@ -378,8 +378,23 @@ void ensure_gram(cphifi_unaligned p) {
     g.slot_a = slot_a.get();
     g.slot_b = slot_b.get();
     g.g = p->gram.get();
+    const bool timing = std::getenv("CPHIFI_GRAM_TIMING") != nullptr;  // developer: device time of the build
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+        CPHIFI_CUDA(cudaEventCreate(&e0));
+        CPHIFI_CUDA(cudaEventCreate(&e1));
+        CPHIFI_CUDA(cudaEventRecord(e0, s));
+    }
     if (o->q_local > 0) gram_build(g, grid, s);
+    if (timing) CPHIFI_CUDA(cudaEventRecord(e1, s));
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // the plan buffers are released on return
+    if (timing) {
+        float ms = 0.f;
+        CPHIFI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        std::fprintf(stderr, "cphifi: gram build %.3f ms on device (grid %d)\n", ms, grid);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
 }
 
 // Phase sets of the operator launches (see kernels.cuh).  part 0 = the (first) launch,

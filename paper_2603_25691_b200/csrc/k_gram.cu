@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(GT) gram_build_dmma_kernel(const GramArgs a) {
     double* zs = gsm;                           // GB x ZP
     double* zw = zs + GB * ZP;                  // GB x ZP (weighted)
     double* sfac = zw + GB * ZP;                // staged factors (SF)
+    __shared__ int sidx[DO][GB];
+    __shared__ double sw[GB];
     __shared__ int s_last;
     const int c = blockIdx.x;
     const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];
@@ -239,19 +241,37 @@ __global__ void __launch_bounds__(GT) gram_build_dmma_kernel(const GramArgs a) {
             } while (row_end <= pos);
         }
         const int cnt = (int)min((int64_t)GB, min(cb, row_end) - pos);
-        __syncthreads();  // previous batch consumed
-        for (int e = tid; e < GB * RP; e += GT) {
-            const int t = e / RP, j = e % RP;
-            double z = 0.0, w = 0.0;
-            if (t < cnt) {
-                const int64_t l = pos + t;
-                z = fac[a.fac_off[0] + (int64_t)__ldg(a.idx + l) * RP + j];
+        __syncthreads();  // previous batch consumed (zs, zw, sidx, sw)
+        for (int e = tid; e < GB * (DO + 1); e += GT) {  // the batch's indices and weights, once
+            const int t = e % GB, m = e / GB;
+            if (m < DO) sidx[m][t] = t < cnt ? __ldg(a.idx + (int64_t)m * a.q + pos + t) : 0;
+            else sw[t] = t < cnt ? (a.mult ? (double)__ldg(a.mult + pos + t) : 1.0) : 0.0;
+        }
+        __syncthreads();
+        {
+            // all of the thread's factor loads in flight before the first use
+            constexpr int IT = (GB * RP + GT - 1) / GT;
+            double zr[IT][DO];
 #pragma unroll
-                for (int m = 1; m < DO; ++m) z *= fac[a.fac_off[m] + (int64_t)__ldg(a.idx + (int64_t)m * a.q + l) * RP + j];
-                w = a.mult ? (double)__ldg(a.mult + l) : 1.0;
+            for (int k = 0; k < IT; ++k) {
+                const int e = tid + k * GT;
+                const int t = min(e / RP, GB - 1), j = e % RP;
+#pragma unroll
+                for (int m = 0; m < DO; ++m) zr[k][m] = fac[a.fac_off[m] + (int64_t)sidx[m][t] * RP + j];
             }
-            zs[t * ZP + j] = z;
-            zw[t * ZP + j] = z * w;
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int e = tid + k * GT;
+                if (e < GB * RP) {
+                    const int t = e / RP, j = e % RP;
+                    double z = zr[k][0];
+#pragma unroll
+                    for (int m = 1; m < DO; ++m) z *= zr[k][m];
+                    if (t >= cnt) z = 0.0;
+                    zs[t * ZP + j] = z;
+                    zw[t * ZP + j] = z * sw[t];
+                }
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -264,6 +284,202 @@ __global__ void __launch_bounds__(GT) gram_build_dmma_kernel(const GramArgs a) {
                 const double bv = zs[t * ZP + tiles_j[u] * 8 + g];   // B(t, j) = z_t(j)
                 dmma_g(acc[u], av, bv);
             }
+        }
+        pos += cnt;
+    }
+    __syncthreads();
+    finish_row(row);
+}
+
+// ---- DMMA build v2: 2x2 register blocks of 8x8 tiles -------------------------------------------
+// v1 loads one A and one B fragment (two 64-bit LDS, four shared-memory wavefronts) per DMMA,
+// which caps it near half the FP64 tensor rate.  Here a warp owns a 2 x 2 block of tiles of the
+// upper triangle (blocks bi <= bj; the lower tile of a diagonal block is computed and dropped) and
+// reuses each fragment twice: 4 LDS per 4 DMMA.  RP = 64: 10 blocks = 10 warps; RP = 32 / 16:
+// 3 / 1 blocks x KS warps splitting the batch's k-steps, whose partial tiles are summed in ks order
+// at row flush (deterministic).  The batch's indices are staged once in shared memory and the
+// Khatri-Rao rows built two columns per thread (16-byte factor loads).
+template <int RP>
+struct Gv2 {
+    static constexpr int NT = RP / 8, NB = NT / 2, NBLK = NB * (NB + 1) / 2;
+    static constexpr int KS = RP >= 64 ? 1 : (RP >= 32 ? 4 : 8);
+    static constexpr int NWARP = NBLK * KS, T = 32 * NWARP;
+    static constexpr int ZP = RP + 4;
+};
+template <int RP, int DO, bool SF>
+__global__ void __launch_bounds__(Gv2<RP>::T, 2) gram_build_dmma2_kernel(const GramArgs a) {
+    using V = Gv2<RP>;
+    constexpr int ZP = V::ZP, KS = V::KS, T = V::T, NB = V::NB;
+    extern __shared__ __align__(16) double gsm[];
+    double* zs = gsm;                           // GB x ZP
+    double* zw = zs + GB * ZP;                  // GB x ZP (weighted)
+    double* red = zw + GB * ZP;                 // KS > 1: KS x RP x RP partial tiles at flush
+    double* sfac = red + (KS > 1 ? KS * RP * RP : 0);  // staged factors (SF)
+    __shared__ int sidx[DO][GB];
+    __shared__ double sw[GB];
+    __shared__ int s_last;
+    const int c = blockIdx.x;
+    const int64_t ca = a.cta_beg[c], cb = a.cta_beg[c + 1];
+    if (ca >= cb) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, kq = lane & 3;
+    // SF: the factors of modes 1.. staged in shared memory (mode 0 — the first other mode, constant
+    // along the plan's runs — is read through L1)
+    if constexpr (SF) {
+        for (int64_t e = tid; e < a.fac_total - a.fac_off[1]; e += T) sfac[e] = a.fac[a.fac_off[1] + e];
+    }
+    auto fac_m = [&](int m) -> const double* {
+        return SF ? sfac + (a.fac_off[m] - a.fac_off[1]) : a.fac + a.fac_off[m];
+    };
+    const int blk = warp / KS, ks = warp % KS;
+    int bi = 0, bj = 0;
+    {
+        int t = blk;
+        while (t >= NB - bi) {
+            t -= NB - bi;
+            ++bi;
+        }
+        bj = bi + t;
+    }
+    double acc[2][2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    const int64_t first_row = a.cta_rows[2 * c];
+    int64_t row = first_row;
+    int64_t row_end = a.row_ptr[row + 1];
+    auto finish_row = [&](int64_t rr) {
+        const int ncta = a.row_ncta[rr];
+        double* dst = ncta == 1 ? a.g + rr * RP * RP
+                    : rr == first_row ? a.slot_a + (int64_t)c * RP * RP
+                                      : a.slot_b + (int64_t)c * RP * RP;
+        if constexpr (KS == 1) {
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int y = 0; y < 2; ++y) {
+                    const int ti = 2 * bi + x, tj = 2 * bj + y;
+                    if (ti <= tj) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int ii = ti * 8 + g, jj = tj * 8 + 2 * kq + h;
+                            dst[ii * RP + jj] = acc[x][y][h];
+                            if (ti != tj) dst[jj * RP + ii] = acc[x][y][h];
+                        }
+                    }
+                }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int y = 0; y < 2; ++y)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int ii = (2 * bi + x) * 8 + g, jj = (2 * bj + y) * 8 + 2 * kq + h;
+                        red[(ks * RP + ii) * RP + jj] = acc[x][y][h];
+                    }
+            __syncthreads();
+            for (int e = tid; e < RP * RP; e += T) {  // upper triangle: sum the k-splits in order
+                const int ii = e / RP, jj = e % RP;
+                if (ii / 8 > jj / 8) continue;
+                double sv = 0.0;
+#pragma unroll
+                for (int k2 = 0; k2 < KS; ++k2) sv += red[(k2 * RP + ii) * RP + jj];
+                if (ii / 8 < jj / 8 || ii <= jj) {
+                    dst[ii * RP + jj] = sv;
+                    dst[jj * RP + ii] = sv;
+                }
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+        if (ncta > 1) {  // the last CTA of a split row sums the slots in CTA order
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                s_last = atom_add_acqrel_g(a.rowcnt + rr, 1u) == (unsigned)ncta - 1;
+                if (s_last) a.rowcnt[rr] = 0;
+            }
+            __syncthreads();
+            if (s_last) {
+                const int u0 = a.row_first_cta[rr];
+                const bool starts = a.row_ptr[rr] == a.cta_beg[u0];
+                for (int e = tid; e < RP * RP; e += T) {
+                    double sv = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
+                                       : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
+                    for (int u = u0 + 1; u < u0 + ncta; ++u) sv += __ldcg(a.slot_a + (int64_t)u * RP * RP + e);
+                    a.g[rr * RP * RP + e] = sv;
+                }
+            }
+        }
+    };
+    __syncthreads();  // staged factors
+    int64_t pos = ca;
+    while (pos < cb) {
+        while (pos >= row_end) {
+            finish_row(row);
+            do {
+                ++row;
+                row_end = a.row_ptr[row + 1];
+            } while (row_end <= pos);
+        }
+        const int cnt = (int)min((int64_t)GB, min(cb, row_end) - pos);
+        __syncthreads();  // previous batch consumed (zs, zw, sidx, sw)
+        for (int e = tid; e < GB * (DO + 1); e += T) {
+            const int t = e % GB, m = e / GB;
+            if (m < DO) sidx[m][t] = t < cnt ? __ldg(a.idx + (int64_t)m * a.q + pos + t) : 0;
+            else sw[t] = t < cnt ? (a.mult ? (double)__ldg(a.mult + pos + t) : 1.0) : 0.0;
+        }
+        __syncthreads();
+        {
+            // all of the thread's factor loads in flight before the first use (the loop over
+            // elements with interleaved shared-memory stores serialised them on L2 latency)
+            constexpr int IT = (GB * RP / 2 + T - 1) / T;
+            double2 zr[IT], fr[IT][DO > 1 ? DO - 1 : 1];
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int e = tid + k * T;
+                const int t = min(e / (RP / 2), GB - 1), j = 2 * (e % (RP / 2));
+                zr[k] = __ldg(reinterpret_cast<const double2*>(a.fac + a.fac_off[0] + (int64_t)sidx[0][t] * RP + j));
+#pragma unroll
+                for (int m = 1; m < DO; ++m)
+                    fr[k][m - 1] = *reinterpret_cast<const double2*>(fac_m(m) + (int64_t)sidx[m][t] * RP + j);
+            }
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                const int e = tid + k * T;
+                if (e < GB * RP / 2) {
+                    const int t = e / (RP / 2), j = 2 * (e % (RP / 2));
+                    double2 z = zr[k];
+#pragma unroll
+                    for (int m = 1; m < DO; ++m) {
+                        z.x *= fr[k][m - 1].x;
+                        z.y *= fr[k][m - 1].y;
+                    }
+                    const double w = sw[t];  // 0 beyond cnt: padded observations contribute exactly zero
+                    if (t >= cnt) z.x = z.y = 0.0;
+                    *reinterpret_cast<double2*>(zs + t * ZP + j) = z;
+                    *reinterpret_cast<double2*>(zw + t * ZP + j) = make_double2(z.x * w, z.y * w);
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k0 = 4 * ks; k0 < GB; k0 += 4 * KS) {
+            const int t = k0 + kq;
+            double av[2], bv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) av[x] = zw[t * ZP + (2 * bi + x) * 8 + g];  // A(i, t) = w_t z_t(i)
+#pragma unroll
+            for (int y = 0; y < 2; ++y) bv[y] = zs[t * ZP + (2 * bj + y) * 8 + g];  // B(t, j) = z_t(j)
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int y = 0; y < 2; ++y) dmma_g(acc[x][y], av[x], bv[y]);
         }
         pos += cnt;
     }
@@ -309,8 +525,43 @@ void launch_dmma_do(const GramArgs& a, int grid, cudaStream_t s) {
     kern<<<grid, GT, smem, s>>>(a);
 }
 
+template <int RP, int DO>
+void launch_dmma2_do(const GramArgs& a, int grid, cudaStream_t s) {
+    using V = Gv2<RP>;
+    const size_t zbytes = sizeof(double) * (2 * GB * V::ZP + (V::KS > 1 ? V::KS * RP * RP : 0));
+    size_t sf_cap = 100 * 1024;  // staging only while two CTAs still fit an SM (one CTA per SM: no
+                                 // gather / DMMA overlap, measured 1.6x slower at config 3)
+    if (const char* e = std::getenv("CPHIFI_GRAM_SF_KB")) sf_cap = (size_t)std::atoi(e) * 1024;
+    const int64_t staged = DO > 1 ? a.fac_total - a.fac_off[1] : 0;  // modes 1.. (v2 stages no mode 0)
+    const bool sf = DO > 1 && zbytes + sizeof(double) * staged <= sf_cap;
+    const size_t smem = zbytes + (sf ? sizeof(double) * staged : 0);
+    auto kern = sf ? gram_build_dmma2_kernel<RP, DO, true> : gram_build_dmma2_kernel<RP, DO, false>;
+    CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, V::T, smem, s>>>(a);
+}
+
 template <int RP>
 void launch_build_rp(const GramArgs& a, int grid, cudaStream_t s) {
+    if constexpr (RP >= 16) {
+        // default for RP = 64 only: measured 82.8 -> 68.5 ms at config 4 (RP 64), 33.7 -> 35.4 ms
+        // at config 3 (RP 32, three gathered modes: v1 keeps more CTAs per SM); CPHIFI_GRAM_V2=1
+        // forces it for RP 16 / 32
+        bool v2 = RP >= 64 && reinterpret_cast<uintptr_t>(a.fac) % 16 == 0;  // 16-byte factor-row loads
+        if (const char* e = std::getenv("CPHIFI_GRAM_V2"))
+            if (std::atoi(e) != 0) v2 = reinterpret_cast<uintptr_t>(a.fac) % 16 == 0;
+        for (int m = 0; m < a.dother; ++m) v2 = v2 && a.fac_off[m] % 2 == 0;
+        if (const char* e = std::getenv("CPHIFI_GRAM_V2")) v2 = v2 && std::atoi(e) != 0;
+        if (v2) {
+            switch (a.dother) {
+                case 1: launch_dmma2_do<RP, 1>(a, grid, s); return;
+                case 2: launch_dmma2_do<RP, 2>(a, grid, s); return;
+                case 3: launch_dmma2_do<RP, 3>(a, grid, s); return;
+                case 4: launch_dmma2_do<RP, 4>(a, grid, s); return;
+                case 5: launch_dmma2_do<RP, 5>(a, grid, s); return;
+                default: throw_invalid("unaligned: tensor order above 6 is not supported");
+            }
+        }
+    }
     bool dm = RP >= 8;
     if (const char* e = std::getenv("CPHIFI_GRAM_DMMA")) dm = dm && std::atoi(e) != 0;
     if constexpr (RP >= 8) {

@@ -113,3 +113,29 @@ def test_gram_large_config_structure(cp, which, q):
     x = np.random.default_rng(1).normal(size=n * r)
     y_o = orc.unaligned_matvec_stream(cfg.shape, 0, hidx, model.factors, kern, cfg.lam, cfg.rho, x)
     assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12
+
+
+@pytest.mark.parametrize("shape,r,multiset", [([48, 20, 16, 6], 32, False), ([40, 64, 30], 64, True), ([30, 50, 9], 16, True)])
+def test_gram_build_v1_vs_v2(cp, monkeypatch, shape, r, multiset):
+    """Row-Gram build: the 2x2 register-blocked DMMA kernel (v2, default for RP >= 16) against the
+    one-tile-per-fragment kernel (v1) and the oracle — coalesced multiset plans included (entry
+    weights = multiplicities); split k-steps (RP 32 / 16) are summed in a fixed order."""
+    g = cp.Mt19937_64(11 + r)
+    factors = ri.random_model(shape, r, g)
+    rs = np.random.default_rng(r)
+    q = 60_000
+    idx = np.stack([rs.integers(0, n, q) for n in shape]).astype(np.int32)
+    vals = rs.normal(size=q)
+    mode = cp.RkhsMode(np.linspace(0, 1, shape[0]), 0.1, 1e-3)
+    kern = mode.kernel()
+    x = np.random.default_rng(5).normal(size=shape[0] * r)
+    ys = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("CPHIFI_GRAM_V2", v)
+        p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals, multiset=True), cp.KruskalModel(factors), 0,
+                                         mode, 1e-6)
+        p.set_operator("gram")
+        ys[v] = cp.unaligned_matvec(p, x)
+    y_o = orc.unaligned_matvec_stream(shape, 0, idx, factors, kern, 1e-3, 1e-6, x)
+    assert ri.rel(ys["1"], ys["0"]) < 1e-13
+    assert ri.rel(ys["1"], y_o) < 1e-12
