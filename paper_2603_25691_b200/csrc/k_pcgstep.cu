@@ -69,13 +69,31 @@ __device__ __forceinline__ double cta_total(double v, double* sh) {  // CTA sum,
     return t;
 }
 
+// JT consecutive doubles from shared memory, 16 bytes at a time when JT is even (the callers'
+// offsets are multiples of JT doubles from a 16-byte aligned row start)
+template <int JT>
+__device__ __forceinline__ void ld_vec(double (&v)[JT], const double* p) {
+    if constexpr (JT % 2 == 0) {
+#pragma unroll
+        for (int u = 0; u < JT; u += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(p + u);
+            v[u] = t.x;
+            v[u + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < JT; ++u) v[u] = p[u];
+    }
+}
+
 template <int JT>
 __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a) {
     constexpr int RP = JT * SW;
     constexpr int LDU = RP + 2;
     extern __shared__ __align__(16) double smem[];
     double* suv = smem;              // suv[m * LDU + j] = U_V(m, j)
-    double* sr = suv + RP * LDU;     // r~ block, then t, column-major [m][q]
+    double* suvt = suv + RP * LDU;   // suvt[m * LDU + j] = U_V(j, m)
+    double* sr = suvt + RP * LDU;    // r~ block, then t, column-major [m][q]
     __shared__ double sh[1 + SW];
     const int64_t n = a.n;
     const int r = a.r;
@@ -88,7 +106,11 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
     for (int k = 0; k < (RP * RP + ST - 1) / ST; ++k) {  // U_V staged once (used in step 3)
         const int e = threadIdx.x + k * ST;
         const int m = e % RP, j = e / RP;
-        if (e < RP * RP) suv[m * LDU + j] = (m < r && j < r) ? a.uv[m + (int64_t)r * j] : 0.0;
+        if (e < RP * RP) {
+            const double u = (m < r && j < r) ? a.uv[m + (int64_t)r * j] : 0.0;
+            suv[m * LDU + j] = u;
+            suvt[j * LDU + m] = u;
+        }
     }
     // Every phase loads all of a thread's JT elements of each operand into registers before any
     // store (the vectors may alias as far as the compiler knows: interleaved load / store chains
@@ -195,9 +217,10 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
 #pragma unroll
         for (int u = 0; u < JT; ++u) acc[u] = 0.0;
 #pragma unroll 4
-        for (int m = 0; m < r; ++m) {
+        for (int m = 0; m < r; ++m) {  // JT contiguous U_V(m, j0 ..) as 16-byte broadcast loads
             const double v = sr[m * SRB + q];
-            const double* um = suv + m * LDU + j0;
+            double um[JT];
+            ld_vec<JT>(um, suv + m * LDU + j0);
 #pragma unroll
             for (int u = 0; u < JT; ++u) acc[u] = fma(v, um[u], acc[u]);
         }
@@ -210,10 +233,12 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
 #pragma unroll
         for (int u = 0; u < JT; ++u) acc[u] = 0.0;
 #pragma unroll 4
-        for (int m = 0; m < r; ++m) {
+        for (int m = 0; m < r; ++m) {  // U_V(j0 .., m) from the transposed copy
             const double v = sr[m * SRB + q];
+            double um[JT];
+            ld_vec<JT>(um, suvt + m * LDU + j0);
 #pragma unroll
-            for (int u = 0; u < JT; ++u) acc[u] = fma(v, suv[(j0 + u) * LDU + m], acc[u]);
+            for (int u = 0; u < JT; ++u) acc[u] = fma(v, um[u], acc[u]);
         }
 #pragma unroll
         for (int u = 0; u < JT; ++u) {
@@ -258,7 +283,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
 template <int JT>
 size_t step_smem() {
     constexpr int RP = JT * SW;
-    return sizeof(double) * (RP * (RP + 2) + RP * SRB);
+    return sizeof(double) * (2 * RP * (RP + 2) + RP * SRB);
 }
 
 template <int JT>
