@@ -3,6 +3,7 @@
 // counts iterations and clears the condition after N.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o while_body while_body.cu -lcuda
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { std::printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
@@ -16,8 +17,8 @@ __global__ void ctl(int* it, int n, cudaGraphConditionalHandle h) {
 }
 __global__ void ctl_plain(int* it) { ++*it; }
 
-int main() {
-    const int N = 1000, n = 262144;
+int main(int argc, char** argv) {
+    const int N = 1000, n = argc > 1 ? atoi(argv[1]) : 262144;  // elements per work kernel
     double* v;
     int* it;
     CK(cudaMalloc(&v, n * 8));
@@ -92,8 +93,8 @@ int main() {
             CK(cudaEventElapsedTime(&ms, a, b));
             best3 = ms < best3 ? ms : best3;
         }
-        std::printf("K=%d kernels + ctl per iteration: WHILE %.2f us/iter, unrolled graph %.2f us/iter, stream %.2f us/iter\n",
-                    K, best * 1e3f / N, best2 * 1e3f / N, best3 * 1e3f / N);
+        std::printf("n=%d K=%d kernels + ctl per iteration: WHILE %.2f us/iter, unrolled graph %.2f us/iter, stream %.2f us/iter\n",
+                    n, K, best * 1e3f / N, best2 * 1e3f / N, best3 * 1e3f / N);
         cudaGraphExecDestroy(ex);
         cudaGraphExecDestroy(ex2);
         cudaGraphDestroy(g);
