@@ -1864,12 +1864,12 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             p->pcg_step.alloc(1 + pcg_step_fused_partials(n, ctx->num_sms));
             CPHIFI_CUDA(cudaMemsetAsync(p->pcg_step.get(), 0, sizeof(double), s));
         }
-        auto step_fused = [&](PcgCtl* c, cudaGraphConditionalHandle h) {
+        auto step_fused = [&](PcgCtl* c, cudaGraphConditionalHandle h, bool set_cond = true) {
             PcgStepArgs sa;
             sa.n = n; sa.r = (int)r;
             sa.uv = p->uv.get(); sa.dmat = p->dmat.get();
             sa.x = x; sa.res = res; sa.p = pv; sa.z = z; sa.ap = ap;
-            sa.st = st; sa.ctl = c; sa.h = h;
+            sa.st = st; sa.ctl = c; sa.h = h; sa.set_cond = set_cond ? 1 : 0;
             sa.barrier = reinterpret_cast<unsigned long long*>(p->pcg_step.get());
             sa.partial = p->pcg_step.get() + 1;
             pcg_step_fused(sa, ctx->num_sms, s);
@@ -2043,6 +2043,47 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                     }
                     done = true;
                 }
+            }
+            if (!done && fused_step && rel > cfg->tol && it < cfg->max_iter) {
+                // speculative host loop: iteration k + 1 is enqueued before iteration k's residual
+                // is read back (event + pinned snapshot), so the GPU never idles on the host round
+                // trip; the fused step of an iteration after the stopping one returns at entry
+                // (ctl->stop, set on device exactly where solvers.hpp:59-80 leaves the loop)
+                PcgCtl hc{};
+                hc.tol = cfg->tol;
+                hc.max_iter = cfg->max_iter;
+                hc.it = it;
+                h2d(ctl, &hc, sizeof(PcgCtl), s);
+                PcgState* snap = reinterpret_cast<PcgState*>(hs);  // two pinned slots
+                static_assert(2 * sizeof(PcgState) <= 64 * sizeof(double), "host scalar area");
+                cudaEvent_t ev[2] = {nullptr, nullptr};
+                CPHIFI_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+                CPHIFI_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+                struct EvGuard {
+                    cudaEvent_t* e;
+                    ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
+                } evg{ev};
+                auto enqueue = [&](int slot) {
+                    apply_a(pv, ap);
+                    step_fused(ctl, cudaGraphConditionalHandle{}, false);
+                    CPHIFI_CUDA(cudaMemcpyAsync(snap + slot, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+                    CPHIFI_CUDA(cudaEventRecord(ev[slot], s));
+                };
+                enqueue(0);
+                for (int k = 0;; ++k) {
+                    const int slot = k & 1;
+                    if (it + 1 < cfg->max_iter) enqueue(slot ^ 1);  // may be skipped on device
+                    CPHIFI_CUDA(cudaEventSynchronize(ev[slot]));
+                    const PcgState hs2 = snap[slot];
+                    ++matvecs;
+                    if (hs2.flag == 1) throw_runtime("pcg: non-finite value encountered");
+                    if (hs2.flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
+                    ++it;
+                    rel = hs2.rel;
+                    if (cfg->record_history) hist.push_back(rel);
+                    if (!(rel > cfg->tol) || it >= cfg->max_iter) break;
+                }
+                done = true;
             }
             while (!done && rel > cfg->tol && it < cfg->max_iter) {
                 if (fused_step) {  // step B runs inside the same launch (harmless after the last one)

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
     const int64_t nblk = (n + SRB - 1) / SRB;
     const int c = blockIdx.x, C = gridDim.x;
     PcgState* st = a.st;
+    // a speculatively enqueued iteration after the stopping one (host loop) does nothing
+    if (a.ctl && *(volatile const int*)&a.ctl->stop) return;
     const double rz_old = st->rz;
 #pragma unroll
     for (int k = 0; k < (RP * RP + ST - 1) / ST; ++k) {  // U_V staged once (used in step 3)
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
             if (cc->hist && it - 1 < cc->hist_cap) cc->hist[it - 1] = rel;
             if (flag != 0 || !(rel > cc->tol) || it >= cc->max_iter) {
                 cc->stop = 1;
-                cudaGraphSetConditional(a.h, 0);
+                if (a.set_cond) cudaGraphSetConditional(a.h, 0);
             }
         }
     }

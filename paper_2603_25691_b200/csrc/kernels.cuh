@@ -232,6 +232,7 @@ struct PcgStepArgs {
     PcgState* st = nullptr;
     PcgCtl* ctl = nullptr;         // loop control (graph body), or nullptr
     cudaGraphConditionalHandle h{};
+    int set_cond = 0;              // 1: inside the graph's WHILE body (clear `h` on stop)
     double* partial = nullptr;     // pcg_step_fused_partials(n, num_sms) doubles
     unsigned long long* barrier = nullptr;  // zero-initialised once per plan
 };

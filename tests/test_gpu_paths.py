@@ -206,8 +206,9 @@ def test_mttkrp_v3_odd_rank_many_outer(cp, monkeypatch):
         assert ri.rel(cp.mttkrp(t, cp.KruskalModel(factors), 0), bo) < 1e-12, (v1, v3)
 
 
-@pytest.mark.parametrize("fused,skipzero", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
-def test_pcg_large_n_step_variants(cp, monkeypatch, fused, skipzero):
+@pytest.mark.parametrize("fused,skipzero,graph", [("0", "0", "1"), ("1", "0", "1"), ("0", "1", "1"), ("1", "1", "1"),
+                                                  ("1", "1", "0"), ("0", "1", "0")])
+def test_pcg_large_n_step_variants(cp, monkeypatch, fused, skipzero, graph):
     """Large-n eigenbasis PCG: the one-launch cooperative vector step (k_pcgstep.cu) and the GEMMs
     that skip the clamped null space of K (mu_i = 0 rows / columns) against the oracle — each
     setting on a fresh plan (the captured solve graph bakes both in).  Residual history within
@@ -226,14 +227,15 @@ def test_pcg_large_n_step_variants(cp, monkeypatch, fused, skipzero):
     mode.set_eig(ek.u, ek.d)
     cfg = cp.PcgConfig(1e-9, 500, record_history=True)
     res = {}
-    for f, z in (("0", "0"), (fused, skipzero)):
+    for f, z, gr in (("0", "0", "1"), (fused, skipzero, graph)):
         monkeypatch.setenv("CPHIFI_PCG_FUSED", f)
         monkeypatch.setenv("CPHIFI_PCG_SKIPZERO", z)
+        monkeypatch.setenv("CPHIFI_PCG_GRAPH", gr)  # "0" + fused: the speculative host loop
         p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), 0, mode, 1e-6)
         p.set_operator("gram")
         rep = cp.SolveReport()
-        res[(f, z)] = (cp.solve_unaligned_pcg(p, cfg, rep), rep)
-    (w0, r0), (w1, r1) = res[("0", "0")], res[(fused, skipzero)]
+        res[(f, z, gr)] = (cp.solve_unaligned_pcg(p, cfg, rep), rep)
+    (w0, r0), (w1, r1) = res[("0", "0", "1")], res[(fused, skipzero, graph)]
     sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 0, kern, 1e-3, 1e-6)
     orep = orc.SolveReport()
     wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-9, 500), ek, orc.sym_eig(sub.v), report=orep)
