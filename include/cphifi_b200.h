@@ -219,6 +219,21 @@ int cphifi_gram_khatri_rao(cphifi_ctx ctx, int d, const int64_t* shape, int64_t 
 int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
                                    const double* v, const double* u_v,
                                    const double* sigma_v, double* w_out);
+/* ---- aligned baselines: the reference's comparison solvers on device --- */
+/* aligned_matvec (aligned.hpp:58-67): y = vec(diag(d_k) X V + lambda X), X n x r column-major. */
+int cphifi_aligned_matvec(cphifi_ctx ctx, int64_t n, int64_t r, const double* x, const double* d_k,
+                          const double* v, double lambda, double* y);
+/* solve_aligned_pcg (aligned.hpp:72-100): PCG (solvers.hpp:38-88) on (V kron D_K + lambda I)
+ * vec(Wbar) = vec(U_K' B) with the diagonal preconditioner diag(V) kron D_K + lambda I, then
+ * W = U_K Wbar.  warm_start (n x r) may be NULL (the reference rotates it: U_K' W0). */
+int cphifi_solve_aligned_pcg(cphifi_mode mode, int64_t r, const double* b, const double* v,
+                             const cphifi_pcg_config* cfg, cphifi_solve_report* report,
+                             const double* warm_start, double* w_out);
+/* solve_aligned_direct (aligned.hpp:28-37): the rn x rn system V kron K + lambda I materialised
+ * and Cholesky-solved (cuSOLVER potrf/potrs); std::invalid_argument when rn > direct_cap
+ * (reference default 6000), std::runtime_error when not positive definite. */
+int cphifi_solve_aligned_direct(cphifi_mode mode, int64_t r, const double* b, const double* v,
+                                int64_t direct_cap, double* w_out);
 /* Fused aligned update for mode k: MTTKRP + Gram + decoupled solve, one device pass,
  * eig(V) on device.  b_out / v_out may be NULL. */
 int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,

@@ -435,3 +435,55 @@ def solve_aligned_decoupled(b, ek: SymEig, ev: SymEig, lam, threads=1) -> np.nda
                                              _d(_f64(ev.u)), _d(np.ascontiguousarray(ev.d)),
                                              ctypes.c_double(lam), _d(b), _d(w), threads))
     return w
+
+
+def aligned_matvec(x, dk, v, lam) -> np.ndarray:
+    """aligned.hpp:58-67: vec(diag(d_K) (X V) + lambda X) with X = reshape(x, n, r) (column-major)."""
+    dk = np.asarray(dk, dtype=np.float64).reshape(-1)
+    v = np.asarray(v, dtype=np.float64)
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
+    n, r = dk.size, v.shape[0]
+    if x.size != n * r:
+        raise InvalidArgument("aligned_matvec: size mismatch")
+    xm = x.reshape((n, r), order="F")
+    return (dk[:, None] * (xm @ v) + lam * xm).reshape(-1, order="F")
+
+
+def solve_aligned_pcg(b, ek: SymEig, v, lam, cfg: PcgConfig, report: SolveReport | None = None,
+                      warm_start=None) -> np.ndarray:
+    """aligned.hpp:72-100: PCG on (V kron D_K + lambda I) vec(Wbar) = vec(U_K' B), diagonal
+    preconditioner 1 / (V(j,j) d_K(i) + lambda) (:83-89), warm start rotated (:92-96), W = U_K Wbar."""
+    b = np.asarray(b, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    n, r = b.shape
+    bbar = (ek.u.T @ b).reshape(-1, order="F")
+    dinv = (1.0 / (np.diag(v)[None, :] * ek.d[:, None] + lam)).reshape(-1, order="F")
+    x0 = None
+    if warm_start is not None:
+        x0 = (ek.u.T @ np.asarray(warm_start, dtype=np.float64)).reshape(-1, order="F")
+    wbar = pcg(lambda x: aligned_matvec(x, ek.d, v, lam), lambda x: dinv * x, bbar, cfg, report, x0)
+    return ek.u @ wbar.reshape((n, r), order="F")
+
+
+def solve_aligned_direct(b, kernel, v, lam, direct_cap=6000) -> np.ndarray:
+    """aligned.hpp:28-37: (V kron K + lambda I) vec(W) = vec(B) by Cholesky (solvers.hpp:91-96)."""
+    b = np.asarray(b, dtype=np.float64)
+    n, r = b.shape
+    if n * r > direct_cap:
+        raise InvalidArgument("solve_aligned_direct: rn exceeds memory cap")
+    sys_ = np.kron(np.asarray(v, dtype=np.float64), np.asarray(kernel, dtype=np.float64))
+    sys_[np.diag_indices_from(sys_)] += lam
+    try:
+        c = np.linalg.cholesky(sys_)
+    except np.linalg.LinAlgError:
+        raise RuntimeFailure("cholesky_solve: matrix is not positive definite")
+    w = np.linalg.solve(c.T, np.linalg.solve(c, b.reshape(-1, order="F")))
+    return w.reshape((n, r), order="F")
+
+
+def aligned_residual_dense(b, kernel, v, lam, w) -> float:
+    """aligned.hpp:104-108: ||K W V + lambda W - B|| / ||B||."""
+    b = np.asarray(b, dtype=np.float64)
+    res = kernel @ w @ v + lam * w - b
+    bn = float(np.linalg.norm(b))
+    return float(np.linalg.norm(res)) / bn if bn != 0.0 else float(np.linalg.norm(res))

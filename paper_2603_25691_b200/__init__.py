@@ -36,6 +36,7 @@ __all__ = [
     "read_observations", "write_observations", "update_finite_mode_unaligned", "unaligned_relative_error",
     "UnalignedAlsState", "FitIteration", "AlignedAlsState", "update_finite_mode_aligned",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
+    "aligned_matvec", "solve_aligned_pcg", "solve_aligned_direct",
     "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
 
@@ -660,6 +661,7 @@ class AlignedSubproblem:
     b: np.ndarray
     v: np.ndarray
     mode: RkhsMode
+    direct_cap: int = 6000  # guard on rn for the materialised path (aligned.hpp:20)
 
     def n(self):
         return self.b.shape[0]
@@ -681,6 +683,55 @@ def solve_aligned_decoupled(p: AlignedSubproblem, v_eig: SymEig | None = None) -
     else:
         call("cphifi_solve_aligned_decoupled", p.mode.handle, r, _dp(b), _dp(v), c_double_p(), c_double_p(),
              _dp(w))
+    return w
+
+
+def aligned_matvec(x, d_k, v, lam, ctx: Context | None = None) -> np.ndarray:
+    """aligned.hpp:58-67 on device: vec(diag(d_k) X V + lambda X), X = reshape(x, n, r)."""
+    ctx = ctx or default_context()
+    d_k = np.ascontiguousarray(d_k, dtype=np.float64).reshape(-1)
+    v = _f64(v)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    n, r = d_k.size, v.shape[0]
+    if x.size != n * r:
+        raise CphifiInvalidArgument("aligned_matvec: size mismatch")
+    y = np.zeros(n * r)
+    call("cphifi_aligned_matvec", ctx.handle, n, r, _dp(x), _dp(d_k), _dp(v), float(lam), _dp(y))
+    return y
+
+
+def solve_aligned_pcg(p: AlignedSubproblem, cfg: PcgConfig | None = None, report: SolveReport | None = None,
+                      warm_start=None) -> np.ndarray:
+    """aligned.hpp:72-100 on device (PCG on the eigen-rotated system, diagonal preconditioner)."""
+    cfg = cfg or PcgConfig()
+    b = _f64(p.b)
+    n, r = b.shape
+    ccfg = _capi.PcgConfigC(cfg.tol, int(cfg.max_iter), int(bool(cfg.record_history)))
+    cap = int(cfg.max_iter) + 2
+    hist = np.zeros(cap)
+    rep = _capi.SolveReportC()
+    rep.residual_history = _dp(hist)
+    rep.history_capacity = cap
+    w = np.zeros((n, r), order="F")
+    ws = None if warm_start is None else _f64(warm_start)
+    call("cphifi_solve_aligned_pcg", p.mode.handle, r, _dp(b), _dp(_f64(p.v)), ctypes.byref(ccfg), ctypes.byref(rep),
+         _dp(ws) if ws is not None else c_double_p(), _dp(w))
+    if report is not None:
+        report.iterations = rep.iterations
+        report.relative_residual = rep.relative_residual
+        report.wall_time_s = rep.wall_time_s
+        report.converged = bool(rep.converged)
+        report.residual_history = list(hist[: rep.history_len]) if cfg.record_history else []
+        report.matvecs = rep.matvecs
+    return w
+
+
+def solve_aligned_direct(p: AlignedSubproblem) -> np.ndarray:
+    """aligned.hpp:28-37 on device: V kron K + lambda I materialised, Cholesky (cuSOLVER)."""
+    b = _f64(p.b)
+    n, r = b.shape
+    w = np.zeros((n, r), order="F")
+    call("cphifi_solve_aligned_direct", p.mode.handle, r, _dp(b), _dp(_f64(p.v)), int(p.direct_cap), _dp(w))
     return w
 
 

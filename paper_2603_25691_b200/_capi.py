@@ -132,6 +132,13 @@ _SIGS = [
      [_H, ctypes.c_int, c_int64_p, ctypes.c_int64, ctypes.POINTER(c_double_p), ctypes.c_int, c_double_p]),
     ("cphifi_solve_aligned_decoupled", ctypes.c_int,
      [_H, ctypes.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
+    ("cphifi_aligned_matvec", ctypes.c_int,
+     [_H, ctypes.c_int64, ctypes.c_int64, c_double_p, c_double_p, c_double_p, ctypes.c_double, c_double_p]),
+    ("cphifi_solve_aligned_pcg", ctypes.c_int,
+     [_H, ctypes.c_int64, c_double_p, c_double_p, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC),
+      c_double_p, c_double_p]),
+    ("cphifi_solve_aligned_direct", ctypes.c_int,
+     [_H, ctypes.c_int64, c_double_p, c_double_p, ctypes.c_int64, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,
      [_H, _H, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(c_double_p), c_double_p, c_double_p, c_double_p]),
     ("cphifi_obs_file_info", ctypes.c_int,

@@ -2294,6 +2294,164 @@ int cphifi_solve_aligned_decoupled(cphifi_mode mode, int64_t r, const double* b,
     });
 }
 
+// ---- aligned baselines -----------------------------------------------------
+int cphifi_aligned_matvec(cphifi_ctx ctx, int64_t n, int64_t r, const double* x, const double* d_k, const double* v,
+                          double lambda, double* y) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(x, "x");
+        need(d_k, "d_k");
+        need(v, "v");
+        need(y, "y");
+        if (n < 0 || r < 0) throw_invalid("aligned_matvec: size mismatch");
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> dx(n * r), dd(n), dv(r * r), dy(n * r);
+        h2d(dx.get(), x, sizeof(double) * n * r, s);
+        h2d(dd.get(), d_k, sizeof(double) * n, s);
+        h2d(dv.get(), v, sizeof(double) * r * r, s);
+        aligned_matvec_dev(dx.get(), dd.get(), dv.get(), n, r, lambda, dy.get(), s);
+        d2h_sync(y, dy.get(), sizeof(double) * n * r, s);
+    });
+}
+
+// solve_aligned_pcg (aligned.hpp:72-100) with the pcg recurrence of solvers.hpp:38-88 (the same
+// device vector kernels as the unaligned host loop), host-driven
+int cphifi_solve_aligned_pcg(cphifi_mode mode, int64_t r, const double* b, const double* v,
+                             const cphifi_pcg_config* cfg, cphifi_solve_report* report, const double* warm_start,
+                             double* w_out) {
+    return guard([&] {
+        need(mode, "mode");
+        need(b, "b");
+        need(v, "v");
+        need(cfg, "cfg");
+        need(w_out, "w_out");
+        if (r < 1) throw_invalid("solve_aligned_pcg: rank must be positive");
+        const auto t0 = std::chrono::steady_clock::now();
+        cphifi_ctx ctx = mode->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        mode_eig_once(mode);  // ek = mode->eig() (kernel.hpp:77-83)
+        const int64_t n = mode->n, nr = n * r;
+        DevBuf<double> db(nr), dv(r * r), bbar(nr), x(nr), res(nr), z(nr), pv(nr), ap(nr), dinv(nr);
+        DevBuf<double> aux(RED_PARTIALS + (sizeof(PcgState) + 7) / 8);
+        double* partial = aux.get();
+        PcgState* st = reinterpret_cast<PcgState*>(partial + RED_PARTIALS);
+        CPHIFI_CUDA(cudaMemsetAsync(aux.get(), 0, sizeof(double) * aux.n, s));
+        h2d(db.get(), b, sizeof(double) * nr, s);
+        h2d(dv.get(), v, sizeof(double) * r * r, s);
+        auto rot = [&](bool transpose, const double* in, double* out) {  // out = U_K' in  /  U_K in
+            GemmArgs g;
+            g.m = n; g.n = r; g.k = n;
+            g.a = mode->u.get();
+            if (transpose) { g.a_rs = n; g.a_cs = 1; } else { g.a_rs = 1; g.a_cs = n; }
+            g.b = in; g.b_rs = 1; g.b_cs = n;
+            g.c = out; g.c_rs = 1; g.c_cs = n;
+            gemm(g, ctx->num_sms, s);
+        };
+        rot(true, db.get(), bbar.get());  // bbar = U_K' B
+        aligned_dinv(mode->mu.get(), dv.get(), n, r, mode->lambda, dinv.get(), s);
+        auto apply_a = [&](const double* in, double* out) {
+            aligned_matvec_dev(in, mode->mu.get(), dv.get(), n, r, mode->lambda, out, s);
+        };
+        auto apply_m = [&](const double* in, double* out) { hadamard(dinv.get(), in, nr, out, s); };
+        if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
+        double* hs = ctx->host_scalars;
+        dot_to(bbar.get(), bbar.get(), nr, partial, &st->bnorm, s);
+        d2h_sync(hs, &st->bnorm, sizeof(double), s);
+        const double bnorm = std::sqrt(hs[0]);
+        std::vector<double> hist;
+        cphifi_solve_report rep{};
+        int it = 0, matvecs = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {  // solvers.hpp:49-53
+            CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
+            rep.converged = 1;
+        } else {
+            CPHIFI_CUDA(cudaMemcpyAsync(&st->bnorm, &bnorm, sizeof(double), cudaMemcpyHostToDevice, s));
+            if (warm_start) {  // x0 = vec(U_K' W0)  (aligned.hpp:92-96)
+                h2d(ap.get(), warm_start, sizeof(double) * nr, s);
+                rot(true, ap.get(), x.get());
+                apply_a(x.get(), ap.get());
+                ++matvecs;
+                axpby(res.get(), bbar.get(), 1.0, ap.get(), -1.0, nr, s);
+            } else {
+                CPHIFI_CUDA(cudaMemsetAsync(x.get(), 0, sizeof(double) * nr, s));
+                CPHIFI_CUDA(cudaMemcpyAsync(res.get(), bbar.get(), sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
+            }
+            apply_m(res.get(), z.get());
+            pcg_init(res.get(), z.get(), pv.get(), nr, st, partial, s);
+            PcgState hst;
+            d2h_sync(&hst, st, sizeof(PcgState), s);
+            rel = hst.rel;
+            if (cfg->record_history) hist.push_back(rel);
+            while (rel > cfg->tol && it < cfg->max_iter) {
+                apply_a(pv.get(), ap.get());
+                ++matvecs;
+                pcg_step_a(x.get(), res.get(), pv.get(), ap.get(), nr, st, partial, s);
+                d2h_sync(&hst, st, sizeof(PcgState), s);
+                if (hst.flag == 1) throw_runtime("pcg: non-finite value encountered");
+                if (hst.flag == 2) throw_runtime("pcg: operator not positive definite (p'Ap <= 0)");
+                ++it;
+                rel = hst.rel;
+                if (cfg->record_history) hist.push_back(rel);
+                if (rel <= cfg->tol) break;
+                apply_m(res.get(), z.get());
+                pcg_step_b(res.get(), z.get(), pv.get(), nr, st, partial, s);
+            }
+            rep.iterations = it;
+            rep.relative_residual = rel;
+            rep.converged = rel <= cfg->tol;
+        }
+        rot(false, x.get(), ap.get());  // W = U_K Wbar
+        d2h_sync(w_out, ap.get(), sizeof(double) * nr, s);
+        rep.matvecs = matvecs;
+        rep.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (report) {
+            double* hbuf = report->residual_history;
+            const int hcap = report->history_capacity;
+            rep.residual_history = hbuf;
+            rep.history_capacity = hcap;
+            rep.history_len = (int32_t)hist.size();
+            if (hbuf) std::memcpy(hbuf, hist.data(), sizeof(double) * std::min<size_t>(hist.size(), (size_t)std::max(hcap, 0)));
+            *report = rep;
+        }
+    });
+}
+
+// solve_aligned_direct (aligned.hpp:28-37): Cholesky of the materialised Kronecker system
+int cphifi_solve_aligned_direct(cphifi_mode mode, int64_t r, const double* b, const double* v, int64_t direct_cap,
+                                double* w_out) {
+    return guard([&] {
+        need(mode, "mode");
+        need(b, "b");
+        need(v, "v");
+        need(w_out, "w_out");
+        if (r < 1) throw_invalid("solve_aligned_direct: rank must be positive");
+        const int64_t n = mode->n, rn = n * r;
+        if (rn > direct_cap) throw_invalid("solve_aligned_direct: rn exceeds memory cap");
+        cphifi_ctx ctx = mode->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> dv(r * r), sys((size_t)rn * rn), rhs(rn);
+        h2d(dv.get(), v, sizeof(double) * r * r, s);
+        h2d(rhs.get(), b, sizeof(double) * rn, s);
+        kron_system(dv.get(), mode->kernel.get(), n, r, mode->lambda, sys.get(), s);
+        int lwork = 0;
+        CPHIFI_SOLVER(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, (int)rn, sys.get(), (int)rn, &lwork));
+        DevBuf<double> work(std::max(lwork, 1));
+        DevBuf<int> info(1);
+        CPHIFI_SOLVER(cusolverDnDpotrf(ctx->solver, CUBLAS_FILL_MODE_LOWER, (int)rn, sys.get(), (int)rn, work.get(), lwork,
+                                       info.get()));
+        int hinfo = 0;
+        d2h_sync(&hinfo, info.get(), sizeof(int), s);
+        if (hinfo != 0) throw_runtime("cholesky_solve: matrix is not positive definite");
+        CPHIFI_SOLVER(cusolverDnDpotrs(ctx->solver, CUBLAS_FILL_MODE_LOWER, (int)rn, 1, sys.get(), (int)rn, rhs.get(),
+                                       (int)rn, info.get()));
+        d2h_sync(w_out, rhs.get(), sizeof(double) * rn, s);
+    });
+}
+
 int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, const double* const* factors,
                                int iters, double* w_out, double* ms_out) {
     return guard([&] {

@@ -259,6 +259,15 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
               cudaStream_t s);
 // dst <- src (n doubles), a kernel copy when 16-byte aligned (mapped host memory allowed)
 void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s);
+// ---- aligned baselines (k_aligned.cu) ------------------------------------
+void aligned_matvec_dev(const double* x, const double* dk, const double* v, int64_t n, int64_t r, double lambda,
+                        double* y, cudaStream_t s);
+void aligned_dinv(const double* dk, const double* v, int64_t n, int64_t r, double lambda, double* dinv,
+                  cudaStream_t s);
+void hadamard(const double* a, const double* b, int64_t cnt, double* out, cudaStream_t s);
+void kron_system(const double* v, const double* kmat, int64_t n, int64_t r, double lambda, double* sys,
+                 cudaStream_t s);
+
 // Grid of the deterministic vector reductions (dot_to / PCG steps); their `partial` scratch needs
 // RED_PARTIALS doubles (RED_GRID partials + the ticket word).
 constexpr int RED_GRID = 296;
