@@ -339,10 +339,18 @@ void ensure_gram(cphifi_unaligned p) {
     const size_t rp2 = (size_t)p->rp * p->rp;
     p->gram.alloc((size_t)p->n * rp2);
     CPHIFI_CUDA(cudaMemsetAsync(p->gram.get(), 0, sizeof(double) * p->n * rp2, s));
-    // The build's own row-aligned partition, ~4 CTAs per SM: each CTA alternates a gather phase
-    // and a DMMA phase around barriers, so one CTA per SM (the stream plan's grid) left it
-    // latency-bound.
-    const int cmax = 4 * ctx->num_sms;
+    // The build's own row-aligned partition, sized from the chosen kernel's occupancy (each CTA
+    // alternates a gather phase and a DMMA phase around barriers, so several per SM overlap them).  Measured (profiles/prof_gram_grid.sh): config 3 (v1) 27.4 ms at 4 CTAs/SM
+    // -> 24.7 at 8; config 4 (v2, 2 resident) 68.3 at 4 -> 61.8 at 2 (no partial second wave).
+    GramArgs probe;
+    probe.rp = p->rp;
+    probe.dother = o->d - 1;
+    probe.fac = p->fac.get();
+    for (int m = 0; m < o->d - 1; ++m) probe.fac_off[m] = p->fac_off[m];
+    probe.fac_total = (int64_t)p->fac.n;
+    int per_sm = gram_build_occupancy(probe);
+    if (const char* e = std::getenv("CPHIFI_GRAM_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+    const int cmax = per_sm * ctx->num_sms;
     PartitionPlan plan;
     {
         std::vector<int64_t> rp_host(p->n + 1);

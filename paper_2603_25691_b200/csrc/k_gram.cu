@@ -513,6 +513,16 @@ __global__ void gram_apply_kernel(const double* __restrict__ g, const double* __
     yhat[e] = s;
 }
 
+// grid == -1: partition-density query (CTAs per SM for the kernel gram_build would launch,
+// from its occupancy), answered through g_occ instead of launching
+thread_local int g_occ = 0;
+template <class K>
+bool occ_query(K kern, int grid, int threads, size_t smem) {
+    if (grid != -1) return false;
+    CPHIFI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ, kern, threads, smem));
+    return true;
+}
+
 template <int RP, int DO>
 void launch_dmma_do(const GramArgs& a, int grid, cudaStream_t s) {
     const size_t zbytes = sizeof(double) * 2 * GB * (RP + 4);
@@ -522,6 +532,10 @@ void launch_dmma_do(const GramArgs& a, int grid, cudaStream_t s) {
     const size_t smem = zbytes + (sf ? sizeof(double) * a.fac_total : 0);
     auto kern = sf ? gram_build_dmma_kernel<RP, DO, true> : gram_build_dmma_kernel<RP, DO, false>;
     CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (occ_query(kern, grid, GT, smem)) {
+        g_occ *= 2;  // v1: two waves' worth of CTAs — the finer row partition balanced better (config 3
+        return;      // 27.4 -> 24.7 ms), while v2's one wave avoids a partial second wave (config 4)
+    }
     kern<<<grid, GT, smem, s>>>(a);
 }
 
@@ -537,6 +551,7 @@ void launch_dmma2_do(const GramArgs& a, int grid, cudaStream_t s) {
     const size_t smem = zbytes + (sf ? sizeof(double) * staged : 0);
     auto kern = sf ? gram_build_dmma2_kernel<RP, DO, true> : gram_build_dmma2_kernel<RP, DO, false>;
     CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (occ_query(kern, grid, V::T, smem)) return;
     kern<<<grid, V::T, smem, s>>>(a);
 }
 
@@ -576,6 +591,10 @@ void launch_build_rp(const GramArgs& a, int grid, cudaStream_t s) {
             }
         }
     }
+    if (grid == -1) {  // FMA build: the query reports the default partition density
+        g_occ = 4;
+        return;
+    }
     switch (a.dother) {
         case 1: gram_build_kernel<RP, 1><<<grid, GT, 0, s>>>(a); break;
         case 2: gram_build_kernel<RP, 2><<<grid, GT, 0, s>>>(a); break;
@@ -587,6 +606,19 @@ void launch_build_rp(const GramArgs& a, int grid, cudaStream_t s) {
 }
 
 }  // namespace
+
+int gram_build_occupancy(const GramArgs& a) {
+    g_occ = 0;
+    switch (a.rp) {
+        case 4: launch_build_rp<4>(a, -1, nullptr); break;
+        case 8: launch_build_rp<8>(a, -1, nullptr); break;
+        case 16: launch_build_rp<16>(a, -1, nullptr); break;
+        case 32: launch_build_rp<32>(a, -1, nullptr); break;
+        case 64: launch_build_rp<64>(a, -1, nullptr); break;
+        default: throw_invalid("gram operator: padded rank above 64 is not supported");
+    }
+    return std::max(g_occ, 1);
+}
 
 void gram_build(const GramArgs& a, int grid, cudaStream_t s) {
     switch (a.rp) {

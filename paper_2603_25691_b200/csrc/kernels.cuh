@@ -194,6 +194,7 @@ struct GramArgs {
     double* g = nullptr;       // n x rp x rp
 };
 void gram_build(const GramArgs& a, int grid, cudaStream_t s);
+int gram_build_occupancy(const GramArgs& a);  // partition CTAs per SM for the build gram_build picks
 void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
                 cudaStream_t s);
 
