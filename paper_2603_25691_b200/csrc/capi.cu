@@ -552,7 +552,15 @@ bool pcg_eigbasis(cphifi_unaligned p) {
     return on && p->mode;
 }
 
-void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
+// leading rows / columns of the eigenbasis that the large-n operator skips (mode_nzero; 0 when off)
+int64_t rot_null_rows(cphifi_unaligned p) {
+    int64_t z = 0;
+    if (const char* e = std::getenv("CPHIFI_PCG_SKIPZERO"); !e || std::atoi(e) != 0) z = mode_nzero(p->mode);
+    return z >= p->n ? 0 : z;
+}
+
+// null_rows = false: the caller supplies rows i < z of y~ (= rho x~) itself (the fused PCG step)
+void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows = true) {
     need_mode(p);
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
@@ -575,18 +583,26 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
         return;
     }
     // rows / columns of the clamped null space (mu_i = 0) drop out of both GEMMs (mode_nzero)
-    int64_t z = 0;
-    if (const char* e = std::getenv("CPHIFI_PCG_SKIPZERO"); !e || std::atoi(e) != 0) z = mode_nzero(p->mode);
-    if (z >= n) z = 0;
+    const int64_t z = rot_null_rows(p);
     GemmArgs g;  // Xhat = U diag(mu) x~  -> row-major padded copy for the gather
     g.m = n; g.n = r; g.k = n - z;
     g.a = mode_um(p->mode) + z * n; g.a_rs = 1; g.a_cs = n;
     g.b = xt + z; g.b_rs = 1; g.b_cs = n;
     g.c2 = p->xhat_rm.get(); g.ld2 = p->rp;
-    gemm(g, ctx->num_sms, ctx->stream);
     const double* gr = p->op == 1 ? p->gram.get() : nullptr;
-    if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), n, p->rp, p->yhat_rm.get(), ctx->stream);
-    else launch_phase_b(p, fused_args(p, PH_B));
+    bool fuse_gram = gr && p->rp <= 64 && gemm_tma_ok(g);  // split-K reduction + row-Gram apply in one launch
+    if (const char* e = std::getenv("CPHIFI_GRAM_EPI")) fuse_gram = fuse_gram && std::atoi(e) != 0;
+    if (fuse_gram) {
+        g.epi = EPI_GRAM; g.c2 = nullptr;
+        g.gram = gr; g.row_ptr = p->obs->row_ptr.get(); g.rp = p->rp; g.yhat = p->yhat_rm.get();
+    }
+    gemm(g, ctx->num_sms, ctx->stream);
+    if (fuse_gram) {
+    } else if (gr) {
+        gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), n, p->rp, p->yhat_rm.get(), ctx->stream);
+    } else {
+        launch_phase_b(p, fused_args(p, PH_B));
+    }
     allreduce_yhat(p);
     GemmArgs h;  // y~ = mu o (U' Yhat + lambda x~) + rho x~   (rows i >= z)
     h.m = n - z; h.n = r; h.k = n;
@@ -596,7 +612,7 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt) {
     h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get() + z; h.e1 = xt + z; h.ld_e = n;
     h.beta1 = p->mode->lambda; h.beta2 = p->rho;
     gemm(h, ctx->num_sms, ctx->stream);
-    if (z > 0) scale_row_block(yt, xt, z, n, r, p->rho, ctx->stream);  // y~ = rho x~  (rows i < z)
+    if (z > 0 && null_rows) scale_row_block(yt, xt, z, n, r, p->rho, ctx->stream);  // y~ = rho x~  (rows i < z)
 }
 
 void precond_rot(cphifi_unaligned p, const double* rt, double* zt) {
@@ -1878,6 +1894,8 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             sa.uv = p->uv.get(); sa.dmat = p->dmat.get();
             sa.x = x; sa.res = res; sa.p = pv; sa.z = z; sa.ap = ap;
             sa.st = st; sa.ctl = c; sa.h = h; sa.set_cond = set_cond ? 1 : 0;
+            sa.null_rows = rot_null_rows(p);  // Ap rows i < z = rho p: matvec_rot leaves them to the step
+            sa.rho = p->rho;
             sa.barrier = reinterpret_cast<unsigned long long*>(p->pcg_step.get());
             sa.partial = p->pcg_step.get() + 1;
             pcg_step_fused(sa, ctx->num_sms, s);
@@ -1906,11 +1924,12 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                     pcg_loopctl(st, ctl, h, s);
                 },
                 [&](cudaGraphConditionalHandle h) {
-                    apply_a(pv, ap);
                     if (fused_step) {
+                        matvec_rot(p, pv, ap, false);
                         step_fused(ctl, h);
                         return;
                     }
+                    apply_a(pv, ap);
                     pcg_step_a_ctl(x, res, pv, ap, nr, st, partial, ctl, h, s);
                     apply_m(res, z);
                     pcg_step_b(res, z, pv, nr, st, partial, s);
@@ -2020,7 +2039,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 // pcg_ctl clears the condition; no host round trip per iteration
                 if (ensure_pcg_graph(p, rot, [&](cudaGraphConditionalHandle h) {
                         if (fused_step) {
-                            apply_a(pv, ap);
+                            matvec_rot(p, pv, ap, false);
                             step_fused(ctl, h);
                             return;
                         }
@@ -2072,7 +2091,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                     ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
                 } evg{ev};
                 auto enqueue = [&](int slot) {
-                    apply_a(pv, ap);
+                    matvec_rot(p, pv, ap, false);
                     step_fused(ctl, cudaGraphConditionalHandle{}, false);
                     CPHIFI_CUDA(cudaMemcpyAsync(snap + slot, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
                     CPHIFI_CUDA(cudaEventRecord(ev[slot], s));
@@ -2095,7 +2114,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             }
             while (!done && rel > cfg->tol && it < cfg->max_iter) {
                 if (fused_step) {  // step B runs inside the same launch (harmless after the last one)
-                    apply_a(pv, ap);
+                    matvec_rot(p, pv, ap, false);
                     step_fused(nullptr, cudaGraphConditionalHandle{});
                 } else {
                     body_a();

@@ -1121,6 +1121,49 @@ bool gemm_tma_ok(const GemmArgs& g) {
            g.k < (1LL << 31) && g.m < (1LL << 31);
 }
 
+// EPI_GRAM: split-K reduction of Xhat rows (partials summed in p order, as reduce_epi_kernel) fused
+// with the row-Gram apply Yhat(i, a) = sum_b G_i(b, a) Xhat(i, b) (b ascending, as gram_apply):
+// bit-identical to the two launches it replaces.  GR rows per CTA, RP threads per row.
+template <int RP>
+__global__ void __launch_bounds__(RP * 2) reduce_gram_kernel(const double* __restrict__ work, int P, int64_t m,
+                                                             int64_t ncols, const GemmArgs g) {
+    constexpr int GR = 2;
+    __shared__ double xs[GR][RP];
+    const int rr = threadIdx.x / RP, a = threadIdx.x % RP;
+    const int64_t i = (int64_t)blockIdx.x * GR + rr;
+    double x = 0.0;
+    if (i < m && a < ncols)
+        for (int p = 0; p < P; ++p) x += work[(int64_t)p * m * ncols + i + m * a];
+    xs[rr][a] = x;
+    __syncthreads();
+    if (i >= m || g.row_ptr[i + 1] == g.row_ptr[i]) return;  // rows without observations stay zero
+    const double* gi = g.gram + i * RP * RP + a;
+    constexpr int U = RP < 16 ? RP : 16;
+    double s = 0.0;
+#pragma unroll
+    for (int b0 = 0; b0 < RP; b0 += U) {
+        double gv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) gv[u] = __ldcs(gi + (b0 + u) * RP);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s = fma(gv[u], xs[rr][b0 + u], s);
+    }
+    g.yhat[i * RP + a] = s;
+}
+
+void launch_reduce_gram(const double* work, int P, int64_t m, int64_t ncols, const GemmArgs& g, cudaStream_t s) {
+    const unsigned grid = (unsigned)((m + 1) / 2);
+    switch (g.rp) {
+        case 4: reduce_gram_kernel<4><<<grid, 8, 0, s>>>(work, P, m, ncols, g); break;
+        case 8: reduce_gram_kernel<8><<<grid, 16, 0, s>>>(work, P, m, ncols, g); break;
+        case 16: reduce_gram_kernel<16><<<grid, 32, 0, s>>>(work, P, m, ncols, g); break;
+        case 32: reduce_gram_kernel<32><<<grid, 64, 0, s>>>(work, P, m, ncols, g); break;
+        case 64: reduce_gram_kernel<64><<<grid, 128, 0, s>>>(work, P, m, ncols, g); break;
+        default: throw_invalid("gemm: EPI_GRAM needs a padded rank in [4, 64]");
+    }
+    CPHIFI_CHECK_LAUNCH();
+}
+
 template <int BN>
 void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
     static thread_local GrowScratch work;
@@ -1151,6 +1194,10 @@ void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
     constexpr int WC = BN >= 16 ? 16 : BN;
     if (brow) launch_v3<BN, 32, WC, true>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
     else launch_v3<BN, 32, WC, false>(a, tm_a, tm_b, mt, P, nt, chunks, chunks, wout, work.get(), s);
+    if (g.epi == EPI_GRAM) {
+        launch_reduce_gram(work.get(), (int)P, g.m, g.n, g, s);
+        return;
+    }
     const int64_t cnt = g.m * (g.c2 ? std::max(g.n, g.ld2) : g.n);
     reduce_epi_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(work.get(), (int)P, g.m,
                                                                                                   g.n, g);
@@ -1162,6 +1209,7 @@ void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     if (g.k <= 0) {
         // empty contraction: run a zero-K GEMM (epilogue only) through the S=1 path
     }
+    if (g.epi == EPI_GRAM && !(g.k > 0 && gemm_tma_ok(g))) throw_invalid("gemm: EPI_GRAM needs the tensor-map path");
     if (g.k > 0 && gemm_tma_ok(g)) {
         if (g.n <= 8) gemm_tma_t<8>(g, num_sms, s);
         else if (g.n <= 16) gemm_tma_t<16>(g, num_sms, s);

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
         for (int u = 0; u < JT; ++u) {
             const bool ok = i < n && j0 + u < r;
             pv[u] = ok ? pp[i + n * (j0 + u)] : 0.0;
-            av[u] = ok ? ap[i + n * (j0 + u)] : 0.0;
+            av[u] = ok && i >= a.null_rows ? ap[i + n * (j0 + u)] : a.rho * pv[u];
         }
 #pragma unroll
         for (int u = 0; u < JT; ++u) t = fma(pv[u], av[u], t);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
             const bool ok = i < n && j0 + u < r;
             const int64_t e = i + n * (j0 + u);
             pv[u] = ok ? pp[e] : 0.0;
-            av[u] = ok ? ap[e] : 0.0;
+            av[u] = ok && i >= a.null_rows ? ap[e] : a.rho * pv[u];
             xv[u] = ok ? a.x[e] : 0.0;
             rv[u] = ok ? a.res[e] : 0.0;
         }

@@ -13,7 +13,9 @@ enum EpiOp : int {
     EPI_AXPY2 = 1,    // C = (AB + beta1*E1) + beta2*E2     (unaligned.hpp:112-114 order)
     EPI_HADAMARD = 2, // C = AB .* E1                        (unaligned.hpp:137)
     EPI_SCALE_DIV = 3, // C = AB / (e_row[i]*e_col[j] + beta1) with zero-denominator flag
-    EPI_ROWSCALE = 4   // C = e_row[i] * (AB + beta1*E1) + beta2*E1   (E1 may be null: 0)
+    EPI_ROWSCALE = 4,  // C = e_row[i] * (AB + beta1*E1) + beta2*E1   (E1 may be null: 0)
+    EPI_GRAM = 5       // Yhat(i,:) = G_i (AB)(i,:) for rows with observations (row-Gram operator;
+                       // tensor-map GEMM path only: the split-K reduction and the apply in one kernel)
 };
 
 struct GemmArgs {
@@ -27,8 +29,14 @@ struct GemmArgs {
     double beta1 = 0.0, beta2 = 0.0;
     const double* e_row = nullptr; const double* e_col = nullptr;
     int* flag = nullptr;  // set to 1 if EPI_SCALE_DIV meets a zero denominator
+    // EPI_GRAM: n x rp x rp row Grams, CSR row pointers, Yhat (n x rp row-major) out; rp >= n cols
+    const double* gram = nullptr;
+    const int64_t* row_ptr = nullptr;
+    int64_t rp = 0;
+    double* yhat = nullptr;
 };
 void gemm(const GemmArgs& g, int num_sms, cudaStream_t s);
+bool gemm_tma_ok(const GemmArgs& g);
 
 // ---- dense MTTKRP for mode 0 (tensor.hpp:174-182): B = T_(1) * Z with Z generated on the
 // fly from the factors (khatri_rao order, last listed factor fastest).  T is the local
@@ -234,6 +242,8 @@ struct PcgStepArgs {
     PcgCtl* ctl = nullptr;         // loop control (graph body), or nullptr
     cudaGraphConditionalHandle h{};
     int set_cond = 0;              // 1: inside the graph's WHILE body (clear `h` on stop)
+    int64_t null_rows = 0;         // rows i < null_rows of Ap are rho p (not written by the operator)
+    double rho = 0.0;
     double* partial = nullptr;     // pcg_step_fused_partials(n, num_sms) doubles
     unsigned long long* barrier = nullptr;  // zero-initialised once per plan
 };

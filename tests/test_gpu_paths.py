@@ -245,3 +245,37 @@ def test_pcg_large_n_step_variants(cp, monkeypatch, fused, skipzero, graph):
     h0, h1 = np.asarray(r0.residual_history), np.asarray(r1.residual_history)
     assert h0.size == h1.size and np.all(np.abs(h1 - h0) <= 1e-6 * h0), (h0, h1)
     assert ri.rel(w1, w0) < 1e-9 and ri.rel(w1, wo) < 1e-6
+
+
+def test_pcg_gram_epilogue_bitwise(cp, monkeypatch):
+    """Large-n eigenbasis PCG with the row-Gram operator: the split-K reduction fused with the
+    row-Gram apply (EPI_GRAM, one launch) sums in the same order as the two launches it replaces,
+    so the solve is bit-identical; and it matches the oracle."""
+    g = np.random.default_rng(602)
+    shape, r, q = [1100, 20, 16], 16, 30000
+    pts = np.sort(g.uniform(0, 1, shape[0]))
+    lin = g.choice(int(np.prod(shape)), size=q, replace=False)
+    idx = np.array(np.unravel_index(lin, shape, order="F"), dtype=np.int64)
+    vals = g.normal(size=q)
+    factors = [np.zeros((shape[0], r))] + [g.normal(size=(n, r)) for n in shape[1:]]
+    mode = cp.RkhsMode(pts, 0.3, 1e-3)
+    kern = mode.kernel()
+    ek = orc.sym_eig(kern)
+    mode.set_eig(ek.u, ek.d)
+    assert shape[0] - (ek.d == 0).sum() >= 520  # the GEMM keeps k >= 512: tensor-map path with EPI_GRAM
+    cfg = cp.PcgConfig(1e-9, 300, record_history=True)
+    res = {}
+    for epi in ("0", "1"):
+        monkeypatch.setenv("CPHIFI_GRAM_EPI", epi)
+        p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), 0, mode, 1e-6)
+        p.set_operator("gram")
+        rep = cp.SolveReport()
+        res[epi] = (cp.solve_unaligned_pcg(p, cfg, rep), rep)
+    (w0, r0), (w1, r1) = res["0"], res["1"]
+    assert r1.iterations == r0.iterations and r1.residual_history == r0.residual_history
+    assert np.array_equal(w0, w1)
+    sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 0, kern, 1e-3, 1e-6)
+    orep = orc.SolveReport()
+    wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-9, 300), ek, orc.sym_eig(sub.v), report=orep)
+    assert r1.converged and abs(r1.iterations - orep.iterations) <= 1, (r1.iterations, orep.iterations)
+    assert ri.rel(w1, wo) < 1e-6
