@@ -560,7 +560,10 @@ int64_t rot_null_rows(cphifi_unaligned p) {
 }
 
 // null_rows = false: the caller supplies rows i < z of y~ (= rho x~) itself (the fused PCG step)
-void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows = true) {
+// parts / nparts non-null: the output GEMM's split-K partials are left unreduced for the fused PCG
+// step (EPI_PARTIALS; *parts = nullptr when that GEMM does not take the tensor-map path)
+void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows = true,
+                const double** parts = nullptr, int* nparts = nullptr) {
     need_mode(p);
     cphifi_ctx ctx = p->obs->ctx;
     const int64_t n = p->n, r = p->r;
@@ -611,6 +614,19 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows
     h.c = yt + z; h.c_rs = 1; h.c_cs = n;
     h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get() + z; h.e1 = xt + z; h.ld_e = n;
     h.beta1 = p->mode->lambda; h.beta2 = p->rho;
+    if (parts) {
+        *parts = nullptr;
+        // opt-in (CPHIFI_PCG_AP_PARTS=1): measured slower at config 4 (12.25 vs 12.07 ms: the step's
+        // partial-sum loads cost more than the reduce_epi launch they replace)
+        bool on = false;
+        if (const char* e = std::getenv("CPHIFI_PCG_AP_PARTS"))
+            on = std::atoi(e) != 0 && gemm_tma_ok(h) && gemm_splitk_depth(h, ctx->num_sms) <= 8;  // step unrolls <= 8
+        if (on) {
+            h.epi = EPI_PARTIALS;
+            h.parts_out = parts;
+            h.p_out = nparts;
+        }
+    }
     gemm(h, ctx->num_sms, ctx->stream);
     if (z > 0 && null_rows) scale_row_block(yt, xt, z, n, r, p->rho, ctx->stream);  // y~ = rho x~  (rows i < z)
 }
@@ -1888,6 +1904,8 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             p->pcg_step.alloc(1 + pcg_step_fused_partials(n, ctx->num_sms));
             CPHIFI_CUDA(cudaMemsetAsync(p->pcg_step.get(), 0, sizeof(double), s));
         }
+        const double* ap_parts = nullptr;  // set by matvec_rot(..., &ap_parts, &ap_np) per operator call
+        int ap_np = 0;
         auto step_fused = [&](PcgCtl* c, cudaGraphConditionalHandle h, bool set_cond = true) {
             PcgStepArgs sa;
             sa.n = n; sa.r = (int)r;
@@ -1896,6 +1914,10 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             sa.st = st; sa.ctl = c; sa.h = h; sa.set_cond = set_cond ? 1 : 0;
             sa.null_rows = rot_null_rows(p);  // Ap rows i < z = rho p: matvec_rot leaves them to the step
             sa.rho = p->rho;
+            sa.ap_parts = ap_parts;  // unreduced output GEMM (EPI_PARTIALS), or null: Ap as written
+            sa.ap_p = ap_np;
+            sa.mu = p->mode->mu.get();
+            sa.lambda = p->mode->lambda;
             sa.barrier = reinterpret_cast<unsigned long long*>(p->pcg_step.get());
             sa.partial = p->pcg_step.get() + 1;
             pcg_step_fused(sa, ctx->num_sms, s);
@@ -1925,7 +1947,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 },
                 [&](cudaGraphConditionalHandle h) {
                     if (fused_step) {
-                        matvec_rot(p, pv, ap, false);
+                        matvec_rot(p, pv, ap, false, &ap_parts, &ap_np);
                         step_fused(ctl, h);
                         return;
                     }
@@ -2039,7 +2061,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                 // pcg_ctl clears the condition; no host round trip per iteration
                 if (ensure_pcg_graph(p, rot, [&](cudaGraphConditionalHandle h) {
                         if (fused_step) {
-                            matvec_rot(p, pv, ap, false);
+                            matvec_rot(p, pv, ap, false, &ap_parts, &ap_np);
                             step_fused(ctl, h);
                             return;
                         }
@@ -2091,7 +2113,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                     ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
                 } evg{ev};
                 auto enqueue = [&](int slot) {
-                    matvec_rot(p, pv, ap, false);
+                    matvec_rot(p, pv, ap, false, &ap_parts, &ap_np);
                     step_fused(ctl, cudaGraphConditionalHandle{}, false);
                     CPHIFI_CUDA(cudaMemcpyAsync(snap + slot, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
                     CPHIFI_CUDA(cudaEventRecord(ev[slot], s));
@@ -2114,7 +2136,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
             }
             while (!done && rel > cfg->tol && it < cfg->max_iter) {
                 if (fused_step) {  // step B runs inside the same launch (harmless after the last one)
-                    matvec_rot(p, pv, ap, false);
+                    matvec_rot(p, pv, ap, false, &ap_parts, &ap_np);
                     step_fused(nullptr, cudaGraphConditionalHandle{});
                 } else {
                     body_a();

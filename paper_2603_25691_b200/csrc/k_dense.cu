@@ -1165,6 +1165,13 @@ void launch_reduce_gram(const double* work, int P, int64_t m, int64_t ncols, con
 }
 
 template <int BN>
+int64_t splitk_depth_t(const GemmArgs& g, int num_sms) {  // as gemm_tma_t below
+    const int mt = (int)((g.m + BMM - 1) / BMM), nt = (int)((g.n + BN - 1) / BN);
+    const int64_t chunks = (g.k + BK - 1) / BK;
+    return std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms / (mt * nt), chunks));
+}
+
+template <int BN>
 void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
     static thread_local GrowScratch work;
     int dev = 0;
@@ -1198,10 +1205,21 @@ void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
         launch_reduce_gram(work.get(), (int)P, g.m, g.n, g, s);
         return;
     }
+    if (g.epi == EPI_PARTIALS) {
+        *g.parts_out = work.get();
+        *g.p_out = (int)P;
+        return;
+    }
     const int64_t cnt = g.m * (g.c2 ? std::max(g.n, g.ld2) : g.n);
     reduce_epi_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4 * num_sms), 256, 0, s>>>(work.get(), (int)P, g.m,
                                                                                                   g.n, g);
     CPHIFI_CHECK_LAUNCH();
+}
+
+int gemm_splitk_depth(const GemmArgs& g, int num_sms) {
+    if (g.n <= 8) return (int)splitk_depth_t<8>(g, num_sms);
+    if (g.n <= 16) return (int)splitk_depth_t<16>(g, num_sms);
+    return (int)splitk_depth_t<32>(g, num_sms);
 }
 
 void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
@@ -1209,7 +1227,8 @@ void gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     if (g.k <= 0) {
         // empty contraction: run a zero-K GEMM (epilogue only) through the S=1 path
     }
-    if (g.epi == EPI_GRAM && !(g.k > 0 && gemm_tma_ok(g))) throw_invalid("gemm: EPI_GRAM needs the tensor-map path");
+    if ((g.epi == EPI_GRAM || g.epi == EPI_PARTIALS) && !(g.k > 0 && gemm_tma_ok(g)))
+        throw_invalid("gemm: EPI_GRAM / EPI_PARTIALS need the tensor-map path");
     if (g.k > 0 && gemm_tma_ok(g)) {
         if (g.n <= 8) gemm_tma_t<8>(g, num_sms, s);
         else if (g.n <= 16) gemm_tma_t<16>(g, num_sms, s);

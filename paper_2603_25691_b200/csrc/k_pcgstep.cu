@@ -119,8 +119,26 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
     // serialised on L2 latency).
     const double* __restrict__ pp = a.p;
     const double* __restrict__ ap = a.ap;
+    const int64_t am = n - a.null_rows;  // rows of the operator GEMM's output
+    // Ap(i, j): rho p for the null-space rows; else the operator's output, or its split-K partials
+    // reduced in p order with the EPI_ROWSCALE epilogue (bit-identical to reduce_epi_kernel)
+    auto ap_at = [&](int64_t i, int j, double pvv) -> double {
+        if (i < a.null_rows) return a.rho * pvv;
+        if (!a.ap_parts) return ap[i + n * j];
+        const int64_t e = (i - a.null_rows) + am * j;
+        constexpr int PMAX = 8;  // split-K depth of the operator GEMM (148 SMs / tiles, capped by the host)
+        double pt[PMAX];
+#pragma unroll
+        for (int q2 = 0; q2 < PMAX; ++q2) pt[q2] = q2 < a.ap_p ? __ldcg(a.ap_parts + (int64_t)q2 * am * r + e) : 0.0;
+        double v = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < PMAX; ++q2)
+            if (q2 < a.ap_p) v += pt[q2];
+        return a.mu[i] * (v + a.lambda * pvv) + a.rho * pvv;
+    };
     // ---- 1: pap = p'Ap --------------------------------------------------------------------
     double t = 0.0;
+    double av0[JT];  // the first own block's Ap, reused by phase 2
     for (int64_t b = c; b < nblk; b += C) {
         const int64_t i = b * SRB + q;
         double pv[JT], av[JT];
@@ -128,10 +146,14 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
         for (int u = 0; u < JT; ++u) {
             const bool ok = i < n && j0 + u < r;
             pv[u] = ok ? pp[i + n * (j0 + u)] : 0.0;
-            av[u] = ok && i >= a.null_rows ? ap[i + n * (j0 + u)] : a.rho * pv[u];
+            av[u] = ok ? ap_at(i, j0 + u, pv[u]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < JT; ++u) t = fma(pv[u], av[u], t);
+        if (b == c) {
+#pragma unroll
+            for (int u = 0; u < JT; ++u) av0[u] = av[u];
+        }
     }
     t = cta_total(t, sh);
     if (threadIdx.x == 0) a.partial[c] = t;
@@ -149,7 +171,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
             const bool ok = i < n && j0 + u < r;
             const int64_t e = i + n * (j0 + u);
             pv[u] = ok ? pp[e] : 0.0;
-            av[u] = ok && i >= a.null_rows ? ap[e] : a.rho * pv[u];
+            av[u] = !ok ? 0.0 : (b == c ? av0[u] : ap_at(i, j0 + u, pv[u]));
             xv[u] = ok ? a.x[e] : 0.0;
             rv[u] = ok ? a.res[e] : 0.0;
         }

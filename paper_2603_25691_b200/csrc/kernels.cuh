@@ -14,8 +14,10 @@ enum EpiOp : int {
     EPI_HADAMARD = 2, // C = AB .* E1                        (unaligned.hpp:137)
     EPI_SCALE_DIV = 3, // C = AB / (e_row[i]*e_col[j] + beta1) with zero-denominator flag
     EPI_ROWSCALE = 4,  // C = e_row[i] * (AB + beta1*E1) + beta2*E1   (E1 may be null: 0)
-    EPI_GRAM = 5       // Yhat(i,:) = G_i (AB)(i,:) for rows with observations (row-Gram operator;
+    EPI_GRAM = 5,      // Yhat(i,:) = G_i (AB)(i,:) for rows with observations (row-Gram operator;
                        // tensor-map GEMM path only: the split-K reduction and the apply in one kernel)
+    EPI_PARTIALS = 6   // no reduction: *parts_out = the P split-K partials (P x m x n, column-major
+                       // each), *p_out = P, for a consumer that reduces them itself (tensor-map path)
 };
 
 struct GemmArgs {
@@ -34,9 +36,12 @@ struct GemmArgs {
     const int64_t* row_ptr = nullptr;
     int64_t rp = 0;
     double* yhat = nullptr;
+    const double** parts_out = nullptr;  // EPI_PARTIALS
+    int* p_out = nullptr;
 };
 void gemm(const GemmArgs& g, int num_sms, cudaStream_t s);
 bool gemm_tma_ok(const GemmArgs& g);
+int gemm_splitk_depth(const GemmArgs& g, int num_sms);  // split-K partials of the tensor-map path
 
 // ---- dense MTTKRP for mode 0 (tensor.hpp:174-182): B = T_(1) * Z with Z generated on the
 // fly from the factors (khatri_rao order, last listed factor fastest).  T is the local
@@ -244,6 +249,12 @@ struct PcgStepArgs {
     int set_cond = 0;              // 1: inside the graph's WHILE body (clear `h` on stop)
     int64_t null_rows = 0;         // rows i < null_rows of Ap are rho p (not written by the operator)
     double rho = 0.0;
+    // non-null: rows i >= null_rows of Ap come as the operator GEMM's split-K partials (EPI_PARTIALS,
+    // P x (n - null_rows) x r) and get its EPI_ROWSCALE epilogue here: mu_i (sum + lambda p) + rho p
+    const double* ap_parts = nullptr;
+    int ap_p = 0;
+    const double* mu = nullptr;
+    double lambda = 0.0;
     double* partial = nullptr;     // pcg_step_fused_partials(n, num_sms) doubles
     unsigned long long* barrier = nullptr;  // zero-initialised once per plan
 };

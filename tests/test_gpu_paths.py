@@ -265,8 +265,9 @@ def test_pcg_gram_epilogue_bitwise(cp, monkeypatch):
     assert shape[0] - (ek.d == 0).sum() >= 520  # the GEMM keeps k >= 512: tensor-map path with EPI_GRAM
     cfg = cp.PcgConfig(1e-9, 300, record_history=True)
     res = {}
-    for epi in ("0", "1"):
-        monkeypatch.setenv("CPHIFI_GRAM_EPI", epi)
+    for epi in ("0", "1", "parts"):  # "parts": + the output GEMM's split-K partials reduced in the step
+        monkeypatch.setenv("CPHIFI_GRAM_EPI", "0" if epi == "0" else "1")
+        monkeypatch.setenv("CPHIFI_PCG_AP_PARTS", "1" if epi == "parts" else "0")
         p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals), cp.KruskalModel(factors), 0, mode, 1e-6)
         p.set_operator("gram")
         rep = cp.SolveReport()
@@ -274,6 +275,8 @@ def test_pcg_gram_epilogue_bitwise(cp, monkeypatch):
     (w0, r0), (w1, r1) = res["0"], res["1"]
     assert r1.iterations == r0.iterations and r1.residual_history == r0.residual_history
     assert np.array_equal(w0, w1)
+    w2, r2 = res["parts"]  # same sums; the epilogue's FMA contraction may differ by an ulp
+    assert r2.iterations == r0.iterations and ri.rel(w2, w0) < 1e-10
     sub = orc.make_unaligned_subproblem(shape, idx, vals, factors, 0, kern, 1e-3, 1e-6)
     orep = orc.SolveReport()
     wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-9, 300), ek, orc.sym_eig(sub.v), report=orep)
