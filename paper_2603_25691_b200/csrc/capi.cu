@@ -620,7 +620,7 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows
         // partial-sum loads cost more than the reduce_epi launch they replace)
         bool on = false;
         if (const char* e = std::getenv("CPHIFI_PCG_AP_PARTS"))
-            on = std::atoi(e) != 0 && gemm_tma_ok(h) && gemm_splitk_depth(h, ctx->num_sms) <= 8;  // step unrolls <= 8
+            on = std::atoi(e) != 0 && gemm_tma_ok(h) && gemm_splitk_depth(h, ctx->num_sms) <= 4;  // step unrolls <= 4
         if (on) {
             h.epi = EPI_PARTIALS;
             h.parts_out = parts;
@@ -1495,23 +1495,8 @@ bool host_matvec_graph(cphifi_unaligned p, const double* x, double* y) {
             CPHIFI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhy), p->hv_hy, 0));
             CPHIFI_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
             try {
-                // optional: x read from host memory by the operator launch itself (every CTA copies a
-                // slice, one grid barrier) instead of a copy node — measured slower on B200 (config 1
-                // e2e 26.3k vs 27.8k matvecs/s: the extra barrier outweighs one graph node), so off
-                bool fused_in = false;
-                if (const char* e = std::getenv("CPHIFI_HOST_X_FUSED"))
-                    fused_in = p->small_n && p->prefetch && p->mode && std::atoi(e) != 0;
-                if (fused_in) {
-                    FusedArgs a = fused_args(p, matvec_phases(p, false, 0));
-                    a.x = p->vx.get();
-                    a.x_host = dhx;
-                    a.y = p->vy.get();
-                    a.gram = p->op == 1 ? p->gram.get() : nullptr;
-                    launch_fused(p, a);
-                } else {
-                    copy_doubles(p->vx.get(), dhx, nr, ctx->stream);
-                    matvec_dev(p, p->vx.get(), p->vy.get());
-                }
+                copy_doubles(p->vx.get(), dhx, nr, ctx->stream);
+                matvec_dev(p, p->vx.get(), p->vy.get());
                 copy_doubles(dhy, p->vy.get(), nr, ctx->stream);
             } catch (...) {
                 cudaGraph_t junk = nullptr;

@@ -190,7 +190,6 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
     const int64_t i0 = a.n * c / C, i1 = a.n * (c + 1) / C;  // this CTA's y rows (PH_C2)
     const double* kc2 = a.kmat_c2 ? a.kmat_c2 : a.kmat;      // PH_C2 columns (U in the eigenbasis)
     const bool pf = a.prefetch && a.x != nullptr && (a.phases & (PH_AL | PH_C2));
-    const bool xh = a.x_host != nullptr;  // X arrives from host memory: staged after the copy barrier
     // ---- entry, before any dependent load: one thread issues the bulk copies that need no plan
     // data (even n: 16-byte aligned columns), so their HBM latency overlaps the plan reads
     const bool tma_entry = (a.n % 2) == 0;
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
         const unsigned colb = (unsigned)(a.n * 8);
         unsigned bytes = 0;
         if (tma_fac) bytes += (unsigned)(a.fac_total * 8);
-        if (pf && !xh) bytes += colb * (unsigned)a.r;
+        if (pf) bytes += colb * (unsigned)a.r;
         if (pf && (a.phases & PH_C2)) bytes += colb * (unsigned)(i1 - i0);
         tma::mbar_expect_tx(&s_fbar, bytes);
         if (tma_fac)
@@ -210,8 +209,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
                 tma::bulk_g2s(reinterpret_cast<unsigned char*>(sfac) + b0, reinterpret_cast<const unsigned char*>(a.fac) + b0,
                               (unsigned)min((int64_t)32768, a.fac_total * 8 - b0), &s_fbar);
         if (pf) {
-            if (!xh)
-                for (int j = 0; j < (int)a.r; ++j) tma::bulk_g2s(xs + ldx * j, a.x + a.n * j, colb, &s_fbar);
+            for (int j = 0; j < (int)a.r; ++j) tma::bulk_g2s(xs + ldx * j, a.x + a.n * j, colb, &s_fbar);
             if (a.phases & PH_C2)
                 for (int64_t i = i0; i < i1; ++i)
                     tma::bulk_g2s(kcs + (MAXLOC + i - i0) * a.n, kc2 + i * a.n, colb, &s_fbar);
@@ -277,8 +275,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
     if (pf) {
         if (!tma_entry) {
             const int nn = (int)a.n, nr = (int)(a.n * a.r), odd = (int)(ldx - a.n);  // small n: n * r <= 8192
-            if (!xh)
-                for (int e = threadIdx.x; e < nr; e += FT) cp_async8(xs + e + odd * (e / nn), a.x + e);
+            for (int e = threadIdx.x; e < nr; e += FT) cp_async8(xs + e + odd * (e / nn), a.x + e);
             if (a.phases & PH_C2)
                 for (int64_t i = i0; i < i1; ++i)
                     for (int64_t k = threadIdx.x; k < a.n; k += FT)
@@ -295,36 +292,6 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
     }
     const double* fac = SMEMF ? sfac : a.fac;
     dbg_mark(8);  // prefetch issued
-
-    // ---- host-buffer input: every CTA copies its slice of x (mapped host memory, one PCIe round
-    // trip: all loads issued before the stores) into the device buffer while the prefetch above is
-    // in flight; a grid barrier publishes it; X is then staged from L2 ----------------------------
-    if (xh) {
-        const int64_t nr = a.n * a.r;
-        const int64_t per = (nr + C - 1) / C;
-        const int64_t e0 = (int64_t)c * per, e1 = min(nr, e0 + per);
-        double* xd = const_cast<double*>(a.x);
-        constexpr int XU = 4;
-        double v[XU];
-        for (int64_t e = e0 + threadIdx.x; e < e1; e += (int64_t)FT * XU) {
-#pragma unroll
-            for (int u = 0; u < XU; ++u) {
-                const int64_t k = e + (int64_t)u * FT;
-                v[u] = k < e1 ? a.x_host[k] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < XU; ++u) {
-                const int64_t k = e + (int64_t)u * FT;
-                if (k < e1) xd[k] = v[u];
-            }
-        }
-        grid_barrier(a.barrier);
-        if (pf) {
-            const int64_t odd = ldx - a.n;
-            for (int64_t e = threadIdx.x; e < nr; e += FT) xs[e + odd * (e / a.n)] = __ldcg(a.x + e);
-        }
-        __syncthreads();
-    }
 
     // ---- phase A: Xhat rows -----------------------------------------------------------------
     if (a.phases & PH_AL) {  // only the rows this CTA's observations touch, from shared memory

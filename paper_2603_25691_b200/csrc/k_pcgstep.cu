@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
         if (i < a.null_rows) return a.rho * pvv;
         if (!a.ap_parts) return ap[i + n * j];
         const int64_t e = (i - a.null_rows) + am * j;
-        constexpr int PMAX = 8;  // split-K depth of the operator GEMM (148 SMs / tiles, capped by the host)
+        constexpr int PMAX = 4;  // split-K depth of the operator GEMM (148 SMs / tiles, capped by the host)
         double pt[PMAX];
 #pragma unroll
         for (int q2 = 0; q2 < PMAX; ++q2) pt[q2] = q2 < a.ap_p ? __ldcg(a.ap_parts + (int64_t)q2 * am * r + e) : 0.0;
@@ -213,8 +213,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
     }
     // ---- 3: z = M^-1 r on the own row blocks, rz'; 4: p = z + beta p ----------------------------
     // z and the thread's r values stay in registers for phase 4 when the CTA owns one row block
-    constexpr int MAXB = 1;
-    double zkeep[MAXB][JT];
+    double zkeep[JT];  // the first own block's z
     t = 0.0;
     int nb_own = 0;
     for (int64_t b = c; b < nblk; b += C, ++nb_own) {
@@ -271,9 +270,9 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
                 t = fma(rmine[u], acc[u], t);
             }
         }
-        if (nb_own < MAXB) {
+        if (nb_own == 0) {
 #pragma unroll
-            for (int u = 0; u < JT; ++u) zkeep[nb_own][u] = acc[u];
+            for (int u = 0; u < JT; ++u) zkeep[u] = acc[u];
         }
     }
     t = cta_total(t, sh);
@@ -289,7 +288,7 @@ __global__ void __launch_bounds__(ST) pcg_step_fused_kernel(const PcgStepArgs a)
         for (int u = 0; u < JT; ++u) {
             const bool ok = i < n && j0 + u < r;
             const int64_t e = i + n * (j0 + u);
-            zv[u] = nb_own < MAXB ? zkeep[0][u] : (ok ? a.z[e] : 0.0);
+            zv[u] = nb_own == 0 ? zkeep[u] : (ok ? a.z[e] : 0.0);
             pv[u] = ok ? a.p[e] : 0.0;
         }
 #pragma unroll

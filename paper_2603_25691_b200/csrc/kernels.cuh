@@ -139,9 +139,6 @@ struct FusedArgs {
     const int32_t* mult = nullptr;      // coalesced plan: operator weight of entry l (dot mode)
     const double* kmat = nullptr;       // n x n column-major, symmetric
     const double* x = nullptr;          // n x r column-major
-    const double* x_host = nullptr;     // non-null (small n, host-buffer call): x lives in mapped host
-                                        // memory; the CTAs copy it to `x` (a device buffer) at entry,
-                                        // overlapping the plan prefetch, then one grid barrier
     double* y = nullptr;                // n x r column-major
     double* xhat_rm = nullptr;          // n x rp
     double* yhat_rm = nullptr;          // n x rp

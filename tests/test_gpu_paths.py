@@ -122,12 +122,8 @@ def test_pcg_graph_loop_matches_host_loop(cp, monkeypatch):
     assert rep.iterations == 3 and len(rep.residual_history) == 4 and not rep.converged
 
 
-@pytest.mark.parametrize("x_fused", ["0", "1"])
-def test_host_matvec_graph_vs_plain(cp, monkeypatch, x_fused):
-    """Host-buffer operator call through the cached graph: copy node + operator (default) or the
-    operator reading x from mapped host memory itself (CPHIFI_HOST_X_FUSED=1), vs the oracle."""
+def test_host_matvec_graph_vs_plain(cp, monkeypatch):
     import torch
-    monkeypatch.setenv("CPHIFI_HOST_X_FUSED", x_fused)
     c, p, sub, ek = _config1_problem(cp, shared=False)
     n, r = c.shape[0], c.r
     xs = [torch.randn(n * r, dtype=torch.float64).pin_memory() for _ in range(2)]

@@ -1,0 +1,49 @@
+"""Register-spill guard for the headline kernels (CPU: nvcc cross-compiles for sm_100a here).
+
+The config-1 operator kernel runs two 512-thread CTAs per SM, so it has 64 registers per thread;
+a change that makes it spill costs the headline several percent (measured: an extra entry path
+added 28 B of spill stores and dropped the bench from ~60k to ~57.7k matvecs/s).  This compiles
+the kernel's translation unit with `-Xptxas -v` and requires zero spills for the instantiations
+the benchmarks launch.
+"""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2603_25691_b200", "csrc")
+
+
+def _ptxas_report(src):
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available")
+    out = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xptxas", "-v",
+                          "-c", os.path.join(CSRC, src), "-o", os.devnull, "-I", CSRC],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    report, fn = {}, None
+    for line in out.stderr.splitlines():
+        m = re.search(r"Function properties for (\S+)", line)
+        if m:
+            fn = m.group(1)
+            continue
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+        if m and fn:
+            report[fn] = (int(m.group(1)), int(m.group(2)))
+            fn = None
+    return report
+
+
+@pytest.mark.parametrize("src,pattern", [
+    ("k_fused.cu", r"fused_matvec_kernelILi16ELi2ELb1E"),   # config 1: rp 16, 2 other modes, staged factors
+    ("k_pcgstep.cu", r"pcg_step_fused_kernelILi8E"),        # config 4 PCG vector step (r 64)
+])
+def test_no_spills(src, pattern):
+    rep = _ptxas_report(src)
+    hits = {k: v for k, v in rep.items() if re.search(pattern, k)}
+    assert hits, f"no instantiation matching {pattern} in {src}"
+    for k, (st, ld) in hits.items():
+        assert st == 0 and ld == 0, f"{k}: {st} B spill stores, {ld} B spill loads"
