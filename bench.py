@@ -120,7 +120,7 @@ def cpu_port_matvec(c, threads, seconds):
     """The oracle's fused streaming restatement on `threads` host cores (test/bench baseline)."""
     import numpy as np
     from oracle import oracle as orc
-    from paper_2603_25691_b200.configs import kernel_matrix
+    from inputs.configs import kernel_matrix
     kern = kernel_matrix(c.points, c.kernel, c.ell)
     factors = [None] + c.factors[1:]
     x = np.random.default_rng(0).normal(size=c.shape[0] * c.r)
@@ -164,12 +164,12 @@ def run_reference(args, rank):
     if rank != 0:
         return
     from oracle import oracle as orc
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     orc.build()
     c = configs.config1()
     threads = orc.max_threads()
     import numpy as np
-    from paper_2603_25691_b200.configs import kernel_matrix
+    from inputs.configs import kernel_matrix
     kern = kernel_matrix(c.points, c.kernel, c.ell)
     factors = [None] + c.factors[1:]
     x = np.random.default_rng(0).normal(size=c.shape[0] * c.r)

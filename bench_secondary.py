@@ -111,7 +111,7 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     n, r, d, q = cfg.shape[0], cfg.r, len(cfg.shape), cfg.q
     lib = _capi.load()
     t0 = time.perf_counter()
-    idx, vals = configs.generate_device(cfg, ctx)
+    idx, vals = cp.synth_observations_device(cfg, ctx)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
@@ -189,7 +189,7 @@ def als_updates(ctx, p, c):
     from the previous W as AlsState does) and config 2 (aligned decoupled), wall clock per update
     plus the device-timed split (solve / factor update + error terms)."""
     import paper_2603_25691_b200 as cp
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     out = {}
     cfg = cp.PcgConfig(c.tol, c.max_iter)
     u = cp.update_infinite_mode_unaligned(p, cfg)

@@ -307,31 +307,16 @@ int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t
                                const double* const* factors, int iters, double* w_out,
                                double* ms_out);
 
-/* ---- host-side seeded generators (test/bench inputs; no device work) -------------- */
-/* std::mt19937_64 with libstdc++'s uniform_real_distribution / uniform_int_distribution
- * / normal_distribution algorithms, reproduced bit-exactly (pinned by tests/golden). */
-typedef struct cphifi_rng_s* cphifi_rng;
-int cphifi_rng_create(uint64_t seed, cphifi_rng* out);
-int cphifi_rng_destroy(cphifi_rng rng);
-int cphifi_rng_next_u64(cphifi_rng rng, uint64_t* n_out, int64_t count);
-int cphifi_rng_uniform_real(cphifi_rng rng, double lo, double hi, double* out, int64_t count);
-int cphifi_rng_uniform_int(cphifi_rng rng, int64_t lo, int64_t hi, int64_t* out, int64_t count);
-/* normal_distribution(mean, stddev) draws; the distribution's cached second variate is
- * kept in the rng handle (one distribution object per handle). */
-int cphifi_rng_normal(cphifi_rng rng, double mean, double stddev, double* out, int64_t count);
-/* Discard the cached variate (equivalent to constructing a fresh normal_distribution). */
-int cphifi_rng_normal_reset(cphifi_rng rng);
+/* ---- device-side test / bench inputs (no solver work) ------------------------------ */
 /* Device-side seeded observations (configs 3-4 scale; not the solver path).  q draws; mode m
  * uniform on [0, shape[m]) except mode zipf_mode (>= 0) with P(i) ~ (i+1)^-zipf_s; value =
  * sum_j prod_m A_m(i_m, j) + noise_std * N(0,1) with factors[m] host n_m x r column-major.
- * Counter-based (splitmix64 of seed, observation, stream), bit-reproducible.  idx_out (d x q
- * int32) and vals_out (q fp64) are DEVICE buffers on the context's GPU. */
+ * Counter-based (splitmix64 of seed, observation, stream; inputs/synth_math.h), bit-identical to
+ * the host generator inputs/synth_host.cpp.  idx_out (d x q int32) and vals_out (q fp64) are
+ * DEVICE buffers on the context's GPU. */
 int cphifi_synth_observations(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, uint64_t seed,
                               int zipf_mode, double zipf_s, int64_t r, const double* const* factors,
                               double noise_std, int32_t* idx_out, double* vals_out);
-/* sample_uniform's index draw (observations.hpp:90-121): q distinct linear indices of
- * [0, n_total) by partial Fisher-Yates with a sparse map, seeded mt19937_64(seed). */
-int cphifi_sample_uniform_linear(int64_t n_total, int64_t q, uint64_t seed, int64_t* picked);
 
 #ifdef __cplusplus
 }

@@ -4,7 +4,7 @@ No public dataset is involved: the configs are synthetic by definition.  Configs
 drawn with the reference's own RNG stack (std::mt19937_64 + libstdc++ normal_distribution,
 seed 0; sampler = sample_uniform, observations.hpp:90-121).  Configs 2-4 draw the small factor
 matrices the same way and the bulk noise / indices with numpy's PCG64 (config 2) or on the
-device with a counter-based generator (configs 3-4, see synth_observations).
+device with a counter-based generator (configs 3-4: inputs/synth_math.h, the same bits on the host and on the device).
 
 Noise "N(0, 1e-2)" is read as VARIANCE 1e-2 (std 0.1); SURVEY §8d records the choice.
 """
@@ -49,8 +49,21 @@ class UnalignedConfig:
 
 
 def _rng(seed):
-    import paper_2603_25691_b200 as cp
-    return cp.Mt19937_64(seed)
+    from . import Mt19937_64
+    return Mt19937_64(seed)
+
+
+def sample_uniform(shape, tensor_flat, q, seed):
+    """sample_uniform (observations.hpp:90-121) on a column-major tensor: (d, q) int32 indices of q
+    distinct entries (partial Fisher-Yates, mt19937_64(seed)) and their values."""
+    from . import sample_uniform_linear
+    picked = sample_uniform_linear(int(np.prod(shape)), q, seed)
+    idx = np.zeros((len(shape), q), dtype=np.int32)
+    lin = picked.copy()
+    for k, s in enumerate(shape):
+        idx[k] = lin % s
+        lin //= s
+    return idx, np.asarray(tensor_flat)[picked]
 
 
 def _normal_matrix(rng, rows, cols):
@@ -93,10 +106,9 @@ def config0() -> AlignedConfig:
 def config1() -> UnalignedConfig:
     """Unaligned version of config 0: q = 200k distinct entries (10 %), PCG tol 1e-8."""
     c0 = config0()
-    from . import sample_uniform, DenseTensor
-    obs = sample_uniform(DenseTensor(c0.shape, c0.tensor), 200_000, 1)
+    idx, vals = sample_uniform(c0.shape, c0.tensor, 200_000, 1)
     return UnalignedConfig("config1", c0.shape, c0.r, 1e-3, 1e-6, 1e-8, 500, c0.points, "gaussian", 0.1,
-                           c0.factors, c0.w_true, obs.index_array(), obs.values())
+                           c0.factors, c0.w_true, idx, vals)
 
 
 def config2() -> AlignedConfig:
@@ -126,10 +138,9 @@ def small_unaligned(shape=(40, 12, 10), r=4, q=1500, seed=5) -> UnalignedConfig:
     factors = [a1] + others
     t = _full_3way(*factors) if len(shape) == 3 else None
     t = t + rng.normal(0.0, 0.1, t.size)
-    from . import sample_uniform, DenseTensor
-    obs = sample_uniform(DenseTensor(list(shape), t), q, seed + 1)
+    idx, vals = sample_uniform(list(shape), t, q, seed + 1)
     return UnalignedConfig("small", list(shape), r, 1e-3, 1e-6, 1e-8, 500, pts, "gaussian", 0.1, factors, w,
-                           obs.index_array(), obs.values())
+                           idx, vals)
 
 
 # ---- configs 3 and 4: observations generated on the device --------------------------------
@@ -186,22 +197,11 @@ def config4() -> DeviceUnalignedConfig:
                                  [a1] + others, w, 1_000_000_000, 4, 0, 1.1, coalesce=True)
 
 
-def generate_device(cfg: DeviceUnalignedConfig, ctx, q: int | None = None):
-    """Draw the observations on cfg's GPU: returns torch tensors idx (d, q) int32, vals (q,) f64."""
-    import ctypes
-
-    import torch
-
-    from . import _capi
-    q = cfg.q if q is None else q
-    d = len(cfg.shape)
-    dev = torch.device("cuda", ctx.device)
-    idx = torch.empty((d, q), dtype=torch.int32, device=dev)
-    vals = torch.empty(q, dtype=torch.float64, device=dev)
-    shape = np.ascontiguousarray(cfg.shape, dtype=np.int64)
-    facs = [np.asfortranarray(f) for f in cfg.factors]
-    ptrs = (_capi.c_double_p * d)(*[f.ctypes.data_as(_capi.c_double_p) for f in facs])
-    _capi.call("cphifi_synth_observations", ctx.handle, d, shape.ctypes.data_as(_capi.c_int64_p), q,
-               ctypes.c_uint64(cfg.seed), cfg.zipf_mode, cfg.zipf_s, cfg.r, ptrs, cfg.noise_std, idx.data_ptr(),
-               vals.data_ptr())
-    return idx, vals
+def generate_host(cfg: DeviceUnalignedConfig, l0: int = 0, l1: int | None = None, values: bool = True,
+                  threads: int | None = None):
+    """Draws [l0, l1) of cfg's observations on the host (bit-identical to the device generator,
+    paper_2603_25691_b200.synth_observations_device): idx (d, l1 - l0) int32, vals fp64 or None."""
+    from . import synth_observations
+    l1 = cfg.q if l1 is None else l1
+    return synth_observations(cfg.shape, l0, l1, cfg.seed, cfg.zipf_mode, cfg.zipf_s, cfg.factors, cfg.noise_std,
+                              values=values, threads=threads)

@@ -180,45 +180,97 @@ int orc_unaligned_matvec(int64_t n, int64_t r, const double* kmat, double lambda
  * OpenMP over a deterministic contiguous partition of observations, per-thread n x r
  * accumulators merged in thread order.  Multiset semantics (duplicates are summed).
  * Computes yhat only (the scatter-gather core); the caller adds the K multiplies. */
+/* Row-major copy of a column-major n x r matrix (layout only: the streaming passes below read a
+ * factor / Xhat row and update an accumulator row as contiguous memory; no arithmetic changes). */
+static double* to_rows(const double* a, int64_t n, int64_t r) {
+    double* t = (double*)malloc(sizeof(double) * (n * r > 0 ? n * r : 1));
+    if (!t) return NULL;
+    for (int64_t j = 0; j < r; ++j)
+        for (int64_t i = 0; i < n; ++i) t[i * r + j] = a[i + n * j];
+    return t;
+}
+
+/* The per-observation pass of orc_scatter_gather_stream on observations [lo, hi): for each l in
+ * storage order, z = prod of the other factors' rows (ascending mode, from ones), s = xhat(row,:) .
+ * z summed j = 0..r-1, acc(row,:) += s z.  Groups of GRP observations interleave their dots (each
+ * dot keeps its own ascending order) and then apply their updates in storage order, so the result
+ * is bit-identical to the one-observation-at-a-time loop. */
+#define GRP 4
+static void stream_pass(int d, int k, int64_t q, const int32_t* idx, int64_t r, double* const* frows,
+                        const double* xrows, int64_t lo, int64_t hi, double* acc) {
+    const int32_t* ik = idx + (int64_t)k * q;
+    double z[GRP][256];
+    for (int64_t l0 = lo; l0 < hi; l0 += GRP) {
+        const int g = hi - l0 < GRP ? (int)(hi - l0) : GRP;
+        double s[GRP];
+        for (int b = 0; b < g; ++b) {
+            const int64_t l = l0 + b;
+            for (int64_t j = 0; j < r; ++j) z[b][j] = 1.0;
+            for (int i = 0; i < d; ++i) {
+                if (i == k) continue;
+                const double* a = frows[i] + (int64_t)idx[(int64_t)i * q + l] * r;
+                for (int64_t j = 0; j < r; ++j) z[b][j] *= a[j];
+            }
+            s[b] = 0.0;
+        }
+        if (g == GRP) {
+            const double* x0 = xrows + (int64_t)ik[l0] * r;
+            const double* x1 = xrows + (int64_t)ik[l0 + 1] * r;
+            const double* x2 = xrows + (int64_t)ik[l0 + 2] * r;
+            const double* x3 = xrows + (int64_t)ik[l0 + 3] * r;
+            for (int64_t j = 0; j < r; ++j) {
+                s[0] += x0[j] * z[0][j];
+                s[1] += x1[j] * z[1][j];
+                s[2] += x2[j] * z[2][j];
+                s[3] += x3[j] * z[3][j];
+            }
+        } else {
+            for (int b = 0; b < g; ++b) {
+                const double* xr = xrows + (int64_t)ik[l0 + b] * r;
+                for (int64_t j = 0; j < r; ++j) s[b] += xr[j] * z[b][j];
+            }
+        }
+        for (int b = 0; b < g; ++b) {
+            double* ar = acc + (int64_t)ik[l0 + b] * r;
+            for (int64_t j = 0; j < r; ++j) ar[j] += s[b] * z[b][j];
+        }
+    }
+}
+
 int orc_scatter_gather_stream(int d, const int64_t* shape, int k, int64_t q, const int32_t* idx,
                               int64_t r, const double* const* factors, int64_t n,
                               const double* xhat, double* yhat, int threads) {
     if (threads < 1) threads = 1;
+    if (r > 256) return fail(1, "orc_scatter_gather_stream: rank above 256");
     double* part = (double*)calloc((size_t)threads * n * r, sizeof(double));
-    if (!part) return fail(2, "orc_scatter_gather_stream: out of memory");
+    double* frows[16] = {0};
+    double* xrows = to_rows(xhat, n, r);
+    int oom = !part || !xrows;
+    for (int i = 0; i < d && !oom; ++i)
+        if (i != k && !(frows[i] = to_rows(factors[i], shape[i], r))) oom = 1;
+    if (!oom) {
 #pragma omp parallel num_threads(threads)
-    {
+        {
 #ifdef _OPENMP
-        const int t = omp_get_thread_num();
-        const int nt = omp_get_num_threads();
+            const int t = omp_get_thread_num();
+            const int nt = omp_get_num_threads();
 #else
-        const int t = 0, nt = 1;
+            const int t = 0, nt = 1;
 #endif
-        const int64_t lo = q * t / nt, hi = q * (t + 1) / nt;
-        double* acc = part + (int64_t)t * n * r;
-        double z[256];
-        const int32_t* ik = idx + (int64_t)k * q;
-        for (int64_t l = lo; l < hi; ++l) {
-            for (int64_t j = 0; j < r; ++j) z[j] = 1.0;
-            for (int i = 0; i < d; ++i) {
-                if (i == k) continue;
-                const double* a = factors[i];
-                const int64_t row = idx[(int64_t)i * q + l], ni = shape[i];
-                for (int64_t j = 0; j < r; ++j) z[j] *= a[row + ni * j];
-            }
-            const int64_t row = ik[l];
-            double s = 0.0;
-            for (int64_t j = 0; j < r; ++j) s += xhat[row + n * j] * z[j];
-            for (int64_t j = 0; j < r; ++j) acc[row + n * j] += s * z[j];
+            stream_pass(d, k, q, idx, r, frows, xrows, q * t / nt, q * (t + 1) / nt, part + (int64_t)t * n * r);
         }
+        /* merge in thread order (accumulators are row-major) */
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < r; ++j) {
+                double s = 0.0;
+                for (int t = 0; t < threads; ++t) s += part[(int64_t)t * n * r + i * r + j];
+                yhat[i + n * j] = s;
+            }
     }
-    for (int64_t e = 0; e < n * r; ++e) {
-        double s = 0.0;
-        for (int t = 0; t < threads; ++t) s += part[(int64_t)t * n * r + e];
-        yhat[e] = s;
-    }
+    for (int i = 0; i < d; ++i) free(frows[i]);
+    free(xrows);
     free(part);
-    return 0;
+    return oom ? fail(2, "orc_scatter_gather_stream: out of memory") : 0;
 }
 
 /* Streaming sampled MTTKRP with the observed values (RHS B, unaligned.hpp:44). */
@@ -226,39 +278,46 @@ int orc_sampled_mttkrp_stream(int d, const int64_t* shape, int k, int64_t q, con
                               const double* values, int64_t r, const double* const* factors,
                               int64_t n, double* b, int threads) {
     if (threads < 1) threads = 1;
+    if (r > 256) return fail(1, "orc_sampled_mttkrp_stream: rank above 256");
     double* part = (double*)calloc((size_t)threads * n * r, sizeof(double));
-    if (!part) return fail(2, "orc_sampled_mttkrp_stream: out of memory");
+    double* frows[16] = {0};
+    int oom = !part;
+    for (int i = 0; i < d && !oom; ++i)
+        if (i != k && !(frows[i] = to_rows(factors[i], shape[i], r))) oom = 1;
+    if (!oom) {
 #pragma omp parallel num_threads(threads)
-    {
+        {
 #ifdef _OPENMP
-        const int t = omp_get_thread_num();
-        const int nt = omp_get_num_threads();
+            const int t = omp_get_thread_num();
+            const int nt = omp_get_num_threads();
 #else
-        const int t = 0, nt = 1;
+            const int t = 0, nt = 1;
 #endif
-        const int64_t lo = q * t / nt, hi = q * (t + 1) / nt;
-        double* acc = part + (int64_t)t * n * r;
-        double z[256];
-        const int32_t* ik = idx + (int64_t)k * q;
-        for (int64_t l = lo; l < hi; ++l) {
-            for (int64_t j = 0; j < r; ++j) z[j] = 1.0;
-            for (int i = 0; i < d; ++i) {
-                if (i == k) continue;
-                const double* a = factors[i];
-                const int64_t row = idx[(int64_t)i * q + l], ni = shape[i];
-                for (int64_t j = 0; j < r; ++j) z[j] *= a[row + ni * j];
+            const int64_t lo = q * t / nt, hi = q * (t + 1) / nt;
+            double* acc = part + (int64_t)t * n * r;
+            double z[256];
+            const int32_t* ik = idx + (int64_t)k * q;
+            for (int64_t l = lo; l < hi; ++l) {
+                for (int64_t j = 0; j < r; ++j) z[j] = 1.0;
+                for (int i = 0; i < d; ++i) {
+                    if (i == k) continue;
+                    const double* a = frows[i] + (int64_t)idx[(int64_t)i * q + l] * r;
+                    for (int64_t j = 0; j < r; ++j) z[j] *= a[j];
+                }
+                double* ar = acc + (int64_t)ik[l] * r;
+                for (int64_t j = 0; j < r; ++j) ar[j] += values[l] * z[j];
             }
-            const int64_t row = ik[l];
-            for (int64_t j = 0; j < r; ++j) acc[row + n * j] += values[l] * z[j];
         }
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < r; ++j) {
+                double s = 0.0;
+                for (int t = 0; t < threads; ++t) s += part[(int64_t)t * n * r + i * r + j];
+                b[i + n * j] = s;
+            }
     }
-    for (int64_t e = 0; e < n * r; ++e) {
-        double s = 0.0;
-        for (int t = 0; t < threads; ++t) s += part[(int64_t)t * n * r + e];
-        b[e] = s;
-    }
+    for (int i = 0; i < d; ++i) free(frows[i]);
     free(part);
-    return 0;
+    return oom ? fail(2, "orc_sampled_mttkrp_stream: out of memory") : 0;
 }
 
 /* Full streaming matvec (configs 3/4 CPU baseline): xhat = K X; yhat = stream; y = K yhat +

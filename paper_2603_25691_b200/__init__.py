@@ -37,7 +37,7 @@ __all__ = [
     "UnalignedAlsState", "FitIteration", "AlignedAlsState", "update_finite_mode_aligned",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
     "aligned_matvec", "solve_aligned_pcg", "solve_aligned_direct",
-    "aligned_solve", "Mt19937_64", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
+    "aligned_solve", "Mt19937_64", "synth_observations_device", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
 
 
@@ -100,45 +100,10 @@ def default_context() -> Context:
 
 
 # ---- RNG (std::mt19937_64 + libstdc++ distributions; test/bench inputs) -------------------
-class Mt19937_64:
-    def __init__(self, seed: int):
-        h = ctypes.c_void_p()
-        call("cphifi_rng_create", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), ctypes.byref(h))
-        self.h = h
-
-    def __del__(self):
-        if getattr(self, "h", None):
-            _capi.load().cphifi_rng_destroy(self.h)
-
-    def __call__(self) -> int:
-        return int(self.next_u64(1)[0])
-
-    def next_u64(self, count: int) -> np.ndarray:
-        out = np.zeros(count, dtype=np.uint64)
-        call("cphifi_rng_next_u64", self.h, out.ctypes.data_as(_capi.c_uint64_p), count)
-        return out
-
-    def uniform_real(self, lo: float, hi: float, count: int) -> np.ndarray:
-        out = np.zeros(count)
-        call("cphifi_rng_uniform_real", self.h, lo, hi, _dp(out), count)
-        return out
-
-    def uniform_int(self, lo: int, hi: int, count: int = 1) -> np.ndarray:
-        out = np.zeros(count, dtype=np.int64)
-        call("cphifi_rng_uniform_int", self.h, lo, hi, out.ctypes.data_as(c_int64_p), count)
-        return out
-
-    def normal(self, mean: float, std: float, count: int) -> np.ndarray:
-        out = np.zeros(count)
-        call("cphifi_rng_normal", self.h, mean, std, _dp(out), count)
-        return out
-
-    def normal_reset(self) -> None:
-        call("cphifi_rng_normal_reset", self.h)
-
-    def random_matrix(self, rows: int, cols: int, lo=-1.0, hi=1.0) -> np.ndarray:
-        """test_util.hpp:10-17: column-major fill."""
-        return np.asfortranarray(self.uniform_real(lo, hi, rows * cols).reshape((rows, cols), order="F"))
+# The seeded input generators live in the separate `inputs` library (inputs/synth_host.cpp), so
+# that bench.py's reference arm and the oracle never load this package's library.
+from inputs import Mt19937_64  # noqa: E402  (re-exported: the reference tests' RNG)
+from inputs import sample_uniform_linear as _sample_uniform_linear  # noqa: E402
 
 
 # ---- kernel.hpp ------------------------------------------------------------------------
@@ -422,9 +387,9 @@ class _Handle:
 def sample_uniform(source: DenseTensor, q: int, seed: int, multiset: bool = False) -> ObservationSet:
     """observations.hpp:90-121: q distinct entries drawn by partial Fisher-Yates."""
     n_total = source.size()
-    picked = np.zeros(max(q, 0), dtype=np.int64)
-    call("cphifi_sample_uniform_linear", n_total, q, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF),
-         picked.ctypes.data_as(c_int64_p))
+    if q > n_total:
+        raise CphifiInvalidArgument("sample_uniform: q exceeds tensor size")
+    picked = _sample_uniform_linear(n_total, q, seed)
     shape = source.shape()
     idx = np.zeros((len(shape), q), dtype=np.int64)
     lin = picked.copy()
@@ -942,3 +907,21 @@ def aligned_solve(t: DenseTensor, model: KruskalModel, k: int, mode: RkhsMode):
     v = np.zeros((r, r), order="F")
     call("cphifi_aligned_solve", dt.handle, mode.handle, k, r, ptrs, _dp(w), _dp(b), _dp(v))
     return w, b, v
+
+
+def synth_observations_device(cfg, ctx: Context, q: int | None = None):
+    """Draw cfg's observations (inputs.configs.DeviceUnalignedConfig) on cfg's GPU with the
+    counter-based generator (cphifi_synth_observations; bit-identical to inputs.configs.generate_host):
+    returns torch tensors idx (d, q) int32 and vals (q,) fp64."""
+    import torch
+    q = cfg.q if q is None else q
+    d = len(cfg.shape)
+    dev = torch.device("cuda", ctx.device)
+    idx = torch.empty((d, q), dtype=torch.int32, device=dev)
+    vals = torch.empty(q, dtype=torch.float64, device=dev)
+    shape = np.ascontiguousarray(cfg.shape, dtype=np.int64)
+    facs = [np.asfortranarray(f) for f in cfg.factors]
+    ptrs = (c_double_p * d)(*[f.ctypes.data_as(c_double_p) for f in facs])
+    call("cphifi_synth_observations", ctx.handle, d, shape.ctypes.data_as(c_int64_p), q, ctypes.c_uint64(cfg.seed),
+         cfg.zipf_mode, cfg.zipf_s, cfg.r, ptrs, cfg.noise_std, idx.data_ptr(), vals.data_ptr())
+    return idx, vals

@@ -162,14 +162,6 @@ _SIGS = [
     ("cphifi_synth_observations", ctypes.c_int,
      [_H, ctypes.c_int, c_int64_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
       ctypes.POINTER(c_double_p), ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
-    ("cphifi_rng_create", ctypes.c_int, [ctypes.c_uint64, c_void_pp]),
-    ("cphifi_rng_destroy", ctypes.c_int, [_H]),
-    ("cphifi_rng_next_u64", ctypes.c_int, [_H, c_uint64_p, ctypes.c_int64]),
-    ("cphifi_rng_uniform_real", ctypes.c_int, [_H, ctypes.c_double, ctypes.c_double, c_double_p, ctypes.c_int64]),
-    ("cphifi_rng_uniform_int", ctypes.c_int, [_H, ctypes.c_int64, ctypes.c_int64, c_int64_p, ctypes.c_int64]),
-    ("cphifi_rng_normal", ctypes.c_int, [_H, ctypes.c_double, ctypes.c_double, c_double_p, ctypes.c_int64]),
-    ("cphifi_rng_normal_reset", ctypes.c_int, [_H]),
-    ("cphifi_sample_uniform_linear", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, c_int64_p]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

@@ -31,6 +31,7 @@ def _sources():
 def _headers_mtime():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     hs.append(os.path.join(ROOT, "include", "cphifi_b200.h"))
+    hs.append(os.path.join(ROOT, "inputs", "synth_math.h"))
     return max(os.path.getmtime(h) for h in hs)
 
 

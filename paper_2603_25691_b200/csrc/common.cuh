@@ -215,4 +215,3 @@ struct cphifi_tensor_s {
     bool have_norm = false;
 };
 
-struct cphifi_rng_s;

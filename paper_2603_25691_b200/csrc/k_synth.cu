@@ -1,30 +1,16 @@
 // k_synth.cu — seeded synthetic observations generated on the device (configs 3 and 4).
 //
-// BASELINE configs 3/4 hold 2e8 / 1e9 observations (4.8 / 20 GB): they are drawn on the GPU
-// with a counter-based generator so that every draw is a pure function of (seed, l, stream)
-// and the stream is bit-identical run to run (tests/test_synth.py re-derives draws on the host
-// with the same integer arithmetic).  Not part of the solver path.
-//   u64(l, s) = splitmix64(seed ^ splitmix64(l * 0x9E3779B97F4A7C15 + s))
-//   uniform index in [0, n): (u64 >> 32) * n >> 32;  uniform double: (u64 >> 11) * 2^-53
-//   Zipf mode: smallest i with cdf[i] > u (host-built CDF of (i+1)^-s)
-//   value = sum_j prod_m A_m(i_m, j) + noise_std * N(0,1)  (Box-Muller on two uniforms)
+// BASELINE configs 3/4 hold 2e8 / 1e9 observations (4.8 / 20 GB): they are drawn on the GPU with
+// the counter-based generator of inputs/synth_math.h, so every draw is a pure function of (seed, l,
+// stream) and bit-identical to the host generator inputs/synth_host.cpp (the oracle's inputs;
+// tests/test_gpu_synth.py compares the two).  Not part of the solver path.
 #include <cmath>
 
+#include "../../inputs/synth_math.h"
 #include "kernels.cuh"
 
 namespace cphifi {
 namespace {
-
-__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
-    x += 0x9E3779B97F4A7C15ull;
-    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-    return x ^ (x >> 31);
-}
-
-__device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t l, uint64_t s) {
-    return splitmix64(seed ^ splitmix64(l * 0x9E3779B97F4A7C15ull + s));
-}
 
 struct SynthArgs {
     int d = 0;
@@ -44,31 +30,17 @@ __global__ void synth_kernel(const SynthArgs a) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < a.q; l += (int64_t)gridDim.x * blockDim.x) {
         int64_t ix[8];
         for (int m = 0; m < a.d; ++m) {
-            const uint64_t u = draw(a.seed, (uint64_t)l, (uint64_t)m);
-            const uint64_t n = (uint64_t)a.shape[m];
-            if (m == a.zipf_mode) {
-                const double v = (double)(u >> 11) * 0x1.0p-53;
-                int64_t lo = 0, hi = a.shape[m] - 1;  // smallest i with cdf[i] > v
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (a.zipf_cdf[mid] > v) hi = mid; else lo = mid + 1;
-                }
-                ix[m] = lo;
-            } else {
-                ix[m] = (int64_t)(((u >> 32) * n) >> 32);
-            }
+            const uint64_t u = syn_draw(a.seed, (uint64_t)l, (uint64_t)m);
+            ix[m] = m == a.zipf_mode ? syn_zipf_index(u, a.zipf_cdf, a.shape[m]) : syn_uniform_index(u, a.shape[m]);
             a.idx[(int64_t)m * a.q + l] = (int32_t)ix[m];
         }
         double v = 0.0;
         for (int64_t j = 0; j < a.r; ++j) {
             double p = a.fac[0][ix[0] + a.shape[0] * j];
-            for (int m = 1; m < a.d; ++m) p *= a.fac[m][ix[m] + a.shape[m] * j];
-            v += p;
+            for (int m = 1; m < a.d; ++m) p = SYN_MUL(p, a.fac[m][ix[m] + a.shape[m] * j]);
+            v = SYN_ADD(v, p);
         }
-        const uint64_t u1 = draw(a.seed, (uint64_t)l, 64), u2 = draw(a.seed, (uint64_t)l, 65);
-        const double f1 = ((double)(u1 >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
-        const double f2 = (double)(u2 >> 11) * 0x1.0p-53;
-        a.vals[l] = v + a.noise_std * (sqrt(-2.0 * log(f1)) * cos(6.283185307179586 * f2));
+        a.vals[l] = SYN_ADD(v, SYN_MUL(a.noise_std, syn_normal(a.seed, (uint64_t)l)));
     }
 }
 
@@ -90,7 +62,7 @@ void synth_observations(int d, const int64_t* shape, int64_t q, uint64_t seed, i
     a.idx = idx;
     a.vals = vals;
     DevBuf<double> cdf;
-    if (zipf_mode >= 0) {
+    if (zipf_mode >= 0) {  // the host table of inputs/synth_host.cpp inp_zipf_cdf, same arithmetic
         const int64_t n = shape[zipf_mode];
         std::vector<double> h(n);
         double tot = 0.0;

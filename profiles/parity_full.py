@@ -19,13 +19,13 @@ import torch  # noqa: E402
 
 import paper_2603_25691_b200 as cp  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
-from paper_2603_25691_b200 import configs  # noqa: E402
+from inputs import configs  # noqa: E402
 
 
 def run(which, ctx, max_iter, tol):
     cfg = getattr(configs, which)()
     n, r = cfg.shape[0], cfg.r
-    idx_d, vals_d = configs.generate_device(cfg, ctx)
+    idx_d, vals_d = cp.synth_observations_device(cfg, ctx)
     torch.cuda.synchronize()
     idx = idx_d.cpu().numpy().reshape(len(cfg.shape), -1)
     vals = vals_d.cpu().numpy().reshape(-1)

@@ -19,7 +19,7 @@ lib = _capi.load()
 for which in sys.argv[1:] or ["config3"]:
     cfg = getattr(configs, which)()
     n, r = cfg.shape[0], cfg.r
-    idx, vals = configs.generate_device(cfg, ctx)
+    idx, vals = cp.synth_observations_device(cfg, ctx)
     torch.cuda.synchronize()
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
     obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), cfg.q, keepalive=(idx, vals),

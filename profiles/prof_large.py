@@ -37,7 +37,7 @@ def main():
     lib = _capi.load()
     out = {"config": cfg.name, "q": q, "n": n, "r": r, "d": d}
     t0 = time.perf_counter()
-    idx, vals = configs.generate_device(cfg, ctx, q)
+    idx, vals = cp.synth_observations_device(cfg, ctx, q)
     torch.cuda.synchronize()
     out["gen_s"] = time.perf_counter() - t0
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)

@@ -17,7 +17,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2603_25691_b200 as cp  # noqa: E402
-from paper_2603_25691_b200 import configs  # noqa: E402
+from inputs import configs  # noqa: E402
 
 
 def main():
@@ -28,7 +28,7 @@ def main():
     ctx = cp.Context(0)
     cfg = getattr(configs, f"config{args.config}")()
     n, r, q = cfg.shape[0], cfg.r, cfg.q
-    idx, vals = configs.generate_device(cfg, ctx)
+    idx, vals = cp.synth_observations_device(cfg, ctx)
     torch.cuda.synchronize()
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
     obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),

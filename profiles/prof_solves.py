@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 
 import bench_secondary as bs  # noqa: E402
 import paper_2603_25691_b200 as cp  # noqa: E402
-from paper_2603_25691_b200 import configs  # noqa: E402
+from inputs import configs  # noqa: E402
 
 
 def main():

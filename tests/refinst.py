@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import numpy as np
 
-import paper_2603_25691_b200 as cp
+from inputs import Mt19937_64
 from oracle import oracle as orc
 
 
@@ -34,11 +34,8 @@ def random_model(shape, r, rng):
 
 def sample(shape, flat, q, seed):
     """sample_uniform (observations.hpp:90-121): (d, q) int32 indices and values."""
-    import ctypes
-    from paper_2603_25691_b200 import _capi
-    picked = np.zeros(q, dtype=np.int64)
-    _capi.call("cphifi_sample_uniform_linear", int(flat.size), q, ctypes.c_uint64(seed & (2**64 - 1)),
-               picked.ctypes.data_as(_capi.c_int64_p))
+    from inputs import sample_uniform_linear
+    picked = sample_uniform_linear(int(flat.size), q, seed)
     idx = np.zeros((len(shape), q), dtype=np.int32)
     lin = picked.copy()
     for k, s in enumerate(shape):
@@ -70,7 +67,7 @@ class Inst:
 
     def __init__(self, shape, r, q, k, sigma, lam, rho, seed, acceptance_rng=None):
         if acceptance_rng is None:
-            rng = cp.Mt19937_64(seed)
+            rng = Mt19937_64(seed)
             self.flat = random_tensor(shape, rng)
             self.idx, self.vals = sample(shape, self.flat, q, seed + 1)
             self.factors = random_model(shape, r, rng)

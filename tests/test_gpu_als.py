@@ -30,7 +30,7 @@ def _fitted(a_k, others, idx):
 
 
 def test_unaligned_update_config1(cp):
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = configs.config1()
     n, r = c.shape[0], c.r
     mode = cp.RkhsMode(c.points, c.ell, c.lam)
@@ -79,7 +79,7 @@ def test_unaligned_update_small_orders(cp):
 
 @pytest.mark.parametrize("which", ["config0"])
 def test_aligned_update(cp, which):
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = getattr(configs, which)()
     n, r = c.shape[0], c.r
     mode = cp.RkhsMode(c.points, c.ell, c.lam)
@@ -215,7 +215,7 @@ def test_mttkrp_middle_and_last_modes(cp, shape, r):
 def test_aligned_finite_update_and_sweeps(cp):
     """update_finite_mode (aligned, als.hpp:139-143: A_k = B_k V_k^+) and three whole aligned sweeps
     (mode 0 infinite, decoupled) on config 0 vs a numpy restatement with the same eig(K)."""
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = configs.config0()
     n, r = c.shape[0], c.r
     mode = cp.RkhsMode(c.points, c.ell, c.lam)

@@ -74,7 +74,7 @@ def test_gram_auto_resolution(cp):
 
 def test_gram_pcg_config1(cp):
     """Config 1 PCG with the row-Gram operator: iterations within +-1, residual <= 1e-8."""
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = configs.config1()
     mode = cp.RkhsMode(c.points, c.ell, c.lam)
     kern = mode.kernel()
@@ -98,10 +98,10 @@ def test_gram_pcg_config1(cp):
 
 @pytest.mark.parametrize("which,q", [("config3", 2_000_000), ("config4", 3_000_000)])
 def test_gram_large_config_structure(cp, which, q):
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     cfg = getattr(configs, which)()
     ctx = cp.default_context()
-    idx, vals = configs.generate_device(cfg, ctx, q)
+    idx, vals = cp.synth_observations_device(cfg, ctx, q)
     hidx = idx.cpu().numpy()
     n, r = cfg.shape[0], cfg.r
     mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)

@@ -214,7 +214,7 @@ def test_row_order_irrelevant(cp):
 
 def test_config1_pcg_parity(cp):
     """BASELINE config 1 at full size: iterations within +-1 of the oracle, residual <= 1e-8."""
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = configs.config1()
     mode = cp.RkhsMode(c.points, c.ell, c.lam)
     kern = mode.kernel()
@@ -298,7 +298,7 @@ def test_acceptance_c1_decoupled_device(cp):
 @pytest.mark.parametrize("which", ["config0", "config2"])
 def test_aligned_config_parity(cp, which):
     """W relative error <= 1e-10 vs the oracle with a shared eig(K), eig(V)."""
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = getattr(configs, which)()
     mode = cp.RkhsMode(c.points, c.ell, c.lam)
     kern = mode.kernel()
@@ -373,10 +373,10 @@ def test_large_config_structure_vs_oracle(cp, which, q, coalesce):
     device generation -> device sort/CSR plan (multiset) -> operator, against the oracle's
     streaming restatement on the same draws (copied back)."""
     import torch
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     cfg = getattr(configs, which)()
     ctx = cp.default_context()
-    idx, vals = configs.generate_device(cfg, ctx, q)
+    idx, vals = cp.synth_observations_device(cfg, ctx, q)
     hidx, hvals = idx.cpu().numpy(), vals.cpu().numpy()
     n, r = cfg.shape[0], cfg.r
     assert hidx.min() >= 0 and all(hidx[m].max() < cfg.shape[m] for m in range(len(cfg.shape)))

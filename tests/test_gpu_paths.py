@@ -73,7 +73,7 @@ def test_decoupled_sandwich_variants(cp, monkeypatch, n, r):
 
 
 def _config1_problem(cp, shared=True):
-    from paper_2603_25691_b200 import configs
+    from inputs import configs
     c = configs.config1()
     n, r = c.shape[0], c.r
     mode = cp.RkhsMode(c.points, c.ell, c.lam)

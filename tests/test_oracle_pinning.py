@@ -17,8 +17,9 @@ def _built(built_lib):
 
 
 def _cp():
-    import paper_2603_25691_b200 as cp
-    return cp
+    """The seeded generators (inputs/): the oracle tests never load the product library."""
+    import inputs
+    return inputs
 
 
 # ---- kernel.hpp / test_kernel.cpp --------------------------------------------------------
