@@ -1,22 +1,31 @@
 #!/usr/bin/env python
-"""Benchmark: unaligned PCG operator applications (matvecs/s) at BASELINE.json config 1.
+"""Benchmark: unaligned PCG operator applications (matvecs/s) at BASELINE.json config 4.
 
 One "step" = one application of the unaligned normal-equation operator
   y = (F'F + lambda (I kron K) + rho I) x          (unaligned.hpp:101-115)
-over all q = 200,000 observations of config 1 (n=200, 100x100 other modes, r=10), i.e. the
-PCG hot loop.  `value` is device-timed with inputs resident in HBM and the L2 flushed before
-every step (the working set is 3 MB, far below the 126 MB L2); `e2e` is the same metric
-through the C-ABI host-buffer call (x uploaded from pinned host memory, y read back each
-step).  `roofline` reports the scatter-gather kernel (K1) against the measured HBM peak.
+over ALL q = 1e9 draws of config 4 (4096 x 512 x 512, i_1 ~ Zipf(1.1), r = 64): X^ = K X, the
+per-observation gather / scatter (observations.hpp:174-198) as one streaming pass over the plan
+(the q-pass is inside the timed region: the STREAM operator, not the prebuilt row-Gram form), then
+K Y^ + lambda X^ + rho x.  Config 4 is the largest BASELINE config that fits one GPU (BASELINE's
+metric names none), so it is the N = 1 workload.
+
+`value` is device-timed (CUDA events on the library stream) with the plan resident in HBM; every
+application streams the ~2.9 GB coalesced plan, far above the 126 MB L2 (inputs larger than L2).
+`e2e` is the same metric through the reference-facing host-buffer C-ABI call
+(cphifi_unaligned_matvec: x copied in from pinned host memory, y read back, every step).
+`roofline` is the dominant kernel (the streaming scatter-gather, k_stream.cu) against the
+measured HBM peak on the as-given algorithmic bytes of SURVEY §8(d); `cpu_baseline` is the
+oracle's streaming C port on a bounded sample of the same draws.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Under torchrun (N > 1) the observations are sharded over ranks (equal-count slices of the
-i_k-sorted set) and the n x r partial accumulator is NCCL all-reduced every step.
+Under torchrun (N > 1) the observations are sharded over ranks (equal-count slices of the i_k-sorted
+plan) and the n x r partial accumulator is NCCL all-reduced every application.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes
+import glob
 import json
 import os
 import statistics
@@ -29,14 +38,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK_HBM = 6650.0
+METRIC = "unaligned PCG matvecs/s (config 4: q=1e9 draws, 4096x512x512, r=64)"
+WORKLOAD = ("config4: unaligned skewed 3-way 4096x512x512, q=1e9 draws (i_1 ~ Zipf(1.1), i_2, i_3 uniform; "
+            "coalesced plan of the distinct entries with multiplicities), r=64, lambda=1e-5, rho=1e-6; one step = one "
+            "operator application y = (F'F + lambda I(x)K + rho I) x over all q draws (stream operator: the q-pass is "
+            "inside the timed region)")
 
 
 def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return PEAKS_FALLBACK_HBM, "fallback"
+        return PEAKS_FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -53,10 +67,11 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.15)
         except Exception:
             self.proc = None
         return self
@@ -67,7 +82,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
@@ -90,12 +105,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kernel_substr):
+def ncu_traffic(capture, kernel_substr):
     """DRAM bytes per launch (read + write) of the named kernel from the committed `ncu --set full`
-    capture of this bench's own command (profiles/round*/ncu_full_*.json, newest round first)."""
-    import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_full_fused_matvec_config1.json")),
-                       reverse=True):
+    capture of this bench's workload (profiles/round*/<capture>, newest round first)."""
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", capture)), reverse=True):
         try:
             caps = [d for d in json.load(open(path)) if kernel_substr in d["kernel"]]
         except Exception:
@@ -106,101 +119,96 @@ def ncu_traffic(kernel_substr):
 
 
 def alg_bytes_matvec(d, q, n, r):
-    """unaligned matvec algorithmic bytes (int32 index stream read once,
-    K read twice, six n x r fp64 vectors)."""
+    """unaligned matvec algorithmic bytes on the as-given draws (int32 index stream read
+    once, K read twice, six n x r fp64 vectors)."""
     return 4 * d * q + 16 * n * n + 48 * n * r
 
 
+def alg_flops_matvec(d, q, n, r):
+    return (d + 2) * r * q + 4 * n * n * r
+
+
 def alg_bytes_k1(d, q, n, r):
-    """Scatter-gather kernel (K1): the d int32 index streams + Xhat rows read + Yhat written."""
+    """Streaming scatter-gather kernel: the d int32 index streams + Xhat rows read + Yhat written."""
     return 4 * d * q + 16 * n * r
 
 
-def cpu_port_matvec(c, threads, seconds):
-    """The oracle's fused streaming restatement on `threads` host cores (test/bench baseline)."""
+# ---- CPU side (the oracle's streaming port; test infrastructure, never the measured GPU path) ------
+def cpu_config4_sample(threads, q_sample, reps_target_s, seed_off=0):
+    """Time the oracle's fused streaming restatement (oracle/cphifi_oracle.c, SURVEY §8c mode ii) on
+    config 4: the dense part (K X, K Yhat, axpys) timed whole, the per-observation pass on draws
+    [off, off + q_sample) of the same generator, extrapolated to q = 1e9 draws.
+    Returns (seconds per application, detail dict)."""
     import numpy as np
+
+    from inputs import configs
     from oracle import oracle as orc
-    from inputs.configs import kernel_matrix
-    kern = kernel_matrix(c.points, c.kernel, c.ell)
-    factors = [None] + c.factors[1:]
-    x = np.random.default_rng(0).normal(size=c.shape[0] * c.r)
-    orc.unaligned_matvec_stream(c.shape, 0, c.idx, factors, kern, c.lam, c.rho, x, threads)  # warm
-    n_done, t0 = 0, time.perf_counter()
+    cfg = configs.config4()
+    n, r = cfg.shape[0], cfg.r
+    idx, _ = configs.generate_host(cfg, seed_off, seed_off + q_sample, values=False, threads=threads)
+    kern = orc.gaussian_kernel(cfg.points, cfg.ell)
+    factors = [None] + cfg.factors[1:]
+    x = np.random.default_rng(0).normal(size=n * r)
+    empty = np.zeros((3, 0), dtype=np.int32)
+    t0 = time.perf_counter()
+    orc.unaligned_matvec_stream(cfg.shape, 0, empty, factors, kern, cfg.lam, cfg.rho, x, threads)
+    t_dense = time.perf_counter() - t0
+    xhat = np.asfortranarray(np.random.default_rng(1).normal(size=(n, r)))
+    orc.scatter_gather_stream(cfg.shape, 0, idx[:, : min(q_sample, 200_000)], factors, xhat, threads)  # warm
+    reps, t0 = 0, time.perf_counter()
     while True:
-        orc.unaligned_matvec_stream(c.shape, 0, c.idx, factors, kern, c.lam, c.rho, x, threads)
-        n_done += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
+        orc.scatter_gather_stream(cfg.shape, 0, idx, factors, xhat, threads)
+        reps += 1
+        if time.perf_counter() - t0 >= reps_target_s:
             break
-    return n_done / el, n_done
-
-
-def secondary(args, ctx, cp, p, c, lib, x, y, stream, flush):
-    """Other BASELINE configs and the PCG solve, measured in the same run (N = 1)."""
-    import bench_secondary as bs
-    sec = {}
-
-    def attempt(key, fn):
-        try:
-            sec[key] = fn()
-        except Exception as e:  # report, never hide: the key carries the failure
-            sec[key] = {"error": f"{type(e).__name__}: {e}"}
-
-    attempt("fp64_peak", lambda: bs.fp64_peaks(ctx))
-    fp64 = sec["fp64_peak"].get("dmma_tflops", 40.0) if isinstance(sec["fp64_peak"], dict) else 40.0
-    attempt("config1_pcg_solve", lambda: bs.config1_pcg(cp, p, c))
-    attempt("config1_gram_matvec_ms_l2_flushed", lambda: bs.gram_matvec_ms(p, lib, x, y, stream, flush))
-    attempt("config1_precond_apply_ms", lambda: bs.precond_ms(p, lib, c.shape[0], c.r))
-    attempt("config0_aligned", lambda: bs.aligned("config0", ctx, 20, fp64))
-    attempt("config2_aligned", lambda: bs.aligned("config2", ctx, 10, fp64))
-    attempt("als_infinite_update", lambda: bs.als_updates(ctx, p, c))
-    if args.large:
-        attempt("config3", lambda: bs.large("config3", ctx, fp64_tf=fp64))
-        attempt("config4", lambda: bs.large("config4", ctx, fp64_tf=fp64))
-    return sec
+    t_stream = (time.perf_counter() - t0) / reps
+    per_app = t_dense + t_stream * (cfg.q / q_sample)
+    return per_app, {"t_dense_s": t_dense, "t_stream_sample_s": t_stream, "q_sample": q_sample, "reps": reps}
 
 
 def run_reference(args, rank):
+    """The reference arm: the reference CPU path restated (the reference itself, header-only C++ over
+    Eigen, cannot be built here: SURVEY §8c), i.e. the oracle's streaming port, on all host cores, on
+    config 4 — inputs from inputs/ (never the product library)."""
     if rank != 0:
         return
     from oracle import oracle as orc
-    from inputs import configs
     orc.build()
-    c = configs.config1()
     threads = orc.max_threads()
-    import numpy as np
-    from inputs.configs import kernel_matrix
-    kern = kernel_matrix(c.points, c.kernel, c.ell)
-    factors = [None] + c.factors[1:]
-    x = np.random.default_rng(0).normal(size=c.shape[0] * c.r)
-    for _ in range(args.warmup):
-        orc.unaligned_matvec_stream(c.shape, 0, c.idx, factors, kern, c.lam, c.rho, x, threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        orc.unaligned_matvec_stream(c.shape, 0, c.idx, factors, kern, c.lam, c.rho, x, threads)
-    el = time.perf_counter() - t0
-    v = args.steps / el
-    sample = f"config1 full operator application (q=200000) x {args.steps}, fused streaming C port"
+    q_sample = args.cpu_sample
+    for w in range(args.warmup):
+        cpu_config4_sample(threads, min(q_sample, 2_000_000), 0.0, seed_off=w * q_sample)
+    dense, stream = [], []
+    for s in range(args.steps):
+        _, det = cpu_config4_sample(threads, q_sample, 0.0, seed_off=s * q_sample)
+        dense.append(det["t_dense_s"])
+        stream.append(det["t_stream_sample_s"])
+    t_app = statistics.mean(dense) + statistics.mean(stream) * (1e9 / q_sample)
+    v = 1.0 / t_app
+    sample = (f"config 4, each step: the dense part (2 x 4096^2 x 64 GEMMs + axpys) timed whole plus the per-"
+              f"observation streaming pass on {q_sample} consecutive draws of the 1e9 (step s: draws [s*{q_sample}, "
+              f"(s+1)*{q_sample})), extrapolated x{1e9 / q_sample:.0f}; oracle/cphifi_oracle.c fused streaming "
+              f"restatement, {threads} threads")
     print(json.dumps({
-        "impl": "reference", "metric": "unaligned PCG matvecs/s (config 1, q=200k, r=10)", "value": v,
-        "unit": "matvecs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1)",
-        "config": {"workload": "config1: unaligned 200x100x100, q=200000, r=10, lambda=1e-3, rho=1e-6"},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "matvecs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_app, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 4)",
+        "config": {"workload": WORKLOAD, "parallelism": f"CPU, {threads} threads"},
         "cpu_baseline": {"value": v, "unit": "matvecs/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": {"t_dense_s_mean": statistics.mean(dense), "t_stream_sample_s_mean": statistics.mean(stream)},
     }))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
-    ap.add_argument("--secondary", type=int, default=1, help="aligned configs 0/2, PCG solves, FP64 peaks")
-    ap.add_argument("--large", type=int, default=1, help="configs 3/4 at full size inside --secondary")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline: seconds of streaming work")
+    ap.add_argument("--cpu-sample", type=int, default=20_000_000, help="CPU baseline: draws per sample")
+    ap.add_argument("--secondary", type=int, default=1, help="PCG solves, configs 0-3, CPU baselines 0-3")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
@@ -215,7 +223,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2603_25691_b200 as cp
-    from paper_2603_25691_b200 import _capi, configs
+    from inputs import configs
+    from paper_2603_25691_b200 import _capi
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -226,94 +235,60 @@ def main():
         uid = [cp.Context.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.init_comm(world, rank, uid[0])
-
-    c = configs.config1()
-    n, r, d, q = c.shape[0], c.r, len(c.shape), c.idx.shape[1]
-    mode = cp.RkhsMode(c.points, c.ell, c.lam, ctx=ctx)
-    obs = cp.ObservationSet(c.shape, c.idx, c.vals)
-    model = cp.KruskalModel([np.zeros((n, r))] + c.factors[1:])
-    p = cp.make_unaligned_subproblem(obs, model, 0, mode, c.rho, shard=rank, shards=world)
-
     dev = torch.device("cuda", local)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+
+    cfg = configs.config4()
+    n, r, d, q = cfg.shape[0], cfg.r, len(cfg.shape), cfg.q
+    t0 = time.perf_counter()
+    idx, vals = cp.synth_observations_device(cfg, ctx)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    mode = cp.RkhsMode(cfg.points, cfg.ell, cfg.lam, ctx=ctx, kernel=cfg.kernel)
+    obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),
+                                coalesce=cfg.coalesce)
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    t0 = time.perf_counter()
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho, shard=rank, shards=world)
+    plan_s = time.perf_counter() - t0
+    qt, ql = ctypes.c_int64(), ctypes.c_int64()
+    _capi.check(lib.cphifi_obs_info(obs.plan(0, ctx, rank, world).h, ctypes.byref(qt), ctypes.byref(ql), None))
+    del idx, vals
+    obs.release_inputs()
+    torch.cuda.empty_cache()
+    p.set_operator("stream")  # the q-pass inside every application
+
     x = torch.randn(n * r, dtype=torch.float64, device=dev)
     y = torch.empty_like(x)
-    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
-    ms6 = (ctypes.c_double * 6)()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
-    def step(ev=None):
-        with torch.cuda.stream(stream):
-            flush.add_(1)  # evict L2 (outside the events)
-            if ev:
-                ev[0].record(stream)
-            _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
-            if ev:
-                ev[1].record(stream)
+    def app():
+        _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
 
     for _ in range(args.warmup):
-        step()
+        app()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # timed: the K steps captured in ONE CUDA graph (each step = a 256 MB memset node that evicts
-    # L2, then the operator between its own event pair) -- how the operator runs inside the
-    # device-resident PCG loop.  Plain per-call launches (~4 us host launch cost each on this
-    # system, profiles/micro/launch_rate.cu) are measured next to it as value_plain_launch.
-    gms = (ctypes.c_float * args.steps)()
-    cycle_m = 128
-    if world == 1:
-        # Timed region: K applications back to back in ONE CUDA graph between one event pair,
-        # application t on instance t % 128 of config 1 (its own observation plan, kernel matrix,
-        # factors, x, y: ~2 MB touched each, 128 x 2 MB = 2 x the 126 MB L2), so every application starts
-        # L2-cold with no flush inside the timed region -- the "inputs larger than L2" option.
-        insts = []
-        for i in range(cycle_m):
-            mi = cp.RkhsMode(c.points, c.ell, c.lam, ctx=ctx)
-            oi = cp.ObservationSet(c.shape, c.idx, c.vals)
-            pi = cp.make_unaligned_subproblem(oi, model, 0, mi, c.rho)
-            xi = torch.randn(n * r, dtype=torch.float64, device=dev)
-            insts.append((mi, oi, pi, xi, torch.empty_like(xi)))
-        hp = (ctypes.c_void_p * cycle_m)(*[t[2].handle.value for t in insts])
-        hx = (ctypes.c_void_p * cycle_m)(*[t[3].data_ptr() for t in insts])
-        hy = (ctypes.c_void_p * cycle_m)(*[t[4].data_ptr() for t in insts])
-        tot = ctypes.c_float()
-        with ClockSampler(local) as clk:
-            _capi.check(lib.cphifi_unaligned_matvec_cycle_timed(hp, hx, hy, cycle_m, args.steps, ctypes.byref(tot)))
-            torch.cuda.synchronize()
-        total_ms = float(tot.value)
-        # the per-step flush method (one application between its own events, 256 MB memset node
-        # before each, all in one graph) for comparison
-        _capi.check(lib.cphifi_unaligned_matvec_graph_timed(p.handle, x.data_ptr(), y.data_ptr(),
-                                                            flush.data_ptr(), flush.numel() * 4, args.steps, gms))
-        flush_ms = float(sum(gms))
-        del insts
-    else:  # multi-GPU: NCCL stays outside graph capture; plain launches, per-step L2 flush
-        with ClockSampler(local) as clk:
-            for i in range(args.steps):
-                step(evs[i])
-            torch.cuda.synchronize()
-        total_ms = flush_ms = float(sum(a.elapsed_time(b) for a, b in evs))
-    for i in range(args.steps):
-        step(evs[i])
     torch.cuda.synchronize()
-    plain_ms = sum(a.elapsed_time(b) for a, b in evs)
-    # per-kernel split of the same step (instrumented pass, L2 flushed before each step)
-    phases = [0.0] * 6
-    for _ in range(args.steps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
-            flush.add_(1)
-        _capi.check(lib.cphifi_unaligned_matvec_timed(p.handle, x.data_ptr(), y.data_ptr(), 1, ms6))
-        phases = [a + b for a, b in zip(phases, ms6)]
-    # small n on one GPU the graph step IS the fused kernel (one launch between the events)
-    k1_src = total_ms if (world == 1 and n <= 512) else phases[1]
-    t = torch.tensor([total_ms, k1_src, plain_ms, flush_ms], dtype=torch.float64, device=dev)
+            e0.record(stream)
+            for _ in range(args.steps):
+                app()
+            e1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, k1_ms, plain_ms, flush_ms = float(t[0]), float(t[1]), float(t[2]), float(t[3])
-    value = args.steps / (total_ms / 1e3)
+        dist.barrier()
 
-    # e2e: the reference-facing host-buffer call, H2D of x and D2H of y every step
+    # the dominant kernel: per-phase device times of the same application (events around each phase)
+    ms6 = (ctypes.c_double * 6)()
+    _capi.check(lib.cphifi_unaligned_matvec_timed(p.handle, x.data_ptr(), y.data_ptr(), min(args.steps, 10), ms6))
+    launches = ctypes.c_int()
+    _capi.check(lib.cphifi_unaligned_matvec_launches(p.handle, x.data_ptr(), y.data_ptr(), ctypes.byref(launches)))
+
+    # e2e: the reference-facing host-buffer call, x in from pinned host memory and y back, every step
     hx = torch.randn(n * r, dtype=torch.float64).pin_memory().numpy()
     hy = torch.empty(n * r, dtype=torch.float64).pin_memory().numpy()
     xp, yp = hx.ctypes.data_as(_capi.c_double_p), hy.ctypes.data_as(_capi.c_double_p)
@@ -321,71 +296,79 @@ def main():
         _capi.check(lib.cphifi_unaligned_matvec(p.handle, xp, yp))
     if world > 1:
         dist.barrier()
-    e2e_el = 0.0
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.add_(1)
-        stream.synchronize()
-        t0 = time.perf_counter()
         _capi.check(lib.cphifi_unaligned_matvec(p.handle, xp, yp))
-        e2e_el += time.perf_counter() - t0
-    te = torch.tensor([e2e_el], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = args.steps / float(te[0])
+    e2e_s = time.perf_counter() - t0
 
-    # secondary: one full device PCG solve of config 1 (tol 1e-8, max 500)
-    rep = cp.SolveReport()
-    cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
-    rep2 = cp.SolveReport()
-    cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep2)
+    t = torch.tensor([total_ms, ms6[1], ms6[5], e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, k1_ms, app_ms_phased, e2e_s = (float(v) for v in t)
+    value = args.steps / (total_ms / 1e3)
+
+    sec = {}
+    if rank == 0 and world == 1 and args.secondary:
+        import bench_secondary as bs
+        sec = bs.run_all(args, ctx, cp, p, mode, cfg)
+    del p
+    torch.cuda.empty_cache()
 
     if rank == 0:
-        hbm, src = measured_hbm()
-        k1_launch_s = (k1_ms / args.steps) / 1e3
-        fused_whole = world == 1 and n <= 512  # one cooperative kernel = the whole operator
-        k1_bytes = alg_bytes_matvec(d, q, n, r) if fused_whole else alg_bytes_k1(d, q // world, n, r)
-        achieved = k1_bytes / k1_launch_s / 1e9
-        traffic, traffic_src = ncu_traffic("fused_matvec_kernel")
-        mv_bytes = alg_bytes_matvec(d, q, n, r)
+        hbm, hbm_src = measured_hbm()
+        fp64 = sec.get("fp64_peak", {}).get("dmma_tflops") if isinstance(sec.get("fp64_peak"), dict) else None
+        k1_bytes = alg_bytes_k1(d, q // world, n, r)
+        k1_s = k1_ms / 1e3
+        achieved = k1_bytes / k1_s / 1e9
+        traffic, traffic_src = ncu_traffic("ncu_full_stream_config4.json", "stream_kernel")
+        t_app = total_ms / args.steps / 1e3
+        b_alg, f_alg = alg_bytes_matvec(d, q, n, r), alg_flops_matvec(d, q, n, r)
         out = {
-            "metric": "unaligned PCG matvecs/s (config 1, q=200k, r=10)",
-            "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "value_flush_per_step": args.steps / (flush_ms / 1e3),
-            "value_plain_launch": args.steps / (plain_ms / 1e3),
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1)",
-            "config": {"workload": "config1: unaligned 200x100x100, q=200000, r=10, lambda=1e-3, rho=1e-6",
-                       "l2": ("inputs larger than L2: 128 independent config-1 instances (plan, K, factors, x, y) "
-                              "cycled, every application L2-cold; value_flush_per_step = the per-step 256 MB "
-                              "flush method" if world == 1 else "flushed before every timed step (256 MB write)"),
-                       "timing": ("K applications back to back in one CUDA graph between one CUDA event pair"
-                                  if world == 1 else "plain launches, CUDA events around each application"),
-                       "parallelism": f"obs-sharded x{world}, n x r all-reduce per step"},
-            "roofline": {"bound": "hbm", "kernel": "fused_matvec_kernel (whole operator)" if fused_whole
-                         else "fused_matvec_kernel (scatter-gather + fix-up)", "achieved": achieved,
-                         "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": k1_bytes,
-                         "kernel_ms": k1_ms / args.steps},
-            "matvec_hbm_frac": mv_bytes / ((total_ms / args.steps) / 1e3) / 1e9 / hbm,
-            "phase_ms": {nm: v / args.steps for nm, v in
-                         zip(["K_X_gemm", "fused_kernel", "-", "allreduce", "y_gemm_or_C2", "total"], phases)},
-            "e2e": {"value": e2e_value, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * r,
-                    "d2h_bytes_per_step": 8 * n * r},
-            "gpu_launches": (1 if fused_whole else 3) * args.steps,
+            "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, BASELINE config 4; inputs/synth_math.h)",
+            "config": {"workload": WORKLOAD,
+                       "l2": "inputs larger than L2: every application streams the coalesced plan "
+                             f"({ql.value} entries on this rank, ~{12 * ql.value / 1e9:.1f} GB) >> 126 MB L2; no flush",
+                       "timing": "K applications back to back on the library stream between one CUDA event pair",
+                       "parallelism": (f"observations sharded x{world} (equal-count slices of the sorted plan), "
+                                       "n x r all-reduce per application") if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "kernel": "stream_kernel (k_stream.cu: the per-observation gather / scatter)",
+                         "achieved": achieved, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                         "alg_bytes_per_launch": k1_bytes,
+                         "alg_bytes_note": "SURVEY 8(d) as-given bytes of the q-pass: 4 d q (int32 index stream of "
+                                           "the q draws, read once) + 16 n r (Xhat rows read, Yhat written); the "
+                                           "coalesced plan moves fewer bytes (traffic)",
+                         "kernel_ms": k1_ms, "kernel_share_of_step": k1_ms / app_ms_phased},
+            "fp64": {"alg_flops_per_application": f_alg,
+                     "achieved_tflops": f_alg / t_app / 1e12, "peak_tflops_dmma_measured": fp64,
+                     "survey_roofline_frac": (max(b_alg / (hbm * 1e9), f_alg / (fp64 * 1e12)) / t_app) if fp64 else None,
+                     "note": "SURVEY 8(d): t_roof = max(B_alg/HBM, F_alg/P_FP64) on the as-given q draws; dedup of "
+                             "repeated draws and the hoisted first mode make the executed flops lower"},
+            "matvec_hbm_frac": b_alg / t_app / 1e9 / hbm,
+            "phase_ms": {nm: ms6[i] for i, nm in enumerate(["K_X_gemm", "stream_kernel", "-", "allreduce",
+                                                            "y_gemm", "whole_application"])},
+            "e2e": {"value": args.steps / e2e_s, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * r,
+                    "d2h_bytes_per_step": 8 * n * r,
+                    "call": "cphifi_unaligned_matvec (host x in, host y out, synchronous)"},
+            "gpu_launches": launches.value * args.steps,
+            "gpu_launches_per_step": launches.value,
             "clocks": clk.summary(),
-            "pcg_solve": {"iterations": rep2.iterations, "relative_residual": rep2.relative_residual,
-                          "wall_s": rep2.wall_time_s, "setup_s": rep2.setup_s, "matvecs": rep2.matvecs},
+            "setup": {"generate_s": gen_s, "plan_s": plan_s, "q_total": qt.value, "plan_entries_this_rank": ql.value},
         }
         if world == 1:
             from oracle import oracle as orc
             threads = orc.max_threads()
-            v_cpu, n_cpu = cpu_port_matvec(c, threads, args.cpu_seconds)
-            out["cpu_baseline"] = {"value": v_cpu, "unit": "matvecs/s", "cores": threads, "kind": "port",
-                                   "sample": f"config1 full operator application (q=200000) x {n_cpu}, "
-                                             f"fused streaming C restatement, {threads} threads"}
-        if world == 1 and args.secondary:
-            out["secondary"] = secondary(args, ctx, cp, p, c, lib, x, y, stream, flush)
+            t_cpu, det = cpu_config4_sample(threads, args.cpu_sample, args.cpu_seconds)
+            out["cpu_baseline"] = {
+                "value": 1.0 / t_cpu, "unit": "matvecs/s", "cores": threads, "kind": "port",
+                "sample": f"config 4: dense part timed whole + streaming pass over {args.cpu_sample} of the 1e9 draws "
+                          f"(x{det['reps']} for {args.cpu_seconds:.0f} s), extrapolated to q = 1e9; oracle/cphifi_"
+                          f"oracle.c fused streaming restatement, {threads} threads", "detail": det}
+        if sec:
+            out["secondary"] = sec
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

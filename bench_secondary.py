@@ -1,4 +1,6 @@
-"""Secondary measurements reported inside bench.py's JSON line (N = 1 only).
+"""Secondary measurements reported inside bench.py's JSON line (N = 1 only): the config-4 PCG solves
+(stream and row-Gram operators, the G build counted in the solve), configs 0-3 on device, the ALS
+updates, and CPU baselines for configs 0-3 (the oracle's ports, core counts stated).
 
 Everything is device-timed with CUDA events on the library stream unless stated; numbers that
 use the row-Gram operator are labelled as such (it reads G, not the observations, per
@@ -34,7 +36,8 @@ def fp64_peaks(ctx):
 def aligned(which, ctx, iters, fp64_tf):
     """Aligned solve (MTTKRP + Gram + decoupled rotate/divide/rotate; eig(V) reported as setup)."""
     import paper_2603_25691_b200 as cp
-    from paper_2603_25691_b200 import _capi, configs
+    from paper_2603_25691_b200 import _capi
+    from inputs import configs
     c = getattr(configs, which)()
     n, r = c.shape[0], c.r
     mode = cp.RkhsMode(c.points, c.ell, c.lam, ctx=ctx)
@@ -63,42 +66,6 @@ def aligned(which, ctx, iters, fp64_tf):
                                                      else "warm (16 MB tensor < L2)")}
 
 
-def config1_pcg(cp, p, c):
-    """Full device PCG solves of config 1 with both operator forms (wall clock, host loop)."""
-    out = {}
-    for op in ("stream", "gram"):
-        p.set_operator(op)
-        rep = cp.SolveReport()
-        t0 = time.perf_counter()
-        cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)  # first: includes G build for gram
-        first = time.perf_counter() - t0
-        rep = cp.SolveReport()
-        cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
-        out[op] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual, "wall_s": rep.wall_time_s,
-                   "first_call_s": first, "matvecs": rep.matvecs}
-    p.set_operator("stream")
-    return out
-
-
-def gram_matvec_ms(p, lib, x, y, stream, flush, steps=50):
-    import torch
-    from paper_2603_25691_b200 import _capi
-    p.set_operator("gram")
-    _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))  # builds G
-    ts = []
-    for _ in range(steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            flush.add_(1)
-            a.record(stream)
-            _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
-            b.record(stream)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    p.set_operator("stream")
-    return float(np.median(ts))
-
-
 def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     """Configs 3/4 at full size: per-observation operator, row-Gram operator, PCG (row-Gram).
     Config 4's plan coalesces repeated draws (cfg.coalesce): the streamed entries are the distinct
@@ -106,7 +73,8 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     import torch
 
     import paper_2603_25691_b200 as cp
-    from paper_2603_25691_b200 import _capi, configs
+    from paper_2603_25691_b200 import _capi
+    from inputs import configs
     cfg = getattr(configs, which)()
     n, r, d, q = cfg.shape[0], cfg.r, len(cfg.shape), cfg.q
     lib = _capi.load()
@@ -121,6 +89,7 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     t0 = time.perf_counter()
     p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho)
     plan_s = time.perf_counter() - t0
+    p.set_operator("stream")
     qt, ql = ctypes.c_int64(), ctypes.c_int64()
     _capi.check(lib.cphifi_obs_info(obs.plan(0, ctx).h, ctypes.byref(qt), ctypes.byref(ql), None))
     del idx, vals
@@ -184,55 +153,6 @@ def large(which, ctx, iters=3, solve=True, fp64_tf=None):
     return out
 
 
-def als_updates(ctx, p, c):
-    """ALS infinite-mode update on device: config 1 (unaligned, PCG warm-started
-    from the previous W as AlsState does) and config 2 (aligned decoupled), wall clock per update
-    plus the device-timed split (solve / factor update + error terms)."""
-    import paper_2603_25691_b200 as cp
-    from inputs import configs
-    out = {}
-    cfg = cp.PcgConfig(c.tol, c.max_iter)
-    u = cp.update_infinite_mode_unaligned(p, cfg)
-    t0 = time.perf_counter()
-    u2 = cp.update_infinite_mode_unaligned(p, cfg, warm_start=u.w)
-    out["config1_unaligned"] = {"wall_s_warm": time.perf_counter() - t0, "relative_error": u.relative_error,
-                                "iterations_cold": u.report.iterations, "iterations_warm": u2.report.iterations,
-                                "solve_s": u.solve_s, "update_and_error_s": u.update_s}
-    # a whole unaligned ALS sweep on device (mode 0 infinite, modes 1, 2 finite, then the error)
-    st = cp.UnalignedAlsState(cp.ObservationSet(c.shape, c.idx, c.vals), p.mode,
-                              cp.KruskalModel([np.zeros((c.shape[0], c.r))] + c.factors[1:]), rho=c.rho, inner=cfg)
-    its = [st.sweep() for _ in range(4)]  # the first sweep builds the per-mode plans
-    out["config1_unaligned_sweep"] = {"wall_s_per_sweep": float(np.median([it.wall_time_s for it in its[1:]])),
-                                      "first_sweep_s": its[0].wall_time_s,
-                                      "rel_errors": [it.rel_error for it in its],
-                                      "pcg_iterations": [it.pcg_iterations for it in its],
-                                      "note": "infinite mode: PCG warm-started + A_0 = K W; finite modes: row "
-                                              "least squares (row Grams + batched Jacobi pseudo-inverse); error pass"}
-    c2 = configs.config2()
-    n, r = c2.shape[0], c2.r
-    mode = cp.RkhsMode(c2.points, c2.ell, c2.lam, ctx=ctx)
-    t = cp.DenseTensor(c2.shape, c2.tensor)
-    model = cp.KruskalModel([np.zeros((n, r))] + c2.factors[1:])
-    cp.update_infinite_mode_aligned(t, model, 0, mode)  # eig(K), tensor upload, ||T||^2 once
-    t0 = time.perf_counter()
-    ua = cp.update_infinite_mode_aligned(t, model, 0, mode)
-    # whole aligned sweeps on device (mode 0 infinite; modes 1, 2 finite: A_k = B_k V_k^+)
-    g = np.random.default_rng(0)
-    init = [np.zeros((n, r))] + [g.normal(size=(s_, r)) for s_ in c2.shape[1:]]
-    st = cp.AlignedAlsState(t, mode, cp.KruskalModel(init))
-    its = [st.sweep() for _ in range(4)]
-    out["config2_aligned_sweep"] = {"wall_s_per_sweep": float(np.median([it.wall_time_s for it in its[1:]])),
-                                    "rel_errors": [it.rel_error for it in its],
-                                    "note": "MTTKRP for modes 0, 1, 2 on the TMA DMMA ring (k > 0: transposed "
-                                            "unfolding tiles), decoupled solve, B V^+ finite updates, Gram-identity "
-                                            "errors"}
-    out["config2_aligned"] = {"wall_s": time.perf_counter() - t0, "relative_error": ua.relative_error,
-                              "aligned_residual": ua.residual, "solve_s": ua.solve_s,
-                              "update_and_error_s": ua.update_s,
-                              "note": "relative error via ||T||^2 - 2<A,B> + 1'(A'A o V)1: no N-sized pass"}
-    return out
-
-
 def precond_ms(p, lib, n, r, iters=20):
     """Device time of one preconditioner application M^-1 x (unaligned.hpp:135-139), reported
     per PCG iteration next to the operator."""
@@ -255,3 +175,170 @@ def precond_ms(p, lib, n, r, iters=20):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return float(np.median(ts))
+
+
+def config4_solves(cp, p, obs, mode, cfg):
+    """Config 4 PCG solves on the headline plan: the stream operator (the reference's structure), the
+    row-Gram operator (drop-in default; G built inside the solve's setup), and a fresh-factor solve
+    (a new subproblem on the same observation plan: B, V, G, eig(V), PCG — one ALS infinite-mode
+    update's worth of work, unaligned.hpp:35-48 + 143-161)."""
+    import numpy as np
+    out = {}
+    pc = cp.PcgConfig(cfg.tol, cfg.max_iter)
+    for op in ("stream", "gram"):
+        p.set_operator(op)
+        rep = cp.SolveReport()
+        t0 = time.perf_counter()
+        cp.solve_unaligned_pcg(p, pc, rep)
+        first = time.perf_counter() - t0
+        rep2 = cp.SolveReport()
+        cp.solve_unaligned_pcg(p, pc, rep2)
+        out[op] = {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
+                   "first_wall_s": first, "first_setup_s": rep.setup_s, "repeat_wall_s": rep2.wall_time_s,
+                   "repeat_iterations": rep2.iterations}
+    n, r = cfg.shape[0], cfg.r
+    g = np.random.default_rng(5)
+    fac = [np.zeros((n, r))] + [f * (1.0 + 0.01 * g.normal(size=f.shape)) for f in cfg.factors[1:]]
+    t0 = time.perf_counter()
+    p2 = cp.make_unaligned_subproblem(obs, cp.KruskalModel(fac), 0, mode, cfg.rho)
+    t_sub = time.perf_counter() - t0
+    rep = cp.SolveReport()
+    cp.solve_unaligned_pcg(p2, pc, rep)
+    out["fresh_factors_gram"] = {"subproblem_s": t_sub, "pcg_wall_s": rep.wall_time_s, "pcg_setup_s": rep.setup_s,
+                                 "iterations": rep.iterations, "relative_residual": rep.relative_residual,
+                                 "total_s": t_sub + rep.wall_time_s, "operator": p2.operator(),
+                                 "note": "plan reused, fresh other-mode factors: B (one stream pass with the "
+                                         "values), V, G build, eig(V), preconditioner, PCG"}
+    p.set_operator("stream")
+    return out
+
+
+def config1_line(cp, ctx, steps):
+    """Config 1 operator (the previous round's headline) on 128 independent instances cycled in one
+    CUDA graph (>= 128 applications so every application starts L2-cold), and its PCG solve."""
+    import numpy as np
+    import torch
+    from inputs import configs
+    from paper_2603_25691_b200 import _capi
+    lib = _capi.load()
+    c = configs.config1()
+    n, r = c.shape[0], c.r
+    dev = torch.device("cuda", ctx.device)
+    model = cp.KruskalModel([np.zeros((n, r))] + c.factors[1:])
+    m = 128
+    insts = []
+    for _ in range(m):
+        mi = cp.RkhsMode(c.points, c.ell, c.lam, ctx=ctx)
+        oi = cp.ObservationSet(c.shape, c.idx, c.vals)
+        pi = cp.make_unaligned_subproblem(oi, model, 0, mi, c.rho)
+        xi = torch.randn(n * r, dtype=torch.float64, device=dev)
+        insts.append((mi, oi, pi, xi, torch.empty_like(xi)))
+    k = max(steps, 2 * m)
+    hp = (ctypes.c_void_p * m)(*[t[2].handle.value for t in insts])
+    hx = (ctypes.c_void_p * m)(*[t[3].data_ptr() for t in insts])
+    hy = (ctypes.c_void_p * m)(*[t[4].data_ptr() for t in insts])
+    tot = ctypes.c_float()
+    _capi.check(lib.cphifi_unaligned_matvec_cycle_timed(hp, hx, hy, m, k, ctypes.byref(tot)))
+    p = insts[0][2]
+    xh = np.random.default_rng(0).normal(size=n * r)
+    for _ in range(5):
+        cp.unaligned_matvec(p, xh)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        cp.unaligned_matvec(p, xh)
+    e2e = 200 / (time.perf_counter() - t0)
+    rep = cp.SolveReport()
+    cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
+    rep = cp.SolveReport()
+    cp.solve_unaligned_pcg(p, cp.PcgConfig(c.tol, c.max_iter), rep)
+    return {"matvecs_per_s": k / (tot.value / 1e3), "applications": k, "e2e_matvecs_per_s": e2e,
+            "pcg": {"iterations": rep.iterations, "relative_residual": rep.relative_residual,
+                    "wall_s": rep.wall_time_s},
+            "note": "128 independent config-1 instances cycled in one CUDA graph (>= 2 cycles: every application "
+                    "L2-cold); e2e = cphifi_unaligned_matvec with host buffers"}
+
+
+def cpu_baselines(threads):
+    """The oracle's CPU restatements: reference-faithful on 1 core (configs 0-2:
+    materialised Zhat / unfold + Khatri-Rao, two passes) and the fused streaming port on all host
+    cores (configs 1, 3; config 4 is the headline's cpu_baseline).  Same seeded inputs, same units."""
+    import numpy as np
+    from inputs import configs
+    from oracle import oracle as orc
+    out = {}
+
+    def timed(fn, min_s=2.0, max_reps=50):
+        fn()
+        reps, t0 = 0, time.perf_counter()
+        while reps < max_reps:
+            fn()
+            reps += 1
+            if time.perf_counter() - t0 >= min_s:
+                break
+        return (time.perf_counter() - t0) / reps
+
+    for which in ("config0", "config2"):
+        c = getattr(configs, which)()
+        n, r = c.shape[0], c.r
+        kern = orc.gaussian_kernel(c.points, c.ell)
+        ek = orc.sym_eig(kern)
+        fac = [np.zeros((n, r))] + c.factors[1:]
+        t3 = c.tensor.reshape(c.shape, order="F")
+
+        def solve():
+            b = orc.mttkrp(t3, fac, 0, threads=1)
+            v = orc.gram_khatri_rao(fac, 0)
+            return orc.solve_aligned_decoupled(b, ek, orc.sym_eig(v), c.lam, threads=1)
+        t = timed(solve, min_s=2.0, max_reps=5 if which == "config2" else 50)
+        out[which] = {"solves_per_s": 1.0 / t, "cores": 1, "kind": "port (reference-faithful: unfold copy, "
+                      "materialised Khatri-Rao, GEMM, decoupled solve; eig(K) setup excluded)"}
+    c = configs.config1()
+    n, r = c.shape[0], c.r
+    kern = orc.gaussian_kernel(c.points, c.ell)
+    fac = [np.zeros((n, r))] + c.factors[1:]
+    sub = orc.make_unaligned_subproblem(c.shape, c.idx, c.vals, fac, 0, kern, c.lam, c.rho)
+    x = np.random.default_rng(0).normal(size=n * r)
+    t_ref = timed(lambda: orc.unaligned_matvec(sub, x, 1))
+    t_str = timed(lambda: orc.unaligned_matvec_stream(c.shape, 0, c.idx, fac, kern, c.lam, c.rho, x, threads))
+    out["config1"] = {"ref_1core_matvecs_per_s": 1.0 / t_ref, "stream_matvecs_per_s": 1.0 / t_str,
+                      "stream_cores": threads}
+    c3 = configs.config3()
+    qs = 10_000_000
+    idx, _ = configs.generate_host(c3, 0, qs, values=False, threads=threads)
+    kern3 = orc.matern32_kernel(c3.points, c3.ell)
+    fac3 = [None] + c3.factors[1:]
+    x3 = np.random.default_rng(0).normal(size=c3.shape[0] * c3.r)
+    empty = np.zeros((4, 0), dtype=np.int32)
+    t_dense = timed(lambda: orc.unaligned_matvec_stream(c3.shape, 0, empty, fac3, kern3, c3.lam, c3.rho, x3, threads),
+                    min_s=0.5, max_reps=3)
+    xh = np.asfortranarray(np.random.default_rng(1).normal(size=(c3.shape[0], c3.r)))
+    t_s = timed(lambda: orc.scatter_gather_stream(c3.shape, 0, idx, fac3, xh, threads), min_s=3.0, max_reps=10)
+    out["config3"] = {"stream_matvecs_per_s": 1.0 / (t_dense + t_s * c3.q / qs), "stream_cores": threads,
+                      "sample": f"dense part timed whole + streaming pass over {qs} of the 2e8 draws, extrapolated"}
+    return out
+
+
+def run_all(args, ctx, cp, p, mode, cfg):
+    """Everything above, each failure reported in its key (never hidden)."""
+    import torch
+    from oracle import oracle as orc
+    sec = {}
+
+    def attempt(key, fn):
+        try:
+            sec[key] = fn()
+        except Exception as e:  # report, never hide: the key carries the failure
+            sec[key] = {"error": f"{type(e).__name__}: {e}"}
+
+    attempt("fp64_peak", lambda: fp64_peaks(ctx))
+    fp64 = sec["fp64_peak"].get("dmma_tflops", 40.0) if isinstance(sec["fp64_peak"], dict) else 40.0
+    obs = p.obs
+    attempt("config4_pcg", lambda: config4_solves(cp, p, obs, mode, cfg))
+    torch.cuda.empty_cache()
+    attempt("config3", lambda: large("config3", ctx, fp64_tf=fp64))
+    torch.cuda.empty_cache()
+    attempt("config1", lambda: config1_line(cp, ctx, args.steps))
+    attempt("config0_aligned", lambda: aligned("config0", ctx, 20, fp64))
+    attempt("config2_aligned", lambda: aligned("config2", ctx, 10, fp64))
+    attempt("cpu_baselines", lambda: cpu_baselines(orc.max_threads()))
+    return sec

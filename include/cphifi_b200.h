@@ -92,6 +92,16 @@ int cphifi_fp64_peak(cphifi_ctx ctx, double* dfma_tflops, double* dmma_tflops);
 int cphifi_comm_unique_id(uint8_t id_out[128]);
 int cphifi_ctx_init_comm(cphifi_ctx ctx, int nranks, int rank, const uint8_t id[128]);
 int cphifi_ctx_world(cphifi_ctx ctx, int* nranks, int* rank);
+/* Test hook: a VIRTUAL communicator of `nranks` (<= 8) contexts on ONE GPU, each driven by its own
+ * host thread, that stands in for NCCL so every multi-rank code path (sharded observations with the
+ * n x r all-reduce per application, the host-loop PCG, the sharded aligned MTTKRP) runs without a
+ * second GPU.  Collectives sum the ranks' buffers in rank order; like NCCL, every rank must issue
+ * the same collectives in the same order.  Attach with cphifi_ctx_init_vcomm before creating
+ * plans; destroy the communicator after its contexts. */
+typedef struct cphifi_vcomm_s* cphifi_vcomm;
+int cphifi_vcomm_create(int nranks, cphifi_vcomm* out);
+int cphifi_vcomm_destroy(cphifi_vcomm vc);
+int cphifi_ctx_init_vcomm(cphifi_ctx ctx, cphifi_vcomm vc, int rank);
 
 /* ---- mode (RkhsMode, kernel.hpp:53-101) ------------------------------------------- */
 /* RkhsMode(points, sigma, lambda): Gaussian kernel K(i,j)=exp(-(x_i-x_j)^2/(2 sigma^2))
@@ -146,11 +156,12 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r,
 int cphifi_unaligned_destroy(cphifi_unaligned p);
 int cphifi_unaligned_get_b(cphifi_unaligned p, double* b_out);  /* n x r */
 int cphifi_unaligned_get_v(cphifi_unaligned p, double* v_out);  /* r x r */
-/* Operator form used by matvec / PCG.  STREAM (default) is the reference's structure: every
- * application gathers and scatters over all q observations (observations.hpp:174-198).  GRAM
- * uses the exact identity Yhat(i,:) = G_i Xhat(i,:), G_i = sum_{l in row i} z_l z_l', with G
- * built once on first use (O(q rp^2)); each application is then O(n rp^2).  AUTO picks GRAM
- * when rp <= 64 and the rows carry on average >= 2 rp observations. */
+/* Operator form used by matvec / PCG.  STREAM is the reference's structure: every application
+ * gathers and scatters over all q observations (observations.hpp:174-198).  GRAM uses the exact
+ * identity Yhat(i,:) = G_i Xhat(i,:), G_i = sum_{l in row i} z_l z_l', with G built once per plan
+ * (O(q rp^2), counted in the solve's setup_s / wall_time_s); each application is then O(n rp^2).
+ * AUTO picks GRAM when n is not small, rp <= 64 and the rows carry on average >= 2 rp
+ * observations.  A new plan starts with AUTO's choice. */
 #define CPHIFI_OP_STREAM 0
 #define CPHIFI_OP_GRAM 1
 #define CPHIFI_OP_AUTO 2
@@ -189,6 +200,10 @@ int cphifi_unaligned_matvec_cycle_timed(const cphifi_unaligned* ps, const double
  * not in them: the way the operator runs inside the device-resident PCG loop). */
 int cphifi_unaligned_matvec_graph_timed(cphifi_unaligned p, const double* x, double* y, void* flush,
                                         size_t flush_bytes, int steps, float* ms_out);
+/* Benchmark hook: *kernels = how many kernels of this library one operator application launches
+ * (one application captured into a CUDA graph and its kernel nodes counted; the all-reduce of a
+ * multi-rank plan is not a kernel of this library and is left out of the capture). */
+int cphifi_unaligned_matvec_launches(cphifi_unaligned p, const double* x, double* y, int* kernels);
 /* Tracing hook: one operator application on DEVICE buffers with per-CTA %globaltimer stamps
  * (8 per CTA: entry, phase A done, barrier 1, phase B done, barrier 2, fix-up done,
  * barrier 3, exit; 0 = phase not run).  *ctas receives the CTA count. */

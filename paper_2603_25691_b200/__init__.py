@@ -29,7 +29,7 @@ from ._capi import (CphifiDeviceError, CphifiInvalidArgument, CphifiRuntimeError
                     call)
 
 __all__ = [
-    "Context", "default_context", "RkhsMode", "SymEig", "ObservationSet", "DenseTensor", "KruskalModel",
+    "Context", "VirtualComm", "default_context", "RkhsMode", "SymEig", "ObservationSet", "DenseTensor", "KruskalModel",
     "sample_uniform", "full_observations", "make_unaligned_subproblem", "UnalignedSubproblem",
     "unaligned_matvec", "build_preconditioner", "LinearOperator", "solve_unaligned_pcg", "PcgConfig",
     "AlsUpdate", "update_infinite_mode_unaligned", "update_infinite_mode_aligned",
@@ -70,6 +70,11 @@ class Context:
     def init_comm(self, nranks: int, rank: int, uid: bytes) -> None:
         call("cphifi_ctx_init_comm", self.handle, nranks, rank, uid)
 
+    def init_vcomm(self, vc: "VirtualComm", rank: int) -> None:
+        """Join a one-GPU virtual communicator as `rank` (test hook for the multi-rank paths)."""
+        call("cphifi_ctx_init_vcomm", self.handle, vc.handle, rank)
+        self._vc = vc  # the communicator outlives its contexts
+
     def world(self):
         n, r = ctypes.c_int(), ctypes.c_int()
         call("cphifi_ctx_world", self.handle, ctypes.byref(n), ctypes.byref(r))
@@ -86,6 +91,23 @@ class Context:
     def close(self) -> None:
         if getattr(self, "handle", None):
             _capi.load().cphifi_ctx_destroy(self.handle)
+            self.handle = None
+
+
+class VirtualComm:
+    """cphifi_vcomm: `nranks` contexts on ONE GPU, each driven by its own host thread, standing in
+    for NCCL ranks (collectives = rank-order sums); every multi-rank code path runs without a
+    second GPU.  Test hook, see include/cphifi_b200.h."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        call("cphifi_vcomm_create", nranks, ctypes.byref(h))
+        self.handle = h
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _capi.load().cphifi_vcomm_destroy(self.handle)
             self.handle = None
 
 
@@ -440,7 +462,7 @@ class UnalignedSubproblem:
     """unaligned.hpp:18-33 — a device plan: sorted observations, packed factors, B, V."""
 
     def __init__(self, obs: ObservationSet, model: KruskalModel, k: int, mode: RkhsMode, rho: float,
-                 shard: int = 0, shards: int = 1):
+                 shard: int = 0, shards: int = 1, ctx: Context | None = None):
         self.obs = obs
         self.mode = mode
         self.mode_index = k
@@ -451,7 +473,7 @@ class UnalignedSubproblem:
         self._r = model.rank()
         # mode None: a finite-mode subproblem (B, V, row Grams; no operator) for the row updates
         self._n = mode.size() if mode is not None else obs.shape()[k]
-        ctx = mode.ctx if mode is not None else default_context()
+        ctx = mode.ctx if mode is not None else (ctx or default_context())
         arrs, ptrs = _factor_array(model.factors, k)
         plan = obs.plan(k, ctx, shard, shards)
         h = ctypes.c_void_p()
@@ -593,16 +615,18 @@ def _device_tensor(t: DenseTensor, ctx: Context, shard=0, shards=1):
     return cache[key]
 
 
-def mttkrp(t: DenseTensor, model: KruskalModel, k: int, ctx: Context | None = None) -> np.ndarray:
+def mttkrp(t: DenseTensor, model: KruskalModel, k: int, ctx: Context | None = None, shard: int = 0,
+           shards: int = 1) -> np.ndarray:
     """tensor.hpp:174-182 on device: k = 0 (the infinite mode) for any order; k = 1, 2 for 3-way
-    tensors with even n0 (the finite-mode updates)."""
+    tensors with even n0 (the finite-mode updates).  shards > 1: this rank holds mode-1 slab
+    `shard` and B is all-reduced over the communicator."""
     ctx = ctx or default_context()
     if t.order() != model.order():
         raise CphifiInvalidArgument("mttkrp: order mismatch")
     for i in range(t.order()):
         if i != k and t.shape()[i] != model.factors[i].shape[0]:
             raise CphifiInvalidArgument("mttkrp: shape mismatch")
-    dt = _device_tensor(t, ctx)
+    dt = _device_tensor(t, ctx, shard, shards)
     arrs, ptrs = _factor_array(model.factors, k)
     b = np.zeros((t.shape()[k], model.rank()), order="F")
     call("cphifi_mttkrp", dt.handle, k, model.rank(), ptrs, _dp(b))
@@ -774,10 +798,12 @@ def update_infinite_mode_unaligned(p: UnalignedSubproblem, cfg: PcgConfig | None
     return _als_from(c, w, a, sr)
 
 
-def update_finite_mode_unaligned(obs: ObservationSet, model: KruskalModel, k: int) -> np.ndarray:
+def update_finite_mode_unaligned(obs: ObservationSet, model: KruskalModel, k: int, ctx: Context | None = None,
+                                 shard: int = 0, shards: int = 1) -> np.ndarray:
     """update_finite_mode, unaligned branch (als.hpp:144-162) on device: the minimum-norm least-
-    squares row fits of mode k (rows without observations stay zero).  Returns A_k (n_k x r)."""
-    p = UnalignedSubproblem(obs, model, k, None, 1e-6)
+    squares row fits of mode k (rows without observations stay zero).  Returns A_k (n_k x r).
+    shards > 1: this rank's observation shard; the row Grams and B are summed over the ranks."""
+    p = UnalignedSubproblem(obs, model, k, None, 1e-6, shard, shards, ctx=ctx)
     a = np.zeros((p.n(), p.r()), order="F")
     call("cphifi_als_update_finite_unaligned", p.handle, _dp(a))
     return a

@@ -80,6 +80,9 @@ _SIGS = [
     ("cphifi_fp64_peak", ctypes.c_int, [_H, c_double_p, c_double_p]),
     ("cphifi_comm_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("cphifi_ctx_init_comm", ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
+    ("cphifi_vcomm_create", ctypes.c_int, [ctypes.c_int, c_void_pp]),
+    ("cphifi_vcomm_destroy", ctypes.c_int, [_H]),
+    ("cphifi_ctx_init_vcomm", ctypes.c_int, [_H, _H, ctypes.c_int]),
     ("cphifi_ctx_world", ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_mode_create_gaussian", ctypes.c_int,
      [_H, ctypes.c_int64, c_double_p, ctypes.c_double, ctypes.c_double, c_void_pp]),
@@ -114,6 +117,7 @@ _SIGS = [
     ("cphifi_unaligned_precond_apply_device", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p]),
     ("cphifi_solve_unaligned_pcg", ctypes.c_int,
      [_H, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC), c_double_p, c_double_p]),
+    ("cphifi_unaligned_matvec_launches", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_unaligned_matvec_timed", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c_double_p]),
     ("cphifi_unaligned_matvec_cycle_timed", ctypes.c_int,
      [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,

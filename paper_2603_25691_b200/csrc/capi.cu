@@ -14,9 +14,24 @@
 
 using namespace cphifi;
 
+#include <set>
+#include <tuple>
+
 namespace cphifi {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
+
+void func_attr_once(const void* f, cudaFuncAttribute attr, int value) {
+    static std::mutex m;
+    static std::set<std::tuple<const void*, int, int, int>> done;
+    int dev = 0;
+    CPHIFI_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(f, (int)attr, value, dev);
+    std::lock_guard<std::mutex> lk(m);
+    if (done.count(key)) return;
+    CPHIFI_CUDA(cudaFuncSetAttribute(f, attr, value));
+    done.insert(key);
+}
 }  // namespace cphifi
 
 namespace {
@@ -66,10 +81,39 @@ void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     CPHIFI_CUDA(cudaStreamSynchronize(s));
 }
 
-void allreduce(cphifi_ctx ctx, double* buf, size_t count) {
-    if (ctx->comm && ctx->nranks > 1 && count)
-        CPHIFI_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+// More than one rank: NCCL over NVLink, or the one-GPU virtual communicator (test hook).
+bool ctx_multi(cphifi_ctx ctx) { return ctx->nranks > 1 && (ctx->comm || ctx->vcomm); }
+
+// Sum of every rank's `send` into `recv` on every rank (in place allowed), ordered on the context
+// stream.  NCCL: ncclAllReduce.  Virtual communicator: see cphifi_vcomm_s (common.cuh).
+thread_local bool g_count_only = false;  // cphifi_unaligned_matvec_launches: capture this library's kernels only
+
+void allreduce_sum(cphifi_ctx ctx, const double* send, double* recv, size_t count) {
+    if (!ctx_multi(ctx) || !count || g_count_only) {
+        if (send != recv && count)
+            CPHIFI_CUDA(cudaMemcpyAsync(recv, send, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+        return;
+    }
+    if (ctx->comm) {
+        CPHIFI_NCCL(ncclAllReduce(send, recv, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+        return;
+    }
+    cphifi_vcomm_s* vc = ctx->vcomm;
+    const int me = ctx->rank, nr = vc->nranks;
+    if (ctx->vc_scratch.n < count) ctx->vc_scratch.alloc(count);
+    vc->send[me] = send;
+    CPHIFI_CUDA(cudaEventRecord(vc->ready[me], ctx->stream));
+    vc->barrier();  // every rank's send buffer and ready event are published
+    for (int k = 0; k < nr; ++k) CPHIFI_CUDA(cudaStreamWaitEvent(ctx->stream, vc->ready[k], 0));
+    rank_order_sum(vc->send.data(), nr, ctx->vc_scratch.get(), count, ctx->num_sms, ctx->stream);
+    CPHIFI_CUDA(cudaEventRecord(vc->done[me], ctx->stream));
+    vc->barrier();  // every rank has enqueued its reads of the send buffers
+    for (int k = 0; k < nr; ++k) CPHIFI_CUDA(cudaStreamWaitEvent(ctx->stream, vc->done[k], 0));
+    CPHIFI_CUDA(cudaMemcpyAsync(recv, ctx->vc_scratch.get(), sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
 }
+
+void allreduce(cphifi_ctx ctx, double* buf, size_t count) { allreduce_sum(ctx, buf, buf, count); }
 
 int read_flag(cphifi_ctx ctx, int* dflag) {
     int h = 0;
@@ -271,7 +315,7 @@ void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, Partitio
 }
 
 // ---- unaligned pieces ------------------------------------------------------------------
-bool is_multi(cphifi_unaligned p) { return p->obs->ctx->comm && p->obs->ctx->nranks > 1; }
+bool is_multi(cphifi_unaligned p) { return ctx_multi(p->obs->ctx); }
 
 // The complete (all-rank) Yhat: the local one on one GPU, the NCCL sum otherwise.
 double* yhat_result(cphifi_unaligned p) { return is_multi(p) ? p->yhat_sum.get() : p->yhat_rm.get(); }
@@ -279,9 +323,7 @@ double* yhat_result(cphifi_unaligned p) { return is_multi(p) ? p->yhat_sum.get()
 // Out-of-place sum of the ranks' partial Yhat (the local buffer keeps its zero rows).
 void allreduce_yhat(cphifi_unaligned p) {
     cphifi_ctx ctx = p->obs->ctx;
-    if (is_multi(p))
-        CPHIFI_NCCL(ncclAllReduce(p->yhat_rm.get(), p->yhat_sum.get(), (size_t)p->n * p->rp, ncclDouble, ncclSum,
-                                  ctx->comm, ctx->stream));
+    if (is_multi(p)) allreduce_sum(ctx, p->yhat_rm.get(), p->yhat_sum.get(), (size_t)p->n * p->rp);
 }
 
 FusedArgs fused_args(cphifi_unaligned p, unsigned phases) {
@@ -405,6 +447,15 @@ void ensure_gram(cphifi_unaligned p) {
     }
 }
 
+// CPHIFI_OP_AUTO: the row-Gram form pays off when the rows carry on average >= 2 rp observations
+// (each application then costs O(n rp^2) instead of O(q d rp)) and G fits comfortably; small n
+// keeps the single fused launch.  Plans start with this choice (cphifi_unaligned_create).
+int auto_operator(cphifi_unaligned p) {
+    if (!p->mode || p->small_n) return CPHIFI_OP_STREAM;
+    const double g_bytes = 8.0 * (double)p->n * (double)p->rp * (double)p->rp;
+    return (p->rp <= 64 && p->obs->q_local >= 2 * p->rp * p->n && g_bytes <= 8e9) ? CPHIFI_OP_GRAM : CPHIFI_OP_STREAM;
+}
+
 // Phase sets of the operator launches (see kernels.cuh).  part 0 = the (first) launch,
 // part 1 = the launch after the NCCL all-reduce (multi-GPU, small n).
 unsigned matvec_phases(cphifi_unaligned p, bool multi, int part) {
@@ -450,7 +501,7 @@ void need_mode(cphifi_unaligned p) {
 void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     need_mode(p);
     cphifi_ctx ctx = p->obs->ctx;
-    const bool multi = ctx->comm && ctx->nranks > 1;
+    const bool multi = ctx_multi(ctx);
     if (p->op == 1) ensure_gram(p);
     const double* gr = p->op == 1 ? p->gram.get() : nullptr;
     if (p->small_n) {
@@ -487,6 +538,7 @@ void ensure_precond(cphifi_unaligned p) {
     }
     if (!p->dmat.n) {
         p->dmat.alloc(n * r);
+        ++p->veig_gen;  // a new D buffer: graphs captured with the old one are stale
         DevBuf<int> flag(1);
         CPHIFI_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
         precond_diag(p->mode->mu.get(), p->sv.get(), n, r, p->obs->density, p->mode->lambda, p->rho,
@@ -755,10 +807,17 @@ bool pcg_graph_ok(cphifi_unaligned p) {
 // Capture `body` (one PCG iteration) into the body graph of a WHILE conditional node and
 // instantiate it, once per plan and operator form.  The captured pointers are the plan's
 // persistent PCG vectors, so later solves reuse the executable graph.
+// The captured graphs hold device pointers of the mode's eigendecomposition (U, U', U diag(mu), mu)
+// and of the plan's preconditioner (U_V, D): installing new ones must force a recapture.
+uint64_t eig_generation(cphifi_unaligned p) { return ((p->mode ? p->mode->eig_gen : 0) << 32) ^ p->veig_gen; }
+
 template <class F>
 bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
     const int64_t zkey = rot && p->mode ? p->mode->nzero : -1;
-    if (p->pcg_exec && p->pcg_graph_op == p->op && p->pcg_graph_rot == (int)rot && p->pcg_graph_z == zkey) return true;
+    const uint64_t gen = eig_generation(p);
+    if (p->pcg_exec && p->pcg_graph_op == p->op && p->pcg_graph_rot == (int)rot && p->pcg_graph_z == zkey &&
+        p->pcg_graph_gen == gen)
+        return true;
     if (p->pcg_exec) cudaGraphExecDestroy(p->pcg_exec);
     if (p->pcg_graph) cudaGraphDestroy(p->pcg_graph);
     p->pcg_exec = nullptr;
@@ -791,6 +850,7 @@ bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
         p->pcg_graph_op = p->op;
         p->pcg_graph_rot = (int)rot;
         p->pcg_graph_z = zkey;
+        p->pcg_graph_gen = gen;
         return true;
     } catch (const Error& e) {
         if (capturing) {
@@ -811,7 +871,9 @@ bool ensure_pcg_graph(cphifi_unaligned p, bool rot, F&& body) {
 template <class FA, class FW, class FB>
 bool ensure_pcg_full_graph(cphifi_unaligned p, bool rot, FA&& seg_a, FW&& body, FB&& seg_b) {
     const int64_t zkey = rot && p->mode ? p->mode->nzero : -1;
-    if (p->pcgf_exec && p->pcgf_op == p->op && p->pcgf_rot == (int)rot && p->pcgf_z == zkey) return true;
+    const uint64_t gen = eig_generation(p);
+    if (p->pcgf_exec && p->pcgf_op == p->op && p->pcgf_rot == (int)rot && p->pcgf_z == zkey && p->pcgf_gen == gen)
+        return true;
     if (p->pcgf_exec) cudaGraphExecDestroy(p->pcgf_exec);
     if (p->pcgf_graph) cudaGraphDestroy(p->pcgf_graph);
     p->pcgf_exec = nullptr;
@@ -864,6 +926,7 @@ bool ensure_pcg_full_graph(cphifi_unaligned p, bool rot, FA&& seg_a, FW&& body, 
         p->pcgf_op = p->op;
         p->pcgf_rot = (int)rot;
         p->pcgf_z = zkey;
+        p->pcgf_gen = gen;
         return true;
     } catch (const Error& e) {
         if (capturing) {
@@ -964,10 +1027,52 @@ int cphifi_ctx_init_comm(cphifi_ctx ctx, int nranks, int rank, const uint8_t id[
         DeviceGuard dg(ctx->device);
         ncclUniqueId uid;
         std::memcpy(&uid, id, 128);
+        if (ctx->vcomm) throw_invalid("cphifi_ctx_init_comm: the context uses a virtual communicator");
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         ctx->comm = nullptr;
         CPHIFI_NCCL(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
         ctx->nranks = nranks;
+        ctx->rank = rank;
+    });
+}
+
+int cphifi_vcomm_create(int nranks, cphifi_vcomm* out) {
+    return guard([&] {
+        need(out, "out");
+        if (nranks < 1 || nranks > 8) throw_invalid("cphifi_vcomm_create: 1..8 ranks");
+        auto* v = new cphifi_vcomm_s;
+        v->nranks = nranks;
+        v->send.assign(nranks, nullptr);
+        v->ready.assign(nranks, nullptr);
+        v->done.assign(nranks, nullptr);
+        *out = v;
+    });
+}
+
+int cphifi_vcomm_destroy(cphifi_vcomm vc) {
+    return guard([&] {
+        if (!vc) return;
+        for (auto e : vc->ready)
+            if (e) cudaEventDestroy(e);
+        for (auto e : vc->done)
+            if (e) cudaEventDestroy(e);
+        delete vc;
+    });
+}
+
+int cphifi_ctx_init_vcomm(cphifi_ctx ctx, cphifi_vcomm vc, int rank) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(vc, "vc");
+        if (rank < 0 || rank >= vc->nranks) throw_invalid("cphifi_ctx_init_vcomm: bad rank");
+        if (ctx->comm) throw_invalid("cphifi_ctx_init_vcomm: the context already has an NCCL communicator");
+        DeviceGuard dg(ctx->device);
+        std::lock_guard<std::mutex> lk(vc->m);
+        if (vc->ready[rank]) throw_invalid("cphifi_ctx_init_vcomm: rank already taken");
+        CPHIFI_CUDA(cudaEventCreateWithFlags(&vc->ready[rank], cudaEventDisableTiming));
+        CPHIFI_CUDA(cudaEventCreateWithFlags(&vc->done[rank], cudaEventDisableTiming));
+        ctx->vcomm = vc;
+        ctx->nranks = vc->nranks;
         ctx->rank = rank;
     });
 }
@@ -1083,6 +1188,7 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         CPHIFI_CUDA(cudaStreamSynchronize(mode->ctx->stream));
         mode->have_eig = true;
         mode->eig_count = 1;
+        ++mode->eig_gen;  // plans recapture their PCG graphs (eig_generation)
     });
 }
 int cphifi_mode_get_eig(cphifi_mode mode, double* u_out, double* mu_out) {
@@ -1393,7 +1499,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // rows without observations in this shard are never written: keep them zero
         CPHIFI_CUDA(cudaMemsetAsync(p->yhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
         CPHIFI_CUDA(cudaMemsetAsync(p->xhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
-        if (ctx->comm && ctx->nranks > 1) p->yhat_sum.alloc(n * p->rp);
+        if (ctx_multi(ctx)) p->yhat_sum.alloc(n * p->rp);
         p->xhat_cm.alloc(n * r);
         p->t1.alloc(n * r);
         p->t2.alloc(n * r);
@@ -1407,6 +1513,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         p->b.alloc(n * r);
         rm_to_cm(yhat_result(p), n, p->rp, r, p->b.get(), s);
         CPHIFI_CUDA(cudaStreamSynchronize(s));
+        p->op = auto_operator(p);  // the drop-in default (cphifi_unaligned_set_operator overrides)
         *out = hold.release();
     });
 }
@@ -1441,13 +1548,7 @@ int cphifi_unaligned_set_operator(cphifi_unaligned p, int op) {
     return guard([&] {
         need(p, "p");
         if (op < CPHIFI_OP_STREAM || op > CPHIFI_OP_AUTO) throw_invalid("cphifi_unaligned_set_operator: unknown operator");
-        if (op == CPHIFI_OP_AUTO) {
-            // row-Gram pays off when the rows carry on average >= 2 rp observations (each
-            // application then costs O(n rp^2) instead of O(q d rp)) and G fits comfortably
-            const double g_bytes = 8.0 * (double)p->n * (double)p->rp * (double)p->rp;
-            op = (p->rp <= 64 && p->obs->q_local >= 2 * p->rp * p->n && g_bytes <= 8e9) ? CPHIFI_OP_GRAM
-                                                                                         : CPHIFI_OP_STREAM;
-        }
+        if (op == CPHIFI_OP_AUTO) op = auto_operator(p);
         if (op == CPHIFI_OP_GRAM && p->rp > 64) throw_invalid("gram operator: padded rank above 64 is not supported");
         p->op = op;
     });
@@ -1664,7 +1765,7 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
         cphifi_ctx ctx = p->obs->ctx;
         DeviceGuard dg(ctx->device);
         cudaStream_t s = ctx->stream;
-        const bool multi = ctx->comm && ctx->nranks > 1;
+        const bool multi = ctx_multi(ctx);
         cudaEvent_t ev[6];
         for (auto& e : ev) CPHIFI_CUDA(cudaEventCreate(&e));
         double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -1706,6 +1807,51 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
     });
 }
 
+int cphifi_unaligned_matvec_launches(cphifi_unaligned p, const double* x, double* y, int* kernels) {
+    return guard([&] {
+        need(p, "p");
+        need(x, "x");
+        need(y, "y");
+        need(kernels, "kernels");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        if (p->op == 1) ensure_gram(p);
+        matvec_dev(p, x, y);  // lazily built state and launch attributes before the capture
+        CPHIFI_CUDA(cudaStreamSynchronize(s));
+        cudaGraph_t g = nullptr;
+        g_count_only = true;
+        try {
+            CPHIFI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+            try {
+                matvec_dev(p, x, y);
+            } catch (...) {
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(s, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                throw;
+            }
+            CPHIFI_CUDA(cudaStreamEndCapture(s, &g));
+        } catch (...) {
+            g_count_only = false;
+            throw;
+        }
+        g_count_only = false;
+        size_t nn = 0;
+        CPHIFI_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CPHIFI_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        int cnt = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            CPHIFI_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t == cudaGraphNodeTypeKernel) ++cnt;
+        }
+        cudaGraphDestroy(g);
+        *kernels = cnt;
+    });
+}
+
 int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y, uint64_t* stamps, int capacity,
                                   int* ctas) {
     return guard([&] {
@@ -1719,7 +1865,7 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
         const size_t cnt = (size_t)p->grid * TRACE_SLOTS;
         DevBuf<unsigned long long> tr(cnt);
         CPHIFI_CUDA(cudaMemsetAsync(tr.get(), 0, cnt * sizeof(unsigned long long), ctx->stream));
-        const bool multi = ctx->comm && ctx->nranks > 1;
+        const bool multi = ctx_multi(ctx);
         if (p->op == 1) ensure_gram(p);
         if (!p->small_n) xhat_gemm(p, x);
         FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
@@ -1800,6 +1946,7 @@ int cphifi_unaligned_set_v_eig(cphifi_unaligned p, const double* u_v, const doub
         clamp_nonneg(p->sv.get(), r, ctx->stream);
         p->have_veig = true;
         p->dmat.release();
+        ++p->veig_gen;  // the PCG graphs captured U_V / D: recapture (eig_generation)
         CPHIFI_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1871,6 +2018,8 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         if (rot) rotate(p, true, true, p->b.get(), bvec);  // rhs~ = (I x U') vec(K B) = mu o (U' B)
         else gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
+        if (p->op == 1) ensure_gram(p);  // the row-Gram operator's G: per-solve setup, timed as such
+        CPHIFI_CUDA(cudaStreamSynchronize(s));
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;
         auto apply_a = [&](const double* xin, double* yout) {
@@ -2542,7 +2691,7 @@ int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t
         // host launch latency of its kernels (~4 us per plain launch here).  The timed solve is
         // the same MTTKRP -> Gram -> decoupled sequence captured once as a CUDA graph and
         // replayed `iters` times back to back (single GPU; no NCCL inside the capture).
-        if (!(ctx->comm && ctx->nranks > 1)) {
+        if (!(ctx_multi(ctx))) {
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ex = nullptr;
             const int* flag = nullptr;
@@ -2723,12 +2872,18 @@ int cphifi_als_update_finite_unaligned(cphifi_unaligned p, double* a_out) {
         const int64_t n = p->n, r = p->r;
         if (p->rp > 64) throw_invalid("finite-mode update: padded rank above 64 is not supported");
         ensure_gram(p);  // G_i = Z_i' Z_i (this shard's observations)
-        if (is_multi(p) && !p->gram_reduced) {
-            allreduce(ctx, p->gram.get(), (size_t)n * p->rp * p->rp);
-            p->gram_reduced = true;
+        // multi-rank: the row solves need the all-shard Grams; they are summed into a separate
+        // buffer so p->gram keeps this shard's G_i (the GRAM operator applies it per rank and then
+        // sums Yhat over ranks)
+        const double* g_all = p->gram.get();
+        if (is_multi(p)) {
+            const size_t cnt = (size_t)n * p->rp * p->rp;
+            if (p->gram_sum.n < cnt) p->gram_sum.alloc(cnt);
+            allreduce_sum(ctx, p->gram.get(), p->gram_sum.get(), cnt);
+            g_all = p->gram_sum.get();
         }
         DevBuf<double> a(n * r);
-        rowls_solve(p->gram.get(), p->b.get(), n, r, p->rp, a.get(), s);  // b = Z_i' t_i (all shards)
+        rowls_solve(g_all, p->b.get(), n, r, p->rp, a.get(), s);  // b = Z_i' t_i (all shards)
         d2h_sync(a_out, a.get(), sizeof(double) * n * r, s);
     });
 }

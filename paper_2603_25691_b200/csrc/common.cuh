@@ -6,6 +6,7 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <condition_variable>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -76,6 +77,10 @@ struct DevBuf {
     T* get() const { return p; }
 };
 
+// cudaFuncSetAttribute once per (kernel, attribute, device): attributes are per device, so a
+// process-wide "done" flag would leave a second GPU without them.  Thread-safe.
+void func_attr_once(const void* f, cudaFuncAttribute attr, int value);
+
 inline int64_t pow2_at_least(int64_t v, int64_t lo) {
     int64_t p = lo;
     while (p < v) p <<= 1;
@@ -85,12 +90,40 @@ inline int64_t pow2_at_least(int64_t v, int64_t lo) {
 }  // namespace cphifi
 
 // ---- opaque handle definitions -------------------------------------------------------
+// Virtual communicator (test hook, include/cphifi_b200.h): `nranks` contexts on ONE GPU, each
+// driven by its own host thread, exchange partial sums the way NCCL ranks do.  A collective is a
+// host barrier (every rank has published its send buffer and a "ready" event), a rank-order sum
+// on each rank's own stream after waiting on every ready event, and a "done" event every rank
+// waits on before touching its buffers again.  No kernel ever waits on another kernel.
+struct cphifi_vcomm_s {
+    int nranks = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    std::vector<const double*> send;
+    std::vector<cudaEvent_t> ready, done;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t g = gen;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
 struct cphifi_ctx_s {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cusolverDnHandle_t solver = nullptr;
     ncclComm_t comm = nullptr;
+    cphifi_vcomm_s* vcomm = nullptr;     // virtual communicator (one-GPU test hook), or null
+    cphifi::DevBuf<double> vc_scratch;   // this rank's reduction output before the copy-out
     int nranks = 1, rank = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // pinned scratch for small D2H reads (PCG scalars)
@@ -111,6 +144,7 @@ struct cphifi_mode_s {
     cphifi::DevBuf<double> umt;     // diag(mu) U' (the fused kernel's Xhat columns in the eigenbasis)
     bool have_umt = false;
     int64_t nzero = -1;             // leading exactly-zero (clamped) eigenvalues, rounded down to 8; lazily
+    uint64_t eig_gen = 0;           // bumped whenever (U, mu) are replaced: keys the plans' captured graphs
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;
@@ -145,6 +179,7 @@ struct cphifi_unaligned_s {
     // preconditioner state (lazy): eig(V), D
     bool have_veig = false;
     cphifi::DevBuf<double> uv, sv, dmat;
+    uint64_t veig_gen = 0;        // bumped whenever (U_V, sigma_V) / D are replaced (graph key)
     // fused operator kernel launch shape (k_fused.cu)
     int grid = 0;                 // CTAs (all co-resident)
     cphifi::DevBuf<int64_t> cta_beg;        // grid + 1 partition boundaries
@@ -161,7 +196,7 @@ struct cphifi_unaligned_s {
     // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
     int op = 0;
     cphifi::DevBuf<double> gram;            // n x rp x rp (built lazily)
-    bool gram_reduced = false;               // multi-GPU: gram holds the all-shard sum
+    cphifi::DevBuf<double> gram_sum;         // multi-rank finite-mode update: the all-shard row Grams
     cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU)
     cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid
     cphifi::DevBuf<unsigned> barrier;   // grid barrier state
@@ -175,6 +210,7 @@ struct cphifi_unaligned_s {
     cphifi::DevBuf<double> pcg_aux;           // reduction partials | PcgState | PcgCtl
     cphifi::DevBuf<double> pcg_step;          // fused vector step (k_pcgstep.cu): barrier word | partials
     int64_t pcg_graph_z = -1, pcgf_z = -1;    // mode_nzero baked into the captured graphs
+    uint64_t pcg_graph_gen = ~0ull, pcgf_gen = ~0ull;  // eigendecomposition generations baked into them
     cphifi::DevBuf<double> pcg_hist;          // device residual history
     cudaGraph_t pcg_graph = nullptr;
     cudaGraphExec_t pcg_exec = nullptr;

@@ -11,6 +11,8 @@
 // bit-reproducible run to run.
 #include <cooperative_groups.h>
 
+#include <map>
+
 #include "kernels.cuh"
 #include "tma.cuh"
 
@@ -235,13 +237,8 @@ void launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     // largest split (power of two <= 8) that still fits one wave of co-resident CTAs
     while (S < 8 && (int64_t)mt * nt * (2 * S) <= 2 * num_sms && g.k / (2 * S) >= 2 * BK) S *= 2;
     const size_t smem = sizeof(GemmSmem<BN>);
-    static bool attr_set = false;
-    if (!attr_set) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        CPHIFI_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_set = true;
-    }
+    func_attr_once((const void*)gemm_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    func_attr_once((const void*)gemm_dmma_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(mt, S, nt);
     cfg.blockDim = dim3(NT, 1, 1);
@@ -749,12 +746,7 @@ template <int BN, int WR, int WC, bool BROW = false, int AM = 0>
 void launch_v3(const MttkrpArgs& ap, const CUtensorMap& tm_t, const CUtensorMap& tm_a1, int mt, int64_t P, int nt,
                int64_t chunks, int64_t ktiles, const double* wout, double* work, cudaStream_t s) {
     const size_t smem3 = sizeof(Mttkrp3Smem<BN, AM>);
-    static bool attr3 = false;
-    if (!attr3) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v3_kernel<BN, WR, WC, BROW, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem3));
-        attr3 = true;
-    }
+    func_attr_once((const void*)mttkrp_v3_kernel<BN, WR, WC, BROW, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
     mttkrp_v3_kernel<BN, WR, WC, BROW, AM><<<dim3(mt, (unsigned)P, nt), V3<BN, WR, WC>::NC + 32, smem3, s>>>(ap, tm_t, tm_a1, chunks,
                                                                                            ktiles, wout, work);
     const cudaError_t le = cudaGetLastError();
@@ -787,12 +779,7 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
     kr_outer_kernel<<<(unsigned)((n_outer * a.r + 255) / 256), 256, 0, s>>>(aw, n_outer, wout);
     CPHIFI_CHECK_LAUNCH();
     const size_t smem = sizeof(GemmSmem<BN, BMM, STM>) + sizeof(double) * STM * BN;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-        attr_set = true;
-    }
+    func_attr_once((const void*)mttkrp_dmma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     bool v2 = BN <= 32;
     if (const char* e = std::getenv("CPHIFI_MTTKRP_V1")) v2 = v2 && std::atoi(e) == 0;
     // v3 (tensor-map TMA ring) needs 16-byte aligned bases and leading dimensions (even n0 and
@@ -819,12 +806,7 @@ void launch_mttkrp(const MttkrpArgs& a, int num_sms, cudaStream_t s, DevBuf<doub
                 launch_v3<BN, 32, BN, false>(ap, tm_t, tm_a1, mt, P, nt, chunks, ktiles, wout, work.get(), s);
             }
         } else if (v2) {
-            static bool attr2 = false;
-            if (!attr2) {
-                CPHIFI_CUDA(cudaFuncSetAttribute(mttkrp_v2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem));
-                attr2 = true;
-            }
+            func_attr_once((const void*)mttkrp_v2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             mttkrp_v2_kernel<BN><<<dim3(mt, (unsigned)P, nt), NTV, smem, s>>>(aw, chunks, ktiles, wout, work.get());
         }
     }
@@ -1087,6 +1069,17 @@ struct GrowScratch {
     double* get() const { return p; }
 };
 
+// Split-K partials: one grow-only buffer per CUDA stream (each context owns its stream, and all
+// work on a stream — direct launches and the graphs captured from it — runs in stream order, so
+// the buffer is never used by two GEMMs at once; graphs keep the address they captured, which
+// stays valid because outgrown buffers are retired, not freed).
+GrowScratch& stream_scratch(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, GrowScratch> per_stream;
+    std::lock_guard<std::mutex> lk(mu);
+    return per_stream[s];
+}
+
 // The plain GEMM runs the MTTKRP ring with a single Khatri-Rao outer row Wout = 1: one constant
 // buffer per device, filled once outside any graph capture (inside a capture the fill is a
 // captured node in front of the GEMM, and the buffer is filled again on the next uncaptured call).
@@ -1173,7 +1166,7 @@ int64_t splitk_depth_t(const GemmArgs& g, int num_sms) {  // as gemm_tma_t below
 
 template <int BN>
 void gemm_tma_t(const GemmArgs& g, int num_sms, cudaStream_t s) {
-    static thread_local GrowScratch work;
+    GrowScratch& work = stream_scratch(s);
     int dev = 0;
     CPHIFI_CUDA(cudaGetDevice(&dev));
     const bool brow = !(g.b_rs == 1);

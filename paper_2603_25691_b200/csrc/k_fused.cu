@@ -533,11 +533,7 @@ __global__ void __launch_bounds__(FT, 2) fused_matvec_kernel(const FusedArgs a) 
 template <int RP, int DO, bool SMEMF>
 void launch_fused_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     auto kern = fused_matvec_kernel<RP, DO, SMEMF>;
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM));
-        attr = true;
-    }
+    func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
     void* args[] = {const_cast<FusedArgs*>(&a)};
     CPHIFI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(FT), args, smem, s));
 }

@@ -311,12 +311,10 @@ size_t step_smem() {
 
 template <int JT>
 int step_grid(int64_t n, int num_sms) {
-    static int occ = -1;
-    if (occ < 0) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(pcg_step_fused_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)step_smem<JT>()));
-        CPHIFI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pcg_step_fused_kernel<JT>, ST, step_smem<JT>()));
-    }
+    func_attr_once((const void*)pcg_step_fused_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   (int)step_smem<JT>());
+    int occ = 0;  // per device (a query, not cached: cheap next to the cooperative launch)
+    CPHIFI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pcg_step_fused_kernel<JT>, ST, step_smem<JT>()));
     const int64_t nblk = (n + SRB - 1) / SRB;
     return (int)std::max<int64_t>(1, std::min<int64_t>(nblk, (int64_t)num_sms * std::min(std::max(occ, 1), 4)));
 }

@@ -148,11 +148,7 @@ __global__ void __launch_bounds__(LT) rowls_kernel(const double* __restrict__ g,
 template <int RP>
 void rowls_t(const double* g, const double* b, int64_t n, int64_t r, double* a_out, cudaStream_t s) {
     const size_t smem = sizeof(double) * 2 * RP * (RP + 1);
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(rowls_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    func_attr_once((const void*)rowls_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     rowls_kernel<RP><<<(unsigned)n, LT, smem, s>>>(g, b, n, (int)r, a_out);
 }
 

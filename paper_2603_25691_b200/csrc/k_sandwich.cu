@@ -259,11 +259,7 @@ template <int RP, int RB, int PH>
 void launch2_t(const SandArgs& a, cudaStream_t s) {
     auto kern = sandwich2_kernel<RP, RB, PH>;
     const size_t smem = sizeof(Sw2Smem<RP, RB>);
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     constexpr int KC = Sw2<RP>::KC;
     const uint64_t n = (uint64_t)a.n;
     CUtensorMap tf, tm;  // F = U or U' (n x n), M = X (ld ldx) or core (ld n); r columns of M
@@ -297,11 +293,7 @@ template <int RP, int RB, int PH>
 void launch_t(const SandArgs& a, cudaStream_t s) {
     auto kern = sandwich_kernel<RP, RB, PH>;
     const size_t smem = sizeof(SwSmem<RP, RB>);
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned grid = (unsigned)((a.n + RB - 1) / RB);
     kern<<<grid, SW_T, smem, s>>>(a);
     CPHIFI_CHECK_LAUNCH();
@@ -464,11 +456,7 @@ void launch_precond_rot(const double* rt, const double* uv, const double* dmat, 
                         cudaStream_t s) {
     constexpr int RP = JT * PR_W;
     const size_t smem = sizeof(double) * (RP * (RP + 2) + RP * PR_RB);
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(precond_rot_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    func_attr_once((const void*)precond_rot_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     precond_rot_kernel<JT><<<(unsigned)((n + PR_RB - 1) / PR_RB), PR_T, smem, s>>>(rt, uv, dmat, n, (int)r, zt);
     CPHIFI_CHECK_LAUNCH();
 }

@@ -574,11 +574,7 @@ int aux_kind(const FusedArgs& a) { return a.weights ? 2 : (a.mult ? 1 : 0); }
 template <int RP, int DO, bool SF, int AUX, bool PF>
 void launch_t(const FusedArgs& a, int grid, size_t smem, cudaStream_t s) {
     auto kern = stream_kernel<RP, DO, SF, AUX, PF>;
-    static bool attr = false;
-    if (!attr) {
-        CPHIFI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP));
-        attr = true;
-    }
+    func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP);
     kern<<<grid, ST, smem, s>>>(a);
 }
 

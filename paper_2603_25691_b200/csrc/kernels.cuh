@@ -278,6 +278,8 @@ void pcg_init(const double* r, const double* z, double* p, int64_t n, PcgState* 
               cudaStream_t s);
 // dst <- src (n doubles), a kernel copy when 16-byte aligned (mapped host memory allowed)
 void copy_doubles(double* dst, const double* src, int64_t n, cudaStream_t s);
+// out[i] = sum_{s < nsrc} src[s][i] in rank order (virtual communicator reduction, nsrc <= 8)
+void rank_order_sum(const double* const* src, int nsrc, double* out, size_t count, int num_sms, cudaStream_t s);
 // ---- aligned baselines (k_aligned.cu) ------------------------------------
 void aligned_matvec_dev(const double* x, const double* dk, const double* v, int64_t n, int64_t r, double lambda,
                         double* y, cudaStream_t s);

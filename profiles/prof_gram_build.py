@@ -12,7 +12,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2603_25691_b200 as cp  # noqa: E402
-from paper_2603_25691_b200 import _capi, configs  # noqa: E402
+from paper_2603_25691_b200 import _capi  # noqa: E402
+from inputs import configs
 
 ctx = cp.Context(0)
 lib = _capi.load()

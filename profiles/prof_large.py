@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 import paper_2603_25691_b200 as cp
-from paper_2603_25691_b200 import _capi, configs
+from paper_2603_25691_b200 import _capi
+from inputs import configs
 
 
 def main():

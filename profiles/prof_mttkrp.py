@@ -2,7 +2,8 @@ import sys, os, ctypes
 sys.path.insert(0, '/root/repo')
 import numpy as np
 import paper_2603_25691_b200 as cp
-from paper_2603_25691_b200 import _capi, configs
+from paper_2603_25691_b200 import _capi
+from inputs import configs
 c = configs.config2()
 ctx = cp.Context(0)
 n, r = c.shape[0], c.r

@@ -9,7 +9,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2603_25691_b200 as cp  # noqa: E402
-from paper_2603_25691_b200 import _capi, configs  # noqa: E402
+from paper_2603_25691_b200 import _capi  # noqa: E402
+from inputs import configs
 
 c = configs.config1()
 n, r = c.shape[0], c.r

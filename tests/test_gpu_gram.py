@@ -60,11 +60,18 @@ def test_gram_split_rows_and_empty_rows(cp):
 
 
 def test_gram_auto_resolution(cp):
-    c = ri.Inst([10, 8, 8], 4, 600, 0, 0.5, 0.1, 1e-6, 7)   # 60 obs / row >= 2 * rp = 8 -> gram
+    c = ri.Inst([600, 8, 8], 4, 12000, 0, 0.5, 0.1, 1e-6, 7)  # n > 512, 20 obs / row >= 2 * rp = 8 -> gram
     mode = cp.RkhsMode(c.points, c.sigma, c.lam)
     p = cp.make_unaligned_subproblem(cp.ObservationSet(c.shape, c.idx, c.vals), cp.KruskalModel(c.factors), 0, mode,
                                      c.rho)
+    assert p.operator() == "gram"          # a new plan starts with AUTO's choice
+    assert p.set_operator("stream") == "stream"
     assert p.set_operator("auto") == "gram"
+    c1 = ri.Inst([10, 8, 8], 4, 600, 0, 0.5, 0.1, 1e-6, 7)   # small n: the single fused launch -> stream
+    mode1 = cp.RkhsMode(c1.points, c1.sigma, c1.lam)
+    p1 = cp.make_unaligned_subproblem(cp.ObservationSet(c1.shape, c1.idx, c1.vals), cp.KruskalModel(c1.factors), 0,
+                                      mode1, c1.rho)
+    assert p1.operator() == "stream" and p1.set_operator("auto") == "stream"
     c2 = ri.Inst([50, 8, 8], 4, 60, 0, 0.5, 0.1, 1e-6, 8)   # ~1 obs / row -> stream
     mode2 = cp.RkhsMode(c2.points, c2.sigma, c2.lam)
     p2 = cp.make_unaligned_subproblem(cp.ObservationSet(c2.shape, c2.idx, c2.vals), cp.KruskalModel(c2.factors), 0,

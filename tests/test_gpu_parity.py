@@ -389,9 +389,11 @@ def test_large_config_structure_vs_oracle(cp, which, q, coalesce):
     b_o = orc.sampled_mttkrp_stream(cfg.shape, 0, hidx, hvals, model.factors, n)
     assert ri.rel(p.b, b_o) < 1e-12
     x = np.random.default_rng(1).normal(size=n * r)
-    y = cp.unaligned_matvec(p, x)
     y_o = orc.unaligned_matvec_stream(cfg.shape, 0, hidx, model.factors, kern, cfg.lam, cfg.rho, x)
-    assert ri.rel(y, y_o) < 1e-12
+    assert p.operator() == "gram"  # the drop-in default at these sizes (AUTO)
+    for op in ("stream", "gram"):
+        p.set_operator(op)
+        assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12, op
     if cfg.zipf_mode == 0:  # Zipf head: row 0 carries ~16 % of the draws
         frac0 = float((hidx[0] == 0).mean())
         assert 0.14 < frac0 < 0.18
