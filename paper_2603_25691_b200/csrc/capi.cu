@@ -69,6 +69,11 @@ struct DeviceGuard {
     }
 };
 
+// Plan columns carry OBS_PAD slack elements: the streaming kernels' TMA bulk copies round staged
+// columns to 16-byte boundaries (k_stream.cu) or copy whole CH-entry chunks (k_runs.cu, CH = 64)
+// and may read up to that many elements past the last one.
+constexpr int64_t OBS_PAD = 64;
+
 void need(const void* p, const char* what) {
     if (!p) throw_invalid(std::string(what) + ": null argument");
 }
@@ -250,10 +255,17 @@ struct PartitionPlan {
 
 // equal > 0: exactly `equal` CTAs of equal observation count (rows split wherever a boundary
 // falls; the kernel finishes split rows through its slots), else the row-aligned plan below.
-void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, PartitionPlan& pl, int equal = 0) {
+// `given` (non-empty, nondecreasing, from 0 to q): those CTA boundaries as they are.
+void plan_partition(const std::vector<int64_t>& rp, int cmax, int cmin, PartitionPlan& pl, int equal = 0,
+                    const std::vector<int64_t>* given = nullptr) {
     const int64_t n = (int64_t)rp.size() - 1, q = rp[n];
     std::vector<int64_t> starts;
-    if (equal > 0) {  // (empty CTAs dropped: the CTAs sharing a split row must be consecutive)
+    if (given) {
+        starts = *given;
+        starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+        if (starts.size() < 2) starts.assign({0, q});
+        equal = 1;  // no row-aligned search below
+    } else if (equal > 0) {  // (empty CTAs dropped: the CTAs sharing a split row must be consecutive)
         for (int c = 0; c <= equal; ++c) starts.push_back(q * c / equal);
         starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
         if (starts.size() < 2) starts.assign({0, q});
@@ -365,10 +377,192 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
 
 // Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
 // fused kernel restricted to PH_B.
+// The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
+// exist: with more than one part, Yhat is zeroed and every part adds into it, Yhat(i) =
+// (0 + part 0) + part 1 + ... in part order.
 void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
     a.phases = PH_B;
+    if (!p->parts.empty() && !a.weights) {
+        cudaStream_t s = p->obs->ctx->stream;
+        const int dl = p->obs->d - 2;  // the blocked (last) other mode's column / packed factor
+        const bool acc = p->parts.size() > 1;
+        if (acc) CPHIFI_CUDA(cudaMemsetAsync(a.yhat_rm, 0, sizeof(double) * p->n * p->rp, s));
+        for (const StreamPart& sp : p->parts) {
+            if (sp.q == 0) continue;
+            RunsArgs b;
+            b.rp = p->rp;
+            b.ldq = sp.ldq;
+            b.dother = p->obs->d - 1;
+            b.idx = sp.idx;
+            b.mult = sp.mult;
+            b.fac = a.fac;
+            for (int m = 0; m < b.dother; ++m) b.fac_off[m] = a.fac_off[m];
+            b.fac_off[dl] = a.fac_off[dl] + sp.row_lo * p->rp;
+            b.fac_total = b.fac_off[dl] + sp.rows * p->rp;
+            b.row_ptr = sp.row_ptr;
+            b.run_start = sp.run_start.get();
+            b.run_i1 = sp.run_i1.get();
+            b.nruns = sp.nruns;
+            b.warps = sp.warps;
+            b.warp_beg = sp.warp_beg.get();
+            b.warp_rows = sp.warp_rows.get();
+            b.row_first_w = sp.row_first_w.get();
+            b.row_nw = sp.row_nw.get();
+            b.xhat_rm = a.xhat_rm;
+            b.yhat_rm = a.yhat_rm;
+            b.slot_a = p->runs_slot_a.get();
+            b.slot_b = p->runs_slot_b.get();
+            b.rowcnt = a.rowcnt;
+            b.accumulate = acc ? 1 : 0;
+            runs_scatter_gather(b, sp.sf, s);
+        }
+        return;
+    }
     if (p->stream) stream_scatter_gather(a, p->grid, p->stream_sf, p->obs->ctx->stream);
     else launch_fused(p, a);
+}
+
+// The run kernel's parts (StreamPart, common.cuh; k_runs.cu).  When the per-observation factors
+// fit shared memory next to the kernel's per-warp buffers, one part aliases the plan.  Otherwise
+// the last other mode's factor is cut into H row blocks that do fit, and the plan is stably
+// partitioned by block (radix sort on the block id: plan order kept inside each part); each part
+// stages its block (config 4: A_3's 512 rows as 2 x 256, 128 KB each) instead of gathering rows
+// through L1 / L2 — 125 GB of L2 traffic per application, above the L2's bandwidth for 10 ms.
+// Then, per part: the run table and the equal-count warp ranges.  Returns false (no parts) when no
+// block size fits.
+void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_t nw) {
+    cphifi_ctx ctx = p->obs->ctx;
+    cudaStream_t s = ctx->stream;
+    const int64_t q = sp.q;
+    if (q > 0) {
+        DevBuf<int32_t> rs_tmp(q + 1);
+        const int64_t nr = build_run_starts(rows, sp.idx, q, rs_tmp.get(), s);
+        sp.nruns = nr;
+        sp.run_start.alloc(nr + 1);
+        CPHIFI_CUDA(cudaMemcpyAsync(sp.run_start.get(), rs_tmp.get(), sizeof(int32_t) * nr, cudaMemcpyDeviceToDevice, s));
+        const int32_t qq = (int32_t)q;
+        h2d(sp.run_start.get() + nr, &qq, sizeof(int32_t), s);
+        sp.run_i1.alloc(std::max<int64_t>(nr, 1));
+        gather_i32(sp.idx, sp.run_start.get(), 0, nr, sp.run_i1.get(), s);
+    }
+    std::vector<int64_t> rp_host(p->n + 1);
+    d2h_sync(rp_host.data(), sp.row_ptr, sizeof(int64_t) * (p->n + 1), s);
+    // warp ranges of equal COST, cost = entries + C x runs started: a warp's time grows with its
+    // runs as well as its entries (per-run work: the A_1 row, u, the partial last step), so an
+    // equal-count split leaves the warps in sparse rows (short runs) far behind the others
+    double cpr = 12.0;
+    if (const char* e = std::getenv("CPHIFI_RUNS_RUNCOST")) cpr = std::atof(e);
+    std::vector<int64_t> starts;
+    if (q > 0 && cpr > 0.0) {
+        std::vector<int32_t> rs(sp.nruns + 1);
+        d2h_sync(rs.data(), sp.run_start.get(), sizeof(int32_t) * (sp.nruns + 1), s);
+        const double total = (double)q + cpr * (double)sp.nruns;
+        starts.push_back(0);
+        int64_t j = 0;  // run holding the current target
+        for (int64_t wi = 1; wi < nw; ++wi) {
+            const double tgt = total * (double)wi / (double)nw;
+            while (j + 1 < sp.nruns && (double)rs[j + 1] + cpr * (double)(j + 1) <= tgt) ++j;
+            const double c0 = (double)rs[j] + cpr * (double)j;  // cost at run j's start
+            int64_t e = rs[j] + (int64_t)std::max(0.0, tgt - c0 - cpr);
+            e = std::min<int64_t>(std::max<int64_t>(e, rs[j]), rs[j + 1]);
+            starts.push_back(std::max(e, starts.back()));
+        }
+        starts.push_back(q);
+    }
+    PartitionPlan plan;
+    plan_partition(rp_host, (int)nw, (int)nw, plan, (int)nw, starts.empty() ? nullptr : &starts);
+    sp.warps = plan.ctas;
+    sp.warp_beg.alloc(plan.beg.size());
+    h2d(sp.warp_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
+    sp.warp_rows.alloc(plan.rows.size());
+    h2d(sp.warp_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
+    sp.row_first_w.alloc(p->n);
+    h2d(sp.row_first_w.get(), plan.row_first_cta.data(), sizeof(int32_t) * p->n, s);
+    sp.row_nw.alloc(p->n);
+    h2d(sp.row_nw.get(), plan.row_ncta.data(), sizeof(int32_t) * p->n, s);
+    CPHIFI_CUDA(cudaStreamSynchronize(s));  // host plan vectors go out of scope
+}
+
+bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
+    cphifi_obs o = p->obs;
+    cphifi_ctx ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
+    const int d = o->d, k = o->k, dl = d - 2;  // dl: column of the blocked mode in idx_o
+    const bool mult = o->coalesced;
+    const int64_t nw = (int64_t)ctx->num_sms * runs_warps_per_sm();
+    int lm = -1;  // the blocked mode itself (last mode != k)
+    for (int m = d - 1; m >= 0 && lm < 0; --m)
+        if (m != k) lm = m;
+    const int64_t nl = o->shape[lm], rp = p->rp, q = o->q_local;
+    DevBuf<int32_t> rows(std::max<int64_t>(q, 1));
+    row_of_entries(o->row_ptr.get(), p->n, q, rows.get(), s);
+    if (runs_smem_bytes(rp, d - 1, mult, sf_all) <= runs_smem_cap()) {  // one part: the plan itself
+        std::vector<StreamPart> parts(1);
+        StreamPart& sp = parts[0];
+        sp.q = q;
+        sp.ldq = o->ldq;
+        sp.rows = nl;
+        sp.idx = o->idx_o.get();
+        sp.mult = mult ? o->mult.get() : nullptr;
+        sp.row_ptr = o->row_ptr.get();
+        sp.sf = sf_all;
+        finish_part(p, sp, rows.get(), nw);
+        p->parts = std::move(parts);
+        return true;
+    }
+    const int64_t rest = sf_all - nl * rp;  // staged doubles of the other per-observation modes
+    int64_t br = 0;
+    for (int64_t b = nl; b >= 8; b -= 8)
+        if (runs_smem_bytes(rp, d - 1, mult, rest + b * rp) <= runs_smem_cap()) {
+            br = b;
+            break;
+        }
+    if (br < 8) return false;
+    const int H = (int)((nl + br - 1) / br);
+    br = (nl + H - 1) / H;  // balanced blocks
+    DevBuf<int32_t> key(std::max<int64_t>(q, 1)), key_s(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
+        perm(std::max<int64_t>(q, 1)), rows_h(std::max<int64_t>(q, 1));
+    DevBuf<int64_t> bounds(H + 1);
+    block_key(o->idx_o.get() + (int64_t)dl * o->ldq, q, (int32_t)br, key.get(), s);
+    iota32(perm_in.get(), q, s);
+    int bits = 1;
+    while ((1 << bits) < H) ++bits;
+    if (q > 0) {
+        const size_t tb = radix_sort_pairs_bytes(q, bits);
+        DevBuf<unsigned char> tmp(tb);
+        radix_sort_pairs(tmp.get(), tb, key.get(), key_s.get(), perm_in.get(), perm.get(), q, bits, s);
+    }
+    csr_from_sorted(key_s.get(), q, H, bounds.get(), s);  // bounds[h] = first entry of part h
+    std::vector<int64_t> hb(H + 1);
+    d2h_sync(hb.data(), bounds.get(), sizeof(int64_t) * (H + 1), s);
+    std::vector<StreamPart> parts(H);
+    for (int h = 0; h < H; ++h) {
+        StreamPart& sp = parts[h];
+        const int64_t lo = hb[h], cnt = hb[h + 1] - hb[h];
+        sp.q = cnt;
+        sp.ldq = (cnt + 3) / 4 * 4;
+        sp.row_lo = h * br;
+        sp.rows = std::min(br, nl - sp.row_lo);
+        sp.sf = rest + sp.rows * rp;
+        sp.idx_own.alloc((int64_t)(d - 1) * sp.ldq + OBS_PAD);
+        for (int m = 0; m < d - 1; ++m)
+            gather_i32(o->idx_o.get() + (int64_t)m * o->ldq, perm.get(), lo, cnt, sp.idx_own.get() + (int64_t)m * sp.ldq,
+                       s);
+        add_i32(sp.idx_own.get() + (int64_t)dl * sp.ldq, cnt, (int32_t)(-sp.row_lo), s);
+        sp.idx = sp.idx_own.get();
+        if (mult) {
+            sp.mult_own.alloc(cnt + OBS_PAD);
+            gather_i32(o->mult.get(), perm.get(), lo, cnt, sp.mult_own.get(), s);
+            sp.mult = sp.mult_own.get();
+        }
+        gather_i32(rows.get(), perm.get(), lo, cnt, rows_h.get(), s);
+        sp.row_ptr_own.alloc(p->n + 1);
+        csr_from_sorted(rows_h.get(), cnt, p->n, sp.row_ptr_own.get(), s);
+        sp.row_ptr = sp.row_ptr_own.get();
+        finish_part(p, sp, rows_h.get(), nw);
+    }
+    p->parts = std::move(parts);
+    return true;
 }
 
 // Row-Gram operator: build G_i = sum_l z_l z_l' once (k_gram.cu), on first use.
@@ -1205,9 +1399,6 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count) {
 }
 
 // ---- observations (observations.hpp:18-79) --------------------------------------------
-// Plan columns carry OBS_PAD slack elements: k_stream.cu's TMA bulk copies round each staged
-// column to 16-byte boundaries and may read a few elements past the last one.
-constexpr int64_t OBS_PAD = 16;
 int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, const int32_t* idx,
                       const double* values, int k, uint32_t flags, int shard, int shards, cphifi_obs* out) {
     return guard([&] {
@@ -1457,6 +1648,15 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
             if (const char* e = std::getenv("CPHIFI_STREAM_SF")) use_sf = use_sf && std::atoi(e) != 0;
             p->stream_sf = use_sf ? sf : 0;
             cmax = ctx->num_sms;
+            // the operator's q-pass on the run kernel (k_runs.cu) over the plan's parts
+            bool runs = p->mode && runs_supported(p->rp, d - 1);
+            if (const char* e = std::getenv("CPHIFI_RUNS")) runs = runs && std::atoi(e) != 0;
+            if (runs && build_run_parts(p, sf)) {
+                int w = 0;
+                for (const auto& sp : p->parts) w = std::max(w, sp.warps);
+                p->runs_slot_a.alloc((size_t)w * p->rp);
+                p->runs_slot_b.alloc((size_t)w * p->rp);
+            }
         } else {
             p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
             cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);

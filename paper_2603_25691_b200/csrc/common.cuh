@@ -167,6 +167,26 @@ struct cphifi_obs_s {
     bool coalesced = false;
 };
 
+// One part of the operator's q-pass for the run kernel (k_runs.cu): the plan entries whose LAST
+// other-mode index falls in rows [row_lo, row_lo + rows) of that factor (all of them when the
+// whole factor fits shared memory: the part then aliases the plan), in plan order, that index
+// rebased to the block, with their own CSR, run table and per-warp entry ranges.
+struct StreamPart {
+    int64_t q = 0, ldq = 0;              // entries; column stride (multiple of 4)
+    int64_t row_lo = 0, rows = 0;        // block of the last other mode
+    const int32_t* idx = nullptr;        // (d-1) x ldq, last column rebased
+    const int32_t* mult = nullptr;       // coalesced plans
+    const int64_t* row_ptr = nullptr;    // n + 1
+    cphifi::DevBuf<int32_t> idx_own, mult_own;  // owned copies (block parts)
+    cphifi::DevBuf<int64_t> row_ptr_own;
+    int64_t sf = 0;                      // staged factor doubles
+    cphifi::DevBuf<int32_t> run_start, run_i1;  // run table (nruns + 1 / nruns)
+    int64_t nruns = 0;
+    int warps = 0;                       // equal-count warp ranges
+    cphifi::DevBuf<int64_t> warp_beg, warp_rows;
+    cphifi::DevBuf<int32_t> row_first_w, row_nw;
+};
+
 struct cphifi_unaligned_s {
     cphifi_obs obs = nullptr;
     cphifi_mode mode = nullptr;
@@ -192,6 +212,8 @@ struct cphifi_unaligned_s {
     bool prefetch = false;        // X and K columns staged in shared memory (small n * r)
     bool stream = false;          // phase B runs k_stream.cu (large plans) instead of k_fused.cu
     int64_t stream_sf = 0;        // doubles of per-observation factors k_stream.cu stages in smem (0: L1)
+    std::vector<StreamPart> parts;  // non-empty: the operator's q-pass is the run kernel over these parts
+    cphifi::DevBuf<double> runs_slot_a, runs_slot_b;  // warps x rp: split-row partials of the run kernel
     cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters
     // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
     int op = 0;

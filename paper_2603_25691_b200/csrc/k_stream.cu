@@ -341,10 +341,13 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
         const bool split = ncta > 1;
         const int64_t first_row = a.cta_rows[2 * c];
         if (tid < RP) {
-            double* dst = !split ? a.yhat_rm + row * RP
-                        : row == first_row ? a.slot_a + (int64_t)c * RP
-                                           : a.slot_b + (int64_t)c * RP;
-            dst[tid] = red2[tid];
+            if (!split) {
+                double* dst = a.yhat_rm + row * RP + tid;
+                *dst = a.accumulate ? *dst + red2[tid] : red2[tid];
+            } else {
+                double* dst = row == first_row ? a.slot_a + (int64_t)c * RP : a.slot_b + (int64_t)c * RP;
+                dst[tid] = red2[tid];
+            }
         }
         if (split) {  // the last of the row's CTAs to arrive sums the slots in CTA order
             __syncthreads();
@@ -359,7 +362,8 @@ __global__ void __launch_bounds__(ST, 1) stream_kernel(const FusedArgs a) {
                 double s = a.row_ptr[row] == a.cta_beg[u0] ? __ldcg(a.slot_a + (int64_t)u0 * RP + tid)
                                                            : __ldcg(a.slot_b + (int64_t)u0 * RP + tid);
                 for (int u = u0 + 1; u < u0 + ncta; ++u) s += __ldcg(a.slot_a + (int64_t)u * RP + tid);
-                a.yhat_rm[row * RP + tid] = s;
+                double* dst = a.yhat_rm + row * RP + tid;
+                *dst = a.accumulate ? *dst + s : s;
             }
         }
     };

@@ -437,6 +437,69 @@ void gather_f64(const double* src, const int32_t* perm, int64_t lo, int64_t cnt,
     gather_f64_kernel<<<grid_for(cnt, 256), 256, 0, s>>>(src, perm, lo, cnt, dst);
     CPHIFI_CHECK_LAUNCH();
 }
+namespace {
+__global__ void block_key_kernel(const int32_t* col, int64_t q, int32_t rows, int32_t* key) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < q; l += (int64_t)gridDim.x * blockDim.x)
+        key[l] = col[l] / rows;
+}
+__global__ void row_of_kernel(const int64_t* row_ptr, int64_t n, int64_t q, int32_t* rows) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < q; l += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;  // largest i with row_ptr[i] <= l
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (row_ptr[mid] <= l) lo = mid;
+            else hi = mid - 1;
+        }
+        rows[l] = (int32_t)lo;
+    }
+}
+__global__ void add_i32_kernel(int32_t* p, int64_t cnt, int32_t delta) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < cnt; l += (int64_t)gridDim.x * blockDim.x)
+        p[l] += delta;
+}
+}  // namespace
+
+void block_key(const int32_t* col, int64_t q, int32_t rows, int32_t* key, cudaStream_t s) {
+    if (q == 0) return;
+    block_key_kernel<<<grid_for(q, 256), 256, 0, s>>>(col, q, rows, key);
+    CPHIFI_CHECK_LAUNCH();
+}
+void row_of_entries(const int64_t* row_ptr, int64_t n, int64_t q, int32_t* rows, cudaStream_t s) {
+    if (q == 0) return;
+    row_of_kernel<<<grid_for(q, 256), 256, 0, s>>>(row_ptr, n, q, rows);
+    CPHIFI_CHECK_LAUNCH();
+}
+void add_i32(int32_t* p, int64_t cnt, int32_t delta, cudaStream_t s) {
+    if (cnt == 0 || delta == 0) return;
+    add_i32_kernel<<<grid_for(cnt, 256), 256, 0, s>>>(p, cnt, delta);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+namespace {
+__global__ void run_flag_kernel(const int32_t* rows, const int32_t* col0, int64_t q, unsigned char* flag) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < q; l += (int64_t)gridDim.x * blockDim.x)
+        flag[l] = l == 0 || rows[l] != rows[l - 1] || col0[l] != col0[l - 1];
+}
+}  // namespace
+
+int64_t build_run_starts(const int32_t* rows, const int32_t* col0, int64_t q, int32_t* run_start, cudaStream_t s) {
+    if (q == 0) return 0;
+    DevBuf<unsigned char> flag(q);
+    DevBuf<int32_t> iota(q);
+    DevBuf<int64_t> nsel(1);
+    run_flag_kernel<<<grid_for(q, 256), 256, 0, s>>>(rows, col0, q, flag.get());
+    CPHIFI_CHECK_LAUNCH();
+    iota32(iota.get(), q, s);
+    size_t bytes = 0;
+    CPHIFI_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), run_start, nsel.get(), q, s));
+    DevBuf<unsigned char> tmp(bytes);
+    CPHIFI_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, iota.get(), flag.get(), run_start, nsel.get(), q, s));
+    int64_t nr = 0;
+    CPHIFI_CUDA(cudaMemcpyAsync(&nr, nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CPHIFI_CUDA(cudaStreamSynchronize(s));
+    return nr;
+}
+
 void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr, cudaStream_t s) {
     csr_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(keys, q, n, row_ptr);
     CPHIFI_CHECK_LAUNCH();

@@ -137,6 +137,7 @@ struct FusedArgs {
     int64_t fac_total = 0;              // doubles in fac
     const double* weights = nullptr;    // non-null: s_l = weights[l] (RHS B), else Xhat . z_l
     const int32_t* mult = nullptr;      // coalesced plan: operator weight of entry l (dot mode)
+    int accumulate = 0;                 // k_stream.cu: add into yhat_rm instead of overwriting (stream parts > 0)
     const double* kmat = nullptr;       // n x n column-major, symmetric
     const double* x = nullptr;          // n x r column-major
     double* y = nullptr;                // n x r column-major
@@ -183,6 +184,44 @@ size_t stream_smem_bytes(int64_t rp, int dother, int64_t sf_doubles, int aux_byt
 size_t stream_smem_cap();
 // sf_doubles > 0: that many doubles of per-observation factors are staged in shared memory
 void stream_scatter_gather(const FusedArgs& a, int grid, int64_t sf_doubles, cudaStream_t s);
+
+// ---- the operator's q-pass as a run-structured streaming kernel (k_runs.cu) ---------------
+// Per-observation factors staged in shared memory (a factor-block part of the plan when they do
+// not fit), per-warp equal-count entry ranges, a precomputed run table (runs of equal first other
+// index within a row), per-warp TMA rings of plan chunks.  Operator mode only (s_l = Xhat . z_l).
+struct RunsArgs {
+    int64_t rp = 0, ldq = 0;             // padded rank; column stride of idx (multiple of 4)
+    int dother = 0;
+    const int32_t* idx = nullptr;        // dother columns (other modes ascending), plan order
+    const int32_t* mult = nullptr;       // coalesced plan: multiplicities, else null
+    const double* fac = nullptr;         // packed row-major rp-padded factors
+    int64_t fac_off[8] = {0};
+    int64_t fac_total = 0;
+    const int64_t* row_ptr = nullptr;    // n + 1
+    const int32_t* run_start = nullptr;  // nruns + 1 (last = q)
+    const int32_t* run_i1 = nullptr;     // nruns: first other index of each run
+    int64_t nruns = 0;
+    int warps = 0;                       // warp ranges
+    const int64_t* warp_beg = nullptr;   // warps + 1
+    const int64_t* warp_rows = nullptr;  // 2 x warps: first / last row
+    const int32_t* row_first_w = nullptr;  // n: first warp touching the row
+    const int32_t* row_nw = nullptr;       // n: warps touching the row (> 1 = split row)
+    const double* xhat_rm = nullptr;     // n x rp
+    double* yhat_rm = nullptr;           // n x rp
+    double* slot_a = nullptr;            // warps x rp (a warp's first row when shared)
+    double* slot_b = nullptr;            // warps x rp (its last row when shared)
+    unsigned* rowcnt = nullptr;          // n arrival counters, zero between launches
+    int accumulate = 0;                  // add into yhat_rm (stream parts) instead of overwriting
+};
+bool runs_supported(int64_t rp, int dother);
+size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles);
+size_t runs_smem_cap();
+int runs_warps_per_sm();
+int runs_chunk();
+void runs_scatter_gather(const RunsArgs& a, int64_t sf_doubles, cudaStream_t s);
+// run table of a plan: run_start[j] = first entry of run j (entry l starts a run when it starts a
+// row or its first other index differs from entry l-1's); returns the number of runs (synchronous)
+int64_t build_run_starts(const int32_t* rows, const int32_t* col0, int64_t q, int32_t* run_start, cudaStream_t s);
 
 // ---- row-Gram operator (k_gram.cu): Yhat(i,:) = G_i Xhat(i,:), G_i = sum_l z_l z_l' ---------
 struct GramArgs {
@@ -325,6 +364,11 @@ void iota32(int32_t* p, int64_t q, cudaStream_t s);
 void gather_i32(const int32_t* src, const int32_t* perm, int64_t lo, int64_t cnt, int32_t* dst, cudaStream_t s);
 void gather_f64(const double* src, const int32_t* perm, int64_t lo, int64_t cnt, double* dst, cudaStream_t s);
 void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr, cudaStream_t s);
+// stream parts (capi.cu build_stream_parts): key[l] = col[l] / rows; rows[l] = the CSR row of entry l;
+// p[l] += delta
+void block_key(const int32_t* col, int64_t q, int32_t rows, int32_t* key, cudaStream_t s);
+void row_of_entries(const int64_t* row_ptr, int64_t n, int64_t q, int32_t* rows, cudaStream_t s);
+void add_i32(int32_t* p, int64_t cnt, int32_t delta, cudaStream_t s);
 size_t radix_sort_pairs_bytes(int64_t q, int bits);
 void radix_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
                       const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
