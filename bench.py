@@ -13,7 +13,7 @@ metric names none), so it is the N = 1 workload.
 application streams the ~2.9 GB coalesced plan, far above the 126 MB L2 (inputs larger than L2).
 `e2e` is the same metric through the reference-facing host-buffer C-ABI call
 (cphifi_unaligned_matvec: x copied in from pinned host memory, y read back, every step).
-`roofline` is the dominant kernel (the streaming scatter-gather, k_stream.cu) against the
+`roofline` is the dominant kernel (the run-structured scatter-gather, k_runs.cu) against the
 measured HBM peak on the as-given algorithmic bytes of SURVEY §8(d); `cpu_baseline` is the
 oracle's streaming C port on a bounded sample of the same draws.
 
@@ -320,7 +320,9 @@ def main():
         k1_bytes = alg_bytes_k1(d, q // world, n, r)
         k1_s = k1_ms / 1e3
         achieved = k1_bytes / k1_s / 1e9
-        traffic, traffic_src = ncu_traffic("ncu_full_stream_config4.json", "stream_kernel")
+        traffic, traffic_src = ncu_traffic("ncu_full_runs_config4.json", "runs_kernel")
+        if traffic is not None:
+            traffic *= 2  # per application: one launch per factor-block part (2 at config 4)
         t_app = total_ms / args.steps / 1e3
         b_alg, f_alg = alg_bytes_matvec(d, q, n, r), alg_flops_matvec(d, q, n, r)
         out = {
@@ -334,7 +336,8 @@ def main():
                        "timing": "K applications back to back on the library stream between one CUDA event pair",
                        "parallelism": (f"observations sharded x{world} (equal-count slices of the sorted plan), "
                                        "n x r all-reduce per application") if world > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "kernel": "stream_kernel (k_stream.cu: the per-observation gather / scatter)",
+            "roofline": {"bound": "hbm", "kernel": "runs_kernel (k_runs.cu: the per-observation gather / scatter, "
+                                                  "2 launches per application, one per factor-block part)",
                          "achieved": achieved, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                          "alg_bytes_per_launch": k1_bytes,
@@ -348,7 +351,7 @@ def main():
                      "note": "SURVEY 8(d): t_roof = max(B_alg/HBM, F_alg/P_FP64) on the as-given q draws; dedup of "
                              "repeated draws and the hoisted first mode make the executed flops lower"},
             "matvec_hbm_frac": b_alg / t_app / 1e9 / hbm,
-            "phase_ms": {nm: ms6[i] for i, nm in enumerate(["K_X_gemm", "stream_kernel", "-", "allreduce",
+            "phase_ms": {nm: ms6[i] for i, nm in enumerate(["K_X_gemm", "runs_kernel", "-", "allreduce",
                                                             "y_gemm", "whole_application"])},
             "e2e": {"value": args.steps / e2e_s, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * r,
                     "d2h_bytes_per_step": 8 * n * r,

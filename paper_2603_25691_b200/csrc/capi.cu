@@ -74,6 +74,9 @@ struct DeviceGuard {
 // and may read up to that many elements past the last one.
 constexpr int64_t OBS_PAD = 64;
 
+// a kernel's eigenvalues below -PSD_TOL * max(|mu|_max, 1) make it indefinite (not a rounding artefact)
+constexpr double PSD_TOL = 1e-10;
+
 void need(const void* p, const char* what) {
     if (!p) throw_invalid(std::string(what) + ": null argument");
 }
@@ -127,7 +130,8 @@ int read_flag(cphifi_ctx ctx, int* dflag) {
 }
 
 // sym_eig (kernel.hpp:40-49) on a device matrix: symmetry check, syevd, clamp at 0.
-void device_sym_eig(cphifi_ctx ctx, const double* a, int64_t n, double* u_out, double* d_out) {
+// Returns the smallest and largest eigenvalue before the clamp (syevd: ascending order).
+std::pair<double, double> device_sym_eig(cphifi_ctx ctx, const double* a, int64_t n, double* u_out, double* d_out) {
     DevBuf<double> chk(2);
     max_asym(a, n, chk.get(), ctx->stream);
     double h[2];
@@ -144,7 +148,11 @@ void device_sym_eig(cphifi_ctx ctx, const double* a, int64_t n, double* u_out, d
     int hinfo = 0;
     d2h_sync(&hinfo, info.get(), sizeof(int), ctx->stream);
     if (hinfo != 0) throw_runtime("sym_eig: eigendecomposition failed");
+    double ext[2] = {0.0, 0.0};
+    d2h_sync(&ext[0], d_out, sizeof(double), ctx->stream);
+    d2h_sync(&ext[1], d_out + n - 1, sizeof(double), ctx->stream);
     clamp_nonneg(d_out, n, ctx->stream);
+    return {ext[0], ext[1]};
 }
 
 void mode_eig_once(cphifi_mode m) {
@@ -154,7 +162,8 @@ void mode_eig_once(cphifi_mode m) {
         DeviceGuard dg(m->ctx->device);
         m->u.alloc(m->n * m->n);
         m->mu.alloc(m->n);
-        device_sym_eig(m->ctx, m->kernel.get(), m->n, m->u.get(), m->mu.get());
+        const auto ext = device_sym_eig(m->ctx, m->kernel.get(), m->n, m->u.get(), m->mu.get());
+        m->psd = ext.first >= -PSD_TOL * std::max(std::fabs(ext.second), 1.0);
         m->have_eig = true;
         m->eig_count = 1;
     });
@@ -377,11 +386,25 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
 
 // Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
 // fused kernel restricted to PH_B.
+// The run kernel's parts and split-row slots, on the first use (never inside a graph capture: every
+// capture site applies the operator once before capturing, and the solve calls this in its setup).
+void ensure_runs(cphifi_unaligned p) {
+    if (!p->runs_pending) return;
+    p->runs_pending = false;
+    if (build_run_parts(p, p->runs_sf)) {
+        int w = 0;
+        for (const auto& sp : p->parts) w = std::max(w, sp.warps);
+        p->runs_slot_a.alloc((size_t)w * p->rp);
+        p->runs_slot_b.alloc((size_t)w * p->rp);
+    }
+}
+
 // The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
 // exist: with more than one part, Yhat is zeroed and every part adds into it, Yhat(i) =
 // (0 + part 0) + part 1 + ... in part order.
 void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
     a.phases = PH_B;
+    if (!a.weights) ensure_runs(p);
     if (!p->parts.empty() && !a.weights) {
         cudaStream_t s = p->obs->ctx->stream;
         const int dl = p->obs->d - 2;  // the blocked (last) other mode's column / packed factor
@@ -792,10 +815,15 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
 // the preconditioner becomes  M~^-1 r~ = ((r~ U_V) o D) U_V'  — no n x n product.  Two n x n x r
 // GEMMs per iteration instead of four (K X, K Yhat, U'R, U Z).  K differs from its clamped
 // reconstruction by the clamped negative eigenvalues (rounding-level for the configs' kernels).
+// Only for a kernel that is positive semidefinite up to rounding (mode->psd, decided when the
+// eigendecomposition is computed or installed): there the clamped reconstruction differs from K at
+// rounding level.  A markedly indefinite K (a caller-supplied matrix) keeps the original basis, so
+// the operator is the reference's own, K included, and p'Ap <= 0 is detected as the reference does
+// (solvers.hpp:65-68).
 bool pcg_eigbasis(cphifi_unaligned p) {
     bool on = true;
     if (const char* e = std::getenv("CPHIFI_PCG_EIGBASIS")) on = std::atoi(e) != 0;
-    return on && p->mode;
+    return on && p->mode && p->mode->psd;
 }
 
 // leading rows / columns of the eigenbasis that the large-n operator skips (mode_nzero; 0 when off)
@@ -1380,6 +1408,12 @@ int cphifi_mode_set_eig(cphifi_mode mode, const double* u, const double* mu) {
         h2d(mode->mu.get(), mu, sizeof(double) * n, mode->ctx->stream);
         clamp_nonneg(mode->mu.get(), n, mode->ctx->stream);
         CPHIFI_CUDA(cudaStreamSynchronize(mode->ctx->stream));
+        double lo = 0.0, hi = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            lo = std::min(lo, mu[i]);
+            hi = std::max(hi, std::fabs(mu[i]));
+        }
+        mode->psd = lo >= -PSD_TOL * std::max(hi, 1.0);
         mode->have_eig = true;
         mode->eig_count = 1;
         ++mode->eig_gen;  // plans recapture their PCG graphs (eig_generation)
@@ -1648,15 +1682,12 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
             if (const char* e = std::getenv("CPHIFI_STREAM_SF")) use_sf = use_sf && std::atoi(e) != 0;
             p->stream_sf = use_sf ? sf : 0;
             cmax = ctx->num_sms;
-            // the operator's q-pass on the run kernel (k_runs.cu) over the plan's parts
+            // the operator's q-pass on the run kernel (k_runs.cu) over the plan's parts, built on the
+            // first stream-operator application (ensure_runs): a row-Gram solve never needs them
             bool runs = p->mode && runs_supported(p->rp, d - 1);
             if (const char* e = std::getenv("CPHIFI_RUNS")) runs = runs && std::atoi(e) != 0;
-            if (runs && build_run_parts(p, sf)) {
-                int w = 0;
-                for (const auto& sp : p->parts) w = std::max(w, sp.warps);
-                p->runs_slot_a.alloc((size_t)w * p->rp);
-                p->runs_slot_b.alloc((size_t)w * p->rp);
-            }
+            p->runs_pending = runs;
+            p->runs_sf = sf;
         } else {
             p->smem = fused_smem_bytes(p->rp, d - 1, (int64_t)p->fac.n, p->smem_factors, pref);
             cmax = fused_grid(p->rp, d - 1, p->smem_factors, p->smem, ctx->num_sms);
@@ -2219,6 +2250,7 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         else gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
         if (p->op == 1) ensure_gram(p);  // the row-Gram operator's G: per-solve setup, timed as such
+        else ensure_runs(p);             // the stream operator's run tables and warp ranges
         CPHIFI_CUDA(cudaStreamSynchronize(s));
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;

@@ -6,6 +6,8 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cmath>
 #include <condition_variable>
 #include <mutex>
 #include <stdexcept>
@@ -145,6 +147,7 @@ struct cphifi_mode_s {
     bool have_umt = false;
     int64_t nzero = -1;             // leading exactly-zero (clamped) eigenvalues, rounded down to 8; lazily
     uint64_t eig_gen = 0;           // bumped whenever (U, mu) are replaced: keys the plans' captured graphs
+    bool psd = true;                // K positive semidefinite up to rounding (eigenbasis PCG allowed)
     std::once_flag once;
     bool have_eig = false;
     int eig_count = 0;
@@ -214,6 +217,8 @@ struct cphifi_unaligned_s {
     int64_t stream_sf = 0;        // doubles of per-observation factors k_stream.cu stages in smem (0: L1)
     std::vector<StreamPart> parts;  // non-empty: the operator's q-pass is the run kernel over these parts
     cphifi::DevBuf<double> runs_slot_a, runs_slot_b;  // warps x rp: split-row partials of the run kernel
+    bool runs_pending = false;    // parts not built yet (ensure_runs)
+    int64_t runs_sf = 0;          // staged per-observation factor doubles of the whole plan
     cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters
     // row-Gram operator (k_gram.cu): op = 0 per-observation stream, 1 row-Gram
     int op = 0;
