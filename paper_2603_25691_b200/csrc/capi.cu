@@ -386,6 +386,8 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
 
 // Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
 // fused kernel restricted to PH_B.
+bool build_run_parts(cphifi_unaligned p, int64_t sf_all);
+
 // The run kernel's parts and split-row slots, on the first use (never inside a graph capture: every
 // capture site applies the operator once before capturing, and the solve calls this in its setup).
 void ensure_runs(cphifi_unaligned p) {
