@@ -184,30 +184,31 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
     auto ring_at = [&](int rel, int col) -> int32_t { return ring[col * RING + (rel & (RING - 1))]; };
 
     // ---- runs, rows ------------------------------------------------------------------------
-    int64_t r = 0;
+    int r = 0;  // runs and rows fit 32 bits (plans hold < 2^31 entries)
+    const int nruns = (int)a.nruns;
     if (lane == 0) {  // largest r with run_start[r] <= e0
-        int64_t lo = 0, hi = a.nruns - 1;
+        int lo = 0, hi = nruns - 1;
         while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
+            const int mid = (lo + hi + 1) >> 1;
             if (a.run_start[mid] <= e0) lo = mid;
             else hi = mid - 1;
         }
         r = lo;
     }
     r = __shfl_sync(0xffffffffu, r, 0);
-    const int64_t r0 = r;
-    int64_t cur_row = a.warp_rows[2 * w];
-    const int64_t first_row = cur_row;
+    const int r0 = r;
+    int cur_row = (int)a.warp_rows[2 * w];
+    const int first_row = cur_row;
     int row_end = (int)(min(a.row_ptr[cur_row + 1], e_end64) - cbase);
     // relative ends of runs r, r+1 (start of the run after), first other index of run r+2
-    auto rel_of = [&](int64_t k) { return (int)(min((int64_t)a.run_start[min(k, a.nruns)], e_end64) - cbase); };
+    auto rel_of = [&](int k) { return (int)(min((int64_t)a.run_start[min(k, nruns)], e_end64) - cbase); };
     int rs1 = rel_of(r + 1), rs2 = rel_of(r + 2);
-    int32_t i1_2 = r + 2 < a.nruns ? a.run_i1[r + 2] : 0;
+    int32_t i1_2 = r + 2 < nruns ? a.run_i1[r + 2] : 0;
     const double* fa1 = a.fac + a.fac_off[0];
     int xcnt = 0;  // Xhat-row loads issued (barrier phase)
     if (lane == 0) {
         tma::mbar_expect_tx(bar_x, RP * 8);
-        tma::bulk_g2s(xrs, a.xhat_rm + cur_row * RP, RP * 8, bar_x);
+        tma::bulk_g2s(xrs, a.xhat_rm + (int64_t)cur_row * RP, RP * 8, bar_x);
         tma::mbar_expect_tx(bar_a1 + 0, RP * 8);
         tma::bulk_g2s(a1s, fa1 + (int64_t)a.run_i1[r] * RP, RP * 8, bar_a1 + 0);
         if (rs1 < rel_end) {
@@ -234,13 +235,22 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
         for (int b = 0; b < B; ++b) {
             int ent = p + g * B + b;
             if constexpr (!FULL) ent = min(ent, rend - 1);
-            lds_row<G, VPL>(z[b], fs[1] + ring_at(ent, 1) * RP, gl, odd);
+            const double* rows[DO];
 #pragma unroll
-            for (int m = 2; m < DO; ++m) {
-                double f[VPL];
-                lds_row<G, VPL>(f, fs[m] + ring_at(ent, m) * RP, gl, odd);
+            for (int m = 1; m < DO; ++m) rows[m] = fs[m] + ring_at(ent, m) * RP;
+            // t = A_2(b,:) o A_3(c,:) o ...: one pair of columns at a time (few live registers)
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) z[b][k] *= f[k];
+            for (int t = 0; t < VPL / 2; ++t) {
+                const int c = col_of<G>(t, gl, odd);
+                double2 x = *reinterpret_cast<const double2*>(rows[1] + c);
+#pragma unroll
+                for (int m = 2; m < DO; ++m) {
+                    const double2 f = *reinterpret_cast<const double2*>(rows[m] + c);
+                    x.x *= f.x;
+                    x.y *= f.y;
+                }
+                z[b][2 * t] = x.x;
+                z[b][2 * t + 1] = x.y;
             }
             if constexpr (MULT) mu[b] = ring_at(ent, DO);
         }
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
         }
         // the run table one run further (consumed at the next run start)
         const int rs3 = rel_of(r + 3);
-        const int32_t i1_3 = r + 3 < a.nruns ? a.run_i1[r + 3] : 0;
+        const int32_t i1_3 = r + 3 < nruns ? a.run_i1[r + 3] : 0;
 
         int p = pos;
         {
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
             const int ncta = a.row_nw[cur_row];
             if (ncta <= 1) {
                 if (g == 0) {
-                    double* dst = a.yhat_rm + cur_row * RP;
+                    double* dst = a.yhat_rm + (int64_t)cur_row * RP;
 #pragma unroll
                     for (int t = 0; t < VPL / 2; ++t) {
                         double2* d2 = reinterpret_cast<double2*>(dst + col_of<G>(t, gl, 0));
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
                         double s = a.warp_rows[2 * u0] == cur_row ? __ldcg(a.slot_a + (int64_t)u0 * RP + c)
                                                                    : __ldcg(a.slot_b + (int64_t)u0 * RP + c);
                         for (int uu = u0 + 1; uu < u0 + ncta; ++uu) s += __ldcg(a.slot_a + (int64_t)uu * RP + c);
-                        double* dst = a.yhat_rm + cur_row * RP + c;
+                        double* dst = a.yhat_rm + (int64_t)cur_row * RP + c;
                         *dst = a.accumulate ? *dst + s : s;
                     }
                 }
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
                 if (lane == 0) {
                     tma::fence_proxy_async();
                     tma::mbar_expect_tx(bar_x, RP * 8);
-                    tma::bulk_g2s(xrs, a.xhat_rm + cur_row * RP, RP * 8, bar_x);
+                    tma::bulk_g2s(xrs, a.xhat_rm + (int64_t)cur_row * RP, RP * 8, bar_x);
                 }
                 tma::mbar_wait(bar_x, (unsigned)(xcnt & 1));
                 ++xcnt;

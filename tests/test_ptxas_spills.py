@@ -1,4 +1,5 @@
-"""Register-spill guard for the headline kernels (CPU: nvcc cross-compiles for sm_100a here).
+"""Register-spill guard for the kernels the BASELINE configs launch (CPU: nvcc cross-compiles for
+sm_100a here).
 
 The config-1 operator kernel runs two 512-thread CTAs per SM, so it has 64 registers per thread;
 a change that makes it spill costs the headline several percent (measured: an extra entry path
@@ -37,13 +38,21 @@ def _ptxas_report(src):
     return report
 
 
-@pytest.mark.parametrize("src,pattern", [
-    ("k_fused.cu", r"fused_matvec_kernelILi16ELi2ELb1E"),   # config 1: rp 16, 2 other modes, staged factors
-    ("k_pcgstep.cu", r"pcg_step_fused_kernelILi8E"),        # config 4 PCG vector step (r 64)
+# (src, instantiation, allowed spill-load bytes).  Config 3's q-pass layout (G = 4, B = 2) sits at
+# the 128-register limit and spills a few words outside the step loop: measured 4.2 ms per
+# application against 5.3 ms for the spill-free G = 8 layout (profiles/prof_stream.py), so a small,
+# fixed allowance guards it instead of zero.
+@pytest.mark.parametrize("src,pattern,allow", [
+    ("k_fused.cu", r"fused_matvec_kernelILi16ELi2ELb1E", 0),   # config 1: rp 16, 2 other modes, staged factors
+    ("k_pcgstep.cu", r"pcg_step_fused_kernelILi8E", 0),        # config 4 PCG vector step (r 64)
+    ("k_runs.cu", r"runs_kernelILi64ELi2ELb1ELi8ELi2ELb0E", 0),  # config 4 q-pass (the bench headline)
+    ("k_runs.cu", r"runs_kernelILi32ELi3ELb0ELi4ELi2ELb0E", 32),  # config 3 q-pass
+    ("k_gram.cu", r"gram_build_dmma2?_kernelILi(32ELi3|64ELi2)E", 0),  # configs 3 / 4 row-Gram builds
+    ("k_stream.cu", r"stream_kernelILi(32ELi3|64ELi2)ELb[01]ELi2E", 0),  # configs 3 / 4 right-hand side B
 ])
-def test_no_spills(src, pattern):
+def test_no_spills(src, pattern, allow):
     rep = _ptxas_report(src)
     hits = {k: v for k, v in rep.items() if re.search(pattern, k)}
     assert hits, f"no instantiation matching {pattern} in {src}"
     for k, (st, ld) in hits.items():
-        assert st == 0 and ld == 0, f"{k}: {st} B spill stores, {ld} B spill loads"
+        assert st <= allow and ld <= allow, f"{k}: {st} B spill stores, {ld} B spill loads (allowed {allow})"
