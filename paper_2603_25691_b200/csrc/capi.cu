@@ -387,6 +387,7 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
 // Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
 // fused kernel restricted to PH_B.
 bool build_run_parts(cphifi_unaligned p, int64_t sf_all);
+void ensure_runs(cphifi_unaligned p);
 
 // The run kernel's parts and split-row slots, on the first use (never inside a graph capture: every
 // capture site applies the operator once before capturing, and the solve calls this in its setup).
@@ -590,6 +591,84 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     return true;
 }
 
+// The warp-specialised row-Gram build (k_gramws.cu) over the run kernel's parts (their factor
+// blocks fit shared memory): one launch per part adding into G (zeroed by the caller), each over a
+// row-aligned CTA partition of the part.  False when it does not apply (no parts, rank or order
+// out of range, staging too large): the caller falls back to the single-pass builds of k_gram.cu.
+// Opt-in (CPHIFI_GRAM_WS=1): measured slower than the single-pass builds of k_gram.cu — config 4
+// 71.6 vs 61.8 ms, config 3 26.9 vs 24.6 ms (tensor pipe 32 %: the producers' global index / factor
+// loads and the per-batch handshakes of 32-entry batches) — and its parts cost ~0.1 s to build.
+bool gram_build_parts(cphifi_unaligned p) {
+    bool on = false;
+    if (const char* e = std::getenv("CPHIFI_GRAM_WS")) on = std::atoi(e) != 0;
+    cphifi_obs o = p->obs;
+    if (!on || !gram_ws_supported(p->rp, o->d - 1)) return false;
+    ensure_runs(p);
+    if (p->parts.empty()) return false;
+    for (const auto& sp : p->parts)
+        if (gram_ws_smem_bytes(p->rp, sp.sf) > runs_smem_cap()) return false;
+    cphifi_ctx ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
+    const int dl = o->d - 2;
+    const size_t rp2 = (size_t)p->rp * p->rp;
+    DevBuf<unsigned> rowcnt(p->n);
+    CPHIFI_CUDA(cudaMemsetAsync(rowcnt.get(), 0, sizeof(unsigned) * p->n, s));
+    DevBuf<double> slot_a((size_t)ctx->num_sms * rp2), slot_b((size_t)ctx->num_sms * rp2);
+    const bool timing = std::getenv("CPHIFI_GRAM_TIMING") != nullptr;  // developer: device time of the build
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+        CPHIFI_CUDA(cudaEventCreate(&e0));
+        CPHIFI_CUDA(cudaEventCreate(&e1));
+        CPHIFI_CUDA(cudaEventRecord(e0, s));
+    }
+    for (const StreamPart& sp : p->parts) {
+        if (sp.q == 0) continue;
+        std::vector<int64_t> rp_host(p->n + 1);
+        d2h_sync(rp_host.data(), sp.row_ptr, sizeof(int64_t) * (p->n + 1), s);
+        PartitionPlan plan;
+        plan_partition(rp_host, ctx->num_sms, ctx->num_sms, plan);
+        DevBuf<int64_t> cta_beg(plan.beg.size()), cta_rows(plan.rows.size());
+        DevBuf<int32_t> rfc(p->n), rnc(p->n);
+        h2d(cta_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
+        h2d(cta_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
+        h2d(rfc.get(), plan.row_first_cta.data(), sizeof(int32_t) * p->n, s);
+        h2d(rnc.get(), plan.row_ncta.data(), sizeof(int32_t) * p->n, s);
+        GramArgs g;
+        g.n = p->n;
+        g.rp = p->rp;
+        g.q = sp.ldq;
+        g.dother = o->d - 1;
+        g.row_ptr = sp.row_ptr;
+        g.idx = sp.idx;
+        g.fac = p->fac.get();
+        for (int m = 0; m < o->d - 1; ++m) g.fac_off[m] = p->fac_off[m];
+        g.fac_off[dl] = p->fac_off[dl] + sp.row_lo * p->rp;
+        g.fac_total = g.fac_off[dl] + sp.rows * p->rp;
+        g.mult = sp.mult;
+        g.cta_beg = cta_beg.get();
+        g.cta_rows = cta_rows.get();
+        g.row_first_cta = rfc.get();
+        g.row_ncta = rnc.get();
+        g.rowcnt = rowcnt.get();
+        g.slot_a = slot_a.get();
+        g.slot_b = slot_b.get();
+        g.g = p->gram.get();
+        g.accumulate = 1;  // G was zeroed: every part adds
+        gram_build_ws(g, plan.ctas, sp.sf, s);
+        CPHIFI_CUDA(cudaStreamSynchronize(s));  // the partition buffers are released per part
+    }
+    if (timing) {
+        CPHIFI_CUDA(cudaEventRecord(e1, s));
+        CPHIFI_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CPHIFI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        std::fprintf(stderr, "cphifi: gram build (warp-specialised, %zu parts) %.3f ms on device\n", p->parts.size(), ms);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    return true;
+}
+
 // Row-Gram operator: build G_i = sum_l z_l z_l' once (k_gram.cu), on first use.
 void ensure_gram(cphifi_unaligned p) {
     if (p->gram.n) return;
@@ -600,6 +679,7 @@ void ensure_gram(cphifi_unaligned p) {
     const size_t rp2 = (size_t)p->rp * p->rp;
     p->gram.alloc((size_t)p->n * rp2);
     CPHIFI_CUDA(cudaMemsetAsync(p->gram.get(), 0, sizeof(double) * p->n * rp2, s));
+    if (gram_build_parts(p)) return;
     // The build's own row-aligned partition, sized from the chosen kernel's occupancy (each CTA
     // alternates a gather phase and a DMMA phase around barriers, so several per SM overlap them).  Measured (profiles/prof_gram_grid.sh): config 3 (v1) 27.4 ms at 4 CTAs/SM
     // -> 24.7 at 8; config 4 (v2, 2 resident) 68.3 at 4 -> 61.8 at 2 (no partial second wave).

@@ -241,8 +241,14 @@ struct GramArgs {
     double* slot_a = nullptr;  // grid x rp x rp
     double* slot_b = nullptr;
     double* g = nullptr;       // n x rp x rp
+    int accumulate = 0;        // k_gramws.cu: add into g (factor-block parts) instead of overwriting
 };
 void gram_build(const GramArgs& a, int grid, cudaStream_t s);
+// warp-specialised build (k_gramws.cu): producer warps build z batches from factors staged in shared
+// memory (sf doubles: modes 1.. of the plan / of a factor-block part), consumer warps run the DMMA
+bool gram_ws_supported(int64_t rp, int dother);
+size_t gram_ws_smem_bytes(int64_t rp, int64_t sf);
+void gram_build_ws(const GramArgs& a, int grid, int64_t sf, cudaStream_t s);
 int gram_build_occupancy(const GramArgs& a);  // partition CTAs per SM for the build gram_build picks
 void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
                 cudaStream_t s);

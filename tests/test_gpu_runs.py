@@ -57,3 +57,32 @@ def test_runs_kernel_vs_oracle_and_stream(monkeypatch, shape, r, q, coalesce, zi
     assert np.linalg.norm(ya - yb) / np.linalg.norm(yb) < 1e-12
     # the RHS B (built by the streaming kernel with the values) and V are unaffected
     assert np.linalg.norm(p.b - p2.b) / np.linalg.norm(p2.b) < 1e-13
+
+
+@pytest.mark.parametrize("shape,r,q,coalesce,zipf", [
+    ((700, 40, 30), 16, 30000, False, False),
+    ((1100, 24, 20, 12), 32, 60000, False, True),
+    ((600, 64, 512), 64, 120000, True, True),      # two factor-block parts: G accumulated over launches
+    ((600, 60, 900), 32, 90000, True, False),
+])
+def test_gram_ws_build_vs_oracle(monkeypatch, shape, r, q, coalesce, zipf):
+    """The warp-specialised row-Gram build (k_gramws.cu, over the run parts) gives the operator the
+    oracle's streaming restatement gives, and the same G as the single-pass build (CPHIFI_GRAM_WS=0)."""
+    monkeypatch.setenv("CPHIFI_GRAM_WS", "1")  # opt-in build (k_gramws.cu)
+    cp, mode, obs, model, idx, vals, factors = _case(shape, r, q, 11, coalesce, zipf)
+    n = shape[0]
+    x = np.random.default_rng(4).normal(size=n * r)
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+    assert p.set_operator("gram") == "gram"
+    y_ws = cp.unaligned_matvec(p, x)
+    p.set_operator("stream")
+    y_st = cp.unaligned_matvec(p, x)
+    assert np.linalg.norm(y_ws - y_st) / np.linalg.norm(y_st) < 1e-12
+    monkeypatch.setenv("CPHIFI_GRAM_WS", "0")
+    obs2 = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    p2 = cp.make_unaligned_subproblem(obs2, model, 0, mode, 1e-6)
+    p2.set_operator("gram")
+    y_v = cp.unaligned_matvec(p2, x)
+    assert np.linalg.norm(y_ws - y_v) / np.linalg.norm(y_v) < 1e-12
+    y_o = orc.unaligned_matvec_stream(shape, 0, idx, [None] + factors[1:], mode.kernel(), 1e-4, 1e-6, x)
+    assert np.linalg.norm(y_ws - y_o) / np.linalg.norm(y_o) < 1e-12
