@@ -249,6 +249,18 @@ int cphifi_solve_aligned_pcg(cphifi_mode mode, int64_t r, const double* b, const
  * (reference default 6000), std::runtime_error when not positive definite. */
 int cphifi_solve_aligned_direct(cphifi_mode mode, int64_t r, const double* b, const double* v,
                                 int64_t direct_cap, double* w_out);
+/* ---- unaligned direct / dense baselines (unaligned.hpp:52-96, 164-174) ----
+ * solve_unaligned_direct_nonsym: LU solve (cuSOLVER getrf/getrs, lu_solve's residual check and
+ * message, solvers.hpp:99-106) of (G'F + lambda I) vec(W) = vec(B), the system assembled on device
+ * from the row Grams ((G'F)[(j,i),(j',i')] = G_i(j,j') K(i,i')) instead of the q x rn factors;
+ * std::invalid_argument when rn > dense_cap (reference default 6000).  report: iterations 1, the
+ * relative residual, wall time.  assemble_unaligned_sym_dense: the symmetric test oracle
+ * F'F + lambda (I kron K) + rho I (rn x rn, column-major) and vec(K B), F'F = K S with the Gram-scaled
+ * columns S on the DMMA GEMM. */
+int cphifi_solve_unaligned_direct_nonsym(cphifi_unaligned p, int64_t dense_cap, cphifi_solve_report* report,
+                                         double* w_out);
+int cphifi_unaligned_assemble_sym_dense(cphifi_unaligned p, int64_t dense_cap, double* sys_out, double* rhs_out);
+
 /* Fused aligned update for mode k: MTTKRP + Gram + decoupled solve, one device pass,
  * eig(V) on device.  b_out / v_out may be NULL. */
 int cphifi_aligned_solve(cphifi_tensor t, cphifi_mode mode, int k, int64_t r,

@@ -315,6 +315,67 @@ def unaligned_matvec_stream(shape, k, idx, factors, kernel, lam, rho, x, threads
     return y
 
 
+def build_F(p: UnalignedSubproblem, dense_cap=6000) -> np.ndarray:
+    """unaligned.hpp:52-62: F = S'(Z kron K), row l = zhat(l,:) kron khat(l,:) (khat: observations.hpp:161-169)."""
+    if p.n * p.r > dense_cap:
+        raise InvalidArgument("build_F: rn exceeds memory cap")
+    khat = p.kernel[p.idx[p.k], :]
+    f = np.zeros((p.q, p.r * p.n))
+    for j in range(p.r):
+        f[:, j * p.n:(j + 1) * p.n] = p.zhat[:, j:j + 1] * khat
+    return f
+
+
+def build_G(p: UnalignedSubproblem, dense_cap=6000) -> np.ndarray:
+    """unaligned.hpp:65-75: G = S'(Z kron I), row l = zhat(l,:) kron e_{i_k(l)}'."""
+    if p.n * p.r > dense_cap:
+        raise InvalidArgument("build_G: rn exceeds memory cap")
+    g = np.zeros((p.q, p.r * p.n))
+    rows = np.arange(p.q)
+    for j in range(p.r):
+        g[rows, j * p.n + p.idx[p.k]] = p.zhat[:, j]
+    return g
+
+
+def lu_solve(a, b) -> np.ndarray:
+    """solvers.hpp:99-106: partial-pivot LU (LAPACK getrf / getrs via numpy), then the residual check."""
+    try:
+        x = np.linalg.solve(a, b)
+    except np.linalg.LinAlgError:
+        raise RuntimeFailure("lu_solve: matrix is singular or severely ill-conditioned")
+    res = float(np.linalg.norm(a @ x - b))
+    if not np.isfinite(res) or res > 1e-6 * max(float(np.linalg.norm(b)), 1.0):
+        raise RuntimeFailure("lu_solve: matrix is singular or severely ill-conditioned")
+    return x
+
+
+def solve_unaligned_direct_nonsym(p: UnalignedSubproblem, report: SolveReport | None = None, dense_cap=6000):
+    """unaligned.hpp:77-96: LU solve of (G'F + lambda I) vec(W) = vec(B)."""
+    import time
+    t0 = time.perf_counter()
+    sys_ = build_G(p, dense_cap).T @ build_F(p, dense_cap)
+    sys_[np.diag_indices_from(sys_)] += p.lam
+    rhs = p.b.reshape(-1, order="F")
+    w = lu_solve(sys_, rhs)
+    if report is not None:
+        bn = float(np.linalg.norm(rhs))
+        report.iterations = 1
+        report.relative_residual = 0.0 if bn == 0.0 else float(np.linalg.norm(sys_ @ w - rhs)) / bn
+        report.converged = True
+        report.wall_time_s = time.perf_counter() - t0
+    return w.reshape((p.n, p.r), order="F")
+
+
+def assemble_unaligned_sym_dense(p: UnalignedSubproblem, dense_cap=6000):
+    """unaligned.hpp:164-174: (F'F + lambda (I kron K) + rho I, vec(K B))."""
+    if p.n * p.r > dense_cap:
+        raise InvalidArgument("assemble_unaligned_sym_dense: rn exceeds memory cap")
+    f = build_F(p, dense_cap)
+    sys_ = f.T @ f + p.lam * np.kron(np.eye(p.r), p.kernel)
+    sys_[np.diag_indices_from(sys_)] += p.rho
+    return sys_, (p.kernel @ p.b).reshape(-1, order="F")
+
+
 @dataclass
 class Preconditioner:
     """build_preconditioner (unaligned.hpp:120-140) given eig(K) and eig(V)."""

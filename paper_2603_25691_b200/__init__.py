@@ -36,7 +36,8 @@ __all__ = [
     "read_observations", "write_observations", "update_finite_mode_unaligned", "unaligned_relative_error",
     "UnalignedAlsState", "FitIteration", "AlignedAlsState", "update_finite_mode_aligned",
     "SolveReport", "mttkrp", "gram_khatri_rao", "AlignedSubproblem", "solve_aligned_decoupled",
-    "aligned_matvec", "solve_aligned_pcg", "solve_aligned_direct",
+    "aligned_matvec", "solve_aligned_pcg", "solve_aligned_direct", "solve_unaligned_direct_nonsym",
+    "assemble_unaligned_sym_dense",
     "aligned_solve", "Mt19937_64", "synth_observations_device", "CphifiInvalidArgument", "CphifiRuntimeError", "CphifiDeviceError",
 ]
 
@@ -594,6 +595,35 @@ def solve_unaligned_pcg(p: UnalignedSubproblem, cfg: PcgConfig | None = None, re
         report.setup_s = rep.setup_s
         report.matvecs = rep.matvecs
     return w
+
+
+def solve_unaligned_direct_nonsym(p: UnalignedSubproblem, report: SolveReport | None = None,
+                                  dense_cap: int = 6000) -> np.ndarray:
+    """unaligned.hpp:77-96: LU solve of (G'F + lambda I) vec(W) = vec(B) — the nonsymmetric direct
+    baseline, its system assembled on device from the row Grams."""
+    n, r = p.n(), p.r()
+    w = np.zeros((n, r), order="F")
+    rep = _capi.SolveReportC()
+    call("cphifi_solve_unaligned_direct_nonsym", p.handle, int(dense_cap), ctypes.byref(rep), _dp(w))
+    if report is not None:
+        report.iterations = rep.iterations
+        report.relative_residual = rep.relative_residual
+        report.wall_time_s = rep.wall_time_s
+        report.converged = bool(rep.converged)
+        report.residual_history = []
+    return w
+
+
+def assemble_unaligned_sym_dense(p: UnalignedSubproblem, dense_cap: int = 6000):
+    """unaligned.hpp:164-174 (test oracle): (F'F + lambda (I kron K) + rho I, vec(K B)), assembled on
+    device."""
+    rn = p.n() * p.r()
+    if rn > dense_cap:  # checked before allocating the rn x rn host buffer
+        raise CphifiInvalidArgument("assemble_unaligned_sym_dense: rn exceeds memory cap")
+    sys_ = np.zeros((rn, rn), order="F")
+    rhs = np.zeros(rn)
+    call("cphifi_unaligned_assemble_sym_dense", p.handle, int(dense_cap), _dp(sys_), _dp(rhs))
+    return sys_, rhs
 
 
 # ---- aligned path ----------------------------------------------------------------------

@@ -141,6 +141,8 @@ _SIGS = [
     ("cphifi_solve_aligned_pcg", ctypes.c_int,
      [_H, ctypes.c_int64, c_double_p, c_double_p, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC),
       c_double_p, c_double_p]),
+    ("cphifi_solve_unaligned_direct_nonsym", ctypes.c_int, [_H, ctypes.c_int64, ctypes.c_void_p, c_double_p]),
+    ("cphifi_unaligned_assemble_sym_dense", ctypes.c_int, [_H, ctypes.c_int64, c_double_p, c_double_p]),
     ("cphifi_solve_aligned_direct", ctypes.c_int,
      [_H, ctypes.c_int64, c_double_p, c_double_p, ctypes.c_int64, c_double_p]),
     ("cphifi_aligned_solve", ctypes.c_int,

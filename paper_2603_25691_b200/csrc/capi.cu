@@ -2949,6 +2949,113 @@ int cphifi_solve_aligned_direct(cphifi_mode mode, int64_t r, const double* b, co
     });
 }
 
+// ---- unaligned direct / dense baselines (unaligned.hpp:52-96, 164-174) -------
+namespace {
+// The all-shard row Grams of the plan (G_i over every observation of row i): this rank's G, summed
+// over the ranks on a multi-rank plan.
+const double* full_row_grams(cphifi_unaligned p, DevBuf<double>& tmp) {
+    if (p->rp > 64) throw_invalid("gram operator: padded rank above 64 is not supported");
+    ensure_gram(p);
+    if (!is_multi(p)) return p->gram.get();
+    const size_t cnt = (size_t)p->n * p->rp * p->rp;
+    tmp.alloc(cnt);
+    allreduce_sum(p->obs->ctx, p->gram.get(), tmp.get(), cnt);
+    return tmp.get();
+}
+}  // namespace
+
+int cphifi_solve_unaligned_direct_nonsym(cphifi_unaligned p, int64_t dense_cap, cphifi_solve_report* report,
+                                         double* w_out) {
+    return guard([&] {
+        need(p, "p");
+        need(w_out, "w_out");
+        need_mode(p);
+        const auto t0 = std::chrono::steady_clock::now();
+        const int64_t n = p->n, r = p->r, rn = n * r;
+        // build_G(p).transpose() * build_F(p): both materialisations carry the same cap (unaligned.hpp:54, 67)
+        if (rn > dense_cap) throw_invalid("build_F: rn exceeds memory cap");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> gtmp;
+        const double* g = full_row_grams(p, gtmp);
+        DevBuf<double> sys((size_t)rn * rn), a0((size_t)rn * rn), x(rn), res(rn), scal(2);
+        nonsym_system(g, p->mode->kernel.get(), n, r, p->rp, p->mode->lambda, sys.get(), s);
+        CPHIFI_CUDA(cudaMemcpyAsync(a0.get(), sys.get(), sizeof(double) * rn * rn, cudaMemcpyDeviceToDevice, s));
+        CPHIFI_CUDA(cudaMemcpyAsync(x.get(), p->b.get(), sizeof(double) * rn, cudaMemcpyDeviceToDevice, s));
+        // lu_solve (solvers.hpp:99-106): partial-pivot LU, then the residual check
+        int lwork = 0;
+        CPHIFI_SOLVER(cusolverDnDgetrf_bufferSize(ctx->solver, (int)rn, (int)rn, sys.get(), (int)rn, &lwork));
+        DevBuf<double> work(std::max(lwork, 1));
+        DevBuf<int> piv(std::max<int64_t>(rn, 1)), info(1);
+        CPHIFI_SOLVER(cusolverDnDgetrf(ctx->solver, (int)rn, (int)rn, sys.get(), (int)rn, work.get(), piv.get(), info.get()));
+        int hinfo = 0;
+        d2h_sync(&hinfo, info.get(), sizeof(int), s);
+        bool singular = hinfo > 0;
+        if (!singular)
+            CPHIFI_SOLVER(cusolverDnDgetrs(ctx->solver, CUBLAS_OP_N, (int)rn, 1, sys.get(), (int)rn, piv.get(), x.get(),
+                                           (int)rn, info.get()));
+        // res = A x - b with the DMMA GEMM, norms on device
+        GemmArgs gm;
+        gm.m = rn; gm.n = 1; gm.k = rn;
+        gm.a = a0.get(); gm.a_rs = 1; gm.a_cs = rn;
+        gm.b = x.get(); gm.b_rs = 1; gm.b_cs = rn;
+        gm.c = res.get(); gm.c_rs = 1; gm.c_cs = rn;
+        gm.epi = EPI_AXPY2; gm.e1 = p->b.get(); gm.e2 = p->b.get(); gm.ld_e = rn; gm.beta1 = -1.0; gm.beta2 = 0.0;
+        gemm(gm, ctx->num_sms, s);
+        std::vector<double> hres(rn), hb(rn), hx(rn);
+        d2h_sync(hres.data(), res.get(), sizeof(double) * rn, s);
+        d2h_sync(hb.data(), p->b.get(), sizeof(double) * rn, s);
+        d2h_sync(hx.data(), x.get(), sizeof(double) * rn, s);
+        double rr = 0.0, bb = 0.0;
+        for (int64_t i = 0; i < rn; ++i) {
+            rr += hres[i] * hres[i];
+            bb += hb[i] * hb[i];
+        }
+        const double resn = std::sqrt(rr), bn = std::sqrt(bb);
+        if (singular || !std::isfinite(resn) || resn > 1e-6 * std::max(bn, 1.0))
+            throw_runtime("lu_solve: matrix is singular or severely ill-conditioned");
+        std::memcpy(w_out, hx.data(), sizeof(double) * rn);
+        if (report) {
+            cphifi_solve_report rep = *report;
+            rep.iterations = 1;
+            rep.relative_residual = bn == 0.0 ? 0.0 : resn / bn;
+            rep.converged = 1;
+            rep.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            rep.history_len = 0;
+            *report = rep;
+        }
+    });
+}
+
+int cphifi_unaligned_assemble_sym_dense(cphifi_unaligned p, int64_t dense_cap, double* sys_out, double* rhs_out) {
+    return guard([&] {
+        need(p, "p");
+        need(sys_out, "sys_out");
+        need(rhs_out, "rhs_out");
+        need_mode(p);
+        const int64_t n = p->n, r = p->r, rn = n * r;
+        if (rn > dense_cap) throw_invalid("assemble_unaligned_sym_dense: rn exceeds memory cap");
+        cphifi_ctx ctx = p->obs->ctx;
+        DeviceGuard dg(ctx->device);
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> gtmp;
+        const double* g = full_row_grams(p, gtmp);
+        DevBuf<double> sm((size_t)rn * rn), cm((size_t)rn * rn), sys((size_t)rn * rn), rhs(rn);
+        gram_scaled(g, p->mode->kernel.get(), n, r, p->rp, sm.get(), s);
+        GemmArgs gm;  // C = K S  (n x r^2 n)
+        gm.m = n; gm.n = r * r * n; gm.k = n;
+        gm.a = p->mode->kernel.get(); gm.a_rs = 1; gm.a_cs = n;
+        gm.b = sm.get(); gm.b_rs = 1; gm.b_cs = n;
+        gm.c = cm.get(); gm.c_rs = 1; gm.c_cs = n;
+        gemm(gm, ctx->num_sms, s);
+        sym_place(cm.get(), p->mode->kernel.get(), n, r, p->mode->lambda, p->rho, sys.get(), s);
+        gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, rhs.get(), n);  // vec(K B)
+        d2h_sync(sys_out, sys.get(), sizeof(double) * rn * rn, s);
+        d2h_sync(rhs_out, rhs.get(), sizeof(double) * rn, s);
+    });
+}
+
 int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t r, const double* const* factors,
                                int iters, double* w_out, double* ms_out) {
     return guard([&] {

@@ -331,6 +331,14 @@ void aligned_matvec_dev(const double* x, const double* dk, const double* v, int6
 void aligned_dinv(const double* dk, const double* v, int64_t n, int64_t r, double lambda, double* dinv,
                   cudaStream_t s);
 void hadamard(const double* a, const double* b, int64_t cnt, double* out, cudaStream_t s);
+// unaligned direct / dense baselines from the row Grams (k_aligned.cu): the nonsymmetric system
+// G'F + lambda I; S = G_i''(j,j') K(i'',i') scaled columns (F'F = K S, placed by sym_place with
+// lambda (I kron K) + rho I)
+void nonsym_system(const double* g, const double* kmat, int64_t n, int64_t r, int64_t rp, double lambda, double* sys,
+                   cudaStream_t s);
+void gram_scaled(const double* g, const double* kmat, int64_t n, int64_t r, int64_t rp, double* sm, cudaStream_t s);
+void sym_place(const double* cm, const double* kmat, int64_t n, int64_t r, double lambda, double rho, double* sys,
+               cudaStream_t s);
 void kron_system(const double* v, const double* kmat, int64_t n, int64_t r, double lambda, double* sys,
                  cudaStream_t s);
 
