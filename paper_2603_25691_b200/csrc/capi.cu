@@ -855,8 +855,8 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
     const int64_t n = p->n, r = p->r;
     const double* uk = p->mode->u.get();
     if (sandwich_supported(n, r)) {
-        const int64_t rp8 = sandwich_rp(r);
-        if (p->t1.n < (size_t)(n * rp8)) p->t1.alloc(n * rp8);
+        const int64_t need_d = sandwich_scratch_doubles(n, r);
+        if (p->t1.n < (size_t)need_d) p->t1.alloc(need_d);
         SandArgs a;
         a.n = n; a.r = r;
         a.u = uk; a.ut = mode_ut(p->mode);
@@ -1035,8 +1035,8 @@ int* decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     int* flag = thread_flag();
     *flag = 0;
     if (sandwich_supported(n, r)) {
-        const int64_t rp8 = sandwich_rp(r);
-        if (core.n < (size_t)(n * rp8)) core.alloc(n * rp8);
+        const int64_t need_d = sandwich_scratch_doubles(n, r);
+        if (core.n < (size_t)need_d) core.alloc(need_d);
         SandArgs a;
         a.n = n; a.r = r;
         a.u = mode->u.get(); a.ut = mode_ut(mode);

@@ -255,6 +255,159 @@ __global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a, cons
     }
 }
 
+// ---- v3: the n x n x r products on the FP64 tensor cores (DMMA m8n8k4) ------------------------
+// Phase PH computes, for the CTA's RB = 8 rows i, C(i, :) = sum_k F(i, k) M(k, :) with
+//   phase 1: F = U' (so C = U' X), M = X row-major padded (a transposed copy, `xrm`);
+//   phase 2: F = U,                M = the phase-1 core, written row-major padded by phase 1,
+// then the same r x r epilogue as v2.  A stage brings KC k-values of the F rows (tensor-map box
+// RB x KC over F(i, k) = f[i + n k]: shared memory [KC][RB], so an A fragment — 8 rows i x 4 k —
+// is 32 consecutive doubles) and of M (box RPP x KC over the row-major M: [KC][RPP], the pitch
+// RPP = RP + 8 spreads a B fragment's 4 k-rows over all 32 banks).  The 8 warps split every
+// stage's k-steps (warp w: k-steps w, w + 8, ...), each holding RP / 8 accumulator tiles; the
+// warp partials are summed in warp order at the end: deterministic.
+constexpr int SW3_T = 256, SW3_W = 8, SW3_RB = 8, SW3_ST = 4;
+template <int RP>
+struct Sw3 {
+    static constexpr int RPP = RP + 8;                  // B-tile pitch
+    static constexpr int KC = RP >= 64 ? 64 : 128;     // k per stage
+    static constexpr int NTL = RP / 8;                  // 8 x 8 output tiles per CTA
+};
+template <int RP>
+struct Sw3Smem {
+    static constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP;
+    double a[SW3_ST][KC][SW3_RB];
+    double b[SW3_ST][KC][RPP];
+    double red[SW3_W][SW3_RB][RP];
+    double tt[SW3_RB][RP + 1];
+    uint64_t full[SW3_ST];
+};
+__device__ __forceinline__ void dmma_sw(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+template <int RP, int PH>
+__global__ void __launch_bounds__(SW3_T) sandwich3_kernel(const SandArgs a, const __grid_constant__ CUtensorMap tm_f,
+                                                          const __grid_constant__ CUtensorMap tm_m, double* core_rm) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    using SM = Sw3Smem<RP>;
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP, NTL = Sw3<RP>::NTL, RB = SW3_RB;
+    const int64_t n = a.n;
+    const int r = (int)a.r;
+    const int64_t i0 = (int64_t)blockIdx.x * RB;
+    const int rb = (int)min((int64_t)RB, n - i0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nch = (int)((n + KC - 1) / KC);
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < SW3_ST; ++st) tma::mbar_init(&sm.full[st], 1);
+        tma::fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int c) {  // thread 0: two 2-D tensor copies per stage (out-of-range reads as 0)
+        const int st = c % SW3_ST;
+        tma::mbar_expect_tx(&sm.full[st], (unsigned)(sizeof(double) * KC * (RB + RPP)));
+        tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_f, (int)i0, c * KC, &sm.full[st]);
+        tma::tensor_g2s_2d(&sm.b[st][0][0], &tm_m, 0, c * KC, &sm.full[st]);
+    };
+    if (threadIdx.x == 0)
+        for (int c = 0; c < min(nch, SW3_ST); ++c) issue(c);
+    double acc[NTL][2];
+#pragma unroll
+    for (int t = 0; t < NTL; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int fi = lane >> 2, fk = lane & 3;
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % SW3_ST;
+        tma::mbar_wait(&sm.full[st], (unsigned)((c / SW3_ST) & 1));
+        // (k beyond n reads as zero in both operands: the padded k-steps add nothing)
+#pragma unroll
+        for (int ks = warp; ks < KC / 4; ks += SW3_W) {
+            const int k = 4 * ks + fk;
+            const double av = sm.a[st][k][fi];
+#pragma unroll
+            for (int t = 0; t < NTL; ++t) dmma_sw(acc[t], av, sm.b[st][k][8 * t + fi]);
+        }
+        __syncthreads();  // every warp is done with slot st
+        if (threadIdx.x == 0 && c + SW3_ST < nch) {
+            tma::fence_proxy_async();
+            issue(c + SW3_ST);
+        }
+    }
+    // warp partials (C fragment: row fi, columns 8 t + 2 fk + {0, 1}) summed in warp order
+#pragma unroll
+    for (int t = 0; t < NTL; ++t) {
+        sm.red[warp][fi][8 * t + 2 * fk] = acc[t][0];
+        sm.red[warp][fi][8 * t + 2 * fk + 1] = acc[t][1];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RP; e += SW3_T) {
+        const int q = e / RP, jj = e % RP;
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < SW3_W; ++w) t += sm.red[w][q][jj];
+        sm.tt[q][jj] = t;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RPP; e += SW3_T) {
+        const int q = e / RPP, jj = e % RPP;
+        if (q >= rb) continue;
+        const int64_t i = i0 + q;
+        if (jj >= r) {  // zero pad of the row-major core (phase 2's B operand)
+            if constexpr (PH == 1) core_rm[i * RPP + jj] = 0.0;
+            continue;
+        }
+        double c = 0.0;
+        for (int m = 0; m < r; ++m) c = fma(sm.tt[q][m], PH == 1 ? a.uv[m + (int64_t)r * jj] : a.uv[jj + (int64_t)r * m], c);
+        if constexpr (PH == 1) {
+            double out;
+            if (a.op == SW_MUL) {
+                out = c * a.dmat[i + n * jj];
+            } else {
+                const double den = a.e_col[jj] * a.e_row[i] + a.beta;
+                if (den == 0.0) *a.flag = 1;
+                out = c / den;
+            }
+            core_rm[i * RPP + jj] = out;
+        } else {
+            a.y[i + a.ldy * jj] = c;
+        }
+    }
+}
+
+// x (n x r, column stride ldx) -> xrm (n x RPP row-major, zero pad)
+__global__ void to_rows_padded_kernel(const double* __restrict__ x, int64_t ldx, int64_t n, int r, int rpp,
+                                      double* __restrict__ xrm) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rpp; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / rpp;
+        const int j = (int)(e % rpp);
+        xrm[e] = j < r ? x[k + ldx * j] : 0.0;
+    }
+}
+
+template <int RP>
+void launch3_rp(const SandArgs& a, cudaStream_t s) {
+    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP;
+    const uint64_t n = (uint64_t)a.n;
+    double* core_rm = a.core_out;               // n x RPP
+    double* xrm = a.core_out + (size_t)n * RPP;  // n x RPP
+    const size_t smem = sizeof(Sw3Smem<RP>);
+    to_rows_padded_kernel<<<(unsigned)std::min<int64_t>(((int64_t)n * RPP + 255) / 256, 4096), 256, 0, s>>>(
+        a.x, a.ldx, (int64_t)n, (int)a.r, RPP, xrm);
+    CPHIFI_CHECK_LAUNCH();
+    CUtensorMap tf1, tf2, tm1, tm2;
+    const bool ok = encode_tmap_2d_f64(&tf1, a.ut, n, n, n, SW3_RB, KC) && encode_tmap_2d_f64(&tf2, a.u, n, n, n, SW3_RB, KC) &&
+                    encode_tmap_2d_f64(&tm1, xrm, RPP, n, RPP, RPP, KC) &&
+                    encode_tmap_2d_f64(&tm2, core_rm, RPP, n, RPP, RPP, KC);
+    if (!ok) throw Error(CPHIFI_CUDA_ERROR, "sandwich: tensor map encoding failed");
+    const unsigned grid = (unsigned)((a.n + SW3_RB - 1) / SW3_RB);
+    func_attr_once((const void*)sandwich3_kernel<RP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    func_attr_once((const void*)sandwich3_kernel<RP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sandwich3_kernel<RP, 1><<<grid, SW3_T, smem, s>>>(a, tf1, tm1, core_rm);
+    CPHIFI_CHECK_LAUNCH();
+    sandwich3_kernel<RP, 2><<<grid, SW3_T, smem, s>>>(a, tf2, tm2, core_rm);
+    CPHIFI_CHECK_LAUNCH();
+}
+
 template <int RP, int RB, int PH>
 void launch2_t(const SandArgs& a, cudaStream_t s) {
     auto kern = sandwich2_kernel<RP, RB, PH>;
@@ -475,9 +628,28 @@ void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {
     CPHIFI_CHECK_LAUNCH();
 }
 
+int64_t sandwich_scratch_doubles(int64_t n, int64_t r) {
+    const int64_t rp = sandwich_rp(r);
+    return 2 * n * (rp + 8);  // v3: row-major core and X copy, pitch rp + 8 (>= v1 / v2's n x rp)
+}
+
 void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
     a.rp = sandwich_rp(a.r);
     a.core = a.core_out;
+    // v3 (DMMA) from n = 512 on: config 2 (n = 1024, r = 32) decoupled 35.7 -> 31.4 us; at n = 200
+    // (config 0) its 25 CTAs lose to v2 (18.7 vs 14.3 us)
+    bool v3 = a.n >= 512 && a.n % 2 == 0 && reinterpret_cast<uintptr_t>(a.u) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(a.ut) % 16 == 0 && reinterpret_cast<uintptr_t>(a.core_out) % 16 == 0;
+    if (const char* e = std::getenv("CPHIFI_SANDWICH_V3")) v3 = v3 && std::atoi(e) != 0;
+    if (v3) {
+        switch (a.rp) {
+            case 8: launch3_rp<8>(a, s); return;
+            case 16: launch3_rp<16>(a, s); return;
+            case 32: launch3_rp<32>(a, s); return;
+            case 64: launch3_rp<64>(a, s); return;
+            default: break;
+        }
+    }
     // rows per CTA: about two CTAs per SM, at most 8
     int rb = 1;
     while (rb < 8 && (a.n + rb - 1) / rb > 2 * num_sms) rb *= 2;

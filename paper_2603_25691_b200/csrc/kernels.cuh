@@ -99,13 +99,14 @@ struct SandArgs {
     const double* e_col = nullptr;
     double beta = 0.0;
     int* flag = nullptr;                // SW_DIV: set to 1 on a zero denominator
-    double* core_out = nullptr;         // n x rp row-major scratch (phase 1 output)
+    double* core_out = nullptr;         // sandwich_scratch_doubles(n, r) scratch (phase 1 output)
     const double* core = nullptr;       // the same buffer (phase 2 input)
     double* y = nullptr;                // n x r, column stride ldy
     int64_t ldy = 0;
 };
 bool sandwich_supported(int64_t n, int64_t r);
 int64_t sandwich_rp(int64_t r);
+int64_t sandwich_scratch_doubles(int64_t n, int64_t r);  // core_out size the sandwich needs
 void sandwich(SandArgs a, int num_sms, cudaStream_t s);
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
 // eigenbasis preconditioner z~ = ((r~ U_V) o D) U_V' in one launch (r <= 64)

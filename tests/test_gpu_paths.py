@@ -48,7 +48,7 @@ def test_mttkrp_variants_vs_oracle(cp, monkeypatch, shape, r):
     assert np.array_equal(b2, out[("0", "1")])
 
 
-@pytest.mark.parametrize("n,r", [(200, 10), (64, 32), (130, 64), (33, 5), (300, 1)])
+@pytest.mark.parametrize("n,r", [(200, 10), (64, 32), (130, 64), (33, 5), (300, 1), (1024, 32), (2048, 64)])
 def test_decoupled_sandwich_variants(cp, monkeypatch, n, r):
     g = cp.Mt19937_64(7 * n + r)
     pts = np.sort(g.uniform_real(0, 1, n))
@@ -60,11 +60,12 @@ def test_decoupled_sandwich_variants(cp, monkeypatch, n, r):
     v = ri.random_spd(g, r)
     ev = orc.sym_eig(v)
     wo = orc.solve_aligned_decoupled(b, ek, ev, 1e-3)
-    for sw, v1 in (("0", "0"), ("1", "1"), ("1", "0")):
+    for sw, v1, v3 in (("0", "0", "0"), ("1", "1", "0"), ("1", "0", "0"), ("1", "0", "1")):
         monkeypatch.setenv("CPHIFI_SANDWICH", sw)
         monkeypatch.setenv("CPHIFI_SANDWICH_V1", v1)
+        monkeypatch.setenv("CPHIFI_SANDWICH_V3", v3)  # v3: DMMA (even n >= 512)
         w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, v, mode), ev)
-        assert ri.rel(w, wo) < 1e-11, (sw, v1)
+        assert ri.rel(w, wo) < 1e-11, (sw, v1, v3)
     # zero denominator through the mapped status word (sandwich path)
     monkeypatch.setenv("CPHIFI_SANDWICH", "1")
     mode0 = cp.RkhsMode(ri.identity_points(4), 1.0, 0.0)
@@ -93,11 +94,12 @@ def test_precond_sandwich_variants(cp, monkeypatch):
     p.set_v_eig(ev.u, ev.d)
     x = np.random.default_rng(3).normal(size=c.shape[0] * c.r)
     yo = orc.build_preconditioner(sub, ek, ev).apply(x)
-    for sw, v1 in (("0", "0"), ("1", "1"), ("1", "0")):
+    for sw, v1, v3 in (("0", "0", "0"), ("1", "1", "0"), ("1", "0", "0"), ("1", "0", "1")):
         monkeypatch.setenv("CPHIFI_SANDWICH", sw)
         monkeypatch.setenv("CPHIFI_SANDWICH_V1", v1)
+        monkeypatch.setenv("CPHIFI_SANDWICH_V3", v3)
         y = cp.build_preconditioner(p).apply(x)
-        assert ri.rel(y, yo) < 1e-12, (sw, v1)
+        assert ri.rel(y, yo) < 1e-12, (sw, v1, v3)
 
 
 def test_pcg_graph_loop_matches_host_loop(cp, monkeypatch):
