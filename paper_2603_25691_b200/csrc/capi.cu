@@ -2325,14 +2325,24 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
         PcgCtl* ctl = reinterpret_cast<PcgCtl*>(partial + RED_PARTIALS + (sizeof(PcgState) + 7) / 8);
         CPHIFI_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * RED_PARTIALS, s));
         CPHIFI_CUDA(cudaMemsetAsync(st, 0, sizeof(PcgState), s));
+        const bool stime = std::getenv("CPHIFI_SOLVE_TIMING") != nullptr;  // developer: setup phases
+        auto lap = [&](const char* what) {
+            if (!stime) return;
+            CPHIFI_CUDA(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "cphifi: solve setup %s at %.3f ms\n", what,
+                         1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        };
         ensure_precond(p);                                                        // build_preconditioner
+        lap("preconditioner");
         const bool rot = pcg_eigbasis(p);
         if (rot && !p->small_n) mode_nzero(p->mode);  // host read here, never inside a graph capture
         if (rot) rotate(p, true, true, p->b.get(), bvec);  // rhs~ = (I x U') vec(K B) = mu o (U' B)
         else gemm_nn(ctx, n, r, n, p->mode->kernel.get(), n, p->b.get(), n, bvec, n);  // rhs = vec(K B)
+        lap("rhs");
         if (cfg->tol <= 0.0 || cfg->max_iter < 1) throw_invalid("pcg: invalid config");
         if (p->op == 1) ensure_gram(p);  // the row-Gram operator's G: per-solve setup, timed as such
         else ensure_runs(p);             // the stream operator's run tables and warp ranges
+        lap("operator state");
         CPHIFI_CUDA(cudaStreamSynchronize(s));
         const auto t_setup = std::chrono::steady_clock::now();
         double* hs = ctx->host_scalars;
