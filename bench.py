@@ -13,9 +13,11 @@ metric names none), so it is the N = 1 workload.
 application streams the ~2.9 GB coalesced plan, far above the 126 MB L2 (inputs larger than L2).
 `e2e` is the same metric through the reference-facing host-buffer C-ABI call
 (cphifi_unaligned_matvec: x copied in from pinned host memory, y read back, every step).
-`roofline` is the dominant kernel (the run-structured scatter-gather, k_runs.cu) against the
-measured HBM peak on the as-given algorithmic bytes of SURVEY §8(d); `cpu_baseline` is the
-oracle's streaming C port on a bounded sample of the same draws.
+`roofline` is the dominant kernel (the run-structured scatter-gather, k_runs.cu, over the rows
+left to it) against the measured HBM peak on SURVEY §8(d)'s per-draw bytes; `roofline_dense_rows`
+is the q-pass's second kernel (k_dense_rows.cu: the Zipf-head rows whose cells are mostly drawn,
+as FP64 DMMA GEMMs) against the measured DMMA peak; `cpu_baseline` is the oracle's streaming C
+port on a bounded sample of the same draws.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Under torchrun (N > 1) the observations are sharded over ranks (equal-count slices of the i_k-sorted
@@ -292,6 +294,9 @@ def main():
     _capi.check(lib.cphifi_unaligned_matvec_timed(p.handle, x.data_ptr(), y.data_ptr(), min(args.steps, 10), ms6))
     launches = ctypes.c_int()
     _capi.check(lib.cphifi_unaligned_matvec_launches(p.handle, x.data_ptr(), y.data_ptr(), ctypes.byref(launches)))
+    qplan = p.qpass_plan()
+    dfma, dmma = ctypes.c_double(), ctypes.c_double()
+    _capi.check(lib.cphifi_fp64_peak(ctx.handle, ctypes.byref(dfma), ctypes.byref(dmma)))
 
     # e2e: the reference-facing host-buffer call, x in from pinned host memory and y back, every step
     hx = torch.randn(n * r, dtype=torch.float64).pin_memory().numpy()
@@ -306,10 +311,10 @@ def main():
         _capi.check(lib.cphifi_unaligned_matvec(p.handle, xp, yp))
     e2e_s = time.perf_counter() - t0
 
-    t = torch.tensor([total_ms, ms6[1], ms6[5], e2e_s], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, ms6[1], ms6[5], e2e_s, ms6[2]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, k1_ms, app_ms_phased, e2e_s = (float(v) for v in t)
+    total_ms, k1_ms, app_ms_phased, e2e_s, dense_ms = (float(v) for v in t)
     value = args.steps / (total_ms / 1e3)
 
     sec = {}
@@ -322,14 +327,21 @@ def main():
     if rank == 0:
         hbm, hbm_src = measured_hbm()
         fp64 = sec.get("fp64_peak", {}).get("dmma_tflops") if isinstance(sec.get("fp64_peak"), dict) else None
-        k1_bytes = alg_bytes_k1(d, q // world, n, r)
-        k1_s = k1_ms / 1e3
-        achieved = k1_bytes / k1_s / 1e9
+        # the q-pass = the run kernel over the plan's parts (one launch per factor-block part) + the
+        # dense-rows kernel (k_dense_rows.cu, rows whose cells are mostly drawn, as DMMA GEMMs)
+        nparts = max(1, qplan["parts"])
+        sparse_draws = qplan["sparse_draws"] if qplan["sparse_draws"] >= 0 else q // world
+        k1_bytes = alg_bytes_k1(d, sparse_draws, n, r) / nparts  # per launch
+        k1_launch_s = k1_ms / 1e3 / nparts
+        achieved = k1_bytes / k1_launch_s / 1e9
         traffic, traffic_src = ncu_traffic("ncu_full_runs_config4.json", "runs_kernel")
-        if traffic is not None:
-            traffic *= 2  # per application: one launch per factor-block part (2 at config 4)
+        nd = qplan["dense_rows"]
+        n1, n2 = cfg.shape[1], cfg.shape[2]
+        dense_flops = 4.0 * nd * n1 * n2 * r  # two GEMMs per dense row: S = U A_2', P = T A_2 (2 flops / FMA)
+        dtraffic, dtraffic_src = ncu_traffic("ncu_full_dense_config4.json", "dense_rows_kernel")
         t_app = total_ms / args.steps / 1e3
         b_alg, f_alg = alg_bytes_matvec(d, q, n, r), alg_flops_matvec(d, q, n, r)
+        qpass_bytes = alg_bytes_k1(d, q // world, n, r)
         out = {
             "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -340,23 +352,39 @@ def main():
             "parallelism": (f"observations sharded x{world} (equal-count slices of the sorted plan), n x r all-reduce "
                             "per application") if world > 1 else "1 GPU",
             "plan_entries_this_rank": ql.value,
-            "roofline": {"bound": "hbm", "kernel": "runs_kernel (k_runs.cu: the per-observation gather / scatter, "
-                                                  "2 launches per application, one per factor-block part)",
+            "qpass_plan": qplan,
+            "roofline": {"bound": "hbm", "kernel": f"runs_kernel (k_runs.cu: the per-entry gather / scatter over the "
+                                                  f"sparse rows, {nparts} launches per application, one per "
+                                                  f"factor-block part)",
                          "achieved": achieved, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                          "alg_bytes_per_launch": k1_bytes,
-                         "alg_bytes_note": "SURVEY 8(d) as-given bytes of the q-pass: 4 d q (int32 index stream of "
-                                           "the q draws, read once) + 16 n r (Xhat rows read, Yhat written); the "
-                                           "coalesced plan moves fewer bytes (traffic)",
-                         "kernel_ms": k1_ms, "kernel_share_of_step": k1_ms / app_ms_phased},
+                         "alg_bytes_note": "SURVEY 8(d) per-draw bytes (4 d: the int32 index stream) x the draws of "
+                                           "the run kernel's rows (qpass_plan.sparse_draws), + 16 n r (Xhat read, "
+                                           "Yhat written), per launch; traffic = ncu DRAM bytes per launch (the "
+                                           "coalesced plan streams 12 B per distinct entry)",
+                         "kernel_ms_per_launch": k1_launch_s * 1e3, "kernel_ms_per_application": k1_ms,
+                         "kernel_share_of_step": k1_ms / app_ms_phased},
+            "roofline_dense_rows": {"bound": "tensor", "kernel": "dense_rows_kernel (k_dense_rows.cu: the rows whose "
+                                                                 "cells are mostly drawn, two FP64 DMMA GEMMs per row)",
+                                    "achieved": dense_flops / (dense_ms / 1e3) / 1e12 if dense_ms > 0 else None,
+                                    "peak": dmma.value, "peak_source": "measured FP64 DMMA (cphifi_fp64_peak, this run)",
+                                    "unit": "TFLOP/s",
+                                    "frac": (dense_flops / (dense_ms / 1e3) / 1e12 / dmma.value) if dense_ms > 0 else None,
+                                    "traffic": dtraffic, "traffic_source": dtraffic_src,
+                                    "alg_flops_per_launch": dense_flops, "dense_rows": nd,
+                                    "kernel_ms": dense_ms, "kernel_share_of_step": dense_ms / app_ms_phased},
+            "qpass_as_given": {"alg_bytes": qpass_bytes, "ms": k1_ms + dense_ms,
+                               "hbm_frac": qpass_bytes / ((k1_ms + dense_ms) / 1e3) / 1e9 / hbm,
+                               "note": "the whole q-pass (both kernels) on SURVEY 8(d)'s as-given bytes 4 d q + 16 n r"},
             "fp64": {"alg_flops_per_application": f_alg,
                      "achieved_tflops": f_alg / t_app / 1e12, "peak_tflops_dmma_measured": fp64,
                      "survey_roofline_frac": (max(b_alg / (hbm * 1e9), f_alg / (fp64 * 1e12)) / t_app) if fp64 else None,
                      "note": "SURVEY 8(d): t_roof = max(B_alg/HBM, F_alg/P_FP64) on the as-given q draws; dedup of "
                              "repeated draws and the hoisted first mode make the executed flops lower"},
             "matvec_hbm_frac": b_alg / t_app / 1e9 / hbm,
-            "phase_ms": {nm: ms6[i] for i, nm in enumerate(["K_X_gemm", "runs_kernel", "-", "allreduce",
-                                                            "y_gemm", "whole_application"])},
+            "phase_ms": {nm: ms6[i] for i, nm in enumerate(["K_X_gemm", "runs_kernel", "dense_rows_kernel",
+                                                            "allreduce", "y_gemm", "whole_application"])},
             "e2e": {"value": args.steps / e2e_s, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n * r,
                     "d2h_bytes_per_step": 8 * n * r,
                     "call": "cphifi_unaligned_matvec (host x in, host y out, synchronous)"},

@@ -183,7 +183,8 @@ int cphifi_solve_unaligned_pcg(cphifi_unaligned p, const cphifi_pcg_config* cfg,
                                double* w_out);
 /* Benchmark hook: `iters` operator applications on DEVICE buffers x, y with CUDA events on
  * the context stream around each phase; ms_out[0..5] receives the mean milliseconds of
- * [0] Xhat = K X, [1] scatter-gather main kernel (K1), [2] fix-up, [3] all-reduce,
+ * [0] Xhat = K X, [1] scatter-gather main kernel(s) (K1: the run kernel's parts when planned),
+ * [2] the dense-rows kernel (k_dense_rows.cu; 0 when the plan has none), [3] all-reduce,
  * [4] y = K Yhat + lambda Xhat + rho x, [5] the whole matvec. */
 int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y, int iters,
                                   double* ms_out);
@@ -209,6 +210,12 @@ int cphifi_unaligned_matvec_launches(cphifi_unaligned p, const double* x, double
  * barrier 3, exit; 0 = phase not run).  *ctas receives the CTA count. */
 int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y,
                                   uint64_t* stamps, int capacity, int* ctas);
+/* Introspection: the stream operator's q-pass plan (built on first use).  info[0..count) receives
+ * [0] run-kernel parts (0: the whole plan on the stream kernel), [1] rows handled in the GEMM form
+ * (k_dense_rows.cu; CPHIFI_DENSE_MIN sets the density threshold, 0 turns it off), [2] plan entries
+ * left to the run kernel, [3] the draws those entries stand for (-1 without parts), [4] / [5] the
+ * dense grids' padded n_1 / n_2; further slots 0. */
+int cphifi_unaligned_qpass_plan(cphifi_unaligned p, int64_t* info, int count);
 /* Test hook: Yhat = sampled_mttkrp(gather_rows(Xhat)) for a given Xhat (n x r), i.e.
  * observations.hpp:174-198 fused, before the final K multiply (all-reduced). */
 int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, double* yhat_out);

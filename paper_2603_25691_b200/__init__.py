@@ -534,6 +534,14 @@ class UnalignedSubproblem:
         call("cphifi_unaligned_get_v_eig", self.handle, _dp(u), _dp(d))
         return SymEig(u, d)
 
+    def qpass_plan(self) -> dict:
+        """The stream operator's q-pass plan: run-kernel parts, dense rows (GEMM form), entries
+        left to the run kernel (cphifi_unaligned_qpass_plan)."""
+        v = (ctypes.c_int64 * 6)()
+        call("cphifi_unaligned_qpass_plan", self.handle, v, 6)
+        return {"parts": v[0], "dense_rows": v[1], "sparse_entries": v[2], "sparse_draws": v[3],
+                "dense_n1p": v[4], "dense_n2p": v[5]}
+
     def scatter_gather(self, xhat) -> np.ndarray:
         """Yhat = sampled_mttkrp(gather_rows(Xhat)) (observations.hpp:174-198), fused."""
         xhat = _f64(xhat)

@@ -117,6 +117,7 @@ _SIGS = [
     ("cphifi_unaligned_precond_apply_device", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p]),
     ("cphifi_solve_unaligned_pcg", ctypes.c_int,
      [_H, ctypes.POINTER(PcgConfigC), ctypes.POINTER(SolveReportC), c_double_p, c_double_p]),
+    ("cphifi_unaligned_qpass_plan", ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
     ("cphifi_unaligned_matvec_launches", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     ("cphifi_unaligned_matvec_timed", ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c_double_p]),
     ("cphifi_unaligned_matvec_cycle_timed", ctypes.c_int,

@@ -94,6 +94,8 @@ bool ctx_multi(cphifi_ctx ctx) { return ctx->nranks > 1 && (ctx->comm || ctx->vc
 
 // Sum of every rank's `send` into `recv` on every rank (in place allowed), ordered on the context
 // stream.  NCCL: ncclAllReduce.  Virtual communicator: see cphifi_vcomm_s (common.cuh).
+thread_local cudaEvent_t g_dense_event = nullptr;  // cphifi_unaligned_matvec_timed's mid-phase-B event
+thread_local bool g_dense_recorded = false;
 thread_local bool g_count_only = false;  // cphifi_unaligned_matvec_launches: capture this library's kernels only
 
 void allreduce_sum(cphifi_ctx ctx, const double* send, double* recv, size_t count) {
@@ -442,6 +444,28 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
             b.accumulate = acc ? 1 : 0;
             runs_scatter_gather(b, sp.sf, s);
         }
+        if (g_dense_event) {  // cphifi_unaligned_matvec_timed: the run kernel / dense rows split
+            CPHIFI_CUDA(cudaEventRecord(g_dense_event, s));
+            g_dense_recorded = true;
+        }
+        if (p->dense_nd > 0) {  // the dense rows (no entries in any part): written, not accumulated
+            DenseRowsArgs dr;
+            dr.rp = p->rp;
+            dr.n1 = p->dense_n1;
+            dr.n2 = p->dense_n2;
+            dr.n1p = p->dense_n1p;
+            dr.n2p = p->dense_n2p;
+            dr.nd = p->dense_nd;
+            dr.rows = p->dense_rows.get();
+            dr.w = p->dense_w.get();
+            dr.a1 = a.fac + a.fac_off[0];
+            dr.a2 = a.fac + a.fac_off[1];
+            dr.xhat_rm = a.xhat_rm;
+            dr.yhat_rm = a.yhat_rm;
+            dr.partial = p->dense_partial.get();
+            dr.cnt = p->dense_cnt.get();
+            dense_rows_qpass(dr, p->obs->ctx->num_sms, s);
+        }
         return;
     }
     if (p->stream) stream_scatter_gather(a, p->grid, p->stream_sf, p->obs->ctx->stream);
@@ -470,6 +494,15 @@ void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_
         h2d(sp.run_start.get() + nr, &qq, sizeof(int32_t), s);
         sp.run_i1.alloc(std::max<int64_t>(nr, 1));
         gather_i32(sp.idx, sp.run_start.get(), 0, nr, sp.run_i1.get(), s);
+    }
+    sp.draws = q;
+    if (sp.mult && q > 0) {
+        DevBuf<unsigned long long> sum(1);
+        CPHIFI_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), s));
+        sum_i32(sp.mult, q, sum.get(), s);
+        unsigned long long h = 0;
+        d2h_sync(&h, sum.get(), sizeof(h), s);
+        sp.draws = (int64_t)h;
     }
     std::vector<int64_t> rp_host(p->n + 1);
     d2h_sync(rp_host.data(), sp.row_ptr, sizeof(int64_t) * (p->n + 1), s);
@@ -509,6 +542,60 @@ void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // host plan vectors go out of scope
 }
 
+// Dense rows (k_dense_rows.cu): 3-way plans only; a row goes to the GEMM form when its distinct
+// cells cover at least CPHIFI_DENSE_MIN (default 0.3) of its n_1 x n_2 grid — the measured break-even
+// of two DMMA GEMMs per row against the run kernel's per-entry cost — and the grids
+// of all such rows fit CPHIFI_DENSE_MAX_GB (default 16 GB, int32 per cell).  Picks the rows, builds
+// their multiplicity grids and returns the per-row slot table (-1: sparse) on the device, or an empty
+// buffer when no row qualifies.
+DevBuf<int32_t> build_dense_rows(cphifi_unaligned p, const int32_t* rows_of_entry) {
+    cphifi_obs o = p->obs;
+    cphifi_ctx ctx = o->ctx;
+    cudaStream_t s = ctx->stream;
+    DevBuf<int32_t> slot;
+    p->dense_nd = 0;
+    double dmin = 0.3, max_gb = 16.0;
+    if (const char* e = std::getenv("CPHIFI_DENSE_MIN")) dmin = std::atof(e);
+    if (const char* e = std::getenv("CPHIFI_DENSE_MAX_GB")) max_gb = std::atof(e);
+    if (!(dmin > 0.0) || !dense_rows_supported(p->rp, o->d - 1) || !o->lex) return slot;
+    int m1 = -1, m2 = -1;  // the other modes, ascending (plan columns 0 and 1)
+    for (int m = 0; m < o->d; ++m)
+        if (m != o->k) (m1 < 0 ? m1 : m2) = m;
+    const int64_t n1 = o->shape[m1], n2 = o->shape[m2];
+    const int64_t ba = dense_rows_block_a(), bb = dense_rows_block_b();
+    const int64_t n1p = (n1 + ba - 1) / ba * ba, n2p = (n2 + bb - 1) / bb * bb;
+    std::vector<int64_t> rph(p->n + 1);
+    d2h_sync(rph.data(), o->row_ptr.get(), sizeof(int64_t) * (p->n + 1), s);
+    const double cells = (double)n1 * (double)n2;
+    std::vector<int32_t> drows, slot_h(p->n, -1);
+    const int64_t cap = (int64_t)(max_gb * 1e9 / (4.0 * (double)n1p * (double)n2p));
+    for (int64_t i = 0; i < p->n && (int64_t)drows.size() < cap; ++i)
+        if ((double)(rph[i + 1] - rph[i]) >= dmin * cells) {
+            slot_h[i] = (int32_t)drows.size();
+            drows.push_back((int32_t)i);
+        }
+    if (drows.empty()) return slot;
+    const int nd = (int)drows.size();
+    p->dense_nd = nd;
+    p->dense_n1 = n1;
+    p->dense_n2 = n2;
+    p->dense_n1p = n1p;
+    p->dense_n2p = n2p;
+    p->dense_rows.alloc(nd);
+    h2d(p->dense_rows.get(), drows.data(), sizeof(int32_t) * nd, s);
+    slot.alloc(p->n);
+    h2d(slot.get(), slot_h.data(), sizeof(int32_t) * p->n, s);
+    p->dense_w.alloc((size_t)nd * n1p * n2p);
+    CPHIFI_CUDA(cudaMemsetAsync(p->dense_w.get(), 0, sizeof(int32_t) * (size_t)nd * n1p * n2p, s));
+    dense_grid_build(o->idx_o.get(), o->ldq, o->coalesced ? o->mult.get() : nullptr, rows_of_entry, slot.get(),
+                     o->q_local, n1p, n2p, p->dense_w.get(), s);
+    p->dense_partial.alloc((size_t)nd * (n1p / ba) * p->rp);
+    p->dense_cnt.alloc(nd);
+    CPHIFI_CUDA(cudaMemsetAsync(p->dense_cnt.get(), 0, sizeof(unsigned) * nd, s));
+    CPHIFI_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    return slot;
+}
+
 bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     cphifi_obs o = p->obs;
     cphifi_ctx ctx = o->ctx;
@@ -522,7 +609,10 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     const int64_t nl = o->shape[lm], rp = p->rp, q = o->q_local;
     DevBuf<int32_t> rows(std::max<int64_t>(q, 1));
     row_of_entries(o->row_ptr.get(), p->n, q, rows.get(), s);
-    if (runs_smem_bytes(rp, d - 1, mult, sf_all) <= runs_smem_cap()) {  // one part: the plan itself
+    const DevBuf<int32_t> dslot = build_dense_rows(p, rows.get());
+    const bool dense = p->dense_nd > 0;
+    const bool fits = runs_smem_bytes(rp, d - 1, mult, sf_all) <= runs_smem_cap();
+    if (fits && !dense) {  // one part: the plan itself
         std::vector<StreamPart> parts(1);
         StreamPart& sp = parts[0];
         sp.q = q;
@@ -537,28 +627,30 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
         return true;
     }
     const int64_t rest = sf_all - nl * rp;  // staged doubles of the other per-observation modes
-    int64_t br = 0;
-    for (int64_t b = nl; b >= 8; b -= 8)
-        if (runs_smem_bytes(rp, d - 1, mult, rest + b * rp) <= runs_smem_cap()) {
-            br = b;
-            break;
-        }
-    if (br < 8) return false;
+    int64_t br = fits ? nl : 0;
+    for (int64_t b = nl; b >= 8 && br == 0; b -= 8)
+        if (runs_smem_bytes(rp, d - 1, mult, rest + b * rp) <= runs_smem_cap()) br = b;
+    if (br < 8 && !fits) {
+        p->dense_nd = 0;  // no parts: the stream kernel takes the whole plan
+        return false;
+    }
     const int H = (int)((nl + br - 1) / br);
     br = (nl + H - 1) / H;  // balanced blocks
+    // part key = block of the last other mode; the dense rows' entries get key H (dropped)
     DevBuf<int32_t> key(std::max<int64_t>(q, 1)), key_s(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
         perm(std::max<int64_t>(q, 1)), rows_h(std::max<int64_t>(q, 1));
     DevBuf<int64_t> bounds(H + 1);
     block_key(o->idx_o.get() + (int64_t)dl * o->ldq, q, (int32_t)br, key.get(), s);
+    if (dense) dense_key(rows.get(), dslot.get(), q, (int32_t)H, key.get(), s);
     iota32(perm_in.get(), q, s);
     int bits = 1;
-    while ((1 << bits) < H) ++bits;
+    while ((1 << bits) < H + 1) ++bits;
     if (q > 0) {
         const size_t tb = radix_sort_pairs_bytes(q, bits);
         DevBuf<unsigned char> tmp(tb);
         radix_sort_pairs(tmp.get(), tb, key.get(), key_s.get(), perm_in.get(), perm.get(), q, bits, s);
     }
-    csr_from_sorted(key_s.get(), q, H, bounds.get(), s);  // bounds[h] = first entry of part h
+    csr_from_sorted(key_s.get(), q, H, bounds.get(), s);  // bounds[h] = first entry of part h; [H]: dense
     std::vector<int64_t> hb(H + 1);
     d2h_sync(hb.data(), bounds.get(), sizeof(int64_t) * (H + 1), s);
     std::vector<StreamPart> parts(H);
@@ -604,7 +696,7 @@ bool gram_build_parts(cphifi_unaligned p) {
     cphifi_obs o = p->obs;
     if (!on || !gram_ws_supported(p->rp, o->d - 1)) return false;
     ensure_runs(p);
-    if (p->parts.empty()) return false;
+    if (p->parts.empty() || p->dense_nd > 0) return false;  // the parts leave out the dense rows
     for (const auto& sp : p->parts)
         if (gram_ws_smem_bytes(p->rp, sp.sf) > runs_smem_cap()) return false;
     cphifi_ctx ctx = o->ctx;
@@ -2092,10 +2184,13 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
             a.x = x;
             a.y = y;
             a.gram = gr;
+            g_dense_event = ev[2];  // launch_phase_b records it between the run kernel and the dense rows
+            g_dense_recorded = false;
             if (!p->small_n && gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), s);
             else if (!p->small_n) launch_phase_b(p, a);
             else launch_fused(p, a);
-            CPHIFI_CUDA(cudaEventRecord(ev[2], s));
+            g_dense_event = nullptr;
+            if (!g_dense_recorded) CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
             allreduce_yhat(p);
             CPHIFI_CUDA(cudaEventRecord(ev[4], s));
@@ -2241,6 +2336,24 @@ int cphifi_unaligned_scatter_gather(cphifi_unaligned p, const double* xhat, doub
         allreduce_yhat(p);
         rm_to_cm(yhat_result(p), n, p->rp, r, p->vy.get(), ctx->stream);
         d2h_sync(yhat_out, p->vy.get(), sizeof(double) * n * r, ctx->stream);
+    });
+}
+
+int cphifi_unaligned_qpass_plan(cphifi_unaligned p, int64_t* info, int count) {
+    return guard([&] {
+        need(p, "p");
+        need(info, "info");
+        if (count < 1) throw_invalid("cphifi_unaligned_qpass_plan: count must be positive");
+        DeviceGuard dg(p->obs->ctx->device);
+        ensure_runs(p);
+        int64_t q = 0, dr = 0;
+        for (const auto& sp : p->parts) {
+            q += sp.q;
+            dr += sp.draws;
+        }
+        const int64_t v[6] = {(int64_t)p->parts.size(), p->dense_nd, p->parts.empty() ? p->obs->q_local : q,
+                              p->parts.empty() ? -1 : dr, p->dense_n1p, p->dense_n2p};
+        for (int i = 0; i < count; ++i) info[i] = i < 6 ? v[i] : 0;
     });
 }
 

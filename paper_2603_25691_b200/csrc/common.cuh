@@ -185,6 +185,7 @@ struct StreamPart {
     int64_t sf = 0;                      // staged factor doubles
     cphifi::DevBuf<int32_t> run_start, run_i1;  // run table (nruns + 1 / nruns)
     int64_t nruns = 0;
+    int64_t draws = 0;                   // draws the part's entries stand for (sum of multiplicities)
     int warps = 0;                       // equal-count warp ranges
     cphifi::DevBuf<int64_t> warp_beg, warp_rows;
     cphifi::DevBuf<int32_t> row_first_w, row_nw;
@@ -217,6 +218,11 @@ struct cphifi_unaligned_s {
     int64_t stream_sf = 0;        // doubles of per-observation factors k_stream.cu stages in smem (0: L1)
     std::vector<StreamPart> parts;  // non-empty: the operator's q-pass is the run kernel over these parts
     cphifi::DevBuf<double> runs_slot_a, runs_slot_b;  // warps x rp: split-row partials of the run kernel
+    int dense_nd = 0;             // dense rows of the run kernel's plan (k_dense_rows.cu), 0: none
+    int64_t dense_n1 = 0, dense_n2 = 0, dense_n1p = 0, dense_n2p = 0;
+    cphifi::DevBuf<int32_t> dense_rows, dense_w;  // their row indices; nd x n1p x n2p multiplicities
+    cphifi::DevBuf<double> dense_partial;         // per-task partial rows
+    cphifi::DevBuf<unsigned> dense_cnt;           // per-row arrival counters
     bool runs_pending = false;    // parts not built yet (ensure_runs)
     int64_t runs_sf = 0;          // staged per-observation factor doubles of the whole plan
     cphifi::DevBuf<unsigned> rowcnt;   // n per-row arrival counters

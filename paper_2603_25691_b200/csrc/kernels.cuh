@@ -214,6 +214,34 @@ struct RunsArgs {
     unsigned* rowcnt = nullptr;          // n arrival counters, zero between launches
     int accumulate = 0;                  // add into yhat_rm (stream parts) instead of overwriting
 };
+// Dense rows of a 3-way plan (k_dense_rows.cu): the q-pass of rows whose cells are mostly drawn as
+// two DMMA GEMMs per row over the row's multiplicity grid W_i (n1p x n2p int32, zero-padded).
+struct DenseRowsArgs {
+    int64_t rp = 0;
+    int64_t n1 = 0, n2 = 0;              // other-mode sizes (A_1 rows, A_2 rows)
+    int64_t n1p = 0, n2p = 0;            // padded to the kernel's blocks (dense_rows_block_a / _b)
+    int nd = 0;                          // dense rows
+    const int32_t* rows = nullptr;       // nd: their row indices i_k
+    const int32_t* w = nullptr;          // nd x n1p x n2p multiplicities
+    const double* a1 = nullptr;          // n1 x rp row-major
+    const double* a2 = nullptr;          // n2 x rp row-major
+    const double* xhat_rm = nullptr;     // n x rp
+    double* yhat_rm = nullptr;           // n x rp: the dense rows are written (overwritten)
+    double* partial = nullptr;           // nd x (n1p / block_a) x rp scratch
+    unsigned* cnt = nullptr;             // nd arrival counters, zero between launches
+};
+int dense_rows_block_a();
+int dense_rows_block_b();
+bool dense_rows_supported(int64_t rp, int dother);
+void dense_rows_qpass(const DenseRowsArgs& a, int num_sms, cudaStream_t s);
+// W(slot[rows[l]], idx0[l], idx1[l]) += mult[l] (1 without multiplicities) for the entries of dense rows
+void dense_grid_build(const int32_t* idx, int64_t ldq, const int32_t* mult, const int32_t* rows, const int32_t* slot,
+                      int64_t q, int64_t n1p, int64_t n2p, int32_t* w, cudaStream_t s);
+// *out += sum of v[0, q) (nonnegative int32; integer atomics: exact)
+void sum_i32(const int32_t* v, int64_t q, unsigned long long* out, cudaStream_t s);
+// key[l] = dense_key_value for the entries of dense rows (slot[rows[l]] >= 0)
+void dense_key(const int32_t* rows, const int32_t* slot, int64_t q, int32_t dense_key_value, int32_t* key,
+               cudaStream_t s);
 bool runs_supported(int64_t rp, int dother);
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles);
 size_t runs_smem_cap();

@@ -49,6 +49,7 @@ def _ptxas_report(src):
     ("k_runs.cu", r"runs_kernelILi32ELi3ELb0ELi4ELi2ELb0E", 32),  # config 3 q-pass
     ("k_gram.cu", r"gram_build_dmma2?_kernelILi(32ELi3|64ELi2)E", 0),  # configs 3 / 4 row-Gram builds
     ("k_stream.cu", r"stream_kernelILi(32ELi3|64ELi2)ELb[01]ELi2E", 0),  # configs 3 / 4 right-hand side B
+    ("k_dense_rows.cu", r"dense_rows_kernelILi64E", 8),  # config 4 dense rows (one word outside the chunk loop)
 ])
 def test_no_spills(src, pattern, allow):
     rep = _ptxas_report(src)
