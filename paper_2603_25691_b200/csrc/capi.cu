@@ -781,14 +781,19 @@ void ensure_gram(cphifi_unaligned p) {
     probe.fac = p->fac.get();
     for (int m = 0; m < o->d - 1; ++m) probe.fac_off[m] = p->fac_off[m];
     probe.fac_total = (int64_t)p->fac.n;
-    int per_sm = gram_build_occupancy(probe);
+    // the register-fragment build (k_gram3.cu) over an equal-count partition of gram3_units_per_sm
+    // units per SM; else the single-pass builds of k_gram.cu over their row-aligned partition
+    bool v3 = gram3_supported(p->rp, o->d - 1, probe);
+    if (const char* e = std::getenv("CPHIFI_GRAM3")) v3 = v3 && std::atoi(e) != 0;
+    int per_sm = v3 ? gram3_units_per_sm(p->rp) : gram_build_occupancy(probe);
     if (const char* e = std::getenv("CPHIFI_GRAM_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
     const int cmax = per_sm * ctx->num_sms;
     PartitionPlan plan;
     {
         std::vector<int64_t> rp_host(p->n + 1);
         d2h_sync(rp_host.data(), o->row_ptr.get(), sizeof(int64_t) * (p->n + 1), s);
-        plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
+        if (v3) plan_partition(rp_host, cmax, cmax, plan, cmax);
+        else plan_partition(rp_host, cmax, std::min(cmax, ctx->num_sms), plan);
     }
     const int grid = plan.ctas;
     DevBuf<int64_t> cta_beg(plan.beg.size()), cta_rows(plan.rows.size());
@@ -826,7 +831,10 @@ void ensure_gram(cphifi_unaligned p) {
         CPHIFI_CUDA(cudaEventCreate(&e1));
         CPHIFI_CUDA(cudaEventRecord(e0, s));
     }
-    if (o->q_local > 0) gram_build(g, grid, s);
+    if (o->q_local > 0) {
+        if (v3) gram3_build(g, grid, s);
+        else gram_build(g, grid, s);
+    }
     if (timing) CPHIFI_CUDA(cudaEventRecord(e1, s));
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // the plan buffers are released on return
     if (timing) {

@@ -278,7 +278,12 @@ void gram_build(const GramArgs& a, int grid, cudaStream_t s);
 bool gram_ws_supported(int64_t rp, int dother);
 size_t gram_ws_smem_bytes(int64_t rp, int64_t sf);
 void gram_build_ws(const GramArgs& a, int grid, int64_t sf, cudaStream_t s);
-int gram_build_occupancy(const GramArgs& a);  // partition CTAs per SM for the build gram_build picks
+int gram_build_occupancy(const GramArgs& a);
+// register-fragment build (k_gram3.cu): units = contiguous entry ranges of an equal-count partition
+// (cta_beg / cta_rows / row_first_cta / row_ncta over `units`), gram3_units_per_sm(rp) per SM
+bool gram3_supported(int64_t rp, int dother, const GramArgs& a);
+int gram3_units_per_sm(int64_t rp);
+void gram3_build(const GramArgs& a, int units, cudaStream_t s);  // partition CTAs per SM for the build gram_build picks
 void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
                 cudaStream_t s);
 

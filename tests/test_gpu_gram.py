@@ -122,11 +122,15 @@ def test_gram_large_config_structure(cp, which, q):
     assert ri.rel(cp.unaligned_matvec(p, x), y_o) < 1e-12
 
 
-@pytest.mark.parametrize("shape,r,multiset", [([48, 20, 16, 6], 32, False), ([40, 64, 30], 64, True), ([30, 50, 9], 16, True)])
+@pytest.mark.parametrize("shape,r,multiset", [([48, 20, 16, 6], 32, False), ([40, 64, 30], 64, True), ([30, 50, 9], 16, True),
+                                              ([700, 30, 20], 64, False), ([600, 9, 7, 5, 6], 16, True),
+                                              ([520, 40, 36], 24, True)])
 def test_gram_build_v1_vs_v2(cp, monkeypatch, shape, r, multiset):
-    """Row-Gram build: the 2x2 register-blocked DMMA kernel (v2, default for RP >= 16) against the
-    one-tile-per-fragment kernel (v1) and the oracle — coalesced multiset plans included (entry
-    weights = multiplicities); split k-steps (RP 32 / 16) are summed in a fixed order."""
+    """Row-Gram build: the register-fragment kernel (v3, k_gram3.cu, the default for RP 16 / 32 / 64
+    and 2..4 other modes), the 2x2 register-blocked DMMA kernel (v2) and the one-tile-per-fragment
+    kernel (v1) against each other and the oracle — coalesced multiset plans included (entry weights
+    = multiplicities), rows split over many units (small n: the last arrival sums the unit slots),
+    k-steps straddling row ends."""
     g = cp.Mt19937_64(11 + r)
     factors = ri.random_model(shape, r, g)
     rs = np.random.default_rng(r)
@@ -137,12 +141,17 @@ def test_gram_build_v1_vs_v2(cp, monkeypatch, shape, r, multiset):
     kern = mode.kernel()
     x = np.random.default_rng(5).normal(size=shape[0] * r)
     ys = {}
-    for v in ("0", "1"):
-        monkeypatch.setenv("CPHIFI_GRAM_V2", v)
-        p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals, multiset=True), cp.KruskalModel(factors), 0,
-                                         mode, 1e-6)
+    for v, env in (("v1", {"CPHIFI_GRAM3": "0", "CPHIFI_GRAM_V2": "0"}), ("v2", {"CPHIFI_GRAM3": "0", "CPHIFI_GRAM_V2": "1"}),
+                   ("v3", {"CPHIFI_GRAM3": "1"})):
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        p = cp.make_unaligned_subproblem(cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=multiset),
+                                         cp.KruskalModel(factors), 0, mode, 1e-6)
         p.set_operator("gram")
         ys[v] = cp.unaligned_matvec(p, x)
+        assert np.array_equal(ys[v], cp.unaligned_matvec(p, x))
+        monkeypatch.delenv("CPHIFI_GRAM_V2", raising=False)
     y_o = orc.unaligned_matvec_stream(shape, 0, idx, factors, kern, 1e-3, 1e-6, x)
-    assert ri.rel(ys["1"], ys["0"]) < 1e-13
-    assert ri.rel(ys["1"], y_o) < 1e-12
+    assert ri.rel(ys["v2"], ys["v1"]) < 1e-13
+    assert ri.rel(ys["v3"], ys["v1"]) < 1e-13
+    assert ri.rel(ys["v3"], y_o) < 1e-12
