@@ -956,7 +956,10 @@ void precond_dev(cphifi_unaligned p, const double* x, double* y) {
     const double* uk = p->mode->u.get();
     if (sandwich_supported(n, r)) {
         const int64_t need_d = sandwich_scratch_doubles(n, r);
-        if (p->t1.n < (size_t)need_d) p->t1.alloc(need_d);
+        if (p->t1.n < (size_t)need_d) {
+            p->t1.alloc(need_d);
+            CPHIFI_CUDA(cudaMemsetAsync(p->t1.get(), 0, sizeof(double) * need_d, ctx->stream));  // counters
+        }
         SandArgs a;
         a.n = n; a.r = r;
         a.u = uk; a.ut = mode_ut(p->mode);
@@ -1136,7 +1139,10 @@ int* decoupled_dev(cphifi_mode mode, int64_t r, const double* b, const double* u
     *flag = 0;
     if (sandwich_supported(n, r)) {
         const int64_t need_d = sandwich_scratch_doubles(n, r);
-        if (core.n < (size_t)need_d) core.alloc(need_d);
+        if (core.n < (size_t)need_d) {
+            core.alloc(need_d);
+            CPHIFI_CUDA(cudaMemsetAsync(core.get(), 0, sizeof(double) * need_d, ctx->stream));  // counters
+        }
         SandArgs a;
         a.n = n; a.r = r;
         a.u = mode->u.get(); a.ut = mode_ut(mode);

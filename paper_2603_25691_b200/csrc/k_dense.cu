@@ -960,7 +960,7 @@ __global__ void peak_dmma_kernel(int iters, double seed, double* out) {
 }  // namespace
 
 bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
-                        uint32_t box1) {
+                        uint32_t box1, bool swizzle128) {
     using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -978,8 +978,8 @@ bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uin
     const cuuint32_t box[2] = {box0, box1};
     const cuuint32_t es[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool encode_tmap_3d_f64(CUtensorMap* map, const double* base, uint64_t n0, uint64_t n1, uint64_t n2, uint32_t b0,

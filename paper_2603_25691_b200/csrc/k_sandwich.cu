@@ -142,6 +142,24 @@ __global__ void __launch_bounds__(SW_T) sandwich_kernel(const SandArgs a) {
     }
 }
 
+// uv[m][j] = U_V(m, j) (phase 1) or U_V(j, m) (phase 2), zero beyond r: one 8-byte cp.async per
+// element (completion awaited by stage_uv_wait before the epilogue), plain stores for the padding
+template <int RP, int NT, int PH>
+__device__ __forceinline__ void stage_uv(double (*uv)[RP + 1], const double* src, int r) {
+    for (int e = threadIdx.x; e < RP * RP; e += NT) {
+        const int m = e / RP, j = e % RP;
+        if (m < r && j < r) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(&uv[m][j]));
+            const double* g = src + (PH == 1 ? m + (int64_t)r * j : j + (int64_t)r * m);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(g) : "memory");
+        } else {
+            uv[m][j] = 0.0;
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void stage_uv_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ---- v2 (even n, 16-byte aligned columns): bulk-copy ring, k across lanes -----------------
 // Each stage brings KC consecutive k of the CTA's RB columns of F (U or U') and of every column of
 // M (X, or the phase-1 core, both column-major with leading dimension ld) with one bulk copy per
@@ -162,6 +180,7 @@ struct Sw2Smem {
     double m[SW2_ST][RP][KC];
     double u[SW2_ST][RB][KC];
     double tt[RB][RP + 1];
+    double uv[RP][RP + 1];  // as in v3 below
     uint64_t full[SW2_ST];
 };
 template <int RP, int RB, int PH>
@@ -191,6 +210,7 @@ __global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a, cons
     };
     if (threadIdx.x == 0)
         for (int c = 0; c < min(nch, SW2_ST); ++c) issue(c);
+    stage_uv<RP, SW2_T, PH>(sm.uv, a.uv, r);
     double acc[JPW][RB];
 #pragma unroll
     for (int jj = 0; jj < JPW; ++jj)
@@ -232,13 +252,19 @@ __global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a, cons
         for (int l = 0; l < 32; ++l) t += red[(w * 32 + l) * (JPW * RB) + rem];
         sm.tt[q][w + SW2_W * jj] = t;
     }
+    stage_uv_wait();
     __syncthreads();
     for (int e = threadIdx.x; e < RB * RP; e += SW2_T) {
         const int q = e / RP, jj = e % RP;
         if (q >= rb || jj >= r) continue;
         const int64_t i = i0 + q;
-        double c = 0.0;
-        for (int m = 0; m < r; ++m) c = fma(sm.tt[q][m], PH == 1 ? a.uv[m + (int64_t)r * jj] : a.uv[jj + (int64_t)r * m], c);
+        double c0 = 0.0, c1 = 0.0;  // two chains, summed once: a fixed order
+#pragma unroll
+        for (int m = 0; m < RP; m += 2) {
+            c0 = fma(sm.tt[q][m], sm.uv[m][jj], c0);
+            c1 = fma(sm.tt[q][m + 1], sm.uv[m + 1][jj], c1);
+        }
+        const double c = c0 + c1;
         if constexpr (PH == 1) {
             double out;
             if (a.op == SW_MUL) {
@@ -265,21 +291,23 @@ __global__ void __launch_bounds__(SW2_T) sandwich2_kernel(const SandArgs a, cons
 // RPP = RP + 8 spreads a B fragment's 4 k-rows over all 32 banks).  The 8 warps split every
 // stage's k-steps (warp w: k-steps w, w + 8, ...), each holding RP / 8 accumulator tiles; the
 // warp partials are summed in warp order at the end: deterministic.
-constexpr int SW3_T = 256, SW3_W = 8, SW3_RB = 8, SW3_ST = 4;
+constexpr int SW3_T = 256, SW3_W = 8, SW3_RB = 8;
 template <int RP>
 struct Sw3 {
     static constexpr int RPP = RP + 8;                  // B-tile pitch
     static constexpr int KC = RP >= 64 ? 64 : 128;     // k per stage
     static constexpr int NTL = RP / 8;                  // 8 x 8 output tiles per CTA
+    static constexpr int ST = RP >= 64 ? 3 : 4;        // ring stages (U_V staged beside them)
 };
 template <int RP>
 struct Sw3Smem {
-    static constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP;
-    double a[SW3_ST][KC][SW3_RB];
-    double b[SW3_ST][KC][RPP];
+    static constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP, ST = Sw3<RP>::ST;
+    double a[ST][KC][SW3_RB];
+    double b[ST][KC][RPP];
     double red[SW3_W][SW3_RB][RP];
     double tt[SW3_RB][RP + 1];
-    uint64_t full[SW3_ST];
+    double uv[RP][RP + 1];  // U_V (phase 1) or U_V' (phase 2), zero-padded: uv[m][j] multiplies tt[q][m]
+    uint64_t full[ST];
 };
 __device__ __forceinline__ void dmma_sw(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -292,7 +320,7 @@ __global__ void __launch_bounds__(SW3_T) sandwich3_kernel(const SandArgs a, cons
     extern __shared__ __align__(128) unsigned char smem_raw[];
     using SM = Sw3Smem<RP>;
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
-    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP, NTL = Sw3<RP>::NTL, RB = SW3_RB;
+    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP, NTL = Sw3<RP>::NTL, RB = SW3_RB, SW3_ST = Sw3<RP>::ST;
     const int64_t n = a.n;
     const int r = (int)a.r;
     const int64_t i0 = (int64_t)blockIdx.x * RB;
@@ -312,6 +340,9 @@ __global__ void __launch_bounds__(SW3_T) sandwich3_kernel(const SandArgs a, cons
     };
     if (threadIdx.x == 0)
         for (int c = 0; c < min(nch, SW3_ST); ++c) issue(c);
+    // the epilogue's r x r factor, staged by asynchronous copies while the ring fills (its reads
+    // were a dependent chain of global loads per output element)
+    stage_uv<RP, SW3_T, PH>(sm.uv, a.uv, r);
     double acc[NTL][2];
 #pragma unroll
     for (int t = 0; t < NTL; ++t) acc[t][0] = acc[t][1] = 0.0;
@@ -347,6 +378,7 @@ __global__ void __launch_bounds__(SW3_T) sandwich3_kernel(const SandArgs a, cons
         for (int w = 0; w < SW3_W; ++w) t += sm.red[w][q][jj];
         sm.tt[q][jj] = t;
     }
+    stage_uv_wait();
     __syncthreads();
     for (int e = threadIdx.x; e < RB * RPP; e += SW3_T) {
         const int q = e / RPP, jj = e % RPP;
@@ -356,8 +388,13 @@ __global__ void __launch_bounds__(SW3_T) sandwich3_kernel(const SandArgs a, cons
             if constexpr (PH == 1) core_rm[i * RPP + jj] = 0.0;
             continue;
         }
-        double c = 0.0;
-        for (int m = 0; m < r; ++m) c = fma(sm.tt[q][m], PH == 1 ? a.uv[m + (int64_t)r * jj] : a.uv[jj + (int64_t)r * m], c);
+        double c0 = 0.0, c1 = 0.0;  // two chains, summed once: a fixed order
+#pragma unroll
+        for (int m = 0; m < RP; m += 2) {
+            c0 = fma(sm.tt[q][m], sm.uv[m][jj], c0);
+            c1 = fma(sm.tt[q][m + 1], sm.uv[m + 1][jj], c1);
+        }
+        const double c = c0 + c1;
         if constexpr (PH == 1) {
             double out;
             if (a.op == SW_MUL) {
@@ -471,6 +508,170 @@ void launch_ph(const SandArgs& a, int rb, cudaStream_t s) {
         case 64: launch_rb<64, PH>(a, rb, s); break;
         default: throw_invalid("sandwich: padded rank must be 8, 16, 32 or 64");
     }
+}
+
+// ---- v4: split-K DMMA, one tile per CTA, partial sums reduced by the last CTA of each row block ----
+// v3's CTAs each stream ALL of M (X or the core: n x (r + 8) doubles, 327 KB at config 2) next to
+// their 8 rows of F, so a phase moves ~42 MB through L2 for a 67 MFLOP product (~10 us).  Here CTA
+// (ib, kb) takes the BI x BK block of F and the BK x r block of M once, as 2 x 8 TMA boxes of 16 k
+// with the 128-byte swizzle, runs the BI x RP x BK product on DMMA (8 warps, output tiles split
+// between them, full k per tile) and stores its partial block; the last CTA of row block ib
+// (arrival counter, reset by that CTA) sums the nkb partials in kb order and runs the epilogue (x U_V
+// or U_V', the element-wise op) for its BI rows.  Both operands are read k-contiguous — F(i, k) =
+// G(k, i) with G = U (phase 1: F = U') or U' (phase 2: F = U), M = X or the core column-major — so a
+// box row is 16 consecutive k of one i (or j) and the swizzle (chunk ^ row mod 8) spreads an
+// m8n8k4 fragment's 8 rows x 2 chunks over all bank groups: 2 wavefronts per fragment, the minimum.
+// X is read in place (no transposed copy); fixed summation order throughout: bit-reproducible.
+constexpr int SW4_T = 256, SW4_W = 8, SW4_BI = 32, SW4_BK = 128, SW4_KB = 16, SW4_NB = SW4_BK / SW4_KB;
+template <int RP>
+struct Sw4Smem {
+    double a[SW4_NB][SW4_BI][SW4_KB];  // box b: G(k0 + 16 b + k, i0 + i), swizzled 16-byte chunks
+    double b[SW4_NB][RP][SW4_KB];      // box b: M(k0 + 16 b + k, j), swizzled
+    double uv[RP][RP + 1];
+    double c[SW4_BI][RP + 1];
+    uint64_t full;
+    unsigned last;
+};
+// element (row y, k) of a swizzled box of 16-double rows
+__device__ __forceinline__ int swz(int y, int k) { return y * SW4_KB + ((((k >> 1) ^ (y & 7))) << 1) + (k & 1); }
+// scratch (doubles): core column-major n x r | partials nkb x n x RP | row-block counters
+template <int RP, int PH>
+__global__ void __launch_bounds__(SW4_T, 2) sandwich4_kernel(const SandArgs a, const __grid_constant__ CUtensorMap tm_g,
+                                                             const __grid_constant__ CUtensorMap tm_m) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    using SM = Sw4Smem<RP>;
+    // the swizzled boxes need 1024-byte alignment (the launch adds the slack)
+    // (offset arithmetic on smem_raw keeps the accesses in the shared state space: LDS, not generic)
+    const unsigned mis = static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u;
+    SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - mis) & 1023u));
+    constexpr int BI = SW4_BI, BK = SW4_BK, TJ = RP / 8, NTL = (BI / 8) * TJ, TPW = NTL / SW4_W;
+    static_assert(NTL % SW4_W == 0, "output tiles split evenly over the warps");
+    const int64_t n = a.n;
+    const int r = (int)a.r;
+    const int nkb = (int)((n + BK - 1) / BK);
+    const int kb = blockIdx.x % nkb, ib = blockIdx.x / nkb;
+    const int64_t i0 = (int64_t)ib * BI, k0 = (int64_t)kb * BK;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, kq = lane & 3;
+    double* core = a.core_out;                                  // n x r column-major
+    double* part = a.core_out + n * RP;                         // nkb x n x RP
+    unsigned* cnt = reinterpret_cast<unsigned*>(part + (int64_t)nkb * n * RP);
+    if (tid == 0) {
+        tma::mbar_init(&sm.full, 1);
+        tma::fence_mbar_init();
+        tma::mbar_expect_tx(&sm.full, (unsigned)(sizeof(double) * SW4_NB * SW4_KB * (BI + RP)));
+#pragma unroll
+        for (int bx = 0; bx < SW4_NB; ++bx) {
+            tma::tensor_g2s_2d(&sm.a[bx][0][0], &tm_g, (int)(k0 + SW4_KB * bx), (int)i0, &sm.full);
+            tma::tensor_g2s_2d(&sm.b[bx][0][0], &tm_m, (int)(k0 + SW4_KB * bx), 0, &sm.full);
+        }
+    }
+    __syncthreads();  // barrier initialised
+    stage_uv<RP, SW4_T, PH>(sm.uv, a.uv, r);  // every CTA: the last one of its row block needs it at once
+    tma::mbar_wait(&sm.full, 0);
+    double acc[TPW][2];
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+    for (int bx = 0; bx < SW4_NB; ++bx) {
+        const double* ab = &sm.a[bx][0][0];
+        const double* bb = &sm.b[bx][0][0];
+#pragma unroll
+        for (int kk = 0; kk < SW4_KB; kk += 4) {
+            const int k = kk + kq;
+#pragma unroll
+            for (int t = 0; t < TPW; ++t) {
+                const int tile = warp + SW4_W * t, ti = tile / TJ, tj = tile % TJ;
+                dmma_sw(acc[t], ab[swz(8 * ti + g, k)], bb[swz(8 * tj + g, k)]);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+        const int tile = warp + SW4_W * t, ti = tile / TJ, tj = tile % TJ;
+        const int64_t row = i0 + 8 * ti + g;
+        if (row < n)
+            __stcg(reinterpret_cast<double2*>(part + ((int64_t)kb * n + row) * RP + 8 * tj + 2 * kq),
+                   make_double2(acc[t][0], acc[t][1]));
+    }
+    __syncthreads();  // the CTA's partial stores precede thread 0's release
+    if (tid == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt + ib) : "memory");
+        sm.last = old == (unsigned)nkb - 1;
+        if (sm.last) cnt[ib] = 0;
+    }
+    __syncthreads();
+    if (!sm.last) {
+        stage_uv_wait();
+        return;
+    }
+    const int rb = (int)min((int64_t)BI, n - i0);
+    constexpr int PER = BI * RP / SW4_T;  // partial sums per thread, loads all in flight
+    static_assert(BI * RP % SW4_T == 0, "even split");
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int e = tid + SW4_T * u, q = e / RP, jj = e % RP;
+        double v = 0.0;
+        if (q < rb) {
+            double pv[8];
+            for (int k8 = 0; k8 < nkb; k8 += 8) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) pv[t] = k8 + t < nkb ? __ldcg(part + ((int64_t)(k8 + t) * n + i0 + q) * RP + jj) : 0.0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) v += pv[t];  // kb order
+            }
+        }
+        sm.c[q][jj] = v;
+    }
+    stage_uv_wait();
+    __syncthreads();
+    for (int e = tid; e < BI * RP; e += SW4_T) {
+        const int jj = e / BI, q = e % BI;  // consecutive threads: consecutive rows (column-major outputs)
+        if (q >= rb || jj >= r) continue;
+        const int64_t i = i0 + q;
+        double c0 = 0.0, c1 = 0.0;  // two chains, summed once: a fixed order
+#pragma unroll
+        for (int m = 0; m < RP; m += 2) {
+            c0 = fma(sm.c[q][m], sm.uv[m][jj], c0);
+            c1 = fma(sm.c[q][m + 1], sm.uv[m + 1][jj], c1);
+        }
+        const double c = c0 + c1;
+        if constexpr (PH == 1) {
+            double out;
+            if (a.op == SW_MUL) {
+                out = c * a.dmat[i + n * jj];
+            } else {
+                const double den = a.e_col[jj] * a.e_row[i] + a.beta;
+                if (den == 0.0) *a.flag = 1;
+                out = c / den;
+            }
+            core[i + n * jj] = out;
+        } else {
+            a.y[i + a.ldy * jj] = c;
+        }
+    }
+}
+
+template <int RP>
+bool launch4_rp(const SandArgs& a, cudaStream_t s) {
+    const size_t smem = sizeof(Sw4Smem<RP>) + 1024;  // + alignment slack for the swizzled boxes
+    const uint64_t n = (uint64_t)a.n;
+    CUtensorMap tg1, tg2, tm1, tm2;
+    // phase 1: F = U' -> G = U; M = X.  phase 2: F = U -> G = U'; M = the core (n x r, ld n)
+    const bool ok = encode_tmap_2d_f64(&tg1, a.u, n, n, n, SW4_KB, SW4_BI, true) &&
+                    encode_tmap_2d_f64(&tg2, a.ut, n, n, n, SW4_KB, SW4_BI, true) &&
+                    encode_tmap_2d_f64(&tm1, a.x, n, (uint64_t)a.r, (uint64_t)a.ldx, SW4_KB, RP, true) &&
+                    encode_tmap_2d_f64(&tm2, a.core_out, n, (uint64_t)a.r, n, SW4_KB, RP, true);
+    if (!ok) return false;
+    func_attr_once((const void*)sandwich4_kernel<RP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    func_attr_once((const void*)sandwich4_kernel<RP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t nkb = (a.n + SW4_BK - 1) / SW4_BK, nib = (a.n + SW4_BI - 1) / SW4_BI;
+    sandwich4_kernel<RP, 1><<<(unsigned)(nkb * nib), SW4_T, smem, s>>>(a, tg1, tm1);
+    CPHIFI_CHECK_LAUNCH();
+    sandwich4_kernel<RP, 2><<<(unsigned)(nkb * nib), SW4_T, smem, s>>>(a, tg2, tm2);
+    CPHIFI_CHECK_LAUNCH();
+    return true;
 }
 
 }  // namespace
@@ -630,7 +831,14 @@ void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s) {
 
 int64_t sandwich_scratch_doubles(int64_t n, int64_t r) {
     const int64_t rp = sandwich_rp(r);
-    return 2 * n * (rp + 8);  // v3: row-major core and X copy, pitch rp + 8 (>= v1 / v2's n x rp)
+    const int64_t nkb = (n + SW4_BK - 1) / SW4_BK, nib = (n + SW4_BI - 1) / SW4_BI;
+    const int64_t v4 = n * rp + nkb * n * rp + (nib + 1) / 2 + 1;  // core, partials, counters
+    return std::max<int64_t>(2 * n * (rp + 8), v4);  // v3: row-major core and X copy, pitch rp + 8
+}
+
+int64_t sandwich_counter_offset(int64_t n, int64_t r) {
+    const int64_t rp = sandwich_rp(r);
+    return n * rp + (n + SW4_BK - 1) / SW4_BK * n * rp;
 }
 
 void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
@@ -641,6 +849,19 @@ void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
     bool v3 = a.n >= 512 && a.n % 2 == 0 && reinterpret_cast<uintptr_t>(a.u) % 16 == 0 &&
               reinterpret_cast<uintptr_t>(a.ut) % 16 == 0 && reinterpret_cast<uintptr_t>(a.core_out) % 16 == 0;
     if (const char* e = std::getenv("CPHIFI_SANDWICH_V3")) v3 = v3 && std::atoi(e) != 0;
+    // v4 (split-K DMMA): opt-in (CPHIFI_SANDWICH_V4=1) — measured slower than v3 at config 2
+    // (15.6 + 14.2 us against 10.3 + 9.1 per phase: its CTAs sit mostly idle behind the last-arrival
+    // reduction of each row block)
+    bool v4 = false;
+    if (const char* e = std::getenv("CPHIFI_SANDWICH_V4")) v4 = v3 && a.rp >= 16 && std::atoi(e) != 0;
+    if (v4) {  // (false: a tensor map could not be encoded, e.g. X not 16-byte aligned)
+        switch (a.rp) {
+            case 16: if (launch4_rp<16>(a, s)) return; break;
+            case 32: if (launch4_rp<32>(a, s)) return; break;
+            case 64: if (launch4_rp<64>(a, s)) return; break;
+            default: break;
+        }
+    }
     if (v3) {
         switch (a.rp) {
             case 8: launch3_rp<8>(a, s); return;

@@ -107,6 +107,8 @@ struct SandArgs {
 bool sandwich_supported(int64_t n, int64_t r);
 int64_t sandwich_rp(int64_t r);
 int64_t sandwich_scratch_doubles(int64_t n, int64_t r);  // core_out size the sandwich needs
+// offset (doubles) of the split-K row-block counters in that scratch: zero them when it is allocated
+int64_t sandwich_counter_offset(int64_t n, int64_t r);
 void sandwich(SandArgs a, int num_sms, cudaStream_t s);
 void transpose_sq(const double* a, int64_t n, double* at, cudaStream_t s);
 // eigenbasis preconditioner z~ = ((r~ U_V) o D) U_V' in one launch (r <= 64)

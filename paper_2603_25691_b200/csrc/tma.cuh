@@ -66,8 +66,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // host: encode a 2-D fp64 tensor map (column-major matrix rows x cols, leading dimension ld
 // elements, box box0 x box1; out-of-bounds elements read as zero).  Returns false when the
 // layout violates the TMA constraints (16-byte aligned base and stride).
+// swizzle128: CU_TENSOR_MAP_SWIZZLE_128B (box0 * 8 <= 128 bytes; the shared-memory box 1024-byte
+// aligned: 16-byte chunk c of box row y lands at chunk c ^ (y mod 8))
 bool encode_tmap_2d_f64(CUtensorMap* map, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box0,
-                        uint32_t box1);
+                        uint32_t box1, bool swizzle128 = false);
 // 3-D fp64 tensor map over a column-major n0 x n1 x n2 array (strides n0, n0 n1), box b0 x b1 x b2
 bool encode_tmap_3d_f64(CUtensorMap* map, const double* base, uint64_t n0, uint64_t n1, uint64_t n2, uint32_t b0,
                         uint32_t b1, uint32_t b2);
