@@ -602,7 +602,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     cudaStream_t s = ctx->stream;
     const int d = o->d, k = o->k, dl = d - 2;  // dl: column of the blocked mode in idx_o
     const bool mult = o->coalesced;
-    const int64_t nw = (int64_t)ctx->num_sms * runs_warps_per_sm();
+    const int64_t nw = (int64_t)ctx->num_sms * runs_warps_per_sm(p->rp);
     int lm = -1;  // the blocked mode itself (last mode != k)
     for (int m = d - 1; m >= 0 && lm < 0; --m)
         if (m != k) lm = m;

@@ -37,21 +37,19 @@
 namespace cphifi {
 namespace {
 
-constexpr int RT = 512;               // threads per CTA
-constexpr int RNW = RT / 32;          // warps per CTA
-constexpr int CH = 64;                // plan entries per ring chunk (256 B per column: one bulk copy)
 constexpr int NCH = 4;                // ring chunks per warp
-constexpr int RING = NCH * CH;        // ring entries per column (a power of two)
 constexpr int SMEM_CAP = 226 * 1024;  // opt-in maximum minus a little static shared memory
 
-template <int RP, int DO, bool MULT>
+// CTA shape: NW warps (one CTA per SM), ring chunks of CH plan entries (CH x 4 B per column: one
+// bulk copy each)
+template <int RP, int DO, bool MULT, int NW, int CH>
 struct Lay {
     static constexpr int NCOL = DO + (MULT ? 1 : 0);
     static constexpr int NBAR = NCH + 3 + 1;       // ring chunks, A_1 slots, Xhat row
     static constexpr int WBUF = 4 * RP;            // doubles per warp: A_1 x 3, Xhat row
-    static constexpr size_t bars = 128 + 8 * (size_t)RNW * NBAR;
-    static constexpr size_t wbuf = sizeof(double) * (size_t)RNW * WBUF;
-    static constexpr size_t ring = sizeof(int32_t) * (size_t)RNW * NCH * NCOL * CH;
+    static constexpr size_t bars = 128 + 8 * (size_t)NW * NBAR;
+    static constexpr size_t wbuf = sizeof(double) * (size_t)NW * WBUF;
+    static constexpr size_t ring = sizeof(int32_t) * (size_t)NW * NCH * NCOL * CH;
     static size_t bytes(int64_t sf_doubles) { return bars + wbuf + ring + sizeof(double) * (size_t)sf_doubles; }
 };
 
@@ -77,9 +75,10 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
     }
 }
 
-template <int RP, int DO, bool MULT, int G, int B, bool PIPE>
-__global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
-    using L = Lay<RP, DO, MULT>;
+template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH>
+__global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
+    using L = Lay<RP, DO, MULT, NW, CH>;
+    constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* cbar = reinterpret_cast<uint64_t*>(smem_raw);  // CTA: staged factors
@@ -448,13 +447,13 @@ __global__ void __launch_bounds__(RT, 1) runs_kernel(const RunsArgs a) {
     }
 }
 
-template <int RP, int DO, bool MULT, int G, int B, bool PIPE>
+template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW = 16, int CH = 64>
 void launch4(const RunsArgs& a, int64_t sf, cudaStream_t s) {
-    auto kern = runs_kernel<RP, DO, MULT, G, B, PIPE>;
-    const size_t smem = Lay<RP, DO, MULT>::bytes(sf);
+    auto kern = runs_kernel<RP, DO, MULT, G, B, PIPE, NW, CH>;
+    const size_t smem = Lay<RP, DO, MULT, NW, CH>::bytes(sf);
     func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP);
-    const int grid = (a.warps + RNW - 1) / RNW;
-    kern<<<grid, RT, smem, s>>>(a);
+    const int grid = (a.warps + NW - 1) / NW;
+    kern<<<grid, NW * 32, smem, s>>>(a);
     CPHIFI_CHECK_LAUNCH();
 }
 
@@ -462,7 +461,7 @@ void launch4(const RunsArgs& a, int64_t sf, cudaStream_t s) {
 // issued before the current step's reduction (PIPE: two steps' rows live in registers), measured
 // per padded rank (profiles/prof_stream.py; config 4: 8.3 ms vs 9.4 pipelined with B = 1;
 // config 3: 4.2 ms vs 5.3 with G = 8 and 4.7 pipelined): RP = 64: G = 8, B = 2; RP = 32: G = 4,
-// B = 2; RP = 16: G = 4, B = 2, none pipelined.  CPHIFI_RUNS_LAYOUT=1 / 2 select the alternatives.
+// B = 2; RP = 16: G = 4, B = 2, none pipelined.  CPHIFI_RUNS_LAYOUT=1 / 2 / 3 select the alternatives.
 int runs_layout() {
     static const int layout = [] {
         const char* e = std::getenv("CPHIFI_RUNS_LAYOUT");
@@ -476,6 +475,7 @@ void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
     const int lay = runs_layout();
     if constexpr (RP == 64) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 1, true>(a, sf, s);
+        else if (lay == 3) launch4<RP, DO, MULT, 16, 4, false, 20, 32>(a, sf, s);
         else launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
     } else if constexpr (RP == 32) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
@@ -506,15 +506,21 @@ void launch1(const RunsArgs& a, int64_t sf, cudaStream_t s) {
 
 bool runs_supported(int64_t rp, int dother) { return (rp == 16 || rp == 32 || rp == 64) && dother >= 2 && dother <= 4; }
 
+// the CTA shape the launch picks for padded rank rp (layout 3: 24 warps, 32-entry chunks at RP 64)
+// (layout 3 trades registers for warps: G = 16 lanes per entry, 20 warps, 32-entry chunks — measured
+// 4.79 ms against 4.01 for the 16-warp G = 8 layout at config 4; 24 warps with B = 4 / 2: 5.76 / 5.08)
+static int shape_nw(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 20 : 16; }
+static int shape_ch(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 32 : 64; }
+
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {
-    const size_t ncol = (size_t)dother + (mult ? 1 : 0);
-    return 128 + 8 * (size_t)RNW * (NCH + 4) + sizeof(double) * (size_t)RNW * 4 * rp +
-           sizeof(int32_t) * (size_t)RNW * NCH * ncol * CH + sizeof(double) * (size_t)sf_doubles;
+    const size_t ncol = (size_t)dother + (mult ? 1 : 0), nw = (size_t)shape_nw(rp), ch = (size_t)shape_ch(rp);
+    return 128 + 8 * nw * (NCH + 4) + sizeof(double) * nw * 4 * rp + sizeof(int32_t) * nw * NCH * ncol * ch +
+           sizeof(double) * (size_t)sf_doubles;
 }
 
 size_t runs_smem_cap() { return SMEM_CAP; }
-int runs_warps_per_sm() { return RNW; }
-int runs_chunk() { return CH; }
+int runs_warps_per_sm(int64_t rp) { return shape_nw(rp); }
+int runs_chunk(int64_t rp) { return shape_ch(rp); }
 
 void runs_scatter_gather(const RunsArgs& a, int64_t sf_doubles, cudaStream_t s) {
     if (runs_smem_bytes(a.rp, a.dother, a.mult != nullptr, sf_doubles) > SMEM_CAP)

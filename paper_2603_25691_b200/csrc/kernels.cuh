@@ -247,8 +247,8 @@ void dense_key(const int32_t* rows, const int32_t* slot, int64_t q, int32_t dens
 bool runs_supported(int64_t rp, int dother);
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles);
 size_t runs_smem_cap();
-int runs_warps_per_sm();
-int runs_chunk();
+int runs_warps_per_sm(int64_t rp);
+int runs_chunk(int64_t rp);
 void runs_scatter_gather(const RunsArgs& a, int64_t sf_doubles, cudaStream_t s);
 // run table of a plan: run_start[j] = first entry of run j (entry l starts a run when it starts a
 // row or its first other index differs from entry l-1's); returns the number of runs (synchronous)
