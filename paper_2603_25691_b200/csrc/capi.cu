@@ -388,7 +388,7 @@ void launch_fused(cphifi_unaligned p, const FusedArgs& a) {
 
 // Phase B alone (large plans, the RHS build, test hooks): k_stream.cu when planned, else the
 // fused kernel restricted to PH_B.
-bool build_run_parts(cphifi_unaligned p, int64_t sf_all);
+bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q);
 void ensure_runs(cphifi_unaligned p);
 
 // The run kernel's parts and split-row slots, on the first use (never inside a graph capture: every
@@ -396,12 +396,41 @@ void ensure_runs(cphifi_unaligned p);
 void ensure_runs(cphifi_unaligned p) {
     if (!p->runs_pending) return;
     p->runs_pending = false;
-    if (build_run_parts(p, p->runs_sf)) {
-        int w = 0;
-        for (const auto& sp : p->parts) w = std::max(w, sp.warps);
-        p->runs_slot_a.alloc((size_t)w * p->rp);
-        p->runs_slot_b.alloc((size_t)w * p->rp);
+    const auto t0 = std::chrono::steady_clock::now();
+    cphifi_obs o = p->obs;
+    // the plan's q-pass plan for this padded rank, shared by every subproblem on the plan; the key
+    // also carries the tuning knobs the build reads
+    std::string key = std::to_string(p->rp) + "/" + std::to_string(p->runs_sf);
+    for (const char* v : {"CPHIFI_DENSE_MIN", "CPHIFI_DENSE_MAX_GB", "CPHIFI_RUNS_RUNCOST", "CPHIFI_RUNS_LAYOUT"}) {
+        const char* e = std::getenv(v);
+        key += std::string("/") + (e ? e : "-");
     }
+    bool built = false;
+    {
+        std::lock_guard<std::mutex> lk(o->qp_mu);
+        std::shared_ptr<QpassPlan>& slot = o->qp_cache[key];
+        if (!slot) {
+            auto Q = std::make_shared<QpassPlan>();
+            if (!build_run_parts(p, p->runs_sf, *Q)) *Q = QpassPlan();
+            for (const auto& sp : Q->parts) Q->max_warps = std::max(Q->max_warps, sp.warps);
+            slot = Q;
+            built = true;
+        }
+        p->qp = slot;
+    }
+    const QpassPlan& Q = *p->qp;
+    if (!Q.parts.empty()) {  // this subproblem's scratch
+        p->runs_slot_a.alloc((size_t)Q.max_warps * p->rp);
+        p->runs_slot_b.alloc((size_t)Q.max_warps * p->rp);
+    }
+    if (Q.dense_nd > 0) {
+        p->dense_partial.alloc((size_t)Q.dense_nd * (Q.dense_n1p / dense_rows_block_a()) * p->rp);
+        p->dense_cnt.alloc(Q.dense_nd);
+        CPHIFI_CUDA(cudaMemsetAsync(p->dense_cnt.get(), 0, sizeof(unsigned) * Q.dense_nd, o->ctx->stream));
+    }
+    if (std::getenv("CPHIFI_SOLVE_TIMING"))  // developer: host time of the build (or the cache hit)
+        std::fprintf(stderr, "cphifi: q-pass plan %s in %.3f ms\n", built ? "built" : "shared",
+                     1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
 }
 
 // The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
@@ -410,12 +439,13 @@ void ensure_runs(cphifi_unaligned p) {
 void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
     a.phases = PH_B;
     if (!a.weights) ensure_runs(p);
-    if (!p->parts.empty() && !a.weights) {
+    if (p->qp && !p->qp->parts.empty() && !a.weights) {
+        const QpassPlan& Q = *p->qp;
         cudaStream_t s = p->obs->ctx->stream;
         const int dl = p->obs->d - 2;  // the blocked (last) other mode's column / packed factor
-        const bool acc = p->parts.size() > 1;
+        const bool acc = Q.parts.size() > 1;
         if (acc) CPHIFI_CUDA(cudaMemsetAsync(a.yhat_rm, 0, sizeof(double) * p->n * p->rp, s));
-        for (const StreamPart& sp : p->parts) {
+        for (const StreamPart& sp : Q.parts) {
             if (sp.q == 0) continue;
             RunsArgs b;
             b.rp = p->rp;
@@ -448,16 +478,16 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
             CPHIFI_CUDA(cudaEventRecord(g_dense_event, s));
             g_dense_recorded = true;
         }
-        if (p->dense_nd > 0) {  // the dense rows (no entries in any part): written, not accumulated
+        if (Q.dense_nd > 0) {  // the dense rows (no entries in any part): written, not accumulated
             DenseRowsArgs dr;
             dr.rp = p->rp;
-            dr.n1 = p->dense_n1;
-            dr.n2 = p->dense_n2;
-            dr.n1p = p->dense_n1p;
-            dr.n2p = p->dense_n2p;
-            dr.nd = p->dense_nd;
-            dr.rows = p->dense_rows.get();
-            dr.w = p->dense_w.get();
+            dr.n1 = Q.dense_n1;
+            dr.n2 = Q.dense_n2;
+            dr.n1p = Q.dense_n1p;
+            dr.n2p = Q.dense_n2p;
+            dr.nd = Q.dense_nd;
+            dr.rows = Q.dense_rows.get();
+            dr.w = Q.dense_w.get();
             dr.a1 = a.fac + a.fac_off[0];
             dr.a2 = a.fac + a.fac_off[1];
             dr.xhat_rm = a.xhat_rm;
@@ -548,12 +578,12 @@ void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_
 // of all such rows fit CPHIFI_DENSE_MAX_GB (default 16 GB, int32 per cell).  Picks the rows, builds
 // their multiplicity grids and returns the per-row slot table (-1: sparse) on the device, or an empty
 // buffer when no row qualifies.
-DevBuf<int32_t> build_dense_rows(cphifi_unaligned p, const int32_t* rows_of_entry) {
+DevBuf<int32_t> build_dense_rows(cphifi_unaligned p, const int32_t* rows_of_entry, QpassPlan& Q) {
     cphifi_obs o = p->obs;
     cphifi_ctx ctx = o->ctx;
     cudaStream_t s = ctx->stream;
     DevBuf<int32_t> slot;
-    p->dense_nd = 0;
+    Q.dense_nd = 0;
     double dmin = 0.3, max_gb = 16.0;
     if (const char* e = std::getenv("CPHIFI_DENSE_MIN")) dmin = std::atof(e);
     if (const char* e = std::getenv("CPHIFI_DENSE_MAX_GB")) max_gb = std::atof(e);
@@ -576,27 +606,24 @@ DevBuf<int32_t> build_dense_rows(cphifi_unaligned p, const int32_t* rows_of_entr
         }
     if (drows.empty()) return slot;
     const int nd = (int)drows.size();
-    p->dense_nd = nd;
-    p->dense_n1 = n1;
-    p->dense_n2 = n2;
-    p->dense_n1p = n1p;
-    p->dense_n2p = n2p;
-    p->dense_rows.alloc(nd);
-    h2d(p->dense_rows.get(), drows.data(), sizeof(int32_t) * nd, s);
+    Q.dense_nd = nd;
+    Q.dense_n1 = n1;
+    Q.dense_n2 = n2;
+    Q.dense_n1p = n1p;
+    Q.dense_n2p = n2p;
+    Q.dense_rows.alloc(nd);
+    h2d(Q.dense_rows.get(), drows.data(), sizeof(int32_t) * nd, s);
     slot.alloc(p->n);
     h2d(slot.get(), slot_h.data(), sizeof(int32_t) * p->n, s);
-    p->dense_w.alloc((size_t)nd * n1p * n2p);
-    CPHIFI_CUDA(cudaMemsetAsync(p->dense_w.get(), 0, sizeof(int32_t) * (size_t)nd * n1p * n2p, s));
+    Q.dense_w.alloc((size_t)nd * n1p * n2p);
+    CPHIFI_CUDA(cudaMemsetAsync(Q.dense_w.get(), 0, sizeof(int32_t) * (size_t)nd * n1p * n2p, s));
     dense_grid_build(o->idx_o.get(), o->ldq, o->coalesced ? o->mult.get() : nullptr, rows_of_entry, slot.get(),
-                     o->q_local, n1p, n2p, p->dense_w.get(), s);
-    p->dense_partial.alloc((size_t)nd * (n1p / ba) * p->rp);
-    p->dense_cnt.alloc(nd);
-    CPHIFI_CUDA(cudaMemsetAsync(p->dense_cnt.get(), 0, sizeof(unsigned) * nd, s));
+                     o->q_local, n1p, n2p, Q.dense_w.get(), s);
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
     return slot;
 }
 
-bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
+bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
     cphifi_obs o = p->obs;
     cphifi_ctx ctx = o->ctx;
     cudaStream_t s = ctx->stream;
@@ -609,8 +636,8 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     const int64_t nl = o->shape[lm], rp = p->rp, q = o->q_local;
     DevBuf<int32_t> rows(std::max<int64_t>(q, 1));
     row_of_entries(o->row_ptr.get(), p->n, q, rows.get(), s);
-    const DevBuf<int32_t> dslot = build_dense_rows(p, rows.get());
-    const bool dense = p->dense_nd > 0;
+    const DevBuf<int32_t> dslot = build_dense_rows(p, rows.get(), Q);
+    const bool dense = Q.dense_nd > 0;
     const bool fits = runs_smem_bytes(rp, d - 1, mult, sf_all) <= runs_smem_cap();
     if (fits && !dense) {  // one part: the plan itself
         std::vector<StreamPart> parts(1);
@@ -623,7 +650,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
         sp.row_ptr = o->row_ptr.get();
         sp.sf = sf_all;
         finish_part(p, sp, rows.get(), nw);
-        p->parts = std::move(parts);
+        Q.parts = std::move(parts);
         return true;
     }
     const int64_t rest = sf_all - nl * rp;  // staged doubles of the other per-observation modes
@@ -631,7 +658,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     for (int64_t b = nl; b >= 8 && br == 0; b -= 8)
         if (runs_smem_bytes(rp, d - 1, mult, rest + b * rp) <= runs_smem_cap()) br = b;
     if (br < 8 && !fits) {
-        p->dense_nd = 0;  // no parts: the stream kernel takes the whole plan
+        Q.dense_nd = 0;  // no parts: the stream kernel takes the whole plan
         return false;
     }
     const int H = (int)((nl + br - 1) / br);
@@ -639,24 +666,25 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
     // part key = block of the last other mode; the dense rows' entries get key H (dropped)
     DevBuf<int32_t> key(std::max<int64_t>(q, 1)), key_s(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
         perm(std::max<int64_t>(q, 1)), rows_h(std::max<int64_t>(q, 1));
-    DevBuf<int64_t> bounds(H + 1);
     block_key(o->idx_o.get() + (int64_t)dl * o->ldq, q, (int32_t)br, key.get(), s);
+    // the dense rows' entries go to buckets H + block (their own parts, for the row-Gram build)
     if (dense) dense_key(rows.get(), dslot.get(), q, (int32_t)H, key.get(), s);
+    const int nb = dense ? 2 * H : H;
     iota32(perm_in.get(), q, s);
     int bits = 1;
-    while ((1 << bits) < H + 1) ++bits;
+    while ((1 << bits) < nb) ++bits;
     if (q > 0) {
         const size_t tb = radix_sort_pairs_bytes(q, bits);
         DevBuf<unsigned char> tmp(tb);
         radix_sort_pairs(tmp.get(), tb, key.get(), key_s.get(), perm_in.get(), perm.get(), q, bits, s);
     }
-    csr_from_sorted(key_s.get(), q, H, bounds.get(), s);  // bounds[h] = first entry of part h; [H]: dense
-    std::vector<int64_t> hb(H + 1);
-    d2h_sync(hb.data(), bounds.get(), sizeof(int64_t) * (H + 1), s);
-    std::vector<StreamPart> parts(H);
-    for (int h = 0; h < H; ++h) {
-        StreamPart& sp = parts[h];
-        const int64_t lo = hb[h], cnt = hb[h + 1] - hb[h];
+    DevBuf<int64_t> bnd(nb + 1);
+    csr_from_sorted(key_s.get(), q, nb, bnd.get(), s);  // bnd[b] = first entry of bucket b
+    std::vector<int64_t> hb(nb + 1);
+    d2h_sync(hb.data(), bnd.get(), sizeof(int64_t) * (nb + 1), s);
+    auto make_part = [&](StreamPart& sp, int b, bool runs) {
+        const int h = b % H;
+        const int64_t lo = hb[b], cnt = hb[b + 1] - hb[b];
         sp.q = cnt;
         sp.ldq = (cnt + 3) / 4 * 4;
         sp.row_lo = h * br;
@@ -677,35 +705,68 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all) {
         sp.row_ptr_own.alloc(p->n + 1);
         csr_from_sorted(rows_h.get(), cnt, p->n, sp.row_ptr_own.get(), s);
         sp.row_ptr = sp.row_ptr_own.get();
-        finish_part(p, sp, rows_h.get(), nw);
-    }
-    p->parts = std::move(parts);
+        if (runs) finish_part(p, sp, rows_h.get(), nw);
+        else CPHIFI_CUDA(cudaStreamSynchronize(s));  // rows_h is reused by the next part
+    };
+    std::vector<StreamPart> parts(H), dparts(dense ? H : 0);
+    for (int h = 0; h < H; ++h) make_part(parts[h], h, true);
+    for (int h = 0; h < (dense ? H : 0); ++h) make_part(dparts[h], H + h, false);
+    Q.parts = std::move(parts);
+    Q.dense_parts = std::move(dparts);
     return true;
 }
 
-// The warp-specialised row-Gram build (k_gramws.cu) over the run kernel's parts (their factor
-// blocks fit shared memory): one launch per part adding into G (zeroed by the caller), each over a
-// row-aligned CTA partition of the part.  False when it does not apply (no parts, rank or order
-// out of range, staging too large): the caller falls back to the single-pass builds of k_gram.cu.
-// Opt-in (CPHIFI_GRAM_WS=1): measured slower than the single-pass builds of k_gram.cu — config 4
-// 71.6 vs 61.8 ms, config 3 26.9 vs 24.6 ms (tensor pipe 32 %: the producers' global index / factor
-// loads and the per-batch handshakes of 32-entry batches) — and its parts cost ~0.1 s to build.
+// The row-Gram build over the q-pass plan's factor-block parts (the run kernel's parts plus the dense
+// rows' parts: every entry once), one launch per part adding into G (zeroed by the caller):
+//  * opt-in (CPHIFI_GRAM3_PARTS=1), 3-way plans whose factors do not fit shared memory (config 4:
+//    2 x 256 KB): the register-fragment build (k_gram3.cu) with the part's block staged and mode 0
+//    through L1, over an equal-count unit partition of the part (cached on the part);
+//  * opt-in (CPHIFI_GRAM_WS=1): the warp-specialised build (k_gramws.cu) — measured slower than the
+//    single-pass builds of k_gram.cu: config 4 71.6 vs 61.8 ms, config 3 26.9 vs 24.6 ms (tensor
+//    pipe 32 %: the producers' global loads and the handshakes of 32-entry batches).
+// False when neither applies (no parts, rank or order out of range, staging too large): the caller
+// falls back to the single-pass builds.
 bool gram_build_parts(cphifi_unaligned p) {
-    bool on = false;
-    if (const char* e = std::getenv("CPHIFI_GRAM_WS")) on = std::atoi(e) != 0;
+    bool ws = false;
+    if (const char* e = std::getenv("CPHIFI_GRAM_WS")) ws = std::atoi(e) != 0;
+    bool v3 = false;  // opt-in: measured 90 ms at config 4 against 62 for k_gram.cu's batched build (mode 0
+                      // through L1 per entry, four warps per entry stream): CPHIFI_GRAM3_PARTS=1
+    if (const char* e = std::getenv("CPHIFI_GRAM3_PARTS")) v3 = !ws && p->obs->d == 3 && std::atoi(e) != 0;
     cphifi_obs o = p->obs;
-    if (!on || !gram_ws_supported(p->rp, o->d - 1)) return false;
+    if (ws && !gram_ws_supported(p->rp, o->d - 1)) return false;
+    if (!ws && !v3) return false;
+    if (v3) {  // only where the whole-plan staging of k_gram3.cu does not fit
+        GramArgs probe;
+        probe.rp = p->rp;
+        probe.dother = o->d - 1;
+        probe.fac = p->fac.get();
+        for (int m = 0; m < o->d - 1; ++m) probe.fac_off[m] = p->fac_off[m];
+        probe.fac_total = (int64_t)p->fac.n;
+        // whole-plan staging fits: ensure_gram's single launch instead
+        if (gram3_stage(p->rp, o->d - 1, probe) == 2) return false;
+        if (!(p->rp == 16 || p->rp == 32 || p->rp == 64) || reinterpret_cast<uintptr_t>(p->fac.get()) % 16) return false;
+        for (int m = 0; m < o->d - 1; ++m)
+            if (p->fac_off[m] % 2) return false;
+    }
     ensure_runs(p);
-    if (p->parts.empty() || p->dense_nd > 0) return false;  // the parts leave out the dense rows
-    for (const auto& sp : p->parts)
-        if (gram_ws_smem_bytes(p->rp, sp.sf) > runs_smem_cap()) return false;
+    if (!p->qp || p->qp->parts.empty()) return false;
+    QpassPlan& Q = *p->qp;
+    if (ws && Q.dense_nd > 0) return false;  // (the warp-specialised path: run-kernel parts only)
+    std::vector<StreamPart*> all;
+    for (auto& sp : Q.parts) all.push_back(&sp);
+    for (auto& sp : Q.dense_parts) all.push_back(&sp);
+    for (const StreamPart* sp : all) {
+        if (ws && gram_ws_smem_bytes(p->rp, sp->sf) > runs_smem_cap()) return false;
+        if (v3 && sizeof(double) * (size_t)sp->sf > 220 * 1024) return false;
+    }
     cphifi_ctx ctx = o->ctx;
     cudaStream_t s = ctx->stream;
     const int dl = o->d - 2;
     const size_t rp2 = (size_t)p->rp * p->rp;
+    const int units = v3 ? ctx->num_sms * gram3_units_per_sm(p->rp) : ctx->num_sms;
     DevBuf<unsigned> rowcnt(p->n);
     CPHIFI_CUDA(cudaMemsetAsync(rowcnt.get(), 0, sizeof(unsigned) * p->n, s));
-    DevBuf<double> slot_a((size_t)ctx->num_sms * rp2), slot_b((size_t)ctx->num_sms * rp2);
+    DevBuf<double> slot_a((size_t)units * rp2), slot_b((size_t)units * rp2);
     const bool timing = std::getenv("CPHIFI_GRAM_TIMING") != nullptr;  // developer: device time of the build
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing) {
@@ -713,48 +774,60 @@ bool gram_build_parts(cphifi_unaligned p) {
         CPHIFI_CUDA(cudaEventCreate(&e1));
         CPHIFI_CUDA(cudaEventRecord(e0, s));
     }
-    for (const StreamPart& sp : p->parts) {
-        if (sp.q == 0) continue;
-        std::vector<int64_t> rp_host(p->n + 1);
-        d2h_sync(rp_host.data(), sp.row_ptr, sizeof(int64_t) * (p->n + 1), s);
-        PartitionPlan plan;
-        plan_partition(rp_host, ctx->num_sms, ctx->num_sms, plan);
-        DevBuf<int64_t> cta_beg(plan.beg.size()), cta_rows(plan.rows.size());
-        DevBuf<int32_t> rfc(p->n), rnc(p->n);
-        h2d(cta_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
-        h2d(cta_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
-        h2d(rfc.get(), plan.row_first_cta.data(), sizeof(int32_t) * p->n, s);
-        h2d(rnc.get(), plan.row_ncta.data(), sizeof(int32_t) * p->n, s);
+    for (StreamPart* sp : all) {
+        if (sp->q == 0) continue;
+        {  // the part's unit partition, built once and kept with the (shared) plan
+            std::lock_guard<std::mutex> lk(o->qp_mu);
+            if (sp->g_units != units) {
+                std::vector<int64_t> rp_host(p->n + 1);
+                d2h_sync(rp_host.data(), sp->row_ptr, sizeof(int64_t) * (p->n + 1), s);
+                PartitionPlan plan;
+                if (v3) plan_partition(rp_host, units, units, plan, units);
+                else plan_partition(rp_host, units, units, plan);
+                sp->g_beg.alloc(plan.beg.size());
+                sp->g_rows.alloc(plan.rows.size());
+                sp->g_rfc.alloc(p->n);
+                sp->g_rnc.alloc(p->n);
+                h2d(sp->g_beg.get(), plan.beg.data(), sizeof(int64_t) * plan.beg.size(), s);
+                h2d(sp->g_rows.get(), plan.rows.data(), sizeof(int64_t) * plan.rows.size(), s);
+                h2d(sp->g_rfc.get(), plan.row_first_cta.data(), sizeof(int32_t) * p->n, s);
+                h2d(sp->g_rnc.get(), plan.row_ncta.data(), sizeof(int32_t) * p->n, s);
+                CPHIFI_CUDA(cudaStreamSynchronize(s));  // host vectors released
+                sp->g_units = units;  // (the launch takes the partition's own count, g_beg.n - 1)
+            }
+        }
         GramArgs g;
         g.n = p->n;
         g.rp = p->rp;
-        g.q = sp.ldq;
+        g.q = sp->ldq;
         g.dother = o->d - 1;
-        g.row_ptr = sp.row_ptr;
-        g.idx = sp.idx;
+        g.row_ptr = sp->row_ptr;
+        g.idx = sp->idx;
         g.fac = p->fac.get();
         for (int m = 0; m < o->d - 1; ++m) g.fac_off[m] = p->fac_off[m];
-        g.fac_off[dl] = p->fac_off[dl] + sp.row_lo * p->rp;
-        g.fac_total = g.fac_off[dl] + sp.rows * p->rp;
-        g.mult = sp.mult;
-        g.cta_beg = cta_beg.get();
-        g.cta_rows = cta_rows.get();
-        g.row_first_cta = rfc.get();
-        g.row_ncta = rnc.get();
+        g.fac_off[dl] = p->fac_off[dl] + sp->row_lo * p->rp;
+        g.fac_total = g.fac_off[dl] + sp->rows * p->rp;
+        g.mult = sp->mult;
+        g.cta_beg = sp->g_beg.get();
+        g.cta_rows = sp->g_rows.get();
+        g.row_first_cta = sp->g_rfc.get();
+        g.row_ncta = sp->g_rnc.get();
         g.rowcnt = rowcnt.get();
         g.slot_a = slot_a.get();
         g.slot_b = slot_b.get();
         g.g = p->gram.get();
-        g.accumulate = 1;  // G was zeroed: every part adds
-        gram_build_ws(g, plan.ctas, sp.sf, s);
-        CPHIFI_CUDA(cudaStreamSynchronize(s));  // the partition buffers are released per part
+        g.accumulate = 1;  // G was zeroed: every part adds, in part order
+        if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), 1, s);
+        else gram_build_ws(g, (int)(sp->g_beg.n - 1), sp->sf, s);
     }
+    CPHIFI_CUDA(cudaStreamSynchronize(s));  // the slots / counters are released on return
     if (timing) {
         CPHIFI_CUDA(cudaEventRecord(e1, s));
         CPHIFI_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;
         CPHIFI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        std::fprintf(stderr, "cphifi: gram build (warp-specialised, %zu parts) %.3f ms on device\n", p->parts.size(), ms);
+        std::fprintf(stderr, "cphifi: gram build (%s, %zu parts) %.3f ms on device\n", v3 ? "v3 over parts" : "warp-specialised",
+                     all.size(), ms);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
     }
@@ -783,7 +856,8 @@ void ensure_gram(cphifi_unaligned p) {
     probe.fac_total = (int64_t)p->fac.n;
     // the register-fragment build (k_gram3.cu) over an equal-count partition of gram3_units_per_sm
     // units per SM; else the single-pass builds of k_gram.cu over their row-aligned partition
-    bool v3 = gram3_supported(p->rp, o->d - 1, probe);
+    const int stage3 = gram3_stage(p->rp, o->d - 1, probe);
+    bool v3 = stage3 == 2;  // (stage 1 — modes 1.. staged — needs factor-block parts)
     if (const char* e = std::getenv("CPHIFI_GRAM3")) v3 = v3 && std::atoi(e) != 0;
     int per_sm = v3 ? gram3_units_per_sm(p->rp) : gram_build_occupancy(probe);
     if (const char* e = std::getenv("CPHIFI_GRAM_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
@@ -832,7 +906,7 @@ void ensure_gram(cphifi_unaligned p) {
         CPHIFI_CUDA(cudaEventRecord(e0, s));
     }
     if (o->q_local > 0) {
-        if (v3) gram3_build(g, grid, s);
+        if (v3) gram3_build(g, grid, stage3, s);
         else gram_build(g, grid, s);
     }
     if (timing) CPHIFI_CUDA(cudaEventRecord(e1, s));
@@ -2360,13 +2434,15 @@ int cphifi_unaligned_qpass_plan(cphifi_unaligned p, int64_t* info, int count) {
         if (count < 1) throw_invalid("cphifi_unaligned_qpass_plan: count must be positive");
         DeviceGuard dg(p->obs->ctx->device);
         ensure_runs(p);
+        static const QpassPlan none;
+        const QpassPlan& Q = p->qp ? *p->qp : none;
         int64_t q = 0, dr = 0;
-        for (const auto& sp : p->parts) {
+        for (const auto& sp : Q.parts) {
             q += sp.q;
             dr += sp.draws;
         }
-        const int64_t v[6] = {(int64_t)p->parts.size(), p->dense_nd, p->parts.empty() ? p->obs->q_local : q,
-                              p->parts.empty() ? -1 : dr, p->dense_n1p, p->dense_n2p};
+        const int64_t v[6] = {(int64_t)Q.parts.size(), Q.dense_nd, Q.parts.empty() ? p->obs->q_local : q,
+                              Q.parts.empty() ? -1 : dr, Q.dense_n1p, Q.dense_n2p};
         for (int i = 0; i < count; ++i) info[i] = i < 6 ? v[i] : 0;
     });
 }

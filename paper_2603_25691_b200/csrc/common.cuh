@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cmath>
 #include <condition_variable>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -154,22 +156,6 @@ struct cphifi_mode_s {
     std::mutex mu_lock;
 };
 
-struct cphifi_obs_s {
-    cphifi_ctx ctx = nullptr;
-    int d = 0, k = 0;
-    std::vector<int64_t> shape;
-    int64_t q_total = 0;  // all shards
-    int64_t q_local = 0;  // this shard
-    double density = 0.0; // q_total / prod(shape)  (observations.hpp:58-60)
-    bool lex = false;     // plan order is lexicographic (i_k, other modes ascending)
-    cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
-    cphifi::DevBuf<int32_t> idx_o;    // (d-1) columns of stride ldq, other modes ascending, sorted by i_k
-    int64_t ldq = 0;                  // idx_o column stride: q_local rounded up to a multiple of 4
-    cphifi::DevBuf<double> values;    // q_local, sorted (coalesced: summed over duplicates)
-    cphifi::DevBuf<int32_t> mult;     // q_local multiplicities (coalesced plans only)
-    bool coalesced = false;
-};
-
 // One part of the operator's q-pass for the run kernel (k_runs.cu): the plan entries whose LAST
 // other-mode index falls in rows [row_lo, row_lo + rows) of that factor (all of them when the
 // whole factor fits shared memory: the part then aliases the plan), in plan order, that index
@@ -189,6 +175,41 @@ struct StreamPart {
     int warps = 0;                       // equal-count warp ranges
     cphifi::DevBuf<int64_t> warp_beg, warp_rows;
     cphifi::DevBuf<int32_t> row_first_w, row_nw;
+    int g_units = 0;                     // the row-Gram build's equal-count units (built on first use)
+    cphifi::DevBuf<int64_t> g_beg, g_rows;
+    cphifi::DevBuf<int32_t> g_rfc, g_rnc;
+};
+
+// The stream operator's q-pass plan for one padded rank (capi.cu build_run_parts): the run kernel's
+// parts over the sparse rows, the dense rows' multiplicity grids (k_dense_rows.cu), and the dense
+// rows' entries cut into the same factor blocks (the row-Gram build over parts).  It depends only on
+// the observation plan and the padded rank, so every subproblem built on the same plan shares it
+// (cphifi_obs_s::qp_cache): an ALS sweep's fresh subproblems reuse it.
+struct QpassPlan {
+    std::vector<StreamPart> parts;        // non-empty: the q-pass is the run kernel over these
+    std::vector<StreamPart> dense_parts;  // the dense rows' entries, block h in dense_parts[h]
+    int dense_nd = 0;                     // dense rows, 0: none
+    int64_t dense_n1 = 0, dense_n2 = 0, dense_n1p = 0, dense_n2p = 0;
+    cphifi::DevBuf<int32_t> dense_rows, dense_w;  // their row indices; nd x n1p x n2p multiplicities
+    int max_warps = 0;                    // over the parts
+};
+
+struct cphifi_obs_s {
+    cphifi_ctx ctx = nullptr;
+    int d = 0, k = 0;
+    std::vector<int64_t> shape;
+    int64_t q_total = 0;  // all shards
+    int64_t q_local = 0;  // this shard
+    double density = 0.0; // q_total / prod(shape)  (observations.hpp:58-60)
+    bool lex = false;     // plan order is lexicographic (i_k, other modes ascending)
+    cphifi::DevBuf<int64_t> row_ptr;  // n_k + 1, local CSR over sorted i_k
+    cphifi::DevBuf<int32_t> idx_o;    // (d-1) columns of stride ldq, other modes ascending, sorted by i_k
+    int64_t ldq = 0;                  // idx_o column stride: q_local rounded up to a multiple of 4
+    cphifi::DevBuf<double> values;    // q_local, sorted (coalesced: summed over duplicates)
+    cphifi::DevBuf<int32_t> mult;     // q_local multiplicities (coalesced plans only)
+    bool coalesced = false;
+    std::mutex qp_mu;                 // q-pass plans by padded rank (and the tuning knobs they read)
+    std::map<std::string, std::shared_ptr<QpassPlan>> qp_cache;
 };
 
 struct cphifi_unaligned_s {
@@ -216,12 +237,9 @@ struct cphifi_unaligned_s {
     bool prefetch = false;        // X and K columns staged in shared memory (small n * r)
     bool stream = false;          // phase B runs k_stream.cu (large plans) instead of k_fused.cu
     int64_t stream_sf = 0;        // doubles of per-observation factors k_stream.cu stages in smem (0: L1)
-    std::vector<StreamPart> parts;  // non-empty: the operator's q-pass is the run kernel over these parts
+    std::shared_ptr<QpassPlan> qp;  // the plan's shared q-pass plan (ensure_runs); null: not built
     cphifi::DevBuf<double> runs_slot_a, runs_slot_b;  // warps x rp: split-row partials of the run kernel
-    int dense_nd = 0;             // dense rows of the run kernel's plan (k_dense_rows.cu), 0: none
-    int64_t dense_n1 = 0, dense_n2 = 0, dense_n1p = 0, dense_n2p = 0;
-    cphifi::DevBuf<int32_t> dense_rows, dense_w;  // their row indices; nd x n1p x n2p multiplicities
-    cphifi::DevBuf<double> dense_partial;         // per-task partial rows
+    cphifi::DevBuf<double> dense_partial;         // per-task partial rows of the dense-rows kernel
     cphifi::DevBuf<unsigned> dense_cnt;           // per-row arrival counters
     bool runs_pending = false;    // parts not built yet (ensure_runs)
     int64_t runs_sf = 0;          // staged per-observation factor doubles of the whole plan

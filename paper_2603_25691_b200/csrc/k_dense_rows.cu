@@ -255,9 +255,9 @@ __global__ void sum_i32_kernel(const int32_t* v, int64_t q, unsigned long long* 
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
-__global__ void dense_key_kernel(const int32_t* rows, const int32_t* slot, int64_t q, int32_t dense_key, int32_t* key) {
+__global__ void dense_key_kernel(const int32_t* rows, const int32_t* slot, int64_t q, int32_t offset, int32_t* key) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < q; l += (int64_t)gridDim.x * blockDim.x)
-        if (slot[rows[l]] >= 0) key[l] = dense_key;
+        if (slot[rows[l]] >= 0) key[l] += offset;
 }
 
 }  // namespace

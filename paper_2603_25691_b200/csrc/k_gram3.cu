@@ -60,8 +60,11 @@ __host__ __device__ constexpr int pair_index(int ti, int tj) {
     return ti * NT - ti * (ti - 1) / 2 + (tj - ti);
 }
 
-template <int RP, int DO, int TW, bool SF>
+// STAGE: 2 = every factor staged in shared memory; 1 = modes 1.. staged (a factor-block part: mode 0,
+// constant along the plan's runs, read through L1); 0 = none staged
+template <int RP, int DO, int TW, int STAGE>
 __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int units) {
+    constexpr bool SF = STAGE > 0;
     using C = G3<RP, TW>;
     constexpr int NT = C::NT, TPW = C::TPW;
     extern __shared__ __align__(16) double g3s[];
@@ -78,11 +81,13 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
     auto sw = [](int64_t grow) -> int {
         return CPL == 2 ? (int)((grow & 1) << 2) : CPL == 1 ? (int)((grow & 3) << 1) : 0;
     };
+    const int64_t sbeg = STAGE == 2 ? 0 : a.fac_off[1];  // first staged double (a row boundary)
     if constexpr (SF) {
-        for (int64_t e = tid; e < a.fac_total / 2; e += G3T) {
+        const double2* src = reinterpret_cast<const double2*>(a.fac + sbeg);
+        for (int64_t e = tid; e < (a.fac_total - sbeg) / 2; e += G3T) {
             const int jj = (int)(e % (RP / 2));
             const int64_t grow = e / (RP / 2);
-            reinterpret_cast<double2*>(g3s)[e] = __ldg(reinterpret_cast<const double2*>(a.fac) + (e - jj) + (jj ^ sw(grow)));
+            reinterpret_cast<double2*>(g3s)[e] = __ldg(src + (e - jj) + (jj ^ sw(grow)));
         }
     }
     __syncthreads();  // the only CTA-wide barrier: teams are independent from here on
@@ -114,8 +119,9 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int ii = NT * g + ti, jj = NT * (2 * kq + h) + tj;
-                    dst[ii * RP + jj] = acc[uu / TW][h];
-                    if (ti != tj) dst[jj * RP + ii] = acc[uu / TW][h];
+                    const double v = acc[uu / TW][h] + (a.accumulate && nu == 1 ? dst[ii * RP + jj] : 0.0);
+                    dst[ii * RP + jj] = v;
+                    if (ti != tj) dst[jj * RP + ii] = v;
                 }
             }
 #pragma unroll
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
                     double s = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
                                       : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
                     for (int v = u0 + 1; v < u0 + nu; ++v) s += __ldcg(a.slot_a + (int64_t)v * RP * RP + e);
-                    a.g[rr * RP * RP + e] = s;
+                    a.g[rr * RP * RP + e] = a.accumulate ? a.g[rr * RP * RP + e] + s : s;
                 }
             }
         }
@@ -165,8 +171,8 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
 #pragma unroll
     for (int m = 0; m < DO; ++m) {
         gbase[m] = a.fac + a.fac_off[m];
-        sbase[m] = (uint32_t)__cvta_generic_to_shared(g3s) + (uint32_t)(a.fac_off[m] * 8);
-        opar[m] = (int)((a.fac_off[m] / RP) & 3);
+        sbase[m] = (uint32_t)__cvta_generic_to_shared(g3s) + (uint32_t)((a.fac_off[m] - sbeg) * 8);
+        opar[m] = (int)(((a.fac_off[m] - sbeg) / RP) & 3);
     }
     int rb = (int)(row_beg - p0), re = (int)(min(row_end, end) - p0);  // current row, relative
 
@@ -178,12 +184,14 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
         wm = __shfl_sync(0xffffffffu, cur[DO], src);  // 0 outside [beg, end)
 #pragma unroll
         for (int m = 0; m < DO; ++m) {
-            const int swm = SF ? sw(opar[m] + ix[m]) : 0;
+            const bool st = STAGE == 2 || (STAGE == 1 && m >= 1);  // this mode in shared memory
+            const int swm = st ? sw(opar[m] + ix[m]) : 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                const int lc = CPL * g + (SF ? ((c + kq) & (CPL - 1)) : c);  // logical chunk: columns 2 lc, 2 lc + 1
+                // logical chunk (columns 2 lc, 2 lc + 1), every mode in the same kq-rotated order
+                const int lc = CPL * g + (SF ? ((c + kq) & (CPL - 1)) : c);
                 double2 f;
-                if constexpr (SF) {
+                if (st) {
                     const uint32_t ad = sbase[m] + (uint32_t)ix[m] * (RP * 8) + (uint32_t)((lc ^ swm) * 16);
                     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f.x), "=d"(f.y) : "r"(ad));
                 } else {
@@ -288,42 +296,47 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
 }
 
 template <int RP, int DO, int TW>
-void launch_g3(const GramArgs& a, int units, cudaStream_t s) {
+void launch_g3(const GramArgs& a, int units, int stage, cudaStream_t s) {
     using C = G3<RP, TW>;
-    const size_t fbytes = sizeof(double) * (size_t)a.fac_total;
-    const bool sf = fbytes <= 220 * 1024 && a.fac_total % 2 == 0;
     const int grid = (units + C::TEAMS - 1) / C::TEAMS;
-    if (sf) {
-        auto kern = gram3_kernel<RP, DO, TW, true>;
+    const size_t fbytes = sizeof(double) * (size_t)(a.fac_total - (stage == 2 ? 0 : a.fac_off[1]));
+    if (stage == 2) {
+        auto kern = gram3_kernel<RP, DO, TW, 2>;
         func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         kern<<<grid, G3T, fbytes, s>>>(a, units);
-    } else {
-        gram3_kernel<RP, DO, TW, false><<<grid, G3T, 0, s>>>(a, units);
+    } else if (stage == 1) {
+        auto kern = gram3_kernel<RP, DO, TW, 1>;
+        func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        kern<<<grid, G3T, fbytes, s>>>(a, units);
     }
     CPHIFI_CHECK_LAUNCH();
 }
 
 template <int RP, int TW>
-void launch_g3_do(const GramArgs& a, int units, cudaStream_t s) {
+void launch_g3_do(const GramArgs& a, int units, int stage, cudaStream_t s) {
     switch (a.dother) {
-        case 2: launch_g3<RP, 2, TW>(a, units, s); break;
-        case 3: launch_g3<RP, 3, TW>(a, units, s); break;
-        case 4: launch_g3<RP, 4, TW>(a, units, s); break;
+        case 2: launch_g3<RP, 2, TW>(a, units, stage, s); break;
+        case 3: launch_g3<RP, 3, TW>(a, units, stage, s); break;
+        case 4: launch_g3<RP, 4, TW>(a, units, stage, s); break;
         default: throw_invalid("gram build v3: needs 2..4 other modes");
     }
 }
 
 }  // namespace
 
-bool gram3_supported(int64_t rp, int dother, const GramArgs& a) {
-    if (!(rp == 16 || rp == 32 || rp == 64) || dother < 2 || dother > 4) return false;
-    if (reinterpret_cast<uintptr_t>(a.fac) % 16) return false;
-    // staged factors only: read through L1 instead (config 4: 512 KB of factors), the random factor
-    // rows cost 219 ms against 62 for the batched build of k_gram.cu
-    if (sizeof(double) * (size_t)a.fac_total > 220 * 1024 || a.fac_total % 2) return false;
+// 2: all factors fit shared memory; 1: modes 1.. fit (mode 0 through L1); 0: v3 does not apply
+int gram3_stage(int64_t rp, int dother, const GramArgs& a) {
+    if (!(rp == 16 || rp == 32 || rp == 64) || dother < 2 || dother > 4) return 0;
+    if (reinterpret_cast<uintptr_t>(a.fac) % 16) return 0;
     for (int m = 0; m < dother; ++m)
-        if (a.fac_off[m] % 2) return false;
-    return true;
+        if (a.fac_off[m] % 2) return 0;
+    if (a.fac_total % 2) return 0;
+    constexpr size_t cap = 220 * 1024;
+    if (sizeof(double) * (size_t)a.fac_total <= cap) return 2;
+    // (nothing staged — every factor row through L1 — measured 219 ms at config 4 against 62 for
+    // k_gram.cu: not offered)
+    if (sizeof(double) * (size_t)(a.fac_total - a.fac_off[1]) <= cap) return 1;
+    return 0;
 }
 
 int gram3_units_per_sm(int64_t rp) {
@@ -334,11 +347,12 @@ int gram3_units_per_sm(int64_t rp) {
     }
 }
 
-void gram3_build(const GramArgs& a, int units, cudaStream_t s) {
+void gram3_build(const GramArgs& a, int units, int stage, cudaStream_t s) {
+    if (stage < 1 || stage > 2) throw_invalid("gram build v3: nothing staged");
     switch (a.rp) {
-        case 16: launch_g3_do<16, 1>(a, units, s); break;
-        case 32: launch_g3_do<32, 1>(a, units, s); break;
-        case 64: launch_g3_do<64, 4>(a, units, s); break;
+        case 16: launch_g3_do<16, 1>(a, units, stage, s); break;
+        case 32: launch_g3_do<32, 1>(a, units, stage, s); break;
+        case 64: launch_g3_do<64, 4>(a, units, stage, s); break;
         default: throw_invalid("gram build v3: padded rank must be 16, 32 or 64");
     }
 }

@@ -241,7 +241,7 @@ void dense_grid_build(const int32_t* idx, int64_t ldq, const int32_t* mult, cons
                       int64_t q, int64_t n1p, int64_t n2p, int32_t* w, cudaStream_t s);
 // *out += sum of v[0, q) (nonnegative int32; integer atomics: exact)
 void sum_i32(const int32_t* v, int64_t q, unsigned long long* out, cudaStream_t s);
-// key[l] = dense_key_value for the entries of dense rows (slot[rows[l]] >= 0)
+// key[l] += dense_key_value for the entries of dense rows (slot[rows[l]] >= 0)
 void dense_key(const int32_t* rows, const int32_t* slot, int64_t q, int32_t dense_key_value, int32_t* key,
                cudaStream_t s);
 bool runs_supported(int64_t rp, int dother);
@@ -283,9 +283,10 @@ void gram_build_ws(const GramArgs& a, int grid, int64_t sf, cudaStream_t s);
 int gram_build_occupancy(const GramArgs& a);
 // register-fragment build (k_gram3.cu): units = contiguous entry ranges of an equal-count partition
 // (cta_beg / cta_rows / row_first_cta / row_ncta over `units`), gram3_units_per_sm(rp) per SM
-bool gram3_supported(int64_t rp, int dother, const GramArgs& a);
+// 2: every factor staged in shared memory, 1: modes 1.. staged (a factor-block part), 0: not applicable
+int gram3_stage(int64_t rp, int dother, const GramArgs& a);
 int gram3_units_per_sm(int64_t rp);
-void gram3_build(const GramArgs& a, int units, cudaStream_t s);  // partition CTAs per SM for the build gram_build picks
+void gram3_build(const GramArgs& a, int units, int stage, cudaStream_t s);  // partition CTAs per SM for the build gram_build picks
 void gram_apply(const double* g, const double* xhat_rm, const int64_t* row_ptr, int64_t n, int64_t rp, double* yhat_rm,
                 cudaStream_t s);
 

@@ -98,3 +98,56 @@ def test_dense_rows_pcg_matches_runs(monkeypatch):
     w2 = cp.solve_unaligned_pcg(p2, cfg, rep2)
     assert abs(rep1.iterations - rep2.iterations) <= 1
     assert np.linalg.norm(w1 - w2) / np.linalg.norm(w2) < 1e-6
+
+
+@pytest.mark.parametrize("shape,r,q,coalesce,head,frac", [
+    ((600, 300, 512), 64, 900000, True, 5, 0.85),   # factors 415 KB: the build runs over the factor-block parts
+    ((600, 300, 512), 64, 600000, False, 0, 0.0),   # no dense rows: run-kernel parts only
+])
+def test_gram_build_over_parts(monkeypatch, shape, r, q, coalesce, head, frac):
+    """The row-Gram build over the q-pass plan's parts (opt-in: k_gram3.cu, block staged, mode 0
+    through L1; the dense rows' entries in their own parts) gives the operator the oracle gives and the
+    default single-pass build gives."""
+    monkeypatch.setenv("CPHIFI_GRAM3_PARTS", "1")  # (opt-in)
+    cp, mode, obs, model, idx, vals, factors = _case(shape, r, q, 9, coalesce, max(head, 1), frac)
+    n = shape[0]
+    x = np.random.default_rng(4).normal(size=n * r)
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+    assert p.set_operator("gram") == "gram"
+    y3 = cp.unaligned_matvec(p, x)
+    assert np.array_equal(y3, cp.unaligned_matvec(p, x))
+    plan = p.qpass_plan()
+    assert plan["parts"] == 2
+    if frac > 0:
+        assert plan["dense_rows"] > 0
+    kern = mode.kernel()
+    y_o = orc.unaligned_matvec_stream(shape, 0, idx, [np.zeros((n, r))] + factors[1:], kern, 1e-4, 1e-6, x)
+    assert np.linalg.norm(y3 - y_o) / np.linalg.norm(y_o) < 1e-12
+    monkeypatch.setenv("CPHIFI_GRAM3_PARTS", "0")
+    obs2 = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    p2 = cp.make_unaligned_subproblem(obs2, model, 0, mode, 1e-6)
+    p2.set_operator("gram")
+    y1 = cp.unaligned_matvec(p2, x)
+    assert np.linalg.norm(y3 - y1) / np.linalg.norm(y1) < 1e-13
+
+
+def test_qpass_plan_shared_by_subproblems():
+    """Subproblems on the same observation plan share its q-pass plan (built once): a second
+    subproblem with fresh factors reports the same plan and applies the operator the oracle gives."""
+    cp, mode, obs, model, idx, vals, factors = _case((600, 64, 128), 24, 400000, 5, True, 6, 0.7)
+    n, r = 600, 24
+    p1 = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+    p1.set_operator("stream")
+    plan1 = p1.qpass_plan()
+    g = np.random.default_rng(3)
+    f2 = [np.zeros((n, r))] + [f * (1 + 0.1 * g.normal(size=f.shape)) for f in factors[1:]]
+    p2 = cp.make_unaligned_subproblem(obs, cp.KruskalModel(f2), 0, mode, 1e-6)
+    p2.set_operator("stream")
+    assert p2.qpass_plan() == plan1
+    xh = np.asfortranarray(np.random.default_rng(1).normal(size=(n, r)))
+    y2 = p2.scatter_gather(xh)
+    y_o = orc.scatter_gather_stream((600, 64, 128), 0, idx, [None] + f2[1:], xh)
+    assert np.linalg.norm(y2 - y_o) / np.linalg.norm(y_o) < 1e-12
+    y1 = p1.scatter_gather(xh)  # the first subproblem's own factors still apply
+    y1_o = orc.scatter_gather_stream((600, 64, 128), 0, idx, [None] + factors[1:], xh)
+    assert np.linalg.norm(y1 - y1_o) / np.linalg.norm(y1_o) < 1e-12
