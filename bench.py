@@ -340,6 +340,11 @@ def main():
         dense_flops = 4.0 * nd * n1 * n2 * r  # two GEMMs per dense row: S = U A_2', P = T A_2 (2 flops / FMA)
         dtraffic, dtraffic_src = ncu_traffic("ncu_full_dense_config4.json", "dense_rows_kernel")
         t_app = total_ms / args.steps / 1e3
+        clk_sum = clk.summary()
+        clk_mhz = clk_sum.get("sm_mhz") or clk_sum.get("sm_max_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        smem_peak = 128.0 * sms * clk_mhz * 1e6 / 1e9
+        smem_bytes = qplan["sparse_entries_unpadded"] * (d - 2) * 8.0 * r / nparts
         b_alg, f_alg = alg_bytes_matvec(d, q, n, r), alg_flops_matvec(d, q, n, r)
         qpass_bytes = alg_bytes_k1(d, q // world, n, r)
         out = {
@@ -365,6 +370,14 @@ def main():
                                            "coalesced plan streams 12 B per distinct entry)",
                          "kernel_ms_per_launch": k1_launch_s * 1e3, "kernel_ms_per_application": k1_ms,
                          "kernel_share_of_step": k1_ms / app_ms_phased},
+            # the run kernel is bound by the shared-memory crossbar, not HBM: every entry reads its staged
+            # factor rows (the first other mode is hoisted per run) — (d - 2) x 8 r bytes per entry —
+            # against 128 B/clk/SM (B300_MICROARCH.md "smem crossbar BW") x SMs x the sampled SM clock
+            "roofline_smem": {"bound": "smem", "kernel": "runs kernel (per-entry factor-row reads)",
+                              "achieved": smem_bytes / k1_launch_s / 1e9, "peak": smem_peak, "unit": "GB/s",
+                              "frac": smem_bytes / k1_launch_s / 1e9 / smem_peak,
+                              "alg_bytes_per_launch": smem_bytes,
+                              "peak_note": f"128 B/clk/SM x {sms} SMs x {clk_mhz:.0f} MHz (sampled median SM clock)"},
             "roofline_dense_rows": {"bound": "tensor", "kernel": "dense_rows_kernel (k_dense_rows.cu: the rows whose "
                                                                  "cells are mostly drawn, two FP64 DMMA GEMMs per row)",
                                     "achieved": dense_flops / (dense_ms / 1e3) / 1e12 if dense_ms > 0 else None,
@@ -390,7 +403,7 @@ def main():
                     "call": "cphifi_unaligned_matvec (host x in, host y out, synchronous)"},
             "gpu_launches": launches.value * args.steps,
             "gpu_launches_per_step": launches.value,
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
             "setup": {"generate_s": gen_s, "plan_s": plan_s, "q_total": qt.value, "plan_entries_this_rank": ql.value},
         }
         if world == 1:

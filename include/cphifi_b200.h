@@ -214,7 +214,9 @@ int cphifi_unaligned_matvec_trace(cphifi_unaligned p, const double* x, double* y
  * [0] run-kernel parts (0: the whole plan on the stream kernel), [1] rows handled in the GEMM form
  * (k_dense_rows.cu; CPHIFI_DENSE_MIN sets the density threshold, 0 turns it off), [2] plan entries
  * left to the run kernel, [3] the draws those entries stand for (-1 without parts), [4] / [5] the
- * dense grids' padded n_1 / n_2; further slots 0. */
+ * dense grids' padded n_1 / n_2, [6] parts run by the cross-run kernel (k_xruns.cu: their runs
+ * padded to even lengths, so [2] counts the padding; CPHIFI_XRUNS=0 turns it off), [7] the entries
+ * of [2] before the padding; further slots 0. */
 int cphifi_unaligned_qpass_plan(cphifi_unaligned p, int64_t* info, int count);
 /* Test hook: Yhat = sampled_mttkrp(gather_rows(Xhat)) for a given Xhat (n x r), i.e.
  * observations.hpp:174-198 fused, before the final K multiply (all-reduced). */

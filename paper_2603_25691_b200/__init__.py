@@ -536,11 +536,12 @@ class UnalignedSubproblem:
 
     def qpass_plan(self) -> dict:
         """The stream operator's q-pass plan: run-kernel parts, dense rows (GEMM form), entries
-        left to the run kernel (cphifi_unaligned_qpass_plan)."""
-        v = (ctypes.c_int64 * 6)()
-        call("cphifi_unaligned_qpass_plan", self.handle, v, 6)
+        left to the run kernel, parts run by the cross-run kernel k_xruns.cu (their runs padded to even
+        lengths: sparse_entries counts the padding) (cphifi_unaligned_qpass_plan)."""
+        v = (ctypes.c_int64 * 8)()
+        call("cphifi_unaligned_qpass_plan", self.handle, v, 8)
         return {"parts": v[0], "dense_rows": v[1], "sparse_entries": v[2], "sparse_draws": v[3],
-                "dense_n1p": v[4], "dense_n2p": v[5]}
+                "dense_n1p": v[4], "dense_n2p": v[5], "xruns_parts": v[6], "sparse_entries_unpadded": v[7]}
 
     def scatter_gather(self, xhat) -> np.ndarray:
         """Yhat = sampled_mttkrp(gather_rows(Xhat)) (observations.hpp:174-198), fused."""

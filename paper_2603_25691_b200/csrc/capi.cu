@@ -472,7 +472,8 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
             b.slot_b = p->runs_slot_b.get();
             b.rowcnt = a.rowcnt;
             b.accumulate = acc ? 1 : 0;
-            runs_scatter_gather(b, sp.sf, s);
+            if (sp.padded) xruns_scatter_gather(b, sp.sf, s);
+            else runs_scatter_gather(b, sp.sf, s);
         }
         if (g_dense_event) {  // cphifi_unaligned_matvec_timed: the run kernel / dense rows split
             CPHIFI_CUDA(cudaEventRecord(g_dense_event, s));
@@ -525,8 +526,8 @@ void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_
         sp.run_i1.alloc(std::max<int64_t>(nr, 1));
         gather_i32(sp.idx, sp.run_start.get(), 0, nr, sp.run_i1.get(), s);
     }
-    sp.draws = q;
-    if (sp.mult && q > 0) {
+    if (!sp.padded) sp.draws = q;  // (a padded part's draws are counted before its flags are set)
+    if (sp.mult && q > 0 && !sp.padded) {
         DevBuf<unsigned long long> sum(1);
         CPHIFI_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), s));
         sum_i32(sp.mult, q, sum.get(), s);
@@ -554,6 +555,7 @@ void finish_part(cphifi_unaligned p, StreamPart& sp, const int32_t* rows, int64_
             const double c0 = (double)rs[j] + cpr * (double)j;  // cost at run j's start
             int64_t e = rs[j] + (int64_t)std::max(0.0, tgt - c0 - cpr);
             e = std::min<int64_t>(std::max<int64_t>(e, rs[j]), rs[j + 1]);
+            if (sp.padded) e &= ~(int64_t)1;  // pairs of entries never straddle a warp range
             starts.push_back(std::max(e, starts.back()));
         }
         starts.push_back(q);
@@ -643,6 +645,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
         std::vector<StreamPart> parts(1);
         StreamPart& sp = parts[0];
         sp.q = q;
+        sp.q_real = q;
         sp.ldq = o->ldq;
         sp.rows = nl;
         sp.idx = o->idx_o.get();
@@ -663,6 +666,14 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
     }
     const int H = (int)((nl + br - 1) / br);
     br = (nl + H - 1) / H;  // balanced blocks
+    // opt-in (CPHIFI_XRUNS=1; measured slower at config 4, k_xruns.cu): the cross-run kernel for 3-way
+    // coalesced plans whose blocks fit its buffers, over parts padded to even run lengths
+    bool xruns = mult && xruns_supported(rp, d - 1, mult) && xruns_smem_bytes(rp, rest + br * rp) <= runs_smem_cap() &&
+                 xruns_warps_per_sm() == runs_warps_per_sm(rp);
+    {
+        const char* e = std::getenv("CPHIFI_XRUNS");
+        xruns = xruns && e && std::atoi(e) != 0;
+    }
     // part key = block of the last other mode; the dense rows' entries get key H (dropped)
     DevBuf<int32_t> key(std::max<int64_t>(q, 1)), key_s(std::max<int64_t>(q, 1)), perm_in(std::max<int64_t>(q, 1)),
         perm(std::max<int64_t>(q, 1)), rows_h(std::max<int64_t>(q, 1));
@@ -686,6 +697,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
         const int h = b % H;
         const int64_t lo = hb[b], cnt = hb[b + 1] - hb[b];
         sp.q = cnt;
+        sp.q_real = cnt;
         sp.ldq = (cnt + 3) / 4 * 4;
         sp.row_lo = h * br;
         sp.rows = std::min(br, nl - sp.row_lo);
@@ -702,6 +714,35 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
             sp.mult = sp.mult_own.get();
         }
         gather_i32(rows.get(), perm.get(), lo, cnt, rows_h.get(), s);
+        if (runs && xruns && cnt > 0) {  // runs padded to even lengths for k_xruns.cu
+            DevBuf<int32_t> rs(cnt + 1);
+            const int64_t nr = build_run_starts(rows_h.get(), sp.idx_own.get(), cnt, rs.get(), s);
+            const int32_t qq = (int32_t)cnt;
+            h2d(rs.get() + nr, &qq, sizeof(int32_t), s);
+            DevBuf<unsigned long long> sum(1);
+            CPHIFI_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), s));
+            sum_i32(sp.mult, cnt, sum.get(), s);
+            unsigned long long hsum = 0;
+            d2h_sync(&hsum, sum.get(), sizeof(hsum), s);
+            const int64_t qmax = cnt + nr, ldq2 = (qmax + 3) / 4 * 4;
+            DevBuf<int32_t> idx2(2 * ldq2 + OBS_PAD), mult2(qmax + OBS_PAD), rows2(qmax);
+            const int64_t q2 = pad_runs_even(rs.get(), nr, sp.idx_own.get(), sp.idx_own.get() + sp.ldq, sp.mult,
+                                             rows_h.get(), idx2.get(), idx2.get() + ldq2, mult2.get(), rows2.get(),
+                                             cnt, s);
+            sp.q = q2;
+            sp.ldq = ldq2;
+            sp.idx_own = std::move(idx2);
+            sp.idx = sp.idx_own.get();
+            sp.mult_own = std::move(mult2);
+            sp.mult = sp.mult_own.get();
+            sp.draws = (int64_t)hsum;
+            sp.padded = true;
+            sp.row_ptr_own.alloc(p->n + 1);
+            csr_from_sorted(rows2.get(), q2, p->n, sp.row_ptr_own.get(), s);
+            sp.row_ptr = sp.row_ptr_own.get();
+            finish_part(p, sp, rows2.get(), nw);
+            return;
+        }
         sp.row_ptr_own.alloc(p->n + 1);
         csr_from_sorted(rows_h.get(), cnt, p->n, sp.row_ptr_own.get(), s);
         sp.row_ptr = sp.row_ptr_own.get();
@@ -731,7 +772,13 @@ bool gram_build_parts(cphifi_unaligned p) {
     if (const char* e = std::getenv("CPHIFI_GRAM_WS")) ws = std::atoi(e) != 0;
     bool v3 = false;  // opt-in: measured 90 ms at config 4 against 62 for k_gram.cu's batched build (mode 0
                       // through L1 per entry, four warps per entry stream): CPHIFI_GRAM3_PARTS=1
-    if (const char* e = std::getenv("CPHIFI_GRAM3_PARTS")) v3 = !ws && p->obs->d == 3 && std::atoi(e) != 0;
+    // 1: mode 0 through L1 per entry (90 ms at config 4); 3: mode 0 hoisted per run
+    // (CPHIFI_GRAM3_PARTS=3, 109 ms): both slower than k_gram.cu's batched build (62 ms)
+    int v3stage = 1;
+    if (const char* e = std::getenv("CPHIFI_GRAM3_PARTS")) {
+        v3 = !ws && p->obs->d == 3 && std::atoi(e) != 0;
+        if (std::atoi(e) == 3) v3stage = 3;
+    }
     cphifi_obs o = p->obs;
     if (ws && !gram_ws_supported(p->rp, o->d - 1)) return false;
     if (!ws && !v3) return false;
@@ -817,7 +864,7 @@ bool gram_build_parts(cphifi_unaligned p) {
         g.slot_b = slot_b.get();
         g.g = p->gram.get();
         g.accumulate = 1;  // G was zeroed: every part adds, in part order
-        if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), 1, s);
+        if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), v3stage, s);
         else gram_build_ws(g, (int)(sp->g_beg.n - 1), sp->sf, s);
     }
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // the slots / counters are released on return
@@ -2436,14 +2483,17 @@ int cphifi_unaligned_qpass_plan(cphifi_unaligned p, int64_t* info, int count) {
         ensure_runs(p);
         static const QpassPlan none;
         const QpassPlan& Q = p->qp ? *p->qp : none;
-        int64_t q = 0, dr = 0;
+        int64_t q = 0, dr = 0, xp = 0, qr = 0;
         for (const auto& sp : Q.parts) {
             q += sp.q;
             dr += sp.draws;
+            xp += sp.padded ? 1 : 0;
+            qr += sp.q_real;
         }
-        const int64_t v[6] = {(int64_t)Q.parts.size(), Q.dense_nd, Q.parts.empty() ? p->obs->q_local : q,
-                              Q.parts.empty() ? -1 : dr, Q.dense_n1p, Q.dense_n2p};
-        for (int i = 0; i < count; ++i) info[i] = i < 6 ? v[i] : 0;
+        const int64_t v[8] = {(int64_t)Q.parts.size(), Q.dense_nd, Q.parts.empty() ? p->obs->q_local : q,
+                              Q.parts.empty() ? -1 : dr, Q.dense_n1p, Q.dense_n2p, xp,
+                              Q.parts.empty() ? p->obs->q_local : qr};
+        for (int i = 0; i < count; ++i) info[i] = i < 8 ? v[i] : 0;
     });
 }
 

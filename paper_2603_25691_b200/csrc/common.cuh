@@ -175,6 +175,8 @@ struct StreamPart {
     int warps = 0;                       // equal-count warp ranges
     cphifi::DevBuf<int64_t> warp_beg, warp_rows;
     cphifi::DevBuf<int32_t> row_first_w, row_nw;
+    bool padded = false;                 // runs padded to even lengths, run starts flagged (k_xruns.cu)
+    int64_t q_real = 0;                  // entries before the padding
     int g_units = 0;                     // the row-Gram build's equal-count units (built on first use)
     cphifi::DevBuf<int64_t> g_beg, g_rows;
     cphifi::DevBuf<int32_t> g_rfc, g_rnc;

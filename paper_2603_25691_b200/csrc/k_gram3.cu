@@ -24,6 +24,20 @@
 //     staged in shared memory when they fit (config 3: 3 x 64 KB), else read through L1.
 // k-steps sit at fixed 4-aligned positions; a step that straddles a row end is run once per row
 // with the other row's entries masked (rows hold ~1e5 entries, so this is rare).
+//
+// STAGE 3 (3-way factor-block parts, config 4: the factors do not fit shared memory): the first
+// other mode is HOISTED per run instead of gathered per entry.  The plan is lexicographic, so the
+// entries of a row form runs of equal a, and over a run
+//     sum_l w_l z_l z_l' = (A_1(a,:)' A_1(a,:)) o M,   M = sum_{l in run} w_l t_l t_l',  t_l = A_2(b_l,:)
+// (z_l = A_1(a,:) o t_l): the k-steps accumulate M from the staged block's rows alone (no mode-0 load
+// per entry), and a run end folds G += (a a') o M on the accumulator registers (each lane scales its
+// own fragment elements by A_1(a, ii) A_1(a, jj)) and clears M.  A k-step that straddles a run end is
+// run once per run with the other entries masked (a is non-decreasing inside a row); the A_1 rows of
+// the next batch's runs are prefetched into L1 when the batch is loaded.  MEASURED SLOWER (opt-in,
+// CPHIFI_GRAM3_PARTS=3): config 4 108.6 ms against 89.8 ms for STAGE 1 and 61.8 ms for k_gram.cu's
+// batched build (profiles/round2/gram_parts_config4.log) — with ~28-entry runs per part a quarter of
+// the k-steps straddle a run end (a second masked DMMA pass) and every run end pays a fold whose A_1
+// loads wait on L1 / L2.
 #include <climits>
 #include <cstdlib>
 
@@ -61,10 +75,13 @@ __host__ __device__ constexpr int pair_index(int ti, int tj) {
 }
 
 // STAGE: 2 = every factor staged in shared memory; 1 = modes 1.. staged (a factor-block part: mode 0,
-// constant along the plan's runs, read through L1); 0 = none staged
+// constant along the plan's runs, read through L1); 3 = as 1 with mode 0 hoisted per run (DO = 2);
+// 0 = none staged
 template <int RP, int DO, int TW, int STAGE>
 __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int units) {
     constexpr bool SF = STAGE > 0;
+    constexpr bool HOIST = STAGE == 3;
+    static_assert(!HOIST || DO == 2, "gram build v3: the hoisted form is for 3-way plans");
     using C = G3<RP, TW>;
     constexpr int NT = C::NT, TPW = C::TPW;
     extern __shared__ __align__(16) double g3s[];
@@ -98,8 +115,11 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
     if (beg >= end) return;
 
     double acc[TPW][2];
+    double accm[HOIST ? TPW : 1][2];  // HOIST: the current run's M (acc holds G)
 #pragma unroll
     for (int x = 0; x < TPW; ++x) acc[x][0] = acc[x][1] = 0.0;
+#pragma unroll
+    for (int x = 0; x < (HOIST ? TPW : 1); ++x) accm[x][0] = accm[x][1] = 0.0;
 
     const int64_t first_row = a.cta_rows[2 * u];
     int64_t row = first_row;
@@ -160,7 +180,15 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
         const bool ok = e >= beg && e < end;
 #pragma unroll
         for (int m = 0; m < DO; ++m) v[m] = ok ? __ldg(a.idx + (int64_t)m * a.q + e) : 0;
-        v[DO] = ok ? (a.mult ? __ldg(a.mult + e) : 1) : 0;
+        v[DO] = ok ? (a.mult ? (__ldg(a.mult + e) & RUN_MULT_MASK) : 1) : 0;
+        if constexpr (HOIST) {  // the A_1 rows of the runs starting in this batch, into L1
+            const int32_t prev = __shfl_up_sync(0xffffffffu, v[0], 1);
+            if (ok && (lane == 0 || prev != v[0])) {
+                const char* row = reinterpret_cast<const char*>(a.fac + a.fac_off[0] + (int64_t)v[0] * RP);
+#pragma unroll
+                for (int c = 0; c < RP * 8; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + c));
+            }
+        }
     };
     load_batch(0, cur);
     load_batch(32, nxt);
@@ -175,16 +203,18 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
         opar[m] = (int)(((a.fac_off[m] - sbeg) / RP) & 3);
     }
     int rb = (int)(row_beg - p0), re = (int)(min(row_end, end) - p0);  // current row, relative
+    const int ulo = (int)(beg - p0);  // the unit's first entry, relative
 
     // z of entry (kq) of the k-step at batch lane offset src
-    auto build_z = [&](int src, double (&z)[NT], int32_t& wm) {
+    auto build_z = [&](int src, double (&z)[NT], int32_t& wm, int32_t& ea) {
         int32_t ix[DO];
 #pragma unroll
         for (int m = 0; m < DO; ++m) ix[m] = __shfl_sync(0xffffffffu, cur[m], src);
         wm = __shfl_sync(0xffffffffu, cur[DO], src);  // 0 outside [beg, end)
+        ea = ix[0];
 #pragma unroll
-        for (int m = 0; m < DO; ++m) {
-            const bool st = STAGE == 2 || (STAGE == 1 && m >= 1);  // this mode in shared memory
+        for (int m = HOIST ? 1 : 0; m < DO; ++m) {
+            const bool st = STAGE == 2 || (STAGE != 0 && m >= 1);  // this mode in shared memory
             const int swm = st ? sw(opar[m] + ix[m]) : 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
@@ -197,7 +227,7 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
                 } else {
                     f = __ldg(reinterpret_cast<const double2*>(gbase[m] + (int64_t)ix[m] * RP) + lc);
                 }
-                if (m == 0) {
+                if (m == (HOIST ? 1 : 0)) {
                     z[2 * c] = f.x;
                     z[2 * c + 1] = f.y;
                 } else {
@@ -244,11 +274,39 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
 #pragma unroll
             for (int tj = ti; tj < NT; ++tj) {
                 const int uu = pair_index<NT>(ti, tj);
-                if (uu % TW == tw) dmma3(acc[uu / TW], zw[ti], z[tj]);
+                if (uu % TW == tw) {
+                    if constexpr (HOIST) dmma3(accm[uu / TW], zw[ti], z[tj]);
+                    else dmma3(acc[uu / TW], zw[ti], z[tj]);
+                }
             }
+    };
+    // HOIST: the current run's first-mode index (-1: none yet) and its fold G += (a a') o M
+    int cur_a = -1;
+    auto fold = [&]() {
+        if constexpr (HOIST) {
+            if (cur_a >= 0) {
+                const double* ar = a.fac + a.fac_off[0] + (int64_t)cur_a * RP;
+#pragma unroll
+                for (int ti = 0; ti < NT; ++ti)
+#pragma unroll
+                    for (int tj = ti; tj < NT; ++tj) {
+                        const int uu = pair_index<NT>(ti, tj);
+                        if (uu % TW != tw) continue;
+                        const double ai = __ldg(ar + NT * g + ti);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const double s = ai * __ldg(ar + NT * (2 * kq + h) + tj);
+                            acc[uu / TW][h] = fma(s, accm[uu / TW][h], acc[uu / TW][h]);
+                            accm[uu / TW][h] = 0.0;
+                        }
+                    }
+            }
+        }
     };
     // the next non-empty row after the current one (it starts at the current row's end)
     auto next_row = [&]() {
+        fold();
+        cur_a = -1;
         flush(row);
         do {
             ++row;
@@ -267,11 +325,40 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
             load_batch(b0 + 32, nxt);
         }
         const int src = P - b0 + kq;
+        if constexpr (HOIST) {  // one k-step at a time (registers: G and M accumulators)
+#pragma unroll 1
+            for (int h = 0; h < 8; h += 4) {
+                const int Q = P + h;
+                if (Q >= nrel) break;
+                double z[NT];
+                int32_t wm, ea;
+                build_z(src + h, z, wm, ea);
+                if (Q >= rb && Q >= ulo && Q + 4 <= re && __all_sync(0xffffffffu, ea == cur_a)) {  // one run
+                    mma_step(z, wm);
+                    continue;
+                }
+                // a run or row end (or the unit's start / end) inside: once per run of each row
+                const int e = Q + kq;
+                for (;;) {
+                    for (;;) {  // runs of the current row in this k-step, in ascending a
+                        const bool in = e >= rb && e >= ulo && e < re;
+                        if (__any_sync(0xffffffffu, in && ea == cur_a)) mma_step(z, in && ea == cur_a ? wm : 0);
+                        const int nx = (int)__reduce_min_sync(0xffffffffu, (unsigned)(in && ea > cur_a ? ea : INT_MAX));
+                        if (nx == INT_MAX) break;
+                        fold();
+                        cur_a = nx;
+                    }
+                    if (Q + 4 <= re || row_end >= end) break;
+                    next_row();  // the step straddles the row end: the next row's entries of this step
+                }
+            }
+            continue;
+        }
         if (P >= rb && P + 8 <= re) {  // both k-steps inside the current row
             double za[NT], zb[NT];
-            int32_t wa, wb;
-            build_z(src, za, wa);
-            build_z(src + 4, zb, wb);
+            int32_t wa, wb, ka, kb;
+            build_z(src, za, wa, ka);
+            build_z(src + 4, zb, wb, kb);
             mma_step(za, wa);
             mma_step(zb, wb);
             continue;
@@ -282,8 +369,8 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
             const int Q = P + h;
             if (Q >= nrel) break;
             double z[NT];
-            int32_t wm;
-            build_z(src + h, z, wm);
+            int32_t wm, ea;
+            build_z(src + h, z, wm, ea);
             const int e = Q + kq;
             for (;;) {
                 mma_step(z, (e >= rb && e < re) ? wm : 0);
@@ -292,6 +379,7 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
             }
         }
     }
+    fold();
     flush(row);
 }
 
@@ -308,6 +396,14 @@ void launch_g3(const GramArgs& a, int units, int stage, cudaStream_t s) {
         auto kern = gram3_kernel<RP, DO, TW, 1>;
         func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         kern<<<grid, G3T, fbytes, s>>>(a, units);
+    } else if (stage == 3) {
+        if constexpr (DO == 2) {
+            auto kern = gram3_kernel<RP, DO, TW, 3>;
+            func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            kern<<<grid, G3T, fbytes, s>>>(a, units);
+        } else {
+            throw_invalid("gram build v3: the hoisted form needs a 3-way plan");
+        }
     }
     CPHIFI_CHECK_LAUNCH();
 }
@@ -348,7 +444,7 @@ int gram3_units_per_sm(int64_t rp) {
 }
 
 void gram3_build(const GramArgs& a, int units, int stage, cudaStream_t s) {
-    if (stage < 1 || stage > 2) throw_invalid("gram build v3: nothing staged");
+    if (stage < 1 || stage > 3) throw_invalid("gram build v3: nothing staged");
     switch (a.rp) {
         case 16: launch_g3_do<16, 1>(a, units, stage, s); break;
         case 32: launch_g3_do<32, 1>(a, units, stage, s); break;

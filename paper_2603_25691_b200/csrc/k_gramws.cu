@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(Ws<RP>::T, 1) gram_ws_kernel(const GramArgs a)
                 if (lane < cnt) {
 #pragma unroll
                     for (int m = 0; m < DO; ++m) ix[m] = __ldg(a.idx + (int64_t)m * a.q + pos + lane);
-                    wl = a.mult ? (double)__ldg(a.mult + pos + lane) : 1.0;
+                    wl = a.mult ? (double)(__ldg(a.mult + pos + lane) & RUN_MULT_MASK) : 1.0;
                 } else {
 #pragma unroll
                     for (int m = 0; m < DO; ++m) ix[m] = 0;

@@ -75,11 +75,26 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
     }
 }
 
-template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH>
+// VAR (bit mask, measured variants of the inner loop; 0 = the layout above):
+//  RV_IDXS  plan indices of a 16-entry window read once per lane (one LDS.32: lanes 0-15 the
+//           per-observation index, 16-31 the multiplicity) and handed to the entries by shuffles
+//           instead of one broadcast LDS per entry and column (3-way coalesced plans);
+//  RV_PRED  the last, partial step of a run loads only the rows of entries inside the run (lane
+//           groups past the end skip their loads) instead of re-loading the run's last row;
+//  RV_A1REG the run's A_1 row kept in registers from u = Xhat o A_1 to the fold (one row read per run
+//           instead of two);
+//  RV_XREG  the row's Xhat row kept in registers (read once per row instead of once per run).
+constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8;
+
+template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     using L = Lay<RP, DO, MULT, NW, CH>;
     constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
+    constexpr bool IDXS = (VAR & RV_IDXS) != 0, PRED = (VAR & RV_PRED) != 0, A1REG = (VAR & RV_A1REG) != 0,
+                   XREG = (VAR & RV_XREG) != 0;
+    constexpr int WIN = MULT ? 16 : 32;  // RV_IDXS window (entries)
+    static_assert(!IDXS || (DO == 2 && STEP <= WIN / 2), "RV_IDXS: 3-way plans, window >= 2 steps");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* cbar = reinterpret_cast<uint64_t*>(smem_raw);  // CTA: staged factors
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -226,17 +241,45 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     // a step in two halves so the next step's loads can be issued between them (software
     // pipelining: the loads of step k + 1 overlap the dot reduction and update of step k)
     double u[VPL], v[VPL], racc[VPL];  // racc: this lane's share of its lane group's row accumulator
+    double a1r[A1REG ? VPL : 1], xr[XREG ? VPL : 1];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) racc[k] = 0.0;
+    if constexpr (XREG) lds_row<G, VPL>(xr, xrs, gl, odd);
+    // RV_IDXS window: entries [wnd, wnd + WIN); lane l holds column 1 of entry wnd + (l % 16) (l < 16)
+    // or the multiplicity (l >= 16) — WIN = 32 without multiplicities: column 1 of wnd + l
+    int wnd = INT_MIN / 2, widx = 0;
+    auto window = [&](int p) {  // before a step at p: [p, p + STEP) inside the window, landed
+        if constexpr (IDXS) {
+            if (p - wnd > WIN - STEP) {
+                wnd = p;
+                if (wnd + WIN > land_lim || wnd >= refill_at) stage(wnd, min(wnd + WIN, rel_end) - 1);
+                const int e = wnd + (lane % WIN);
+                widx = ring_at(e, (MULT && lane >= 16) ? DO : 1);
+            }
+        } else {
+            if (p + STEP > land_lim || p >= refill_at) stage(p, p + STEP - 1);
+        }
+    };
     auto load = [&](int p, int rend, double (&z)[B][VPL], int (&mu)[B], auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             int ent = p + g * B + b;
+            const bool ok = FULL || ent < rend;
             if constexpr (!FULL) ent = min(ent, rend - 1);
             const double* rows[DO];
+            if constexpr (IDXS) {
+                rows[1] = fs[1] + __shfl_sync(0xffffffffu, widx, ent - wnd) * RP;
+                if constexpr (MULT) mu[b] = __shfl_sync(0xffffffffu, widx, 16 + ent - wnd);
+            } else {
 #pragma unroll
-            for (int m = 1; m < DO; ++m) rows[m] = fs[m] + ring_at(ent, m) * RP;
+                for (int m = 1; m < DO; ++m) rows[m] = fs[m] + ring_at(ent, m) * RP;
+            }
+            if (PRED && !FULL && !ok) {
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) z[b][k] = 0.0;
+                continue;
+            }
             // t = A_2(b,:) o A_3(c,:) o ...: one pair of columns at a time (few live registers)
 #pragma unroll
             for (int t = 0; t < VPL / 2; ++t) {
@@ -251,7 +294,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 z[b][2 * t] = x.x;
                 z[b][2 * t + 1] = x.y;
             }
-            if constexpr (MULT) mu[b] = ring_at(ent, DO);
+            if constexpr (MULT && !IDXS) mu[b] = ring_at(ent, DO);
         }
     };
     auto dots = [&](const double (&z)[B][VPL], double (&d)[B]) {
@@ -292,10 +335,18 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             tma::bulk_g2s(a1s + sl * RP, fa1 + (int64_t)i1_2 * RP, RP * 8, bar_a1 + sl);
         }
         const double* a1 = a1s + (jl % 3) * RP;
-        lds_row<G, VPL>(u, xrs, gl, odd);  // u = Xhat(i,:) o A_1(a,:), one pair at a time
+        if constexpr (XREG) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) u[k] = xr[k];
+        } else {
+            lds_row<G, VPL>(u, xrs, gl, odd);  // u = Xhat(i,:) o A_1(a,:), one pair at a time
+        }
+        if constexpr (A1REG) lds_row<G, VPL>(a1r, a1, gl, odd);
 #pragma unroll
         for (int t = 0; t < VPL / 2; ++t) {
-            const double2 x = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
+            double2 x;
+            if constexpr (A1REG) x = make_double2(a1r[2 * t], a1r[2 * t + 1]);
+            else x = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
             u[2 * t] *= x.x;
             u[2 * t + 1] *= x.y;
             v[2 * t] = 0.0;
@@ -311,7 +362,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             int ma[B], mb[B];
             if constexpr (!PIPE) {
                 for (; p + STEP <= rend; p += STEP) {
-                    if (p + STEP > land_lim || p >= refill_at) stage(p, p + STEP - 1);
+                    window(p);
                     load(p, rend, za, ma, std::true_type{});
                     dots(za, d);
                     finish(p, rend, za, ma, d, std::true_type{});
@@ -319,7 +370,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             }
             bool have = PIPE && p + STEP <= rend;
             if (have) {
-                if (p + STEP > land_lim || p >= refill_at) stage(p, p + STEP - 1);
+                window(p);
                 load(p, rend, za, ma, std::true_type{});
             }
             while (have) {  // unrolled by two: za / zb alternate as current / next
@@ -327,7 +378,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 int pn = p + STEP;
                 bool hn = pn + STEP <= rend;
                 if (hn) {
-                    if (pn + STEP > land_lim || pn >= refill_at) stage(pn, pn + STEP - 1);
+                    window(pn);
                     load(pn, rend, zb, mb, std::true_type{});
                 }
                 finish(p, rend, za, ma, d, std::true_type{});
@@ -338,7 +389,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 pn = p + STEP;
                 hn = pn + STEP <= rend;
                 if (hn) {
-                    if (pn + STEP > land_lim || pn >= refill_at) stage(pn, pn + STEP - 1);
+                    window(pn);
                     load(pn, rend, za, ma, std::true_type{});
                 }
                 finish(p, rend, zb, mb, d, std::true_type{});
@@ -346,7 +397,8 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 have = hn;
             }
             if (p < rend) {  // the last, partial step
-                if (rend > land_lim || p >= refill_at) stage(p, rend - 1);
+                if constexpr (IDXS) window(p);
+                else if (rend > land_lim || p >= refill_at) stage(p, rend - 1);
                 load(p, rend, za, ma, std::false_type{});
                 dots(za, d);
                 finish(p, rend, za, ma, d, std::false_type{});
@@ -356,7 +408,9 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         // groups keep separate partial rows; they are summed once per row, at the flush)
 #pragma unroll
         for (int t = 0; t < VPL / 2; ++t) {
-            const double2 aa = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
+            double2 aa;
+            if constexpr (A1REG) aa = make_double2(a1r[2 * t], a1r[2 * t + 1]);
+            else aa = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
             racc[2 * t] = fma(aa.x, v[2 * t], racc[2 * t]);
             racc[2 * t + 1] = fma(aa.y, v[2 * t + 1], racc[2 * t + 1]);
         }
@@ -441,15 +495,16 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 }
                 tma::mbar_wait(bar_x, (unsigned)(xcnt & 1));
                 ++xcnt;
+                if constexpr (XREG) lds_row<G, VPL>(xr, xrs, gl, odd);
             }
         }
         __syncwarp();
     }
 }
 
-template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW = 16, int CH = 64>
+template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW = 16, int CH = 64, int VAR = 0>
 void launch4(const RunsArgs& a, int64_t sf, cudaStream_t s) {
-    auto kern = runs_kernel<RP, DO, MULT, G, B, PIPE, NW, CH>;
+    auto kern = runs_kernel<RP, DO, MULT, G, B, PIPE, NW, CH, VAR>;
     const size_t smem = Lay<RP, DO, MULT, NW, CH>::bytes(sf);
     func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CAP);
     const int grid = (a.warps + NW - 1) / NW;
@@ -469,6 +524,39 @@ int runs_layout() {
     }();
     return layout;
 }
+// inner-loop variant (RV_* bits; + 16: 12 warps per CTA, up to 168 registers) of the G = 8, B = 2
+// layout at RP = 64 (CPHIFI_RUNS_VAR)
+int runs_var() {
+    static const int var = [] {
+        const char* e = std::getenv("CPHIFI_RUNS_VAR");
+        return e ? std::atoi(e) : 0;
+    }();
+    return var;
+}
+
+template <int RP, int DO, bool MULT>
+void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
+    if constexpr (RP == 64 && DO == 2 && MULT) {
+        switch (runs_var()) {
+            case 1: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 1>(a, sf, s); return;
+            case 2: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 2>(a, sf, s); return;
+            case 3: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 3>(a, sf, s); return;
+            case 4: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 4>(a, sf, s); return;
+            case 7: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 7>(a, sf, s); return;
+            case 20: launch4<RP, DO, MULT, 8, 2, false, 12, 64, 4>(a, sf, s); return;
+            case 23: launch4<RP, DO, MULT, 8, 2, false, 12, 64, 7>(a, sf, s); return;
+            case 28: launch4<RP, DO, MULT, 8, 2, false, 12, 64, 12>(a, sf, s); return;
+            case 31: launch4<RP, DO, MULT, 8, 2, false, 12, 64, 15>(a, sf, s); return;
+            case 80: launch4<RP, DO, MULT, 8, 2, true, 12, 64, 0>(a, sf, s); return;
+            case 81: launch4<RP, DO, MULT, 8, 2, true, 8, 64, 0>(a, sf, s); return;
+            case 82: launch4<RP, DO, MULT, 8, 4, false, 8, 64, 0>(a, sf, s); return;
+            case 83: launch4<RP, DO, MULT, 8, 3, false, 12, 64, 0>(a, sf, s); return;
+            case 84: launch4<RP, DO, MULT, 8, 4, false, 12, 64, 0>(a, sf, s); return;
+            default: break;
+        }
+    }
+    launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
+}
 
 template <int RP, int DO, bool MULT>
 void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
@@ -476,7 +564,7 @@ void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
     if constexpr (RP == 64) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 1, true>(a, sf, s);
         else if (lay == 3) launch4<RP, DO, MULT, 16, 4, false, 20, 32>(a, sf, s);
-        else launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
+        else launch_var<RP, DO, MULT>(a, sf, s);
     } else if constexpr (RP == 32) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
         else if (lay == 2) launch4<RP, DO, MULT, 4, 1, true>(a, sf, s);
@@ -509,7 +597,13 @@ bool runs_supported(int64_t rp, int dother) { return (rp == 16 || rp == 32 || rp
 // the CTA shape the launch picks for padded rank rp (layout 3: 24 warps, 32-entry chunks at RP 64)
 // (layout 3 trades registers for warps: G = 16 lanes per entry, 20 warps, 32-entry chunks — measured
 // 4.79 ms against 4.01 for the 16-warp G = 8 layout at config 4; 24 warps with B = 4 / 2: 5.76 / 5.08)
-static int shape_nw(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 20 : 16; }
+static int shape_nw(int64_t rp) {
+    if (rp == 64 && runs_layout() == 3) return 20;
+    if (rp != 64 || runs_layout() != 0) return 16;
+    const int v = runs_var();
+    if (v == 81 || v == 82) return 8;
+    return (v & 16) || v == 80 || v == 83 || v == 84 ? 12 : 16;
+}
 static int shape_ch(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 32 : 64; }
 
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {

@@ -246,6 +246,19 @@ void dense_key(const int32_t* rows, const int32_t* slot, int64_t q, int32_t dens
                cudaStream_t s);
 bool runs_supported(int64_t rp, int dother);
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles);
+// k_xruns.cu: the q-pass of 3-way coalesced parts with steps across run boundaries.  The part's runs
+// are padded to even lengths (a zero-multiplicity copy of an odd run's last entry) and run starts are
+// flagged in bit 30 of the multiplicity: readers of a padded part's multiplicities mask it off.
+constexpr int32_t RUN_MULT_MASK = (1 << 30) - 1;
+bool xruns_supported(int64_t rp, int dother, bool mult);
+size_t xruns_smem_bytes(int64_t rp, int64_t sf_doubles);
+int xruns_warps_per_sm();
+void xruns_scatter_gather(const RunsArgs& a, int64_t sf_doubles, cudaStream_t s);
+// pads the runs [run_start[r], run_start[r+1]) of a part (columns ia / ib, multiplicities, rows) into
+// oa / ob / om / orow (room for q + nr entries); returns the padded entry count
+int64_t pad_runs_even(const int32_t* run_start, int64_t nr, const int32_t* ia, const int32_t* ib, const int32_t* mult,
+                      const int32_t* rows, int32_t* oa, int32_t* ob, int32_t* om, int32_t* orow, int64_t q,
+                      cudaStream_t s);
 size_t runs_smem_cap();
 int runs_warps_per_sm(int64_t rp);
 int runs_chunk(int64_t rp);

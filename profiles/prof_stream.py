@@ -67,7 +67,8 @@ def main():
         if y_ref is None:
             y_ref = yy
         out["variants"].append({"env": env, "plan_s": plan_s, "stream_ms": ms6[1], "app_ms": ms6[5],
-                                "rel_vs_first": rel, "qpass_plan": p.qpass_plan()})
+                                "rel_vs_first": rel, "qpass_plan": p.qpass_plan(),
+                                "y_sum": float(yy.sum()), "y_norm": float(torch.linalg.norm(yy))})
         print(json.dumps(out["variants"][-1]), flush=True)
         del p
         torch.cuda.empty_cache()
