@@ -759,7 +759,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
 
 // The row-Gram build over the q-pass plan's factor-block parts (the run kernel's parts plus the dense
 // rows' parts: every entry once), one launch per part adding into G (zeroed by the caller):
-//  * opt-in (CPHIFI_GRAM3_PARTS=1), 3-way plans whose factors do not fit shared memory (config 4:
+//  * default (CPHIFI_GRAM3_PARTS=0: off), 3-way plans whose factors do not fit shared memory (config 4:
 //    2 x 256 KB): the register-fragment build (k_gram3.cu) with the part's block staged and mode 0
 //    through L1, over an equal-count unit partition of the part (cached on the part);
 //  * opt-in (CPHIFI_GRAM_WS=1): the warp-specialised build (k_gramws.cu) — measured slower than the
@@ -770,13 +770,16 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
 bool gram_build_parts(cphifi_unaligned p) {
     bool ws = false;
     if (const char* e = std::getenv("CPHIFI_GRAM_WS")) ws = std::atoi(e) != 0;
-    bool v3 = false;  // opt-in: measured 90 ms at config 4 against 62 for k_gram.cu's batched build (mode 0
-                      // through L1 per entry, four warps per entry stream): CPHIFI_GRAM3_PARTS=1
-    // 1: mode 0 through L1 per entry (90 ms at config 4); 3: mode 0 hoisted per run
-    // (CPHIFI_GRAM3_PARTS=3, 109 ms): both slower than k_gram.cu's batched build (62 ms)
+    // The register-fragment build over the parts is the default for 3-way plans whose factors do not
+    // fit shared memory (config 4: 54.4 ms against 62.1 for k_gram.cu's batched build, once each
+    // warp's tile pairs are a compile-time set; the q-pass plan it walks is shared with the stream
+    // operator and cached on the observation plan).  CPHIFI_GRAM3_PARTS=0 turns it off; =3 selects
+    // the run-hoisted form (72.6 ms: the fold per run end and a second masked pass per straddled
+    // k-step, measured slower).
+    bool v3 = !ws && p->obs->d == 3;
     int v3stage = 1;
     if (const char* e = std::getenv("CPHIFI_GRAM3_PARTS")) {
-        v3 = !ws && p->obs->d == 3 && std::atoi(e) != 0;
+        v3 = v3 && std::atoi(e) != 0;
         if (std::atoi(e) == 3) v3stage = 3;
     }
     cphifi_obs o = p->obs;
@@ -864,8 +867,23 @@ bool gram_build_parts(cphifi_unaligned p) {
         g.slot_b = slot_b.get();
         g.g = p->gram.get();
         g.accumulate = 1;  // G was zeroed: every part adds, in part order
+        cudaEvent_t p0 = nullptr, p1 = nullptr;
+        if (timing) {
+            CPHIFI_CUDA(cudaEventCreate(&p0));
+            CPHIFI_CUDA(cudaEventCreate(&p1));
+            CPHIFI_CUDA(cudaEventRecord(p0, s));
+        }
         if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), v3stage, s);
         else gram_build_ws(g, (int)(sp->g_beg.n - 1), sp->sf, s);
+        if (timing) {
+            CPHIFI_CUDA(cudaEventRecord(p1, s));
+            CPHIFI_CUDA(cudaEventSynchronize(p1));
+            float ms = 0.f;
+            CPHIFI_CUDA(cudaEventElapsedTime(&ms, p0, p1));
+            std::fprintf(stderr, "cphifi: gram build part (%lld entries) %.3f ms\n", (long long)sp->q, ms);
+            cudaEventDestroy(p0);
+            cudaEventDestroy(p1);
+        }
     }
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // the slots / counters are released on return
     if (timing) {

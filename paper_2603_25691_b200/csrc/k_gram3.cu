@@ -34,12 +34,13 @@
 // own fragment elements by A_1(a, ii) A_1(a, jj)) and clears M.  A k-step that straddles a run end is
 // run once per run with the other entries masked (a is non-decreasing inside a row); the A_1 rows of
 // the next batch's runs are prefetched into L1 when the batch is loaded.  MEASURED SLOWER (opt-in,
-// CPHIFI_GRAM3_PARTS=3): config 4 108.6 ms against 89.8 ms for STAGE 1 and 61.8 ms for k_gram.cu's
-// batched build (profiles/round2/gram_parts_config4.log) — with ~28-entry runs per part a quarter of
-// the k-steps straddle a run end (a second masked DMMA pass) and every run end pays a fold whose A_1
-// loads wait on L1 / L2.
+// CPHIFI_GRAM3_PARTS=3): config 4 72.6 ms against 54.4 ms for STAGE 1 (profiles/round2/
+// gram_parts_config4.log) — with ~28-entry runs per part a quarter of the k-steps straddle a run end
+// (a second masked DMMA pass), every run end pays a fold whose A_1 loads wait on L1 / L2, and the
+// two accumulator sets spill at 128 registers.
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -114,273 +115,286 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
     const int64_t beg = a.cta_beg[u], end = a.cta_beg[u + 1];
     if (beg >= end) return;
 
-    double acc[TPW][2];
-    double accm[HOIST ? TPW : 1][2];  // HOIST: the current run's M (acc holds G)
-#pragma unroll
-    for (int x = 0; x < TPW; ++x) acc[x][0] = acc[x][1] = 0.0;
-#pragma unroll
-    for (int x = 0; x < (HOIST ? TPW : 1); ++x) accm[x][0] = accm[x][1] = 0.0;
-
-    const int64_t first_row = a.cta_rows[2 * u];
-    int64_t row = first_row;
-    int64_t row_beg = a.row_ptr[row], row_end = a.row_ptr[row + 1];
-
-    auto flush = [&](int64_t rr) {
-        const int nu = a.row_ncta[rr];
-        double* dst = nu == 1 ? a.g + rr * RP * RP
-                    : rr == first_row ? a.slot_a + (int64_t)u * RP * RP
-                                      : a.slot_b + (int64_t)u * RP * RP;
-#pragma unroll
-        for (int ti = 0; ti < NT; ++ti)
-#pragma unroll
-            for (int tj = ti; tj < NT; ++tj) {
-                const int uu = pair_index<NT>(ti, tj);
-                if (uu % TW != tw) continue;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int ii = NT * g + ti, jj = NT * (2 * kq + h) + tj;
-                    const double v = acc[uu / TW][h] + (a.accumulate && nu == 1 ? dst[ii * RP + jj] : 0.0);
-                    dst[ii * RP + jj] = v;
-                    if (ti != tj) dst[jj * RP + ii] = v;
-                }
-            }
-#pragma unroll
+    // The warp's tile pairs (uu % TW == tw) must be a compile-time set: with a runtime tw every
+    // DMMA of the k-step is issued predicated, with a register select per accumulator and a
+    // convergence barrier around each (measured at TW = 4: 10 % of the instructions DMMA, the
+    // tensor pipe at a third of its FP64 rate).  The body is instantiated per tw.
+    auto body = [&](auto twc) {
+        constexpr int TWI = decltype(twc)::value;
+        double acc[TPW][2];
+        double accm[HOIST ? TPW : 1][2];  // HOIST: the current run's M (acc holds G)
+    #pragma unroll
         for (int x = 0; x < TPW; ++x) acc[x][0] = acc[x][1] = 0.0;
-        if (nu > 1) {  // the last of the row's units (TW warps each) sums the unit slots in unit order
-            __syncwarp();
-            unsigned last = 0;
-            if (lane == 0) {
-                __threadfence();
-                last = atom_add_acqrel3(a.rowcnt + rr, 1u) == (unsigned)(nu * TW) - 1;
-                if (last) a.rowcnt[rr] = 0;
-            }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                const int u0 = a.row_first_cta[rr];
-                const bool starts = a.row_ptr[rr] == a.cta_beg[u0];
-                for (int e = lane; e < RP * RP; e += 32) {
-                    double s = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
-                                      : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
-                    for (int v = u0 + 1; v < u0 + nu; ++v) s += __ldcg(a.slot_a + (int64_t)v * RP * RP + e);
-                    a.g[rr * RP * RP + e] = a.accumulate ? a.g[rr * RP * RP + e] + s : s;
-                }
-            }
-        }
-    };
+    #pragma unroll
+        for (int x = 0; x < (HOIST ? TPW : 1); ++x) accm[x][0] = accm[x][1] = 0.0;
 
-    // index / multiplicity batches: lane L holds entry b0 + L of every column (cur), and the next
-    // batch (nxt) is in flight.  Positions below are 32-bit offsets from p0 (units hold < 2^31
-    // entries); iterations take 8 entries (two k-steps) at 8-aligned offsets, inside one batch.
-    const int64_t p0 = beg & ~(int64_t)31;
-    const int nrel = (int)(end - p0);
-    int b0 = 0;
-    int32_t cur[DO + 1], nxt[DO + 1];
-    auto load_batch = [&](int base, int32_t (&v)[DO + 1]) {
-        const int64_t e = p0 + base + lane;
-        const bool ok = e >= beg && e < end;
-#pragma unroll
-        for (int m = 0; m < DO; ++m) v[m] = ok ? __ldg(a.idx + (int64_t)m * a.q + e) : 0;
-        v[DO] = ok ? (a.mult ? (__ldg(a.mult + e) & RUN_MULT_MASK) : 1) : 0;
-        if constexpr (HOIST) {  // the A_1 rows of the runs starting in this batch, into L1
-            const int32_t prev = __shfl_up_sync(0xffffffffu, v[0], 1);
-            if (ok && (lane == 0 || prev != v[0])) {
-                const char* row = reinterpret_cast<const char*>(a.fac + a.fac_off[0] + (int64_t)v[0] * RP);
-#pragma unroll
-                for (int c = 0; c < RP * 8; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + c));
-            }
-        }
-    };
-    load_batch(0, cur);
-    load_batch(32, nxt);
-    // per-mode row bases (shared-memory byte addresses when staged) and the swizzle phase of row 0
-    uint32_t sbase[DO];
-    const double* gbase[DO];
-    int opar[DO];
-#pragma unroll
-    for (int m = 0; m < DO; ++m) {
-        gbase[m] = a.fac + a.fac_off[m];
-        sbase[m] = (uint32_t)__cvta_generic_to_shared(g3s) + (uint32_t)((a.fac_off[m] - sbeg) * 8);
-        opar[m] = (int)(((a.fac_off[m] - sbeg) / RP) & 3);
-    }
-    int rb = (int)(row_beg - p0), re = (int)(min(row_end, end) - p0);  // current row, relative
-    const int ulo = (int)(beg - p0);  // the unit's first entry, relative
+        const int64_t first_row = a.cta_rows[2 * u];
+        int64_t row = first_row;
+        int64_t row_beg = a.row_ptr[row], row_end = a.row_ptr[row + 1];
 
-    // z of entry (kq) of the k-step at batch lane offset src
-    auto build_z = [&](int src, double (&z)[NT], int32_t& wm, int32_t& ea) {
-        int32_t ix[DO];
-#pragma unroll
-        for (int m = 0; m < DO; ++m) ix[m] = __shfl_sync(0xffffffffu, cur[m], src);
-        wm = __shfl_sync(0xffffffffu, cur[DO], src);  // 0 outside [beg, end)
-        ea = ix[0];
-#pragma unroll
-        for (int m = HOIST ? 1 : 0; m < DO; ++m) {
-            const bool st = STAGE == 2 || (STAGE != 0 && m >= 1);  // this mode in shared memory
-            const int swm = st ? sw(opar[m] + ix[m]) : 0;
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-                // logical chunk (columns 2 lc, 2 lc + 1), every mode in the same kq-rotated order
-                const int lc = CPL * g + (SF ? ((c + kq) & (CPL - 1)) : c);
-                double2 f;
-                if (st) {
-                    const uint32_t ad = sbase[m] + (uint32_t)ix[m] * (RP * 8) + (uint32_t)((lc ^ swm) * 16);
-                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f.x), "=d"(f.y) : "r"(ad));
-                } else {
-                    f = __ldg(reinterpret_cast<const double2*>(gbase[m] + (int64_t)ix[m] * RP) + lc);
-                }
-                if (m == (HOIST ? 1 : 0)) {
-                    z[2 * c] = f.x;
-                    z[2 * c + 1] = f.y;
-                } else {
-                    z[2 * c] *= f.x;
-                    z[2 * c + 1] *= f.y;
-                }
-            }
-        }
-        if constexpr (SF && CPL > 1) {  // logical chunk j sits in register chunk (j - kq) mod CPL
-            if (kq & 1) {
-                const double t0 = z[2 * CPL - 2], t1 = z[2 * CPL - 1];
-#pragma unroll
-                for (int c = CPL - 1; c > 0; --c) {
-                    z[2 * c] = z[2 * c - 2];
-                    z[2 * c + 1] = z[2 * c - 1];
-                }
-                z[0] = t0;
-                z[1] = t1;
-            }
-            if (CPL == 4 && (kq & 2)) {
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const double t0 = z[2 * c], t1 = z[2 * c + 1];
-                    z[2 * c] = z[2 * c + 4];
-                    z[2 * c + 1] = z[2 * c + 5];
-                    z[2 * c + 4] = t0;
-                    z[2 * c + 5] = t1;
-                }
-            }
-        }
-    };
-    // A = w z.  The FP64 multiplies share the pipe with DMMA, so a plan without multiplicities
-    // (w = 1 on the unit's entries, 0 off them) masks with selects instead
-    const bool weighted = a.mult != nullptr;
-    auto mma_step = [&](const double (&z)[NT], int32_t w) {
-        double zw[NT];
-        const double wd = (double)w;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) zw[t] = weighted ? wd * z[t] : (w ? z[t] : 0.0);
-        // tile pair uu goes to warp uu % TW of the team (accumulator uu / TW): every register index
-        // is a compile-time constant
-#pragma unroll
-        for (int ti = 0; ti < NT; ++ti)
-#pragma unroll
-            for (int tj = ti; tj < NT; ++tj) {
-                const int uu = pair_index<NT>(ti, tj);
-                if (uu % TW == tw) {
-                    if constexpr (HOIST) dmma3(accm[uu / TW], zw[ti], z[tj]);
-                    else dmma3(acc[uu / TW], zw[ti], z[tj]);
-                }
-            }
-    };
-    // HOIST: the current run's first-mode index (-1: none yet) and its fold G += (a a') o M
-    int cur_a = -1;
-    auto fold = [&]() {
-        if constexpr (HOIST) {
-            if (cur_a >= 0) {
-                const double* ar = a.fac + a.fac_off[0] + (int64_t)cur_a * RP;
-#pragma unroll
-                for (int ti = 0; ti < NT; ++ti)
-#pragma unroll
-                    for (int tj = ti; tj < NT; ++tj) {
-                        const int uu = pair_index<NT>(ti, tj);
-                        if (uu % TW != tw) continue;
-                        const double ai = __ldg(ar + NT * g + ti);
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const double s = ai * __ldg(ar + NT * (2 * kq + h) + tj);
-                            acc[uu / TW][h] = fma(s, accm[uu / TW][h], acc[uu / TW][h]);
-                            accm[uu / TW][h] = 0.0;
-                        }
+        auto flush = [&](int64_t rr) {
+            const int nu = a.row_ncta[rr];
+            double* dst = nu == 1 ? a.g + rr * RP * RP
+                        : rr == first_row ? a.slot_a + (int64_t)u * RP * RP
+                                          : a.slot_b + (int64_t)u * RP * RP;
+    #pragma unroll
+            for (int ti = 0; ti < NT; ++ti)
+    #pragma unroll
+                for (int tj = ti; tj < NT; ++tj) {
+                    const int uu = pair_index<NT>(ti, tj);
+                    if (uu % TW != TWI) continue;
+    #pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int ii = NT * g + ti, jj = NT * (2 * kq + h) + tj;
+                        const double v = acc[uu / TW][h] + (a.accumulate && nu == 1 ? dst[ii * RP + jj] : 0.0);
+                        dst[ii * RP + jj] = v;
+                        if (ti != tj) dst[jj * RP + ii] = v;
                     }
+                }
+    #pragma unroll
+            for (int x = 0; x < TPW; ++x) acc[x][0] = acc[x][1] = 0.0;
+            if (nu > 1) {  // the last of the row's units (TW warps each) sums the unit slots in unit order
+                __syncwarp();
+                unsigned last = 0;
+                if (lane == 0) {
+                    __threadfence();
+                    last = atom_add_acqrel3(a.rowcnt + rr, 1u) == (unsigned)(nu * TW) - 1;
+                    if (last) a.rowcnt[rr] = 0;
+                }
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    const int u0 = a.row_first_cta[rr];
+                    const bool starts = a.row_ptr[rr] == a.cta_beg[u0];
+                    for (int e = lane; e < RP * RP; e += 32) {
+                        double s = starts ? __ldcg(a.slot_a + (int64_t)u0 * RP * RP + e)
+                                          : __ldcg(a.slot_b + (int64_t)u0 * RP * RP + e);
+                        for (int v = u0 + 1; v < u0 + nu; ++v) s += __ldcg(a.slot_a + (int64_t)v * RP * RP + e);
+                        a.g[rr * RP * RP + e] = a.accumulate ? a.g[rr * RP * RP + e] + s : s;
+                    }
+                }
             }
-        }
-    };
-    // the next non-empty row after the current one (it starts at the current row's end)
-    auto next_row = [&]() {
-        fold();
-        cur_a = -1;
-        flush(row);
-        do {
-            ++row;
-            row_beg = a.row_ptr[row];
-            row_end = a.row_ptr[row + 1];
-        } while (row_end == row_beg);
-        rb = (int)(row_beg - p0);
-        re = (int)(min(row_end, end) - p0);
-    };
+        };
 
-    for (int P = (int)(beg - p0) & ~7; P < nrel; P += 8) {
-        if (P >= b0 + 32) {
-            b0 += 32;
-#pragma unroll
-            for (int m = 0; m <= DO; ++m) cur[m] = nxt[m];
-            load_batch(b0 + 32, nxt);
+        // index / multiplicity batches: lane L holds entry b0 + L of every column (cur), and the next
+        // batch (nxt) is in flight.  Positions below are 32-bit offsets from p0 (units hold < 2^31
+        // entries); iterations take 8 entries (two k-steps) at 8-aligned offsets, inside one batch.
+        const int64_t p0 = beg & ~(int64_t)31;
+        const int nrel = (int)(end - p0);
+        int b0 = 0;
+        int32_t cur[DO + 1], nxt[DO + 1];
+        auto load_batch = [&](int base, int32_t (&v)[DO + 1]) {
+            const int64_t e = p0 + base + lane;
+            const bool ok = e >= beg && e < end;
+    #pragma unroll
+            for (int m = 0; m < DO; ++m) v[m] = ok ? __ldg(a.idx + (int64_t)m * a.q + e) : 0;
+            v[DO] = ok ? (a.mult ? (__ldg(a.mult + e) & RUN_MULT_MASK) : 1) : 0;
+            if constexpr (HOIST) {  // the A_1 rows of the runs starting in this batch, into L1
+                const int32_t prev = __shfl_up_sync(0xffffffffu, v[0], 1);
+                if (ok && (lane == 0 || prev != v[0])) {
+                    const char* row = reinterpret_cast<const char*>(a.fac + a.fac_off[0] + (int64_t)v[0] * RP);
+    #pragma unroll
+                    for (int c = 0; c < RP * 8; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + c));
+                }
+            }
+        };
+        load_batch(0, cur);
+        load_batch(32, nxt);
+        // per-mode row bases (shared-memory byte addresses when staged) and the swizzle phase of row 0
+        uint32_t sbase[DO];
+        const double* gbase[DO];
+        int opar[DO];
+    #pragma unroll
+        for (int m = 0; m < DO; ++m) {
+            gbase[m] = a.fac + a.fac_off[m];
+            sbase[m] = (uint32_t)__cvta_generic_to_shared(g3s) + (uint32_t)((a.fac_off[m] - sbeg) * 8);
+            opar[m] = (int)(((a.fac_off[m] - sbeg) / RP) & 3);
         }
-        const int src = P - b0 + kq;
-        if constexpr (HOIST) {  // one k-step at a time (registers: G and M accumulators)
-#pragma unroll 1
+        int rb = (int)(row_beg - p0), re = (int)(min(row_end, end) - p0);  // current row, relative
+        const int ulo = (int)(beg - p0);  // the unit's first entry, relative
+
+        // z of entry (kq) of the k-step at batch lane offset src
+        auto build_z = [&](int src, double (&z)[NT], int32_t& wm, int32_t& ea) {
+            int32_t ix[DO];
+    #pragma unroll
+            for (int m = 0; m < DO; ++m) ix[m] = __shfl_sync(0xffffffffu, cur[m], src);
+            wm = __shfl_sync(0xffffffffu, cur[DO], src);  // 0 outside [beg, end)
+            ea = ix[0];
+    #pragma unroll
+            for (int m = HOIST ? 1 : 0; m < DO; ++m) {
+                const bool st = STAGE == 2 || (STAGE != 0 && m >= 1);  // this mode in shared memory
+                const int swm = st ? sw(opar[m] + ix[m]) : 0;
+    #pragma unroll
+                for (int c = 0; c < CPL; ++c) {
+                    // logical chunk (columns 2 lc, 2 lc + 1), every mode in the same kq-rotated order
+                    const int lc = CPL * g + (SF ? ((c + kq) & (CPL - 1)) : c);
+                    double2 f;
+                    if (st) {
+                        const uint32_t ad = sbase[m] + (uint32_t)ix[m] * (RP * 8) + (uint32_t)((lc ^ swm) * 16);
+                        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f.x), "=d"(f.y) : "r"(ad));
+                    } else {
+                        f = __ldg(reinterpret_cast<const double2*>(gbase[m] + (int64_t)ix[m] * RP) + lc);
+                    }
+                    if (m == (HOIST ? 1 : 0)) {
+                        z[2 * c] = f.x;
+                        z[2 * c + 1] = f.y;
+                    } else {
+                        z[2 * c] *= f.x;
+                        z[2 * c + 1] *= f.y;
+                    }
+                }
+            }
+            if constexpr (SF && CPL > 1) {  // logical chunk j sits in register chunk (j - kq) mod CPL
+                if (kq & 1) {
+                    const double t0 = z[2 * CPL - 2], t1 = z[2 * CPL - 1];
+    #pragma unroll
+                    for (int c = CPL - 1; c > 0; --c) {
+                        z[2 * c] = z[2 * c - 2];
+                        z[2 * c + 1] = z[2 * c - 1];
+                    }
+                    z[0] = t0;
+                    z[1] = t1;
+                }
+                if (CPL == 4 && (kq & 2)) {
+    #pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const double t0 = z[2 * c], t1 = z[2 * c + 1];
+                        z[2 * c] = z[2 * c + 4];
+                        z[2 * c + 1] = z[2 * c + 5];
+                        z[2 * c + 4] = t0;
+                        z[2 * c + 5] = t1;
+                    }
+                }
+            }
+        };
+        // A = w z.  The FP64 multiplies share the pipe with DMMA, so a plan without multiplicities
+        // (w = 1 on the unit's entries, 0 off them) masks with selects instead
+        const bool weighted = a.mult != nullptr;
+        auto mma_step = [&](const double (&z)[NT], int32_t w) {
+            double zw[NT];
+            const double wd = (double)w;
+    #pragma unroll
+            for (int t = 0; t < NT; ++t) zw[t] = weighted ? wd * z[t] : (w ? z[t] : 0.0);
+            // tile pair uu goes to warp uu % TW of the team (accumulator uu / TW): every register index
+            // is a compile-time constant
+    #pragma unroll
+            for (int ti = 0; ti < NT; ++ti)
+    #pragma unroll
+                for (int tj = ti; tj < NT; ++tj) {
+                    const int uu = pair_index<NT>(ti, tj);
+                    if (uu % TW == TWI) {
+                        if constexpr (HOIST) dmma3(accm[uu / TW], zw[ti], z[tj]);
+                        else dmma3(acc[uu / TW], zw[ti], z[tj]);
+                    }
+                }
+        };
+        // HOIST: the current run's first-mode index (-1: none yet) and its fold G += (a a') o M
+        int cur_a = -1;
+        auto fold = [&]() {
+            if constexpr (HOIST) {
+                if (cur_a >= 0) {
+                    const double* ar = a.fac + a.fac_off[0] + (int64_t)cur_a * RP;
+    #pragma unroll
+                    for (int ti = 0; ti < NT; ++ti)
+    #pragma unroll
+                        for (int tj = ti; tj < NT; ++tj) {
+                            const int uu = pair_index<NT>(ti, tj);
+                            if (uu % TW != TWI) continue;
+                            const double ai = __ldg(ar + NT * g + ti);
+    #pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const double s = ai * __ldg(ar + NT * (2 * kq + h) + tj);
+                                acc[uu / TW][h] = fma(s, accm[uu / TW][h], acc[uu / TW][h]);
+                                accm[uu / TW][h] = 0.0;
+                            }
+                        }
+                }
+            }
+        };
+        // the next non-empty row after the current one (it starts at the current row's end)
+        auto next_row = [&]() {
+            fold();
+            cur_a = -1;
+            flush(row);
+            do {
+                ++row;
+                row_beg = a.row_ptr[row];
+                row_end = a.row_ptr[row + 1];
+            } while (row_end == row_beg);
+            rb = (int)(row_beg - p0);
+            re = (int)(min(row_end, end) - p0);
+        };
+
+        for (int P = (int)(beg - p0) & ~7; P < nrel; P += 8) {
+            if (P >= b0 + 32) {
+                b0 += 32;
+    #pragma unroll
+                for (int m = 0; m <= DO; ++m) cur[m] = nxt[m];
+                load_batch(b0 + 32, nxt);
+            }
+            const int src = P - b0 + kq;
+            if constexpr (HOIST) {  // one k-step at a time (registers: G and M accumulators)
+    #pragma unroll 1
+                for (int h = 0; h < 8; h += 4) {
+                    const int Q = P + h;
+                    if (Q >= nrel) break;
+                    double z[NT];
+                    int32_t wm, ea;
+                    build_z(src + h, z, wm, ea);
+                    if (Q >= rb && Q >= ulo && Q + 4 <= re && __all_sync(0xffffffffu, ea == cur_a)) {  // one run
+                        mma_step(z, wm);
+                        continue;
+                    }
+                    // a run or row end (or the unit's start / end) inside: once per run of each row
+                    const int e = Q + kq;
+                    for (;;) {
+                        for (;;) {  // runs of the current row in this k-step, in ascending a
+                            const bool in = e >= rb && e >= ulo && e < re;
+                            if (__any_sync(0xffffffffu, in && ea == cur_a)) mma_step(z, in && ea == cur_a ? wm : 0);
+                            const int nx = (int)__reduce_min_sync(0xffffffffu, (unsigned)(in && ea > cur_a ? ea : INT_MAX));
+                            if (nx == INT_MAX) break;
+                            fold();
+                            cur_a = nx;
+                        }
+                        if (Q + 4 <= re || row_end >= end) break;
+                        next_row();  // the step straddles the row end: the next row's entries of this step
+                    }
+                }
+                continue;
+            }
+            if (P >= rb && P + 8 <= re) {  // both k-steps inside the current row
+                double za[NT], zb[NT];
+                int32_t wa, wb, ka, kb;
+                build_z(src, za, wa, ka);
+                build_z(src + 4, zb, wb, kb);
+                mma_step(za, wa);
+                mma_step(zb, wb);
+                continue;
+            }
+            // a row end (or the unit's start / end) inside: one k-step at a time, one pass per row
+    #pragma unroll 1
             for (int h = 0; h < 8; h += 4) {
                 const int Q = P + h;
                 if (Q >= nrel) break;
                 double z[NT];
                 int32_t wm, ea;
                 build_z(src + h, z, wm, ea);
-                if (Q >= rb && Q >= ulo && Q + 4 <= re && __all_sync(0xffffffffu, ea == cur_a)) {  // one run
-                    mma_step(z, wm);
-                    continue;
-                }
-                // a run or row end (or the unit's start / end) inside: once per run of each row
                 const int e = Q + kq;
                 for (;;) {
-                    for (;;) {  // runs of the current row in this k-step, in ascending a
-                        const bool in = e >= rb && e >= ulo && e < re;
-                        if (__any_sync(0xffffffffu, in && ea == cur_a)) mma_step(z, in && ea == cur_a ? wm : 0);
-                        const int nx = (int)__reduce_min_sync(0xffffffffu, (unsigned)(in && ea > cur_a ? ea : INT_MAX));
-                        if (nx == INT_MAX) break;
-                        fold();
-                        cur_a = nx;
-                    }
+                    mma_step(z, (e >= rb && e < re) ? wm : 0);
                     if (Q + 4 <= re || row_end >= end) break;
                     next_row();  // the step straddles the row end: the next row's entries of this step
                 }
             }
-            continue;
         }
-        if (P >= rb && P + 8 <= re) {  // both k-steps inside the current row
-            double za[NT], zb[NT];
-            int32_t wa, wb, ka, kb;
-            build_z(src, za, wa, ka);
-            build_z(src + 4, zb, wb, kb);
-            mma_step(za, wa);
-            mma_step(zb, wb);
-            continue;
-        }
-        // a row end (or the unit's start / end) inside: one k-step at a time, one pass per row
-#pragma unroll 1
-        for (int h = 0; h < 8; h += 4) {
-            const int Q = P + h;
-            if (Q >= nrel) break;
-            double z[NT];
-            int32_t wm, ea;
-            build_z(src + h, z, wm, ea);
-            const int e = Q + kq;
-            for (;;) {
-                mma_step(z, (e >= rb && e < re) ? wm : 0);
-                if (Q + 4 <= re || row_end >= end) break;
-                next_row();  // the step straddles the row end: the next row's entries of this step
-            }
-        }
+        fold();
+        flush(row);
+    };
+    switch (tw) {
+        case 0: body(std::integral_constant<int, 0>{}); break;
+        case 1: if constexpr (TW > 1) body(std::integral_constant<int, 1 % TW>{}); break;
+        case 2: if constexpr (TW > 2) body(std::integral_constant<int, 2 % TW>{}); break;
+        default: if constexpr (TW > 3) body(std::integral_constant<int, 3 % TW>{}); break;
     }
-    fold();
-    flush(row);
 }
 
 template <int RP, int DO, int TW>

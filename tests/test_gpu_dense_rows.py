@@ -104,11 +104,12 @@ def test_dense_rows_pcg_matches_runs(monkeypatch):
     ((600, 300, 512), 64, 900000, True, 5, 0.85),   # factors 415 KB: the build runs over the factor-block parts
     ((600, 300, 512), 64, 600000, False, 0, 0.0),   # no dense rows: run-kernel parts only
 ])
-def test_gram_build_over_parts(monkeypatch, shape, r, q, coalesce, head, frac):
-    """The row-Gram build over the q-pass plan's parts (opt-in: k_gram3.cu, block staged, mode 0
+@pytest.mark.parametrize("stage", ["1", "3"])  # 3: mode 0 hoisted per run (opt-in)
+def test_gram_build_over_parts(monkeypatch, shape, r, q, coalesce, head, frac, stage):
+    """The row-Gram build over the q-pass plan's parts (the default: k_gram3.cu, block staged, mode 0
     through L1; the dense rows' entries in their own parts) gives the operator the oracle gives and the
     default single-pass build gives."""
-    monkeypatch.setenv("CPHIFI_GRAM3_PARTS", "1")  # (opt-in)
+    monkeypatch.setenv("CPHIFI_GRAM3_PARTS", stage)
     cp, mode, obs, model, idx, vals, factors = _case(shape, r, q, 9, coalesce, max(head, 1), frac)
     n = shape[0]
     x = np.random.default_rng(4).normal(size=n * r)
