@@ -771,8 +771,8 @@ bool gram_build_parts(cphifi_unaligned p) {
     bool ws = false;
     if (const char* e = std::getenv("CPHIFI_GRAM_WS")) ws = std::atoi(e) != 0;
     // The register-fragment build over the parts is the default for 3-way plans whose factors do not
-    // fit shared memory (config 4: 54.4 ms against 62.1 for k_gram.cu's batched build, once each
-    // warp's tile pairs are a compile-time set; the q-pass plan it walks is shared with the stream
+    // fit shared memory (config 4: 40.7 ms against 62.1 for k_gram.cu's batched build, with each
+    // warp's tile pairs a compile-time set and single-warp teams; the q-pass plan it walks is shared with the stream
     // operator and cached on the observation plan).  CPHIFI_GRAM3_PARTS=0 turns it off; =3 selects
     // the run-hoisted form (72.6 ms: the fold per run end and a second masked pass per straddled
     // k-step, measured slower).

@@ -16,9 +16,11 @@
 //   * A(i, k) = w_k z_k(NT i + ti), B(k, j) = z_k(NT j + tj): lane (g, kq) holds both for all tiles,
 //     so every upper-triangle tile pair (ti <= tj) is one DMMA on registers — NT (NT + 1) / 2 DMMA per
 //     k-step with no shared-memory traffic besides the factor rows;
-//   * TW warps (a team) walk the same entries and split the tile pairs (RP = 64: 36 tiles, 18 per
-//     warp); a CTA holds 16 / TW teams, each with its own contiguous entry range (equal-count, split
-//     rows finished by the last arrival summing the units' slots in unit order: deterministic);
+//   * TW warps (a team) walk the same entries and split the tile pairs; a CTA holds (its warps) / TW
+//     teams, each with its own contiguous entry range (equal-count, split rows finished by the last
+//     arrival summing the units' slots in unit order: deterministic).  TW = 1 throughout: at RP = 64
+//     a warp holds all 36 tile pairs with 8 warps per CTA (g3_threads; CPHIFI_GRAM3_TW=4 splits them
+//     over 4 warps of 16, measured 54.3 against 40.7 ms at config 4);
 //   * the plan's indices and multiplicities arrive 32 entries at a time, one coalesced load per
 //     column, one batch ahead, and are handed to the k-step's lanes by shuffles; the factors are
 //     staged in shared memory when they fit (config 3: 3 x 64 KB), else read through L1.
@@ -47,8 +49,12 @@
 namespace cphifi {
 namespace {
 
-constexpr int G3T = 512;           // threads per CTA
-constexpr int G3W = G3T / 32;      // warps per CTA
+// threads per CTA: 16 warps of single-warp teams (TW = 1) up to RP = 32; at RP = 64 a single warp
+// holds all 36 upper-triangle tile pairs (72 accumulator doubles) only with up to 255 registers, so
+// 8 warps per CTA (2 per scheduler: one warp's 36 DMMAs cover the other's z build) — TW > 1 (warps
+// splitting the pairs, each rebuilding the same z) spends ~75 instructions per 9 DMMAs
+template <int RP, int TW>
+constexpr int g3_threads() { return (RP == 64 && TW == 1) ? 256 : 512; }
 
 __device__ __forceinline__ void dmma3(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -66,7 +72,8 @@ struct G3 {
     static constexpr int NT = RP / 8;
     static constexpr int NUP = NT * (NT + 1) / 2;
     static constexpr int TPW = (NUP + TW - 1) / TW;  // tile pairs per warp
-    static constexpr int TEAMS = G3W / TW;
+    static constexpr int THREADS = g3_threads<RP, TW>();
+    static constexpr int TEAMS = THREADS / 32 / TW;
 };
 
 // index of tile pair (ti, tj), ti <= tj, row-major over the upper triangle of NT x NT tiles
@@ -79,7 +86,7 @@ __host__ __device__ constexpr int pair_index(int ti, int tj) {
 // constant along the plan's runs, read through L1); 3 = as 1 with mode 0 hoisted per run (DO = 2);
 // 0 = none staged
 template <int RP, int DO, int TW, int STAGE>
-__global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int units) {
+__global__ void __launch_bounds__(g3_threads<RP, TW>(), 1) gram3_kernel(const GramArgs a, int units) {
     constexpr bool SF = STAGE > 0;
     constexpr bool HOIST = STAGE == 3;
     static_assert(!HOIST || DO == 2, "gram build v3: the hoisted form is for 3-way plans");
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(G3T, 1) gram3_kernel(const GramArgs a, int uni
     const int64_t sbeg = STAGE == 2 ? 0 : a.fac_off[1];  // first staged double (a row boundary)
     if constexpr (SF) {
         const double2* src = reinterpret_cast<const double2*>(a.fac + sbeg);
-        for (int64_t e = tid; e < (a.fac_total - sbeg) / 2; e += G3T) {
+        for (int64_t e = tid; e < (a.fac_total - sbeg) / 2; e += C::THREADS) {
             const int jj = (int)(e % (RP / 2));
             const int64_t grow = e / (RP / 2);
             reinterpret_cast<double2*>(g3s)[e] = __ldg(src + (e - jj) + (jj ^ sw(grow)));
@@ -405,16 +412,16 @@ void launch_g3(const GramArgs& a, int units, int stage, cudaStream_t s) {
     if (stage == 2) {
         auto kern = gram3_kernel<RP, DO, TW, 2>;
         func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        kern<<<grid, G3T, fbytes, s>>>(a, units);
+        kern<<<grid, C::THREADS, fbytes, s>>>(a, units);
     } else if (stage == 1) {
         auto kern = gram3_kernel<RP, DO, TW, 1>;
         func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        kern<<<grid, G3T, fbytes, s>>>(a, units);
+        kern<<<grid, C::THREADS, fbytes, s>>>(a, units);
     } else if (stage == 3) {
         if constexpr (DO == 2) {
             auto kern = gram3_kernel<RP, DO, TW, 3>;
             func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            kern<<<grid, G3T, fbytes, s>>>(a, units);
+            kern<<<grid, C::THREADS, fbytes, s>>>(a, units);
         } else {
             throw_invalid("gram build v3: the hoisted form needs a 3-way plan");
         }
@@ -430,6 +437,16 @@ void launch_g3_do(const GramArgs& a, int units, int stage, cudaStream_t s) {
         case 4: launch_g3<RP, 4, TW>(a, units, stage, s); break;
         default: throw_invalid("gram build v3: needs 2..4 other modes");
     }
+}
+
+// team width at RP = 64: 1 (8 warps per CTA, 255 registers) unless CPHIFI_GRAM3_TW=4 (16 warps, the
+// 36 tile pairs split over 4 warps)
+int g3_tw64() {
+    static const int tw = [] {
+        const char* e = std::getenv("CPHIFI_GRAM3_TW");
+        return e && std::atoi(e) == 4 ? 4 : 1;
+    }();
+    return tw;
 }
 
 }  // namespace
@@ -453,7 +470,7 @@ int gram3_units_per_sm(int64_t rp) {
     switch (rp) {
         case 16: return G3<16, 1>::TEAMS;
         case 32: return G3<32, 1>::TEAMS;
-        default: return G3<64, 4>::TEAMS;
+        default: return g3_tw64() == 4 ? G3<64, 4>::TEAMS : G3<64, 1>::TEAMS;
     }
 }
 
@@ -462,7 +479,10 @@ void gram3_build(const GramArgs& a, int units, int stage, cudaStream_t s) {
     switch (a.rp) {
         case 16: launch_g3_do<16, 1>(a, units, stage, s); break;
         case 32: launch_g3_do<32, 1>(a, units, stage, s); break;
-        case 64: launch_g3_do<64, 4>(a, units, stage, s); break;
+        case 64:
+            if (g3_tw64() == 4) launch_g3_do<64, 4>(a, units, stage, s);
+            else launch_g3_do<64, 1>(a, units, stage, s);
+            break;
         default: throw_invalid("gram build v3: padded rank must be 16, 32 or 64");
     }
 }
