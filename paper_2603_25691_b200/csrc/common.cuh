@@ -274,6 +274,11 @@ struct cphifi_unaligned_s {
     double* hv_hx = nullptr;
     double* hv_hy = nullptr;
     bool hv_failed = false;
+    int hv_op = -1;                           // operator form baked into hv_exec / hd_exec
+    // large x / y in pinned host memory: [DMA in] operator graph [DMA out] (no host staging copy)
+    cudaGraph_t hd_graph = nullptr;
+    cudaGraphExec_t hd_exec = nullptr;
+    int hd_op = -1;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
     int pcg_graph_rot = -1;                   // basis (0 original, 1 eigenbasis) of the captured graph
     // the whole solve after the right-hand side as one graph: [bnorm, x0, M^-1 r0, init, loop
@@ -289,6 +294,8 @@ struct cphifi_unaligned_s {
         if (pcgf_graph) cudaGraphDestroy(pcgf_graph);
         if (hv_exec) cudaGraphExecDestroy(hv_exec);
         if (hv_graph) cudaGraphDestroy(hv_graph);
+        if (hd_exec) cudaGraphExecDestroy(hd_exec);
+        if (hd_graph) cudaGraphDestroy(hd_graph);
         if (hv_hx) cudaFreeHost(hv_hx);
         if (hv_hy) cudaFreeHost(hv_hy);
     }

@@ -284,3 +284,29 @@ def test_pcg_gram_epilogue_bitwise(cp, monkeypatch):
     wo = orc.solve_unaligned_pcg(sub, orc.PcgConfig(1e-9, 300), ek, orc.sym_eig(sub.v), report=orep)
     assert r1.converged and abs(r1.iterations - orep.iterations) <= 1, (r1.iterations, orep.iterations)
     assert ri.rel(w1, wo) < 1e-6
+
+
+def test_host_matvec_pinned_dma_vs_device(cp):
+    """Large x / y in pinned host memory take the DMA path (cudaMemcpyAsync from / to the caller's
+    buffers around an operator-only graph, no host staging copy): bit-identical to the device call,
+    and re-captured when the operator form changes (stream -> gram)."""
+    import torch
+    from paper_2603_25691_b200 import _capi
+    g = np.random.default_rng(3)
+    shape, r, q = (4096, 64, 48), 32, 400000  # n r = 131072 doubles = 1 MB: the DMA path
+    idx = np.stack([g.integers(0, s, q) for s in shape]).astype(np.int32)
+    obs = cp.ObservationSet(shape, idx, g.normal(size=q), multiset=True, coalesce=True)
+    mode = cp.RkhsMode(np.linspace(0, 1, shape[0]), 0.1, 1e-4)
+    p = cp.make_unaligned_subproblem(obs, cp.KruskalModel([np.zeros((shape[0], r))] +
+                                                          [g.normal(size=(s, r)) for s in shape[1:]]), 0, mode, 1e-6)
+    n = shape[0]
+    for op in ("stream", "gram", "stream"):
+        p.set_operator(op)
+        x = torch.randn(n * r, dtype=torch.float64).pin_memory()
+        y = torch.empty(n * r, dtype=torch.float64).pin_memory()
+        _capi.call("cphifi_unaligned_matvec", p.handle, x.numpy().ctypes.data_as(_capi.c_double_p),
+                   y.numpy().ctypes.data_as(_capi.c_double_p))
+        xd, yd = x.cuda(), torch.empty(n * r, dtype=torch.float64, device="cuda")
+        _capi.call("cphifi_unaligned_matvec_device", p.handle, xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(y, yd.cpu()), op
