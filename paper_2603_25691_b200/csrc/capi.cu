@@ -3465,12 +3465,32 @@ int cphifi_aligned_solve_timed(cphifi_tensor t, cphifi_mode mode, int k, int64_t
             cudaGraph_t g = nullptr;
             cudaGraphExec_t ex = nullptr;
             const int* flag = nullptr;
+            // the Gram V = (*_{m != k} A_m'A_m) does not depend on the MTTKRP: a branch of the graph on a
+            // second stream, concurrent with it (forked and joined inside the capture)
+            cudaStream_t s2 = nullptr;
+            cudaEvent_t efork = nullptr, ejoin = nullptr;
+            CPHIFI_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+            CPHIFI_CUDA(cudaEventCreateWithFlags(&efork, cudaEventDisableTiming));
+            CPHIFI_CUDA(cudaEventCreateWithFlags(&ejoin, cudaEventDisableTiming));
+            struct Side {
+                cudaStream_t s;
+                cudaEvent_t a, b;
+                ~Side() {
+                    cudaEventDestroy(a);
+                    cudaEventDestroy(b);
+                    cudaStreamDestroy(s);
+                }
+            } side{s2, efork, ejoin};
             try {
                 CPHIFI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
                 try {
+                    CPHIFI_CUDA(cudaEventRecord(efork, s));
+                    CPHIFI_CUDA(cudaStreamWaitEvent(s2, efork, 0));
+                    gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), s2);
+                    CPHIFI_CUDA(cudaEventRecord(ejoin, s2));
                     mttkrp_dev(t, k, r, fptr, b.get(), work);
-                    gram_kr(t->d, t->shape.data(), r, fptr.data(), k, v.get(), s);
                     flag = decoupled_dev(mode, r, b.get(), uv.get(), sv.get(), w.get(), t1, core);
+                    CPHIFI_CUDA(cudaStreamWaitEvent(s, ejoin, 0));
                 } catch (...) {
                     cudaGraph_t junk = nullptr;
                     cudaStreamEndCapture(s, &junk);
