@@ -401,7 +401,8 @@ void ensure_runs(cphifi_unaligned p) {
     // the plan's q-pass plan for this padded rank, shared by every subproblem on the plan; the key
     // also carries the tuning knobs the build reads
     std::string key = std::to_string(p->rp) + "/" + std::to_string(p->runs_sf);
-    for (const char* v : {"CPHIFI_DENSE_MIN", "CPHIFI_DENSE_MAX_GB", "CPHIFI_RUNS_RUNCOST", "CPHIFI_RUNS_LAYOUT"}) {
+    for (const char* v : {"CPHIFI_DENSE_MIN", "CPHIFI_DENSE_MAX_GB", "CPHIFI_RUNS_RUNCOST", "CPHIFI_RUNS_LAYOUT",
+                          "CPHIFI_RUNS_VAR", "CPHIFI_XRUNS"}) {
         const char* e = std::getenv(v);
         key += std::string("/") + (e ? e : "-");
     }
@@ -413,6 +414,7 @@ void ensure_runs(cphifi_unaligned p) {
             auto Q = std::make_shared<QpassPlan>();
             if (!build_run_parts(p, p->runs_sf, *Q)) *Q = QpassPlan();
             for (const auto& sp : Q->parts) Q->max_warps = std::max(Q->max_warps, sp.warps);
+            for (const auto& sp : Q->dense_parts) Q->max_warps = std::max(Q->max_warps, sp.warps);
             slot = Q;
             built = true;
         }
@@ -431,6 +433,57 @@ void ensure_runs(cphifi_unaligned p) {
     if (std::getenv("CPHIFI_SOLVE_TIMING"))  // developer: host time of the build (or the cache hit)
         std::fprintf(stderr, "cphifi: q-pass plan %s in %.3f ms\n", built ? "built" : "shared",
                      1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+}
+
+// The right-hand side B = sampled_mttkrp(observed values) (observations.hpp:186-188) through the run
+// kernel over every part of the q-pass plan (the run kernel's parts, then the dense rows' parts:
+// every entry once, weights = the entries' values, summed over duplicates in a coalesced plan), added
+// into a zeroed Yhat in part order.  False when the plan has no parts or a part lacks its values.
+bool rhs_over_parts(cphifi_unaligned p, FusedArgs a) {
+    if (std::getenv("CPHIFI_RHS_PARTS") && std::atoi(std::getenv("CPHIFI_RHS_PARTS")) == 0) return false;
+    ensure_runs(p);
+    if (!p->qp || p->qp->parts.empty()) return false;
+    const QpassPlan& Q = *p->qp;
+    std::vector<const StreamPart*> all;
+    for (const auto& sp : Q.parts) all.push_back(&sp);
+    for (const auto& sp : Q.dense_parts) all.push_back(&sp);
+    for (const StreamPart* sp : all)
+        if (sp->q > 0 && (!sp->vals || sp->padded || sp->warps == 0)) return false;
+    cudaStream_t s = p->obs->ctx->stream;
+    const int dl = p->obs->d - 2;
+    CPHIFI_CUDA(cudaMemsetAsync(a.yhat_rm, 0, sizeof(double) * p->n * p->rp, s));
+    for (const StreamPart* spp : all) {
+        const StreamPart& sp = *spp;
+        if (sp.q == 0) continue;
+        RunsArgs b;
+        b.rp = p->rp;
+        b.ldq = sp.ldq;
+        b.dother = p->obs->d - 1;
+        b.idx = sp.idx;
+        b.mult = sp.mult;
+        b.vals = sp.vals;
+        b.fac = a.fac;
+        for (int m = 0; m < b.dother; ++m) b.fac_off[m] = a.fac_off[m];
+        b.fac_off[dl] = a.fac_off[dl] + sp.row_lo * p->rp;
+        b.fac_total = b.fac_off[dl] + sp.rows * p->rp;
+        b.row_ptr = sp.row_ptr;
+        b.run_start = sp.run_start.get();
+        b.run_i1 = sp.run_i1.get();
+        b.nruns = sp.nruns;
+        b.warps = sp.warps;
+        b.warp_beg = sp.warp_beg.get();
+        b.warp_rows = sp.warp_rows.get();
+        b.row_first_w = sp.row_first_w.get();
+        b.row_nw = sp.row_nw.get();
+        b.xhat_rm = a.xhat_rm;
+        b.yhat_rm = a.yhat_rm;
+        b.slot_a = p->runs_slot_a.get();
+        b.slot_b = p->runs_slot_b.get();
+        b.rowcnt = a.rowcnt;
+        b.accumulate = 1;
+        runs_scatter_gather(b, sp.sf, s);
+    }
+    return true;
 }
 
 // The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
@@ -650,6 +703,7 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
         sp.rows = nl;
         sp.idx = o->idx_o.get();
         sp.mult = mult ? o->mult.get() : nullptr;
+        sp.vals = o->values.n ? o->values.get() : nullptr;
         sp.row_ptr = o->row_ptr.get();
         sp.sf = sf_all;
         finish_part(p, sp, rows.get(), nw);
@@ -714,6 +768,11 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
             sp.mult = sp.mult_own.get();
         }
         gather_i32(rows.get(), perm.get(), lo, cnt, rows_h.get(), s);
+        if (o->values.n && !(runs && xruns) && cnt > 0) {  // the observed values, for B over the parts
+            sp.vals_own.alloc(cnt + OBS_PAD);
+            gather_f64(o->values.get(), perm.get(), lo, cnt, sp.vals_own.get(), s);
+            sp.vals = sp.vals_own.get();
+        }
         if (runs && xruns && cnt > 0) {  // runs padded to even lengths for k_xruns.cu
             DevBuf<int32_t> rs(cnt + 1);
             const int64_t nr = build_run_starts(rows_h.get(), sp.idx_own.get(), cnt, rs.get(), s);
@@ -751,7 +810,9 @@ bool build_run_parts(cphifi_unaligned p, int64_t sf_all, QpassPlan& Q) {
     };
     std::vector<StreamPart> parts(H), dparts(dense ? H : 0);
     for (int h = 0; h < H; ++h) make_part(parts[h], h, true);
-    for (int h = 0; h < (dense ? H : 0); ++h) make_part(dparts[h], H + h, false);
+    // the dense rows' parts get run tables and warp ranges too: the right-hand side B runs the run
+    // kernel over every entry (k_runs.cu, RunsArgs::vals)
+    for (int h = 0; h < (dense ? H : 0); ++h) make_part(dparts[h], H + h, true);
     Q.parts = std::move(parts);
     Q.dense_parts = std::move(dparts);
     return true;
@@ -2066,7 +2127,7 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // B = sampled_mttkrp(obs, zhat, k) with the observed values (observations.hpp:186-188)
         FusedArgs a = fused_args(p, PH_B);
         a.weights = obs->values.get();
-        launch_phase_b(p, a);
+        if (!(p->stream && rhs_over_parts(p, a))) launch_phase_b(p, a);
         allreduce_yhat(p);
         p->b.alloc(n * r);
         rm_to_cm(yhat_result(p), n, p->rp, r, p->b.get(), s);

@@ -176,6 +176,8 @@ struct StreamPart {
     cphifi::DevBuf<int64_t> warp_beg, warp_rows;
     cphifi::DevBuf<int32_t> row_first_w, row_nw;
     bool padded = false;                 // runs padded to even lengths, run starts flagged (k_xruns.cu)
+    cphifi::DevBuf<double> vals_own;     // the observed values in part order (the right-hand side B)
+    const double* vals = nullptr;
     int64_t q_real = 0;                  // entries before the padding
     int g_units = 0;                     // the row-Gram build's equal-count units (built on first use)
     cphifi::DevBuf<int64_t> g_beg, g_rows;

@@ -84,7 +84,10 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
 //  RV_A1REG the run's A_1 row kept in registers from u = Xhat o A_1 to the fold (one row read per run
 //           instead of two);
 //  RV_XREG  the row's Xhat row kept in registers (read once per row instead of once per run).
-constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8;
+//  RV_RHS   the right-hand side B instead of the operator: each entry's weight is its observed value
+//           (RunsArgs::vals; summed over duplicates in a coalesced plan) — no dot with Xhat, no
+//           reduction over the lane group, no multiplicity.
+constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32;
 
 template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
@@ -92,7 +95,8 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
     constexpr bool IDXS = (VAR & RV_IDXS) != 0, PRED = (VAR & RV_PRED) != 0, A1REG = (VAR & RV_A1REG) != 0,
-                   XREG = (VAR & RV_XREG) != 0;
+                   XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0;
+    static_assert(!RHS || (!PIPE && !IDXS), "RV_RHS: the plain step loop");
     constexpr int WIN = MULT ? 16 : 32;  // RV_IDXS window (entries)
     static_assert(!IDXS || (DO == 2 && STEP <= WIN / 2), "RV_IDXS: 3-way plans, window >= 2 steps");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -242,6 +246,9 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     // pipelining: the loads of step k + 1 overlap the dot reduction and update of step k)
     double u[VPL], v[VPL], racc[VPL];  // racc: this lane's share of its lane group's row accumulator
     double a1r[A1REG ? VPL : 1], xr[XREG ? VPL : 1];
+    double rv[B];  // RV_RHS: the step's entries' values
+#pragma unroll
+    for (int b = 0; b < B; ++b) rv[b] = 0.0;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) racc[k] = 0.0;
     if constexpr (XREG) lds_row<G, VPL>(xr, xrs, gl, odd);
@@ -268,6 +275,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             const bool ok = FULL || ent < rend;
             if constexpr (!FULL) ent = min(ent, rend - 1);
             const double* rows[DO];
+            if constexpr (RHS) rv[b] = __ldg(a.vals + cbase + ent);
             if constexpr (IDXS) {
                 rows[1] = fs[1] + __shfl_sync(0xffffffffu, widx, ent - wnd) * RP;
                 if constexpr (MULT) mu[b] = __shfl_sync(0xffffffffu, widx, 16 + ent - wnd);
@@ -298,6 +306,11 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         }
     };
     auto dots = [&](const double (&z)[B][VPL], double (&d)[B]) {
+        if constexpr (RHS) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) d[b] = rv[b];
+            return;
+        }
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             double s0 = 0.0, s1 = 0.0;
@@ -311,11 +324,11 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     };
     auto finish = [&](int p, int rend, const double (&z)[B][VPL], const int (&mu)[B], double (&d)[B], auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        group_reduce<B, G>(d, lane);
+        if constexpr (!RHS) group_reduce<B, G>(d, lane);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             double s = d[b];
-            if constexpr (MULT) s *= (double)mu[b];
+            if constexpr (MULT && !RHS) s *= (double)mu[b];
             if constexpr (!FULL) s = p + g * B + b < rend ? s : 0.0;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) v[k] = fma(s, z[b][k], v[k]);
@@ -338,7 +351,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         if constexpr (XREG) {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) u[k] = xr[k];
-        } else {
+        } else if constexpr (!RHS) {
             lds_row<G, VPL>(u, xrs, gl, odd);  // u = Xhat(i,:) o A_1(a,:), one pair at a time
         }
         if constexpr (A1REG) lds_row<G, VPL>(a1r, a1, gl, odd);
@@ -560,6 +573,11 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
 
 template <int RP, int DO, bool MULT>
 void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
+    if (a.vals) {  // the right-hand side B, on the default layout
+        if constexpr (RP == 64) launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_RHS>(a, sf, s);
+        else launch4<RP, DO, MULT, 4, 2, false, 16, 64, RV_RHS>(a, sf, s);
+        return;
+    }
     const int lay = runs_layout();
     if constexpr (RP == 64) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 1, true>(a, sf, s);

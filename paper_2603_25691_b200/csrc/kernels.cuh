@@ -215,6 +215,8 @@ struct RunsArgs {
     double* slot_b = nullptr;            // warps x rp (its last row when shared)
     unsigned* rowcnt = nullptr;          // n arrival counters, zero between launches
     int accumulate = 0;                  // add into yhat_rm (stream parts) instead of overwriting
+    const double* vals = nullptr;        // non-null: the right-hand side B (weights = the entries' values,
+                                         // no dot with Xhat) instead of the operator's q-pass
 };
 // Dense rows of a 3-way plan (k_dense_rows.cu): the q-pass of rows whose cells are mostly drawn as
 // two DMMA GEMMs per row over the row's multiplicity grid W_i (n1p x n2p int32, zero-padded).

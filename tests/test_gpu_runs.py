@@ -86,3 +86,29 @@ def test_gram_ws_build_vs_oracle(monkeypatch, shape, r, q, coalesce, zipf):
     assert np.linalg.norm(y_ws - y_v) / np.linalg.norm(y_v) < 1e-12
     y_o = orc.unaligned_matvec_stream(shape, 0, idx, [None] + factors[1:], mode.kernel(), 1e-4, 1e-6, x)
     assert np.linalg.norm(y_ws - y_o) / np.linalg.norm(y_o) < 1e-12
+
+
+@pytest.mark.parametrize("shape,r,q,coalesce,zipf,dense", [
+    ((600, 50, 256), 64, 80000, True, False, "0"),     # one part (the plan itself)
+    ((600, 64, 512), 64, 120000, True, True, "0"),     # two factor-block parts
+    ((600, 60, 900), 32, 90000, False, False, "0"),    # parts without multiplicities
+    ((300, 40, 512), 64, 900000, True, True, "0.3"),   # dense rows: their parts carry B's entries too
+])
+def test_rhs_over_parts_vs_oracle_and_stream(monkeypatch, shape, r, q, coalesce, zipf, dense):
+    """The right-hand side B = sampled_mttkrp(observed values) (observations.hpp:186-188) through the
+    run kernel over every part of the q-pass plan (weights = values, no dot) against the oracle's
+    streaming restatement and against the streaming kernel (CPHIFI_RHS_PARTS=0)."""
+    monkeypatch.setenv("CPHIFI_DENSE_MIN", dense)
+    cp, mode, obs, model, idx, vals, factors = _case(shape, r, q, 13, coalesce, zipf)
+    n = shape[0]
+    p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+    plan = p.qpass_plan()
+    assert plan["parts"] >= 1
+    if dense != "0":
+        assert plan["dense_rows"] > 0
+    b_orc = orc.sampled_mttkrp_stream(shape, 0, idx, vals, [None] + factors[1:], n)
+    assert np.linalg.norm(p.b - b_orc) / np.linalg.norm(b_orc) < 1e-12
+    monkeypatch.setenv("CPHIFI_RHS_PARTS", "0")
+    obs2 = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    p2 = cp.make_unaligned_subproblem(obs2, model, 0, mode, 1e-6)
+    assert np.linalg.norm(p.b - p2.b) / np.linalg.norm(p2.b) < 1e-13
