@@ -486,6 +486,27 @@ bool rhs_over_parts(cphifi_unaligned p, FusedArgs a) {
     return true;
 }
 
+// The q-pass of the dense rows (k_dense_rows.cu): written into Yhat, not accumulated.
+void launch_dense_rows(cphifi_unaligned p, const FusedArgs& a, cudaStream_t s) {
+    const QpassPlan& Q = *p->qp;
+    DenseRowsArgs dr;
+    dr.rp = p->rp;
+    dr.n1 = Q.dense_n1;
+    dr.n2 = Q.dense_n2;
+    dr.n1p = Q.dense_n1p;
+    dr.n2p = Q.dense_n2p;
+    dr.nd = Q.dense_nd;
+    dr.rows = Q.dense_rows.get();
+    dr.w = Q.dense_w.get();
+    dr.a1 = a.fac + a.fac_off[0];
+    dr.a2 = a.fac + a.fac_off[1];
+    dr.xhat_rm = a.xhat_rm;
+    dr.yhat_rm = a.yhat_rm;
+    dr.partial = p->dense_partial.get();
+    dr.cnt = p->dense_cnt.get();
+    dense_rows_qpass(dr, p->obs->ctx->num_sms, s);
+}
+
 // The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
 // exist: with more than one part, Yhat is zeroed and every part adds into it, Yhat(i) =
 // (0 + part 0) + part 1 + ... in part order.
@@ -498,7 +519,29 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
         const int dl = p->obs->d - 2;  // the blocked (last) other mode's column / packed factor
         const bool acc = Q.parts.size() > 1;
         if (acc) CPHIFI_CUDA(cudaMemsetAsync(a.yhat_rm, 0, sizeof(double) * p->n * p->rp, s));
+        // the dense rows (no entries in any part: written, not accumulated) on the plan's second
+        // stream, concurrent with the parts — their CTAs fill the SMs the run kernel's last warps
+        // leave idle.  Sequential under cphifi_unaligned_matvec_timed (per-kernel device times) and
+        // with CPHIFI_DENSE_CONCURRENT=0.
+        bool conc = Q.dense_nd > 0 && !g_dense_event;
+        if (const char* e = std::getenv("CPHIFI_DENSE_CONCURRENT")) conc = conc && std::atoi(e) != 0;
+        int fork_at = 0;  // (developer: CPHIFI_DENSE_FORK_AT = the part the dense launch is issued after)
+        if (const char* e = std::getenv("CPHIFI_DENSE_FORK_AT")) fork_at = std::atoi(e);
+        if (conc) {
+            if (!p->side) {
+                CPHIFI_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+                CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming));
+                CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_join, cudaEventDisableTiming));
+            }
+            CPHIFI_CUDA(cudaEventRecord(p->side_fork, s));
+            CPHIFI_CUDA(cudaStreamWaitEvent(p->side, p->side_fork, 0));
+        }
+        int part_i = 0;
         for (const StreamPart& sp : Q.parts) {
+            if (conc && part_i++ == fork_at) {
+                launch_dense_rows(p, a, p->side);
+                CPHIFI_CUDA(cudaEventRecord(p->side_join, p->side));
+            }
             if (sp.q == 0) continue;
             RunsArgs b;
             b.rp = p->rp;
@@ -532,24 +575,12 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
             CPHIFI_CUDA(cudaEventRecord(g_dense_event, s));
             g_dense_recorded = true;
         }
-        if (Q.dense_nd > 0) {  // the dense rows (no entries in any part): written, not accumulated
-            DenseRowsArgs dr;
-            dr.rp = p->rp;
-            dr.n1 = Q.dense_n1;
-            dr.n2 = Q.dense_n2;
-            dr.n1p = Q.dense_n1p;
-            dr.n2p = Q.dense_n2p;
-            dr.nd = Q.dense_nd;
-            dr.rows = Q.dense_rows.get();
-            dr.w = Q.dense_w.get();
-            dr.a1 = a.fac + a.fac_off[0];
-            dr.a2 = a.fac + a.fac_off[1];
-            dr.xhat_rm = a.xhat_rm;
-            dr.yhat_rm = a.yhat_rm;
-            dr.partial = p->dense_partial.get();
-            dr.cnt = p->dense_cnt.get();
-            dense_rows_qpass(dr, p->obs->ctx->num_sms, s);
+        if (conc && part_i <= fork_at) {  // (fork point past the last part)
+            launch_dense_rows(p, a, p->side);
+            CPHIFI_CUDA(cudaEventRecord(p->side_join, p->side));
         }
+        if (conc) CPHIFI_CUDA(cudaStreamWaitEvent(s, p->side_join, 0));
+        else if (Q.dense_nd > 0) launch_dense_rows(p, a, s);
         return;
     }
     if (p->stream) stream_scatter_gather(a, p->grid, p->stream_sf, p->obs->ctx->stream);

@@ -281,6 +281,10 @@ struct cphifi_unaligned_s {
     cudaGraph_t hd_graph = nullptr;
     cudaGraphExec_t hd_exec = nullptr;
     int hd_op = -1;
+    // the dense rows' q-pass on a second stream, concurrent with the run kernel's parts (they write
+    // disjoint rows of Yhat): forked after the Yhat zeroing, joined before the output GEMM
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_fork = nullptr, side_join = nullptr;
     int pcg_graph_op = -1;                    // operator form the graph was captured with
     int pcg_graph_rot = -1;                   // basis (0 original, 1 eigenbasis) of the captured graph
     // the whole solve after the right-hand side as one graph: [bnorm, x0, M^-1 r0, init, loop
@@ -298,6 +302,9 @@ struct cphifi_unaligned_s {
         if (hv_graph) cudaGraphDestroy(hv_graph);
         if (hd_exec) cudaGraphExecDestroy(hd_exec);
         if (hd_graph) cudaGraphDestroy(hd_graph);
+        if (side_fork) cudaEventDestroy(side_fork);
+        if (side_join) cudaEventDestroy(side_join);
+        if (side) cudaStreamDestroy(side);
         if (hv_hx) cudaFreeHost(hv_hx);
         if (hv_hy) cudaFreeHost(hv_hy);
     }
