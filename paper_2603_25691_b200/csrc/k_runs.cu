@@ -87,7 +87,10 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
 //  RV_RHS   the right-hand side B instead of the operator: each entry's weight is its observed value
 //           (RunsArgs::vals; summed over duplicates in a coalesced plan) — no dot with Xhat, no
 //           reduction over the lane group, no multiplicity.
-constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32;
+//  RV_S32   the step loop's shared-memory reads (plan indices, factor rows) through 32-bit shared
+//           addresses computed once (ld.shared with explicit addresses) instead of generic pointers
+//           the compiler converts (and, at 128 registers, re-derives) every step.
+constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, RV_S32 = 64;
 
 template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
     constexpr bool IDXS = (VAR & RV_IDXS) != 0, PRED = (VAR & RV_PRED) != 0, A1REG = (VAR & RV_A1REG) != 0,
-                   XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0;
+                   XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0, S32 = (VAR & RV_S32) != 0;
     static_assert(!RHS || (!PIPE && !IDXS), "RV_RHS: the plain step loop");
     constexpr int WIN = MULT ? 16 : 32;  // RV_IDXS window (entries)
     static_assert(!IDXS || (DO == 2 && STEP <= WIN / 2), "RV_IDXS: 3-way plans, window >= 2 steps");
@@ -136,12 +139,15 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         }
     }
     const double* fs[DO];  // fs[m]: staged rows of mode m (m >= 1)
+    uint32_t fs_s[DO];     // (their shared-memory addresses, RV_S32)
     {
         int so = 0;
         fs[0] = nullptr;
+        fs_s[0] = 0;
 #pragma unroll
         for (int m = 1; m < DO; ++m) {
             fs[m] = sfac + so;
+            fs_s[m] = tma::smem_u32(fs[m]);
             so += frows[m] * RP;
         }
     }
@@ -200,6 +206,12 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     };
     // column `col` of the ring is a circular buffer of RING entries: entry rel sits at rel mod RING
     auto ring_at = [&](int rel, int col) -> int32_t { return ring[col * RING + (rel & (RING - 1))]; };
+    const uint32_t ring_s = tma::smem_u32(ring);
+    auto ring_at32 = [&](int rel, int col) -> int32_t {
+        int32_t v;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(ring_s + 4u * (unsigned)(col * RING + (rel & (RING - 1)))));
+        return v;
+    };
 
     // ---- runs, rows ------------------------------------------------------------------------
     int r = 0;  // runs and rows fit 32 bits (plans hold < 2^31 entries)
@@ -279,9 +291,14 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             if constexpr (IDXS) {
                 rows[1] = fs[1] + __shfl_sync(0xffffffffu, widx, ent - wnd) * RP;
                 if constexpr (MULT) mu[b] = __shfl_sync(0xffffffffu, widx, 16 + ent - wnd);
-            } else {
+            } else if constexpr (!S32) {
 #pragma unroll
                 for (int m = 1; m < DO; ++m) rows[m] = fs[m] + ring_at(ent, m) * RP;
+            }
+            uint32_t rows_s[DO];
+            if constexpr (S32 && !IDXS) {
+#pragma unroll
+                for (int m = 1; m < DO; ++m) rows_s[m] = fs_s[m] + (uint32_t)ring_at32(ent, m) * (RP * 8);
             }
             if (PRED && !FULL && !ok) {
 #pragma unroll
@@ -292,17 +309,27 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
 #pragma unroll
             for (int t = 0; t < VPL / 2; ++t) {
                 const int c = col_of<G>(t, gl, odd);
-                double2 x = *reinterpret_cast<const double2*>(rows[1] + c);
+                double2 x;
+                if constexpr (S32 && !IDXS) {
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "r"(rows_s[1] + 8u * c));
+                } else {
+                    x = *reinterpret_cast<const double2*>(rows[1] + c);
+                }
 #pragma unroll
                 for (int m = 2; m < DO; ++m) {
-                    const double2 f = *reinterpret_cast<const double2*>(rows[m] + c);
+                    double2 f;
+                    if constexpr (S32 && !IDXS) {
+                        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f.x), "=d"(f.y) : "r"(rows_s[m] + 8u * c));
+                    } else {
+                        f = *reinterpret_cast<const double2*>(rows[m] + c);
+                    }
                     x.x *= f.x;
                     x.y *= f.y;
                 }
                 z[b][2 * t] = x.x;
                 z[b][2 * t + 1] = x.y;
             }
-            if constexpr (MULT && !IDXS) mu[b] = ring_at(ent, DO);
+            if constexpr (MULT && !IDXS) mu[b] = S32 ? ring_at32(ent, DO) : ring_at(ent, DO);
         }
     };
     auto dots = [&](const double (&z)[B][VPL], double (&d)[B]) {
@@ -539,10 +566,15 @@ int runs_layout() {
 }
 // inner-loop variant (RV_* bits; + 16: 12 warps per CTA, up to 168 registers) of the G = 8, B = 2
 // layout at RP = 64 (CPHIFI_RUNS_VAR)
+// The default inner loop: 32-bit shared addresses + loads of in-run entries only in the partial
+// step (RV_S32 | RV_PRED; config 4: run kernel 4.01 -> 3.87 ms per application, either alone no
+// faster — profiles/round2/runs_variants_config4.txt).  CPHIFI_RUNS_VAR selects another (0: the plain
+// loop).
+constexpr int RV_DEFAULT = RV_S32 | RV_PRED;
 int runs_var() {
     static const int var = [] {
         const char* e = std::getenv("CPHIFI_RUNS_VAR");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : RV_DEFAULT;
     }();
     return var;
 }
@@ -565,10 +597,16 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 82: launch4<RP, DO, MULT, 8, 4, false, 8, 64, 0>(a, sf, s); return;
             case 83: launch4<RP, DO, MULT, 8, 3, false, 12, 64, 0>(a, sf, s); return;
             case 84: launch4<RP, DO, MULT, 8, 4, false, 12, 64, 0>(a, sf, s); return;
+            case 0: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 0>(a, sf, s); return;
+            case 64: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32>(a, sf, s); return;
+            case 70: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED | RV_A1REG>(a, sf, s); return;
+            case 74: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED | RV_XREG>(a, sf, s); return;
+            case 86: launch4<RP, DO, MULT, 8, 2, false, 12, 64, RV_S32 | RV_PRED | RV_A1REG | RV_XREG>(a, sf, s); return;
             default: break;
         }
     }
-    launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
+    if (runs_var() == 0) launch4<RP, DO, MULT, 8, 2, false, 16, 64, 0>(a, sf, s);
+    else launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
 }
 
 template <int RP, int DO, bool MULT>
@@ -586,9 +624,11 @@ void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
     } else if constexpr (RP == 32) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
         else if (lay == 2) launch4<RP, DO, MULT, 4, 1, true>(a, sf, s);
-        else launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
+        else if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
+        else launch4<RP, DO, MULT, 4, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
     } else {
-        launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
+        if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
+        else launch4<RP, DO, MULT, 4, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
     }
 }
 
@@ -620,7 +660,7 @@ static int shape_nw(int64_t rp) {
     if (rp != 64 || runs_layout() != 0) return 16;
     const int v = runs_var();
     if (v == 81 || v == 82) return 8;
-    return (v & 16) || v == 80 || v == 83 || v == 84 ? 12 : 16;
+    return (v & 16) || v == 80 || v == 83 || v == 84 || v == 86 ? 12 : 16;
 }
 static int shape_ch(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 32 : 64; }
 
