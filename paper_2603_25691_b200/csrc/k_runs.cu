@@ -90,7 +90,8 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
 //  RV_S32   the step loop's shared-memory reads (plan indices, factor rows) through 32-bit shared
 //           addresses computed once (ld.shared with explicit addresses) instead of generic pointers
 //           the compiler converts (and, at 128 registers, re-derives) every step.
-constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, RV_S32 = 64;
+//  RV_CHUNKED the staging test once per stretch of landed entries instead of once per step.
+constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, RV_S32 = 64, RV_CHUNKED = 128;
 
 template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
@@ -400,7 +401,19 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         {
             double za[B][VPL], zb[B][VPL], d[B];
             int ma[B], mb[B];
-            if constexpr (!PIPE) {
+            if constexpr (!PIPE && (VAR & RV_CHUNKED)) {
+                // the staging test once per stretch of landed entries, not once per step: every step
+                // starting at or before pend is inside the run, landed and before the next refill
+                while (p + STEP <= rend) {
+                    window(p);
+                    const int pend = min(min(rend, land_lim) - STEP, refill_at - 1);
+                    for (; p <= pend; p += STEP) {
+                        load(p, rend, za, ma, std::true_type{});
+                        dots(za, d);
+                        finish(p, rend, za, ma, d, std::true_type{});
+                    }
+                }
+            } else if constexpr (!PIPE) {
                 for (; p + STEP <= rend; p += STEP) {
                     window(p);
                     load(p, rend, za, ma, std::true_type{});
@@ -568,9 +581,9 @@ int runs_layout() {
 // layout at RP = 64 (CPHIFI_RUNS_VAR)
 // The default inner loop: 32-bit shared addresses + loads of in-run entries only in the partial
 // step (RV_S32 | RV_PRED; config 4: run kernel 4.01 -> 3.87 ms per application, either alone no
-// faster — profiles/round2/runs_variants_config4.txt).  CPHIFI_RUNS_VAR selects another (0: the plain
-// loop).
-constexpr int RV_DEFAULT = RV_S32 | RV_PRED;
+// faster) + the staging test once per landed stretch (RV_CHUNKED: -> 3.66 ms) —
+// profiles/round2/runs_variants_config4.txt.  CPHIFI_RUNS_VAR selects another (0: the plain loop).
+constexpr int RV_DEFAULT = RV_S32 | RV_PRED | RV_CHUNKED;
 int runs_var() {
     static const int var = [] {
         const char* e = std::getenv("CPHIFI_RUNS_VAR");
@@ -602,6 +615,7 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 70: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED | RV_A1REG>(a, sf, s); return;
             case 74: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED | RV_XREG>(a, sf, s); return;
             case 86: launch4<RP, DO, MULT, 8, 2, false, 12, 64, RV_S32 | RV_PRED | RV_A1REG | RV_XREG>(a, sf, s); return;
+            case 66: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED>(a, sf, s); return;
             default: break;
         }
     }
