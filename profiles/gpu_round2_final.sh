@@ -1,4 +1,6 @@
-# round-2 evidence at HEAD: GPU suite, smoke, bench line, reference arm, launch list of the bench command
+# round-2 evidence at HEAD: GPU suite, smoke, bench line, reference arm, launch list of the bench
+# command, ncu --set full of the headline's dominant kernel (the operator's run kernel: the first 4
+# run-kernel launches are the right-hand side B over the parts)
 set -x
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
@@ -8,3 +10,7 @@ python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.js
 C="python bench.py --steps 20 --warmup 3 --secondary 0 --cpu-seconds 1"
 $C > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_l.log 2>&1; echo "ncu1 rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:runs_kernel -s 4 -c 1 -o gpurun_out/prof_runs_final -f $C > gpurun_out/ncu_f.log 2>&1; echo "ncu2 rc=$?"
+ncu -i gpurun_out/prof_runs_final.ncu-rep --page raw --csv > gpurun_out/runs_final_raw.csv 2>&1
+ncu --set full --clock-control none -k regex:dense_rows_kernel -s 3 -c 1 -o gpurun_out/prof_dense_final -f $C > gpurun_out/ncu_d.log 2>&1; echo "ncu3 rc=$?"
+ncu -i gpurun_out/prof_dense_final.ncu-rep --page raw --csv > gpurun_out/dense_final_raw.csv 2>&1
