@@ -37,7 +37,9 @@
 namespace cphifi {
 namespace {
 
-constexpr int NCH = 4;                // ring chunks per warp
+// ring chunks per warp: 4 of 64 entries, or 2 of 128 (the same ring bytes, half the chunk refills)
+template <int CH>
+__host__ __device__ constexpr int nch_of() { return CH >= 128 ? 2 : 4; }
 constexpr int SMEM_CAP = 226 * 1024;  // opt-in maximum minus a little static shared memory
 
 // CTA shape: NW warps (one CTA per SM), ring chunks of CH plan entries (CH x 4 B per column: one
@@ -45,6 +47,7 @@ constexpr int SMEM_CAP = 226 * 1024;  // opt-in maximum minus a little static sh
 template <int RP, int DO, bool MULT, int NW, int CH>
 struct Lay {
     static constexpr int NCOL = DO + (MULT ? 1 : 0);
+    static constexpr int NCH = nch_of<CH>();
     static constexpr int NBAR = NCH + 3 + 1;       // ring chunks, A_1 slots, Xhat row
     static constexpr int WBUF = 4 * RP;            // doubles per warp: A_1 x 3, Xhat row
     static constexpr size_t bars = 128 + 8 * (size_t)NW * NBAR;
@@ -96,6 +99,7 @@ constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, 
 template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     using L = Lay<RP, DO, MULT, NW, CH>;
+    constexpr int NCH = nch_of<CH>();
     constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
     constexpr bool IDXS = (VAR & RV_IDXS) != 0, PRED = (VAR & RV_PRED) != 0, A1REG = (VAR & RV_A1REG) != 0,
@@ -584,6 +588,7 @@ int runs_layout() {
 // faster) + the staging test once per landed stretch (RV_CHUNKED: -> 3.66 ms) —
 // profiles/round2/runs_variants_config4.txt.  CPHIFI_RUNS_VAR selects another (0: the plain loop).
 constexpr int RV_DEFAULT = RV_S32 | RV_PRED | RV_CHUNKED;
+constexpr int DEF_CH = 128;  // with 2 chunks in flight (nch_of): config 4 3.66 -> 3.62 ms
 int runs_var() {
     static const int var = [] {
         const char* e = std::getenv("CPHIFI_RUNS_VAR");
@@ -616,11 +621,12 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 74: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED | RV_XREG>(a, sf, s); return;
             case 86: launch4<RP, DO, MULT, 8, 2, false, 12, 64, RV_S32 | RV_PRED | RV_A1REG | RV_XREG>(a, sf, s); return;
             case 66: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED>(a, sf, s); return;
+            case 1194: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_DEFAULT>(a, sf, s); return;  // 4 x 64
             default: break;
         }
     }
     if (runs_var() == 0) launch4<RP, DO, MULT, 8, 2, false, 16, 64, 0>(a, sf, s);
-    else launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
+    else launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s);
 }
 
 template <int RP, int DO, bool MULT>
@@ -639,10 +645,10 @@ void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
         else if (lay == 2) launch4<RP, DO, MULT, 4, 1, true>(a, sf, s);
         else if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
-        else launch4<RP, DO, MULT, 4, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
+        else launch4<RP, DO, MULT, 4, 2, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s);
     } else {
         if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
-        else launch4<RP, DO, MULT, 4, 2, false, 16, 64, RV_DEFAULT>(a, sf, s);
+        else launch4<RP, DO, MULT, 4, 2, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s);
     }
 }
 
@@ -676,11 +682,17 @@ static int shape_nw(int64_t rp) {
     if (v == 81 || v == 82) return 8;
     return (v & 16) || v == 80 || v == 83 || v == 84 || v == 86 ? 12 : 16;
 }
-static int shape_ch(int64_t rp) { return rp == 64 && runs_layout() == 3 ? 32 : 64; }
+static int shape_ch(int64_t rp) {
+    if (rp == 64 && runs_layout() == 3) return 32;
+    if (runs_layout() != 0) return 64;
+    const int v = runs_var();
+    return v == RV_DEFAULT ? DEF_CH : 64;
+}
 
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {
     const size_t ncol = (size_t)dother + (mult ? 1 : 0), nw = (size_t)shape_nw(rp), ch = (size_t)shape_ch(rp);
-    return 128 + 8 * nw * (NCH + 4) + sizeof(double) * nw * 4 * rp + sizeof(int32_t) * nw * NCH * ncol * ch +
+    const size_t nch = ch >= 128 ? 2 : 4;
+    return 128 + 8 * nw * (nch + 4) + sizeof(double) * nw * 4 * rp + sizeof(int32_t) * nw * nch * ncol * ch +
            sizeof(double) * (size_t)sf_doubles;
 }
 
