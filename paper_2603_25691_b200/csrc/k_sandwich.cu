@@ -445,6 +445,217 @@ void launch3_rp(const SandArgs& a, cudaStream_t s) {
     CPHIFI_CHECK_LAUNCH();
 }
 
+// ---- v5: v3 with the M operand multicast across a thread-block cluster ------------------------
+// v3's CTAs (128 at config 2) each stream ALL of M (X or the core: n x (r + 8) doubles) next to
+// their 8 rows of F: ~49 MB of L2 -> SM traffic per phase against 8 MB of F, and the phase waits
+// on it (ncu: 11 us per phase, tensor pipe 27 %, L2 11 %).  Here the CL CTAs of a cluster share
+// every M chunk: CTA q copies k-rows [q KC / CL, (q + 1) KC / CL) of the chunk and multicasts them
+// into the same slot of every CTA of the cluster (its F box stays CTA-local), so a CTA pulls 1/CL
+// of M from L2.  A slot is refilled only once every CTA of the cluster is done with it: each CTA
+// arrives on the `empty` barrier of every peer (remote mbarrier arrive) and waits on its own
+// (CL arrivals) before issuing into the slot.  Same fragments, warp split and summation order as
+// v3: bit-identical to it.
+template <int RP>
+struct Sw5Smem {
+    Sw3Smem<RP> s3;
+    uint64_t empty[Sw3<RP>::ST];
+};
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, unsigned cta) {
+    unsigned remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(tma::smem_u32(bar)), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(tma::smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 2-D tensor-map copy multicast to the CTAs of `mask` (same smem offsets, complete_tx on each
+// CTA's barrier at the offset of `bar`)
+__device__ __forceinline__ void tensor_g2s_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                                 uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(tma::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tma::smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+template <int RP, int PH, int CL>
+__global__ void __launch_bounds__(SW3_T) sandwich5_kernel(const SandArgs a, const __grid_constant__ CUtensorMap tm_f,
+                                                          const __grid_constant__ CUtensorMap tm_m, double* core_rm) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Sw5Smem<RP>& sm5 = *reinterpret_cast<Sw5Smem<RP>*>(smem_raw);
+    Sw3Smem<RP>& sm = sm5.s3;
+    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP, NTL = Sw3<RP>::NTL, RB = SW3_RB, ST = Sw3<RP>::ST;
+    constexpr int KS = KC / CL;  // k-rows of every M chunk this CTA copies for the cluster
+    static_assert(KC % CL == 0 && (KS * RPP * 8) % 128 == 0, "multicast slices 128-byte aligned");
+    const int64_t n = a.n;
+    const int r = (int)a.r;
+    const int64_t i0 = (int64_t)blockIdx.x * RB;
+    const int rb = (int)min((int64_t)RB, n - i0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nch = (int)((n + KC - 1) / KC);
+    const unsigned q = cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < ST; ++st) {
+            tma::mbar_init(&sm.full[st], 1);
+            tma::mbar_init(&sm5.empty[st], CL);
+        }
+        tma::fence_mbar_init();
+    }
+    cluster_sync_all();  // every CTA's barriers initialised before a peer's multicast lands
+    auto issue = [&](int c) {  // thread 0: own F box, this CTA's slice of the M chunk to the cluster
+        const int st = c % ST;
+        tma::mbar_expect_tx(&sm.full[st], (unsigned)(sizeof(double) * KC * (RB + RPP)));
+        tma::tensor_g2s_2d(&sm.a[st][0][0], &tm_f, (int)i0, c * KC, &sm.full[st]);
+        tensor_g2s_2d_mc(&sm.b[st][q * KS][0], &tm_m, 0, c * KC + (int)q * KS, &sm.full[st], (uint16_t)((1u << CL) - 1));
+    };
+    if (threadIdx.x == 0)
+        for (int c = 0; c < min(nch, ST); ++c) issue(c);
+    stage_uv<RP, SW3_T, PH>(sm.uv, a.uv, r);
+    double acc[NTL][2];
+#pragma unroll
+    for (int t = 0; t < NTL; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int fi = lane >> 2, fk = lane & 3;
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % ST;
+        tma::mbar_wait(&sm.full[st], (unsigned)((c / ST) & 1));
+#pragma unroll
+        for (int ks = warp; ks < KC / 4; ks += SW3_W) {
+            const int k = 4 * ks + fk;
+            const double av = sm.a[st][k][fi];
+#pragma unroll
+            for (int t = 0; t < NTL; ++t) dmma_sw(acc[t], av, sm.b[st][k][8 * t + fi]);
+        }
+        __syncthreads();  // every warp is done with slot st
+        if (threadIdx.x == 0 && c + ST < nch) {
+            for (unsigned p = 0; p < (unsigned)CL; ++p) mbar_arrive_cluster(&sm5.empty[st], p);
+            mbar_wait_cluster(&sm5.empty[st], (unsigned)((c / ST) & 1));  // the whole cluster is done with st
+            tma::fence_proxy_async();
+            issue(c + ST);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NTL; ++t) {
+        sm.red[warp][fi][8 * t + 2 * fk] = acc[t][0];
+        sm.red[warp][fi][8 * t + 2 * fk + 1] = acc[t][1];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RP; e += SW3_T) {
+        const int qq = e / RP, jj = e % RP;
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < SW3_W; ++w) t += sm.red[w][qq][jj];
+        sm.tt[qq][jj] = t;
+    }
+    stage_uv_wait();
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * RPP; e += SW3_T) {
+        const int qq = e / RPP, jj = e % RPP;
+        if (qq >= rb) continue;
+        const int64_t i = i0 + qq;
+        if (jj >= r) {
+            if constexpr (PH == 1) core_rm[i * RPP + jj] = 0.0;
+            continue;
+        }
+        double c0 = 0.0, c1 = 0.0;  // two chains, summed once: a fixed order (as v3)
+#pragma unroll
+        for (int m = 0; m < RP; m += 2) {
+            c0 = fma(sm.tt[qq][m], sm.uv[m][jj], c0);
+            c1 = fma(sm.tt[qq][m + 1], sm.uv[m + 1][jj], c1);
+        }
+        const double c = c0 + c1;
+        if constexpr (PH == 1) {
+            double out;
+            if (a.op == SW_MUL) {
+                out = c * a.dmat[i + n * jj];
+            } else {
+                const double den = a.e_col[jj] * a.e_row[i] + a.beta;
+                if (den == 0.0) *a.flag = 1;
+                out = c / den;
+            }
+            core_rm[i * RPP + jj] = out;
+        } else {
+            a.y[i + a.ldy * jj] = c;
+        }
+    }
+    cluster_sync_all();  // no CTA leaves while a peer may still arrive on its barriers
+}
+
+template <int RP, int PH, int CL>
+void launch5_ph(const SandArgs& a, const CUtensorMap& tf, const CUtensorMap& tm, double* core_rm, unsigned grid,
+                cudaStream_t s) {
+    auto kern = sandwich5_kernel<RP, PH, CL>;
+    const size_t smem = sizeof(Sw5Smem<RP>);
+    func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(SW3_T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CPHIFI_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tf, tm, core_rm));
+}
+
+// false: no cluster size divides the grid (the caller takes v3)
+template <int RP>
+bool launch5_rp(const SandArgs& a, int cl_max, cudaStream_t s) {
+    constexpr int KC = Sw3<RP>::KC, RPP = Sw3<RP>::RPP;
+    const uint64_t n = (uint64_t)a.n;
+    const unsigned grid = (unsigned)((a.n + SW3_RB - 1) / SW3_RB);
+    int cl = 8;
+    while (cl > 1 && (cl > cl_max || grid % cl != 0 || KC % cl != 0 || ((KC / cl) * RPP * 8) % 128 != 0)) cl /= 2;
+    if (cl < 2) return false;
+    double* core_rm = a.core_out;
+    double* xrm = a.core_out + (size_t)n * RPP;
+    to_rows_padded_kernel<<<(unsigned)std::min<int64_t>(((int64_t)n * RPP + 255) / 256, 4096), 256, 0, s>>>(
+        a.x, a.ldx, (int64_t)n, (int)a.r, RPP, xrm);
+    CPHIFI_CHECK_LAUNCH();
+    CUtensorMap tf1, tf2, tm1, tm2;
+    const uint32_t ks = (uint32_t)(KC / cl);
+    const bool ok = encode_tmap_2d_f64(&tf1, a.ut, n, n, n, SW3_RB, KC) && encode_tmap_2d_f64(&tf2, a.u, n, n, n, SW3_RB, KC) &&
+                    encode_tmap_2d_f64(&tm1, xrm, RPP, n, RPP, RPP, ks) &&
+                    encode_tmap_2d_f64(&tm2, core_rm, RPP, n, RPP, RPP, ks);
+    if (!ok) throw Error(CPHIFI_CUDA_ERROR, "sandwich: tensor map encoding failed");
+    switch (cl) {
+        case 8:
+            launch5_ph<RP, 1, 8>(a, tf1, tm1, core_rm, grid, s);
+            launch5_ph<RP, 2, 8>(a, tf2, tm2, core_rm, grid, s);
+            break;
+        case 4:
+            launch5_ph<RP, 1, 4>(a, tf1, tm1, core_rm, grid, s);
+            launch5_ph<RP, 2, 4>(a, tf2, tm2, core_rm, grid, s);
+            break;
+        default:
+            launch5_ph<RP, 1, 2>(a, tf1, tm1, core_rm, grid, s);
+            launch5_ph<RP, 2, 2>(a, tf2, tm2, core_rm, grid, s);
+            break;
+    }
+    return true;
+}
+
 template <int RP, int RB, int PH>
 void launch2_t(const SandArgs& a, cudaStream_t s) {
     auto kern = sandwich2_kernel<RP, RB, PH>;
@@ -861,6 +1072,23 @@ void sandwich(SandArgs a, int num_sms, cudaStream_t s) {
             case 64: if (launch4_rp<64>(a, s)) return; break;
             default: break;
         }
+    }
+    // v5 (v3 + cluster multicast of the M chunks): opt-in, CPHIFI_SANDWICH_V5=k caps the cluster
+    // size at k.  Measured slower at config 2 (decoupled 26.1 us with v3; v5 with clusters of 2 / 4
+    // / 8: 33.2 / 35.3 / 68.1 us — the cluster-wide slot release per chunk serialises the CTAs the
+    // per-CTA rings kept independent; profiles/round2c/sandwich_v5.txt)
+    int v5 = 0;
+    if (const char* e = std::getenv("CPHIFI_SANDWICH_V5")) v5 = std::atoi(e);
+    if (v3 && v5 >= 2) {
+        bool done = false;
+        switch (a.rp) {
+            case 8: done = launch5_rp<8>(a, v5, s); break;
+            case 16: done = launch5_rp<16>(a, v5, s); break;
+            case 32: done = launch5_rp<32>(a, v5, s); break;
+            case 64: done = launch5_rp<64>(a, v5, s); break;
+            default: break;
+        }
+        if (done) return;
     }
     if (v3) {
         switch (a.rp) {

@@ -60,14 +60,20 @@ def test_decoupled_sandwich_variants(cp, monkeypatch, n, r):
     v = ri.random_spd(g, r)
     ev = orc.sym_eig(v)
     wo = orc.solve_aligned_decoupled(b, ek, ev, 1e-3)
-    for sw, v1, v3, v4 in (("0", "0", "0", "0"), ("1", "1", "0", "0"), ("1", "0", "0", "0"), ("1", "0", "1", "0"),
-                           ("1", "0", "1", "1")):
+    ws = {}
+    for sw, v1, v3, v4, v5 in (("0", "0", "0", "0", "0"), ("1", "1", "0", "0", "0"), ("1", "0", "0", "0", "0"),
+                               ("1", "0", "1", "0", "0"), ("1", "0", "1", "1", "0"), ("1", "0", "1", "0", "8"),
+                               ("1", "0", "1", "0", "2")):
         monkeypatch.setenv("CPHIFI_SANDWICH", sw)
         monkeypatch.setenv("CPHIFI_SANDWICH_V1", v1)
         monkeypatch.setenv("CPHIFI_SANDWICH_V3", v3)  # v3: DMMA (even n >= 512)
         monkeypatch.setenv("CPHIFI_SANDWICH_V4", v4)  # v4: split-K DMMA (opt-in)
+        monkeypatch.setenv("CPHIFI_SANDWICH_V5", v5)  # v5: v3 + cluster multicast (cap on the cluster size)
         w = cp.solve_aligned_decoupled(cp.AlignedSubproblem(b, v, mode), ev)
-        assert ri.rel(w, wo) < 1e-11, (sw, v1, v3, v4)
+        assert ri.rel(w, wo) < 1e-11, (sw, v1, v3, v4, v5)
+        ws[v5 if v3 == "1" and v4 == "0" else None] = w
+    # v5 keeps v3's fragments and summation order: bit-identical
+    assert np.array_equal(ws["8"], ws["0"]) and np.array_equal(ws["2"], ws["0"])
     # zero denominator through the mapped status word (sandwich path)
     monkeypatch.setenv("CPHIFI_SANDWICH", "1")
     mode0 = cp.RkhsMode(ri.identity_points(4), 1.0, 0.0)
@@ -96,14 +102,15 @@ def test_precond_sandwich_variants(cp, monkeypatch):
     p.set_v_eig(ev.u, ev.d)
     x = np.random.default_rng(3).normal(size=c.shape[0] * c.r)
     yo = orc.build_preconditioner(sub, ek, ev).apply(x)
-    for sw, v1, v3, v4 in (("0", "0", "0", "0"), ("1", "1", "0", "0"), ("1", "0", "0", "0"), ("1", "0", "1", "0"),
-                           ("1", "0", "1", "1")):
+    for sw, v1, v3, v4, v5 in (("0", "0", "0", "0", "0"), ("1", "1", "0", "0", "0"), ("1", "0", "0", "0", "0"),
+                               ("1", "0", "1", "0", "0"), ("1", "0", "1", "1", "0"), ("1", "0", "1", "0", "8")):
         monkeypatch.setenv("CPHIFI_SANDWICH", sw)
         monkeypatch.setenv("CPHIFI_SANDWICH_V1", v1)
         monkeypatch.setenv("CPHIFI_SANDWICH_V3", v3)
         monkeypatch.setenv("CPHIFI_SANDWICH_V4", v4)
+        monkeypatch.setenv("CPHIFI_SANDWICH_V5", v5)
         y = cp.build_preconditioner(p).apply(x)
-        assert ri.rel(y, yo) < 1e-12, (sw, v1, v3, v4)
+        assert ri.rel(y, yo) < 1e-12, (sw, v1, v3, v4, v5)
 
 
 def test_pcg_graph_loop_matches_host_loop(cp, monkeypatch):
