@@ -622,6 +622,10 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 86: launch4<RP, DO, MULT, 8, 2, false, 12, 64, RV_S32 | RV_PRED | RV_A1REG | RV_XREG>(a, sf, s); return;
             case 66: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_S32 | RV_PRED>(a, sf, s); return;
             case 1194: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_DEFAULT>(a, sf, s); return;  // 4 x 64
+            // the default inner loop with one entry per lane group and step (2 x 128 ring; 119
+            // registers, no spills): 3.91 vs 3.62 ms at config 4.  (G = 4 with B = 1 / 2 and G = 8
+            // with B = 3 spill 204-664 B at 128 registers.)
+            case 4099: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s); return;
             default: break;
         }
     }
@@ -686,7 +690,7 @@ static int shape_ch(int64_t rp) {
     if (rp == 64 && runs_layout() == 3) return 32;
     if (runs_layout() != 0) return 64;
     const int v = runs_var();
-    return v == RV_DEFAULT ? DEF_CH : 64;
+    return (v == RV_DEFAULT || v >= 4096) ? DEF_CH : 64;
 }
 
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {
