@@ -108,7 +108,10 @@ class VirtualComm:
 
     def __del__(self):
         if getattr(self, "handle", None):
-            _capi.load().cphifi_vcomm_destroy(self.handle)
+            try:
+                _capi.load().cphifi_vcomm_destroy(self.handle)
+            except AttributeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.handle = None
 
 
@@ -167,7 +170,10 @@ class RkhsMode:
 
     def __del__(self):
         if getattr(self, "handle", None):
-            _capi.load().cphifi_mode_destroy(self.handle)
+            try:
+                _capi.load().cphifi_mode_destroy(self.handle)
+            except AttributeError:  # interpreter shutdown: module globals already cleared
+                pass
 
     def size(self) -> int:
         n = ctypes.c_int64()
@@ -403,7 +409,10 @@ class _Handle:
 
     def __del__(self):
         if self.h:
-            getattr(_capi.load(), self.destroy)(self.h)
+            try:
+                getattr(_capi.load(), self.destroy)(self.h)
+            except AttributeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
 

@@ -507,6 +507,14 @@ void launch_dense_rows(cphifi_unaligned p, const FusedArgs& a, cudaStream_t s) {
     dense_rows_qpass(dr, p->obs->ctx->num_sms, s);
 }
 
+// the plan's second stream (and its fork / join events), created on first use
+void ensure_side_stream(cphifi_unaligned p) {
+    if (p->side) return;
+    CPHIFI_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming));
+    CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_join, cudaEventDisableTiming));
+}
+
 // The operator's q-pass (not the RHS build) runs the run kernel over the plan's parts when they
 // exist: with more than one part, Yhat is zeroed and every part adds into it, Yhat(i) =
 // (0 + part 0) + part 1 + ... in part order.
@@ -528,11 +536,7 @@ void launch_phase_b(cphifi_unaligned p, FusedArgs a) {
         int fork_at = 0;  // (developer: CPHIFI_DENSE_FORK_AT = the part the dense launch is issued after)
         if (const char* e = std::getenv("CPHIFI_DENSE_FORK_AT")) fork_at = std::atoi(e);
         if (conc) {
-            if (!p->side) {
-                CPHIFI_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
-                CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming));
-                CPHIFI_CUDA(cudaEventCreateWithFlags(&p->side_join, cudaEventDisableTiming));
-            }
+            ensure_side_stream(p);
             CPHIFI_CUDA(cudaEventRecord(p->side_fork, s));
             CPHIFI_CUDA(cudaStreamWaitEvent(p->side, p->side_fork, 0));
         }
@@ -916,7 +920,16 @@ bool gram_build_parts(cphifi_unaligned p) {
         CPHIFI_CUDA(cudaEventCreate(&e1));
         CPHIFI_CUDA(cudaEventRecord(e0, s));
     }
-    for (StreamPart* sp : all) {
+    // opt-in (CPHIFI_GRAM_CONCURRENT=1): the dense rows' parts (rows disjoint from the run-kernel
+    // parts': G rows and row counters disjoint) on the plan's second stream with their own unit
+    // slots, concurrent with the sparse parts — each stream keeps its parts in part order, so every
+    // G_i sums in the same order (bit-identical).  Measured slower at config 4 (53.5 against 41.8 ms,
+    // profiles/round2c/gram_concurrent.txt): every part's unit partition is planned as exactly one
+    // wave of the whole GPU, and two builds sharing the SMs turn each into two uneven waves.
+    bool conc = false;
+    if (const char* e = std::getenv("CPHIFI_GRAM_CONCURRENT")) conc = !timing && !Q.dense_parts.empty() && !Q.parts.empty() && std::atoi(e) != 0;
+    DevBuf<double> slot_a2, slot_b2;
+    for (StreamPart* sp : all) {  // every part's unit partition first (host round trips), then the launches
         if (sp->q == 0) continue;
         {  // the part's unit partition, built once and kept with the (shared) plan
             std::lock_guard<std::mutex> lk(o->qp_mu);
@@ -938,6 +951,9 @@ bool gram_build_parts(cphifi_unaligned p) {
                 sp->g_units = units;  // (the launch takes the partition's own count, g_beg.n - 1)
             }
         }
+    }
+    for (StreamPart* sp : all) {
+        if (sp->q == 0) continue;
         GramArgs g;
         g.n = p->n;
         g.rp = p->rp;
@@ -959,14 +975,27 @@ bool gram_build_parts(cphifi_unaligned p) {
         g.slot_b = slot_b.get();
         g.g = p->gram.get();
         g.accumulate = 1;  // G was zeroed: every part adds, in part order
+        cudaStream_t ls = s;
+        if (conc && sp >= &Q.dense_parts.front() && sp <= &Q.dense_parts.back()) {
+            if (!slot_a2.n) {  // first dense part: fork the side stream off the main one
+                slot_a2.alloc((size_t)units * rp2);
+                slot_b2.alloc((size_t)units * rp2);
+                ensure_side_stream(p);
+                CPHIFI_CUDA(cudaEventRecord(p->side_fork, s));
+                CPHIFI_CUDA(cudaStreamWaitEvent(p->side, p->side_fork, 0));
+            }
+            g.slot_a = slot_a2.get();
+            g.slot_b = slot_b2.get();
+            ls = p->side;
+        }
         cudaEvent_t p0 = nullptr, p1 = nullptr;
         if (timing) {
             CPHIFI_CUDA(cudaEventCreate(&p0));
             CPHIFI_CUDA(cudaEventCreate(&p1));
             CPHIFI_CUDA(cudaEventRecord(p0, s));
         }
-        if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), v3stage, s);
-        else gram_build_ws(g, (int)(sp->g_beg.n - 1), sp->sf, s);
+        if (v3) gram3_build(g, (int)(sp->g_beg.n - 1), v3stage, ls);
+        else gram_build_ws(g, (int)(sp->g_beg.n - 1), sp->sf, ls);
         if (timing) {
             CPHIFI_CUDA(cudaEventRecord(p1, s));
             CPHIFI_CUDA(cudaEventSynchronize(p1));
@@ -976,6 +1005,10 @@ bool gram_build_parts(cphifi_unaligned p) {
             cudaEventDestroy(p0);
             cudaEventDestroy(p1);
         }
+    }
+    if (slot_a2.n) {  // join
+        CPHIFI_CUDA(cudaEventRecord(p->side_join, p->side));
+        CPHIFI_CUDA(cudaStreamWaitEvent(s, p->side_join, 0));
     }
     CPHIFI_CUDA(cudaStreamSynchronize(s));  // the slots / counters are released on return
     if (timing) {

@@ -117,6 +117,14 @@ def test_gram_build_over_parts(monkeypatch, shape, r, q, coalesce, head, frac, s
     assert p.set_operator("gram") == "gram"
     y3 = cp.unaligned_matvec(p, x)
     assert np.array_equal(y3, cp.unaligned_matvec(p, x))
+    # the dense rows' parts built concurrently on the plan's second stream (opt-in) instead of after
+    # the sparse ones on one stream: every G_i sums in the same order, bit-identical
+    monkeypatch.setenv("CPHIFI_GRAM_CONCURRENT", "1")
+    obs_s = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    p_s = cp.make_unaligned_subproblem(obs_s, model, 0, mode, 1e-6)
+    p_s.set_operator("gram")
+    assert np.array_equal(cp.unaligned_matvec(p_s, x), y3)
+    monkeypatch.delenv("CPHIFI_GRAM_CONCURRENT")
     plan = p.qpass_plan()
     assert plan["parts"] == 2
     if frac > 0:
