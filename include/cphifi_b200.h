@@ -134,16 +134,28 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count); /* eig_factorization_co
 /* multiset input: merge repeated multi-indices into one plan entry carrying its multiplicity
    (operator weight) and summed value (right-hand side); q_local then counts distinct entries */
 #define CPHIFI_OBS_COALESCE_DUPLICATES 4u
+/* shards > 1: cut the sorted order into equal counts of observations [q*s/S, q*(s+1)/S) instead
+   of the default cost-balanced cut (below) */
+#define CPHIFI_OBS_SHARD_EQUAL_COUNT 8u
 /* Build the observation plan for infinite mode k: q multi-indices stored as d int32
  * arrays (idx[m*q + l] = index of observation l in mode m), fp64 values.  The plan sorts
- * by i_k on device (stable), builds CSR row pointers, and keeps the contiguous
- * equal-count shard [q*s/S, q*(s+1)/S) of the sorted order (s = shard, S = shards; use
- * 0/1 for a single GPU).  Range errors throw "ObservationSet: index out of range". */
+ * by i_k on device (stable), builds CSR row pointers, and keeps one contiguous shard of the
+ * sorted order (s = shard, S = shards; use 0/1 for a single GPU).  Shards are cost-balanced:
+ * a row counts its plan entries (distinct cells when coalescing), or the fixed cost of the GEMM
+ * form when the q-pass runs it as a dense row, and cuts fall on row boundaries unless one row
+ * exceeds a quarter of a shard — so a skewed set (config 4's Zipf rows) spreads its q-pass
+ * TIME, not its draws, evenly over the GPUs; every rank derives the same cuts.
+ * Range errors throw "ObservationSet: index out of range". */
 int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q,
                       const int32_t* idx, const double* values, int k, uint32_t flags,
                       int shard, int shards, cphifi_obs* out);
 int cphifi_obs_destroy(cphifi_obs obs);
 int cphifi_obs_info(cphifi_obs obs, int64_t* q_total, int64_t* q_local, double* density);
+/* Row ranges of this shard (multiples of 8 rows of mode k): it OWNS rows [own_lo, own_hi) — a
+ * partition of [0, n_k) over the shards — and its observations lie in rows [own_lo, hull_hi).  The
+ * row-sharded operator (large n, stream operator) contracts only these rows of K on each rank and
+ * all-reduces the n x r partial result.  One shard: [0, n_k), n_k. */
+int cphifi_obs_shard_rows(cphifi_obs obs, int64_t* own_lo, int64_t* own_hi, int64_t* hull_hi);
 
 /* ---- unaligned subproblem (unaligned.hpp:18-161) ---------------------------------- */
 /* make_unaligned_subproblem(obs, model, k, mode, rho) (unaligned.hpp:35-48): factors[m]

@@ -309,6 +309,7 @@ class ObservationSet:
         self._values = vals
         self.multiset = multiset
         self.coalesce = bool(coalesce and multiset)
+        self.equal_count_shards = False  # shards > 1: equal counts of observations instead of balanced cost
         self._plans = {}
         if not multiset and vals.size > 1:
             strides = np.cumprod([1] + self._shape[:-1]).astype(np.int64)
@@ -341,12 +342,14 @@ class ObservationSet:
         return int(self._idx[k, l])
 
     def plan(self, k: int, ctx: Context, shard: int = 0, shards: int = 1):
-        key = (k, id(ctx), shard, shards)
+        key = (k, id(ctx), shard, shards, self.equal_count_shards)
         if key not in self._plans:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
             flags = (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0) if self.multiset \
                 else _capi.OBS_REJECT_DUPLICATES
+            if self.equal_count_shards:
+                flags |= _capi.OBS_SHARD_EQUAL_COUNT
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p),
                  self.num_obs(), self._idx.ctypes.data, self._values.ctypes.data, k, flags, shard, shards,
                  ctypes.byref(h))
@@ -368,6 +371,7 @@ class DeviceObservations:
         self._keep = tuple(keepalive)
         self._plans = {}
         self.multiset = True
+        self.equal_count_shards = False
 
     def shape(self):
         return list(self._shape)
@@ -382,13 +386,14 @@ class DeviceObservations:
         return float(self._q) / float(np.prod(np.asarray(self._shape, dtype=np.float64)))
 
     def plan(self, k: int, ctx: "Context", shard: int = 0, shards: int = 1):
-        key = (k, id(ctx), shard, shards)
+        key = (k, id(ctx), shard, shards, self.equal_count_shards)
         if key not in self._plans:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p), self._q,
                  ctypes.c_void_p(self._idx_ptr), ctypes.c_void_p(self._vals_ptr), k,
-                 _capi.OBS_DEVICE_INPUT | (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0),
+                 _capi.OBS_DEVICE_INPUT | (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0)
+                 | (_capi.OBS_SHARD_EQUAL_COUNT if self.equal_count_shards else 0),
                  shard, shards, ctypes.byref(h))
             self._plans[key] = _Handle(h, "cphifi_obs_destroy", deps=(ctx,))
         return self._plans[key]

@@ -21,6 +21,7 @@ OK, INVALID_ARGUMENT, RUNTIME_ERROR, CUDA_ERROR, NCCL_ERROR = 0, 1, 2, 3, 4
 OBS_DEVICE_INPUT = 1
 OBS_REJECT_DUPLICATES = 2
 OBS_COALESCE_DUPLICATES = 4
+OBS_SHARD_EQUAL_COUNT = 8
 TENSOR_DEVICE_INPUT = 1
 
 
@@ -102,6 +103,7 @@ _SIGS = [
       ctypes.c_uint32, ctypes.c_int, ctypes.c_int, c_void_pp]),
     ("cphifi_obs_destroy", ctypes.c_int, [_H]),
     ("cphifi_obs_info", ctypes.c_int, [_H, c_int64_p, c_int64_p, c_double_p]),
+    ("cphifi_obs_shard_rows", ctypes.c_int, [_H, c_int64_p, c_int64_p, c_int64_p]),
     ("cphifi_unaligned_create", ctypes.c_int,
      [_H, _H, ctypes.c_int64, ctypes.POINTER(c_double_p), ctypes.c_double, c_void_pp]),
     ("cphifi_unaligned_destroy", ctypes.c_int, [_H]),

@@ -70,9 +70,11 @@ struct DeviceGuard {
 };
 
 // Plan columns carry OBS_PAD slack elements: the streaming kernels' TMA bulk copies round staged
-// columns to 16-byte boundaries (k_stream.cu) or copy whole CH-entry chunks (k_runs.cu, CH = 64)
-// and may read up to that many elements past the last one.
-constexpr int64_t OBS_PAD = 64;
+// columns to 16-byte boundaries (k_stream.cu) or copy whole CH-entry chunks from a 16-byte aligned
+// base (k_runs.cu / k_xruns.cu, CH <= 128: up to CH + 2 elements past the last one — 64 was the
+// slack of the former 64-entry chunks, and a part ending in the last 256 bytes of its allocation
+// faulted now and then).
+constexpr int64_t OBS_PAD = 256;
 
 // a kernel's eigenvalues below -PSD_TOL * max(|mu|_max, 1) make it indefinite (not a rounding artefact)
 constexpr double PSD_TOL = 1e-10;
@@ -1154,6 +1156,61 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
     gemm(g, ctx->num_sms, ctx->stream);
 }
 
+// Row-sharded operator (large n, sharded observations, stream operator): the shards are contiguous
+// in the plan order, so rank s's observations touch only the rows [own_lo, hull_hi) — it needs only
+// those rows of Xhat = K X and its partial Yhat is zero elsewhere.  Both dense contractions shrink
+// to the rank's rows: Xhat[rows,:] = K[rows,:] X, then, with lambda K X folded into the operand,
+//     y_s = K[:, rows] (Yhat_s[rows,:] + lambda X[owned rows,:])  (+ rho x on shard 0),
+// and ONE n x r all-reduce of y_s replaces the Yhat all-reduce: sum_s y_s =
+// K (Yhat + lambda X) + rho x.  Without it the two n x n x r GEMMs are replicated on every rank
+// (config 4: 0.18 of the 0.9 ms an 8-way shard takes).  CPHIFI_ROW_SHARDED=0 restores the replicated form.
+bool row_sharded(cphifi_unaligned p) {
+    cphifi_obs o = p->obs;
+    if (o->shards <= 1 || p->small_n || p->op == 1) return false;
+    if (ctx_multi(o->ctx) && o->ctx->nranks != o->shards) return false;
+    const char* e = std::getenv("CPHIFI_ROW_SHARDED");
+    return !(e && std::atoi(e) == 0);
+}
+
+void xhat_gemm_rows(cphifi_unaligned p, const double* x) {
+    cphifi_ctx ctx = p->obs->ctx;
+    const int64_t lo = p->obs->own_lo, hi = p->obs->hull_hi;
+    GemmArgs g;
+    g.m = hi - lo; g.n = p->r; g.k = p->n;
+    g.a = p->mode->kernel.get() + lo; g.a_rs = 1; g.a_cs = p->n;
+    g.b = x; g.b_rs = 1; g.b_cs = p->n;
+    g.c = p->xhat_cm.get() + lo; g.c_rs = 1; g.c_cs = p->n;
+    g.c2 = p->xhat_rm.get() + lo * p->rp; g.ld2 = p->rp;
+    gemm(g, ctx->num_sms, ctx->stream);
+}
+
+void y_gemm_rows(cphifi_unaligned p, const double* x, double* y) {
+    cphifi_obs o = p->obs;
+    cphifi_ctx ctx = o->ctx;
+    const int64_t lo = o->own_lo, hi = o->hull_hi, n = p->n;
+    if (!p->yhat_sum.n) p->yhat_sum.alloc(n * p->rp);
+    if (!p->y_part.n) p->y_part.alloc(n * p->r);
+    shard_operand(p->yhat_rm.get(), x, n, p->r, p->rp, lo, hi, o->own_lo, o->own_hi, p->mode->lambda,
+                  p->yhat_sum.get(), ctx->stream);
+    GemmArgs g;
+    g.m = n; g.n = p->r; g.k = hi - lo;
+    g.a = p->mode->kernel.get() + lo * n; g.a_rs = 1; g.a_cs = n;
+    g.b = p->yhat_sum.get() + lo * p->rp; g.b_rs = p->rp; g.b_cs = 1;
+    g.c = p->y_part.get(); g.c_rs = 1; g.c_cs = n;
+    if (o->shard == 0) {  // rho x once
+        g.epi = EPI_AXPY2;
+        g.e1 = x; g.e2 = x; g.ld_e = n;
+        g.beta1 = 0.0; g.beta2 = p->rho;
+    }
+    if (g.k > 0) {
+        gemm(g, ctx->num_sms, ctx->stream);
+    } else {  // a shard without rows: its share is rho x (shard 0) or nothing
+        CPHIFI_CUDA(cudaMemsetAsync(p->y_part.get(), 0, sizeof(double) * n * p->r, ctx->stream));
+        if (o->shard == 0) axpby(p->y_part.get(), x, p->rho, p->y_part.get(), 0.0, n * p->r, ctx->stream);
+    }
+    allreduce_sum(ctx, p->y_part.get(), y, (size_t)n * p->r);
+}
+
 // y = vec(K Yhat + lambda Xhat) + rho x with Xhat = K X  (unaligned.hpp:101-115).
 // Small n on one GPU: ONE cooperative launch.  Otherwise DMMA GEMMs around the fused
 // scatter-gather, with the NCCL all-reduce of Yhat between them on multi-GPU.
@@ -1178,6 +1235,12 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
             a.phases = matvec_phases(p, multi, 1);
             launch_fused(p, a);
         }
+        return;
+    }
+    if (row_sharded(p)) {
+        xhat_gemm_rows(p, x);
+        launch_phase_b(p, fused_args(p, PH_B));
+        y_gemm_rows(p, x, y);
         return;
     }
     xhat_gemm(p, x);
@@ -1885,6 +1948,94 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count) {
 }
 
 // ---- observations (observations.hpp:18-79) --------------------------------------------
+namespace {
+// The dense-row rule of the q-pass plan (build_dense_rows): a 3-way row whose entries cover at least
+// this share of its n_1 x n_2 grid runs as two DMMA GEMMs, at the cost of ~DENSE_ROW_COST_CELLS x
+// cells entries on the run kernel (config 4, B200: 2.26 us per dense row against 33.8 ps per sparse
+// entry of a 512 x 512 grid).
+double dense_min_density() {
+    double dmin = 0.3;
+    if (const char* e = std::getenv("CPHIFI_DENSE_MIN")) dmin = std::atof(e);
+    return dmin;
+}
+// A dense row costs ~DENSE_ROW_COST_CELLS x cells plan entries of the run kernel, a sparse row its
+// entries plus ~RUN_COST_ENTRIES per run (run start, partial last step, fold; two factor-block
+// parts at config 4): fitted on the B200 to config 4's shards timed alone (26.8 ps per entry, 0.29 us
+// per 512-run row, 2.3 us per dense row of a 512 x 512 grid; profiles/round2d/shard_cuts_config4.json).
+constexpr double DENSE_ROW_COST_CELLS = 0.32;
+constexpr double RUN_COST_ENTRIES = 21.0;
+
+bool shard_equal_count(uint32_t flags) {
+    if (flags & CPHIFI_OBS_SHARD_EQUAL_COUNT) return true;
+    const char* e = std::getenv("CPHIFI_SHARD_EQUAL_COUNT");
+    return e && std::atoi(e) != 0;
+}
+
+// Cost-balanced shards of the sorted draws (SURVEY §8e shards the observations; equal counts of
+// DRAWS leave a skewed plan — config 4's Zipf rows — with all the sparse rows, 63 % of the q-pass
+// time, on the last rank: 1.4x at 8 shards).  The cost of row i is its plan entries (distinct cells
+// when the plan coalesces, draws otherwise) plus a per-run term, or the dense-row equivalent when
+// the q-pass would run it as GEMMs; shard s ends where the cost prefix reaches (s + 1) / S of the
+// total, snapped to the nearer row boundary (whole rows keep the single-GPU dense / sparse split
+// and never share a Yhat row between ranks) unless that row alone is more than a quarter of a
+// shard, which is then cut inside by draw count.  Every rank computes the same cuts from the same
+// sorted keys.  rp = row pointers of ALL draws (host); returns the S + 1 monotone cut positions.
+std::vector<int64_t> balanced_shard_cuts(const uint64_t* keys, int64_t q, int64_t nk, uint64_t span, int d,
+                                         int64_t n_first, bool coalesce, int shards,
+                                         const std::vector<int64_t>& rp, cudaStream_t s) {
+    std::vector<unsigned long long> dist;
+    if (coalesce) {
+        DevBuf<unsigned long long> cnt_d(nk);
+        dist.resize(nk);
+        row_distinct_counts(keys, q, nk, span, cnt_d.get(), s);
+        d2h_sync(dist.data(), cnt_d.get(), sizeof(unsigned long long) * nk, s);
+    }
+    const double cells = (double)span, dmin = dense_min_density();
+    std::vector<double> pre(nk + 1, 0.0);
+    for (int64_t i = 0; i < nk; ++i) {
+        const double e = coalesce ? (double)dist[i] : (double)(rp[i + 1] - rp[i]);
+        double c = e + RUN_COST_ENTRIES * std::min(e, (double)n_first);
+        if (d == 3 && dmin > 0.0 && e >= dmin * cells) c = DENSE_ROW_COST_CELLS * cells;
+        pre[i + 1] = pre[i] + c;
+    }
+    const double total = pre[nk];
+    std::vector<int64_t> cuts(shards + 1, 0);
+    cuts[shards] = q;
+    for (int t = 1; t < shards; ++t) {
+        int64_t pos = q * t / shards;
+        if (total > 0.0) {
+            const double target = total * (double)t / (double)shards;
+            int64_t i = std::upper_bound(pre.begin(), pre.end(), target) - pre.begin() - 1;  // pre[i] <= target
+            i = std::min<int64_t>(std::max<int64_t>(i, 0), nk - 1);
+            const double ci = pre[i + 1] - pre[i];
+            if (ci <= total / (4.0 * shards)) pos = target - pre[i] < pre[i + 1] - target ? rp[i] : rp[i + 1];
+            else pos = rp[i] + (int64_t)std::llround((target - pre[i]) / ci * (double)(rp[i + 1] - rp[i]));
+        }
+        cuts[t] = std::min(q, std::max(cuts[t - 1], pos));
+    }
+    return cuts;
+}
+
+// Row ranges of the shards (multiples of 8 rows, the GEMM operands' alignment): shard s owns rows
+// [floor8(first row of s), floor8(first row of s + 1)), a partition of [0, n_k); its observations lie
+// in rows [own_lo, hull_hi), hull_hi covering the row it may share with shard s + 1.
+void shard_rows(cphifi_obs o, const std::vector<int64_t>& cuts, const std::vector<int64_t>& rp, int shard) {
+    const int64_t nk = (int64_t)rp.size() - 1;
+    const int S = (int)cuts.size() - 1;
+    auto first_row = [&](int t) -> int64_t {  // the row holding draw cuts[t] (the largest i with rp[i] <= cut)
+        if (t <= 0) return 0;
+        if (t >= S) return nk;
+        const int64_t i = (int64_t)(std::upper_bound(rp.begin(), rp.end(), cuts[t]) - rp.begin()) - 1;
+        return std::min<int64_t>(std::max<int64_t>(i, 0), nk) / 8 * 8;
+    };
+    o->shards = S;
+    o->shard = shard;
+    o->own_lo = first_row(shard);
+    o->own_hi = shard + 1 >= S ? nk : first_row(shard + 1);
+    o->hull_hi = shard + 1 >= S ? nk : std::min(nk, o->own_hi + 8);
+}
+}  // namespace
+
 int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, const int32_t* idx,
                       const double* values, int k, uint32_t flags, int shard, int shards, cphifi_obs* out) {
     return guard([&] {
@@ -1947,9 +2098,8 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
         unsigned __int128 prod = 1;
         for (int m = 0; m < d; ++m) prod *= (unsigned __int128)shape[m];
         const bool lex = prod <= ((unsigned __int128)1 << 63);
-        const int64_t lo = q * shard / shards, hi = q * (shard + 1) / shards;
-        const int64_t ql = hi - lo;
-        o->q_local = ql;
+        // equal-count cut of the sorted order; replaced below by the cost-balanced cut
+        int64_t lo = q * shard / shards, hi = q * (shard + 1) / shards;
         o->lex = lex;
         const int64_t qa = std::max<int64_t>(q, 1);
         DevBuf<int32_t> perm_in(qa), perm_out(qa);
@@ -2005,6 +2155,27 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
             }
         }
         key = DevBuf<uint64_t>();
+        o->own_hi = o->hull_hi = nk;
+        if (shards > 1 && q > 0) {
+            // row pointers of ALL draws, the (cost-balanced or equal-count) cuts, the shards' row ranges
+            DevBuf<int64_t> rp_d(nk + 1);
+            std::vector<int64_t> rp(nk + 1);
+            if (lex) csr_from_sorted64(key_s.get(), q, nk, span, rp_d.get(), s);
+            else csr_from_sorted(keys_out.get(), q, nk, rp_d.get(), s);
+            d2h_sync(rp.data(), rp_d.get(), sizeof(int64_t) * (nk + 1), s);
+            std::vector<int64_t> cuts(shards + 1);
+            for (int t = 0; t <= shards; ++t) cuts[t] = q * t / shards;
+            if (lex && !shard_equal_count(flags)) {
+                int mf = 0;  // the first other mode: the run kernel's runs
+                while (mf == k) ++mf;
+                cuts = balanced_shard_cuts(key_s.get(), q, nk, span, d, shape[mf], coalesce, shards, rp, s);
+            }
+            lo = cuts[shard];
+            hi = cuts[shard + 1];
+            shard_rows(o, cuts, rp, shard);
+        }
+        const int64_t ql = hi - lo;
+        o->q_local = ql;
         if (coalesce) {
             // merge repeated multi-indices of this shard: one entry per distinct key, carrying its
             // multiplicity (operator weight) and summed value (RHS); indices decoded from the key
@@ -2048,6 +2219,15 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
         else csr_from_sorted(keys_out.get() + lo, ql, nk, o->row_ptr.get(), s);
         CPHIFI_CUDA(cudaStreamSynchronize(s));
         *out = hold.release();
+    });
+}
+
+int cphifi_obs_shard_rows(cphifi_obs obs, int64_t* own_lo, int64_t* own_hi, int64_t* hull_hi) {
+    return guard([&] {
+        need(obs, "obs");
+        if (own_lo) *own_lo = obs->own_lo;
+        if (own_hi) *own_hi = obs->own_hi;
+        if (hull_hi) *hull_hi = obs->hull_hi;
     });
 }
 
@@ -2182,7 +2362,8 @@ int cphifi_unaligned_create(cphifi_obs obs, cphifi_mode mode, int64_t r, const d
         // rows without observations in this shard are never written: keep them zero
         CPHIFI_CUDA(cudaMemsetAsync(p->yhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
         CPHIFI_CUDA(cudaMemsetAsync(p->xhat_rm.get(), 0, sizeof(double) * n * p->rp, s));
-        if (ctx_multi(ctx)) p->yhat_sum.alloc(n * p->rp);
+        if (ctx_multi(ctx) || obs->shards > 1) p->yhat_sum.alloc(n * p->rp);
+        if (obs->shards > 1) p->y_part.alloc(n * r);  // row-sharded operator (y_gemm_rows)
         p->xhat_cm.alloc(n * r);
         p->t1.alloc(n * r);
         p->t2.alloc(n * r);
@@ -2524,7 +2705,9 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
         const double* gr = p->op == 1 ? p->gram.get() : nullptr;
         for (int it = 0; it < iters; ++it) {
             CPHIFI_CUDA(cudaEventRecord(ev[0], s));
-            if (!p->small_n) xhat_gemm(p, x);
+            const bool rows = row_sharded(p);
+            if (rows) xhat_gemm_rows(p, x);
+            else if (!p->small_n) xhat_gemm(p, x);
             CPHIFI_CUDA(cudaEventRecord(ev[1], s));
             FusedArgs a = fused_args(p, matvec_phases(p, multi, 0));
             a.x = x;
@@ -2538,9 +2721,11 @@ int cphifi_unaligned_matvec_timed(cphifi_unaligned p, const double* x, double* y
             g_dense_event = nullptr;
             if (!g_dense_recorded) CPHIFI_CUDA(cudaEventRecord(ev[2], s));
             CPHIFI_CUDA(cudaEventRecord(ev[3], s));
-            allreduce_yhat(p);
+            if (!rows) allreduce_yhat(p);
             CPHIFI_CUDA(cudaEventRecord(ev[4], s));
-            if (!p->small_n) {
+            if (rows) {
+                y_gemm_rows(p, x, y);  // (its all-reduce of y inside this phase)
+            } else if (!p->small_n) {
                 y_gemm(p, x, y);
             } else if (multi) {
                 a.phases = matvec_phases(p, multi, 1);

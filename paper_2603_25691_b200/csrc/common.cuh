@@ -212,6 +212,10 @@ struct cphifi_obs_s {
     cphifi::DevBuf<double> values;    // q_local, sorted (coalesced: summed over duplicates)
     cphifi::DevBuf<int32_t> mult;     // q_local multiplicities (coalesced plans only)
     bool coalesced = false;
+    // multi-rank row ranges (capi.cu shard_rows), multiples of 8 rows: this rank OWNS rows [own_lo,
+    // own_hi) (a partition of [0, n_k) over the shards) and its observations lie inside [own_lo, hull_hi)
+    int shards = 1, shard = 0;
+    int64_t own_lo = 0, own_hi = 0, hull_hi = 0;
     std::mutex qp_mu;                 // q-pass plans by padded rank (and the tuning knobs they read)
     std::map<std::string, std::shared_ptr<QpassPlan>> qp_cache;
 };
@@ -252,7 +256,8 @@ struct cphifi_unaligned_s {
     int op = 0;
     cphifi::DevBuf<double> gram;            // n x rp x rp (built lazily)
     cphifi::DevBuf<double> gram_sum;         // multi-rank finite-mode update: the all-shard row Grams
-    cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU)
+    cphifi::DevBuf<double> yhat_sum;   // n x rp NCCL all-reduce output (multi-GPU); the row-sharded output operand
+    cphifi::DevBuf<double> y_part;     // n x r: this rank's K[:, rows] B[rows, :] (row-sharded operator)
     cphifi::DevBuf<int64_t> cta_rows;   // 2 x grid
     cphifi::DevBuf<unsigned> barrier;   // grid barrier state
     cphifi::DevBuf<double> slot_a, slot_b;  // grid x rp

@@ -311,6 +311,52 @@ __global__ void csr64_kernel(const uint64_t* keys, int64_t q, int64_t n, uint64_
     row_ptr[i] = lo;
 }
 
+// cnt[i] += the number of DISTINCT keys of row i (sorted keys, row = key / span): each warp walks a
+// contiguous stretch 32 keys at a time; a stretch inside one row (the common case) adds one ballot
+// count to a warp-held running sum, flushed by one atomic per row change
+__global__ void row_distinct_kernel(const uint64_t* keys, int64_t q, uint64_t span, unsigned long long* cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t per = ((q + nwarp - 1) / nwarp + 31) / 32 * 32;
+    const int64_t lo = warp * per, hi = min(q, lo + per);
+    int64_t cur = -1;
+    unsigned long long acc = 0;
+    for (int64_t b = lo; b < hi; b += 32) {
+        const int64_t l = b + lane;
+        const bool in = l < hi;
+        const uint64_t key = in ? keys[l] : 0;
+        const bool first = in && (l == 0 || keys[l - 1] != key);
+        const int64_t row = in ? (int64_t)(key / span) : -1;
+        const int64_t r0 = __shfl_sync(0xffffffffu, row, 0);
+        if (__all_sync(0xffffffffu, !in || row == r0)) {
+            if (r0 != cur) {
+                if (lane == 0 && acc) atomicAdd(cnt + cur, acc);
+                cur = r0;
+                acc = 0;
+            }
+            acc += (unsigned long long)__popc(__ballot_sync(0xffffffffu, first));
+        } else if (first) {
+            atomicAdd(cnt + row, 1ull);
+        }
+    }
+    if (lane == 0 && acc) atomicAdd(cnt + cur, acc);
+}
+
+// Row-sharded output operand: B(i,:) = Yhat(i,:) + lambda X(i,:) on the rows this rank owns, Yhat(i,:)
+// on the other rows of [lo, hi) (X column-major n x r, Yhat / B row-major with stride rp)
+__global__ void shard_operand_kernel(const double* __restrict__ yhat, const double* __restrict__ x, int64_t n,
+                                     int64_t r, int64_t rp, int64_t lo, int64_t hi, int64_t own_lo, int64_t own_hi,
+                                     double lambda, double* __restrict__ b) {
+    const int64_t cnt = (hi - lo) * rp;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = lo + e / rp, c = e % rp;
+        double v = yhat[i * rp + c];
+        if (c < r && i >= own_lo && i < own_hi) v += lambda * x[i + n * c];
+        b[i * rp + c] = v;
+    }
+}
+
 __global__ void decode_keys_kernel(const uint64_t* keys, int64_t nu, int d, int k, const int64_t* stride,
                                    const int64_t* shape, int32_t* idx_o, int64_t ldq) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nu; l += (int64_t)gridDim.x * blockDim.x) {
@@ -507,6 +553,22 @@ void csr_from_sorted(const int32_t* keys, int64_t q, int64_t n, int64_t* row_ptr
 
 void csr_from_sorted64(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, int64_t* row_ptr, cudaStream_t s) {
     csr64_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(keys, q, n, span, row_ptr);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+void row_distinct_counts(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, unsigned long long* cnt,
+                         cudaStream_t s) {
+    CPHIFI_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * n, s));
+    if (q == 0) return;
+    row_distinct_kernel<<<grid_for(q, 256 * 32), 256, 0, s>>>(keys, q, span, cnt);
+    CPHIFI_CHECK_LAUNCH();
+}
+
+void shard_operand(const double* yhat, const double* x, int64_t n, int64_t r, int64_t rp, int64_t lo, int64_t hi,
+                   int64_t own_lo, int64_t own_hi, double lambda, double* b, cudaStream_t s) {
+    if (hi <= lo) return;
+    shard_operand_kernel<<<grid_for((hi - lo) * rp, 256), 256, 0, s>>>(yhat, x, n, r, rp, lo, hi, own_lo, own_hi,
+                                                                      lambda, b);
     CPHIFI_CHECK_LAUNCH();
 }
 

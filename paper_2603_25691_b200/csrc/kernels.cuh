@@ -439,6 +439,12 @@ size_t radix_sort_pairs_bytes(int64_t q, int bits);
 void radix_sort_pairs(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out,
                       const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);
 void csr_from_sorted64(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, int64_t* row_ptr, cudaStream_t s);
+// cnt[i] = distinct keys of row i (sorted lexicographic keys, row = key / span), i < n
+void row_distinct_counts(const uint64_t* keys, int64_t q, int64_t n, uint64_t span, unsigned long long* cnt,
+                         cudaStream_t s);
+// b(i,:) = yhat(i,:) (+ lambda x(i,:) on the owned rows) for rows [lo, hi): the row-sharded output GEMM's operand
+void shard_operand(const double* yhat, const double* x, int64_t n, int64_t r, int64_t rp, int64_t lo, int64_t hi,
+                   int64_t own_lo, int64_t own_hi, double lambda, double* b, cudaStream_t s);
 size_t radix_sort_pairs64_bytes(int64_t q, int bits);
 void radix_sort_pairs64(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
                         const int32_t* vals_in, int32_t* vals_out, int64_t q, int bits, cudaStream_t s);

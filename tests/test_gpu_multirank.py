@@ -132,3 +132,66 @@ def test_multirank_aligned_config2(ctx, S):
     for k in range(S):
         assert np.array_equal(res[k], res[0])
     assert rel(res[0], ref) <= 1e-12
+
+
+def _skewed_case(d3: bool):
+    """A Zipf-skewed multiset (the head rows saturate their grids, the tail is sparse), n = 640."""
+    rng = np.random.default_rng(5)
+    n, r = 640, 16
+    shape = [n, 48, 40] if d3 else [n, 12, 10, 8]
+    q = 300_000
+    pz = 1.0 / np.arange(1, n + 1) ** 1.1
+    i0 = rng.choice(n, size=q, p=pz / pz.sum())
+    idx = np.stack([i0] + [rng.integers(0, s, size=q) for s in shape[1:]]).astype(np.int32)
+    vals = rng.normal(size=q)
+    pts = np.sort(rng.uniform(size=n))
+    factors = [np.asfortranarray(rng.normal(size=(s, r))) for s in shape]
+    return shape, r, idx, vals, pts, factors
+
+
+@pytest.mark.parametrize("d3", [True, False])
+@pytest.mark.parametrize("coalesce", [True, False])
+@pytest.mark.parametrize("S", [2, 3, 8])
+def test_balanced_shards_partials_sum(ctx, S, coalesce, d3):
+    """Cost-balanced shards (capi.cu balanced_shard_cuts) and the row-sharded operator: with no
+    communicator attached every shard returns its partial y_s = K[:, rows](Yhat_s + lambda X[owned])
+    (+ rho x on shard 0); the partials of all shards sum to the unsharded application — for the
+    balanced cut and the equal-count cut alike — and the cuts partition the observations."""
+    import ctypes
+
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import _capi
+    shape, r, idx, vals, pts, factors = _skewed_case(d3)
+    n, q = shape[0], vals.size
+    mode = cp.RkhsMode(pts, 0.05, 1e-3, ctx=ctx)
+    model = cp.KruskalModel([np.zeros((n, r))] + factors[1:])
+    x = np.random.default_rng(3).normal(size=n * r)
+    lib = _capi.load()
+
+    def q_local(obs, s, S_):
+        qt, ql = ctypes.c_int64(), ctypes.c_int64()
+        _capi.check(lib.cphifi_obs_info(obs.plan(0, ctx, s, S_).h, ctypes.byref(qt), ctypes.byref(ql), None))
+        return ql.value
+
+    obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    pref = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+    pref.set_operator("stream")
+    yref = cp.unaligned_matvec(pref, x)
+    counts = {}
+    for equal in (False, True):
+        obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+        obs.equal_count_shards = equal
+        ysum = np.zeros_like(yref)
+        for s in range(S):
+            p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6, shard=s, shards=S)
+            p.set_operator("stream")
+            ysum += cp.unaligned_matvec(p, x)
+        assert rel(ysum, yref) <= 1e-12, (equal, rel(ysum, yref))
+        counts[equal] = [q_local(obs, s, S) for s in range(S)]
+    if not coalesce:
+        assert sum(counts[False]) == q and sum(counts[True]) == q
+        assert counts[True] == [q * (s + 1) // S - q * s // S for s in range(S)]
+        # the skew: the balanced cut gives the saturated head rows' shard more draws than an equal share
+        assert counts[False][0] > counts[True][0]
+    else:
+        assert sum(counts[False]) == q_local(cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=True), 0, 1)
