@@ -320,7 +320,7 @@ def main():
     sec = {}
     if rank == 0 and world == 1 and args.secondary:
         import bench_secondary as bs
-        sec = bs.run_all(args, ctx, cp, p, mode, cfg)
+        sec = bs.run_all(args, ctx, cp, p, mode, cfg, t1_ms=total_ms / args.steps)
     del p
     torch.cuda.empty_cache()
 
@@ -354,8 +354,9 @@ def main():
             "data": DATA,
             "config": CONFIG,
             "timing": "K applications back to back on the library stream between one CUDA event pair",
-            "parallelism": (f"observations sharded x{world} (equal-count slices of the sorted plan), n x r all-reduce "
-                            "per application") if world > 1 else "1 GPU",
+            "parallelism": (f"observations sharded x{world} (cost-balanced row-aligned slices of the sorted plan), "
+                            "each rank contracts its own rows of K, one n x r all-reduce per application")
+            if world > 1 else "1 GPU",
             "plan_entries_this_rank": ql.value,
             "qpass_plan": qplan,
             "roofline": {"bound": "hbm", "kernel": f"runs_kernel (k_runs.cu: the per-entry gather / scatter over the "

@@ -213,6 +213,49 @@ def config4_solves(cp, p, obs, mode, cfg):
     return out
 
 
+def config4_shards(cp, ctx, mode, cfg, t1_ms, counts=(2, 4, 8), iters=10):
+    """Config 4 cut into S cost-balanced observation shards (capi.cu balanced_shard_cuts), each
+    shard's row-sharded operator application timed ALONE on this GPU (one shard at a time, no
+    communicator: the call returns the shard's partial y_s).  The slowest shard bounds the S-GPU
+    application; the n x r all-reduce of the partials (2 MB over NVLink) is NOT in these times."""
+    import numpy as np
+    import torch
+    from paper_2603_25691_b200 import _capi
+    lib = _capi.load()
+    dev = torch.device("cuda", ctx.device)
+    n, r, q = cfg.shape[0], cfg.r, cfg.q
+    idx, vals = cp.synth_observations_device(cfg, ctx)
+    model = cp.KruskalModel([np.zeros((n, r))] + cfg.factors[1:])
+    x = torch.randn(n * r, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    out = {"t1_ms": t1_ms, "note": "every shard timed alone on one GPU; all-reduce of the n x r partials not included"}
+    for S in counts:
+        ms = []
+        for s in range(S):
+            obs = cp.DeviceObservations(cfg.shape, idx.data_ptr(), vals.data_ptr(), q, keepalive=(idx, vals),
+                                        coalesce=cfg.coalesce)
+            p = cp.make_unaligned_subproblem(obs, model, 0, mode, cfg.rho, shard=s, shards=S)
+            p.set_operator("stream")
+            for _ in range(3):
+                _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(iters):
+                    _capi.check(lib.cphifi_unaligned_matvec_device(p.handle, x.data_ptr(), y.data_ptr()))
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1) / iters)
+            del p, obs
+            torch.cuda.empty_cache()
+        out[f"S{S}"] = {"shard_ms": ms, "max_ms": max(ms), "projected_speedup": t1_ms / max(ms)}
+    del idx, vals
+    torch.cuda.empty_cache()
+    return out
+
+
 def config1_line(cp, ctx, steps):
     """Config 1 operator (the previous round's headline) on 128 independent instances cycled in one
     CUDA graph (>= 128 applications so every application starts L2-cold), and its PCG solve."""
@@ -318,7 +361,7 @@ def cpu_baselines(threads):
     return out
 
 
-def run_all(args, ctx, cp, p, mode, cfg):
+def run_all(args, ctx, cp, p, mode, cfg, t1_ms=None):
     """Everything above, each failure reported in its key (never hidden)."""
     import torch
     from oracle import oracle as orc
@@ -335,6 +378,8 @@ def run_all(args, ctx, cp, p, mode, cfg):
     obs = p.obs
     attempt("config4_pcg", lambda: config4_solves(cp, p, obs, mode, cfg))
     torch.cuda.empty_cache()
+    if t1_ms:
+        attempt("config4_shards", lambda: config4_shards(cp, ctx, mode, cfg, t1_ms))
     attempt("config3", lambda: large("config3", ctx, fp64_tf=fp64))
     torch.cuda.empty_cache()
     attempt("config1", lambda: config1_line(cp, ctx, args.steps))
