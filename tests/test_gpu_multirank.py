@@ -195,3 +195,43 @@ def test_balanced_shards_partials_sum(ctx, S, coalesce, d3):
         assert counts[False][0] > counts[True][0]
     else:
         assert sum(counts[False]) == q_local(cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=True), 0, 1)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("S", [3, 8])
+def test_multirank_skewed_dense_rows(ctx, S):
+    """The Zipf-skewed coalesced 3-way multiset under the virtual communicator: cost-balanced
+    row-aligned shards (dense rows on the head ranks, sparse rows on the tail ranks), the
+    row-sharded stream operator with its all-reduce of the n x r partial y, and the PCG solve on
+    the sharded plan — against the unsharded plan; every rank holds the same bits."""
+    import paper_2603_25691_b200 as cp
+    shape, r, idx, vals, pts, factors = _skewed_case(True)
+    n = shape[0]
+    obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=True)
+    model = cp.KruskalModel([np.zeros((n, r))] + factors[1:])
+    x = np.random.default_rng(11).normal(size=n * r)
+    cfg = cp.PcgConfig(1e-8, 500)
+
+    def solve(cx, rank, S_):
+        mode = cp.RkhsMode(pts, 0.05, 1e-3, ctx=cx)
+        p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6, shard=rank, shards=S_)
+        p.set_operator("stream")
+        y = cp.unaligned_matvec(p, x)
+        rep = cp.SolveReport()
+        w = cp.solve_unaligned_pcg(p, cfg, rep)
+        return dict(y=y, b=p.b, kw=mode.kernel() @ w, it=rep.iterations, rel=rep.relative_residual,
+                    dense=p.qpass_plan()["dense_rows"])
+
+    ref = solve(ctx, 0, 1)
+    assert ref["dense"] > 0  # the head rows run as GEMMs
+    res = run_ranks(S, solve)
+    assert sum(o["dense"] for o in res) == ref["dense"]  # whole rows per rank: the single-GPU dense / sparse split
+    for k in range(1, S):
+        assert np.array_equal(res[k]["y"], res[0]["y"])
+        assert np.array_equal(res[k]["kw"], res[0]["kw"])
+    assert rel(res[0]["y"], ref["y"]) <= 1e-12
+    assert rel(res[0]["b"], ref["b"]) <= 1e-12
+    # ~135 iterations on this ill-conditioned multiset: the ranks' partial sums are added in another
+    # order than the unsharded plan's, and the rounding drift moves the stopping iteration by a few
+    assert abs(res[0]["it"] - ref["it"]) <= 4 and res[0]["rel"] <= 1e-8
+    assert rel(res[0]["kw"], ref["kw"]) <= 1e-6
