@@ -139,3 +139,64 @@ def test_sharded_als_terms_gloo():
     for rank, rel_err, row_err in res:
         assert rel_err < 1e-13, (rank, rel_err)
         assert row_err < 1e-9, (rank, row_err)
+
+
+def _row_sharded_worker(rank, world, port, out_q):
+    """The row-sharded operator's multi-GPU scheme (capi.cu xhat_gemm_rows / y_gemm_rows) on CPU:
+    cost-balanced row-aligned shards (paper_2603_25691_b200/sharding.py, the host restatement of
+    the device cut), each rank contracts only its rows of K — Xhat[rows,:] = K[rows,:] X, its
+    shard's partial Yhat, y_s = K[:, rows](Yhat_s[rows,:] + lambda X[owned rows,:]) (+ rho x on rank
+    0) — and ONE all-reduce of the n x r partials gives the reference operator (unaligned.hpp:101-115)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+        from paper_2603_25691_b200 import sharding
+        from tests import refinst as ri
+        inst = ri.Inst([40, 7, 6], 5, 900, 0, 0.6, 0.1, 1e-6, 77)
+        n, r = 40, 5
+        keys = (inst.idx[0].astype(np.int64) * 7 + inst.idx[1]) * 6 + inst.idx[2]
+        order = np.argsort(keys, kind="stable")
+        idx = inst.idx[:, order]
+        cuts, rp = sharding.shard_cuts(inst.idx, inst.shape, 0, world, coalesce=False)
+        lo, hi = cuts[rank], cuts[rank + 1]
+        own_lo, own_hi, hull_hi = sharding.shard_row_ranges(cuts, rp, rank)
+        x = np.random.default_rng(5).normal(size=n * r)
+        xm = x.reshape(r, n).T  # column-major n x r
+        kern = inst.kernel
+        xhat = np.zeros((n, r))
+        xhat[own_lo:hull_hi] = kern[own_lo:hull_hi, :] @ xm  # only this rank's rows of Xhat
+        yhat = orc.scatter_gather_stream(inst.shape, 0, idx[:, lo:hi], inst.factors, np.asfortranarray(xhat), threads=1)
+        assert not np.any(yhat[:own_lo]) and not np.any(yhat[hull_hi:])  # the shard touches only its rows
+        op = yhat[own_lo:hull_hi].copy()
+        op[:own_hi - own_lo] += inst.lam * xm[own_lo:own_hi]
+        y_s = kern[:, own_lo:hull_hi] @ op
+        if rank == 0:
+            y_s = y_s + inst.rho * xm
+        t = torch.from_numpy(np.ascontiguousarray(y_s))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ref = orc.unaligned_matvec(inst.sub, x).reshape(r, n).T
+        err = float(np.linalg.norm(t.numpy() - ref) / np.linalg.norm(ref))
+        out_q.put((rank, err, (own_lo, own_hi, hull_hi), hi - lo))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_operator_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, rows, cnt in res:
+        assert err < 1e-12, (rank, err)
+        assert cnt > 0
+    assert res[0][2][0] == 0 and res[0][2][1] == res[1][2][0] and res[1][2][1] == 40  # owned rows partition [0, n)
+    assert sum(c for _, _, _, c in res) == 900

@@ -1,0 +1,96 @@
+"""The multi-GPU observation cut (paper_2603_25691_b200/sharding.py, the host restatement of
+capi.cu's balanced_shard_cuts / shard_rows): properties on CPU, and the device cut against it."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2603_25691_b200 import sharding
+
+
+def _skewed(d3=True, n=640, q=300_000, seed=5):
+    rng = np.random.default_rng(seed)
+    shape = [n, 48, 40] if d3 else [n, 12, 10, 8]
+    pz = 1.0 / np.arange(1, n + 1) ** 1.1
+    i0 = rng.choice(n, size=q, p=pz / pz.sum())
+    idx = np.stack([i0] + [rng.integers(0, s, size=q) for s in shape[1:]]).astype(np.int32)
+    return shape, idx
+
+
+@pytest.mark.parametrize("d3", [True, False])
+@pytest.mark.parametrize("coalesce", [True, False])
+@pytest.mark.parametrize("S", [2, 3, 8])
+def test_cuts_partition_rows_and_balance(S, coalesce, d3):
+    shape, idx = _skewed(d3)
+    q, n = idx.shape[1], shape[0]
+    cuts, rp = sharding.shard_cuts(idx, shape, 0, S, coalesce)
+    assert cuts[0] == 0 and cuts[-1] == q and all(a <= b for a, b in zip(cuts, cuts[1:]))
+    if d3:  # the head rows are dense (capped cost): no row exceeds a quarter shard, every cut is row-aligned
+        assert all(c in set(rp.tolist()) for c in cuts)
+    own = [sharding.shard_row_ranges(cuts, rp, s) for s in range(S)]
+    assert own[0][0] == 0 and own[-1][1] == n
+    for s in range(S):
+        lo, hi, hull = own[s]
+        assert lo % 8 == 0 and (hi % 8 == 0 or hi == n) and lo <= hi <= hull <= n
+        if s + 1 < S:
+            assert own[s + 1][0] == hi  # owned rows partition [0, n)
+        if cuts[s + 1] > cuts[s]:  # the shard's observations lie inside [own_lo, hull_hi)
+            r0 = int(np.searchsorted(rp, cuts[s], side="right")) - 1
+            r1 = int(np.searchsorted(rp, cuts[s + 1] - 1, side="right")) - 1
+            assert lo <= r0 and r1 < hull
+    # modelled cost per shard within 15 % of the mean (row granularity), where equal counts are far off
+    keys, span = sharding.sorted_keys(idx, shape, 0)
+
+    def shard_cost(c):
+        out = []
+        for s in range(S):
+            kk = keys[c[s]:c[s + 1]]
+            rows = (kk // np.uint64(span)).astype(np.int64)
+            ent = np.bincount(rows[np.r_[True, kk[1:] != kk[:-1]]] if coalesce else rows, minlength=n).astype(float)
+            cost = ent + sharding.RUN_COST_ENTRIES * np.minimum(ent, shape[1])
+            if d3:
+                cost = np.where(ent >= 0.3 * span, sharding.DENSE_ROW_COST_CELLS * span, cost)
+            out.append(cost.sum())
+        return np.array(out)
+
+    bal = shard_cost(cuts)
+    assert bal.max() <= 1.15 * bal.mean()
+    eq, _ = sharding.shard_cuts(idx, shape, 0, S, coalesce, equal_count=True)
+    assert eq == [q * t // S for t in range(S + 1)]
+
+
+def test_cut_inside_a_dominant_row():
+    """One row holding most of the (uncoalesced, 4-way) observations is cut inside, by draw count."""
+    rng = np.random.default_rng(1)
+    shape, q = [16, 6, 5, 4], 20_000
+    i0 = np.where(rng.uniform(size=q) < 0.9, 3, rng.integers(0, 16, size=q))
+    idx = np.stack([i0] + [rng.integers(0, s, size=q) for s in shape[1:]]).astype(np.int32)
+    cuts, rp = sharding.shard_cuts(idx, shape, 0, 4, coalesce=False)
+    inside = [c for c in cuts[1:-1] if rp[3] < c < rp[4]]
+    assert len(inside) >= 2
+    sizes = np.diff(cuts)
+    assert sizes.max() <= 1.2 * sizes.mean()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d3", [True, False])
+@pytest.mark.parametrize("coalesce", [True, False])
+@pytest.mark.parametrize("S", [3, 8])
+def test_device_cut_matches_host(ctx, S, coalesce, d3):
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import _capi
+    lib = _capi.load()
+    shape, idx = _skewed(d3)
+    vals = np.random.default_rng(2).normal(size=idx.shape[1])
+    cuts, rp = sharding.shard_cuts(idx, shape, 0, S, coalesce)
+    keys, _ = sharding.sorted_keys(idx, shape, 0)
+    obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    for s in range(S):
+        h = obs.plan(0, ctx, s, S).h
+        qt, ql = ctypes.c_int64(), ctypes.c_int64()
+        _capi.check(lib.cphifi_obs_info(h, ctypes.byref(qt), ctypes.byref(ql), None))
+        kk = keys[cuts[s]:cuts[s + 1]]
+        assert ql.value == (np.unique(kk).size if coalesce else kk.size)
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _capi.check(lib.cphifi_obs_shard_rows(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        assert (a.value, b.value, c.value) == sharding.shard_row_ranges(cuts, rp, s)
