@@ -137,6 +137,10 @@ int cphifi_mode_eig_count(cphifi_mode mode, int* count); /* eig_factorization_co
 /* shards > 1: cut the sorted order into equal counts of observations [q*s/S, q*(s+1)/S) instead
    of the default cost-balanced cut (below) */
 #define CPHIFI_OBS_SHARD_EQUAL_COUNT 8u
+/* shards > 1: balance the shards' PLAN ENTRIES (distinct cells when coalescing) instead of their
+   modelled q-pass time — the right cut when the plan is used with the row-Gram operator, whose
+   build costs 2 rp^2 flops per plan entry whether the row is dense or not (same row-aligned cuts) */
+#define CPHIFI_OBS_SHARD_BY_ENTRIES 16u
 /* Build the observation plan for infinite mode k: q multi-indices stored as d int32
  * arrays (idx[m*q + l] = index of observation l in mode m), fp64 values.  The plan sorts
  * by i_k on device (stable), builds CSR row pointers, and keeps one contiguous shard of the

@@ -310,6 +310,7 @@ class ObservationSet:
         self.multiset = multiset
         self.coalesce = bool(coalesce and multiset)
         self.equal_count_shards = False  # shards > 1: equal counts of observations instead of balanced cost
+        self.shard_by_entries = False    # shards > 1: balance plan entries (row-Gram build) instead of q-pass time
         self._plans = {}
         if not multiset and vals.size > 1:
             strides = np.cumprod([1] + self._shape[:-1]).astype(np.int64)
@@ -342,7 +343,7 @@ class ObservationSet:
         return int(self._idx[k, l])
 
     def plan(self, k: int, ctx: Context, shard: int = 0, shards: int = 1):
-        key = (k, id(ctx), shard, shards, self.equal_count_shards)
+        key = (k, id(ctx), shard, shards, self.equal_count_shards, self.shard_by_entries)
         if key not in self._plans:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
@@ -350,6 +351,8 @@ class ObservationSet:
                 else _capi.OBS_REJECT_DUPLICATES
             if self.equal_count_shards:
                 flags |= _capi.OBS_SHARD_EQUAL_COUNT
+            if self.shard_by_entries:
+                flags |= _capi.OBS_SHARD_BY_ENTRIES
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p),
                  self.num_obs(), self._idx.ctypes.data, self._values.ctypes.data, k, flags, shard, shards,
                  ctypes.byref(h))
@@ -372,6 +375,7 @@ class DeviceObservations:
         self._plans = {}
         self.multiset = True
         self.equal_count_shards = False
+        self.shard_by_entries = False
 
     def shape(self):
         return list(self._shape)
@@ -386,14 +390,15 @@ class DeviceObservations:
         return float(self._q) / float(np.prod(np.asarray(self._shape, dtype=np.float64)))
 
     def plan(self, k: int, ctx: "Context", shard: int = 0, shards: int = 1):
-        key = (k, id(ctx), shard, shards, self.equal_count_shards)
+        key = (k, id(ctx), shard, shards, self.equal_count_shards, self.shard_by_entries)
         if key not in self._plans:
             h = ctypes.c_void_p()
             shape = np.ascontiguousarray(self._shape, dtype=np.int64)
             call("cphifi_obs_create", ctx.handle, len(self._shape), shape.ctypes.data_as(c_int64_p), self._q,
                  ctypes.c_void_p(self._idx_ptr), ctypes.c_void_p(self._vals_ptr), k,
                  _capi.OBS_DEVICE_INPUT | (_capi.OBS_COALESCE_DUPLICATES if self.coalesce else 0)
-                 | (_capi.OBS_SHARD_EQUAL_COUNT if self.equal_count_shards else 0),
+                 | (_capi.OBS_SHARD_EQUAL_COUNT if self.equal_count_shards else 0)
+                 | (_capi.OBS_SHARD_BY_ENTRIES if self.shard_by_entries else 0),
                  shard, shards, ctypes.byref(h))
             self._plans[key] = _Handle(h, "cphifi_obs_destroy", deps=(ctx,))
         return self._plans[key]

@@ -22,6 +22,7 @@ OBS_DEVICE_INPUT = 1
 OBS_REJECT_DUPLICATES = 2
 OBS_COALESCE_DUPLICATES = 4
 OBS_SHARD_EQUAL_COUNT = 8
+OBS_SHARD_BY_ENTRIES = 16
 TENSOR_DEVICE_INPUT = 1
 
 

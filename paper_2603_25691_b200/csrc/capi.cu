@@ -1981,7 +1981,7 @@ bool shard_equal_count(uint32_t flags) {
 // shard, which is then cut inside by draw count.  Every rank computes the same cuts from the same
 // sorted keys.  rp = row pointers of ALL draws (host); returns the S + 1 monotone cut positions.
 std::vector<int64_t> balanced_shard_cuts(const uint64_t* keys, int64_t q, int64_t nk, uint64_t span, int d,
-                                         int64_t n_first, bool coalesce, int shards,
+                                         int64_t n_first, bool coalesce, bool by_entries, int shards,
                                          const std::vector<int64_t>& rp, cudaStream_t s) {
     std::vector<unsigned long long> dist;
     if (coalesce) {
@@ -1994,8 +1994,11 @@ std::vector<int64_t> balanced_shard_cuts(const uint64_t* keys, int64_t q, int64_
     std::vector<double> pre(nk + 1, 0.0);
     for (int64_t i = 0; i < nk; ++i) {
         const double e = coalesce ? (double)dist[i] : (double)(rp[i + 1] - rp[i]);
-        double c = e + RUN_COST_ENTRIES * std::min(e, (double)n_first);
-        if (d == 3 && dmin > 0.0 && e >= dmin * cells) c = DENSE_ROW_COST_CELLS * cells;
+        double c = e;  // by_entries: the row-Gram build's cost (2 rp^2 flops per plan entry, dense row or not)
+        if (!by_entries) {
+            c = e + RUN_COST_ENTRIES * std::min(e, (double)n_first);
+            if (d == 3 && dmin > 0.0 && e >= dmin * cells) c = DENSE_ROW_COST_CELLS * cells;
+        }
         pre[i + 1] = pre[i] + c;
     }
     const double total = pre[nk];
@@ -2168,7 +2171,8 @@ int cphifi_obs_create(cphifi_ctx ctx, int d, const int64_t* shape, int64_t q, co
             if (lex && !shard_equal_count(flags)) {
                 int mf = 0;  // the first other mode: the run kernel's runs
                 while (mf == k) ++mf;
-                cuts = balanced_shard_cuts(key_s.get(), q, nk, span, d, shape[mf], coalesce, shards, rp, s);
+                cuts = balanced_shard_cuts(key_s.get(), q, nk, span, d, shape[mf], coalesce,
+                                           (flags & CPHIFI_OBS_SHARD_BY_ENTRIES) != 0, shards, rp, s);
             }
             lo = cuts[shard];
             hi = cuts[shard + 1];

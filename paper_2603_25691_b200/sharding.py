@@ -37,7 +37,7 @@ def sorted_keys(idx: np.ndarray, shape, k: int):
 
 
 def shard_cuts(idx: np.ndarray, shape, k: int, shards: int, coalesce: bool, equal_count: bool = False,
-               dense_min: float = DENSE_MIN):
+               dense_min: float = DENSE_MIN, by_entries: bool = False):
     """(cuts, rp): the S + 1 cut positions in the sorted draws and the row pointers of all draws."""
     keys, span = sorted_keys(idx, shape, k)
     q, nk, d = keys.size, int(shape[k]), len(shape)
@@ -53,8 +53,8 @@ def shard_cuts(idx: np.ndarray, shape, k: int, shards: int, coalesce: bool, equa
     else:
         ent = draws
     n_first = float(shape[1 if k == 0 else 0])
-    cost = ent + RUN_COST_ENTRIES * np.minimum(ent, n_first)
-    if d == 3 and dense_min > 0.0:
+    cost = ent if by_entries else ent + RUN_COST_ENTRIES * np.minimum(ent, n_first)
+    if d == 3 and dense_min > 0.0 and not by_entries:
         cost = np.where(ent >= dense_min * float(span), DENSE_ROW_COST_CELLS * float(span), cost)
     pre = np.concatenate([[0.0], np.cumsum(cost)])  # the same left-to-right double sum as the host loop
     total = float(pre[nk])

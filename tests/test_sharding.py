@@ -72,19 +72,33 @@ def test_cut_inside_a_dominant_row():
     assert sizes.max() <= 1.2 * sizes.mean()
 
 
+def test_by_entries_balances_plan_entries():
+    """The row-Gram build's cut: plan entries (distinct cells) per shard within a row of equal."""
+    shape, idx = _skewed(True)
+    keys, _ = sharding.sorted_keys(idx, shape, 0)
+    cuts, rp = sharding.shard_cuts(idx, shape, 0, 8, coalesce=True, by_entries=True)
+    ent = np.array([np.unique(keys[cuts[s]:cuts[s + 1]]).size for s in range(8)], dtype=float)
+    assert ent.max() <= 1.1 * ent.mean()
+    cuts_t, _ = sharding.shard_cuts(idx, shape, 0, 8, coalesce=True)
+    ent_t = np.array([np.unique(keys[cuts_t[s]:cuts_t[s + 1]]).size for s in range(8)], dtype=float)
+    assert ent_t.max() > 1.5 * ent_t.mean()  # the q-pass-time cut gives the dense head rows' ranks more entries
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("by_entries", [False, True])
 @pytest.mark.parametrize("d3", [True, False])
 @pytest.mark.parametrize("coalesce", [True, False])
 @pytest.mark.parametrize("S", [3, 8])
-def test_device_cut_matches_host(ctx, S, coalesce, d3):
+def test_device_cut_matches_host(ctx, S, coalesce, d3, by_entries):
     import paper_2603_25691_b200 as cp
     from paper_2603_25691_b200 import _capi
     lib = _capi.load()
     shape, idx = _skewed(d3)
     vals = np.random.default_rng(2).normal(size=idx.shape[1])
-    cuts, rp = sharding.shard_cuts(idx, shape, 0, S, coalesce)
+    cuts, rp = sharding.shard_cuts(idx, shape, 0, S, coalesce, by_entries=by_entries)
     keys, _ = sharding.sorted_keys(idx, shape, 0)
     obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+    obs.shard_by_entries = by_entries
     for s in range(S):
         h = obs.plan(0, ctx, s, S).h
         qt, ql = ctypes.c_int64(), ctypes.c_int64()
