@@ -1961,8 +1961,9 @@ double dense_min_density() {
 // A dense row costs ~DENSE_ROW_COST_CELLS x cells plan entries of the run kernel, a sparse row its
 // entries plus ~RUN_COST_ENTRIES per run (run start, partial last step, fold; two factor-block
 // parts at config 4): fitted on the B200 to config 4's shards timed alone (26.8 ps per entry, 0.29 us
-// per 512-run row, 2.3 us per dense row of a 512 x 512 grid; profiles/round2d/shard_cuts_config4.json).
-constexpr double DENSE_ROW_COST_CELLS = 0.32;
+// per 512-run row, 2.3 us per dense row of a 512 x 512 grid; profiles/round2d/shard_cuts_config4.json;
+// the dense share raised from 0.32 after the run kernel's RV_FOLDZ loop: 8 shards 0.75-0.86 -> 0.79-0.81 ms).
+constexpr double DENSE_ROW_COST_CELLS = 0.345;
 constexpr double RUN_COST_ENTRIES = 21.0;
 
 bool shard_equal_count(uint32_t flags) {

@@ -94,7 +94,14 @@ __device__ __forceinline__ void lds_row(double (&v)[VPL], const double* row, int
 //           addresses computed once (ld.shared with explicit addresses) instead of generic pointers
 //           the compiler converts (and, at 128 registers, re-derives) every step.
 //  RV_CHUNKED the staging test once per stretch of landed entries instead of once per step.
-constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, RV_S32 = 64, RV_CHUNKED = 128;
+//  RV_FOLDZ the run's A_1 row folded into every entry's row instead of into u and the run's sum: with
+//           z' = A_1(a,:) o t the dot is Xhat(i,:) . z' and the row accumulator takes w x z' directly, so a
+//           lane keeps the Xhat row (read once per ROW), the A_1 row (once per run) and the row
+//           accumulator — the same registers as u, v and the accumulator — and a run reads one row
+//           from shared memory instead of three (Xhat, A_1 for u, A_1 for the fold): 32 fewer
+//           shared-memory wavefronts per run and warp for RP / G more multiplies per entry and lane.
+constexpr int RV_IDXS = 1, RV_PRED = 2, RV_A1REG = 4, RV_XREG = 8, RV_RHS = 32, RV_S32 = 64, RV_CHUNKED = 128,
+              RV_FOLDZ = 256;
 
 template <int RP, int DO, bool MULT, int G, int B, bool PIPE, int NW, int CH, int VAR>
 __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
@@ -103,8 +110,10 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
     constexpr int RNW = NW, RING = NCH * CH;
     constexpr int VPL = RP / G, NCOL = L::NCOL, NGR = 32 / G, STEP = NGR * B;
     constexpr bool IDXS = (VAR & RV_IDXS) != 0, PRED = (VAR & RV_PRED) != 0, A1REG = (VAR & RV_A1REG) != 0,
-                   XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0, S32 = (VAR & RV_S32) != 0;
+                   XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0, S32 = (VAR & RV_S32) != 0,
+                   FOLDZ = (VAR & RV_FOLDZ) != 0;
     static_assert(!RHS || (!PIPE && !IDXS), "RV_RHS: the plain step loop");
+    static_assert(!FOLDZ || (!RHS && !PIPE && !A1REG && !XREG), "RV_FOLDZ: the plain operator loop");
     constexpr int WIN = MULT ? 16 : 32;  // RV_IDXS window (entries)
     static_assert(!IDXS || (DO == 2 && STEP <= WIN / 2), "RV_IDXS: 3-way plans, window >= 2 steps");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -269,6 +278,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) racc[k] = 0.0;
     if constexpr (XREG) lds_row<G, VPL>(xr, xrs, gl, odd);
+    if constexpr (FOLDZ) lds_row<G, VPL>(u, xrs, gl, odd);  // RV_FOLDZ: u = the Xhat row, v = the run's A_1 row
     // RV_IDXS window: entries [wnd, wnd + WIN); lane l holds column 1 of entry wnd + (l % 16) (l < 16)
     // or the multiplicity (l >= 16) — WIN = 32 without multiplicities: column 1 of wnd + l
     int wnd = INT_MIN / 2, widx = 0;
@@ -331,6 +341,10 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                     x.x *= f.x;
                     x.y *= f.y;
                 }
+                if constexpr (FOLDZ) {
+                    x.x *= v[2 * t];
+                    x.y *= v[2 * t + 1];
+                }
                 z[b][2 * t] = x.x;
                 z[b][2 * t + 1] = x.y;
             }
@@ -363,7 +377,10 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             if constexpr (MULT && !RHS) s *= (double)mu[b];
             if constexpr (!FULL) s = p + g * B + b < rend ? s : 0.0;
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) v[k] = fma(s, z[b][k], v[k]);
+            for (int k = 0; k < VPL; ++k) {
+                if constexpr (FOLDZ) racc[k] = fma(s, z[b][k], racc[k]);
+                else v[k] = fma(s, z[b][k], v[k]);
+            }
         }
     };
 
@@ -380,22 +397,26 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
             tma::bulk_g2s(a1s + sl * RP, fa1 + (int64_t)i1_2 * RP, RP * 8, bar_a1 + sl);
         }
         const double* a1 = a1s + (jl % 3) * RP;
-        if constexpr (XREG) {
+        if constexpr (FOLDZ) {
+            lds_row<G, VPL>(v, a1, gl, odd);
+        } else if constexpr (XREG) {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) u[k] = xr[k];
         } else if constexpr (!RHS) {
             lds_row<G, VPL>(u, xrs, gl, odd);  // u = Xhat(i,:) o A_1(a,:), one pair at a time
         }
         if constexpr (A1REG) lds_row<G, VPL>(a1r, a1, gl, odd);
+        if constexpr (!FOLDZ) {
 #pragma unroll
-        for (int t = 0; t < VPL / 2; ++t) {
-            double2 x;
-            if constexpr (A1REG) x = make_double2(a1r[2 * t], a1r[2 * t + 1]);
-            else x = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
-            u[2 * t] *= x.x;
-            u[2 * t + 1] *= x.y;
-            v[2 * t] = 0.0;
-            v[2 * t + 1] = 0.0;
+            for (int t = 0; t < VPL / 2; ++t) {
+                double2 x;
+                if constexpr (A1REG) x = make_double2(a1r[2 * t], a1r[2 * t + 1]);
+                else x = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
+                u[2 * t] *= x.x;
+                u[2 * t + 1] *= x.y;
+                v[2 * t] = 0.0;
+                v[2 * t + 1] = 0.0;
+            }
         }
         // the run table one run further (consumed at the next run start)
         const int rs3 = rel_of(r + 3);
@@ -463,13 +484,15 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
         }
         // run complete: this lane's share of A_1(a,:) o v folded into its row accumulator (lane
         // groups keep separate partial rows; they are summed once per row, at the flush)
+        if constexpr (!FOLDZ) {
 #pragma unroll
-        for (int t = 0; t < VPL / 2; ++t) {
-            double2 aa;
-            if constexpr (A1REG) aa = make_double2(a1r[2 * t], a1r[2 * t + 1]);
-            else aa = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
-            racc[2 * t] = fma(aa.x, v[2 * t], racc[2 * t]);
-            racc[2 * t + 1] = fma(aa.y, v[2 * t + 1], racc[2 * t + 1]);
+            for (int t = 0; t < VPL / 2; ++t) {
+                double2 aa;
+                if constexpr (A1REG) aa = make_double2(a1r[2 * t], a1r[2 * t + 1]);
+                else aa = *reinterpret_cast<const double2*>(a1 + col_of<G>(t, gl, odd));
+                racc[2 * t] = fma(aa.x, v[2 * t], racc[2 * t]);
+                racc[2 * t + 1] = fma(aa.y, v[2 * t + 1], racc[2 * t + 1]);
+            }
         }
         pos = rend;
         ++r;
@@ -553,6 +576,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                 tma::mbar_wait(bar_x, (unsigned)(xcnt & 1));
                 ++xcnt;
                 if constexpr (XREG) lds_row<G, VPL>(xr, xrs, gl, odd);
+                if constexpr (FOLDZ) lds_row<G, VPL>(u, xrs, gl, odd);
             }
         }
         __syncwarp();
@@ -588,6 +612,11 @@ int runs_layout() {
 // faster) + the staging test once per landed stretch (RV_CHUNKED: -> 3.66 ms) —
 // profiles/round2/runs_variants_config4.txt.  CPHIFI_RUNS_VAR selects another (0: the plain loop).
 constexpr int RV_DEFAULT = RV_S32 | RV_PRED | RV_CHUNKED;
+// ... and, for coalesced 3-way plans at RP = 64 (config 4: ~32-entry runs per part), the A_1 row folded
+// into the entries' rows (RV_FOLDZ, all-entry loads in the partial step): run kernel 3.62 -> 3.53 ms,
+// application 174.4 -> 180.5 matvecs/s; no spills at 128 registers (the former default spilled 40 B).
+// CPHIFI_RUNS_VAR=194 selects the former default.
+constexpr int RV_DEFAULT_FOLDZ = RV_S32 | RV_CHUNKED | RV_FOLDZ;
 constexpr int DEF_CH = 128;  // with 2 chunks in flight (nch_of): config 4 3.66 -> 3.62 ms
 int runs_var() {
     static const int var = [] {
@@ -596,10 +625,18 @@ int runs_var() {
     }();
     return var;
 }
+bool runs_var_chosen() {
+    static const bool set = std::getenv("CPHIFI_RUNS_VAR") != nullptr;
+    return set;
+}
 
 template <int RP, int DO, bool MULT>
 void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
     if constexpr (RP == 64 && DO == 2 && MULT) {
+        if (!runs_var_chosen()) {
+            launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s);
+            return;
+        }
         switch (runs_var()) {
             case 1: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 1>(a, sf, s); return;
             case 2: launch4<RP, DO, MULT, 8, 2, false, 16, 64, 2>(a, sf, s); return;
@@ -626,6 +663,10 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             // registers, no spills): 3.91 vs 3.62 ms at config 4.  (G = 4 with B = 1 / 2 and G = 8
             // with B = 3 spill 204-664 B at 128 registers.)
             case 4099: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s); return;
+            case 450: launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
+            case 451: launch4<RP, DO, MULT, 8, 3, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
+            case 452: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
+            case 453: launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s); return;
             default: break;
         }
     }

@@ -15,7 +15,7 @@ import math
 import numpy as np
 
 DENSE_MIN = 0.3               # build_dense_rows: a 3-way row this full runs as two DMMA GEMMs
-DENSE_ROW_COST_CELLS = 0.32   # ... at the cost of this many plan entries per grid cell
+DENSE_ROW_COST_CELLS = 0.345  # ... at the cost of this many plan entries per grid cell
 RUN_COST_ENTRIES = 21.0       # per-run work of the run kernel, in entries
 
 
