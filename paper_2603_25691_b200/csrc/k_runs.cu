@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(NW * 32, 1) runs_kernel(const RunsArgs a) {
                    XREG = (VAR & RV_XREG) != 0, RHS = (VAR & RV_RHS) != 0, S32 = (VAR & RV_S32) != 0,
                    FOLDZ = (VAR & RV_FOLDZ) != 0;
     static_assert(!RHS || (!PIPE && !IDXS), "RV_RHS: the plain step loop");
-    static_assert(!FOLDZ || (!RHS && !PIPE && !A1REG && !XREG), "RV_FOLDZ: the plain operator loop");
+    static_assert(!FOLDZ || (!RHS && !A1REG && !XREG), "RV_FOLDZ: the operator loop");
     constexpr int WIN = MULT ? 16 : 32;  // RV_IDXS window (entries)
     static_assert(!IDXS || (DO == 2 && STEP <= WIN / 2), "RV_IDXS: 3-way plans, window >= 2 steps");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -667,6 +667,8 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 451: launch4<RP, DO, MULT, 8, 3, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
             case 452: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
             case 453: launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s); return;
+            case 454: launch4<RP, DO, MULT, 8, 1, true, 16, DEF_CH, RV_S32 | RV_FOLDZ>(a, sf, s); return;
+            case 455: launch4<RP, DO, MULT, 8, 2, true, 16, DEF_CH, RV_S32 | RV_FOLDZ>(a, sf, s); return;
             default: break;
         }
     }
