@@ -668,6 +668,10 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 452: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
             case 453: launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s); return;
             case 454: launch4<RP, DO, MULT, 8, 1, true, 16, DEF_CH, RV_S32 | RV_FOLDZ>(a, sf, s); return;
+            case 456: launch4<RP, DO, MULT, 16, 4, false, 20, 32, RV_FOLDZ>(a, sf, s); return;
+            case 457: launch4<RP, DO, MULT, 16, 2, false, 24, 32, RV_FOLDZ>(a, sf, s); return;
+            case 458: launch4<RP, DO, MULT, 16, 4, false, 24, 32, RV_FOLDZ>(a, sf, s); return;
+            case 459: launch4<RP, DO, MULT, 16, 2, false, 20, 32, RV_FOLDZ>(a, sf, s); return;
             case 455: launch4<RP, DO, MULT, 8, 2, true, 16, DEF_CH, RV_S32 | RV_FOLDZ>(a, sf, s); return;
             default: break;
         }
@@ -727,13 +731,16 @@ static int shape_nw(int64_t rp) {
     if (rp != 64 || runs_layout() != 0) return 16;
     const int v = runs_var();
     if (v == 81 || v == 82) return 8;
+    if (v == 456 || v == 459) return 20;
+    if (v == 457 || v == 458) return 24;
     return (v & 16) || v == 80 || v == 83 || v == 84 || v == 86 ? 12 : 16;
 }
 static int shape_ch(int64_t rp) {
     if (rp == 64 && runs_layout() == 3) return 32;
     if (runs_layout() != 0) return 64;
     const int v = runs_var();
-    return (v == RV_DEFAULT || v >= 4096) ? DEF_CH : 64;
+    if (v >= 456 && v <= 459) return 32;
+    return (v == RV_DEFAULT || v >= 4096 || (v >= 450 && v <= 455)) ? DEF_CH : 64;
 }
 
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {
