@@ -696,6 +696,7 @@ void launch3(const RunsArgs& a, int64_t sf, cudaStream_t s) {
         if (lay == 1) launch4<RP, DO, MULT, 8, 2, false>(a, sf, s);
         else if (lay == 2) launch4<RP, DO, MULT, 4, 1, true>(a, sf, s);
         else if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
+        else if (runs_var_chosen() && runs_var() == 448) launch4<RP, DO, MULT, 4, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s);
         else launch4<RP, DO, MULT, 4, 2, false, 16, DEF_CH, RV_DEFAULT>(a, sf, s);
     } else {
         if (runs_var() == 0) launch4<RP, DO, MULT, 4, 2, false>(a, sf, s);
@@ -740,7 +741,7 @@ static int shape_ch(int64_t rp) {
     if (runs_layout() != 0) return 64;
     const int v = runs_var();
     if (v >= 456 && v <= 459) return 32;
-    return (v == RV_DEFAULT || v >= 4096 || (v >= 450 && v <= 455)) ? DEF_CH : 64;
+    return (v == RV_DEFAULT || v >= 4096 || (v >= 448 && v <= 455)) ? DEF_CH : 64;
 }
 
 size_t runs_smem_bytes(int64_t rp, int dother, bool mult, int64_t sf_doubles) {
