@@ -316,6 +316,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, k1_ms, app_ms_phased, e2e_s, dense_ms = (float(v) for v in t)
     value = args.steps / (total_ms / 1e3)
+    # per-rank q-pass shares (cost-balanced shards give the head ranks the dense rows and the tail ranks the
+    # sparse rows): the rooflines below describe the rank whose kernel took longest
+    mine = torch.tensor([ms6[1], ms6[2], qplan["sparse_draws"], qplan["parts"], qplan["dense_rows"],
+                         qplan["sparse_entries_unpadded"], ql.value, ms6[5]], dtype=torch.float64, device=dev)
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(per_rank, mine)
+    per_rank = [[float(v) for v in pr.tolist()] for pr in per_rank]
+    jr = max(range(len(per_rank)), key=lambda j: per_rank[j][0])  # the rank with the slowest run kernel
+    jd = max(range(len(per_rank)), key=lambda j: per_rank[j][1])  # ... the slowest dense-rows kernel
+    qplan = dict(qplan, sparse_draws=int(per_rank[jr][2]), parts=int(per_rank[jr][3]),
+                 sparse_entries_unpadded=int(per_rank[jr][5]), dense_rows=int(per_rank[jd][4]))
+    k1_ms, dense_ms = per_rank[jr][0], per_rank[jd][1]
 
     sec = {}
     if rank == 0 and world == 1 and args.secondary:
@@ -359,6 +373,9 @@ def main():
             if world > 1 else "1 GPU",
             "plan_entries_this_rank": ql.value,
             "qpass_plan": qplan,
+            "per_rank": [{"rank": j, "runs_kernel_ms": pr[0], "dense_rows_kernel_ms": pr[1], "sparse_draws": int(pr[2]),
+                          "dense_rows": int(pr[4]), "plan_entries": int(pr[6]), "application_ms": pr[7]}
+                         for j, pr in enumerate(per_rank)],
             "roofline": {"bound": "hbm", "kernel": f"runs_kernel (k_runs.cu: the per-entry gather / scatter over the "
                                                   f"sparse rows, {nparts} launches per application, one per "
                                                   f"factor-block part)",
