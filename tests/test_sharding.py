@@ -108,3 +108,58 @@ def test_device_cut_matches_host(ctx, S, coalesce, d3, by_entries):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _capi.check(lib.cphifi_obs_shard_rows(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         assert (a.value, b.value, c.value) == sharding.shard_row_ranges(cuts, rp, s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["tiny", "one_row", "more_shards_than_rows", "empty_rows"])
+def test_device_cut_edge_cases(ctx, case):
+    """Few observations, one occupied row, more shards than rows, long stretches of empty rows: the
+    device cut equals the host restatement, the shards partition the observations, and the shards'
+    partial results (row-sharded operator at n > 512) sum to the unsharded application."""
+    import paper_2603_25691_b200 as cp
+    from paper_2603_25691_b200 import _capi
+    lib = _capi.load()
+    rng = np.random.default_rng(9)
+    n, S = 520, 4
+    if case == "tiny":
+        shape, q = [n, 5, 4], 5
+        i0 = rng.integers(0, n, size=q)
+    elif case == "one_row":
+        shape, q = [n, 5, 4], 2000
+        i0 = np.full(q, 77)
+    elif case == "more_shards_than_rows":
+        shape, q, S = [n, 6, 5], 600, 8
+        i0 = rng.choice([3, 400, 519], size=q)
+    else:
+        shape, q = [n, 6, 5], 3000
+        i0 = rng.choice(np.r_[0:4, 500:520], size=q)
+    idx = np.stack([i0] + [rng.integers(0, s, size=q) for s in shape[1:]]).astype(np.int32)
+    vals = rng.normal(size=q)
+    r = 8
+    factors = [np.asfortranarray(rng.normal(size=(s, r))) for s in shape]
+    mode = cp.RkhsMode(np.sort(rng.uniform(size=n)), 0.05, 1e-3, ctx=ctx)
+    model = cp.KruskalModel([np.zeros((n, r))] + factors[1:])
+    x = rng.normal(size=n * r)
+    for coalesce in (True, False):
+        cuts, rp = sharding.shard_cuts(idx, shape, 0, S, coalesce)
+        keys, _ = sharding.sorted_keys(idx, shape, 0)
+        obs = cp.ObservationSet(shape, idx, vals, multiset=True, coalesce=coalesce)
+        pref = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6)
+        pref.set_operator("stream")
+        yref = cp.unaligned_matvec(pref, x)
+        ysum, total = np.zeros_like(yref), 0
+        for s in range(S):
+            h = obs.plan(0, ctx, s, S).h
+            qt, ql = ctypes.c_int64(), ctypes.c_int64()
+            _capi.check(lib.cphifi_obs_info(h, ctypes.byref(qt), ctypes.byref(ql), None))
+            kk = keys[cuts[s]:cuts[s + 1]]
+            assert ql.value == (np.unique(kk).size if coalesce else kk.size), (case, coalesce, s)
+            total += kk.size
+            a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            _capi.check(lib.cphifi_obs_shard_rows(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+            assert (a.value, b.value, c.value) == sharding.shard_row_ranges(cuts, rp, s)
+            p = cp.make_unaligned_subproblem(obs, model, 0, mode, 1e-6, shard=s, shards=S)
+            p.set_operator("stream")
+            ysum += cp.unaligned_matvec(p, x)
+        assert total == q
+        assert np.linalg.norm(ysum - yref) <= 1e-12 * np.linalg.norm(yref), (case, coalesce)
