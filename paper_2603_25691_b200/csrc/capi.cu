@@ -1156,7 +1156,7 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
     gemm(g, ctx->num_sms, ctx->stream);
 }
 
-// Row-sharded operator (large n, sharded observations, stream operator): the shards are contiguous
+// Row-sharded operator (large n, sharded observations; stream and row-Gram operators): the shards are contiguous
 // in the plan order, so rank s's observations touch only the rows [own_lo, hull_hi) — it needs only
 // those rows of Xhat = K X and its partial Yhat is zero elsewhere.  Both dense contractions shrink
 // to the rank's rows: Xhat[rows,:] = K[rows,:] X, then, with lambda K X folded into the operand,
@@ -1166,7 +1166,7 @@ void y_gemm(cphifi_unaligned p, const double* x, double* y) {
 // (config 4: 0.18 of the 0.9 ms an 8-way shard takes).  CPHIFI_ROW_SHARDED=0 restores the replicated form.
 bool row_sharded(cphifi_unaligned p) {
     cphifi_obs o = p->obs;
-    if (o->shards <= 1 || p->small_n || p->op == 1) return false;
+    if (o->shards <= 1 || p->small_n) return false;
     if (ctx_multi(o->ctx) && o->ctx->nranks != o->shards) return false;
     const char* e = std::getenv("CPHIFI_ROW_SHARDED");
     return !(e && std::atoi(e) == 0);
@@ -1239,7 +1239,8 @@ void matvec_dev(cphifi_unaligned p, const double* x, double* y) {
     }
     if (row_sharded(p)) {
         xhat_gemm_rows(p, x);
-        launch_phase_b(p, fused_args(p, PH_B));
+        if (gr) gram_apply(gr, p->xhat_rm.get(), p->obs->row_ptr.get(), p->n, p->rp, p->yhat_rm.get(), ctx->stream);
+        else launch_phase_b(p, fused_args(p, PH_B));
         y_gemm_rows(p, x, y);
         return;
     }
@@ -1348,6 +1349,53 @@ int64_t rot_null_rows(cphifi_unaligned p) {
 // null_rows = false: the caller supplies rows i < z of y~ (= rho x~) itself (the fused PCG step)
 // parts / nparts non-null: the output GEMM's split-K partials are left unreduced for the fused PCG
 // step (EPI_PARTIALS; *parts = nullptr when that GEMM does not take the tensor-map path)
+// The eigenbasis operator on a row-sharded plan (see row_sharded): rank s contracts only its rows of
+// U diag(mu) and U' — Xhat[rows,:] = (U diag(mu))[rows, z:] x~[z:], its q-pass or row-Gram apply,
+// y~_s = mu o (U[rows, z:]' Yhat_s[rows,:]) — the ridge terms (lambda mu + rho) x~ are diagonal in the
+// eigenbasis and added on shard 0 alone, and ONE all-reduce of the n x r partials replaces the
+// Yhat all-reduce.  Every rank ends with the same bits (the all-reduce's result).
+bool row_sharded_rot(cphifi_unaligned p) {
+    cphifi_obs o = p->obs;
+    if (o->shards <= 1 || p->small_n) return false;
+    if (ctx_multi(o->ctx) && o->ctx->nranks != o->shards) return false;
+    const char* e = std::getenv("CPHIFI_ROW_SHARDED");
+    return !(e && std::atoi(e) == 0);
+}
+
+void matvec_rot_rows(cphifi_unaligned p, const double* xt, double* yt, int64_t z, bool null_rows) {
+    cphifi_obs o = p->obs;
+    cphifi_ctx ctx = o->ctx;
+    const int64_t n = p->n, r = p->r;
+    int64_t lo = o->own_lo, hi = o->hull_hi;
+    if (hi <= lo) {  // a shard without rows: contract 8 rows of zeros
+        lo = std::max<int64_t>(0, std::min(lo, n - 8)) / 8 * 8;
+        hi = std::min(n, lo + 8);
+    }
+    if (!p->y_part.n) p->y_part.alloc(n * r);
+    GemmArgs g;  // Xhat[rows,:] -> row-major padded copy for the gather
+    g.m = hi - lo; g.n = r; g.k = n - z;
+    g.a = mode_um(p->mode) + z * n + lo; g.a_rs = 1; g.a_cs = n;
+    g.b = xt + z; g.b_rs = 1; g.b_cs = n;
+    g.c2 = p->xhat_rm.get() + lo * p->rp; g.ld2 = p->rp;
+    gemm(g, ctx->num_sms, ctx->stream);
+    if (p->op == 1) gram_apply(p->gram.get(), p->xhat_rm.get(), o->row_ptr.get(), n, p->rp, p->yhat_rm.get(), ctx->stream);
+    else launch_phase_b(p, fused_args(p, PH_B));
+    GemmArgs h;  // y~_s = mu o (U[rows, z:]' Yhat_s[rows,:]) (+ (lambda mu + rho) x~ on shard 0), rows i >= z
+    h.m = n - z; h.n = r; h.k = hi - lo;
+    h.a = mode_ut(p->mode) + z + lo * n; h.a_rs = 1; h.a_cs = n;
+    h.b = p->yhat_rm.get() + lo * p->rp; h.b_rs = p->rp; h.b_cs = 1;
+    h.c = p->y_part.get() + z; h.c_rs = 1; h.c_cs = n;
+    h.epi = EPI_ROWSCALE; h.e_row = p->mode->mu.get() + z; h.ld_e = n;
+    if (o->shard == 0) {
+        h.e1 = xt + z;
+        h.beta1 = p->mode->lambda; h.beta2 = p->rho;
+    }
+    gemm(h, ctx->num_sms, ctx->stream);
+    if (z > 0) scale_row_block(p->y_part.get(), xt, z, n, r, 0.0, ctx->stream);  // rows i < z of the partial: zero
+    allreduce_sum(ctx, p->y_part.get(), yt, (size_t)n * r);
+    if (z > 0 && null_rows) scale_row_block(yt, xt, z, n, r, p->rho, ctx->stream);  // y~ = rho x~  (rows i < z)
+}
+
 void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows = true,
                 const double** parts = nullptr, int* nparts = nullptr) {
     need_mode(p);
@@ -1373,6 +1421,10 @@ void matvec_rot(cphifi_unaligned p, const double* xt, double* yt, bool null_rows
     }
     // rows / columns of the clamped null space (mu_i = 0) drop out of both GEMMs (mode_nzero)
     const int64_t z = rot_null_rows(p);
+    if (!parts && row_sharded_rot(p)) {
+        matvec_rot_rows(p, xt, yt, z, null_rows);
+        return;
+    }
     GemmArgs g;  // Xhat = U diag(mu) x~  -> row-major padded copy for the gather
     g.m = n; g.n = r; g.k = n - z;
     g.a = mode_um(p->mode) + z * n; g.a_rs = 1; g.a_cs = n;
