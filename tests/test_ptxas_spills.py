@@ -7,6 +7,7 @@ added 28 B of spill stores and dropped the bench from ~60k to ~57.7k matvecs/s).
 the kernel's translation unit with `-Xptxas -v` and requires zero spills for the instantiations
 the benchmarks launch.
 """
+import functools
 import os
 import re
 import shutil
@@ -17,6 +18,7 @@ import pytest
 CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2603_25691_b200", "csrc")
 
 
+@functools.lru_cache(maxsize=None)  # one compile per translation unit (k_runs.cu alone takes a minute)
 def _ptxas_report(src):
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     if not os.path.exists(nvcc):
@@ -42,7 +44,7 @@ def _ptxas_report(src):
 # the 128-register limit and spills a few words outside the step loop: measured 4.2 ms per
 # application against 5.3 ms for the spill-free G = 8 layout (profiles/prof_stream.py), so a small,
 # fixed allowance guards it instead of zero.
-@pytest.mark.parametrize("src,pattern,allow", [
+CASES = [
     ("k_fused.cu", r"fused_matvec_kernelILi16ELi2ELb1E", 0),   # config 1: rp 16, 2 other modes, staged factors
     ("k_pcgstep.cu", r"pcg_step_fused_kernelILi8E", 0),        # config 4 PCG vector step (r 64)
     ("k_runs.cu", r"runs_kernelILi64ELi2ELb1ELi8ELi2ELb0ELi16ELi128ELi448E", 0),  # config 4 q-pass (the headline: RV_FOLDZ loop)
@@ -51,9 +53,21 @@ def _ptxas_report(src):
     ("k_gram.cu", r"gram_build_dmma2?_kernelILi(32ELi3|64ELi2)E", 0),  # configs 3 / 4 row-Gram builds
     ("k_stream.cu", r"stream_kernelILi(32ELi3|64ELi2)ELb[01]ELi2E", 0),  # configs 3 / 4 right-hand side B
     ("k_dense_rows.cu", r"dense_rows_kernelILi64E", 8),  # config 4 dense rows (one word outside the chunk loop)
-])
+]
+
+
+@functools.lru_cache(maxsize=None)
+def _all_reports():
+    """Every guarded translation unit compiled once, side by side (nvcc is single-threaded per unit)."""
+    from concurrent.futures import ThreadPoolExecutor
+    srcs = sorted({c[0] for c in CASES})
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        return dict(zip(srcs, ex.map(_ptxas_report, srcs)))
+
+
+@pytest.mark.parametrize("src,pattern,allow", CASES)
 def test_no_spills(src, pattern, allow):
-    rep = _ptxas_report(src)
+    rep = _all_reports()[src]
     hits = {k: v for k, v in rep.items() if re.search(pattern, k)}
     assert hits, f"no instantiation matching {pattern} in {src}"
     for k, (st, ld) in hits.items():
