@@ -668,6 +668,7 @@ void launch_var(const RunsArgs& a, int64_t sf, cudaStream_t s) {
             case 452: launch4<RP, DO, MULT, 8, 1, false, 16, DEF_CH, RV_DEFAULT | RV_FOLDZ>(a, sf, s); return;
             case 453: launch4<RP, DO, MULT, 8, 2, false, 16, DEF_CH, RV_DEFAULT_FOLDZ>(a, sf, s); return;
             case 454: launch4<RP, DO, MULT, 8, 1, true, 16, DEF_CH, RV_S32 | RV_FOLDZ>(a, sf, s); return;
+            case 460: launch4<RP, DO, MULT, 8, 2, false, 16, 64, RV_IDXS | RV_FOLDZ>(a, sf, s); return;
             case 456: launch4<RP, DO, MULT, 16, 4, false, 20, 32, RV_FOLDZ>(a, sf, s); return;
             case 457: launch4<RP, DO, MULT, 16, 2, false, 24, 32, RV_FOLDZ>(a, sf, s); return;
             case 458: launch4<RP, DO, MULT, 16, 4, false, 24, 32, RV_FOLDZ>(a, sf, s); return;
